@@ -1,0 +1,285 @@
+// extern "C" boundary (include/phif_b200.h). No exception crosses it.
+#include <csignal>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <execinfo.h>
+#include <unistd.h>
+
+#include "../../include/phif_b200.h"
+#include "engine.h"
+
+struct phif_matrix {
+  std::unique_ptr<phif::Matrix> m;
+  cudaStream_t stream;
+};
+struct phif_factor {
+  std::unique_ptr<phif::Factorization> f;
+};
+
+namespace {
+
+void segv_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "[phif] fatal signal, native backtrace:\n";
+  if (write(2, msg, sizeof(msg) - 1) < 0) {}
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+
+struct InstallHandler {
+  InstallHandler() {
+    if (getenv("PHIF_DEBUG")) signal(SIGSEGV, segv_handler);
+  }
+} install_handler;
+
+void set_err(phif_error* e, int code, const char* msg) {
+  if (!e) return;
+  e->code = code;
+  e->pivot = e->level = e->stage = e->group = -1;
+  std::snprintf(e->message, sizeof(e->message), "%s", msg);
+}
+
+template <class Fn>
+int guarded(phif_error* err, Fn&& fn) {
+  try {
+    fn();
+    if (err) err->code = PHIF_OK;
+    return PHIF_OK;
+  } catch (const phif::NotSpd& e) {
+    if (err) {
+      err->code = PHIF_NOT_SPD;
+      err->pivot = e.pivot;
+      err->level = e.level;
+      err->stage = e.stage;
+      err->group = e.group;
+      std::snprintf(err->message, sizeof(err->message), "matrix not positive definite at pivot %d", e.pivot);
+    }
+    return PHIF_NOT_SPD;
+  } catch (const std::exception& e) {
+    set_err(err, PHIF_ERROR, e.what());
+    return PHIF_ERROR;
+  } catch (...) {
+    set_err(err, PHIF_ERROR, "unknown error");
+    return PHIF_ERROR;
+  }
+}
+
+bool is_device(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+extern "C" {
+
+int phif_version(void) { return 1; }
+
+int phif_matrix_create(const int64_t* rowptr, const int32_t* col, const double* val, int64_t n, void* stream,
+                       phif_matrix** out, phif_error* err) {
+  return guarded(err, [&] {
+    auto* A = new phif_matrix;
+    A->stream = (cudaStream_t)stream;
+    A->m = phif::matrix_create(rowptr, col, val, n, A->stream);
+    cudaStreamSynchronize(A->stream);
+    *out = A;
+  });
+}
+
+void phif_matrix_free(phif_matrix* A) { delete A; }
+
+int phif_factorize(const phif_matrix* A, int dim, int n, int m, double eps, int method, void* stream, int timing,
+                   phif_factor** out, phif_error* err) {
+  return guarded(err, [&] {
+    auto* F = new phif_factor;
+    try {
+      F->f = phif::factorize(*A->m, dim, n, m, eps, method, (cudaStream_t)stream, timing != 0);
+    } catch (...) {
+      delete F;
+      throw;
+    }
+    *out = F;
+  });
+}
+
+void phif_factor_free(phif_factor* F) { delete F; }
+
+int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err) {
+  return guarded(err, [&] {
+    phif::Factorization& f = *F->f;
+    const size_t bytes = (size_t)f.spec.N * nrhs * sizeof(double);
+    if (is_device(x)) {
+      phif::apply(f, x, nrhs, mode);
+      cudaStreamSynchronize(f.stream);
+    } else {
+      phif::DBuf d;
+      d.alloc(bytes, f.stream);
+      cudaMemcpyAsync(d.p, x, bytes, cudaMemcpyHostToDevice, f.stream);
+      phif::apply(f, d.as<double>(), nrhs, mode);
+      cudaMemcpyAsync(x, d.p, bytes, cudaMemcpyDeviceToHost, f.stream);
+      cudaStreamSynchronize(f.stream);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw phif::CudaError(cudaGetErrorString(e));
+  });
+}
+
+int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, int nrhs, double tol, int maxit,
+             void* stream, int* iters, double* relres, int* converged, phif_error* err) {
+  int brk = 0;
+  int rc = guarded(err, [&] {
+    cudaStream_t s = F ? F->f->stream : (cudaStream_t)stream;
+    const size_t bytes = (size_t)A->m->N * nrhs * sizeof(double);
+    phif::DBuf db, dx;
+    const double* bd = b;
+    double* xd = x;
+    const bool xdev = is_device(x);
+    if (!is_device(b)) {
+      db.alloc(bytes, s);
+      cudaMemcpyAsync(db.p, b, bytes, cudaMemcpyHostToDevice, s);
+      bd = db.as<double>();
+    }
+    if (!xdev) {
+      dx.alloc(bytes, s);
+      xd = dx.as<double>();
+    }
+    phif::PcgResult r = phif::pcg(*A->m, F ? F->f.get() : nullptr, bd, xd, nrhs, tol, maxit, s);
+    if (!xdev) cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    for (int c = 0; c < nrhs; ++c) {
+      if (iters) iters[c] = r.iters[c];
+      if (relres) relres[c] = r.relres[c];
+      if (converged) converged[c] = r.converged[c];
+    }
+    brk = r.breakdown;
+  });
+  if (rc == PHIF_OK && brk) {
+    set_err(err, PHIF_BREAKDOWN, "non-finite PCG recurrence value");
+    if (err) err->group = brk;
+    return PHIF_BREAKDOWN;
+  }
+  return rc;
+}
+
+int phif_solve_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
+                     double* value, int* iters, int* converged, double* rel_achieved, phif_error* err) {
+  return guarded(err, [&] {
+    phif::PowerResult r = phif::solve_error(*A->m, *F->f, x0, rel_tol, maxit);
+    *value = r.value;
+    *iters = r.iters;
+    *converged = r.converged;
+    *rel_achieved = r.rel;
+  });
+}
+
+size_t phif_stats_json(const phif_factor* F, char* buf, size_t cap) {
+  const std::string s = F->f->stats_json();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return s.size();
+}
+
+int phif_num_levels(const phif_factor* F) { return (int)F->f->levels.size(); }
+
+int phif_skeleton_sets(const phif_factor* F, int level, int64_t* counts, int32_t* rank, int32_t* nred,
+                       int32_t* skel_dofs, int32_t* red_dofs) {
+  const auto& lv = F->f->levels;
+  if (level < 0 || level >= (int)lv.size()) return PHIF_ERROR;
+  const phif::LevelRT& L = *lv[level];
+  const phif::Groups& G = L.plan.grp;
+  const int nsk = L.plan.root ? 0 : (int)L.plan.skeleton.size();
+  int64_t rs = 0, ks = 0;
+  for (int t = 0; t < nsk; ++t) {
+    rs += L.h_rank[t];
+    ks += G.size(L.plan.skeleton[t]) - L.h_rank[t];
+  }
+  counts[0] = nsk;
+  counts[1] = rs;
+  counts[2] = ks;
+  if (!rank) return PHIF_OK;
+  // the engine keeps S/R lists on device; recompute from the device copies
+  std::vector<int> S(rs), R(ks);
+  if (rs) cudaMemcpy(S.data(), L.s_S.p, rs * sizeof(int), cudaMemcpyDeviceToHost);
+  if (ks) cudaMemcpy(R.data(), L.s_R.p, ks * sizeof(int), cudaMemcpyDeviceToHost);
+  for (int t = 0; t < nsk; ++t) {
+    rank[t] = L.h_rank[t];
+    if (nred) nred[t] = G.size(L.plan.skeleton[t]) - L.h_rank[t];
+  }
+  if (skel_dofs) std::memcpy(skel_dofs, S.data(), rs * sizeof(int));
+  if (red_dofs) std::memcpy(red_dofs, R.data(), ks * sizeof(int));
+  return PHIF_OK;
+}
+
+int64_t phif_classify(int dim, int n, int m, int level, const int32_t* active, int64_t nactive, int32_t* group_of,
+                      int32_t* kind_of_group, int64_t kind_cap) {
+  try {
+    phif::Spec s;
+    s.init(dim, n, m);
+    std::vector<int> act(active, active + nactive);
+    phif::Groups g = phif::classify_set(s, level, act);
+    std::vector<int> pos_of(s.N, -1);
+    for (int64_t i = 0; i < nactive; ++i) pos_of[active[i]] = (int)i;
+    for (int gi = 0; gi < g.G; ++gi)
+      for (int64_t q = g.off[gi]; q < g.off[gi + 1]; ++q) group_of[pos_of[g.mem[q]]] = gi;
+    if (kind_of_group)
+      for (int gi = 0; gi < g.G && gi < kind_cap; ++gi) kind_of_group[gi] = g.kind[gi];
+    return g.G;
+  } catch (...) {
+    return -1;
+  }
+}
+
+size_t phif_plan_dryrun(int dim, int n, int m, const int64_t* rowptr, const int32_t* col, int keep, char* buf,
+                        size_t cap) {
+  std::string out;
+  try {
+    phif::Spec s;
+    s.init(dim, n, m);
+    std::vector<std::unique_ptr<phif::LevelPlan>> lv;
+    std::vector<uint8_t> alive;
+    out = "[";
+    for (int l = 0; l <= s.L; ++l) {
+      lv.push_back(std::make_unique<phif::LevelPlan>());
+      phif::LevelPlan& P = *lv.back();
+      std::vector<std::pair<int, int>> pairs;
+      if (l == 0) {
+        P.grp = phif::classify_all(s);
+        pairs = phif::pattern_from_csr(P.grp, s.N, rowptr, col);
+      } else {
+        P.grp = phif::classify_next(s, lv[l - 1]->grp, alive);
+        pairs = phif::pattern_next(*lv[l - 1], P.grp);
+      }
+      phif::build_level(s, P, std::move(pairs));
+      out += (l ? "," : "") + phif::level_json(P);
+      alive.assign(P.grp.mem.size(), 0);
+      for (int g = 0; g < P.grp.G; ++g) {
+        if (P.grp.kind[g] == 0) continue;
+        for (int64_t q = P.grp.off[g]; q < P.grp.off[g + 1]; ++q) {
+          const int64_t pos = q - P.grp.off[g];
+          alive[q] = (P.grp.kind[g] != 1 || keep < 0 || pos < keep) ? 1 : 0;
+        }
+      }
+    }
+    out += "]";
+  } catch (const std::exception& e) {
+    out = std::string("{\"error\":\"") + e.what() + "\"}";
+  }
+  if (buf && cap) {
+    const size_t k = std::min(cap - 1, out.size());
+    std::memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return out.size();
+}
+
+}  // extern "C"

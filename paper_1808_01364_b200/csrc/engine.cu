@@ -1,0 +1,774 @@
+// Host driver: per level plan -> device structures -> batched stage launches.
+//
+// factorize() restates SPEC.md:275-283 (level loop, root Cholesky as the level-L
+// elimination), apply() SPEC.md:293-310 (record replay), pcg() SPEC.md:360-378,
+// solve_error() SPEC.md:418-426 (e_s in the symmetric G-congruence form).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+#include "engine.h"
+
+namespace phif {
+
+static bool debug_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("PHIF_DEBUG") ? 1 : 0;
+  return on == 1;
+}
+#define DBG(...)                                  \
+  do {                                            \
+    if (debug_on()) {                             \
+      fprintf(stderr, "[phif] " __VA_ARGS__);     \
+      fprintf(stderr, "\n");                      \
+      fflush(stderr);                             \
+    }                                             \
+  } while (0)
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+DBuf& DBuf::operator=(DBuf&& o) noexcept {
+  if (this != &o) {
+    release();
+    p = o.p;
+    bytes = o.bytes;
+    s = o.s;
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+
+void DBuf::alloc(size_t nbytes, cudaStream_t st, bool zero) {
+  release();
+  s = st;
+  bytes = std::max<size_t>(nbytes, 8);
+  CK(cudaMallocAsync(&p, bytes, st));
+  if (zero) CK(cudaMemsetAsync(p, 0, bytes, st));
+}
+
+void DBuf::release() {
+  if (p) cudaFreeAsync(p, s);
+  p = nullptr;
+  bytes = 0;
+}
+
+LevelDev LevelRT::dev() const {
+  LevelDev d;
+  d.G = plan.grp.G;
+  d.goff = goff.as<int64_t>();
+  d.mem = mem.as<int>();
+  d.gsize = gsize.as<int>();
+  d.pool = pool.as<double>();
+  d.boff = boff.as<int64_t>();
+  d.bg = bg.as<int>();
+  d.bh = bh.as<int>();
+  d.adj_off = adj_off.as<int64_t>();
+  d.adj_nbr = adj_nbr.as<int>();
+  d.adj_blk = adj_blk.as<int>();
+  d.diag_blk = diag_blk.as<int>();
+  return d;
+}
+
+std::unique_ptr<Matrix> matrix_create(const int64_t* rowptr, const int* col, const double* val, int64_t N,
+                                      cudaStream_t s) {
+  auto A = std::make_unique<Matrix>();
+  A->N = N;
+  A->nnz = rowptr[N];
+  A->h_rowptr.assign(rowptr, rowptr + N + 1);
+  A->h_col.assign(col, col + A->nnz);
+  A->rowptr.alloc((N + 1) * sizeof(int64_t), s);
+  A->col.alloc(A->nnz * sizeof(int), s);
+  A->val.alloc(A->nnz * sizeof(double), s);
+  CK(cudaMemcpyAsync(A->rowptr.p, rowptr, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(A->col.p, col, A->nnz * sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(A->val.p, val, A->nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  return A;
+}
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+double ms_since(clk::time_point t0) {
+  return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
+
+void check_status(Factorization& F, int level, int stage) {
+  DevStatus h;
+  CK(cudaMemcpyAsync(&h, F.status.p, sizeof(h), cudaMemcpyDeviceToHost, F.stream));
+  CK(cudaStreamSynchronize(F.stream));
+  CK(cudaGetLastError());
+  if (h.first_bad != ~0ull) {
+    const int op = (int)(h.first_bad >> 32), piv = (int)(h.first_bad & 0xffffffffu);
+    throw NotSpd(piv, level, stage, op);
+  }
+}
+
+void upload_structure(LevelRT& L, cudaStream_t s) {
+  const LevelPlan& p = L.plan;
+  const Groups& g = p.grp;
+  upload(L.goff, g.off, s);
+  upload(L.mem, g.mem, s);
+  std::vector<int> gs(g.G);
+  for (int i = 0; i < g.G; ++i) gs[i] = g.size(i);
+  upload(L.gsize, gs, s);
+  upload(L.boff, p.boff, s);
+  upload(L.bg, p.pat.bg, s);
+  upload(L.bh, p.pat.bh, s);
+  upload(L.adj_off, p.pat.adj_off, s);
+  upload(L.adj_nbr, p.pat.adj_nbr, s);
+  upload(L.adj_blk, p.pat.adj_blk, s);
+  std::vector<int> diag(g.G, -1);
+  for (size_t b = 0; b < p.pat.bg.size(); ++b)
+    if (p.pat.bg[b] == p.pat.bh[b]) diag[p.pat.bg[b]] = (int)b;
+  upload(L.diag_blk, diag, s);
+}
+
+}  // namespace
+
+std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m, double eps, int method,
+                                         cudaStream_t s, bool timing) {
+  configure_kernels();
+  auto F = std::make_unique<Factorization>();
+  F->spec.init(dim, n, m);
+  F->method = method;
+  F->eps = method == 2 ? 0.0 : eps;
+  F->stream = s;
+  const Spec& sp = F->spec;
+  if (sp.N != A.N) throw std::runtime_error("matrix order does not match the grid spec");
+  auto t_start = clk::now();
+  double plan_ms = 0.0;
+  F->alive.alloc(sp.N * sizeof(int), s);
+  {
+    std::vector<int> ones(sp.N, 1);
+    CK(cudaMemcpyAsync(F->alive.p, ones.data(), sp.N * sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  F->status.alloc(sizeof(DevStatus), s);
+  cudaEvent_t ev[16];
+  if (timing)
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<uint8_t> alive_mem;  // survivors of the previous level, per member position
+  for (int lev = 0; lev <= sp.L; ++lev) {
+    auto tp = clk::now();
+    F->levels.push_back(std::make_unique<LevelRT>());
+    LevelRT& L = *F->levels.back();
+    LevelRT* prev = lev > 0 ? F->levels[lev - 1].get() : nullptr;
+    if (lev == 0) {
+      L.plan.grp = classify_all(sp);
+      pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.data(), A.h_col.data());
+    } else {
+      L.plan.grp = classify_next(sp, prev->plan.grp, alive_mem);
+      pairs = pattern_next(prev->plan, L.plan.grp);
+    }
+    DBG("level %d: grouped G=%d", lev, L.plan.grp.G);
+    build_level(sp, L.plan, std::move(pairs));
+    DBG("level %d: planned blocks=%zu pool=%lld", lev, L.plan.pat.bg.size(), (long long)L.plan.pool_doubles);
+    const LevelPlan& P = L.plan;
+    const Groups& G = P.grp;
+    L.S = (int64_t)G.mem.size();
+    // ---------------- host-side descriptors for this level ----------------
+    const int p = (int)P.interior.size();
+    std::vector<int64_t> P_off(p), U_off(p), I_off(p), B_off(p), cwork(p);
+    std::vector<int> nbr_w(P.cell_nbr.size());
+    std::vector<int> Bdofs;
+    int64_t rec = 0, uacc = 0, bacc = 0, wacc = 0;
+    for (int t = 0; t < p; ++t) {
+      const int nn = P.cell_n[t], bb = P.cell_b[t];
+      P_off[t] = rec;
+      rec += (int64_t)(nn + bb) * nn;
+      U_off[t] = uacc;
+      uacc += (int64_t)bb * bb;
+      I_off[t] = G.off[P.interior[t]];
+      B_off[t] = bacc;
+      bacc += bb;
+      cwork[t] = wacc;
+      wacc += nn + bb;
+      for (int64_t j = P.cell_nbr_off[t]; j < P.cell_nbr_off[t + 1]; ++j) {
+        const int h = P.cell_nbr[j];
+        nbr_w[j] = G.size(h);
+        for (int64_t q = G.off[h]; q < G.off[h + 1]; ++q) Bdofs.push_back(G.mem[q]);
+      }
+    }
+    L.cell_work_unit = wacc;
+    L.wbuf_unit = bacc;
+    // boundary reduction lists (x_B -= X^T y in fixed cell order)
+    {
+      std::vector<std::pair<int, int>> dr(Bdofs.size());
+      for (size_t i = 0; i < Bdofs.size(); ++i) dr[i] = {Bdofs[i], (int)i};
+      std::sort(dr.begin(), dr.end());
+      std::vector<int> dof, rows;
+      std::vector<int64_t> off;
+      for (size_t i = 0; i < dr.size(); ++i) {
+        if (i == 0 || dr[i].first != dr[i - 1].first) {
+          dof.push_back(dr[i].first);
+          off.push_back((int64_t)i);
+        }
+        rows.push_back(dr[i].second);
+      }
+      off.push_back((int64_t)dr.size());
+      L.nbd = (int)dof.size();
+      upload(L.bd_dof, dof, s);
+      upload(L.bd_off, off, s);
+      upload(L.bd_rows, rows, s);
+    }
+    // precondition records
+    const int r = P.root ? 0 : (int)P.precond.size();
+    const bool do_prec = (method != 0) && !P.root;
+    std::vector<int64_t> L_off(r), Lg_off(G.G, -1), pI_off(r), pwork(r);
+    std::vector<int> pn(r);
+    int64_t pw = 0;
+    for (int t = 0; t < r; ++t) {
+      const int g = P.precond[t], k = G.size(g);
+      if (do_prec) {
+        L_off[t] = rec;
+        Lg_off[g] = rec;
+        rec += (int64_t)k * k;
+      }
+      pn[t] = k;
+      pI_off[t] = G.off[g];
+      pwork[t] = pw;
+      pw += k;
+    }
+    L.prec_work_unit = pw;
+    // skeleton records / workspaces (upper bounds; ranks known after the ID)
+    const int nsk = P.root ? 0 : (int)P.skeleton.size();
+    std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk);
+    int64_t work = 0, iwork = 0, aw = 0;
+    for (int t = 0; t < nsk; ++t) {
+      const int g = P.skeleton[t], k = G.size(g);
+      int64_t rows = 0;
+      for (int64_t q = P.sk_nbr_off[t]; q < P.sk_nbr_off[t + 1]; ++q) rows += G.size(P.sk_nbr[q]);
+      T_off[t] = rec;
+      rec += (int64_t)k * k;
+      SP_off[t] = rec;
+      rec += (int64_t)k * k;
+      work_off[t] = work;
+      work += std::max<int64_t>((std::max<int64_t>(rows, 1)) * k + 2 * k, 2 * (int64_t)k * k);
+      iwork_off[t] = iwork;
+      iwork += 3 * (int64_t)k;
+      awork[t] = aw;
+      aw += k;
+    }
+    L.skel_work_unit = aw;
+    L.rec_doubles = rec;
+    plan_ms += ms_since(tp);
+    // ---------------- device structures ----------------
+    DBG("level %d: rec=%lld", lev, (long long)rec);
+    upload_structure(L, s);
+    L.pool.alloc(std::max<int64_t>(P.pool_doubles, 1) * sizeof(double), s, /*zero=*/true);
+    L.rec.alloc(std::max<int64_t>(rec, 1) * sizeof(double), s);
+    F->rec_bytes += rec * (int64_t)sizeof(double);
+    LevelDev dv = L.dev();
+    if (timing) CK(cudaEventRecord(ev[0], s));
+    if (lev == 0) {
+      std::vector<int> gid(sp.N), pos(sp.N);
+      for (int g = 0; g < G.G; ++g)
+        for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) {
+          gid[G.mem[q]] = g;
+          pos[G.mem[q]] = (int)(q - G.off[g]);
+        }
+      DBuf dgid, dpos;
+      upload(dgid, gid, s);
+      upload(dpos, pos, s);
+      launch_ingest(dv, dgid.as<int>(), dpos.as<int>(), A.rowptr.as<int64_t>(), A.col.as<int>(),
+                    A.val.as<double>(), sp.N, s);
+      CK(cudaStreamSynchronize(s));
+    } else {
+      RepackArgs ra;
+      ra.nblk = (int)P.pat.bg.size();
+      ra.nbg = L.bg.as<int>();
+      ra.nbh = L.bh.as<int>();
+      ra.nboff = L.boff.as<int64_t>();
+      ra.ngoff = L.goff.as<int64_t>();
+      DBuf sg, spos;
+      upload(sg, G.src_group, s);
+      upload(spos, G.src_pos, s);
+      ra.nsrc_group = sg.as<int>();
+      ra.nsrc_pos = spos.as<int>();
+      ra.npool = L.pool.as<double>();
+      ra.opool = prev->pool.as<double>();
+      ra.oboff = prev->boff.as<int64_t>();
+      ra.oadj_off = prev->adj_off.as<int64_t>();
+      ra.oadj_nbr = prev->adj_nbr.as<int>();
+      ra.oadj_blk = prev->adj_blk.as<int>();
+      ra.ogsize = prev->gsize.as<int>();
+      launch_repack(ra, s);
+      CK(cudaStreamSynchronize(s));
+      prev->pool.release();
+    }
+    if (timing) CK(cudaEventRecord(ev[1], s));
+    // ---------------- stage 1: cell elimination ----------------
+    upload(L.c_interior, P.interior, s);
+    upload(L.c_nbr_off, P.cell_nbr_off, s);
+    upload(L.c_nbr_blk, P.cell_nbr_blk, s);
+    upload(L.c_nbr_col, P.cell_nbr_col, s);
+    upload(L.c_nbr_w, nbr_w, s);
+    upload(L.c_n, P.cell_n, s);
+    upload(L.c_b, P.cell_b, s);
+    upload(L.c_P_off, P_off, s);
+    upload(L.c_U_off, U_off, s);
+    upload(L.c_I_off, I_off, s);
+    upload(L.c_B, Bdofs, s);
+    upload(L.c_B_off, B_off, s);
+    upload(L.c_work_off, cwork, s);
+    DBuf U;
+    U.alloc(std::max<int64_t>(uacc, 1) * sizeof(double), s);
+    CellArgs ca;
+    ca.p = p;
+    ca.interior = L.c_interior.as<int>();
+    ca.nbr_off = L.c_nbr_off.as<int64_t>();
+    ca.nbr_blk = L.c_nbr_blk.as<int>();
+    ca.nbr_col = L.c_nbr_col.as<int>();
+    ca.nbr_w = L.c_nbr_w.as<int>();
+    ca.n = L.c_n.as<int>();
+    ca.b = L.c_b.as<int>();
+    ca.rec = L.rec.as<double>();
+    ca.P_off = L.c_P_off.as<int64_t>();
+    ca.U = U.as<double>();
+    ca.U_off = L.c_U_off.as<int64_t>();
+    CK(cudaMemsetAsync(F->status.p, 0xff, sizeof(DevStatus), s));
+    if (timing) CK(cudaEventRecord(ev[2], s));
+    DBG("level %d: cells p=%d", lev, p);
+    launch_cell(dv, ca, F->status.as<DevStatus>(), s);
+    if (timing) CK(cudaEventRecord(ev[3], s));
+    check_status(*F, lev, P.root ? ST_ROOT : ST_ELIMINATE);
+    DBuf tb, to, cc, cr, ccol;
+    upload(tb, P.tgt_blk, s);
+    upload(to, P.tgt_off, s);
+    upload(cc, P.con_cell, s);
+    upload(cr, P.con_row, s);
+    upload(ccol, P.con_col, s);
+    SchurArgs sa;
+    sa.ntgt = (int)P.tgt_blk.size();
+    sa.tgt_blk = tb.as<int>();
+    sa.tgt_off = to.as<int64_t>();
+    sa.con_cell = cc.as<int>();
+    sa.con_row = cr.as<int>();
+    sa.con_col = ccol.as<int>();
+    sa.cell_b = L.c_b.as<int>();
+    sa.U = U.as<double>();
+    sa.U_off = L.c_U_off.as<int64_t>();
+    if (timing) CK(cudaEventRecord(ev[4], s));
+    DBG("level %d: schur targets=%d", lev, sa.ntgt);
+    launch_schur(dv, sa, s);
+    if (timing) CK(cudaEventRecord(ev[5], s));
+    U.release();
+    if (P.root) {
+      if (timing) {
+        CK(cudaEventSynchronize(ev[5]));
+        float a;
+        cudaEventElapsedTime(&a, ev[0], ev[1]); L.t_ms[0] = a;
+        cudaEventElapsedTime(&a, ev[2], ev[3]); L.t_ms[1] = a;
+        cudaEventElapsedTime(&a, ev[4], ev[5]); L.t_ms[1] += a;
+      }
+      L.pool.release();
+      break;
+    }
+    // ---------------- stage 2: block Jacobi ----------------
+    upload(L.p_groups, P.precond, s);
+    upload(L.p_L_off, L_off, s);
+    upload(L.p_L_off_of_group, Lg_off, s);
+    upload(L.p_scale_blk, P.scale_blk, s);
+    upload(L.p_n, pn, s);
+    upload(L.p_I_off, pI_off, s);
+    upload(L.p_work_off, pwork, s);
+    PrecArgs pa;
+    pa.r = do_prec ? r : 0;
+    pa.groups = L.p_groups.as<int>();
+    pa.rec = L.rec.as<double>();
+    pa.L_off = L.p_L_off.as<int64_t>();
+    pa.L_off_of_group = L.p_L_off_of_group.as<int64_t>();
+    pa.nscale = do_prec ? (int)P.scale_blk.size() : 0;
+    pa.scale_blk = L.p_scale_blk.as<int>();
+    if (timing) CK(cudaEventRecord(ev[6], s));
+    DBG("level %d: precondition r=%d scale=%d", lev, pa.r, pa.nscale);
+    launch_prec_factor(dv, pa, F->status.as<DevStatus>(), s);
+    check_status(*F, lev, ST_PRECONDITION);
+    launch_prec_scale(dv, pa, s);
+    if (timing) CK(cudaEventRecord(ev[7], s));
+    // ---------------- stage 3: skeletonization ----------------
+    upload(L.s_groups, P.skeleton, s);
+    upload(L.s_nbr_off, P.sk_nbr_off, s);
+    upload(L.s_nbr, P.sk_nbr, s);
+    upload(L.s_nbr_blk, P.sk_nbr_blk, s);
+    upload(L.s_order, P.wave_order, s);
+    L.s_rank.alloc(std::max(nsk, 1) * sizeof(int), s, true);
+    upload(L.s_T_off, T_off, s);
+    upload(L.s_P_off, SP_off, s);
+    upload(L.s_work_off, work_off, s);
+    upload(L.s_iwork_off, iwork_off, s);
+    F->red.alloc(std::max<size_t>(G.mem.size(), 1), s, true);
+    DBuf wk, iwk;
+    wk.alloc(std::max<int64_t>(work, 1) * sizeof(double), s);
+    iwk.alloc(std::max<int64_t>(iwork, 1) * sizeof(int), s);
+    SkelArgs ka;
+    ka.nsk = nsk;
+    ka.groups = L.s_groups.as<int>();
+    ka.nbr_off = L.s_nbr_off.as<int64_t>();
+    ka.nbr = L.s_nbr.as<int>();
+    ka.nbr_blk = L.s_nbr_blk.as<int>();
+    ka.alive = F->alive.as<int>();
+    ka.red = F->red.as<uint8_t>();
+    ka.rank = L.s_rank.as<int>();
+    ka.eps = F->eps;
+    ka.work = wk.as<double>();
+    ka.work_off = L.s_work_off.as<int64_t>();
+    ka.iwork = iwk.as<int>();
+    ka.iwork_off = L.s_iwork_off.as<int64_t>();
+    ka.rec = L.rec.as<double>();
+    ka.T_off = L.s_T_off.as<int64_t>();
+    ka.P_off = L.s_P_off.as<int64_t>();
+    if (timing) CK(cudaEventRecord(ev[8], s));
+    for (int w = 0; w < P.nwaves; ++w) {
+      ka.order = L.s_order.as<int>() + P.wave_off[w];
+      launch_skel_id(dv, ka, (int)(P.wave_off[w + 1] - P.wave_off[w]), s);
+    }
+    if (timing) CK(cudaEventRecord(ev[9], s));
+    DBG("level %d: skeleton update nsk=%d waves=%d", lev, nsk, P.nwaves);
+    launch_skel_update(dv, ka, F->status.as<DevStatus>(), s);
+    if (timing) CK(cudaEventRecord(ev[10], s));
+    check_status(*F, lev, ST_SKELETONIZE);
+    // ranks and redundant flags back to the host (planning of the next level)
+    L.h_rank.resize(nsk);
+    std::vector<uint8_t> red(G.mem.size());
+    if (nsk) CK(cudaMemcpyAsync(L.h_rank.data(), L.s_rank.p, nsk * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (!red.empty()) CK(cudaMemcpyAsync(red.data(), F->red.p, red.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    tp = clk::now();
+    alive_mem.assign(G.mem.size(), 0);
+    for (int g = 0; g < G.G; ++g)
+      if (G.kind[g] != 0)
+        for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) alive_mem[q] = red[q] ? 0 : 1;
+    // skeleton apply descriptors
+    std::vector<int> sr(nsk), skt(nsk), Sd, Rd;
+    std::vector<int64_t> S_off(nsk), R_off(nsk);
+    int64_t rsum = 0;
+    for (int t = 0; t < nsk; ++t) {
+      const int g = P.skeleton[t];
+      sr[t] = L.h_rank[t];
+      skt[t] = G.size(g) - L.h_rank[t];
+      rsum += sr[t];
+      S_off[t] = (int64_t)Sd.size();
+      R_off[t] = (int64_t)Rd.size();
+      for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) (red[q] ? Rd : Sd).push_back(G.mem[q]);
+    }
+    L.rho_max = nsk ? *std::max_element(sr.begin(), sr.end()) : 0;
+    L.rho_mean = nsk ? (double)rsum / nsk : 0.0;
+    upload(L.s_r, sr, s);
+    upload(L.s_kt, skt, s);
+    upload(L.s_S, Sd, s);
+    upload(L.s_S_off, S_off, s);
+    upload(L.s_R, Rd, s);
+    upload(L.s_R_off, R_off, s);
+    upload(L.s_awork_off, awork, s);
+    plan_ms += ms_since(tp);
+    if (timing) {
+      CK(cudaEventSynchronize(ev[10]));
+      float a;
+      cudaEventElapsedTime(&a, ev[0], ev[1]); L.t_ms[0] = a;
+      cudaEventElapsedTime(&a, ev[2], ev[3]); L.t_ms[1] = a;
+      cudaEventElapsedTime(&a, ev[4], ev[5]); L.t_ms[1] += a;
+      cudaEventElapsedTime(&a, ev[6], ev[7]); L.t_ms[2] = a;
+      cudaEventElapsedTime(&a, ev[8], ev[9]); L.t_ms[3] = a;
+      cudaEventElapsedTime(&a, ev[9], ev[10]); L.t_ms[4] = a;
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  F->t_factor_ms = ms_since(t_start);
+  F->t_plan_ms = plan_ms;
+  if (timing)
+    for (auto& e : ev) cudaEventDestroy(e);
+  F->red.release();
+  return F;
+}
+
+// ---------------------------------------------------------------------------
+// apply: mode 0 = F^-1 (up then down), 1 = G^-1 (up), 2 = G^-T (down)
+// ---------------------------------------------------------------------------
+static void ensure_work(Factorization& F, int k) {
+  int64_t need = 1, needw = 1;
+  for (auto& lp : F.levels) {
+    need = std::max(need, std::max(lp->cell_work_unit, std::max(lp->prec_work_unit, lp->skel_work_unit)));
+    needw = std::max(needw, lp->wbuf_unit);
+  }
+  const size_t wb = (size_t)need * k * sizeof(double), bb = (size_t)needw * k * sizeof(double);
+  if (wb > F.work_cap) {
+    F.work.alloc(wb, F.stream);
+    F.work_cap = wb;
+  }
+  if (bb > F.wbuf_cap) {
+    F.wbuf.alloc(bb, F.stream);
+    F.wbuf_cap = bb;
+  }
+}
+
+static ApplyCellArgs cell_args(Factorization& F, LevelRT& L) {
+  ApplyCellArgs a;
+  a.p = (int)L.plan.interior.size();
+  a.n = L.c_n.as<int>();
+  a.b = L.c_b.as<int>();
+  a.I = L.mem.as<int>();
+  a.I_off = L.c_I_off.as<int64_t>();
+  a.B = L.c_B.as<int>();
+  a.B_off = L.c_B_off.as<int64_t>();
+  a.rec = L.rec.as<double>();
+  a.P_off = L.c_P_off.as<int64_t>();
+  a.work = F.work.as<double>();
+  a.work_off = L.c_work_off.as<int64_t>();
+  a.wbuf = F.wbuf.as<double>();
+  return a;
+}
+
+static ApplyPrecArgs prec_args(Factorization& F, LevelRT& L) {
+  ApplyPrecArgs a;
+  a.r = (F.method != 0 && !L.plan.root) ? (int)L.plan.precond.size() : 0;
+  a.n = L.p_n.as<int>();
+  a.I = L.mem.as<int>();
+  a.I_off = L.p_I_off.as<int64_t>();
+  a.rec = L.rec.as<double>();
+  a.L_off = L.p_L_off.as<int64_t>();
+  a.work = F.work.as<double>();
+  a.work_off = L.p_work_off.as<int64_t>();
+  return a;
+}
+
+static ApplySkelArgs skel_args(Factorization& F, LevelRT& L) {
+  ApplySkelArgs a;
+  a.nsk = L.plan.root ? 0 : (int)L.plan.skeleton.size();
+  a.r = L.s_r.as<int>();
+  a.kt = L.s_kt.as<int>();
+  a.S = L.s_S.as<int>();
+  a.S_off = L.s_S_off.as<int64_t>();
+  a.R = L.s_R.as<int>();
+  a.R_off = L.s_R_off.as<int64_t>();
+  a.rec = L.rec.as<double>();
+  a.T_off = L.s_T_off.as<int64_t>();
+  a.P_off = L.s_P_off.as<int64_t>();
+  a.work = F.work.as<double>();
+  a.work_off = L.s_awork_off.as<int64_t>();
+  return a;
+}
+
+void apply(Factorization& F, double* x, int k, int mode) {
+  ensure_work(F, k);
+  cudaStream_t s = F.stream;
+  if (mode == 0 || mode == 1) {
+    for (auto& lp : F.levels) {
+      LevelRT& L = *lp;
+      launch_apply_cell(cell_args(F, L), x, k, true, s);
+      launch_apply_reduce(L.bd_dof.as<int>(), L.bd_off.as<int64_t>(), L.bd_rows.as<int>(), F.wbuf.as<double>(),
+                          L.nbd, x, k, s);
+      if (L.plan.root) break;
+      launch_apply_prec(prec_args(F, L), x, k, true, s);
+      launch_apply_skel(skel_args(F, L), x, k, true, s);
+    }
+  }
+  if (mode == 0 || mode == 2) {
+    for (int li = (int)F.levels.size() - 1; li >= 0; --li) {
+      LevelRT& L = *F.levels[li];
+      if (!L.plan.root) {
+        launch_apply_skel(skel_args(F, L), x, k, false, s);
+        launch_apply_prec(prec_args(F, L), x, k, false, s);
+      }
+      launch_apply_cell(cell_args(F, L), x, k, false, s);
+    }
+  }
+  CK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// PCG: per-column scalars, converged columns frozen,
+// true residual every 50 iterations, BreakdownError on non-finite values.
+// ---------------------------------------------------------------------------
+PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int k, double tol, int maxit,
+              cudaStream_t s) {
+  const int64_t N = A.N;
+  const size_t vb = (size_t)N * k * sizeof(double);
+  DBuf R, Z, Pv, Q, part, sc;
+  R.alloc(vb, s);
+  Z.alloc(vb, s);
+  Pv.alloc(vb, s);
+  Q.alloc(vb, s);
+  part.alloc((size_t)dot_part_blocks() * k * sizeof(double), s);
+  sc.alloc(8 * (size_t)k * sizeof(double), s);
+  double* rz = sc.as<double>();
+  double* pq = rz + k;
+  double* alpha = pq + k;
+  double* beta = alpha + k;
+  double* rn2 = beta + k;
+  double* rzn = rn2 + k;
+  double* bn2 = rzn + k;
+  DBuf act;
+  act.alloc(k * sizeof(int), s);
+  const int64_t* rp = A.rowptr.as<int64_t>();
+  const int* ci = A.col.as<int>();
+  const double* va = A.val.as<double>();
+  PcgResult res;
+  res.iters.assign(k, 0);
+  res.relres.assign(k, 1.0);
+  res.converged.assign(k, 0);
+  std::vector<int> active(k, 1);
+  std::vector<double> h_bn(k), h_rn(k), h_al(k), h_be(k);
+  CK(cudaMemsetAsync(x, 0, vb, s));
+  CK(cudaMemcpyAsync(R.p, b, vb, cudaMemcpyDeviceToDevice, s));
+  launch_dot(b, b, N, k, part.as<double>(), bn2, s);
+  CK(cudaMemcpyAsync(h_bn.data(), bn2, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int c = 0; c < k; ++c) {
+    h_bn[c] = std::sqrt(h_bn[c]);
+    if (h_bn[c] == 0.0) {
+      active[c] = 0;
+      res.relres[c] = 0.0;
+      res.converged[c] = 1;
+    }
+  }
+  auto precond = [&](double* dst, const double* src) {
+    CK(cudaMemcpyAsync(dst, src, vb, cudaMemcpyDeviceToDevice, s));
+    if (F) apply(*F, dst, k, 0);
+  };
+  precond(Z.as<double>(), R.as<double>());
+  CK(cudaMemcpyAsync(Pv.p, Z.p, vb, cudaMemcpyDeviceToDevice, s));
+  launch_dot(R.as<double>(), Z.as<double>(), N, k, part.as<double>(), rz, s);
+  int it = 0;
+  auto all_done = [&]() {
+    for (int c = 0; c < k; ++c)
+      if (active[c]) return false;
+    return true;
+  };
+  while (!all_done() && it < maxit) {
+    ++it;
+    CK(cudaMemcpyAsync(act.p, active.data(), k * sizeof(int), cudaMemcpyHostToDevice, s));
+    launch_spmv(rp, ci, va, Pv.as<double>(), Q.as<double>(), N, k, s);
+    launch_dot(Pv.as<double>(), Q.as<double>(), N, k, part.as<double>(), pq, s);
+    launch_ratio(rz, pq, act.as<int>(), alpha, k, s);
+    launch_axpy(x, Pv.as<double>(), alpha, 1.0, act.as<int>(), N, k, s);
+    if (it % 50 == 0) {
+      launch_spmv(rp, ci, va, x, Q.as<double>(), N, k, s);
+      launch_sub(R.as<double>(), b, Q.as<double>(), act.as<int>(), N, k, s);
+    } else {
+      launch_axpy(R.as<double>(), Q.as<double>(), alpha, -1.0, act.as<int>(), N, k, s);
+    }
+    launch_dot(R.as<double>(), R.as<double>(), N, k, part.as<double>(), rn2, s);
+    CK(cudaMemcpyAsync(h_rn.data(), rn2, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_al.data(), alpha, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < k; ++c) {
+      if (!active[c]) continue;
+      const double rr = std::sqrt(h_rn[c]) / h_bn[c];
+      if (!std::isfinite(h_al[c]) || !std::isfinite(rr)) {
+        res.breakdown = it;
+        return res;
+      }
+      res.relres[c] = rr;
+      res.iters[c] = it;
+      if (rr <= tol) {
+        active[c] = 0;
+        res.converged[c] = 1;
+      }
+    }
+    if (all_done()) break;
+    CK(cudaMemcpyAsync(act.p, active.data(), k * sizeof(int), cudaMemcpyHostToDevice, s));
+    precond(Z.as<double>(), R.as<double>());
+    launch_dot(R.as<double>(), Z.as<double>(), N, k, part.as<double>(), rzn, s);
+    launch_ratio(rzn, rz, act.as<int>(), beta, k, s);
+    CK(cudaMemcpyAsync(h_be.data(), beta, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    launch_xpby(Pv.as<double>(), Z.as<double>(), beta, act.as<int>(), N, k, s);
+    // rz <- rzn for active columns (inactive columns keep rz; unused afterwards)
+    CK(cudaMemcpyAsync(rz, rzn, k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < k; ++c)
+      if (active[c] && !std::isfinite(h_be[c])) {
+        res.breakdown = it;
+        return res;
+      }
+  }
+  CK(cudaStreamSynchronize(s));
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// e_s = ||I - G^-1 A G^-T||_2 by power iteration
+// ---------------------------------------------------------------------------
+PowerResult solve_error(const Matrix& A, Factorization& F, const double* x0, double rel_tol, int maxit) {
+  cudaStream_t s = F.stream;
+  const int64_t N = A.N;
+  DBuf X, Y, T, part, sc;
+  X.alloc(N * sizeof(double), s);
+  Y.alloc(N * sizeof(double), s);
+  T.alloc(N * sizeof(double), s);
+  part.alloc(dot_part_blocks() * sizeof(double), s);
+  sc.alloc(4 * sizeof(double), s);
+  double* nrm2 = sc.as<double>();
+  CK(cudaMemcpyAsync(X.p, x0, N * sizeof(double), cudaMemcpyHostToDevice, s));
+  launch_dot(X.as<double>(), X.as<double>(), N, 1, part.as<double>(), nrm2, s);
+  launch_scale(X.as<double>(), X.as<double>(), nrm2, N, s);
+  PowerResult pr;
+  double prev = -1.0, est = 0.0;
+  for (int it = 1; it <= maxit; ++it) {
+    CK(cudaMemcpyAsync(T.p, X.p, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    apply(F, T.as<double>(), 1, 2);   // G^-T x
+    launch_spmv(A.rowptr.as<int64_t>(), A.col.as<int>(), A.val.as<double>(), T.as<double>(), Y.as<double>(), N,
+                1, s);
+    apply(F, Y.as<double>(), 1, 1);   // G^-1 A G^-T x
+    launch_xmy(Y.as<double>(), X.as<double>(), N, s);
+    launch_dot(Y.as<double>(), Y.as<double>(), N, 1, part.as<double>(), nrm2, s);
+    double h;
+    CK(cudaMemcpyAsync(&h, nrm2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    est = std::sqrt(h);
+    pr.iters = it;
+    pr.value = est;
+    if (est == 0.0) {
+      pr.converged = 1;
+      pr.rel = 0.0;
+      return pr;
+    }
+    if (prev >= 0.0) {
+      const double rel = std::fabs(est - prev) / est;
+      pr.rel = rel;
+      if (rel <= rel_tol) {
+        pr.converged = 1;
+        return pr;
+      }
+    }
+    prev = est;
+    launch_scale(X.as<double>(), Y.as<double>(), nrm2, N, s);
+  }
+  return pr;
+}
+
+std::string Factorization::stats_json() const {
+  std::ostringstream o;
+  o.precision(17);
+  const char* mname[] = {"hif", "phif", "exact"};
+  o << "{\"method\":\"" << mname[method] << "\",\"eps\":" << eps << ",\"N\":" << spec.N << ",\"L\":" << spec.L
+    << ",\"t_factor_ms\":" << t_factor_ms << ",\"t_plan_ms\":" << t_plan_ms << ",\"mem_bytes\":" << rec_bytes
+    << ",\"levels\":[";
+  for (size_t i = 0; i < levels.size(); ++i) {
+    const LevelRT& L = *levels[i];
+    const LevelPlan& P = L.plan;
+    o << (i ? "," : "") << "{\"level\":" << P.level << ",\"S\":" << L.S << ",\"p\":" << P.interior.size()
+      << ",\"q\":" << (P.root ? 0 : P.skeleton.size()) << ",\"r\":" << (P.root ? 0 : P.precond.size())
+      << ",\"blocks\":" << P.pat.bg.size() << ",\"waves\":" << P.nwaves << ",\"rho_max\":" << L.rho_max
+      << ",\"rho_mean\":" << L.rho_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
+      << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
+      << L.t_ms[4] << ",\"record_bytes\":" << L.rec_doubles * 8 << "}";
+  }
+  const LevelRT& R = *levels.back();
+  o << "],\"SL\":" << (R.plan.interior.empty() ? 0 : R.plan.cell_n[0]) << "}";
+  return o.str();
+}
+
+}  // namespace phif

@@ -1,0 +1,748 @@
+// Batched stage kernels of the B200 PHIF engine (sm_100a, FP64).
+//
+// One CTA per cell / group / block; all dense algebra through dla.cuh
+// (DMMA GEMM core). Reference semantics are cited per kernel.
+#include <cfloat>
+#include <cstdio>
+
+#include "dla.cuh"
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace phif {
+
+static_assert(NT == 256, "kernels assume 256-thread CTAs");
+
+__device__ __forceinline__ int find_blk(const int64_t* adj_off, const int* adj_nbr, const int* adj_blk, int g,
+                                        int h) {
+  int64_t lo = adj_off[g], hi = adj_off[g + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int v = adj_nbr[mid];
+    if (v < h) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < adj_off[g + 1] && adj_nbr[lo] == h) return adj_blk[lo];
+  return -1;
+}
+
+__device__ __forceinline__ void report_bad(DevStatus* st, int op, int pivot) {
+  const unsigned long long v = ((unsigned long long)(unsigned)op << 32) | (unsigned)pivot;
+  atomicMin(&st->first_bad, v);
+}
+
+// ---------------------------------------------------------------------------
+// Level-0 ingest: scatter the CSR of A into the dense group-pair blocks.
+// ---------------------------------------------------------------------------
+__global__ void k_ingest(LevelDev lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
+                         const double* val, int64_t N) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const int g = gid[r], pr = pos[r];
+  for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+    const int c = col[e];
+    const int h = gid[c];
+    if (h < g) continue;
+    const int blk = find_blk(lv.adj_off, lv.adj_nbr, lv.adj_blk, g, h);
+    if (blk < 0) continue;
+    lv.pool[lv.boff[blk] + (int64_t)pr * lv.gsize[h] + pos[c]] = val[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1: cell elimination.
+// Panel P = [A_II ; A_BI] ((n+b) x n) -> partial Cholesky -> [L ; X^T]; U = X^T X.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus* st) {
+  extern __shared__ double smem[];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int I = ca.interior[t], n = ca.n[t], b = ca.b[t];
+  double* P = ca.rec + ca.P_off[t];
+  const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
+  for (int64_t e = tid; e < (int64_t)n * n; e += NT) P[e] = A[e];
+  for (int64_t j = ca.nbr_off[t]; j < ca.nbr_off[t + 1]; ++j) {
+    const int w = ca.nbr_w[j], c0 = ca.nbr_col[j];
+    const double* S = lv.pool + lv.boff[ca.nbr_blk[j]];
+    for (int64_t e = tid; e < (int64_t)n * w; e += NT) {
+      const int i = (int)(e / w), r = (int)(e % w);
+      P[(int64_t)(n + c0 + r) * n + i] = S[e];
+    }
+  }
+  __syncthreads();
+  const int info = cta_potrf_panel(P, n + b, n, n, smem);
+  if (info >= 0) {
+    if (tid == 0) report_bad(st, t, info);
+    return;
+  }
+  if (b > 0)
+    cta_gemm<false, true>(b, b, n, 1.0, P + (int64_t)n * n, n, P + (int64_t)n * n, n, 0.0, ca.U + ca.U_off[t], b,
+                          false, smem + GEMM_OFF);
+}
+
+// A_BB -= sum_c X_c^T X_c, owner-computes per target block, contributions in cell order.
+__global__ void __launch_bounds__(NT) k_schur(LevelDev lv, SchurArgs sa) {
+  const int tau = blockIdx.x;
+  const int blk = sa.tgt_blk[tau];
+  const int rows = lv.gsize[lv.bg[blk]], cols = lv.gsize[lv.bh[blk]];
+  double* dst = lv.pool + lv.boff[blk];
+  const int64_t c0 = sa.tgt_off[tau], c1 = sa.tgt_off[tau + 1];
+  for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += NT) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    double s = dst[e];
+    for (int64_t c = c0; c < c1; ++c) {
+      const int cell = sa.con_cell[c];
+      const int bb = sa.cell_b[cell];
+      s -= sa.U[sa.U_off[cell] + (int64_t)(sa.con_row[c] + i) * bb + sa.con_col[c] + j];
+    }
+    dst[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2: block Jacobi.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_prec_factor(LevelDev lv, PrecArgs pa, DevStatus* st) {
+  extern __shared__ double smem[];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int g = pa.groups[t], k = lv.gsize[g];
+  double* A = lv.pool + lv.boff[lv.diag_blk[g]];
+  double* L = pa.rec + pa.L_off[t];
+  for (int64_t e = tid; e < (int64_t)k * k; e += NT) L[e] = A[e];
+  __syncthreads();
+  const int info = cta_potrf_panel(L, k, k, k, smem);
+  if (info >= 0) {
+    if (tid == 0) report_bad(st, t, info);
+    return;
+  }
+  for (int64_t e = tid; e < (int64_t)k * k; e += NT) A[e] = (e / k == e % k) ? 1.0 : 0.0;
+}
+
+__global__ void __launch_bounds__(NT) k_prec_scale(LevelDev lv, PrecArgs pa) {
+  extern __shared__ double smem[];
+  const int blk = pa.scale_blk[blockIdx.x];
+  const int g = lv.bg[blk], h = lv.bh[blk];
+  const int kg = lv.gsize[g], kh = lv.gsize[h];
+  double* B = lv.pool + lv.boff[blk];
+  const double* Lg = pa.rec + pa.L_off_of_group[g];
+  const double* Lh = pa.rec + pa.L_off_of_group[h];
+  cta_trsm_left(Lg, kg, kg, B, kh, kh, false, smem);
+  cta_trsm_right_lt(Lh, kh, kh, B, kg, kh, smem);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 3a: interpolative decomposition of A_{R,I}, one wave of mutually
+// independent separators (kernels.py:84-119).
+// CPQR follows LAPACK dgeqp3/dlaqp2 (oracle/dense.py:cpqr_dlaqp2).
+// ---------------------------------------------------------------------------
+struct ArgMax {
+  double v;
+  int i;
+};
+
+__device__ __forceinline__ ArgMax better(ArgMax a, ArgMax b) {
+  // larger value wins; ties -> lower index (idamax returns the first maximum)
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__device__ ArgMax cta_argmax(ArgMax x, double* sred) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = better(x, y);
+  }
+  int* sidx = reinterpret_cast<int*>(sred + 16);
+  __syncthreads();
+  if (lane == 0) {
+    sred[w] = x.v;
+    sidx[w] = x.i;
+  }
+  __syncthreads();
+  ArgMax r{sred[0], sidx[0]};
+  for (int k = 1; k < NT / 32; ++k) r = better(r, ArgMax{sred[k], sidx[k]});
+  __syncthreads();
+  return r;
+}
+
+// Exclusive CTA scan of 0/1 flags; returns this thread's offset, *total = count.
+__device__ int cta_scan_flag(int f, int* sint, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  const int inwarp = __popc(bal & ((1u << lane) - 1u));
+  __syncthreads();
+  if (lane == 0) sint[w] = __popc(bal);
+  __syncthreads();
+  int base = 0, tot = 0;
+  for (int k = 0; k < NT / 32; ++k) {
+    if (k < w) base += sint[k];
+    tot += sint[k];
+  }
+  __syncthreads();
+  *total = tot;
+  return base + inwarp;
+}
+
+// Column-pivoted Householder QR of W (m x k, column-major, ldw), in place.
+__device__ void cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double* vn1, double* vn2, double* sred) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  const double tol3z = sqrt(DBL_EPSILON * 0.5);
+  for (int j = tid; j < k; j += NT) perm[j] = j;
+  for (int j = warp; j < k; j += nw) {
+    const double* c = W + (int64_t)j * ldw;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s += c[r] * c[r];
+    s = warp_sum(s);
+    if (lane == 0) vn1[j] = vn2[j] = sqrt(s);
+  }
+  __syncthreads();
+  const int mn = min(m, k);
+  double* sh = sred + 32;  // [0] tau
+  for (int i = 0; i < mn; ++i) {
+    ArgMax loc{-1.0, 0x7fffffff};
+    for (int j = i + tid; j < k; j += NT) loc = better(loc, ArgMax{vn1[j], j});
+    const int p = cta_argmax(loc, sred).i;
+    if (p != i) {
+      double* ci = W + (int64_t)i * ldw;
+      double* cp = W + (int64_t)p * ldw;
+      for (int r = tid; r < m; r += NT) {
+        const double tmp = ci[r];
+        ci[r] = cp[r];
+        cp[r] = tmp;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const int ti = perm[p];
+        perm[p] = perm[i];
+        perm[i] = ti;
+        vn1[p] = vn1[i];
+        vn2[p] = vn2[i];
+      }
+      __syncthreads();
+    }
+    // Householder reflector for column i, rows i..m-1 (dlarfg)
+    double* ci = W + (int64_t)i * ldw;
+    double part = 0.0;
+    for (int r = i + 1 + tid; r < m; r += NT) part += ci[r] * ci[r];
+    const double xnorm = sqrt(cta_sum(part, sred));
+    const double alpha = ci[i];
+    double tau = 0.0, beta = alpha;
+    if (xnorm != 0.0) {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      const double scal = 1.0 / (alpha - beta);
+      for (int r = i + 1 + tid; r < m; r += NT) ci[r] *= scal;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ci[i] = beta;
+      sh[0] = tau;
+    }
+    __syncthreads();
+    // apply H to trailing columns, then downdate partial norms (dlarf + dlaqp2 loop 10)
+    for (int j = i + 1 + warp; j < k; j += nw) {
+      double* cj = W + (int64_t)j * ldw;
+      if (tau != 0.0) {
+        double s = 0.0;
+        for (int r = i + 1 + lane; r < m; r += 32) s += ci[r] * cj[r];
+        s = warp_sum(s) + cj[i];
+        const double tw = tau * s;
+        __syncwarp();
+        if (lane == 0) cj[i] -= tw;
+        for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= tw * ci[r];
+        __syncwarp();
+      }
+      const double v1 = vn1[j];
+      if (v1 != 0.0) {
+        double tt = fabs(cj[i]) / v1;
+        tt = 1.0 - tt * tt;
+        tt = tt < 0.0 ? 0.0 : tt;
+        const double rr = v1 / vn2[j];
+        const double t2 = tt * rr * rr;
+        if (t2 <= tol3z) {
+          double s = 0.0;
+          if (i < m - 1) {
+            for (int r = i + 1 + lane; r < m; r += 32) s += cj[r] * cj[r];
+            s = sqrt(warp_sum(s));
+          }
+          __syncwarp();
+          if (lane == 0) vn1[j] = vn2[j] = s;
+        } else {
+          __syncwarp();
+          if (lane == 0) vn1[j] = v1 * sqrt(tt);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
+  extern __shared__ double smem[];
+  double* sred = smem + RED_OFF;
+  int* sint = reinterpret_cast<int*>(smem);  // scan scratch (first doubles are free here)
+  const int tid = threadIdx.x;
+  const int s = sk.order[blockIdx.x];
+  const int g = sk.groups[s];
+  const int k = lv.gsize[g];
+  const int64_t gof = lv.goff[g];
+  int64_t rows_max = 0;
+  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) rows_max += lv.gsize[sk.nbr[q]];
+  double* W = sk.work + sk.work_off[s];
+  const int64_t ldw = rows_max > 0 ? rows_max : 1;
+  double* vn1 = W + (int64_t)k * ldw;
+  double* vn2 = vn1 + k;
+  int* iw = sk.iwork + sk.iwork_off[s];
+  int* perm = iw;
+  int* sidx = iw + k;
+  int* flag = iw + 2 * k;
+  // gather A_{R,I}: alive rows of every coupled group, rows with a nonzero entry only
+  int m = 0;
+  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) {
+    const int h = sk.nbr[q], kh = lv.gsize[h];
+    const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+    const bool stored_gh = g < h;   // block(g,h): |g| x |h|, else block(h,g): |h| x |g|
+    const int* hm = lv.mem + lv.goff[h];
+    for (int r0 = 0; r0 < kh; r0 += NT) {
+      const int r = r0 + tid;
+      int keep = 0;
+      if (r < kh && sk.alive[hm[r]]) {
+        for (int c = 0; c < k; ++c) {
+          const double v = stored_gh ? B[(int64_t)c * kh + r] : B[(int64_t)r * k + c];
+          if (v != 0.0) {
+            keep = 1;
+            break;
+          }
+        }
+      }
+      int total;
+      const int off = cta_scan_flag(keep, sint, &total);
+      if (keep) {
+        const int row = m + off;
+        for (int c = 0; c < k; ++c)
+          W[(int64_t)c * ldw + row] = stored_gh ? B[(int64_t)c * kh + r] : B[(int64_t)r * k + c];
+      }
+      m += total;
+    }
+  }
+  __syncthreads();
+  uint8_t* red = sk.red + gof;
+  if (m == 0) {  // no coupling: every column redundant (kernels.py:95-98)
+    for (int j = tid; j < k; j += NT) {
+      red[j] = 1;
+      sk.alive[lv.mem[gof + j]] = 0;
+    }
+    if (tid == 0) sk.rank[s] = 0;
+    return;
+  }
+  cta_cpqr(W, m, k, ldw, perm, vn1, vn2, sred);
+  __shared__ int s_rank;
+  if (tid == 0) {
+    const int mn = min(m, k);
+    const double d0 = fabs(W[0]);
+    const double cut = fmax(sk.eps, DBL_EPSILON * (double)max(m, k)) * d0;
+    int r = 0;
+    for (int i = 0; i < mn; ++i)
+      if (fabs(W[(int64_t)i * ldw + i]) > cut) ++r;
+    s_rank = r;
+    for (int j = 0; j < k; ++j) flag[j] = 0;
+    for (int i = r; i < k; ++i) flag[perm[i]] = 1;
+    int ns = 0, nr = 0;
+    for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns++;
+  }
+  __syncthreads();
+  const int r = s_rank, kt = k - r;
+  // T = R11^-1 R12 (pivot order), in place over R12 columns
+  for (int j = r + tid; j < k; j += NT) {
+    double* cj = W + (int64_t)j * ldw;
+    for (int i = r - 1; i >= 0; --i) {
+      double v = cj[i];
+      for (int l = i + 1; l < r; ++l) v -= W[(int64_t)l * ldw + i] * cj[l];
+      cj[i] = v / W[(int64_t)i * ldw + i];
+    }
+  }
+  __syncthreads();
+  double* T = sk.rec + sk.T_off[s];
+  for (int64_t e = tid; e < (int64_t)r * kt; e += NT) {
+    const int i = (int)(e / kt), j = r + (int)(e % kt);
+    T[(int64_t)sidx[perm[i]] * kt + sidx[perm[j]]] = W[(int64_t)j * ldw + i];
+  }
+  for (int j = tid; j < k; j += NT) {
+    red[j] = (uint8_t)flag[j];
+    if (flag[j]) sk.alive[lv.mem[gof + j]] = 0;
+  }
+  if (tid == 0) sk.rank[s] = r;
+}
+
+// ---------------------------------------------------------------------------
+// Stage 3b: zeroing + elimination of the redundant DOFs.
+// Panel [A~_rr ; A~_sr] ((kt+r) x kt) -> [L~ ; X~^T];  A_ss -= X~^T X~.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, DevStatus* st) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int s = blockIdx.x;
+  const int g = sk.groups[s];
+  const int k = lv.gsize[g];
+  const int r = sk.rank[s], kt = k - r;
+  if (kt == 0) return;
+  const uint8_t* red = sk.red + lv.goff[g];
+  int* iw = sk.iwork + sk.iwork_off[s];
+  int* skl = iw;       // r
+  int* rdl = iw + k;   // kt
+  if (tid == 0) {
+    int a = 0, c = 0;
+    for (int j = 0; j < k; ++j) {
+      if (red[j]) rdl[c++] = j;
+      else skl[a++] = j;
+    }
+  }
+  __syncthreads();
+  double* A = lv.pool + lv.boff[lv.diag_blk[g]];
+  double* Pn = sk.rec + sk.P_off[s];
+  const double* T = sk.rec + sk.T_off[s];
+  double* Ass = sk.work + sk.work_off[s];
+  double* Asr = Ass + (int64_t)r * r;
+  for (int64_t e = tid; e < (int64_t)kt * kt; e += NT) {
+    const int c = (int)(e / kt), d = (int)(e % kt);
+    Pn[e] = A[(int64_t)rdl[c] * k + rdl[d]];
+  }
+  for (int64_t e = tid; e < (int64_t)r * r; e += NT) {
+    const int a = (int)(e / r), b = (int)(e % r);
+    Ass[e] = A[(int64_t)skl[a] * k + skl[b]];
+  }
+  double* Ast = Pn + (int64_t)kt * kt;
+  for (int64_t e = tid; e < (int64_t)r * kt; e += NT) {
+    const int a = (int)(e / kt), c = (int)(e % kt);
+    const double v = A[(int64_t)skl[a] * k + rdl[c]];
+    Asr[e] = v;
+    Ast[e] = v;
+  }
+  __syncthreads();
+  double* gsm = smem + GEMM_OFF;
+  if (r > 0) {
+    cta_gemm<false, false>(r, kt, r, -1.0, Ass, r, T, kt, 1.0, Ast, kt, false, gsm);      // Ast = Asr - Ass T
+    cta_gemm<true, false>(kt, kt, r, -1.0, T, kt, Ast, kt, 1.0, Pn, kt, false, gsm);      // Att -= T^T Ast
+    cta_gemm<true, false>(kt, kt, r, -1.0, Asr, kt, T, kt, 1.0, Pn, kt, false, gsm);      // Att -= Asr^T T
+  }
+  const int info = cta_potrf_panel(Pn, kt + r, kt, kt, smem);
+  if (info >= 0) {
+    if (tid == 0) report_bad(st, s, info);
+    return;
+  }
+  if (r > 0) {
+    cta_gemm<false, true>(r, r, kt, -1.0, Ast, kt, Ast, kt, 1.0, Ass, r, false, gsm);     // A_ss -= X~^T X~
+    for (int64_t e = tid; e < (int64_t)r * r; e += NT) {
+      const int a = (int)(e / r), b = (int)(e % r);
+      A[(int64_t)skl[a] * k + skl[b]] = Ass[e];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Level transition: carry the surviving live matrix into the next grouping.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_repack(RepackArgs ra) {
+  const int b = blockIdx.x;
+  const int G = ra.nbg[b], H = ra.nbh[b];
+  const int64_t oG = ra.ngoff[G], oH = ra.ngoff[H];
+  const int rows = (int)(ra.ngoff[G + 1] - oG), cols = (int)(ra.ngoff[H + 1] - oH);
+  double* dst = ra.npool + ra.nboff[b];
+  for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += NT) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    const int og = ra.nsrc_group[oG + i], pi = ra.nsrc_pos[oG + i];
+    const int oh = ra.nsrc_group[oH + j], pj = ra.nsrc_pos[oH + j];
+    double v = 0.0;
+    if (og <= oh) {
+      const int blk = find_blk(ra.oadj_off, ra.oadj_nbr, ra.oadj_blk, og, oh);
+      if (blk >= 0) v = ra.opool[ra.oboff[blk] + (int64_t)pi * ra.ogsize[oh] + pj];
+    } else {
+      const int blk = find_blk(ra.oadj_off, ra.oadj_nbr, ra.oadj_blk, oh, og);
+      if (blk >= 0) v = ra.opool[ra.oboff[blk] + (int64_t)pj * ra.ogsize[og] + pi];
+    }
+    dst[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Record replay (apply F^-1, G^-1, G^-T)
+// x is N x k row-major (DOF-major, right-hand sides contiguous).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gather_rows(double* Y, const double* x, const int* idx, int n, int k) {
+  for (int64_t e = threadIdx.x; e < (int64_t)n * k; e += NT) Y[e] = x[(int64_t)idx[e / k] * k + e % k];
+}
+__device__ __forceinline__ void scatter_rows(double* x, const double* Y, const int* idx, int n, int k) {
+  for (int64_t e = threadIdx.x; e < (int64_t)n * k; e += NT) x[(int64_t)idx[e / k] * k + e % k] = Y[e];
+}
+
+__global__ void __launch_bounds__(NT) k_apply_cell(ApplyCellArgs a, double* x, int k, int up) {
+  extern __shared__ double smem[];
+  const int t = blockIdx.x;
+  const int n = a.n[t], b = a.b[t];
+  const int* I = a.I + a.I_off[t];
+  const int* B = a.B + a.B_off[t];
+  const double* P = a.rec + a.P_off[t];
+  double* Y = a.work + a.work_off[t] * k;
+  gather_rows(Y, x, I, n, k);
+  __syncthreads();
+  if (up) {
+    cta_trsm_left(P, n, n, Y, k, k, false, smem);
+    scatter_rows(x, Y, I, n, k);
+    if (b > 0)
+      cta_gemm<false, false>(b, k, n, 1.0, P + (int64_t)n * n, n, Y, k, 0.0, a.wbuf + a.B_off[t] * k, k, false,
+                             smem + GEMM_OFF);
+  } else {
+    if (b > 0) {
+      double* Z = Y + (int64_t)n * k;
+      gather_rows(Z, x, B, b, k);
+      __syncthreads();
+      cta_gemm<true, false>(n, k, b, -1.0, P + (int64_t)n * n, n, Z, k, 1.0, Y, k, false, smem + GEMM_OFF);
+    }
+    cta_trsm_left(P, n, n, Y, k, k, true, smem);
+    scatter_rows(x, Y, I, n, k);
+  }
+}
+
+// x_B -= sum of cell contributions, fixed cell order per boundary DOF
+__global__ void k_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd,
+                               double* x, int k) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nd * k) return;
+  const int i = (int)(e / k), c = (int)(e % k);
+  double s = x[(int64_t)dof[i] * k + c];
+  for (int64_t q = off[i]; q < off[i + 1]; ++q) s -= wbuf[(int64_t)rows[q] * k + c];
+  x[(int64_t)dof[i] * k + c] = s;
+}
+
+__global__ void __launch_bounds__(NT) k_apply_prec(ApplyPrecArgs a, double* x, int k, int up) {
+  extern __shared__ double smem[];
+  const int t = blockIdx.x;
+  const int n = a.n[t];
+  const int* I = a.I + a.I_off[t];
+  double* Y = a.work + a.work_off[t] * k;
+  gather_rows(Y, x, I, n, k);
+  __syncthreads();
+  cta_trsm_left(a.rec + a.L_off[t], n, n, Y, k, k, !up, smem);
+  scatter_rows(x, Y, I, n, k);
+}
+
+__global__ void __launch_bounds__(NT) k_apply_skel(ApplySkelArgs a, double* x, int k, int up) {
+  extern __shared__ double smem[];
+  const int t = blockIdx.x;
+  const int r = a.r[t], kt = a.kt[t];
+  if (kt == 0) return;
+  const int* S = a.S + a.S_off[t];
+  const int* R = a.R + a.R_off[t];
+  const double* T = a.rec + a.T_off[t];
+  const double* P = a.rec + a.P_off[t];
+  const double* PB = P + (int64_t)kt * kt;
+  double* Ys = a.work + a.work_off[t] * k;
+  double* Yr = Ys + (int64_t)r * k;
+  gather_rows(Ys, x, S, r, k);
+  gather_rows(Yr, x, R, kt, k);
+  __syncthreads();
+  double* gsm = smem + GEMM_OFF;
+  if (up) {
+    if (r > 0) cta_gemm<true, false>(kt, k, r, -1.0, T, kt, Ys, k, 1.0, Yr, k, false, gsm);
+    cta_trsm_left(P, kt, kt, Yr, k, k, false, smem);
+    if (r > 0) cta_gemm<false, false>(r, k, kt, -1.0, PB, kt, Yr, k, 1.0, Ys, k, false, gsm);
+  } else {
+    if (r > 0) cta_gemm<true, false>(kt, k, r, -1.0, PB, kt, Ys, k, 1.0, Yr, k, false, gsm);
+    cta_trsm_left(P, kt, kt, Yr, k, k, true, smem);
+    if (r > 0) cta_gemm<false, false>(r, k, kt, -1.0, T, kt, Yr, k, 1.0, Ys, k, false, gsm);
+  }
+  scatter_rows(x, Ys, S, r, k);
+  scatter_rows(x, Yr, R, kt, k);
+}
+
+// ---------------------------------------------------------------------------
+// Krylov vector kernels (x is N x k row-major)
+// ---------------------------------------------------------------------------
+__global__ void k_spmv(const int64_t* rowptr, const int* col, const double* val, const double* x, double* y,
+                       int64_t N, int k) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * k) return;
+  const int64_t r = e / k;
+  const int c = (int)(e % k);
+  double s = 0.0;
+  for (int64_t q = rowptr[r]; q < rowptr[r + 1]; ++q) s += val[q] * x[(int64_t)col[q] * k + c];
+  y[e] = s;
+}
+
+// per-block partial column dot products: part[blk*k + c] = sum over the block's rows
+__global__ void k_dot_part(const double* a, const double* b, int64_t N, int k, double* part) {
+  extern __shared__ double sh[];
+  const int c = threadIdx.x % k;           // blockDim.x is a multiple of k
+  const int lanes = blockDim.x / k;
+  const int row0 = threadIdx.x / k;
+  double s = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * lanes + row0; r < N; r += (int64_t)gridDim.x * lanes)
+    s += a[r * k + c] * b[r * k + c];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double t = 0.0;
+    for (int l = 0; l < lanes; ++l) t += sh[l * k + threadIdx.x];
+    part[(int64_t)blockIdx.x * k + threadIdx.x] = t;
+  }
+}
+
+__global__ void k_dot_final(const double* part, int nblk, int k, double* out) {
+  const int c = threadIdx.x;
+  if (c >= k) return;
+  double t = 0.0;
+  for (int b = 0; b < nblk; ++b) t += part[(int64_t)b * k + c];
+  out[c] = t;
+}
+
+// y[:,c] += s * coef[c] * x[:,c] for active columns
+__global__ void k_axpy(double* y, const double* x, const double* coef, double s, const int* active, int64_t N,
+                       int k) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * k) return;
+  const int c = (int)(e % k);
+  if (active && !active[c]) return;
+  y[e] += s * coef[c] * x[e];
+}
+
+// p[:,c] = z[:,c] + coef[c] * p[:,c] for active columns
+__global__ void k_xpby(double* p, const double* z, const double* coef, const int* active, int64_t N, int k) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * k) return;
+  const int c = (int)(e % k);
+  if (active && !active[c]) return;
+  p[e] = z[e] + coef[c] * p[e];
+}
+
+// r[:,c] = b[:,c] - q[:,c] for active columns
+__global__ void k_sub(double* r, const double* b, const double* q, const int* active, int64_t N, int k) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * k) return;
+  const int c = (int)(e % k);
+  if (active && !active[c]) return;
+  r[e] = b[e] - q[e];
+}
+
+// out[c] = num[c] / den[c] for active, else 0
+__global__ void k_ratio(const double* num, const double* den, const int* active, double* out, int k) {
+  const int c = threadIdx.x;
+  if (c >= k) return;
+  out[c] = (active == nullptr || active[c]) ? num[c] / den[c] : 0.0;
+}
+
+// y = x - y (power iteration residual), y /= scale handled by k_scale
+__global__ void k_xmy(double* y, const double* x, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) y[e] = x[e] - y[e];
+}
+
+__global__ void k_scale(double* y, const double* x, const double* nrm2, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) y[e] = x[e] / sqrt(nrm2[0]);
+}
+
+// ---------------------------------------------------------------------------
+// Launch wrappers
+// ---------------------------------------------------------------------------
+static constexpr size_t SMEM_BYTES = (size_t)SMEM_DOUBLES * sizeof(double);
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
+                   const double* val, int64_t N, cudaStream_t s) {
+  if (N == 0) return;
+  k_ingest<<<nblk(N, 256), 256, 0, s>>>(lv, gid, pos, rowptr, col, val, N);
+}
+void launch_cell(const LevelDev& lv, const CellArgs& a, DevStatus* st, cudaStream_t s) {
+  if (a.p == 0) return;
+  k_cell<<<a.p, NT, SMEM_BYTES, s>>>(lv, a, st);
+}
+void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s) {
+  if (a.ntgt == 0) return;
+  k_schur<<<a.ntgt, NT, 0, s>>>(lv, a);
+}
+void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s) {
+  if (a.r == 0) return;
+  k_prec_factor<<<a.r, NT, SMEM_BYTES, s>>>(lv, a, st);
+}
+void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
+  if (a.nscale == 0) return;
+  k_prec_scale<<<a.nscale, NT, SMEM_BYTES, s>>>(lv, a);
+}
+void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s) {
+  if (count == 0) return;
+  k_skel_id<<<count, NT, SMEM_BYTES, s>>>(lv, a);
+}
+void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s) {
+  if (a.nsk == 0) return;
+  k_skel_update<<<a.nsk, NT, SMEM_BYTES, s>>>(lv, a, st);
+}
+void launch_repack(const RepackArgs& a, cudaStream_t s) {
+  if (a.nblk == 0) return;
+  k_repack<<<a.nblk, NT, 0, s>>>(a);
+}
+void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s) {
+  if (a.p == 0) return;
+  k_apply_cell<<<a.p, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
+}
+void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd, double* x,
+                         int k, cudaStream_t s) {
+  if (nd == 0) return;
+  k_apply_reduce<<<nblk((int64_t)nd * k, 256), 256, 0, s>>>(dof, off, rows, wbuf, nd, x, k);
+}
+void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s) {
+  if (a.r == 0) return;
+  k_apply_prec<<<a.r, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
+}
+void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s) {
+  if (a.nsk == 0) return;
+  k_apply_skel<<<a.nsk, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
+}
+void launch_spmv(const int64_t* rowptr, const int* col, const double* val, const double* x, double* y, int64_t N,
+                 int k, cudaStream_t s) {
+  k_spmv<<<nblk(N * k, 256), 256, 0, s>>>(rowptr, col, val, x, y, N, k);
+}
+int dot_part_blocks() { return 592; }
+void launch_dot(const double* a, const double* b, int64_t N, int k, double* part, double* out, cudaStream_t s) {
+  const int threads = (256 / k) * k;
+  const int blocks = dot_part_blocks();
+  k_dot_part<<<blocks, threads, threads * sizeof(double), s>>>(a, b, N, k, part);
+  k_dot_final<<<1, 32 * ((k + 31) / 32), 0, s>>>(part, blocks, k, out);
+}
+void launch_axpy(double* y, const double* x, const double* coef, double sgn, const int* active, int64_t N, int k,
+                 cudaStream_t s) {
+  k_axpy<<<nblk(N * k, 256), 256, 0, s>>>(y, x, coef, sgn, active, N, k);
+}
+void launch_xpby(double* p, const double* z, const double* coef, const int* active, int64_t N, int k,
+                 cudaStream_t s) {
+  k_xpby<<<nblk(N * k, 256), 256, 0, s>>>(p, z, coef, active, N, k);
+}
+void launch_sub(double* r, const double* b, const double* q, const int* active, int64_t N, int k, cudaStream_t s) {
+  k_sub<<<nblk(N * k, 256), 256, 0, s>>>(r, b, q, active, N, k);
+}
+void launch_ratio(const double* num, const double* den, const int* active, double* out, int k, cudaStream_t s) {
+  k_ratio<<<1, 32 * ((k + 31) / 32), 0, s>>>(num, den, active, out, k);
+}
+void launch_xmy(double* y, const double* x, int64_t n, cudaStream_t s) { k_xmy<<<nblk(n, 256), 256, 0, s>>>(y, x, n); }
+void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cudaStream_t s) {
+  k_scale<<<nblk(n, 256), 256, 0, s>>>(y, x, nrm2, n);
+}
+
+void configure_kernels() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const int bytes = (int)SMEM_BYTES;
+  cudaFuncSetAttribute(k_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_prec_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_prec_scale, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_skel_id, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_skel_update, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_apply_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_apply_prec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_apply_skel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace phif

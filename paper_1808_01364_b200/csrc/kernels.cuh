@@ -1,0 +1,106 @@
+// Kernel parameter blocks and launch wrappers of the B200 PHIF engine.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace phif {
+
+// Status word: (op << 32 | pivot) of the lowest failing op; ~0ull when none.
+struct DevStatus {
+  unsigned long long first_bad;
+};
+
+struct LevelDev {
+  // groups
+  int G;
+  const int64_t* goff;   // G+1
+  const int* mem;        // members
+  const int* gsize;      // G
+  // blocks
+  double* pool;
+  const int64_t* boff;
+  const int* bg;
+  const int* bh;
+  const int64_t* adj_off;
+  const int* adj_nbr;
+  const int* adj_blk;
+  const int* diag_blk;   // per group: block id of (g,g)
+};
+
+struct CellArgs {
+  int p;
+  const int* interior;      // group ids
+  const int64_t* nbr_off;   // p+1
+  const int* nbr_blk;
+  const int* nbr_col;
+  const int* nbr_w;
+  const int* n;
+  const int* b;
+  double* rec;              // record pool
+  const int64_t* P_off;     // panel (n+b) x n
+  double* U;                // Schur workspace
+  const int64_t* U_off;     // b x b
+};
+
+struct SchurArgs {
+  int ntgt;
+  const int* tgt_blk;
+  const int64_t* tgt_off;
+  const int* con_cell;
+  const int* con_row;
+  const int* con_col;
+  const int* cell_b;
+  const double* U;
+  const int64_t* U_off;
+};
+
+struct PrecArgs {
+  int r;
+  const int* groups;
+  double* rec;
+  const int64_t* L_off;           // per precond index
+  const int64_t* L_off_of_group;  // per group id (-1 if none)
+  int nscale;
+  const int* scale_blk;
+};
+
+struct SkelArgs {
+  int nsk;
+  const int* groups;         // skeleton group ids
+  const int64_t* nbr_off;
+  const int* nbr;
+  const int* nbr_blk;
+  const int* order;          // wave order slice
+  int* alive;                // per DOF (global)
+  uint8_t* red;              // per member position of the level (1 = redundant)
+  int* rank;                 // per skeleton
+  double eps;
+  double* work;              // per skeleton workspace
+  const int64_t* work_off;
+  int* iwork;
+  const int64_t* iwork_off;
+  double* rec;
+  const int64_t* T_off;      // r x kt
+  const int64_t* P_off;      // (kt + r) x kt
+};
+
+struct RepackArgs {
+  int nblk;
+  // new level
+  const int* nbg;
+  const int* nbh;
+  const int64_t* nboff;
+  const int64_t* ngoff;
+  const int* nsrc_group;   // per new member
+  const int* nsrc_pos;
+  double* npool;
+  // old level
+  const double* opool;
+  const int64_t* oboff;
+  const int64_t* oadj_off;
+  const int* oadj_nbr;
+  const int* oadj_blk;
+  const int* ogsize;
+};
+
+}  // namespace phif

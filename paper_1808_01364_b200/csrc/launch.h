@@ -1,0 +1,79 @@
+// Host-callable launch wrappers (implemented in kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+
+namespace phif {
+
+struct ApplyCellArgs {
+  int p;
+  const int* n;
+  const int* b;
+  const int* I;
+  const int64_t* I_off;
+  const int* B;
+  const int64_t* B_off;   // also the row offset of the cell's contribution inside wbuf
+  const double* rec;
+  const int64_t* P_off;
+  double* work;
+  const int64_t* work_off;  // (n+b) * k doubles per cell (scaled by k on the host)
+  double* wbuf;
+};
+
+struct ApplyPrecArgs {
+  int r;
+  const int* n;
+  const int* I;
+  const int64_t* I_off;
+  const double* rec;
+  const int64_t* L_off;
+  double* work;
+  const int64_t* work_off;
+};
+
+struct ApplySkelArgs {
+  int nsk;
+  const int* r;
+  const int* kt;
+  const int* S;
+  const int64_t* S_off;
+  const int* R;
+  const int64_t* R_off;
+  const double* rec;
+  const int64_t* T_off;
+  const int64_t* P_off;
+  double* work;
+  const int64_t* work_off;
+};
+
+void configure_kernels();
+void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
+                   const double* val, int64_t N, cudaStream_t s);
+void launch_cell(const LevelDev& lv, const CellArgs& a, DevStatus* st, cudaStream_t s);
+void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s);
+void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s);
+void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
+void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s);
+void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s);
+void launch_repack(const RepackArgs& a, cudaStream_t s);
+void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s);
+void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd, double* x,
+                         int k, cudaStream_t s);
+void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s);
+void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s);
+void launch_spmv(const int64_t* rowptr, const int* col, const double* val, const double* x, double* y, int64_t N,
+                 int k, cudaStream_t s);
+int dot_part_blocks();
+void launch_dot(const double* a, const double* b, int64_t N, int k, double* part, double* out, cudaStream_t s);
+void launch_axpy(double* y, const double* x, const double* coef, double sgn, const int* active, int64_t N, int k,
+                 cudaStream_t s);
+void launch_xpby(double* p, const double* z, const double* coef, const int* active, int64_t N, int k,
+                 cudaStream_t s);
+void launch_sub(double* r, const double* b, const double* q, const int* active, int64_t N, int k, cudaStream_t s);
+void launch_ratio(const double* num, const double* den, const int* active, double* out, int k, cudaStream_t s);
+void launch_xmy(double* y, const double* x, int64_t n, cudaStream_t s);
+void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cudaStream_t s);
+
+}  // namespace phif

@@ -1,0 +1,398 @@
+// Host-side level planner (see planner.h).
+#include "planner.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <numeric>
+#include <sstream>
+#include <stdexcept>
+
+namespace phif {
+
+void Spec::init(int d, int nn, int mm) {
+  dim = d;
+  n = nn;
+  m = mm;
+  int cells = n / m, l = 0;
+  while ((1 << (l + 1)) <= cells) ++l;
+  L = l;
+  N = 1;
+  for (int i = 0; i < dim; ++i) N *= (n - 1);
+}
+
+namespace {
+
+struct KeyInfo {
+  int per, sz;
+};
+
+inline void coords_of(const Spec& s, int64_t dof, int c[3]) {
+  const int64_t side = s.n - 1;
+  c[0] = (int)(dof % side) + 1;
+  c[1] = (int)((dof / side) % side) + 1;
+  c[2] = s.dim == 3 ? (int)(dof / (side * side)) + 1 : 0;
+}
+
+// group key (x-major cell index, kind bits last), hierarchy.py:124-133
+inline int64_t key_of(const Spec& s, int level, int64_t dof, int q[3], int& bits) {
+  const int sz = s.m << level, per = s.n / sz;
+  int c[3];
+  coords_of(s, dof, c);
+  bits = 0;
+  int64_t key = 0;
+  for (int d = 0; d < s.dim; ++d) {
+    q[d] = c[d] / sz;
+    if (c[d] % sz == 0) bits |= 1 << d;
+    key = key * per + q[d];
+  }
+  return (key << s.dim) | bits;
+}
+
+inline int popc(int b) { return __builtin_popcount((unsigned)b); }
+
+void finalize_groups(const Spec& s, Groups& g, const std::vector<int64_t>& keys_sorted_members,
+                     const std::vector<int64_t>& key_of_group) {
+  (void)keys_sorted_members;
+  g.G = (int)key_of_group.size();
+  g.q.assign(3 * (size_t)g.G, 0);
+  g.bits.assign(g.G, 0);
+  g.kind.assign(g.G, 0);
+  for (int i = 0; i < g.G; ++i) {
+    int q[3] = {0, 0, 0}, b = 0;
+    key_of(s, g.level, g.mem[g.off[i]], q, b);
+    for (int d = 0; d < 3; ++d) g.q[3 * i + d] = q[d];
+    g.bits[i] = b;
+    g.kind[i] = popc(b);
+  }
+}
+
+}  // namespace
+
+Groups classify_all(const Spec& s) {
+  Groups g;
+  g.level = 0;
+  const int sz = s.m, per = s.n / sz;
+  int64_t nkeys = 1;
+  for (int d = 0; d < s.dim; ++d) nkeys *= per;
+  nkeys <<= s.dim;
+  std::vector<int> key(s.N);
+  std::vector<int64_t> cnt(nkeys + 1, 0);
+  for (int64_t i = 0; i < s.N; ++i) {
+    int q[3], b;
+    key[i] = (int)key_of(s, 0, i, q, b);
+    cnt[key[i] + 1]++;
+  }
+  for (int64_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+  g.mem.resize(s.N);
+  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+  for (int64_t i = 0; i < s.N; ++i) g.mem[fill[key[i]]++] = (int)i;
+  std::vector<int64_t> gkeys;
+  g.off.clear();
+  for (int64_t k = 0; k < nkeys; ++k)
+    if (cnt[k + 1] > cnt[k]) {
+      gkeys.push_back(k);
+      g.off.push_back(cnt[k]);
+    }
+  g.off.push_back(s.N);
+  finalize_groups(s, g, {}, gkeys);
+  return g;
+}
+
+Groups classify_set(const Spec& s, int level, const std::vector<int>& active) {
+  Groups g;
+  g.level = level;
+  std::vector<std::pair<int64_t, int>> items;
+  items.reserve(active.size());
+  for (int dof : active) {
+    if (dof < 0 || dof >= s.N) throw std::runtime_error("classify: DOF outside the domain");
+    int q[3], b;
+    items.emplace_back(key_of(s, level, dof, q, b), dof);
+  }
+  std::sort(items.begin(), items.end());
+  std::vector<int64_t> gkeys;
+  g.mem.resize(items.size());
+  for (size_t i = 0; i < items.size(); ++i) {
+    if (i == 0 || items[i].first != items[i - 1].first) {
+      gkeys.push_back(items[i].first);
+      g.off.push_back((int64_t)i);
+    }
+    g.mem[i] = items[i].second;
+  }
+  g.off.push_back((int64_t)items.size());
+  finalize_groups(s, g, {}, gkeys);
+  return g;
+}
+
+Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_t>& alive) {
+  Groups g;
+  g.level = prev.level + 1;
+  struct Item {
+    int64_t key;
+    int dof, src, pos;
+  };
+  std::vector<Item> items;
+  items.reserve(prev.mem.size());
+  for (int pg = 0; pg < prev.G; ++pg)
+    for (int64_t p = prev.off[pg]; p < prev.off[pg + 1]; ++p)
+      if (alive[p]) {
+        int q[3], b;
+        const int dof = prev.mem[p];
+        items.push_back({key_of(s, g.level, dof, q, b), dof, pg, (int)(p - prev.off[pg])});
+      }
+  std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+    return a.key != b.key ? a.key < b.key : a.dof < b.dof;
+  });
+  std::vector<int64_t> gkeys;
+  g.mem.resize(items.size());
+  g.src_group.resize(items.size());
+  g.src_pos.resize(items.size());
+  for (size_t i = 0; i < items.size(); ++i) {
+    if (i == 0 || items[i].key != items[i - 1].key) {
+      gkeys.push_back(items[i].key);
+      g.off.push_back((int64_t)i);
+    }
+    g.mem[i] = items[i].dof;
+    g.src_group[i] = items[i].src;
+    g.src_pos[i] = items[i].pos;
+  }
+  g.off.push_back((int64_t)items.size());
+  finalize_groups(s, g, {}, gkeys);
+  return g;
+}
+
+int Pattern::find(int g, int h) const {
+  if (g > h) std::swap(g, h);
+  const int* b = adj_nbr.data() + adj_off[g];
+  const int* e = adj_nbr.data() + adj_off[g + 1];
+  const int* it = std::lower_bound(b, e, h);
+  if (it == e || *it != h) return -1;
+  return adj_blk[adj_off[g] + (it - adj_nbr.data() - adj_off[g])];
+}
+
+std::vector<std::pair<int, int>> pattern_from_csr(const Groups& g, int64_t N, const int64_t* rowptr,
+                                                  const int* col) {
+  std::vector<int> gid(N, -1);
+  for (int i = 0; i < g.G; ++i)
+    for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) gid[g.mem[p]] = i;
+  std::vector<int> last(g.G, -1);
+  std::vector<std::pair<int, int>> pairs;
+  pairs.reserve(g.G * 8);
+  for (int i = 0; i < g.G; ++i)
+    for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) {
+      const int r = g.mem[p];
+      for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+        const int h = gid[col[e]];
+        if (h >= i && last[h] != i) {
+          last[h] = i;
+          pairs.emplace_back(i, h);
+        }
+      }
+    }
+  return pairs;
+}
+
+std::vector<std::pair<int, int>> pattern_next(const LevelPlan& prev, const Groups& next) {
+  std::vector<int> old2new(prev.grp.G, -1);
+  for (int G = 0; G < next.G; ++G)
+    for (int64_t p = next.off[G]; p < next.off[G + 1]; ++p) {
+      const int og = next.src_group[p];
+      if (old2new[og] >= 0 && old2new[og] != G)
+        throw std::runtime_error("planner: an old group split across new groups");
+      old2new[og] = G;
+    }
+  std::vector<std::pair<int, int>> pairs;
+  pairs.reserve(prev.pat.bg.size());
+  for (size_t b = 0; b < prev.pat.bg.size(); ++b) {
+    const int og = prev.pat.bg[b], oh = prev.pat.bh[b];
+    if (prev.grp.kind[og] == 0 || prev.grp.kind[oh] == 0) continue;
+    const int G = old2new[og], H = old2new[oh];
+    if (G < 0 || H < 0) continue;
+    pairs.emplace_back(std::min(G, H), std::max(G, H));
+  }
+  return pairs;
+}
+
+static void sort_unique(std::vector<std::pair<int, int>>& v) {
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+}
+
+static void build_adjacency(int G, const std::vector<std::pair<int, int>>& pairs, Pattern& pat) {
+  pat.bg.resize(pairs.size());
+  pat.bh.resize(pairs.size());
+  std::vector<int64_t> deg(G + 1, 0);
+  for (size_t b = 0; b < pairs.size(); ++b) {
+    pat.bg[b] = pairs[b].first;
+    pat.bh[b] = pairs[b].second;
+    deg[pairs[b].first + 1]++;
+    if (pairs[b].first != pairs[b].second) deg[pairs[b].second + 1]++;
+  }
+  for (int i = 0; i < G; ++i) deg[i + 1] += deg[i];
+  pat.adj_off = deg;
+  pat.adj_nbr.assign(deg[G], 0);
+  pat.adj_blk.assign(deg[G], 0);
+  std::vector<int64_t> fill(deg.begin(), deg.end() - 1);
+  // pairs are sorted by (g,h): for each g, entries (g,h) arrive in ascending h, but the
+  // reverse entries (h -> g) interleave, so sort each row afterwards
+  for (size_t b = 0; b < pairs.size(); ++b) {
+    const int g = pairs[b].first, h = pairs[b].second;
+    pat.adj_nbr[fill[g]] = h;
+    pat.adj_blk[fill[g]++] = (int)b;
+    if (g != h) {
+      pat.adj_nbr[fill[h]] = g;
+      pat.adj_blk[fill[h]++] = (int)b;
+    }
+  }
+  std::vector<std::pair<int, int>> tmp;
+  for (int g = 0; g < G; ++g) {
+    const int64_t a = deg[g], e = deg[g + 1];
+    tmp.clear();
+    for (int64_t p = a; p < e; ++p) tmp.emplace_back(pat.adj_nbr[p], pat.adj_blk[p]);
+    std::sort(tmp.begin(), tmp.end());
+    for (int64_t p = a; p < e; ++p) {
+      pat.adj_nbr[p] = tmp[p - a].first;
+      pat.adj_blk[p] = tmp[p - a].second;
+    }
+  }
+}
+
+void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> pairs) {
+  Groups& g = lp.grp;
+  lp.level = g.level;
+  lp.root = (g.level == s.L);
+  for (int i = 0; i < g.G; ++i) pairs.emplace_back(i, i);
+  sort_unique(pairs);
+  Pattern in;
+  build_adjacency(g.G, pairs, in);
+  lp.interior.clear();
+  lp.precond.clear();
+  lp.skeleton.clear();
+  for (int i = 0; i < g.G; ++i) {
+    if (g.kind[i] == 0) {
+      lp.interior.push_back(i);
+    } else {
+      lp.precond.push_back(i);
+      if (g.kind[i] == 1) lp.skeleton.push_back(i);
+    }
+  }
+  // elimination fill among each cell's boundary groups
+  for (int I : lp.interior) {
+    std::vector<int> nb;
+    for (int64_t p = in.adj_off[I]; p < in.adj_off[I + 1]; ++p)
+      if (in.adj_nbr[p] != I) {
+        if (g.kind[in.adj_nbr[p]] == 0) throw std::runtime_error("planner: two interior groups coupled");
+        nb.push_back(in.adj_nbr[p]);
+      }
+    for (size_t a = 0; a < nb.size(); ++a)
+      for (size_t b = a; b < nb.size(); ++b) pairs.emplace_back(nb[a], nb[b]);
+  }
+  sort_unique(pairs);
+  build_adjacency(g.G, pairs, lp.pat);
+  const Pattern& pat = lp.pat;
+  // pool
+  lp.boff.resize(pat.bg.size());
+  int64_t acc = 0;
+  for (size_t b = 0; b < pat.bg.size(); ++b) {
+    lp.boff[b] = acc;
+    acc += (int64_t)g.size(pat.bg[b]) * g.size(pat.bh[b]);
+  }
+  lp.pool_doubles = acc;
+  // cells
+  const int p = (int)lp.interior.size();
+  lp.cell_nbr_off.assign(1, 0);
+  lp.cell_nbr.clear();
+  lp.cell_nbr_blk.clear();
+  lp.cell_nbr_col.clear();
+  lp.cell_n.assign(p, 0);
+  lp.cell_b.assign(p, 0);
+  struct Con {
+    int tgt, cell, row, col;
+  };
+  std::vector<Con> cons;
+  for (int t = 0; t < p; ++t) {
+    const int I = lp.interior[t];
+    int bcols = 0;
+    const int64_t first = (int64_t)lp.cell_nbr.size();
+    for (int64_t q = pat.adj_off[I]; q < pat.adj_off[I + 1]; ++q) {
+      const int h = pat.adj_nbr[q];
+      if (h == I) continue;
+      if (h < I) throw std::runtime_error("planner: interior group is not first in its closure");
+      lp.cell_nbr.push_back(h);
+      lp.cell_nbr_blk.push_back(pat.adj_blk[q]);
+      lp.cell_nbr_col.push_back(bcols);
+      bcols += g.size(h);
+    }
+    lp.cell_nbr_off.push_back((int64_t)lp.cell_nbr.size());
+    lp.cell_n[t] = g.size(I);
+    lp.cell_b[t] = bcols;
+    const int64_t last = (int64_t)lp.cell_nbr.size();
+    for (int64_t a = first; a < last; ++a)
+      for (int64_t b = a; b < last; ++b) {
+        const int blk = pat.find(lp.cell_nbr[a], lp.cell_nbr[b]);
+        if (blk < 0) throw std::runtime_error("planner: missing fill block");
+        cons.push_back({blk, t, lp.cell_nbr_col[a], lp.cell_nbr_col[b]});
+      }
+  }
+  std::stable_sort(cons.begin(), cons.end(), [](const Con& a, const Con& b) { return a.tgt < b.tgt; });
+  lp.tgt_blk.clear();
+  lp.tgt_off.assign(1, 0);
+  lp.con_cell.resize(cons.size());
+  lp.con_row.resize(cons.size());
+  lp.con_col.resize(cons.size());
+  for (size_t i = 0; i < cons.size(); ++i) {
+    if (i == 0 || cons[i].tgt != cons[i - 1].tgt) {
+      if (i) lp.tgt_off.push_back((int64_t)i);
+      lp.tgt_blk.push_back(cons[i].tgt);
+    }
+    lp.con_cell[i] = cons[i].cell;
+    lp.con_row[i] = cons[i].row;
+    lp.con_col[i] = cons[i].col;
+  }
+  if (!cons.empty()) lp.tgt_off.push_back((int64_t)cons.size());
+  // block Jacobi scaling targets
+  lp.scale_blk.clear();
+  for (size_t b = 0; b < pat.bg.size(); ++b)
+    if (pat.bg[b] != pat.bh[b] && g.kind[pat.bg[b]] != 0 && g.kind[pat.bh[b]] != 0) lp.scale_blk.push_back((int)b);
+  // skeleton neighbours + dependency waves (sequential semantics)
+  const int nsk = (int)lp.skeleton.size();
+  std::vector<int> sk_index(g.G, -1);
+  for (int i = 0; i < nsk; ++i) sk_index[lp.skeleton[i]] = i;
+  lp.sk_nbr_off.assign(1, 0);
+  lp.sk_nbr.clear();
+  lp.sk_nbr_blk.clear();
+  lp.sk_wave.assign(nsk, 0);
+  lp.nwaves = 0;
+  for (int i = 0; i < nsk; ++i) {
+    const int gg = lp.skeleton[i];
+    int w = 0;
+    for (int64_t q = pat.adj_off[gg]; q < pat.adj_off[gg + 1]; ++q) {
+      const int h = pat.adj_nbr[q];
+      if (h == gg || g.kind[h] == 0) continue;
+      lp.sk_nbr.push_back(h);
+      lp.sk_nbr_blk.push_back(pat.adj_blk[q]);
+      const int j = sk_index[h];
+      if (j >= 0 && j < i) w = std::max(w, lp.sk_wave[j] + 1);
+    }
+    lp.sk_nbr_off.push_back((int64_t)lp.sk_nbr.size());
+    lp.sk_wave[i] = w;
+    lp.nwaves = std::max(lp.nwaves, w + 1);
+  }
+  lp.wave_order.resize(nsk);
+  std::iota(lp.wave_order.begin(), lp.wave_order.end(), 0);
+  std::stable_sort(lp.wave_order.begin(), lp.wave_order.end(),
+                   [&](int a, int b) { return lp.sk_wave[a] < lp.sk_wave[b]; });
+  lp.wave_off.assign(lp.nwaves + 1, 0);
+  for (int i = 0; i < nsk; ++i) lp.wave_off[lp.sk_wave[i] + 1]++;
+  for (int w = 0; w < lp.nwaves; ++w) lp.wave_off[w + 1] += lp.wave_off[w];
+}
+
+std::string level_json(const LevelPlan& lp) {
+  std::ostringstream o;
+  o << "{\"level\":" << lp.level << ",\"G\":" << lp.grp.G << ",\"S\":" << lp.grp.mem.size()
+    << ",\"p\":" << lp.interior.size() << ",\"q\":" << lp.skeleton.size() << ",\"r\":" << lp.precond.size()
+    << ",\"blocks\":" << lp.pat.bg.size() << ",\"pool_doubles\":" << lp.pool_doubles
+    << ",\"waves\":" << lp.nwaves << "}";
+  return o.str();
+}
+
+}  // namespace phif
