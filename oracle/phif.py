@@ -217,6 +217,103 @@ def _regroup(old: _Store, groups, N):
     return new
 
 
+def store_from_dense(A, groups):
+    """Block store of a dense symmetric matrix for the given index groups (test helper)."""
+    A = np.asarray(A, dtype=np.float64)
+    st = _Store([np.asarray(g, dtype=np.int64) for g in groups])
+    for g in range(len(groups)):
+        for h in range(g, len(groups)):
+            blk = A[np.ix_(st.members[g], st.members[h])]
+            if np.any(blk != 0.0) or g == h:
+                st.put(g, h, blk.copy())
+    return st
+
+
+def store_to_dense(st, N):
+    """Dense live matrix (eliminated DOFs appear as identity rows/cols)."""
+    D = np.eye(N)
+    alive = np.concatenate([m for m in st.members if len(m)]) if any(len(m) for m in st.members) else []
+    D[np.ix_(alive, alive)] = 0.0
+    for (g, h), blk in st.blk.items():
+        D[np.ix_(st.members[g], st.members[h])] = blk
+        D[np.ix_(st.members[h], st.members[g])] = blk.T
+    return D
+
+
+def eliminate_cells(store, interior, level=None, stage="eliminate", stats=None):
+    """Stage 1: block elimination of each interior group, in order."""
+    recs = []
+    for t, gi in enumerate(interior):
+        nb = store.neighbours(gi)
+        Aii = store.get(gi, gi)
+        Abt = np.hstack([store.get(gi, h) for h in nb]) if nb else np.zeros((len(Aii), 0))
+        try:
+            Lc = cholesky(Aii)
+        except NotSpdError as e:
+            raise NotSpdError(e.pivot, level, stage, t, stats) from None
+        X = tri_solve(Lc, Abt)
+        off = np.cumsum([0] + [len(store.members[h]) for h in nb])
+        for a, ha in enumerate(nb):
+            Xa = X[:, off[a]:off[a + 1]]
+            for b in range(a, len(nb)):
+                store.add(ha, nb[b], -(Xa.T @ X[:, off[b]:off[b + 1]]))
+        Bidx = np.concatenate([store.members[h] for h in nb]) if nb else np.zeros(0, np.int64)
+        recs.append(Eliminate(store.members[gi].copy(), Bidx, Lc, X))
+        store.drop_group(gi)
+    return recs
+
+
+def precondition_blocks(store, groups, level=None, stats=None):
+    """Stage 2: two-sided block-Jacobi scaling, A_gg -> I."""
+    recs = []
+    for t, g in enumerate(groups):
+        try:
+            Lg = cholesky(store.get(g, g))
+        except NotSpdError as e:
+            raise NotSpdError(e.pivot, level, "precondition", t, stats) from None
+        for h in store.neighbours(g):
+            if g < h:
+                store.blk[(g, h)] = scipy.linalg.solve_triangular(Lg, store.blk[(g, h)], lower=True)
+            else:
+                store.blk[(h, g)] = scipy.linalg.solve_triangular(Lg, store.blk[(h, g)].T, lower=True).T
+        store.put(g, g, np.eye(len(Lg)))
+        recs.append(Precondition(store.members[g].copy(), Lg))
+    return recs
+
+
+def skeletonize_separators(store, groups, eps, level=None, stats=None):
+    """Stage 3: sequential ID + zeroing + elimination of ~I."""
+    recs, ranks = [], []
+    for t, g in enumerate(groups):
+        nb = store.neighbours(g)
+        k = len(store.members[g])
+        M = np.vstack([store.get(h, g) for h in nb]) if nb else np.zeros((0, k))
+        M = M[np.any(M != 0.0, axis=1)]
+        idr = interpolative_decomposition(M, eps)
+        sk, rd, T = idr.skeleton, idr.redundant, idr.interp
+        ranks.append(len(sk))
+        if len(rd) == 0:
+            continue
+        Agg = store.get(g, g)
+        Arr = Agg[np.ix_(rd, rd)]
+        Asr = Agg[np.ix_(sk, rd)]
+        Ass = Agg[np.ix_(sk, sk)]
+        Att = Arr - T.T @ Asr - Asr.T @ T + T.T @ Ass @ T
+        Ast = Asr - Ass @ T
+        try:
+            Lt = cholesky(Att)
+        except NotSpdError as e:
+            raise NotSpdError(e.pivot, level, "skeletonize", t, stats) from None
+        Xt = tri_solve(Lt, Ast.T)
+        mem = store.members[g]
+        recs.append(Skeletonize(mem[rd].copy(), mem[sk].copy(), T, Lt, Xt, t))
+        Anew = Ass - Xt.T @ Xt
+        store.put(g, g, np.zeros((k, k)))
+        store.shrink(g, sk)
+        store.put(g, g, Anew)
+    return recs, ranks
+
+
 def factorize(A, spec, eps: float, method: str = "phif") -> Factorization:
     """Oracle factorization (see module docstring). A: object with `.csr` or a scipy matrix."""
     method = method.lower()
@@ -239,79 +336,19 @@ def factorize(A, spec, eps: float, method: str = "phif") -> Factorization:
         recs = LevelRecords(lev)
         st = {"level": lev, "S": int(len(active)), "p": part.p, "q": part.q, "r": part.r,
               "t_regroup": time.perf_counter() - t0}
-        stage = "root" if lev == Lmax else "eliminate"
-
         t0 = time.perf_counter()
-        for t, gi in enumerate(part.interior):
-            nb = store.neighbours(gi)
-            Aii = store.get(gi, gi)
-            Abt = np.hstack([store.get(gi, h) for h in nb]) if nb else np.zeros((len(Aii), 0))
-            try:
-                Lc = cholesky(Aii)
-            except NotSpdError as e:
-                raise NotSpdError(e.pivot, lev, stage, t, stats) from None
-            X = tri_solve(Lc, Abt)
-            off = np.cumsum([0] + [len(store.members[h]) for h in nb])
-            for a, ha in enumerate(nb):
-                Xa = X[:, off[a]:off[a + 1]]
-                for b in range(a, len(nb)):
-                    Xb = X[:, off[b]:off[b + 1]]
-                    store.add(ha, nb[b], -(Xa.T @ Xb))
-            Bidx = np.concatenate([store.members[h] for h in nb]) if nb else np.zeros(0, np.int64)
-            recs.eliminate.append(Eliminate(store.members[gi].copy(), Bidx, Lc, X))
-            store.drop_group(gi)
+        recs.eliminate = eliminate_cells(store, part.interior, lev, "root" if lev == Lmax else "eliminate", stats)
         st["t_eliminate"] = time.perf_counter() - t0
         if lev == Lmax:
             levels.append(recs)
             stats_levels.append(st)
             break
-
         t0 = time.perf_counter()
         if method != "hif":
-            for t, g in enumerate(part.precond):
-                try:
-                    Lg = cholesky(store.get(g, g))
-                except NotSpdError as e:
-                    raise NotSpdError(e.pivot, lev, "precondition", t, stats) from None
-                for h in store.neighbours(g):
-                    if g < h:
-                        store.blk[(g, h)] = scipy.linalg.solve_triangular(Lg, store.blk[(g, h)], lower=True)
-                    else:
-                        store.blk[(h, g)] = scipy.linalg.solve_triangular(
-                            Lg, store.blk[(h, g)].T, lower=True).T
-                store.put(g, g, np.eye(len(Lg)))
-                recs.precondition.append(Precondition(store.members[g].copy(), Lg))
+            recs.precondition = precondition_blocks(store, part.precond, lev, stats)
         st["t_precondition"] = time.perf_counter() - t0
-
         t0 = time.perf_counter()
-        ranks = []
-        for t, g in enumerate(part.skeleton):
-            nb = store.neighbours(g)
-            k = len(store.members[g])
-            M = np.vstack([store.get(h, g) for h in nb]) if nb else np.zeros((0, k))
-            M = M[np.any(M != 0.0, axis=1)]
-            idr = interpolative_decomposition(M, eps)
-            sk, rd, T = idr.skeleton, idr.redundant, idr.interp
-            ranks.append(len(sk))
-            if len(rd) == 0:
-                continue
-            Agg = store.get(g, g)
-            Arr = Agg[np.ix_(rd, rd)]
-            Asr = Agg[np.ix_(sk, rd)]
-            Ass = Agg[np.ix_(sk, sk)]
-            Att = Arr - T.T @ Asr - Asr.T @ T + T.T @ Ass @ T
-            Ast = Asr - Ass @ T
-            try:
-                Lt = cholesky(Att)
-            except NotSpdError as e:
-                raise NotSpdError(e.pivot, lev, "skeletonize", t, stats) from None
-            Xt = tri_solve(Lt, Ast.T)
-            mem = store.members[g]
-            recs.skeletonize.append(Skeletonize(mem[rd].copy(), mem[sk].copy(), T, Lt, Xt, t))
-            Anew = Ass - Xt.T @ Xt
-            store.put(g, g, np.zeros((k, k)))
-            store.shrink(g, sk)
-            store.put(g, g, Anew)
+        recs.skeletonize, ranks = skeletonize_separators(store, part.skeleton, eps, lev, stats)
         st["t_skeletonize"] = time.perf_counter() - t0
         st["rho_max"] = int(max(ranks)) if ranks else 0
         st["rho_mean"] = float(np.mean(ranks)) if ranks else 0.0

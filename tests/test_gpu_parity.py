@@ -1,0 +1,141 @@
+"""GPU parity: the B200 path (through the C-ABI) vs the CPU oracle on identical seeded inputs.
+
+North-star criteria (BASELINE.json): identical skeleton sets (pivot gaps > 1e-12),
+e_s within 2x, PCG iteration counts within +-1, solution relative difference <= 1e-8,
+NotSpd reported at the same (level, stage, group, pivot).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+from oracle import diagnostics as odiag  # noqa: E402
+from oracle import krylov as okry  # noqa: E402
+from oracle import phif as ophif  # noqa: E402
+from oracle.errors import NotSpdError as OracleNotSpd  # noqa: E402
+from paper_1808_01364_b200 import NotSpdError  # noqa: E402
+from paper_1808_01364_b200 import diagnostics as gdiag  # noqa: E402
+from paper_1808_01364_b200 import factorization as gfac  # noqa: E402
+from paper_1808_01364_b200 import krylov as gkry  # noqa: E402
+from paper_1808_01364_b200.grid import (CONFIGS, CoefficientField, GridSpec, assemble_operator,  # noqa: E402
+                                        baseline_problem, baseline_rhs, generate_field)
+
+X_TOL = 1e-8          # final solution relative difference
+APPLY_TOL = 1e-8      # F^-1 b relative difference
+
+
+def _small(dim, n, m, seed=1, contrast=1e4):
+    spec = GridSpec(dim, n, m)
+    return spec, assemble_operator(generate_field(spec, seed, contrast), 0.0)
+
+
+CASES = [
+    ("exact-2d", lambda: _small(2, 16, 4), "exact", 0.0, 1e-12),
+    ("phif-2d", lambda: _small(2, 32, 4), "phif", 1e-6, 1e-12),
+    ("hif-2d", lambda: _small(2, 32, 8), "hif", 1e-6, 1e-12),
+    ("exact-3d", lambda: _small(3, 16, 4), "exact", 0.0, 1e-12),
+    ("phif-3d", lambda: _small(3, 16, 4), "phif", 1e-3, 1e-12),
+    ("c1", lambda: baseline_problem("c1", 0)[:2], "phif", 1e-6, 1e-12),
+    ("c2-n128-phif", lambda: baseline_problem("c2", 0, 128)[:2], "phif", 1e-3, 1e-12),
+    ("c2-n128-hif", lambda: baseline_problem("c2", 0, 128)[:2], "hif", 1e-3, 1e-12),
+    ("c3-n128-1e-4", lambda: baseline_problem("c3", 0, 128)[:2], "phif", 1e-4, 1e-12),
+    ("c4-n32", lambda: baseline_problem("c4", 0, 32)[:2], "phif", 1e-3, 1e-12),
+    ("c5-n32", lambda: baseline_problem("c5", 0, 32)[:2], "phif", 1e-2, 1e-10),
+]
+
+
+def _redundant_sets(Fo, lev):
+    return {tuple(int(v) for v in np.sort(r.redundant)) for r in Fo.levels[lev].skeletonize}
+
+
+@pytest.mark.parametrize("name,make,method,eps,tol", CASES, ids=[c[0] for c in CASES])
+def test_parity_with_oracle(name, make, method, eps, tol):
+    spec, A = make()
+    try:
+        Fo = ophif.factorize(A, spec, eps, method)
+    except OracleNotSpd as e:
+        with pytest.raises(NotSpdError) as g:
+            gfac.factorize(A, spec, eps, method)
+        assert (g.value.level, g.value.stage, g.value.group, g.value.pivot) == (e.level, e.stage, e.group, e.pivot)
+        return
+    Fg = gfac.factorize(A, spec, eps, method)
+    assert Fg.SL == Fo.SL
+    for lev in range(spec.levels):
+        got = {tuple(int(v) for v in np.sort(r)) for _, r in Fg.skeleton_sets(lev) if len(r)}
+        assert got == _redundant_sets(Fo, lev), f"skeleton sets differ at level {lev}"
+    B = np.random.default_rng(7).standard_normal((A.n, 4))
+    yo, yg = ophif.apply_inverse(Fo, B), gfac.apply_inverse(Fg, B)
+    assert np.linalg.norm(yg - yo) <= APPLY_TOL * np.linalg.norm(yo)
+    b = np.random.default_rng([0, 1]).standard_normal(A.n)
+    xo, ro = okry.pcg(A, b, precond=Fo, tol=tol)
+    xg, rg = gkry.pcg(A, b, precond=Fg, tol=tol)
+    assert abs(rg.n_i - ro.n_i) <= 1
+    assert np.linalg.norm(xg - xo) <= X_TOL * np.linalg.norm(xo)
+    eo = odiag.estimate_solve_error(A, Fo).value
+    eg = gdiag.estimate_solve_error(A, Fg).value
+    assert eg <= 2 * eo + 1e-14 and eo <= 2 * eg + 1e-14
+
+
+def test_c3_loose_tolerance_not_spd_parity():
+    """c3's contrast-1e8 field at eps = 1e-2 loses positive definiteness (PAPER.md Remark 2)."""
+    spec, A = baseline_problem("c3", 1, 256)[:2]
+    with pytest.raises(OracleNotSpd) as e:
+        ophif.factorize(A, spec, 1e-2, "phif")
+    with pytest.raises(NotSpdError) as g:
+        gfac.factorize(A, spec, 1e-2, "phif")
+    assert (g.value.level, g.value.stage, g.value.group, g.value.pivot) == (e.value.level, e.value.stage,
+                                                                            e.value.group, e.value.pivot)
+
+
+def test_not_spd_input_location():
+    spec = GridSpec(2, 16, 4)
+    A = assemble_operator(CoefficientField(spec, np.ones(spec.shape), 0, 1.0, 1.0)).csr.tolil()
+    A[spec.id_of([[6, 2]])[0], spec.id_of([[6, 2]])[0]] = -1.0
+    with pytest.raises(NotSpdError) as g:
+        gfac.factorize(sp.csr_matrix(A), spec, 1e-6, "phif")
+    assert (g.value.level, g.value.stage, g.value.group) == (0, "eliminate", 4)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 32), (3, 16)])
+def test_exact_mode_acceptance(dim, n):
+    """SPEC.md AC1: exact mode, ||I - A F^-1|| <= 1e-9 (e_s form), 5 seeds."""
+    for seed in range(5):
+        spec = GridSpec(dim, n, 4)
+        A = assemble_operator(generate_field(spec, seed))
+        F = gfac.factorize(A, spec, 0.0, "exact")
+        assert gdiag.estimate_solve_error(A, F).value <= 1e-9
+
+
+def test_pcg_spec_examples_on_gpu():
+    b = np.random.default_rng(5).standard_normal(7)
+    x, rep = gkry.pcg(sp.identity(7, format="csr"), b)
+    assert rep.n_i == 1 and np.allclose(x, b)
+    A3 = sp.csr_matrix(np.array([[4.0, 2.0, 0.0], [2.0, 3.0, 1.0], [0.0, 1.0, 2.0]]))
+    x, rep = gkry.pcg(A3, np.array([1.0, 0.0, 0.0]))
+    assert np.allclose(x, [5 / 12, -1 / 3, 1 / 6], atol=1e-10)
+
+
+def test_multi_rhs_block_equals_single_solves():
+    spec, A = baseline_problem("c1", 0)[:2]
+    F = gfac.factorize(A, spec, 1e-6, "phif")
+    B = baseline_rhs("c1", A.n, 0, 8)
+    X, rep = gkry.pcg(A, B, precond=F)
+    for c in (0, 5):
+        x, r1 = gkry.pcg(A, B[:, c], precond=F)
+        assert r1.n_i == rep.n_i[c]
+        assert np.linalg.norm(x - X[:, c]) <= 1e-12 * np.linalg.norm(x)
+
+
+def test_apply_inverse_symmetry_and_ginv_on_gpu():
+    spec, A = baseline_problem("c4", 0, 32)[:2]
+    F = gfac.factorize(A, spec, 1e-3, "phif")
+    rng = np.random.default_rng(8)
+    u, v = rng.standard_normal(A.n), rng.standard_normal(A.n)
+    a, b = gfac.apply_inverse(F, u) @ v, u @ gfac.apply_inverse(F, v)
+    assert abs(a - b) <= 1e-12 * abs(a)
+    w = gfac.apply_ginv_t(F, gfac.apply_ginv(F, u))
+    assert np.linalg.norm(w - gfac.apply_inverse(F, u)) <= 1e-12 * np.linalg.norm(w)
