@@ -63,6 +63,9 @@ typedef struct phif_error {
 
 int phif_version(void);
 
+/* Number of engine kernel launches issued so far in this process (evidence counter). */
+long long phif_launch_count(void);
+
 /* Symmetric CSR (full pattern, sorted columns) from host arrays; uploaded to HBM. */
 int phif_matrix_create(const int64_t* rowptr, const int32_t* col, const double* val, int64_t n, void* stream,
                        phif_matrix** out, phif_error* err);

@@ -27,7 +27,7 @@ STAGES = {0: "eliminate", 1: "precondition", 2: "skeletonize", 3: "root"}
 
 _lib = None
 
-EXPORTS = ("phif_version", "phif_matrix_create", "phif_matrix_free", "phif_factorize", "phif_factor_free",
+EXPORTS = ("phif_version", "phif_launch_count", "phif_matrix_create", "phif_matrix_free", "phif_factorize", "phif_factor_free",
            "phif_apply", "phif_pcg", "phif_solve_error", "phif_stats_json", "phif_skeleton_sets",
            "phif_num_levels", "phif_classify", "phif_plan_dryrun")
 
@@ -42,6 +42,7 @@ def lib():
     L = C.CDLL(LIB_PATH)
     P, D, I64, I = C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_int
     L.phif_version.restype = I
+    L.phif_launch_count.restype = C.c_longlong
     L.phif_matrix_create.argtypes = [P, P, P, I64, P, C.POINTER(P), C.POINTER(phif_error)]
     L.phif_matrix_create.restype = I
     L.phif_matrix_free.argtypes = [P]

@@ -82,6 +82,8 @@ extern "C" {
 
 int phif_version(void) { return 1; }
 
+long long phif_launch_count(void) { return phif::launch_count(); }
+
 int phif_matrix_create(const int64_t* rowptr, const int32_t* col, const double* val, int64_t n, void* stream,
                        phif_matrix** out, phif_error* err) {
   return guarded(err, [&] {

@@ -203,6 +203,16 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     L.cell_work_unit = wacc;
     L.wbuf_unit = bacc;
+    for (int t = 0; t < p; ++t) {
+      const double nn = P.cell_n[t], bb = P.cell_b[t];
+      L.fl[1] += nn * nn * nn / 3.0 + nn * nn * bb + nn * bb * bb;
+      L.by[1] += 8.0 * (nn * nn + nn * bb + (nn + bb) * nn + bb * bb);
+    }
+    for (size_t q = 0; q < P.tgt_blk.size(); ++q) {
+      const int blk = P.tgt_blk[q];
+      L.by[1] += 8.0 * 2.0 * G.size(P.pat.bg[blk]) * G.size(P.pat.bh[blk]);
+    }
+    for (size_t b = 0; b < P.pat.bg.size(); ++b) L.by[0] += 8.0 * 2.0 * G.size(P.pat.bg[b]) * G.size(P.pat.bh[b]);
     // boundary reduction lists (x_B -= X^T y in fixed cell order)
     {
       std::vector<std::pair<int, int>> dr(Bdofs.size());
@@ -242,6 +252,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       pw += k;
     }
     L.prec_work_unit = pw;
+    if (do_prec) {
+      for (int t = 0; t < r; ++t) {
+        const double k = pn[t];
+        L.fl[2] += k * k * k / 3.0;
+        L.by[2] += 8.0 * 3.0 * k * k;
+      }
+      for (int b : P.scale_blk) {
+        const double kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
+        L.fl[2] += kg * kg * kh + kg * kh * kh;
+        L.by[2] += 8.0 * 2.0 * kg * kh;
+      }
+    }
     // skeleton records / workspaces (upper bounds; ranks known after the ID)
     const int nsk = P.root ? 0 : (int)P.skeleton.size();
     std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk);
@@ -405,6 +427,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     upload(L.s_nbr_blk, P.sk_nbr_blk, s);
     upload(L.s_order, P.wave_order, s);
     L.s_rank.alloc(std::max(nsk, 1) * sizeof(int), s, true);
+    L.s_rows.alloc(std::max(nsk, 1) * sizeof(int), s, true);
     upload(L.s_T_off, T_off, s);
     upload(L.s_P_off, SP_off, s);
     upload(L.s_work_off, work_off, s);
@@ -422,6 +445,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     ka.alive = F->alive.as<int>();
     ka.red = F->red.as<uint8_t>();
     ka.rank = L.s_rank.as<int>();
+    ka.rows = L.s_rows.as<int>();
     ka.eps = F->eps;
     ka.work = wk.as<double>();
     ka.work_off = L.s_work_off.as<int64_t>();
@@ -442,8 +466,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     check_status(*F, lev, ST_SKELETONIZE);
     // ranks and redundant flags back to the host (planning of the next level)
     L.h_rank.resize(nsk);
+    std::vector<int> h_rows(nsk);
     std::vector<uint8_t> red(G.mem.size());
     if (nsk) CK(cudaMemcpyAsync(L.h_rank.data(), L.s_rank.p, nsk * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (nsk) CK(cudaMemcpyAsync(h_rows.data(), L.s_rows.p, nsk * sizeof(int), cudaMemcpyDeviceToHost, s));
     if (!red.empty()) CK(cudaMemcpyAsync(red.data(), F->red.p, red.size(), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     tp = clk::now();
@@ -463,6 +489,16 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       S_off[t] = (int64_t)Sd.size();
       R_off[t] = (int64_t)Rd.size();
       for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) (red[q] ? Rd : Sd).push_back(G.mem[q]);
+    }
+    for (int t = 0; t < nsk; ++t) {
+      const double mm = h_rows[t], kk = sr[t] + skt[t], rr = sr[t], kt = skt[t];
+      const double a = std::max(mm, kk), b = std::min(mm, kk);
+      L.fl[3] += 2.0 * a * b * b - 2.0 * b * b * b / 3.0 + rr * rr * kt;   // GEQP3 + T solve
+      L.by[3] += 8.0 * (mm * kk + rr * kt) + 4.0 * kk;
+      if (kt > 0) {
+        L.fl[4] += 2.0 * rr * rr * kt + 4.0 * rr * kt * kt + kt * kt * kt / 3.0 + kt * kt * rr + kt * rr * rr;
+        L.by[4] += 8.0 * (kk * kk + rr * rr + (kt + rr) * kt + rr * kt);
+      }
     }
     L.rho_max = nsk ? *std::max_element(sr.begin(), sr.end()) : 0;
     L.rho_mean = nsk ? (double)rsum / nsk : 0.0;
@@ -764,7 +800,9 @@ std::string Factorization::stats_json() const {
       << ",\"blocks\":" << P.pat.bg.size() << ",\"waves\":" << P.nwaves << ",\"rho_max\":" << L.rho_max
       << ",\"rho_mean\":" << L.rho_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
       << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
-      << L.t_ms[4] << ",\"record_bytes\":" << L.rec_doubles * 8 << "}";
+      << L.t_ms[4] << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]
+      << "," << L.fl[2] << "," << L.fl[3] << "," << L.fl[4] << "],\"bytes\":[" << L.by[0] << "," << L.by[1] << ","
+      << L.by[2] << "," << L.by[3] << "," << L.by[4] << "]}";
   }
   const LevelRT& R = *levels.back();
   o << "],\"SL\":" << (R.plan.interior.empty() ? 0 : R.plan.cell_n[0]) << "}";

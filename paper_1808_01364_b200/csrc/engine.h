@@ -78,6 +78,9 @@ struct LevelRT {
   int64_t skel_work_unit = 0;
   // stats
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
+  // algorithmic work per stage (0 repack, 1 eliminate+schur, 2 precondition, 3 id, 4 skel update)
+  double fl[6] = {0, 0, 0, 0, 0, 0}, by[6] = {0, 0, 0, 0, 0, 0};
+  DBuf s_rows;
   int rho_max = 0;
   double rho_mean = 0.0;
   int64_t S = 0;

@@ -2,6 +2,7 @@
 //
 // One CTA per cell / group / block; all dense algebra through dla.cuh
 // (DMMA GEMM core). Reference semantics are cited per kernel.
+#include <atomic>
 #include <cfloat>
 #include <cstdio>
 
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
     }
   }
   __syncthreads();
+  if (tid == 0) sk.rows[s] = m;
   uint8_t* red = sk.red + gof;
   if (m == 0) {  // no coupling: every column redundant (kernels.py:95-98)
     for (int j = tid; j < k; j += NT) {
@@ -646,6 +648,9 @@ __global__ void k_scale(double* y, const double* x, const double* nrm2, int64_t 
 // ---------------------------------------------------------------------------
 // Launch wrappers
 // ---------------------------------------------------------------------------
+std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+
 static constexpr size_t SMEM_BYTES = (size_t)SMEM_DOUBLES * sizeof(double);
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -653,80 +658,103 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
                    const double* val, int64_t N, cudaStream_t s) {
   if (N == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_ingest<<<nblk(N, 256), 256, 0, s>>>(lv, gid, pos, rowptr, col, val, N);
 }
 void launch_cell(const LevelDev& lv, const CellArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.p == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_cell<<<a.p, NT, SMEM_BYTES, s>>>(lv, a, st);
 }
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s) {
   if (a.ntgt == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_schur<<<a.ntgt, NT, 0, s>>>(lv, a);
 }
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.r == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_prec_factor<<<a.r, NT, SMEM_BYTES, s>>>(lv, a, st);
 }
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
   if (a.nscale == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_prec_scale<<<a.nscale, NT, SMEM_BYTES, s>>>(lv, a);
 }
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s) {
   if (count == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_skel_id<<<count, NT, SMEM_BYTES, s>>>(lv, a);
 }
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.nsk == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_skel_update<<<a.nsk, NT, SMEM_BYTES, s>>>(lv, a, st);
 }
 void launch_repack(const RepackArgs& a, cudaStream_t s) {
   if (a.nblk == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_repack<<<a.nblk, NT, 0, s>>>(a);
 }
 void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.p == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_cell<<<a.p, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
 }
 void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd, double* x,
                          int k, cudaStream_t s) {
   if (nd == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_reduce<<<nblk((int64_t)nd * k, 256), 256, 0, s>>>(dof, off, rows, wbuf, nd, x, k);
 }
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.r == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_prec<<<a.r, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
 }
 void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.nsk == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_skel<<<a.nsk, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
 }
 void launch_spmv(const int64_t* rowptr, const int* col, const double* val, const double* x, double* y, int64_t N,
                  int k, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_spmv<<<nblk(N * k, 256), 256, 0, s>>>(rowptr, col, val, x, y, N, k);
 }
 int dot_part_blocks() { return 592; }
 void launch_dot(const double* a, const double* b, int64_t N, int k, double* part, double* out, cudaStream_t s) {
   const int threads = (256 / k) * k;
   const int blocks = dot_part_blocks();
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_dot_part<<<blocks, threads, threads * sizeof(double), s>>>(a, b, N, k, part);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_dot_final<<<1, 32 * ((k + 31) / 32), 0, s>>>(part, blocks, k, out);
 }
 void launch_axpy(double* y, const double* x, const double* coef, double sgn, const int* active, int64_t N, int k,
                  cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_axpy<<<nblk(N * k, 256), 256, 0, s>>>(y, x, coef, sgn, active, N, k);
 }
 void launch_xpby(double* p, const double* z, const double* coef, const int* active, int64_t N, int k,
                  cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_xpby<<<nblk(N * k, 256), 256, 0, s>>>(p, z, coef, active, N, k);
 }
 void launch_sub(double* r, const double* b, const double* q, const int* active, int64_t N, int k, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_sub<<<nblk(N * k, 256), 256, 0, s>>>(r, b, q, active, N, k);
 }
 void launch_ratio(const double* num, const double* den, const int* active, double* out, int k, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_ratio<<<1, 32 * ((k + 31) / 32), 0, s>>>(num, den, active, out, k);
 }
-void launch_xmy(double* y, const double* x, int64_t n, cudaStream_t s) { k_xmy<<<nblk(n, 256), 256, 0, s>>>(y, x, n); }
+void launch_xmy(double* y, const double* x, int64_t n, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_xmy<<<nblk(n, 256), 256, 0, s>>>(y, x, n);
+}
 void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   k_scale<<<nblk(n, 256), 256, 0, s>>>(y, x, nrm2, n);
 }
 

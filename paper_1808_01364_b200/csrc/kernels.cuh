@@ -74,6 +74,7 @@ struct SkelArgs {
   int* alive;                // per DOF (global)
   uint8_t* red;              // per member position of the level (1 = redundant)
   int* rank;                 // per skeleton
+  int* rows;                 // per skeleton: rows of A_{R,I} after filtering
   double eps;
   double* work;              // per skeleton workspace
   const int64_t* work_off;

@@ -49,6 +49,7 @@ struct ApplySkelArgs {
 };
 
 void configure_kernels();
+long long launch_count();   // kernel launches issued so far (all streams)
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
                    const double* val, int64_t N, cudaStream_t s);
 void launch_cell(const LevelDev& lv, const CellArgs& a, DevStatus* st, cudaStream_t s);

@@ -249,6 +249,11 @@ CONFIGS = {
     "c3": BaselineConfig("c3", 2, 2048, 16, 1e-6, (1e-2, 1e-4), "phif", 8, 1e-12, "thresh_2d_s4_1e4",
                          "2D 2047^2, smoothed-threshold a in {1e-4,1e4} (std 4), b=1e-6, m=16, "
                          "eps 1e-2/1e-4, PHIF, 8 RHS, tol 1e-12"),
+    # c3 geometry with the paper's contrast (a in {1e-2, 1e2}): the specified
+    # contrast-1e8 field loses positive definiteness at level 1 for eps 1e-2 and 1e-4
+    "c3p": BaselineConfig("c3p", 2, 2048, 16, 1e-6, (1e-4,), "phif", 8, 1e-12, "thresh_2d_s4_1e2",
+                          "2D 2047^2, smoothed-threshold a in {1e-2,1e2} (std 4), b=1e-6, m=16, eps 1e-4, "
+                          "PHIF, 8 RHS, tol 1e-12 (c3 with the paper's contrast)"),
     "c4": BaselineConfig("c4", 3, 64, 4, 0.0, (1e-3,), "phif", 1, 1e-12, "smooth_log3_s2",
                          "3D 63^3, a=10^(3(2Us-1)) Us smoothed uniform (std 2), m=4, eps 1e-3, PHIF"),
     "c5": BaselineConfig("c5", 3, 128, 4, 0.0, (1e-2,), "phif", 32, 1e-10, "thresh_3d_s3_1e3",
