@@ -4,11 +4,11 @@ set -euo pipefail
 cd "$(dirname "$0")"
 OUT=../libphif_b200.so
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
-FLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-O3,-g --expt-relaxed-constexpr"
+FLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-O3,-g,-fopenmp --expt-relaxed-constexpr"
 mkdir -p build
 $NVCC $FLAGS -c planner.cpp -o build/planner.o
 $NVCC $FLAGS -c kernels.cu -o build/kernels.o ${PTXAS_V:+-Xptxas -v}
 $NVCC $FLAGS -c engine.cu -o build/engine.o
 $NVCC $FLAGS -c capi.cu -o build/capi.o
-$NVCC -shared -gencode arch=compute_100a,code=sm_100a -o $OUT build/planner.o build/kernels.o build/engine.o build/capi.o -lcudart -Xlinker -export-dynamic
+$NVCC -shared -gencode arch=compute_100a,code=sm_100a -o $OUT build/planner.o build/kernels.o build/engine.o build/capi.o -lcudart -lgomp -Xlinker -export-dynamic
 echo "built $(realpath $OUT)"

@@ -1,4 +1,5 @@
 // extern "C" boundary (include/phif_b200.h). No exception crosses it.
+#include <chrono>
 #include <csignal>
 #include <cstdio>
 #include <cstdlib>
@@ -253,6 +254,7 @@ size_t phif_plan_dryrun(int dim, int n, int m, const int64_t* rowptr, const int3
     for (int l = 0; l <= s.L; ++l) {
       lv.push_back(std::make_unique<phif::LevelPlan>());
       phif::LevelPlan& P = *lv.back();
+      auto t1 = std::chrono::steady_clock::now();
       std::vector<std::pair<int, int>> pairs;
       if (l == 0) {
         P.grp = phif::classify_all(s);
@@ -261,7 +263,13 @@ size_t phif_plan_dryrun(int dim, int n, int m, const int64_t* rowptr, const int3
         P.grp = phif::classify_next(s, lv[l - 1]->grp, alive);
         pairs = phif::pattern_next(*lv[l - 1], P.grp);
       }
+      auto t2 = std::chrono::steady_clock::now();
       phif::build_level(s, P, std::move(pairs));
+      auto t3 = std::chrono::steady_clock::now();
+      if (getenv("PHIF_DEBUG"))
+        fprintf(stderr, "level %d: classify+pattern %.1f ms build %.1f ms\n", l,
+                std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                std::chrono::duration<double, std::milli>(t3 - t2).count());
       out += (l ? "," : "") + phif::level_json(P);
       alive.assign(P.grp.mem.size(), 0);
       for (int g = 0; g < P.grp.G; ++g) {

@@ -16,6 +16,8 @@
 
 namespace phif {
 
+constexpr int BIG_N = 192;   // cells with |I| >= BIG_N take the tile-parallel path
+
 static bool debug_on() {
   static int on = -1;
   if (on < 0) on = getenv("PHIF_DEBUG") ? 1 : 0;
@@ -132,6 +134,114 @@ void upload_structure(LevelRT& L, cudaStream_t s) {
     if (p.pat.bg[b] == p.pat.bh[b]) diag[p.pat.bg[b]] = (int)b;
   upload(L.diag_blk, diag, s);
 }
+
+// Work lists for the tile-parallel big-cell path (one level).
+struct BigPlan {
+  static constexpr int T = 64;
+  DBuf d_n, d_b, d_P, d_U, d_op, d_linv, d_list;
+  DBuf d_cell, d_i, d_j;
+  std::vector<int64_t> diag_off, trsm_off, upd_off;   // per step offsets into the work arrays
+  std::vector<int> steps_k0;
+  int64_t syrk_off = 0, syrk_n = 0;
+  int nbig = 0;
+  void build(const std::vector<int>& big, const std::vector<int>& cn, const std::vector<int>& cb, double* rec,
+             const std::vector<int64_t>& P_off, double* U, const std::vector<int64_t>& U_off, cudaStream_t s) {
+    nbig = (int)big.size();
+    std::vector<int> n(nbig), b(nbig), op(nbig);
+    std::vector<double*> Pp(nbig), Up(nbig);
+    int nmax = 0;
+    for (int c = 0; c < nbig; ++c) {
+      const int t = big[c];
+      n[c] = cn[t];
+      b[c] = cb[t];
+      op[c] = t;
+      Pp[c] = rec + P_off[t];
+      Up[c] = U + U_off[t];
+      nmax = std::max(nmax, n[c]);
+    }
+    std::vector<int> wc, wi, wj;
+    for (int k0 = 0; k0 < nmax; k0 += T) {
+      steps_k0.push_back(k0);
+      diag_off.push_back((int64_t)wc.size());
+      for (int c = 0; c < nbig; ++c)
+        if (n[c] > k0) {
+          wc.push_back(c);
+          wi.push_back(0);
+          wj.push_back(0);
+        }
+      trsm_off.push_back((int64_t)wc.size());
+      for (int c = 0; c < nbig; ++c) {
+        if (n[c] <= k0) continue;
+        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = n[c] + b[c];
+        const int ntr = (rows - base + T - 1) / T;
+        for (int it = 0; it < ntr; ++it) {
+          wc.push_back(c);
+          wi.push_back(it);
+          wj.push_back(0);
+        }
+      }
+      upd_off.push_back((int64_t)wc.size());
+      for (int c = 0; c < nbig; ++c) {
+        if (n[c] <= k0) continue;
+        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = n[c] + b[c];
+        if (base >= n[c]) continue;
+        const int nr = (rows - base + T - 1) / T, nc = (n[c] - base + T - 1) / T;
+        for (int it = 0; it < nr; ++it)
+          for (int jt = 0; jt < nc; ++jt) {
+            if (jt > it && base + T * (it + 1) <= n[c]) continue;
+            wc.push_back(c);
+            wi.push_back(it);
+            wj.push_back(jt);
+          }
+      }
+    }
+    diag_off.push_back((int64_t)wc.size());
+    syrk_off = (int64_t)wc.size();
+    for (int c = 0; c < nbig; ++c) {
+      const int nb = (b[c] + T - 1) / T;
+      for (int it = 0; it < nb; ++it)
+        for (int jt = 0; jt < nb; ++jt) {
+          wc.push_back(c);
+          wi.push_back(it);
+          wj.push_back(jt);
+        }
+    }
+    syrk_n = (int64_t)wc.size() - syrk_off;
+    upload(d_n, n, s);
+    upload(d_b, b, s);
+    upload(d_op, op, s);
+    upload(d_P, Pp, s);
+    upload(d_U, Up, s);
+    d_linv.alloc((size_t)nbig * T * T * sizeof(double), s);
+    upload(d_cell, wc, s);
+    upload(d_i, wi, s);
+    upload(d_j, wj, s);
+  }
+  BigArgs args(int64_t off, int64_t cnt, int k0) const {
+    BigArgs a;
+    a.ncell = nbig;
+    a.n = d_n.as<int>();
+    a.b = d_b.as<int>();
+    a.P = d_P.as<double* const>();
+    a.U = d_U.as<double* const>();
+    a.Linv = d_linv.as<double>();
+    a.op = d_op.as<int>();
+    a.w_cell = d_cell.as<int>() + off;
+    a.w_i = d_i.as<int>() + off;
+    a.w_j = d_j.as<int>() + off;
+    a.nwork = (int)cnt;
+    a.k0 = k0;
+    return a;
+  }
+  void run(DevStatus* st, cudaStream_t s) const {
+    for (size_t q = 0; q < steps_k0.size(); ++q) {
+      const int k0 = steps_k0[q];
+      const int64_t d0 = diag_off[q], t0 = trsm_off[q], u0 = upd_off[q], e = diag_off[q + 1];
+      launch_big_step(args(d0, t0 - d0, k0), args(t0, u0 - t0, k0), args(u0, e - u0, k0), st, s);
+    }
+    launch_big_syrk(args(syrk_off, syrk_n, 0), s);
+  }
+};
 
 }  // namespace
 
@@ -266,12 +376,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     // skeleton records / workspaces (upper bounds; ranks known after the ID)
     const int nsk = P.root ? 0 : (int)P.skeleton.size();
-    std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk);
+    std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk), rows_bound(nsk);
     int64_t work = 0, iwork = 0, aw = 0;
     for (int t = 0; t < nsk; ++t) {
       const int g = P.skeleton[t], k = G.size(g);
       int64_t rows = 0;
       for (int64_t q = P.sk_nbr_off[t]; q < P.sk_nbr_off[t + 1]; ++q) rows += G.size(P.sk_nbr[q]);
+      rows_bound[t] = rows;
       T_off[t] = rec;
       rec += (int64_t)k * k;
       SP_off[t] = rec;
@@ -360,10 +471,26 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     ca.P_off = L.c_P_off.as<int64_t>();
     ca.U = U.as<double>();
     ca.U_off = L.c_U_off.as<int64_t>();
+    ca.list = nullptr;
     CK(cudaMemsetAsync(F->status.p, 0xff, sizeof(DevStatus), s));
+    // small cells: one CTA each; big cells (n >= BIG_N): tile-parallel 64-wide steps
+    std::vector<int> small_cells, big_cells;
+    for (int t = 0; t < p; ++t) (P.cell_n[t] >= BIG_N ? big_cells : small_cells).push_back(t);
+    DBG("level %d: cells p=%d (big %zu)", lev, p, big_cells.size());
+    DBuf d_small_cells;
+    upload(d_small_cells, small_cells, s);
+    BigPlan bp;
+    if (!big_cells.empty()) bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
     if (timing) CK(cudaEventRecord(ev[2], s));
-    DBG("level %d: cells p=%d", lev, p);
-    launch_cell(dv, ca, F->status.as<DevStatus>(), s);
+    if (!small_cells.empty()) {
+      ca.list = d_small_cells.as<int>();
+      launch_cell(dv, ca, (int)small_cells.size(), F->status.as<DevStatus>(), s);
+    }
+    if (!big_cells.empty()) {
+      upload(bp.d_list, big_cells, s);
+      launch_big_build(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), s);
+      bp.run(F->status.as<DevStatus>(), s);
+    }
     if (timing) CK(cudaEventRecord(ev[3], s));
     check_status(*F, lev, P.root ? ST_ROOT : ST_ELIMINATE);
     DBuf tb, to, cc, cr, ccol;
@@ -455,9 +582,76 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     ka.T_off = L.s_T_off.as<int64_t>();
     ka.P_off = L.s_P_off.as<int64_t>();
     if (timing) CK(cudaEventRecord(ev[8], s));
-    for (int w = 0; w < P.nwaves; ++w) {
-      ka.order = L.s_order.as<int>() + P.wave_off[w];
-      launch_skel_id(dv, ka, (int)(P.wave_off[w + 1] - P.wave_off[w]), s);
+    {
+      // per wave: small separators -> one CTA each; large ones -> gather + team CPQR
+      static int num_sms = 0;
+      if (!num_sms) CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0));
+      std::vector<int> small_list, large_list, team_face, team_off_all;
+      std::vector<int64_t> small_off(P.nwaves + 1, 0), large_off(P.nwaves + 1, 0), toff_off(P.nwaves + 1, 0),
+          slot_off(P.nwaves + 1, 0);
+      std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0);
+      for (int w = 0; w < P.nwaves; ++w) {
+        std::vector<int> large;
+        for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
+          const int t = P.wave_order[q];
+          const int k = G.size(P.skeleton[t]);
+          if (k > 48 && rows_bound[t] * k > 100000) large.push_back(t);
+          else small_list.push_back(t);
+        }
+        small_off[w + 1] = (int64_t)small_list.size();
+        int vcap = 0;
+        double wsum = 0.0;
+        for (int t : large) {
+          vcap = std::max<int>(vcap, (int)std::min<int64_t>(rows_bound[t], 16384));
+          wsum += (double)rows_bound[t] * G.size(P.skeleton[t]) * G.size(P.skeleton[t]);
+        }
+        int budget = large.empty() ? 0 : team_blocks_per_sm(vcap) * num_sms;
+        budget = std::max<int>(budget, (int)large.size());
+        toff_off[w] = (int64_t)team_off_all.size();
+        team_off_all.push_back(0);
+        int tot = 0;
+        for (int t : large) {
+          const int k = G.size(P.skeleton[t]);
+          const double wf = (double)rows_bound[t] * k * k;
+          int Pf = (int)(budget * wf / wsum);
+          Pf = std::max(1, std::min(Pf, std::min(64, std::max(1, k / 4))));
+          if (tot + Pf > budget) Pf = std::max(1, budget - tot - (int)(large.size() - 1));
+          tot += Pf;
+          team_face.push_back(t);
+          team_off_all.push_back(tot);
+          large_list.push_back(t);
+        }
+        large_off[w + 1] = (int64_t)large_list.size();
+        slot_off[w + 1] = slot_off[w] + tot;
+        wave_blocks[w] = tot;
+        wave_vcap[w] = vcap;
+      }
+      DBuf d_small, d_large, d_toff, hdr, sv, si;
+      upload(d_small, small_list, s);
+      upload(d_large, large_list, s);
+      upload(d_toff, team_off_all, s);
+      hdr.alloc(std::max<size_t>(large_list.size(), 1) * sizeof(TeamHdr), s, true);
+      sv.alloc(std::max<int64_t>(slot_off[P.nwaves], 1) * sizeof(double), s);
+      si.alloc(std::max<int64_t>(slot_off[P.nwaves], 1) * sizeof(int), s);
+      for (int w = 0; w < P.nwaves; ++w) {
+        ka.order = d_small.as<int>() + small_off[w];
+        launch_skel_id(dv, ka, (int)(small_off[w + 1] - small_off[w]), s);
+        const int nl = (int)(large_off[w + 1] - large_off[w]);
+        if (nl) {
+          launch_skel_gather(dv, ka, d_large.as<int>() + large_off[w], nl, s);
+          TeamArgs ta;
+          ta.nface = nl;
+          ta.face = d_large.as<int>() + large_off[w];
+          ta.team_off = d_toff.as<int>() + toff_off[w];
+          ta.hdr = hdr.as<TeamHdr>() + large_off[w];
+          ta.slot_v = sv.as<double>() + slot_off[w];
+          ta.slot_i = si.as<int>() + slot_off[w];
+          ta.vcap = wave_vcap[w];
+          launch_skel_team(dv, ka, ta, wave_blocks[w], s);
+        }
+      }
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));
     }
     if (timing) CK(cudaEventRecord(ev[9], s));
     DBG("level %d: skeleton update nsk=%d waves=%d", lev, nsk, P.nwaves);

@@ -56,7 +56,7 @@ __global__ void k_ingest(LevelDev lv, const int* gid, const int* pos, const int6
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus* st) {
   extern __shared__ double smem[];
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int t = ca.list ? ca.list[blockIdx.x] : blockIdx.x, tid = threadIdx.x;
   const int I = ca.interior[t], n = ca.n[t], b = ca.b[t];
   double* P = ca.rec + ca.P_off[t];
   const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
@@ -280,26 +280,12 @@ __device__ void cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double
   }
 }
 
-__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
-  extern __shared__ double smem[];
-  double* sred = smem + RED_OFF;
-  int* sint = reinterpret_cast<int*>(smem);  // scan scratch (first doubles are free here)
+// Gather A_{R,I} of skeleton s into W (column-major, ld = rows bound): alive rows of every
+// coupled group, only rows with a nonzero entry. Returns m (all threads).
+__device__ int skel_gather(const LevelDev& lv, const SkelArgs& sk, int s, double* W, int64_t ldw, int* sint) {
   const int tid = threadIdx.x;
-  const int s = sk.order[blockIdx.x];
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
-  const int64_t gof = lv.goff[g];
-  int64_t rows_max = 0;
-  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) rows_max += lv.gsize[sk.nbr[q]];
-  double* W = sk.work + sk.work_off[s];
-  const int64_t ldw = rows_max > 0 ? rows_max : 1;
-  double* vn1 = W + (int64_t)k * ldw;
-  double* vn2 = vn1 + k;
-  int* iw = sk.iwork + sk.iwork_off[s];
-  int* perm = iw;
-  int* sidx = iw + k;
-  int* flag = iw + 2 * k;
-  // gather A_{R,I}: alive rows of every coupled group, rows with a nonzero entry only
   int m = 0;
   for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) {
     const int h = sk.nbr[q], kh = lv.gsize[h];
@@ -329,14 +315,48 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
     }
   }
   __syncthreads();
+  return m;
+}
+
+__device__ __forceinline__ int64_t skel_ldw(const LevelDev& lv, const SkelArgs& sk, int s) {
+  int64_t rows_max = 0;
+  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) rows_max += lv.gsize[sk.nbr[q]];
+  return rows_max > 0 ? rows_max : 1;
+}
+
+// no coupling: every column redundant (kernels.py:95-98)
+__device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s) {
+  const int g = sk.groups[s], k = lv.gsize[g];
+  const int64_t gof = lv.goff[g];
+  for (int j = threadIdx.x; j < k; j += NT) {
+    sk.red[gof + j] = 1;
+    sk.alive[lv.mem[gof + j]] = 0;
+  }
+  if (threadIdx.x == 0) sk.rank[s] = 0;
+}
+
+__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
+  extern __shared__ double smem[];
+  double* sred = smem + RED_OFF;
+  int* sint = reinterpret_cast<int*>(smem);  // scan scratch (first doubles are free here)
+  const int tid = threadIdx.x;
+  const int s = sk.order[blockIdx.x];
+  const int g = sk.groups[s];
+  const int k = lv.gsize[g];
+  const int64_t gof = lv.goff[g];
+  const int64_t ldw = skel_ldw(lv, sk, s);
+  double* W = sk.work + sk.work_off[s];
+  double* vn1 = W + (int64_t)k * ldw;
+  double* vn2 = vn1 + k;
+  int* iw = sk.iwork + sk.iwork_off[s];
+  int* perm = iw;
+  int* sidx = iw + k;
+  int* flag = iw + 2 * k;
+  const int m = skel_gather(lv, sk, s, W, ldw, sint);
   if (tid == 0) sk.rows[s] = m;
   uint8_t* red = sk.red + gof;
-  if (m == 0) {  // no coupling: every column redundant (kernels.py:95-98)
-    for (int j = tid; j < k; j += NT) {
-      red[j] = 1;
-      sk.alive[lv.mem[gof + j]] = 0;
-    }
-    if (tid == 0) sk.rank[s] = 0;
+  if (m == 0) {
+    skel_all_redundant(lv, sk, s);
     return;
   }
   cta_cpqr(W, m, k, ldw, perm, vn1, vn2, sred);
@@ -376,6 +396,241 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
     if (flag[j]) sk.alive[lv.mem[gof + j]] = 0;
   }
   if (tid == 0) sk.rank[s] = r;
+}
+
+// Large separators: gather only (one CTA per face); the team kernel does the CPQR.
+__global__ void __launch_bounds__(NT) k_skel_gather(LevelDev lv, SkelArgs sk, const int* faces) {
+  extern __shared__ double smem[];
+  const int s = faces[blockIdx.x];
+  const int64_t ldw = skel_ldw(lv, sk, s);
+  double* W = sk.work + sk.work_off[s];
+  const int m = skel_gather(lv, sk, s, W, ldw, reinterpret_cast<int*>(smem));
+  if (threadIdx.x == 0) sk.rows[s] = m;
+}
+
+// ---------------------------------------------------------------------------
+// Team CPQR: one separator per team of P co-resident CTAs (cooperative launch).
+// Column j is owned by CTA j % P; per pivot step two team barriers: after the
+// local argmax, and after the owner of column i swapped in the pivot and formed
+// the reflector. Same arithmetic as cta_cpqr (dlaqp2 semantics).
+// All loads of data written by other CTAs bypass L1 (ld.global.cg).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void team_sync(TeamHdr* h, int P) {
+  __syncthreads();
+  if (threadIdx.x == 0 && P > 1) {
+    volatile unsigned* vgen = &h->gen;
+    const unsigned g0 = *vgen;
+    __threadfence();
+    if (atomicAdd(&h->count, 1u) == (unsigned)(P - 1)) {
+      h->count = 0;
+      __threadfence();
+      atomicAdd(&h->gen, 1u);
+    } else {
+      while (*vgen == g0) __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, TeamArgs ta) {
+  extern __shared__ double smem[];
+  double* sred = smem + RED_OFF;
+  double* vs = smem + SMEM_DOUBLES;          // Householder vector (if it fits)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  int f = 0;
+  while (f + 1 < ta.nface && ta.team_off[f + 1] <= (int)blockIdx.x) ++f;
+  const int c = blockIdx.x - ta.team_off[f];
+  const int P = ta.team_off[f + 1] - ta.team_off[f];
+  TeamHdr* hdr = ta.hdr + f;
+  double* slot_v = ta.slot_v + ta.team_off[f];
+  int* slot_i = ta.slot_i + ta.team_off[f];
+  const int s = ta.face[f];
+  const int g = sk.groups[s];
+  const int k = lv.gsize[g];
+  const int64_t gof = lv.goff[g];
+  const int64_t ldw = skel_ldw(lv, sk, s);
+  double* W = sk.work + sk.work_off[s];
+  double* vn1 = W + (int64_t)k * ldw;
+  double* vn2 = vn1 + k;
+  int* iw = sk.iwork + sk.iwork_off[s];
+  int* perm = iw;
+  int* sidx = iw + k;
+  int* flag = iw + 2 * k;
+  const int m = __ldcg(sk.rows + s);
+  if (m == 0) {
+    if (c == 0) skel_all_redundant(lv, sk, s);
+    return;
+  }
+  const bool v_in_smem = m <= ta.vcap;
+  const double tol3z = sqrt(DBL_EPSILON * 0.5);
+  // owned columns: j = c + P*t
+  for (int j = c + P * tid; j < k; j += P * NT) perm[j] = j;
+  for (int j = c + P * warp; j < k; j += P * nw) {
+    const double* cj = W + (int64_t)j * ldw;
+    double a = 0.0;
+    for (int r = lane; r < m; r += 32) {
+      const double x = __ldcg(cj + r);
+      a += x * x;
+    }
+    a = warp_sum(a);
+    if (lane == 0) {
+      __stcg(vn1 + j, sqrt(a));
+      __stcg(vn2 + j, sqrt(a));
+    }
+  }
+  team_sync(hdr, P);
+  const int mn = min(m, k);
+  for (int i = 0; i < mn; ++i) {
+    // (a) pivot: first index of the largest partial norm (idamax)
+    ArgMax loc{-1.0, 0x7fffffff};
+    const int jfirst = i + ((c - i % P) + P) % P;    // first owned column >= i
+    for (int j = jfirst + P * tid; j < k; j += P * NT) loc = better(loc, ArgMax{__ldcg(vn1 + j), j});
+    const ArgMax mine = cta_argmax(loc, sred);
+    if (tid == 0) {
+      __stcg(slot_v + c, mine.v);
+      __stcg(slot_i + c, mine.i);
+    }
+    team_sync(hdr, P);
+    ArgMax best{-1.0, 0x7fffffff};
+    for (int q = 0; q < P; ++q) best = better(best, ArgMax{__ldcg(slot_v + q), __ldcg(slot_i + q)});
+    const int p = best.i;
+    // (b) owner of column i: swap in the pivot column, form the reflector (dlarfg)
+    double* ci = W + (int64_t)i * ldw;
+    if (c == i % P) {
+      if (p != i) {
+        double* cp = W + (int64_t)p * ldw;
+        for (int r = tid; r < m; r += NT) {
+          const double a = __ldcg(ci + r), b = __ldcg(cp + r);
+          __stcg(ci + r, b);
+          __stcg(cp + r, a);
+        }
+        if (tid == 0) {
+          const int ti = __ldcg(perm + p);
+          __stcg(perm + p, __ldcg(perm + i));
+          __stcg(perm + i, ti);
+          __stcg(vn1 + p, __ldcg(vn1 + i));
+          __stcg(vn2 + p, __ldcg(vn2 + i));
+        }
+        __syncthreads();
+      }
+      double part = 0.0;
+      for (int r = i + 1 + tid; r < m; r += NT) {
+        const double x = __ldcg(ci + r);
+        part += x * x;
+      }
+      const double xnorm = sqrt(cta_sum(part, sred));
+      const double alpha = __ldcg(ci + i);
+      double tau = 0.0, beta = alpha;
+      if (xnorm != 0.0) {
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        tau = (beta - alpha) / beta;
+        const double scal = 1.0 / (alpha - beta);
+        for (int r = i + 1 + tid; r < m; r += NT) __stcg(ci + r, __ldcg(ci + r) * scal);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __stcg(ci + i, beta);
+        __stcg(&hdr->tau, tau);
+      }
+    }
+    team_sync(hdr, P);
+    const double tau = __ldcg(&hdr->tau);
+    // (c) apply H to owned trailing columns and downdate their norms
+    const double* v = ci;
+    if (v_in_smem) {
+      for (int r = i + 1 + tid; r < m; r += NT) vs[r] = __ldcg(ci + r);
+      __syncthreads();
+      v = vs;
+    }
+    const int jnext = (i + 1) + ((c - (i + 1) % P) + P) % P;   // first owned column > i
+    for (int j = jnext + P * warp; j < k; j += P * nw) {
+      double* cj = W + (int64_t)j * ldw;
+      if (tau != 0.0) {
+        double a = 0.0;
+        for (int r = i + 1 + lane; r < m; r += 32) a += (v_in_smem ? v[r] : __ldcg(v + r)) * __ldcg(cj + r);
+        a = warp_sum(a) + __ldcg(cj + i);
+        const double tw = tau * a;
+        __syncwarp();
+        if (lane == 0) __stcg(cj + i, __ldcg(cj + i) - tw);
+        for (int r = i + 1 + lane; r < m; r += 32)
+          __stcg(cj + r, __ldcg(cj + r) - tw * (v_in_smem ? v[r] : __ldcg(v + r)));
+        __syncwarp();
+      }
+      const double v1 = __ldcg(vn1 + j);
+      if (v1 != 0.0) {
+        double tt = fabs(__ldcg(cj + i)) / v1;
+        tt = 1.0 - tt * tt;
+        tt = tt < 0.0 ? 0.0 : tt;
+        const double rr = v1 / __ldcg(vn2 + j);
+        if (tt * rr * rr <= tol3z) {
+          double a = 0.0;
+          if (i < m - 1) {
+            for (int r = i + 1 + lane; r < m; r += 32) {
+              const double x = __ldcg(cj + r);
+              a += x * x;
+            }
+            a = sqrt(warp_sum(a));
+          }
+          __syncwarp();
+          if (lane == 0) {
+            __stcg(vn1 + j, a);
+            __stcg(vn2 + j, a);
+          }
+        } else {
+          __syncwarp();
+          if (lane == 0) __stcg(vn1 + j, v1 * sqrt(tt));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  team_sync(hdr, P);
+  // rank (identical on every CTA), natural-order maps by CTA 0
+  __shared__ int s_rank;
+  if (tid == 0) {
+    const double d0 = fabs(__ldcg(W));
+    const double cut = fmax(sk.eps, DBL_EPSILON * (double)max(m, k)) * d0;
+    int r = 0;
+    for (int i = 0; i < mn; ++i)
+      if (fabs(__ldcg(W + (int64_t)i * ldw + i)) > cut) ++r;
+    s_rank = r;
+    if (c == 0) {
+      for (int j = 0; j < k; ++j) flag[j] = 0;
+      for (int i = r; i < k; ++i) flag[__ldcg(perm + i)] = 1;
+      int ns = 0, nr = 0;
+      for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns++;
+    }
+  }
+  team_sync(hdr, P);
+  const int r = s_rank, kt = k - r;
+  // T = R11^-1 R12 for owned columns (warp per column, lanes over the inner sum)
+  for (int j = r + ((c - r % P) + P) % P + P * warp; j < k; j += P * nw) {
+    double* cj = W + (int64_t)j * ldw;
+    for (int i = r - 1; i >= 0; --i) {
+      double a = 0.0;
+      for (int l = i + 1 + lane; l < r; l += 32) a += __ldcg(W + (int64_t)l * ldw + i) * __ldcg(cj + l);
+      a = warp_sum(a);
+      __syncwarp();
+      if (lane == 0) __stcg(cj + i, (__ldcg(cj + i) - a) / __ldcg(W + (int64_t)i * ldw + i));
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  double* T = sk.rec + sk.T_off[s];
+  for (int j = r + ((c - r % P) + P) % P; j < k; j += P) {
+    const int col = __ldcg(sidx + __ldcg(perm + j));
+    for (int i = tid; i < r; i += NT) T[(int64_t)__ldcg(sidx + __ldcg(perm + i)) * kt + col] = __ldcg(W + (int64_t)j * ldw + i);
+  }
+  if (c == 0) {
+    uint8_t* red = sk.red + gof;
+    for (int j = tid; j < k; j += NT) {
+      const int fl = __ldcg(flag + j);
+      red[j] = (uint8_t)fl;
+      if (fl) sk.alive[lv.mem[gof + j]] = 0;
+    }
+    if (tid == 0) sk.rank[s] = r;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -439,6 +694,184 @@ __global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, De
     for (int64_t e = tid; e < (int64_t)r * r; e += NT) {
       const int a = (int)(e / r), b = (int)(e % r);
       A[(int64_t)skl[a] * k + skl[b]] = Ass[e];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Big cells: 64-wide right-looking steps, every step tile-parallel over all
+// big cells of the level (diag factor -> panel TRSM as GEMM with the explicit
+// 64x64 inverse -> trailing update tiles), then U = X^T X by tiles.
+// ---------------------------------------------------------------------------
+constexpr int BT = 64, BLD = 65;
+
+// one CTA per big cell still active at this step
+__global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
+  extern __shared__ double smem[];
+  double* D = smem;                 // BT x BLD
+  double* Li = smem + BT * BLD;     // BT x BLD (inverse)
+  __shared__ int sflag;
+  const int c = a.w_cell[blockIdx.x];
+  const int n = a.n[c], k0 = a.k0, kb = min(BT, n - k0);
+  double* P = a.P[c];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < BT * BT; e += NT) {
+    const int i = e / BT, j = e % BT;
+    D[i * BLD + j] = (i < kb && j <= i) ? P[(int64_t)(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
+    Li[i * BLD + j] = 0.0;
+  }
+  if (tid == 0) sflag = -1;
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    const double d = D[j * BLD + j];
+    if (!(d > 0.0)) {
+      if (tid == 0) sflag = j;
+      break;
+    }
+    const double ljj = sqrt(d);
+    __syncthreads();
+    if (tid == 0) D[j * BLD + j] = ljj;
+    for (int i = j + 1 + tid; i < kb; i += NT) D[i * BLD + j] /= ljj;
+    __syncthreads();
+    const int m = kb - j - 1;
+    for (int e = tid; e < m * m; e += NT) {
+      const int i = j + 1 + e / m, k = j + 1 + e % m;
+      if (k <= i) D[i * BLD + k] -= D[i * BLD + j] * D[k * BLD + j];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (sflag >= 0) {
+    if (tid == 0) report_bad(st, a.op[c], k0 + sflag);
+    return;
+  }
+  // inverse of the lower factor: column `col` of Li solves D x = e_col (thread per column)
+  for (int col = tid; col < BT; col += NT) {
+    for (int i = col; i < BT; ++i) {
+      double v = (i == col) ? 1.0 : 0.0;
+      for (int l = col; l < i; ++l) v -= D[i * BLD + l] * Li[l * BLD + col];
+      Li[i * BLD + col] = v / D[i * BLD + i];
+    }
+  }
+  __syncthreads();
+  double* Lo = a.Linv + (int64_t)c * BT * BT;
+  for (int e = tid; e < BT * BT; e += NT) {
+    const int i = e / BT, j = e % BT;
+    Lo[e] = Li[i * BLD + j];
+    if (i < kb && j < kb) P[(int64_t)(k0 + i) * n + k0 + j] = (j <= i) ? D[i * BLD + j] : 0.0;
+  }
+  // zero the strict upper part above this diagonal block (rows < k0, cols k0..k0+kb)
+  for (int64_t e = tid; e < (int64_t)k0 * kb; e += NT) P[(e / kb) * n + k0 + e % kb] = 0.0;
+}
+
+// acc += A (64 x 64) * B^T (64 x 64) on DMMA, both tiles row-major in smem (ld BLD)
+__device__ __forceinline__ void tile_mma_nt(const double* sA, const double* sB, double acc[2][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+#pragma unroll 4
+  for (int ks = 0; ks < BT; ks += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) af[x] = sA[(wm * 16 + x * 8 + g) * BLD + ks + t];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) bf[y] = sB[(wn * 32 + y * 8 + g) * BLD + ks + t];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+  }
+}
+
+// panel rows below the diagonal block: X = P[rows, k0:k0+64] * Linv^T (in place)
+__global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
+  extern __shared__ double smem[];
+  double* sA = smem;
+  double* sB = smem + BT * BLD;
+  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x];
+  const int n = a.n[c], rows = n + a.b[c], k0 = a.k0, kb = min(BT, n - k0);
+  const int r0 = k0 + kb + BT * it;
+  double* P = a.P[c];
+  const double* Li = a.Linv + (int64_t)c * BT * BT;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < BT * BT; e += NT) {
+    const int i = e / BT, j = e % BT;
+    sA[i * BLD + j] = (r0 + i < rows && j < kb) ? P[(int64_t)(r0 + i) * n + k0 + j] : 0.0;
+    sB[i * BLD + j] = Li[e];
+  }
+  __syncthreads();
+  double acc[2][4][2] = {};
+  tile_mma_nt(sA, sB, acc);
+  const int lane = tid & 31, warp = tid >> 5, wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
+        if (r0 + i < rows && j < kb) P[(int64_t)(r0 + i) * n + k0 + j] = acc[x][y][z];
+      }
+}
+
+// trailing update tile (i, j): C -= A_i A_j^T, K = this step's 64 columns
+__global__ void __launch_bounds__(NT) k_big_update(BigArgs a) {
+  extern __shared__ double smem[];
+  double* sA = smem;
+  double* sB = smem + BT * BLD;
+  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
+  const int n = a.n[c], rows = n + a.b[c], k0 = a.k0, kb = min(BT, n - k0);
+  const int base = k0 + kb;
+  const int r0 = base + BT * it, c0 = base + BT * jt;
+  double* P = a.P[c];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < BT * BT; e += NT) {
+    const int i = e / BT, j = e % BT;
+    sA[i * BLD + j] = (r0 + i < rows && j < kb) ? P[(int64_t)(r0 + i) * n + k0 + j] : 0.0;
+    sB[i * BLD + j] = (c0 + i < n && j < kb) ? P[(int64_t)(c0 + i) * n + k0 + j] : 0.0;
+  }
+  __syncthreads();
+  double acc[2][4][2] = {};
+  tile_mma_nt(sA, sB, acc);
+  const int lane = tid & 31, warp = tid >> 5, wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int i = r0 + wm * 16 + x * 8 + g, j = c0 + wn * 32 + y * 8 + 2 * t + z;
+        if (i < rows && j < n && (i >= n || j <= i)) P[(int64_t)i * n + j] -= acc[x][y][z];
+      }
+}
+
+// U = X^T X where X^T = P[n:n+b, 0:n]: one 64x64 output tile per CTA, K = n
+__global__ void __launch_bounds__(NT) k_big_syrk(BigArgs a) {
+  extern __shared__ double smem[];
+  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
+  const int n = a.n[c], b = a.b[c];
+  const double* PB = a.P[c] + (int64_t)n * n;
+  double* U = a.U[c];
+  const int i0 = BT * it, j0 = BT * jt;
+  cta_gemm<false, true>(min(BT, b - i0), min(BT, b - j0), n, 1.0, PB + (int64_t)i0 * n, n, PB + (int64_t)j0 * n,
+                        n, 0.0, U + (int64_t)i0 * b + j0, b, false, smem + GEMM_OFF);
+}
+
+// build panels [A_II ; A_BI] of big cells, grid-stride over (cell, chunk)
+__global__ void k_big_build(LevelDev lv, CellArgs ca, const int* big_cells, int nbig, int chunks) {
+  const int bc = blockIdx.x / chunks, ch = blockIdx.x % chunks;
+  if (bc >= nbig) return;
+  const int t = big_cells[bc];
+  const int I = ca.interior[t], n = ca.n[t];
+  double* P = ca.rec + ca.P_off[t];
+  const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
+  const int64_t stride = (int64_t)chunks * blockDim.x;
+  for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)n * n; e += stride) P[e] = A[e];
+  for (int64_t j = ca.nbr_off[t]; j < ca.nbr_off[t + 1]; ++j) {
+    const int w = ca.nbr_w[j], c0 = ca.nbr_col[j];
+    const double* S = lv.pool + lv.boff[ca.nbr_blk[j]];
+    for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)n * w; e += stride) {
+      const int i = (int)(e / w), r = (int)(e % w);
+      P[(int64_t)(n + c0 + r) * n + i] = S[e];
     }
   }
 }
@@ -661,10 +1094,10 @@ void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_ingest<<<nblk(N, 256), 256, 0, s>>>(lv, gid, pos, rowptr, col, val, N);
 }
-void launch_cell(const LevelDev& lv, const CellArgs& a, DevStatus* st, cudaStream_t s) {
-  if (a.p == 0) return;
+void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st, cudaStream_t s) {
+  if (count == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_cell<<<a.p, NT, SMEM_BYTES, s>>>(lv, a, st);
+  k_cell<<<count, NT, SMEM_BYTES, s>>>(lv, a, st);
 }
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s) {
   if (a.ntgt == 0) return;
@@ -685,6 +1118,59 @@ void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream
   if (count == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_skel_id<<<count, NT, SMEM_BYTES, s>>>(lv, a);
+}
+void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces, int count, cudaStream_t s) {
+  if (count == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_skel_gather<<<count, NT, SMEM_BYTES, s>>>(lv, a, faces);
+}
+int team_blocks_per_sm(int vcap) {
+  static int cached_cap = -1, cached = 0;
+  if (vcap == cached_cap) return cached;
+  const size_t bytes = SMEM_BYTES + (size_t)vcap * sizeof(double);
+  cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_skel_team, NT, bytes);
+  cached_cap = vcap;
+  cached = nb;
+  return nb;
+}
+void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s) {
+  if (nblocks == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const size_t bytes = SMEM_BYTES + (size_t)t.vcap * sizeof(double);
+  cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  LevelDev lv2 = lv;
+  SkelArgs a2 = a;
+  TeamArgs t2 = t;
+  void* args[] = {&lv2, &a2, &t2};
+  cudaLaunchCooperativeKernel((void*)k_skel_team, dim3(nblocks), dim3(NT), args, bytes, s);
+}
+static constexpr size_t BIG_SMEM = 2 * BT * BLD * sizeof(double);
+void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s) {
+  if (!nbig) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int chunks = 64;
+  k_big_build<<<nbig * chunks, 256, 0, s>>>(lv, ca, big_cells, nbig, chunks);
+}
+void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s) {
+  if (diag.nwork) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_big_diag<<<diag.nwork, NT, BIG_SMEM, s>>>(diag, st);
+  }
+  if (trsm.nwork) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_big_trsm<<<trsm.nwork, NT, BIG_SMEM, s>>>(trsm);
+  }
+  if (upd.nwork) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_big_update<<<upd.nwork, NT, BIG_SMEM, s>>>(upd);
+  }
+}
+void launch_big_syrk(const BigArgs& a, cudaStream_t s) {
+  if (!a.nwork) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_big_syrk<<<a.nwork, NT, SMEM_BYTES, s>>>(a);
 }
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.nsk == 0) return;
@@ -771,6 +1257,10 @@ void configure_kernels() {
   cudaFuncSetAttribute(k_apply_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_apply_prec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_apply_skel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_big_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
+  cudaFuncSetAttribute(k_big_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
+  cudaFuncSetAttribute(k_big_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
+  cudaFuncSetAttribute(k_big_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace phif

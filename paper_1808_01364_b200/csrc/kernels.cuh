@@ -29,6 +29,7 @@ struct LevelDev {
 
 struct CellArgs {
   int p;
+  const int* list;          // cells handled by the one-CTA kernel (nullptr = all)
   const int* interior;      // group ids
   const int64_t* nbr_off;   // p+1
   const int* nbr_blk;
@@ -85,6 +86,22 @@ struct SkelArgs {
   const int64_t* P_off;      // (kt + r) x kt
 };
 
+struct TeamHdr {
+  unsigned count;
+  unsigned gen;
+  double tau;
+};
+
+struct TeamArgs {
+  int nface;
+  const int* face;       // skeleton index per team
+  const int* team_off;   // nface+1 CTA offsets
+  TeamHdr* hdr;          // per team
+  double* slot_v;        // per CTA
+  int* slot_i;           // per CTA
+  int vcap;              // Householder vector staged in smem when m <= vcap
+};
+
 struct RepackArgs {
   int nblk;
   // new level
@@ -102,6 +119,28 @@ struct RepackArgs {
   const int* oadj_nbr;
   const int* oadj_blk;
   const int* ogsize;
+};
+
+}  // namespace phif
+
+namespace phif {
+
+// Tile-parallel path for big cells (one level's big cells batched): the panel
+// P_c ((n+b) x n row-major, ld n) is factored right-looking in 64-wide steps.
+struct BigArgs {
+  int ncell;
+  const int* n;            // per big cell
+  const int* b;
+  double* const* P;        // panel base per big cell
+  double* const* U;        // Schur output per big cell (b x b)
+  double* Linv;            // 64 x 64 scratch per big cell
+  const int* op;           // original op index (status reporting)
+  // per-step tile work list: (cell, row tile, col tile)
+  const int* w_cell;
+  const int* w_i;
+  const int* w_j;
+  int nwork;
+  int k0;                  // current step's panel start
 };
 
 }  // namespace phif

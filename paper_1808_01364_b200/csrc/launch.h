@@ -52,11 +52,17 @@ void configure_kernels();
 long long launch_count();   // kernel launches issued so far (all streams)
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
                    const double* val, int64_t N, cudaStream_t s);
-void launch_cell(const LevelDev& lv, const CellArgs& a, DevStatus* st, cudaStream_t s);
+void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st, cudaStream_t s);
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s);
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s);
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s);
+void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces, int count, cudaStream_t s);
+int team_blocks_per_sm(int vcap);
+void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s);
+void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s);
+void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
+void launch_big_syrk(const BigArgs& a, cudaStream_t s);
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s);
 void launch_repack(const RepackArgs& a, cudaStream_t s);
 void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s);

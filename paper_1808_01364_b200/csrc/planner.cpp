@@ -77,10 +77,38 @@ Groups classify_all(const Spec& s) {
   nkeys <<= s.dim;
   std::vector<int> key(s.N);
   std::vector<int64_t> cnt(nkeys + 1, 0);
-  for (int64_t i = 0; i < s.N; ++i) {
-    int q[3], b;
-    key[i] = (int)key_of(s, 0, i, q, b);
-    cnt[key[i] + 1]++;
+  {
+    // per-axis tables: cell index and on-line bit of every lattice coordinate
+    const int side = s.n - 1;
+    std::vector<int> qa(side + 1), ba(side + 1);
+    for (int c = 1; c <= side; ++c) {
+      qa[c] = c / sz;
+      ba[c] = (c % sz == 0) ? 1 : 0;
+    }
+    const int64_t plane = (int64_t)side * side;
+    const int nz = s.dim == 3 ? side : 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t yz = 0; yz < (int64_t)side * nz; ++yz) {
+      const int y = (int)(yz % side) + 1, z = s.dim == 3 ? (int)(yz / side) + 1 : 0;
+      int64_t base = 0;
+      int bits_yz = 0;
+      if (s.dim == 2) {
+        base = 0;
+        bits_yz = ba[y] << 1;
+      } else {
+        base = 0;
+        bits_yz = (ba[y] << 1) | (ba[z] << 2);
+      }
+      const int64_t row0 = (int64_t)(y - 1) * side + (s.dim == 3 ? (int64_t)(z - 1) * plane : 0);
+      for (int x = 1; x <= side; ++x) {
+        int64_t k = qa[x];
+        k = k * per + qa[y];
+        if (s.dim == 3) k = k * per + qa[z];
+        key[row0 + x - 1] = (int)((k << s.dim) | (ba[x] | bits_yz));
+      }
+      (void)base;
+    }
+    for (int64_t i = 0; i < s.N; ++i) cnt[key[i] + 1]++;
   }
   for (int64_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
   g.mem.resize(s.N);
@@ -172,22 +200,29 @@ int Pattern::find(int g, int h) const {
 std::vector<std::pair<int, int>> pattern_from_csr(const Groups& g, int64_t N, const int64_t* rowptr,
                                                   const int* col) {
   std::vector<int> gid(N, -1);
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < g.G; ++i)
     for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) gid[g.mem[p]] = i;
-  std::vector<int> last(g.G, -1);
   std::vector<std::pair<int, int>> pairs;
-  pairs.reserve(g.G * 8);
-  for (int i = 0; i < g.G; ++i)
-    for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) {
-      const int r = g.mem[p];
-      for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
-        const int h = gid[col[e]];
-        if (h >= i && last[h] != i) {
-          last[h] = i;
-          pairs.emplace_back(i, h);
+#pragma omp parallel
+  {
+    std::vector<std::pair<int, int>> mine;
+    std::vector<int> seen;
+#pragma omp for schedule(static) nowait
+    for (int i = 0; i < g.G; ++i) {
+      seen.clear();
+      for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) {
+        const int r = g.mem[p];
+        for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+          const int h = gid[col[e]];
+          if (h >= i && std::find(seen.begin(), seen.end(), h) == seen.end()) seen.push_back(h);
         }
       }
+      for (int h : seen) mine.emplace_back(i, h);
     }
+#pragma omp critical
+    pairs.insert(pairs.end(), mine.begin(), mine.end());
+  }
   return pairs;
 }
 
