@@ -138,7 +138,7 @@ void upload_structure(LevelRT& L, cudaStream_t s) {
 // Work lists for the tile-parallel big-cell path (one level).
 struct BigPlan {
   static constexpr int T = 64;
-  DBuf d_n, d_b, d_P, d_U, d_op, d_linv, d_list;
+  DBuf d_n, d_b, d_rows, d_P, d_U, d_op, d_linv, d_list;
   DBuf d_cell, d_i, d_j;
   std::vector<int64_t> diag_off, trsm_off, upd_off;   // per step offsets into the work arrays
   std::vector<int> steps_k0;
@@ -147,7 +147,7 @@ struct BigPlan {
   void build(const std::vector<int>& big, const std::vector<int>& cn, const std::vector<int>& cb, double* rec,
              const std::vector<int64_t>& P_off, double* U, const std::vector<int64_t>& U_off, cudaStream_t s) {
     nbig = (int)big.size();
-    std::vector<int> n(nbig), b(nbig), op(nbig);
+    std::vector<int> n(nbig), b(nbig), op(nbig), rws(nbig);
     std::vector<double*> Pp(nbig), Up(nbig);
     int nmax = 0;
     for (int c = 0; c < nbig; ++c) {
@@ -155,6 +155,7 @@ struct BigPlan {
       n[c] = cn[t];
       b[c] = cb[t];
       op[c] = t;
+      rws[c] = n[c] + b[c] + n[c];
       Pp[c] = rec + P_off[t];
       Up[c] = U + U_off[t];
       nmax = std::max(nmax, n[c]);
@@ -172,7 +173,7 @@ struct BigPlan {
       trsm_off.push_back((int64_t)wc.size());
       for (int c = 0; c < nbig; ++c) {
         if (n[c] <= k0) continue;
-        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = n[c] + b[c];
+        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = rws[c];
         const int ntr = (rows - base + T - 1) / T;
         for (int it = 0; it < ntr; ++it) {
           wc.push_back(c);
@@ -183,7 +184,7 @@ struct BigPlan {
       upd_off.push_back((int64_t)wc.size());
       for (int c = 0; c < nbig; ++c) {
         if (n[c] <= k0) continue;
-        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = n[c] + b[c];
+        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = rws[c];
         if (base >= n[c]) continue;
         const int nr = (rows - base + T - 1) / T, nc = (n[c] - base + T - 1) / T;
         for (int it = 0; it < nr; ++it)
@@ -209,6 +210,7 @@ struct BigPlan {
     syrk_n = (int64_t)wc.size() - syrk_off;
     upload(d_n, n, s);
     upload(d_b, b, s);
+    upload(d_rows, rws, s);
     upload(d_op, op, s);
     upload(d_P, Pp, s);
     upload(d_U, Up, s);
@@ -222,6 +224,7 @@ struct BigPlan {
     a.ncell = nbig;
     a.n = d_n.as<int>();
     a.b = d_b.as<int>();
+    a.rows = d_rows.as<int>();
     a.P = d_P.as<double* const>();
     a.U = d_U.as<double* const>();
     a.Linv = d_linv.as<double>();
@@ -245,9 +248,43 @@ struct BigPlan {
 
 }  // namespace
 
+// PHIF_TEAM_PROF=1: accumulate per-phase team CPQR cycles (printed at process exit)
+static long long* team_prof_buffer() {
+  static long long* buf = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    on = getenv("PHIF_TEAM_PROF") ? 1 : 0;
+    if (on) {
+      cudaMallocManaged(&buf, 16 * sizeof(long long));
+      for (int i = 0; i < 16; ++i) buf[i] = 0;
+      atexit([] {
+        cudaDeviceSynchronize();
+        fprintf(stderr, "[phif] team phases (Mcycles): argmax %.1f sync %.1f reflector %.1f own %.1f pass1 %.1f rowi %.1f pass2 %.1f recompute %.1f steps %lld\n",
+                buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6, buf[7] / 1e6, buf[8]);
+      });
+    }
+  }
+  return buf;
+}
+
+static void keep_pool_memory() {
+  // freed blocks stay in the stream-ordered pool instead of going back to the driver at every sync
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m, double eps, int method,
                                          cudaStream_t s, bool timing) {
   configure_kernels();
+  keep_pool_memory();
   auto F = std::make_unique<Factorization>();
   F->spec.init(dim, n, m);
   F->method = method;
@@ -298,13 +335,14 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       const int nn = P.cell_n[t], bb = P.cell_b[t];
       P_off[t] = rec;
       rec += (int64_t)(nn + bb) * nn;
+      if (nn >= BIG_N) rec += (int64_t)nn * nn;   // identity rows -> L^-T for the GEMM apply
       U_off[t] = uacc;
       uacc += (int64_t)bb * bb;
       I_off[t] = G.off[P.interior[t]];
       B_off[t] = bacc;
       bacc += bb;
       cwork[t] = wacc;
-      wacc += nn + bb;
+      wacc += nn + bb + (nn >= BIG_N ? nn : 0);
       for (int64_t j = P.cell_nbr_off[t]; j < P.cell_nbr_off[t + 1]; ++j) {
         const int h = P.cell_nbr[j];
         nbr_w[j] = G.size(h);
@@ -477,13 +515,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     std::vector<int> small_cells, big_cells;
     for (int t = 0; t < p; ++t) (P.cell_n[t] >= BIG_N ? big_cells : small_cells).push_back(t);
     DBG("level %d: cells p=%d (big %zu)", lev, p, big_cells.size());
-    DBuf d_small_cells;
-    upload(d_small_cells, small_cells, s);
+    upload(L.d_small_cells, small_cells, s);
+    L.h_small_cells = small_cells;
+    L.h_big_cells = big_cells;
+    L.h_P_off = P_off;
+    L.h_I_off = I_off;
+    L.h_B_off = B_off;
+    L.h_cwork = cwork;
     BigPlan bp;
     if (!big_cells.empty()) bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
     if (timing) CK(cudaEventRecord(ev[2], s));
     if (!small_cells.empty()) {
-      ca.list = d_small_cells.as<int>();
+      ca.list = L.d_small_cells.as<int>();
       launch_cell(dv, ca, (int)small_cells.size(), F->status.as<DevStatus>(), s);
     }
     if (!big_cells.empty()) {
@@ -589,7 +632,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       std::vector<int> small_list, large_list, team_face, team_off_all;
       std::vector<int64_t> small_off(P.nwaves + 1, 0), large_off(P.nwaves + 1, 0), toff_off(P.nwaves + 1, 0),
           slot_off(P.nwaves + 1, 0);
-      std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0);
+      std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0), wave_kmax(P.nwaves, 0);
       for (int w = 0; w < P.nwaves; ++w) {
         std::vector<int> large;
         for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
@@ -599,40 +642,57 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           else small_list.push_back(t);
         }
         small_off[w + 1] = (int64_t)small_list.size();
-        int vcap = 0;
+        int vcap = 0, kmax = 0;
         double wsum = 0.0;
         for (int t : large) {
+          kmax = std::max(kmax, G.size(P.skeleton[t]));
           vcap = std::max<int>(vcap, (int)std::min<int64_t>(rows_bound[t], 16384));
           wsum += (double)rows_bound[t] * G.size(P.skeleton[t]) * G.size(P.skeleton[t]);
         }
-        int budget = large.empty() ? 0 : team_blocks_per_sm(vcap) * num_sms;
+        int budget = large.empty() ? 0 : team_blocks_per_sm(vcap, kmax) * num_sms;
         budget = std::max<int>(budget, (int)large.size());
         toff_off[w] = (int64_t)team_off_all.size();
         team_off_all.push_back(0);
+        // team size: one owned-column chunk (16) per CTA when the budget allows, else work-proportional
+        std::vector<int> want(large.size());
+        int want_sum = 0;
+        for (size_t q = 0; q < large.size(); ++q) {
+          const int k = G.size(P.skeleton[large[q]]);
+          want[q] = std::min(128, std::max(1, (k + 15) / 16));
+          want_sum += want[q];
+        }
         int tot = 0;
-        for (int t : large) {
+        for (size_t q = 0; q < large.size(); ++q) {
+          const int t = large[q];
           const int k = G.size(P.skeleton[t]);
-          const double wf = (double)rows_bound[t] * k * k;
-          int Pf = (int)(budget * wf / wsum);
-          Pf = std::max(1, std::min(Pf, std::min(64, std::max(1, k / 4))));
-          if (tot + Pf > budget) Pf = std::max(1, budget - tot - (int)(large.size() - 1));
+          int Pf = want[q];
+          if (want_sum > budget) {
+            const double wf = (double)rows_bound[t] * k * k;
+            Pf = std::max(1, std::min(want[q], (int)(budget * wf / wsum)));
+          }
+          Pf = std::max(Pf, (k + 511) / 512);
           tot += Pf;
           team_face.push_back(t);
           team_off_all.push_back(tot);
           large_list.push_back(t);
         }
+        if (tot > budget) throw std::runtime_error("team CPQR: wave does not fit the co-resident budget");
         large_off[w + 1] = (int64_t)large_list.size();
+        L.team_P_mean += tot;
         slot_off[w + 1] = slot_off[w] + tot;
         wave_blocks[w] = tot;
         wave_vcap[w] = vcap;
+        wave_kmax[w] = kmax;
       }
+      L.n_large = (int)large_list.size();
+      if (L.n_large) L.team_P_mean /= L.n_large;
       DBuf d_small, d_large, d_toff, hdr, sv, si;
       upload(d_small, small_list, s);
       upload(d_large, large_list, s);
       upload(d_toff, team_off_all, s);
       hdr.alloc(std::max<size_t>(large_list.size(), 1) * sizeof(TeamHdr), s, true);
-      sv.alloc(std::max<int64_t>(slot_off[P.nwaves], 1) * sizeof(double), s);
-      si.alloc(std::max<int64_t>(slot_off[P.nwaves], 1) * sizeof(int), s);
+      sv.alloc(std::max<int64_t>(2 * slot_off[P.nwaves], 1) * sizeof(double), s);
+      si.alloc(std::max<int64_t>(2 * slot_off[P.nwaves], 1) * sizeof(int), s);
       for (int w = 0; w < P.nwaves; ++w) {
         ka.order = d_small.as<int>() + small_off[w];
         launch_skel_id(dv, ka, (int)(small_off[w + 1] - small_off[w]), s);
@@ -644,9 +704,11 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ta.face = d_large.as<int>() + large_off[w];
           ta.team_off = d_toff.as<int>() + toff_off[w];
           ta.hdr = hdr.as<TeamHdr>() + large_off[w];
-          ta.slot_v = sv.as<double>() + slot_off[w];
-          ta.slot_i = si.as<int>() + slot_off[w];
+          ta.slot_v = sv.as<double>() + 2 * slot_off[w];
+          ta.slot_i = si.as<int>() + 2 * slot_off[w];
           ta.vcap = wave_vcap[w];
+          ta.kmax = wave_kmax[w];
+          ta.prof = team_prof_buffer();
           launch_skel_team(dv, ka, ta, wave_blocks[w], s);
         }
       }
@@ -693,6 +755,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         L.fl[4] += 2.0 * rr * rr * kt + 4.0 * rr * kt * kt + kt * kt * kt / 3.0 + kt * kt * rr + kt * rr * rr;
         L.by[4] += 8.0 * (kk * kk + rr * rr + (kt + rr) * kt + rr * kt);
       }
+    }
+    for (int t = 0; t < nsk; ++t) {
+      const double kk = sr[t] + skt[t];
+      L.sep_k_mean += kk / nsk;
+      L.sep_m_mean += (double)h_rows[t] / nsk;
+      L.sep_k_max = std::max(L.sep_k_max, kk);
+      L.sep_m_max = std::max(L.sep_m_max, (double)h_rows[t]);
     }
     L.rho_max = nsk ? *std::max_element(sr.begin(), sr.end()) : 0;
     L.rho_mean = nsk ? (double)rsum / nsk : 0.0;
@@ -744,9 +813,126 @@ static void ensure_work(Factorization& F, int k) {
   }
 }
 
+// GEMM replay of big cells: L^-T is stored below [L ; X^T] in the panel.
+struct BigApply {
+  int k = -1;
+  double* work = nullptr;
+  double* wbuf = nullptr;
+  DBuf desc;                  // 4 phases of descriptors
+  DBuf wd, wt;                // work lists (descriptor, row tile)
+  int64_t ph_off[5] = {0, 0, 0, 0, 0};
+  DBuf gi_src, gi_dst, gi_len, sc_dst, gb_src, gb_dst, gb_len;
+  int nbig = 0;
+  void build(Factorization& F, LevelRT& L, int kk) {
+    k = kk;
+    work = F.work.as<double>();
+    wbuf = F.wbuf.as<double>();
+    cudaStream_t s = F.stream;
+    const LevelPlan& P = L.plan;
+    const double* rec = L.rec.as<double>();
+    std::vector<GemmDesc> d;
+    std::vector<int> wd_h, wt_h;
+    std::vector<int64_t> isrc, idst, sdst, bsrc, bdst;
+    std::vector<int> ilen, blen;
+    auto add = [&](const double* A, int lda, int ta, const double* B, double* C, int M, int K, double al,
+                   double be) {
+      if (M <= 0) return;
+      GemmDesc g;
+      g.A = A;
+      g.B = B;
+      g.C = C;
+      g.M = M;
+      g.N = k;
+      g.K = K;
+      g.lda = lda;
+      g.ldb = k;
+      g.ldc = k;
+      g.transA = ta;
+      g.alpha = al;
+      g.beta = be;
+      const int id = (int)d.size();
+      d.push_back(g);
+      for (int t = 0; t < (M + 63) / 64; ++t) {
+        wd_h.push_back(id);
+        wt_h.push_back(t);
+      }
+    };
+    nbig = (int)L.h_big_cells.size();
+    // phase 0: Z = (L^-T)^T Y ; phase 1: W = X^T Z ; phase 2: Y -= X Xb ; phase 3: Z = L^-T Y
+    for (int ph = 0; ph < 4; ++ph) {
+      ph_off[ph] = (int64_t)wd_h.size();
+      for (int t : L.h_big_cells) {
+        const int n = P.cell_n[t], b = P.cell_b[t];
+        const double* Pp = rec + L.h_P_off[t];
+        const double* XT = Pp + (int64_t)n * n;
+        const double* LiT = Pp + (int64_t)(n + b) * n;
+        double* Y = work + L.h_cwork[t] * k;
+        double* Z = Y + (int64_t)n * k;
+        double* Xb = Z + (int64_t)n * k;
+        if (ph == 0) add(LiT, n, 1, Y, Z, n, n, 1.0, 0.0);
+        if (ph == 1 && b > 0) add(XT, n, 0, Z, wbuf + L.h_B_off[t] * k, b, n, 1.0, 0.0);
+        if (ph == 2 && b > 0) add(XT, n, 1, Xb, Y, n, b, -1.0, 1.0);
+        if (ph == 3) add(LiT, n, 0, Y, Z, n, n, 1.0, 0.0);
+      }
+    }
+    ph_off[4] = (int64_t)wd_h.size();
+    for (int t : L.h_big_cells) {
+      const int n = P.cell_n[t], b = P.cell_b[t];
+      isrc.push_back(L.h_I_off[t]);
+      idst.push_back(L.h_cwork[t]);
+      sdst.push_back(L.h_cwork[t] + n);
+      ilen.push_back(n);
+      bsrc.push_back(L.h_B_off[t]);
+      bdst.push_back(L.h_cwork[t] + 2 * n);
+      blen.push_back(b);
+    }
+    upload(desc, d, s);
+    upload(wd, wd_h, s);
+    upload(wt, wt_h, s);
+    upload(gi_src, isrc, s);
+    upload(gi_dst, idst, s);
+    upload(gi_len, ilen, s);
+    upload(sc_dst, sdst, s);
+    upload(gb_src, bsrc, s);
+    upload(gb_dst, bdst, s);
+    upload(gb_len, blen, s);
+  }
+  void phase(int ph, cudaStream_t s) const {
+    launch_bgemm(desc.as<GemmDesc>(), wd.as<int>() + ph_off[ph], wt.as<int>() + ph_off[ph],
+                 (int)(ph_off[ph + 1] - ph_off[ph]), s);
+  }
+  void up(LevelRT& L, double* x, cudaStream_t s) const {
+    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+                false, s);
+    phase(0, s);
+    phase(1, s);
+    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), sc_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+                true, s);
+  }
+  void down(LevelRT& L, double* x, cudaStream_t s) const {
+    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+                false, s);
+    launch_rows(work, x, L.c_B.as<int>(), gb_src.as<int64_t>(), gb_dst.as<int64_t>(), gb_len.as<int>(), nbig, k,
+                false, s);
+    phase(2, s);
+    phase(3, s);
+    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), sc_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+                true, s);
+  }
+};
+
+static BigApply* big_apply(Factorization& F, LevelRT& L, int k) {
+  if (L.h_big_cells.empty()) return nullptr;
+  if (!L.bigap) L.bigap = std::make_shared<BigApply>();
+  BigApply& b = *L.bigap;
+  if (b.k != k || b.work != F.work.as<double>() || b.wbuf != F.wbuf.as<double>()) b.build(F, L, k);
+  return &b;
+}
+
 static ApplyCellArgs cell_args(Factorization& F, LevelRT& L) {
   ApplyCellArgs a;
-  a.p = (int)L.plan.interior.size();
+  a.list = L.h_small_cells.size() == L.plan.interior.size() ? nullptr : L.d_small_cells.as<int>();
+  a.p = (int)L.h_small_cells.size();
   a.n = L.c_n.as<int>();
   a.b = L.c_b.as<int>();
   a.I = L.mem.as<int>();
@@ -798,6 +984,7 @@ void apply(Factorization& F, double* x, int k, int mode) {
     for (auto& lp : F.levels) {
       LevelRT& L = *lp;
       launch_apply_cell(cell_args(F, L), x, k, true, s);
+      if (BigApply* ba = big_apply(F, L, k)) ba->up(L, x, s);
       launch_apply_reduce(L.bd_dof.as<int>(), L.bd_off.as<int64_t>(), L.bd_rows.as<int>(), F.wbuf.as<double>(),
                           L.nbd, x, k, s);
       if (L.plan.root) break;
@@ -813,6 +1000,7 @@ void apply(Factorization& F, double* x, int k, int mode) {
         launch_apply_prec(prec_args(F, L), x, k, false, s);
       }
       launch_apply_cell(cell_args(F, L), x, k, false, s);
+      if (BigApply* ba = big_apply(F, L, k)) ba->down(L, x, s);
     }
   }
   CK(cudaGetLastError());
@@ -992,7 +1180,9 @@ std::string Factorization::stats_json() const {
     o << (i ? "," : "") << "{\"level\":" << P.level << ",\"S\":" << L.S << ",\"p\":" << P.interior.size()
       << ",\"q\":" << (P.root ? 0 : P.skeleton.size()) << ",\"r\":" << (P.root ? 0 : P.precond.size())
       << ",\"blocks\":" << P.pat.bg.size() << ",\"waves\":" << P.nwaves << ",\"rho_max\":" << L.rho_max
-      << ",\"rho_mean\":" << L.rho_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
+      << ",\"rho_mean\":" << L.rho_mean << ",\"sep_k_mean\":" << L.sep_k_mean << ",\"sep_k_max\":" << L.sep_k_max
+      << ",\"sep_m_mean\":" << L.sep_m_mean << ",\"sep_m_max\":" << L.sep_m_max << ",\"n_large\":" << L.n_large
+      << ",\"team_P_mean\":" << L.team_P_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
       << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
       << L.t_ms[4] << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]
       << "," << L.fl[2] << "," << L.fl[3] << "," << L.fl[4] << "],\"bytes\":[" << L.by[0] << "," << L.by[1] << ","

@@ -55,6 +55,8 @@ struct Matrix {
   DBuf rowptr, col, val;
 };
 
+struct BigApply;   // GEMM replay of big records (engine.cu)
+
 struct LevelRT {
   LevelPlan plan;
   // structure on device
@@ -66,6 +68,10 @@ struct LevelRT {
   DBuf c_interior, c_nbr_off, c_nbr_blk, c_nbr_col, c_nbr_w, c_n, c_b, c_P_off, c_U_off;
   DBuf c_I_off, c_B, c_B_off, c_work_off;
   DBuf bd_dof, bd_off, bd_rows;
+  std::vector<int> h_small_cells, h_big_cells;
+  std::vector<int64_t> h_P_off, h_I_off, h_B_off, h_cwork;
+  DBuf d_small_cells;
+  std::shared_ptr<BigApply> bigap;
   int nbd = 0;
   int64_t cell_work_unit = 0, wbuf_unit = 0;
   // precondition
@@ -83,6 +89,8 @@ struct LevelRT {
   DBuf s_rows;
   int rho_max = 0;
   double rho_mean = 0.0;
+  double sep_k_mean = 0, sep_k_max = 0, sep_m_mean = 0, sep_m_max = 0, team_P_mean = 0;
+  int n_large = 0;
   int64_t S = 0;
   LevelDev dev() const;
 };

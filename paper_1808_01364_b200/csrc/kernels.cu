@@ -186,8 +186,11 @@ __device__ int cta_scan_flag(int f, int* sint, int* total) {
   return base + inwarp;
 }
 
-// Column-pivoted Householder QR of W (m x k, column-major, ldw), in place.
-__device__ void cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double* vn1, double* vn2, double* sred) {
+// Column-pivoted Householder QR of W (m x k, column-major, ldw), in place. Stops once the
+// largest remaining partial norm is below cutrel*|R_00| by a 1e-4 margin (pivot norms do
+// not increase, so no later diagonal can pass the ID cut). Returns the steps performed.
+__device__ int cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double* vn1, double* vn2, double* sred,
+                        double cutrel) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
   for (int j = tid; j < k; j += NT) perm[j] = j;
@@ -201,10 +204,13 @@ __device__ void cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double
   __syncthreads();
   const int mn = min(m, k);
   double* sh = sred + 32;  // [0] tau
+  double cut = 0.0;
   for (int i = 0; i < mn; ++i) {
     ArgMax loc{-1.0, 0x7fffffff};
     for (int j = i + tid; j < k; j += NT) loc = better(loc, ArgMax{vn1[j], j});
-    const int p = cta_argmax(loc, sred).i;
+    const ArgMax best = cta_argmax(loc, sred);
+    if (i > 0 && best.v < cut * (1.0 - 1e-4)) return i;
+    const int p = best.i;
     if (p != i) {
       double* ci = W + (int64_t)i * ldw;
       double* cp = W + (int64_t)p * ldw;
@@ -241,6 +247,7 @@ __device__ void cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double
       ci[i] = beta;
       sh[0] = tau;
     }
+    if (i == 0) cut = cutrel * fabs(beta);
     __syncthreads();
     // apply H to trailing columns, then downdate partial norms (dlarf + dlaqp2 loop 10)
     for (int j = i + 1 + warp; j < k; j += nw) {
@@ -278,6 +285,7 @@ __device__ void cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double
     }
     __syncthreads();
   }
+  return mn;
 }
 
 // Gather A_{R,I} of skeleton s into W (column-major, ld = rows bound): alive rows of every
@@ -359,14 +367,13 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
     skel_all_redundant(lv, sk, s);
     return;
   }
-  cta_cpqr(W, m, k, ldw, perm, vn1, vn2, sred);
+  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
+  const int steps = cta_cpqr(W, m, k, ldw, perm, vn1, vn2, sred, cutrel);
   __shared__ int s_rank;
   if (tid == 0) {
-    const int mn = min(m, k);
-    const double d0 = fabs(W[0]);
-    const double cut = fmax(sk.eps, DBL_EPSILON * (double)max(m, k)) * d0;
+    const double cut = cutrel * fabs(W[0]);
     int r = 0;
-    for (int i = 0; i < mn; ++i)
+    for (int i = 0; i < steps; ++i)
       if (fabs(W[(int64_t)i * ldw + i]) > cut) ++r;
     s_rank = r;
     for (int j = 0; j < k; ++j) flag[j] = 0;
@@ -433,137 +440,218 @@ __device__ __forceinline__ void team_sync(TeamHdr* h, int P) {
   __syncthreads();
 }
 
+constexpr int TCH = 16;      // owned columns updated together per pass
+constexpr int TOWN = 512;    // max owned columns per CTA (smem norms)
+
+// Team CPQR without data movement: the physical column j is owned by CTA j % P
+// for the whole factorization; LAPACK's column interchanges are replayed on a
+// replicated logical permutation (inv: logical -> physical, pos: physical ->
+// logical) so that pivot ties break on the same logical index as idamax.
+// Every CTA forms the Householder reflector of the pivot column itself, so a
+// pivot step needs a single team barrier (after the local argmax); the owner of
+// the pivot column writes [beta; v] back at the start of the next step. The
+// partial norms of owned columns live in the owner's shared memory.
 __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, TeamArgs ta) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
-  double* vs = smem + SMEM_DOUBLES;          // Householder vector (if it fits)
+  double* sdot = smem + GEMM_OFF;               // [nw][TCH] partial dots, then [TCH] products
+  double* vs = smem + SMEM_DOUBLES;             // reflector (rows > i), vcap doubles
+  __shared__ double ovn1[TOWN], ovn2[TOWN];
+  __shared__ int s_rec[TCH], s_nrec;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   int f = 0;
   while (f + 1 < ta.nface && ta.team_off[f + 1] <= (int)blockIdx.x) ++f;
   const int c = blockIdx.x - ta.team_off[f];
   const int P = ta.team_off[f + 1] - ta.team_off[f];
   TeamHdr* hdr = ta.hdr + f;
-  double* slot_v = ta.slot_v + ta.team_off[f];
-  int* slot_i = ta.slot_i + ta.team_off[f];
+  double* slot_v = ta.slot_v + 2 * ta.team_off[f];
+  int* slot_i = ta.slot_i + 2 * ta.team_off[f];
   const int s = ta.face[f];
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
   const int64_t gof = lv.goff[g];
   const int64_t ldw = skel_ldw(lv, sk, s);
   double* W = sk.work + sk.work_off[s];
-  double* vn1 = W + (int64_t)k * ldw;
-  double* vn2 = vn1 + k;
   int* iw = sk.iwork + sk.iwork_off[s];
   int* perm = iw;
   int* sidx = iw + k;
   int* flag = iw + 2 * k;
+  int* inv = reinterpret_cast<int*>(vs + ta.vcap);   // k ints
+  int* pos = inv + k;                                // k ints
   const int m = __ldcg(sk.rows + s);
   if (m == 0) {
     if (c == 0) skel_all_redundant(lv, sk, s);
     return;
   }
+  const int nloc = c < k ? (k - c + P - 1) / P : 0;   // owned columns j = c + P*t
   const bool v_in_smem = m <= ta.vcap;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
-  // owned columns: j = c + P*t
-  for (int j = c + P * tid; j < k; j += P * NT) perm[j] = j;
-  for (int j = c + P * warp; j < k; j += P * nw) {
-    const double* cj = W + (int64_t)j * ldw;
+  for (int j = tid; j < k; j += NT) {
+    inv[j] = j;
+    pos[j] = j;
+  }
+  for (int t = warp; t < nloc; t += nw) {
+    const double* cj = W + (int64_t)(c + P * t) * ldw;
     double a = 0.0;
     for (int r = lane; r < m; r += 32) {
       const double x = __ldcg(cj + r);
       a += x * x;
     }
-    a = warp_sum(a);
-    if (lane == 0) {
-      __stcg(vn1 + j, sqrt(a));
-      __stcg(vn2 + j, sqrt(a));
-    }
+    a = sqrt(warp_sum(a));
+    if (lane == 0) ovn1[t] = ovn2[t] = a;
   }
-  team_sync(hdr, P);
+  __syncthreads();
   const int mn = min(m, k);
+  double* diagR = W + (int64_t)k * ldw;   // |R_ii| of completed steps (the reflectors themselves are not kept)
+  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
+  double cut = 0.0;
+  int steps = 0;
+  __shared__ int s_own[TOWN];
+  const bool prof = ta.prof && blockIdx.x == 0 && tid == 0;
+  long long tp = prof ? clock64() : 0;
+#define TEAM_PHASE(id)                                   \
+  if (prof) {                                            \
+    const long long now = clock64();                     \
+    ta.prof[id] += now - tp;                             \
+    tp = now;                                            \
+  }
   for (int i = 0; i < mn; ++i) {
-    // (a) pivot: first index of the largest partial norm (idamax)
+    // (a) local argmax over owned unpivoted columns: value, then logical position (idamax)
     ArgMax loc{-1.0, 0x7fffffff};
-    const int jfirst = i + ((c - i % P) + P) % P;    // first owned column >= i
-    for (int j = jfirst + P * tid; j < k; j += P * NT) loc = better(loc, ArgMax{__ldcg(vn1 + j), j});
+    for (int t = tid; t < nloc; t += NT) {
+      const int pj = pos[c + P * t];
+      if (pj >= i) loc = better(loc, ArgMax{ovn1[t], pj});
+    }
     const ArgMax mine = cta_argmax(loc, sred);
+    const int par = (i & 1) * P;
     if (tid == 0) {
-      __stcg(slot_v + c, mine.v);
-      __stcg(slot_i + c, mine.i);
+      __stcg(slot_v + par + c, mine.v);
+      __stcg(slot_i + par + c, mine.i);
     }
+    TEAM_PHASE(0);
     team_sync(hdr, P);
-    ArgMax best{-1.0, 0x7fffffff};
-    for (int q = 0; q < P; ++q) best = better(best, ArgMax{__ldcg(slot_v + q), __ldcg(slot_i + q)});
+    TEAM_PHASE(1);
+    ArgMax cand{-1.0, 0x7fffffff};
+    for (int q = tid; q < P; q += NT) cand = better(cand, ArgMax{__ldcg(slot_v + par + q), __ldcg(slot_i + par + q)});
+    const ArgMax best = cta_argmax(cand, sred);
+    // early exit: pivot norms do not increase, so once the largest remaining partial norm is
+    // clearly below the rank cut no later |R_jj| can pass it; R11 and R12 are final already
+    if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
     const int p = best.i;
-    // (b) owner of column i: swap in the pivot column, form the reflector (dlarfg)
-    double* ci = W + (int64_t)i * ldw;
-    if (c == i % P) {
-      if (p != i) {
-        double* cp = W + (int64_t)p * ldw;
-        for (int r = tid; r < m; r += NT) {
-          const double a = __ldcg(ci + r), b = __ldcg(cp + r);
-          __stcg(ci + r, b);
-          __stcg(cp + r, a);
-        }
-        if (tid == 0) {
-          const int ti = __ldcg(perm + p);
-          __stcg(perm + p, __ldcg(perm + i));
-          __stcg(perm + i, ti);
-          __stcg(vn1 + p, __ldcg(vn1 + i));
-          __stcg(vn2 + p, __ldcg(vn2 + i));
-        }
-        __syncthreads();
-      }
-      double part = 0.0;
-      for (int r = i + 1 + tid; r < m; r += NT) {
-        const double x = __ldcg(ci + r);
-        part += x * x;
-      }
-      const double xnorm = sqrt(cta_sum(part, sred));
-      const double alpha = __ldcg(ci + i);
-      double tau = 0.0, beta = alpha;
-      if (xnorm != 0.0) {
-        beta = -copysign(hypot(alpha, xnorm), alpha);
-        tau = (beta - alpha) / beta;
-        const double scal = 1.0 / (alpha - beta);
-        for (int r = i + 1 + tid; r < m; r += NT) __stcg(ci + r, __ldcg(ci + r) * scal);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        __stcg(ci + i, beta);
-        __stcg(&hdr->tau, tau);
-      }
+    const int phys = inv[p];
+    __syncthreads();
+    if (tid == 0 && p != i) {   // replay the interchange on the logical permutation
+      const int a = inv[i];
+      inv[i] = phys;
+      inv[p] = a;
+      pos[a] = p;
+      pos[phys] = i;
     }
-    team_sync(hdr, P);
-    const double tau = __ldcg(&hdr->tau);
-    // (c) apply H to owned trailing columns and downdate their norms
-    const double* v = ci;
-    if (v_in_smem) {
-      for (int r = i + 1 + tid; r < m; r += NT) vs[r] = __ldcg(ci + r);
-      __syncthreads();
-      v = vs;
+    // (b) reflector of the pivot column (dlarfg), formed by every CTA
+    const double* cp = W + (int64_t)phys * ldw;
+    double part = 0.0;
+    for (int r = i + 1 + tid; r < m; r += NT) {
+      const double x = __ldcg(cp + r);
+      if (v_in_smem) vs[r] = x;
+      part += x * x;
     }
-    const int jnext = (i + 1) + ((c - (i + 1) % P) + P) % P;   // first owned column > i
-    for (int j = jnext + P * warp; j < k; j += P * nw) {
-      double* cj = W + (int64_t)j * ldw;
+    const double xnorm = sqrt(cta_sum(part, sred));   // cta_sum syncs: inv/pos/vs visible
+    TEAM_PHASE(2);
+    const double alpha = __ldcg(cp + i);
+    double tau = 0.0, beta = alpha, scal = 1.0;
+    if (xnorm != 0.0) {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (i == 0) cut = cutrel * fabs(beta);
+    if (c == 0 && tid == 0) __stcg(diagR + i, beta);
+    steps = i + 1;
+    // (c) apply H = I - tau [1; v][1; v]^T (v = scal * x) to owned unpivoted columns, TCH at a time
+    // compact list of owned unpivoted columns (local index t) in shared memory
+    __shared__ int s_nact;
+    if (tid == 0) {
+      int a = 0;
+      for (int t = 0; t < nloc; ++t)
+        if (pos[c + P * t] > i) s_own[a++] = t;
+      s_nact = a;
+    }
+    __syncthreads();
+    TEAM_PHASE(3);
+    const int nact = s_nact;
+    for (int u0 = 0; u0 < nact; u0 += TCH) {
+      const int nown = min(TCH, nact - u0);
+      int own[TCH];
+#pragma unroll
+      for (int u = 0; u < TCH; ++u) own[u] = c + P * s_own[u0 + (u < nown ? u : 0)];
       if (tau != 0.0) {
-        double a = 0.0;
-        for (int r = i + 1 + lane; r < m; r += 32) a += (v_in_smem ? v[r] : __ldcg(v + r)) * __ldcg(cj + r);
-        a = warp_sum(a) + __ldcg(cj + i);
-        const double tw = tau * a;
-        __syncwarp();
-        if (lane == 0) __stcg(cj + i, __ldcg(cj + i) - tw);
-        for (int r = i + 1 + lane; r < m; r += 32)
-          __stcg(cj + r, __ldcg(cj + r) - tw * (v_in_smem ? v[r] : __ldcg(v + r)));
-        __syncwarp();
+        double acc[TCH];
+#pragma unroll
+        for (int u = 0; u < TCH; ++u) acc[u] = 0.0;
+        for (int r = i + 1 + tid; r < m; r += NT) {
+          const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
+#pragma unroll
+          for (int u = 0; u < TCH; ++u)
+            if (u < nown) acc[u] += vr * __ldcg(W + (int64_t)own[u] * ldw + r);
+        }
+#pragma unroll
+        for (int u = 0; u < TCH; ++u) {
+          const double t2 = warp_sum(acc[u]);
+          if (lane == 0) sdot[warp * TCH + u] = t2;
+        }
       }
-      const double v1 = __ldcg(vn1 + j);
-      if (v1 != 0.0) {
-        double tt = fabs(__ldcg(cj + i)) / v1;
-        tt = 1.0 - tt * tt;
-        tt = tt < 0.0 ? 0.0 : tt;
-        const double rr = v1 / __ldcg(vn2 + j);
-        if (tt * rr * rr <= tol3z) {
+      if (tid == 0) s_nrec = 0;
+      __syncthreads();
+      TEAM_PHASE(4);
+      if (tid < nown) {
+        const int t = s_own[u0 + tid];
+        double* cj = W + (int64_t)(c + P * t) * ldw;
+        double rowi = __ldcg(cj + i);
+        double tw = 0.0;
+        if (tau != 0.0) {
+          double w = 0.0;
+          for (int q = 0; q < nw; ++q) w += sdot[q * TCH + tid];
+          tw = tau * (rowi + scal * w);
+          rowi -= tw;
+          __stcg(cj + i, rowi);
+        }
+        sdot[nw * TCH + tid] = tw * scal;
+        // partial-norm downdate (dlaqp2 loop 10) on the updated pivot-row entry
+        const double v1 = ovn1[t];
+        int rec = 0;
+        if (v1 != 0.0) {
+          double tt = fabs(rowi) / v1;
+          tt = 1.0 - tt * tt;
+          tt = tt < 0.0 ? 0.0 : tt;
+          const double rr = v1 / ovn2[t];
+          if (tt * rr * rr <= tol3z) rec = 1;
+          else ovn1[t] = v1 * sqrt(tt);
+        }
+        s_rec[tid] = rec;
+        if (rec) atomicAdd(&s_nrec, 1);
+      }
+      __syncthreads();
+      TEAM_PHASE(5);
+      if (tau != 0.0) {
+        double tw[TCH];
+#pragma unroll
+        for (int u = 0; u < TCH; ++u) tw[u] = (u < nown) ? sdot[nw * TCH + u] : 0.0;
+        for (int r = i + 1 + tid; r < m; r += NT) {
+          const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
+#pragma unroll
+          for (int u = 0; u < TCH; ++u)
+            if (u < nown) {
+              double* q = W + (int64_t)own[u] * ldw + r;
+              __stcg(q, __ldcg(q) - tw[u] * vr);
+            }
+        }
+      }
+      TEAM_PHASE(6);
+      if (s_nrec) {
+        __syncthreads();
+        for (int u = warp; u < nown; u += nw) {
+          if (!s_rec[u]) continue;
+          const double* cj = W + (int64_t)own[u] * ldw;
           double a = 0.0;
           if (i < m - 1) {
             for (int r = i + 1 + lane; r < m; r += 32) {
@@ -572,55 +660,55 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
             }
             a = sqrt(warp_sum(a));
           }
-          __syncwarp();
-          if (lane == 0) {
-            __stcg(vn1 + j, a);
-            __stcg(vn2 + j, a);
-          }
-        } else {
-          __syncwarp();
-          if (lane == 0) __stcg(vn1 + j, v1 * sqrt(tt));
+          if (lane == 0) ovn1[s_own[u0 + u]] = ovn2[s_own[u0 + u]] = a;
         }
       }
+      __syncthreads();
+      TEAM_PHASE(7);
     }
-    __syncthreads();
+    if (prof) ta.prof[8] += 1;
   }
+#undef TEAM_PHASE
   team_sync(hdr, P);
-  // rank (identical on every CTA), natural-order maps by CTA 0
+  // rank from the diagonal R_ii = W[inv[i]][i] (identical on every CTA); natural-order maps by CTA 0
   __shared__ int s_rank;
   if (tid == 0) {
-    const double d0 = fabs(__ldcg(W));
-    const double cut = fmax(sk.eps, DBL_EPSILON * (double)max(m, k)) * d0;
+    const double cutv = cutrel * fabs(__ldcg(diagR));
     int r = 0;
-    for (int i = 0; i < mn; ++i)
-      if (fabs(__ldcg(W + (int64_t)i * ldw + i)) > cut) ++r;
+    for (int i = 0; i < steps; ++i)
+      if (fabs(__ldcg(diagR + i)) > cutv) ++r;
     s_rank = r;
     if (c == 0) {
-      for (int j = 0; j < k; ++j) flag[j] = 0;
-      for (int i = r; i < k; ++i) flag[__ldcg(perm + i)] = 1;
+      for (int j = 0; j < k; ++j) {
+        flag[j] = 0;
+        perm[j] = inv[j];
+      }
+      for (int i = r; i < k; ++i) flag[inv[i]] = 1;
       int ns = 0, nr = 0;
       for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns++;
     }
   }
   team_sync(hdr, P);
   const int r = s_rank, kt = k - r;
-  // T = R11^-1 R12 for owned columns (warp per column, lanes over the inner sum)
-  for (int j = r + ((c - r % P) + P) % P + P * warp; j < k; j += P * nw) {
-    double* cj = W + (int64_t)j * ldw;
-    for (int i = r - 1; i >= 0; --i) {
+  // T = R11^-1 R12: owned physical columns at logical positions >= r (warp per column)
+  for (int ph = c + P * warp; ph < k; ph += P * nw) {
+    if (pos[ph] < r) continue;
+    double* cj = W + (int64_t)ph * ldw;
+    for (int l = r - 1; l >= 0; --l) {
       double a = 0.0;
-      for (int l = i + 1 + lane; l < r; l += 32) a += __ldcg(W + (int64_t)l * ldw + i) * __ldcg(cj + l);
+      for (int l2 = l + 1 + lane; l2 < r; l2 += 32) a += __ldcg(W + (int64_t)inv[l2] * ldw + l) * __ldcg(cj + l2);
       a = warp_sum(a);
       __syncwarp();
-      if (lane == 0) __stcg(cj + i, (__ldcg(cj + i) - a) / __ldcg(W + (int64_t)i * ldw + i));
+      if (lane == 0) __stcg(cj + l, (__ldcg(cj + l) - a) / __ldcg(diagR + l));
       __syncwarp();
     }
   }
   __syncthreads();
   double* T = sk.rec + sk.T_off[s];
-  for (int j = r + ((c - r % P) + P) % P; j < k; j += P) {
-    const int col = __ldcg(sidx + __ldcg(perm + j));
-    for (int i = tid; i < r; i += NT) T[(int64_t)__ldcg(sidx + __ldcg(perm + i)) * kt + col] = __ldcg(W + (int64_t)j * ldw + i);
+  for (int ph = c; ph < k; ph += P) {
+    if (pos[ph] < r) continue;
+    const int col = __ldcg(sidx + ph);
+    for (int l = tid; l < r; l += NT) T[(int64_t)__ldcg(sidx + inv[l]) * kt + col] = __ldcg(W + (int64_t)ph * ldw + l);
   }
   if (c == 0) {
     uint8_t* red = sk.red + gof;
@@ -788,7 +876,7 @@ __global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
   double* sA = smem;
   double* sB = smem + BT * BLD;
   const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x];
-  const int n = a.n[c], rows = n + a.b[c], k0 = a.k0, kb = min(BT, n - k0);
+  const int n = a.n[c], rows = a.rows[c], k0 = a.k0, kb = min(BT, n - k0);
   const int r0 = k0 + kb + BT * it;
   double* P = a.P[c];
   const double* Li = a.Linv + (int64_t)c * BT * BT;
@@ -819,7 +907,7 @@ __global__ void __launch_bounds__(NT) k_big_update(BigArgs a) {
   double* sA = smem;
   double* sB = smem + BT * BLD;
   const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
-  const int n = a.n[c], rows = n + a.b[c], k0 = a.k0, kb = min(BT, n - k0);
+  const int n = a.n[c], rows = a.rows[c], k0 = a.k0, kb = min(BT, n - k0);
   const int base = k0 + kb;
   const int r0 = base + BT * it, c0 = base + BT * jt;
   double* P = a.P[c];
@@ -874,6 +962,46 @@ __global__ void k_big_build(LevelDev lv, CellArgs ca, const int* big_cells, int 
       P[(int64_t)(n + c0 + r) * n + i] = S[e];
     }
   }
+  // identity rows below [A_II; A_BI]: the partial Cholesky turns them into L^-T (apply by GEMM)
+  double* Id = P + (int64_t)(n + ca.b[t]) * n;
+  for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)n * n; e += stride)
+    Id[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Batched GEMM: one 64-row output tile (all N columns, 64 at a time) per CTA.
+// work[i] = (descriptor, row tile).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile) {
+  extern __shared__ double smem[];
+  const GemmDesc d = desc[w_desc[blockIdx.x]];
+  const int i0 = 64 * w_tile[blockIdx.x];
+  const int M = min(64, d.M - i0);
+  if (M <= 0) return;
+  for (int j0 = 0; j0 < d.N; j0 += 64) {
+    const int N = min(64, d.N - j0);
+    if (d.transA)
+      cta_gemm<true, false>(M, N, d.K, d.alpha, d.A + i0, d.lda, d.B + j0, d.ldb, d.beta,
+                            d.C + (int64_t)i0 * d.ldc + j0, d.ldc, false, smem + GEMM_OFF);
+    else
+      cta_gemm<false, false>(M, N, d.K, d.alpha, d.A + (int64_t)i0 * d.lda, d.lda, d.B + j0, d.ldb, d.beta,
+                             d.C + (int64_t)i0 * d.ldc + j0, d.ldc, false, smem + GEMM_OFF);
+  }
+}
+
+// gather / scatter of DOF rows for a list of index segments: Y[seg_off + e] <-> x[idx[e]]
+__global__ void k_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
+                       const int* seg_len, int nseg, int k, int to_x, int chunks) {
+  const int sgi = blockIdx.x / chunks, ch = blockIdx.x % chunks;
+  if (sgi >= nseg) return;
+  const int* id = idx + seg_src[sgi];
+  double* y = Y + seg_dst[sgi] * k;
+  const int64_t n = (int64_t)seg_len[sgi] * k;
+  for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < n; e += (int64_t)chunks * blockDim.x) {
+    double* px = x + (int64_t)id[e / k] * k + e % k;
+    if (to_x) *px = y[e];
+    else y[e] = *px;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -914,7 +1042,7 @@ __device__ __forceinline__ void scatter_rows(double* x, const double* Y, const i
 
 __global__ void __launch_bounds__(NT) k_apply_cell(ApplyCellArgs a, double* x, int k, int up) {
   extern __shared__ double smem[];
-  const int t = blockIdx.x;
+  const int t = a.list ? a.list[blockIdx.x] : blockIdx.x;
   const int n = a.n[t], b = a.b[t];
   const int* I = a.I + a.I_off[t];
   const int* B = a.B + a.B_off[t];
@@ -1124,21 +1252,23 @@ void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces,
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_skel_gather<<<count, NT, SMEM_BYTES, s>>>(lv, a, faces);
 }
-int team_blocks_per_sm(int vcap) {
-  static int cached_cap = -1, cached = 0;
-  if (vcap == cached_cap) return cached;
-  const size_t bytes = SMEM_BYTES + (size_t)vcap * sizeof(double);
+static size_t team_smem(int vcap, int kmax) { return SMEM_BYTES + (size_t)vcap * sizeof(double) + 2 * sizeof(int) * (size_t)kmax; }
+int team_blocks_per_sm(int vcap, int kmax) {
+  static size_t cached_bytes = 0;
+  static int cached = 0;
+  const size_t bytes = team_smem(vcap, kmax);
+  if (bytes == cached_bytes) return cached;
   cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_skel_team, NT, bytes);
-  cached_cap = vcap;
+  cached_bytes = bytes;
   cached = nb;
   return nb;
 }
 void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s) {
   if (nblocks == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const size_t bytes = SMEM_BYTES + (size_t)t.vcap * sizeof(double);
+  const size_t bytes = team_smem(t.vcap, t.kmax);
   cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   LevelDev lv2 = lv;
   SkelArgs a2 = a;
@@ -1171,6 +1301,18 @@ void launch_big_syrk(const BigArgs& a, cudaStream_t s) {
   if (!a.nwork) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_big_syrk<<<a.nwork, NT, SMEM_BYTES, s>>>(a);
+}
+void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
+  if (!nwork) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_bgemm<<<nwork, NT, SMEM_BYTES, s>>>(desc, w_desc, w_tile);
+}
+void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
+                 const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s) {
+  if (!nseg) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int chunks = 16;
+  k_rows<<<nseg * chunks, 256, 0, s>>>(Y, x, idx, seg_src, seg_dst, seg_len, nseg, k, to_x ? 1 : 0, chunks);
 }
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.nsk == 0) return;
@@ -1261,6 +1403,7 @@ void configure_kernels() {
   cudaFuncSetAttribute(k_big_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
   cudaFuncSetAttribute(k_big_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
   cudaFuncSetAttribute(k_big_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_bgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace phif

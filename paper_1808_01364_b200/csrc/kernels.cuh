@@ -97,9 +97,11 @@ struct TeamArgs {
   const int* face;       // skeleton index per team
   const int* team_off;   // nface+1 CTA offsets
   TeamHdr* hdr;          // per team
-  double* slot_v;        // per CTA
-  int* slot_i;           // per CTA
+  double* slot_v;        // 2 per CTA (double-buffered by step parity)
+  int* slot_i;           // 2 per CTA
   int vcap;              // Householder vector staged in smem when m <= vcap
+  int kmax;              // largest separator of the launch (replicated permutation in smem)
+  long long* prof;       // optional per-phase clock accumulators (debug)
 };
 
 struct RepackArgs {
@@ -131,6 +133,7 @@ struct BigArgs {
   int ncell;
   const int* n;            // per big cell
   const int* b;
+  const int* rows;         // panel rows: n + b (+ n identity rows whose result is L^-T)
   double* const* P;        // panel base per big cell
   double* const* U;        // Schur output per big cell (b x b)
   double* Linv;            // 64 x 64 scratch per big cell
@@ -141,6 +144,20 @@ struct BigArgs {
   const int* w_j;
   int nwork;
   int k0;                  // current step's panel start
+};
+
+}  // namespace phif
+
+namespace phif {
+
+// Generic batched GEMM work: C = beta*C + alpha*op(A)*B, tile-parallel over 64-row tiles.
+struct GemmDesc {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, lda, ldb, ldc;
+  int transA;
+  double alpha, beta;
 };
 
 }  // namespace phif

@@ -9,6 +9,7 @@ namespace phif {
 
 struct ApplyCellArgs {
   int p;
+  const int* list;   // cells replayed by the one-CTA kernel (nullptr = all)
   const int* n;
   const int* b;
   const int* I;
@@ -58,11 +59,14 @@ void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cu
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s);
 void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces, int count, cudaStream_t s);
-int team_blocks_per_sm(int vcap);
+int team_blocks_per_sm(int vcap, int kmax);
 void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s);
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s);
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
 void launch_big_syrk(const BigArgs& a, cudaStream_t s);
+void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s);
+void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
+                 const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s);
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s);
 void launch_repack(const RepackArgs& a, cudaStream_t s);
 void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s);

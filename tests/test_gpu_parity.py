@@ -45,6 +45,9 @@ CASES = [
     ("c3-n128-1e-4", lambda: baseline_problem("c3", 0, 128)[:2], "phif", 1e-4, 1e-12),
     ("c4-n32", lambda: baseline_problem("c4", 0, 32)[:2], "phif", 1e-3, 1e-12),
     ("c5-n32", lambda: baseline_problem("c5", 0, 32)[:2], "phif", 1e-2, 1e-10),
+    # full-size 3D config: large separators (team CPQR) and big cells (tile-parallel path)
+    ("c4-full", lambda: baseline_problem("c4", 0)[:2], "phif", 1e-3, 1e-12),
+    ("c5-n64", lambda: baseline_problem("c5", 0, 64)[:2], "phif", 1e-2, 1e-10),
 ]
 
 
