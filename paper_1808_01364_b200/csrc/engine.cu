@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <sstream>
 
@@ -18,6 +19,10 @@ namespace phif {
 
 constexpr int BIG_N = 192;   // cells with |I| >= BIG_N take the tile-parallel path
 
+static std::chrono::steady_clock::time_point g_dbg_t0 = std::chrono::steady_clock::now();
+static double dbg_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g_dbg_t0).count();
+}
 static bool debug_on() {
   static int on = -1;
   if (on < 0) on = getenv("PHIF_DEBUG") ? 1 : 0;
@@ -26,7 +31,8 @@ static bool debug_on() {
 #define DBG(...)                                  \
   do {                                            \
     if (debug_on()) {                             \
-      fprintf(stderr, "[phif] " __VA_ARGS__);     \
+      fprintf(stderr, "[phif %9.2f] ", dbg_ms());  \
+      fprintf(stderr, __VA_ARGS__);               \
       fprintf(stderr, "\n");                      \
       fflush(stderr);                             \
     }                                             \
@@ -50,16 +56,59 @@ DBuf& DBuf::operator=(DBuf&& o) noexcept {
   return *this;
 }
 
+// Caching device allocator: blocks come from cudaMalloc once and are recycled by size class
+// (never returned to the driver). Safe because every engine buffer is used on one stream in
+// order, so a block released here is only handed out again to later work on that stream.
+namespace {
+struct DeviceCache {
+  std::multimap<size_t, void*> free_blocks;
+  size_t cached = 0;
+  static size_t round(size_t b) {
+    if (b <= (1u << 20)) return (b + 511) & ~size_t(511);
+    return (b + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+  }
+  void* get(size_t& b) {
+    b = round(b);
+    auto it = free_blocks.lower_bound(b);
+    if (it != free_blocks.end() && it->first <= b + b / 4) {
+      void* p = it->second;
+      b = it->first;
+      cached -= b;
+      free_blocks.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, b) != cudaSuccess) {
+      cudaGetLastError();
+      // release cached blocks and retry once
+      for (auto& kv : free_blocks) cudaFree(kv.second);
+      free_blocks.clear();
+      cached = 0;
+      CK(cudaMalloc(&p, b));
+    }
+    return p;
+  }
+  void put(void* p, size_t b) {
+    free_blocks.emplace(b, p);
+    cached += b;
+  }
+};
+DeviceCache& dcache() {
+  static DeviceCache* c = new DeviceCache();   // intentionally leaked: outlives static destructors
+  return *c;
+}
+}  // namespace
+
 void DBuf::alloc(size_t nbytes, cudaStream_t st, bool zero) {
   release();
   s = st;
   bytes = std::max<size_t>(nbytes, 8);
-  CK(cudaMallocAsync(&p, bytes, st));
+  p = dcache().get(bytes);
   if (zero) CK(cudaMemsetAsync(p, 0, bytes, st));
 }
 
 void DBuf::release() {
-  if (p) cudaFreeAsync(p, s);
+  if (p) dcache().put(p, bytes);
   p = nullptr;
   bytes = 0;
 }
@@ -285,6 +334,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
                                          cudaStream_t s, bool timing) {
   configure_kernels();
   keep_pool_memory();
+  g_dbg_t0 = std::chrono::steady_clock::now();
   auto F = std::make_unique<Factorization>();
   F->spec.init(dim, n, m);
   F->method = method;
@@ -363,19 +413,24 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     for (size_t b = 0; b < P.pat.bg.size(); ++b) L.by[0] += 8.0 * 2.0 * G.size(P.pat.bg[b]) * G.size(P.pat.bh[b]);
     // boundary reduction lists (x_B -= X^T y in fixed cell order)
     {
-      std::vector<std::pair<int, int>> dr(Bdofs.size());
-      for (size_t i = 0; i < Bdofs.size(); ++i) dr[i] = {Bdofs[i], (int)i};
-      std::sort(dr.begin(), dr.end());
-      std::vector<int> dof, rows;
+      // counting sort of wbuf rows by boundary DOF (rows of one DOF stay in cell order)
+      std::vector<int> cnt(sp.N + 1, 0);
+      for (int d : Bdofs) cnt[d + 1]++;
+      std::vector<int> dof;
       std::vector<int64_t> off;
-      for (size_t i = 0; i < dr.size(); ++i) {
-        if (i == 0 || dr[i].first != dr[i - 1].first) {
-          dof.push_back(dr[i].first);
-          off.push_back((int64_t)i);
+      int64_t acc2 = 0;
+      std::vector<int64_t> start(sp.N, 0);
+      for (int64_t d = 0; d < sp.N; ++d) {
+        start[d] = acc2;
+        if (cnt[d + 1]) {
+          dof.push_back((int)d);
+          off.push_back(acc2);
+          acc2 += cnt[d + 1];
         }
-        rows.push_back(dr[i].second);
       }
-      off.push_back((int64_t)dr.size());
+      off.push_back(acc2);
+      std::vector<int> rows(Bdofs.size());
+      for (size_t i = 0; i < Bdofs.size(); ++i) rows[start[Bdofs[i]]++] = (int)i;
       L.nbd = (int)dof.size();
       upload(L.bd_dof, dof, s);
       upload(L.bd_off, off, s);
@@ -438,8 +493,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     // ---------------- device structures ----------------
     DBG("level %d: rec=%lld", lev, (long long)rec);
     upload_structure(L, s);
+    DBG("level %d: structure uploaded", lev);
     L.pool.alloc(std::max<int64_t>(P.pool_doubles, 1) * sizeof(double), s, /*zero=*/true);
+    if (debug_on()) cudaStreamSynchronize(s);
+    DBG("level %d: pool allocated", lev);
     L.rec.alloc(std::max<int64_t>(rec, 1) * sizeof(double), s);
+    if (debug_on()) cudaStreamSynchronize(s);
+    DBG("level %d: records allocated", lev);
     F->rec_bytes += rec * (int64_t)sizeof(double);
     LevelDev dv = L.dev();
     if (timing) CK(cudaEventRecord(ev[0], s));
@@ -480,6 +540,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       prev->pool.release();
     }
     if (timing) CK(cudaEventRecord(ev[1], s));
+    DBG("level %d: ingest/repack done", lev);
     // ---------------- stage 1: cell elimination ----------------
     upload(L.c_interior, P.interior, s);
     upload(L.c_nbr_off, P.cell_nbr_off, s);
@@ -524,6 +585,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.h_cwork = cwork;
     BigPlan bp;
     if (!big_cells.empty()) bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
+    DBG("level %d: big plan built (%zu work items)", lev, bp.steps_k0.empty() ? (size_t)0 : (size_t)bp.syrk_off);
     if (timing) CK(cudaEventRecord(ev[2], s));
     if (!small_cells.empty()) {
       ca.list = L.d_small_cells.as<int>();
@@ -536,6 +598,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     if (timing) CK(cudaEventRecord(ev[3], s));
     check_status(*F, lev, P.root ? ST_ROOT : ST_ELIMINATE);
+    DBG("level %d: cells done", lev);
     DBuf tb, to, cc, cr, ccol;
     upload(tb, P.tgt_blk, s);
     upload(to, P.tgt_off, s);
@@ -588,6 +651,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     DBG("level %d: precondition r=%d scale=%d", lev, pa.r, pa.nscale);
     launch_prec_factor(dv, pa, F->status.as<DevStatus>(), s);
     check_status(*F, lev, ST_PRECONDITION);
+    DBG("level %d: precondition factor done", lev);
     launch_prec_scale(dv, pa, s);
     if (timing) CK(cudaEventRecord(ev[7], s));
     // ---------------- stage 3: skeletonization ----------------
@@ -720,6 +784,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     launch_skel_update(dv, ka, F->status.as<DevStatus>(), s);
     if (timing) CK(cudaEventRecord(ev[10], s));
     check_status(*F, lev, ST_SKELETONIZE);
+    DBG("level %d: skeleton update done", lev);
     // ranks and redundant flags back to the host (planning of the next level)
     L.h_rank.resize(nsk);
     std::vector<int> h_rows(nsk);
@@ -773,6 +838,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     upload(L.s_R_off, R_off, s);
     upload(L.s_awork_off, awork, s);
     plan_ms += ms_since(tp);
+    DBG("level %d: next-level inputs ready", lev);
     if (timing) {
       CK(cudaEventSynchronize(ev[10]));
       float a;

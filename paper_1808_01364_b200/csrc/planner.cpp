@@ -6,6 +6,7 @@
 #include <numeric>
 #include <sstream>
 #include <stdexcept>
+#include <tuple>
 
 namespace phif {
 
@@ -152,38 +153,83 @@ Groups classify_set(const Spec& s, int level, const std::vector<int>& active) {
 }
 
 Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_t>& alive) {
+  // Every surviving DOF of an old group lands in the same new group (the old group's
+  // on-line axes stay on-line iff their line index is even; free coordinates stay inside
+  // the same cell), so the new grouping is a bucket sort of old groups by their new key
+  // followed by a per-group merge of survivors in ascending DOF order (hierarchy.py:145).
   Groups g;
   g.level = prev.level + 1;
-  struct Item {
-    int64_t key;
-    int dof, src, pos;
-  };
-  std::vector<Item> items;
-  items.reserve(prev.mem.size());
-  for (int pg = 0; pg < prev.G; ++pg)
+  const int per = s.n / (s.m << g.level);
+  int64_t nkeys = 1;
+  for (int d = 0; d < s.dim; ++d) nkeys *= per;
+  nkeys <<= s.dim;
+  std::vector<int64_t> okey(prev.G, -1);
+  std::vector<int> osurv(prev.G, 0);
+#pragma omp parallel for schedule(static)
+  for (int pg = 0; pg < prev.G; ++pg) {
+    int cnt = 0;
+    int64_t first = -1;
     for (int64_t p = prev.off[pg]; p < prev.off[pg + 1]; ++p)
       if (alive[p]) {
-        int q[3], b;
-        const int dof = prev.mem[p];
-        items.push_back({key_of(s, g.level, dof, q, b), dof, pg, (int)(p - prev.off[pg])});
+        if (cnt == 0) first = p;
+        ++cnt;
       }
-  std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
-    return a.key != b.key ? a.key < b.key : a.dof < b.dof;
-  });
-  std::vector<int64_t> gkeys;
-  g.mem.resize(items.size());
-  g.src_group.resize(items.size());
-  g.src_pos.resize(items.size());
-  for (size_t i = 0; i < items.size(); ++i) {
-    if (i == 0 || items[i].key != items[i - 1].key) {
-      gkeys.push_back(items[i].key);
-      g.off.push_back((int64_t)i);
+    osurv[pg] = cnt;
+    if (cnt) {
+      int q[3], b;
+      okey[pg] = key_of(s, g.level, prev.mem[first], q, b);
     }
-    g.mem[i] = items[i].dof;
-    g.src_group[i] = items[i].src;
-    g.src_pos[i] = items[i].pos;
   }
-  g.off.push_back((int64_t)items.size());
+  // bucket old groups by new key (stable: ascending old group index)
+  std::vector<int64_t> kcnt(nkeys + 1, 0);
+  for (int pg = 0; pg < prev.G; ++pg)
+    if (okey[pg] >= 0) kcnt[okey[pg] + 1]++;
+  for (int64_t k = 0; k < nkeys; ++k) kcnt[k + 1] += kcnt[k];
+  std::vector<int> order(kcnt[nkeys]);
+  {
+    std::vector<int64_t> fill(kcnt.begin(), kcnt.end() - 1);
+    for (int pg = 0; pg < prev.G; ++pg)
+      if (okey[pg] >= 0) order[fill[okey[pg]]++] = pg;
+  }
+  std::vector<int64_t> gkeys;
+  std::vector<int64_t> gsrc_off;   // new group -> range in `order`
+  int64_t total = 0;
+  std::vector<int64_t> moff;
+  for (int64_t k = 0; k < nkeys; ++k)
+    if (kcnt[k + 1] > kcnt[k]) {
+      gkeys.push_back(k);
+      gsrc_off.push_back(kcnt[k]);
+      moff.push_back(total);
+      for (int64_t q = kcnt[k]; q < kcnt[k + 1]; ++q) total += osurv[order[q]];
+    }
+  gsrc_off.push_back(kcnt[nkeys]);
+  moff.push_back(total);
+  const int G = (int)gkeys.size();
+  g.off = moff;
+  g.mem.resize(total);
+  g.src_group.resize(total);
+  g.src_pos.resize(total);
+#pragma omp parallel
+  {
+    std::vector<std::tuple<int, int, int>> seg;
+#pragma omp for schedule(dynamic, 64)
+    for (int G0 = 0; G0 < G; ++G0) {
+      seg.clear();
+      for (int64_t q = gsrc_off[G0]; q < gsrc_off[G0 + 1]; ++q) {
+        const int pg = order[q];
+        for (int64_t p = prev.off[pg]; p < prev.off[pg + 1]; ++p)
+          if (alive[p]) seg.emplace_back(prev.mem[p], pg, (int)(p - prev.off[pg]));
+      }
+      std::sort(seg.begin(), seg.end());
+      int64_t o = g.off[G0];
+      for (auto& t : seg) {
+        g.mem[o] = std::get<0>(t);
+        g.src_group[o] = std::get<1>(t);
+        g.src_pos[o] = std::get<2>(t);
+        ++o;
+      }
+    }
+  }
   finalize_groups(s, g, {}, gkeys);
   return g;
 }
@@ -291,14 +337,78 @@ static void build_adjacency(int G, const std::vector<std::pair<int, int>>& pairs
   }
 }
 
+// per-group sorted, de-duplicated "upper" neighbour lists (h >= g) from unsorted pairs
+static void upper_lists(int G, const std::vector<std::pair<int, int>>& pairs, std::vector<int64_t>& off,
+                        std::vector<int>& nbr) {
+  off.assign(G + 1, 0);
+  for (const auto& pr : pairs) off[pr.first + 1]++;
+  for (int i = 0; i < G; ++i) off[i + 1] += off[i];
+  nbr.assign(off[G], 0);
+  {
+    std::vector<int64_t> fill(off.begin(), off.end() - 1);
+    for (const auto& pr : pairs) nbr[fill[pr.first]++] = pr.second;
+  }
+  std::vector<int64_t> keep(G + 1, 0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int gi = 0; gi < G; ++gi) {
+    int* b = nbr.data() + off[gi];
+    int* e = nbr.data() + off[gi + 1];
+    std::sort(b, e);
+    keep[gi + 1] = std::unique(b, e) - b;
+  }
+  for (int i = 0; i < G; ++i) keep[i + 1] += keep[i];
+  std::vector<int> out(keep[G]);
+#pragma omp parallel for schedule(static)
+  for (int gi = 0; gi < G; ++gi)
+    std::copy(nbr.begin() + off[gi], nbr.begin() + off[gi] + (keep[gi + 1] - keep[gi]), out.begin() + keep[gi]);
+  off.swap(keep);
+  nbr.swap(out);
+}
+
+// symmetric adjacency (rows sorted by neighbour) from upper lists; block ids in (g, h) order
+static void adjacency_from_upper(int G, const std::vector<int64_t>& uoff, const std::vector<int>& unbr,
+                                 Pattern& pat) {
+  const int64_t nb = uoff[G];
+  pat.bg.resize(nb);
+  pat.bh.resize(nb);
+  std::vector<int64_t> ndown(G + 1, 0);
+  for (int gi = 0; gi < G; ++gi)
+    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) {
+      pat.bg[q] = gi;
+      pat.bh[q] = unbr[q];
+      if (unbr[q] != gi) ndown[unbr[q] + 1]++;
+    }
+  pat.adj_off.assign(G + 1, 0);
+  for (int gi = 0; gi < G; ++gi) pat.adj_off[gi + 1] = pat.adj_off[gi] + ndown[gi + 1] + (uoff[gi + 1] - uoff[gi]);
+  pat.adj_nbr.assign(pat.adj_off[G], 0);
+  pat.adj_blk.assign(pat.adj_off[G], 0);
+  std::vector<int64_t> fill(pat.adj_off.begin(), pat.adj_off.end() - 1);
+  // lower neighbours first, in increasing order (outer loop over ascending g)
+  for (int gi = 0; gi < G; ++gi)
+    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) {
+      const int h = unbr[q];
+      if (h == gi) continue;
+      pat.adj_nbr[fill[h]] = gi;
+      pat.adj_blk[fill[h]++] = (int)q;
+    }
+#pragma omp parallel for schedule(static)
+  for (int gi = 0; gi < G; ++gi) {
+    int64_t f = fill[gi];
+    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) {
+      pat.adj_nbr[f] = unbr[q];
+      pat.adj_blk[f++] = (int)q;
+    }
+  }
+}
+
 void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> pairs) {
   Groups& g = lp.grp;
   lp.level = g.level;
   lp.root = (g.level == s.L);
   for (int i = 0; i < g.G; ++i) pairs.emplace_back(i, i);
-  sort_unique(pairs);
-  Pattern in;
-  build_adjacency(g.G, pairs, in);
+  std::vector<int64_t> uoff;
+  std::vector<int> unbr;
+  upper_lists(g.G, pairs, uoff, unbr);
   lp.interior.clear();
   lp.precond.clear();
   lp.skeleton.clear();
@@ -310,80 +420,113 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       if (g.kind[i] == 1) lp.skeleton.push_back(i);
     }
   }
-  // elimination fill among each cell's boundary groups
+  // an interior group is the first group of its cell closure: every coupling of it is an upper entry
+  for (int gi = 0; gi < g.G; ++gi)
+    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q)
+      if (unbr[q] != gi && g.kind[unbr[q]] == 0)
+        throw std::runtime_error(g.kind[gi] == 0 ? "planner: two interior groups coupled"
+                                                 : "planner: interior group is not first in its closure");
+  // elimination fill among each cell's boundary groups (SPEC.md:251)
+  pairs.clear();
+  for (int gi = 0; gi < g.G; ++gi)
+    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) pairs.emplace_back(gi, unbr[q]);
   for (int I : lp.interior) {
-    std::vector<int> nb;
-    for (int64_t p = in.adj_off[I]; p < in.adj_off[I + 1]; ++p)
-      if (in.adj_nbr[p] != I) {
-        if (g.kind[in.adj_nbr[p]] == 0) throw std::runtime_error("planner: two interior groups coupled");
-        nb.push_back(in.adj_nbr[p]);
-      }
-    for (size_t a = 0; a < nb.size(); ++a)
-      for (size_t b = a; b < nb.size(); ++b) pairs.emplace_back(nb[a], nb[b]);
+    const int64_t a0 = uoff[I], a1 = uoff[I + 1];
+    for (int64_t a = a0; a < a1; ++a) {
+      if (unbr[a] == I) continue;
+      for (int64_t b = a; b < a1; ++b) pairs.emplace_back(unbr[a], unbr[b]);
+    }
   }
-  sort_unique(pairs);
-  build_adjacency(g.G, pairs, lp.pat);
+  upper_lists(g.G, pairs, uoff, unbr);
+  adjacency_from_upper(g.G, uoff, unbr, lp.pat);
   const Pattern& pat = lp.pat;
+  const int64_t nblocks = (int64_t)pat.bg.size();
   // pool
-  lp.boff.resize(pat.bg.size());
+  lp.boff.resize(nblocks);
   int64_t acc = 0;
-  for (size_t b = 0; b < pat.bg.size(); ++b) {
+  for (int64_t b = 0; b < nblocks; ++b) {
     lp.boff[b] = acc;
     acc += (int64_t)g.size(pat.bg[b]) * g.size(pat.bh[b]);
   }
   lp.pool_doubles = acc;
-  // cells
+  // cells: boundary = neighbour groups of I (all after I); Schur targets = pairs of them
   const int p = (int)lp.interior.size();
-  lp.cell_nbr_off.assign(1, 0);
-  lp.cell_nbr.clear();
-  lp.cell_nbr_blk.clear();
-  lp.cell_nbr_col.clear();
+  lp.cell_nbr_off.assign(p + 1, 0);
   lp.cell_n.assign(p, 0);
   lp.cell_b.assign(p, 0);
-  struct Con {
-    int tgt, cell, row, col;
-  };
-  std::vector<Con> cons;
   for (int t = 0; t < p; ++t) {
     const int I = lp.interior[t];
+    lp.cell_nbr_off[t + 1] = lp.cell_nbr_off[t] + (uoff[I + 1] - uoff[I] - 1);
+  }
+  const int64_t ncn = lp.cell_nbr_off[p];
+  lp.cell_nbr.assign(ncn, 0);
+  lp.cell_nbr_blk.assign(ncn, 0);
+  lp.cell_nbr_col.assign(ncn, 0);
+  std::vector<int64_t> ccount(p + 1, 0);
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < p; ++t) {
+    const int I = lp.interior[t];
+    int64_t o = lp.cell_nbr_off[t];
     int bcols = 0;
-    const int64_t first = (int64_t)lp.cell_nbr.size();
-    for (int64_t q = pat.adj_off[I]; q < pat.adj_off[I + 1]; ++q) {
-      const int h = pat.adj_nbr[q];
+    for (int64_t q = uoff[I]; q < uoff[I + 1]; ++q) {
+      const int h = unbr[q];
       if (h == I) continue;
-      if (h < I) throw std::runtime_error("planner: interior group is not first in its closure");
-      lp.cell_nbr.push_back(h);
-      lp.cell_nbr_blk.push_back(pat.adj_blk[q]);
-      lp.cell_nbr_col.push_back(bcols);
+      lp.cell_nbr[o] = h;
+      lp.cell_nbr_blk[o] = (int)q;
+      lp.cell_nbr_col[o] = bcols;
       bcols += g.size(h);
+      ++o;
     }
-    lp.cell_nbr_off.push_back((int64_t)lp.cell_nbr.size());
     lp.cell_n[t] = g.size(I);
     lp.cell_b[t] = bcols;
-    const int64_t last = (int64_t)lp.cell_nbr.size();
-    for (int64_t a = first; a < last; ++a)
-      for (int64_t b = a; b < last; ++b) {
-        const int blk = pat.find(lp.cell_nbr[a], lp.cell_nbr[b]);
-        if (blk < 0) throw std::runtime_error("planner: missing fill block");
-        cons.push_back({blk, t, lp.cell_nbr_col[a], lp.cell_nbr_col[b]});
-      }
+    const int64_t w = lp.cell_nbr_off[t + 1] - lp.cell_nbr_off[t];
+    ccount[t + 1] = w * (w + 1) / 2;
   }
-  std::stable_sort(cons.begin(), cons.end(), [](const Con& a, const Con& b) { return a.tgt < b.tgt; });
+  for (int t = 0; t < p; ++t) ccount[t + 1] += ccount[t];
+  const int64_t ncons = ccount[p];
+  std::vector<int> ctgt(ncons), ccell(ncons), crow(ncons), ccol(ncons);
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < p; ++t) {
+    int64_t o = ccount[t];
+    const int64_t first = lp.cell_nbr_off[t], last = lp.cell_nbr_off[t + 1];
+    for (int64_t a = first; a < last; ++a) {
+      const int ha = lp.cell_nbr[a];
+      const int* rb = unbr.data() + uoff[ha];
+      const int* re = unbr.data() + uoff[ha + 1];
+      for (int64_t b = a; b < last; ++b) {
+        const int* it = std::lower_bound(rb, re, lp.cell_nbr[b]);
+        ctgt[o] = (int)(it - unbr.data());   // block id = position in the upper lists
+        ccell[o] = t;
+        crow[o] = lp.cell_nbr_col[a];
+        ccol[o] = lp.cell_nbr_col[b];
+        ++o;
+      }
+    }
+  }
+  // group contributions by target block (counting sort; stable in cell order)
+  std::vector<int64_t> tcnt(nblocks + 1, 0);
+  for (int64_t i = 0; i < ncons; ++i) tcnt[ctgt[i] + 1]++;
+  for (int64_t b = 0; b < nblocks; ++b) tcnt[b + 1] += tcnt[b];
+  lp.con_cell.resize(ncons);
+  lp.con_row.resize(ncons);
+  lp.con_col.resize(ncons);
+  {
+    std::vector<int64_t> fill(tcnt.begin(), tcnt.end() - 1);
+    for (int64_t i = 0; i < ncons; ++i) {
+      const int64_t o = fill[ctgt[i]]++;
+      lp.con_cell[o] = ccell[i];
+      lp.con_row[o] = crow[i];
+      lp.con_col[o] = ccol[i];
+    }
+  }
   lp.tgt_blk.clear();
   lp.tgt_off.assign(1, 0);
-  lp.con_cell.resize(cons.size());
-  lp.con_row.resize(cons.size());
-  lp.con_col.resize(cons.size());
-  for (size_t i = 0; i < cons.size(); ++i) {
-    if (i == 0 || cons[i].tgt != cons[i - 1].tgt) {
-      if (i) lp.tgt_off.push_back((int64_t)i);
-      lp.tgt_blk.push_back(cons[i].tgt);
+  for (int64_t b = 0; b < nblocks; ++b)
+    if (tcnt[b + 1] > tcnt[b]) {
+      lp.tgt_blk.push_back((int)b);
+      lp.tgt_off.push_back(tcnt[b + 1]);
     }
-    lp.con_cell[i] = cons[i].cell;
-    lp.con_row[i] = cons[i].row;
-    lp.con_col[i] = cons[i].col;
-  }
-  if (!cons.empty()) lp.tgt_off.push_back((int64_t)cons.size());
+  if (lp.tgt_blk.empty()) lp.tgt_off.assign(1, 0);
   // block Jacobi scaling targets
   lp.scale_blk.clear();
   for (size_t b = 0; b < pat.bg.size(); ++b)

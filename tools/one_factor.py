@@ -7,5 +7,7 @@ name, eps = sys.argv[1], float(sys.argv[2])
 n = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] != "-" else None
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 spec, A, _ = baseline_problem(name, 0, n)
+F = None
 for _ in range(reps):
+    F = None
     t = time.time(); F = gf.factorize(A, spec, eps, CONFIGS[name].method); print("factorize %.1f ms SL %d" % ((time.time() - t) * 1e3, F.SL), flush=True)
