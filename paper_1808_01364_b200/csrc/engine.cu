@@ -308,8 +308,8 @@ static long long* team_prof_buffer() {
       for (int i = 0; i < 16; ++i) buf[i] = 0;
       atexit([] {
         cudaDeviceSynchronize();
-        fprintf(stderr, "[phif] team phases (Mcycles): argmax %.1f sync %.1f reflector %.1f own %.1f pass1 %.1f rowi %.1f pass2 %.1f recompute %.1f steps %lld\n",
-                buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6, buf[7] / 1e6, buf[8]);
+        fprintf(stderr, "[phif] team phases CTA0 (Mcycles): argmax+publish %.1f sync %.1f reflector %.1f pass1(smem) %.1f pass1(L2) %.1f pass2(smem) %.1f pass2(L2) %.1f | steps %lld | QR %.1f [panel %.1f update %.1f syncs %.1f] CPQR %.1f finish %.1f\n",
+                buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6, buf[8], buf[11] / 1e6, buf[14] / 1e6, buf[7] / 1e6, buf[15] / 1e6, buf[12] / 1e6, buf[13] / 1e6);
       });
     }
   }
@@ -696,7 +696,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       std::vector<int> small_list, large_list, team_face, team_off_all;
       std::vector<int64_t> small_off(P.nwaves + 1, 0), large_off(P.nwaves + 1, 0), toff_off(P.nwaves + 1, 0),
           slot_off(P.nwaves + 1, 0);
-      std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0), wave_kmax(P.nwaves, 0);
+      std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0), wave_kmax(P.nwaves, 0), wave_mmax(P.nwaves, 0);
       for (int w = 0; w < P.nwaves; ++w) {
         std::vector<int> large;
         for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
@@ -710,10 +710,11 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         double wsum = 0.0;
         for (int t : large) {
           kmax = std::max(kmax, G.size(P.skeleton[t]));
+          wave_mmax[w] = std::max<int>(wave_mmax[w], (int)rows_bound[t]);
           vcap = std::max<int>(vcap, (int)std::min<int64_t>(rows_bound[t], 16384));
           wsum += (double)rows_bound[t] * G.size(P.skeleton[t]) * G.size(P.skeleton[t]);
         }
-        int budget = large.empty() ? 0 : team_blocks_per_sm(vcap, kmax) * num_sms;
+        int budget = large.empty() ? 0 : team_blocks_per_sm(vcap, kmax, team_colcap(vcap, kmax)) * num_sms;
         budget = std::max<int>(budget, (int)large.size());
         toff_off[w] = (int64_t)team_off_all.size();
         team_off_all.push_back(0);
@@ -725,6 +726,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           want[q] = std::min(128, std::max(1, (k + 15) / 16));
           want_sum += want[q];
         }
+        std::vector<int> Pv(large.size());
         int tot = 0;
         for (size_t q = 0; q < large.size(); ++q) {
           const int t = large[q];
@@ -734,13 +736,22 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
             const double wf = (double)rows_bound[t] * k * k;
             Pf = std::max(1, std::min(want[q], (int)(budget * wf / wsum)));
           }
-          Pf = std::max(Pf, (k + 511) / 512);
-          tot += Pf;
-          team_face.push_back(t);
-          team_off_all.push_back(tot);
-          large_list.push_back(t);
+          Pv[q] = std::max(Pf, (k + 511) / 512);
+          tot += Pv[q];
         }
-        if (tot > budget) throw std::runtime_error("team CPQR: wave does not fit the co-resident budget");
+        while (tot > budget) {   // trim the largest teams until the wave is co-resident
+          size_t qm = std::max_element(Pv.begin(), Pv.end()) - Pv.begin();
+          if (Pv[qm] <= (G.size(P.skeleton[large[qm]]) + 511) / 512) throw std::runtime_error("team CPQR: wave too large");
+          --Pv[qm];
+          --tot;
+        }
+        tot = 0;
+        for (size_t q = 0; q < large.size(); ++q) {
+          tot += Pv[q];
+          team_face.push_back(large[q]);
+          team_off_all.push_back(tot);
+          large_list.push_back(large[q]);
+        }
         large_off[w + 1] = (int64_t)large_list.size();
         L.team_P_mean += tot;
         slot_off[w + 1] = slot_off[w] + tot;
@@ -756,6 +767,12 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       upload(d_toff, team_off_all, s);
       hdr.alloc(std::max<size_t>(large_list.size(), 1) * sizeof(TeamHdr), s, true);
       sv.alloc(std::max<int64_t>(2 * slot_off[P.nwaves], 1) * sizeof(double), s);
+      int64_t cand_ld = 1;
+      for (int w = 0; w < P.nwaves; ++w) cand_ld = std::max<int64_t>(cand_ld, wave_mmax[w]);
+      int64_t max_blocks = 1;
+      for (int w = 0; w < P.nwaves; ++w) max_blocks = std::max<int64_t>(max_blocks, wave_blocks[w]);
+      DBuf cand;
+      cand.alloc((size_t)2 * max_blocks * cand_ld * sizeof(double), s);
       si.alloc(std::max<int64_t>(2 * slot_off[P.nwaves], 1) * sizeof(int), s);
       for (int w = 0; w < P.nwaves; ++w) {
         ka.order = d_small.as<int>() + small_off[w];
@@ -772,6 +789,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ta.slot_i = si.as<int>() + 2 * slot_off[w];
           ta.vcap = wave_vcap[w];
           ta.kmax = wave_kmax[w];
+          ta.cand = cand.as<double>();
+          ta.cand_ld = cand_ld;
+          ta.colcap = team_colcap(wave_vcap[w], wave_kmax[w]);
           ta.prof = team_prof_buffer();
           launch_skel_team(dv, ka, ta, wave_blocks[w], s);
         }

@@ -441,24 +441,29 @@ __device__ __forceinline__ void team_sync(TeamHdr* h, int P) {
 }
 
 constexpr int TCH = 16;      // owned columns updated together per pass
+
+__device__ __forceinline__ int nloc_all(int k, int c, int P) { return c < k ? (k - c + P - 1) / P : 0; }
 constexpr int TOWN = 512;    // max owned columns per CTA (smem norms)
 
-// Team CPQR without data movement: the physical column j is owned by CTA j % P
-// for the whole factorization; LAPACK's column interchanges are replayed on a
-// replicated logical permutation (inv: logical -> physical, pos: physical ->
-// logical) so that pivot ties break on the same logical index as idamax.
-// Every CTA forms the Householder reflector of the pivot column itself, so a
-// pivot step needs a single team barrier (after the local argmax); the owner of
-// the pivot column writes [beta; v] back at the start of the next step. The
-// partial norms of owned columns live in the owner's shared memory.
+// Team CPQR (dgeqp3/dlaqp2 semantics) of one large separator by a team of P co-resident CTAs.
+//  * Column j is owned by CTA j % P; LAPACK's column interchanges are replayed on a replicated
+//    logical permutation (inv: logical -> physical, pos: physical -> logical), so pivot ties
+//    break on the same logical index as idamax and no data moves.
+//  * The first `ns` owned columns of a CTA live in its shared memory (master copy, no per-step
+//    L2 traffic); the rest are streamed from L2. Each CTA publishes its local pivot candidate
+//    to a global staging column before the (single) team barrier of a step, so every CTA can
+//    form the winning Householder reflector right after it.
+//  * Only R's diagonal and strictly-upper part are kept (Q is never needed); the loop stops
+//    once the largest remaining partial norm is below the rank cut (see cta_cpqr).
 __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, TeamArgs ta) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
   double* sdot = smem + GEMM_OFF;               // [nw][TCH] partial dots, then [TCH] products
   double* vs = smem + SMEM_DOUBLES;             // reflector (rows > i), vcap doubles
   __shared__ double ovn1[TOWN], ovn2[TOWN];
-  __shared__ int s_rec[TCH], s_nrec;
+  __shared__ int s_rec[TCH], s_nrec, s_nact, s_own[TOWN];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  const long long t_kernel0 = clock64();
   int f = 0;
   while (f + 1 < ta.nface && ta.team_off[f + 1] <= (int)blockIdx.x) ++f;
   const int c = blockIdx.x - ta.team_off[f];
@@ -466,6 +471,7 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
   TeamHdr* hdr = ta.hdr + f;
   double* slot_v = ta.slot_v + 2 * ta.team_off[f];
   int* slot_i = ta.slot_i + 2 * ta.team_off[f];
+  double* cand_base = ta.cand + (int64_t)2 * ta.team_off[f] * ta.cand_ld;   // 2P staging columns
   const int s = ta.face[f];
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
@@ -478,35 +484,240 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
   int* flag = iw + 2 * k;
   int* inv = reinterpret_cast<int*>(vs + ta.vcap);   // k ints
   int* pos = inv + k;                                // k ints
-  const int m = __ldcg(sk.rows + s);
-  if (m == 0) {
+  double* colbuf = vs + ta.vcap + k + 1;             // smem-resident owned columns (ld m)
+  const int m0 = __ldcg(sk.rows + s);
+  if (m0 == 0) {
     if (c == 0) skel_all_redundant(lv, sk, s);
     return;
   }
-  const int nloc = c < k ? (k - c + P - 1) / P : 0;   // owned columns j = c + P*t
+  // ---- row reduction: blocked Householder QR W = Q [R0; 0] (m0 > k) -----------------------
+  // CPQR pivots depend only on A^T A, so the CPQR of R0 selects the same columns as the CPQR
+  // of A (up to rounding) while every later step touches k instead of m0 rows. Panels of nbq
+  // columns are factored by one CTA in shared memory; the compact-WY update of the trailing
+  // columns is done by their owners (two team barriers per panel).
+  int m = m0;
+  const long long t_qr0 = clock64();
+  if (m0 > k) {
+    const int nbq = max(1, min(8, ta.colcap / m0));
+    double* qT = cand_base;            // team scratch: T (8 x 8) of the current panel
+    for (int j0 = 0, pi = 0; j0 < k; j0 += nbq, ++pi) {
+      const int jb = min(nbq, k - j0);
+      const int ldp = m0 - j0;
+      double* Pn = colbuf;             // panel (jb x ldp, column-major) / staged V for the update
+      const bool qprof = ta.prof && blockIdx.x == 0 && tid == 0;
+      long long tq0 = qprof ? clock64() : 0;
+      if (c == pi % P) {
+        for (int64_t e = tid; e < (int64_t)jb * ldp; e += NT) {
+          const int jj = (int)(e / ldp), rr = (int)(e % ldp);
+          Pn[e] = __ldcg(W + (int64_t)(j0 + jj) * ldw + j0 + rr);
+        }
+        __syncthreads();
+        __shared__ double s_tau[8];
+        for (int jj = 0; jj < jb; ++jj) {
+          double* col = Pn + (int64_t)jj * ldp;
+          double part = 0.0;
+          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) part += col[rr] * col[rr];
+          const double xnorm = sqrt(cta_sum(part, sred));
+          const double alpha = col[jj];
+          double tau = 0.0, beta = alpha, scal = 1.0;
+          if (xnorm != 0.0) {
+            beta = -copysign(hypot(alpha, xnorm), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+          }
+          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) col[rr] *= scal;
+          __syncthreads();
+          if (tid == 0) {
+            col[jj] = beta;
+            s_tau[jj] = tau;
+          }
+          // apply H_jj to the remaining panel columns: thread row strips, CTA-reduced dots
+          __shared__ double s_pd[8][8];
+          double acc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) {
+            const double vr = col[rr];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (jj + 1 + u < jb) acc[u] += vr * Pn[(int64_t)(jj + 1 + u) * ldp + rr];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double t2 = warp_sum(acc[u]);
+            if (lane == 0) s_pd[warp][u] = t2;
+          }
+          __syncthreads();
+          __shared__ double s_tw[8];
+          if (tid < 8 && jj + 1 + tid < jb) {
+            double a = Pn[(int64_t)(jj + 1 + tid) * ldp + jj];
+            for (int q2 = 0; q2 < nw; ++q2) a += s_pd[q2][tid];
+            const double tw = tau * a;
+            Pn[(int64_t)(jj + 1 + tid) * ldp + jj] -= tw;
+            s_tw[tid] = tw;
+          }
+          __syncthreads();
+          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) {
+            const double vr = col[rr];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (jj + 1 + u < jb) Pn[(int64_t)(jj + 1 + u) * ldp + rr] -= s_tw[u] * vr;
+          }
+          __syncthreads();
+        }
+        // compact WY factor T (upper triangular): H_1 ... H_jb = I - V T V^T
+        __shared__ double s_G[8][8];
+        for (int ab = warp; ab < jb * jb; ab += nw) {
+          const int a = ab / jb, b = ab % jb;
+          double x = 0.0;
+          if (a < b) {
+            for (int rr = b + lane; rr < ldp; rr += 32)
+              x += (rr == a ? 1.0 : Pn[(int64_t)a * ldp + rr]) * (rr == b ? 1.0 : Pn[(int64_t)b * ldp + rr]);
+            x = warp_sum(x);
+          }
+          if (lane == 0) s_G[a][b] = x;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double T[8][8];
+          for (int i2 = 0; i2 < jb; ++i2) {
+            for (int a = 0; a < i2; ++a) {
+              double x = 0.0;
+              for (int b = a; b < i2; ++b) x += T[a][b] * s_G[b][i2];
+              T[a][i2] = -s_tau[i2] * x;
+            }
+            T[i2][i2] = s_tau[i2];
+            for (int a = i2 + 1; a < jb; ++a) T[a][i2] = 0.0;
+          }
+          for (int a = 0; a < jb; ++a)
+            for (int b = 0; b < jb; ++b) __stcg(qT + a * 8 + b, T[a][b]);
+        }
+        for (int64_t e = tid; e < (int64_t)jb * ldp; e += NT) {
+          const int jj = (int)(e / ldp), rr = (int)(e % ldp);
+          __stcg(W + (int64_t)(j0 + jj) * ldw + j0 + rr, Pn[e]);
+        }
+      }
+      if (qprof) { const long long t1 = clock64(); ta.prof[14] += t1 - tq0; tq0 = t1; }
+      team_sync(hdr, P);
+      if (qprof) { const long long t1 = clock64(); ta.prof[15] += t1 - tq0; tq0 = t1; }
+      // trailing update of owned columns j >= j0 + jb: a <- a - V (T^T (V^T a))
+      const int jstart = j0 + jb;
+      const int tfirst = jstart <= c ? 0 : (jstart - c + P - 1) / P;
+      if (tfirst < nloc_all(k, c, P)) {
+        for (int64_t e = tid; e < (int64_t)jb * ldp; e += NT) {
+          const int jj = (int)(e / ldp), rr = (int)(e % ldp);
+          Pn[e] = rr < jj ? 0.0 : (rr == jj ? 1.0 : __ldcg(W + (int64_t)(j0 + jj) * ldw + j0 + rr));
+        }
+        __shared__ double s_T[8][8];
+        if (tid < 64) s_T[tid / 8][tid % 8] = (tid / 8 < jb && tid % 8 < jb) ? __ldcg(qT + tid) : 0.0;
+        __syncthreads();
+        // owned trailing columns two at a time: thread row strips, CTA-reduced V^T a
+        const int nl = nloc_all(k, c, P);
+        __shared__ double s_w[8][2][8];
+        __shared__ double s_z[2][8];
+        for (int t0 = tfirst; t0 < nl; t0 += 2) {
+          const int nt = min(2, nl - t0);
+          double* cj0 = W + (int64_t)(c + P * t0) * ldw + j0;
+          double* cj1 = W + (int64_t)(c + P * (t0 + nt - 1)) * ldw + j0;
+          double w0[8], w1[8];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) w0[a] = w1[a] = 0.0;
+          for (int rr = tid; rr < ldp; rr += NT) {
+            const double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+              if (a < jb) {
+                const double va = Pn[(int64_t)a * ldp + rr];
+                w0[a] += va * x0;
+                w1[a] += va * x1;
+              }
+          }
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            const double y0 = warp_sum(w0[a]), y1 = warp_sum(w1[a]);
+            if (lane == 0) {
+              s_w[warp][0][a] = y0;
+              s_w[warp][1][a] = y1;
+            }
+          }
+          __syncthreads();
+          if (tid < 16) {
+            const int q2 = tid >> 3, b = tid & 7;
+            double x = 0.0;
+            if (b < jb)
+              for (int a = 0; a <= b; ++a) {
+                double wa = 0.0;
+                for (int ww = 0; ww < nw; ++ww) wa += s_w[ww][q2][a];
+                x += s_T[a][b] * wa;
+              }
+            s_z[q2][b] = x;
+          }
+          __syncthreads();
+          for (int rr = tid; rr < ldp; rr += NT) {
+            double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              if (b < jb) {
+                const double vb = Pn[(int64_t)b * ldp + rr];
+                x0 -= vb * s_z[0][b];
+                x1 -= vb * s_z[1][b];
+              }
+            __stcg(cj0 + rr, x0);
+            if (nt == 2) __stcg(cj1 + rr, x1);
+          }
+          __syncthreads();
+        }
+      }
+      if (qprof) { const long long t1 = clock64(); ta.prof[7] += t1 - tq0; tq0 = t1; }
+      team_sync(hdr, P);
+      if (qprof) { const long long t1 = clock64(); ta.prof[15] += t1 - tq0; tq0 = t1; }
+    }
+    // R0 = rows 0..k-1 of W: clear the reflector entries below the diagonal of owned columns
+    for (int t = 0; t < nloc_all(k, c, P); ++t) {
+      const int j = c + P * t;
+      double* cj = W + (int64_t)j * ldw;
+      for (int rr = j + 1 + tid; rr < k; rr += NT) __stcg(cj + rr, 0.0);
+    }
+    m = k;
+    team_sync(hdr, P);
+  }
+  if (ta.prof && blockIdx.x == 0 && tid == 0) ta.prof[11] += clock64() - t_qr0;
+  const long long t_cp0 = clock64();
+  const int nloc = nloc_all(k, c, P);                 // owned columns j = c + P*t
+  const int ncap = ta.colcap / m;
+  const int ns = min(nloc, ncap);                     // owned columns t < ns live in smem
   const bool v_in_smem = m <= ta.vcap;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
   for (int j = tid; j < k; j += NT) {
     inv[j] = j;
     pos[j] = j;
   }
+  for (int64_t e = tid; e < (int64_t)ns * m; e += NT) {
+    const int t = (int)(e / m), r = (int)(e % m);
+    colbuf[e] = __ldcg(W + (int64_t)(c + P * t) * ldw + r);
+  }
+  __syncthreads();
   for (int t = warp; t < nloc; t += nw) {
-    const double* cj = W + (int64_t)(c + P * t) * ldw;
     double a = 0.0;
-    for (int r = lane; r < m; r += 32) {
-      const double x = __ldcg(cj + r);
-      a += x * x;
+    if (t < ns) {
+      const double* cj = colbuf + (int64_t)t * m;
+      for (int r = lane; r < m; r += 32) a += cj[r] * cj[r];
+    } else {
+      const double* cj = W + (int64_t)(c + P * t) * ldw;
+      for (int r = lane; r < m; r += 32) {
+        const double x = __ldcg(cj + r);
+        a += x * x;
+      }
     }
     a = sqrt(warp_sum(a));
     if (lane == 0) ovn1[t] = ovn2[t] = a;
   }
   __syncthreads();
   const int mn = min(m, k);
-  double* diagR = W + (int64_t)k * ldw;   // |R_ii| of completed steps (the reflectors themselves are not kept)
-  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
+  double* diagR = W + (int64_t)k * ldw;   // R_ii of completed steps
+  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m0, k));
   double cut = 0.0;
   int steps = 0;
-  __shared__ int s_own[TOWN];
   const bool prof = ta.prof && blockIdx.x == 0 && tid == 0;
   long long tp = prof ? clock64() : 0;
 #define TEAM_PHASE(id)                                   \
@@ -523,6 +734,15 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       if (pj >= i) loc = better(loc, ArgMax{ovn1[t], pj});
     }
     const ArgMax mine = cta_argmax(loc, sred);
+    // publish the local candidate if it lives in shared memory
+    if (mine.i != 0x7fffffff) {
+      const int tb = (inv[mine.i] - c) / P;
+      if (tb < ns) {
+        const double* src = colbuf + (int64_t)tb * m;
+        double* dst = cand_base + (int64_t)(((i & 1) * P) + c) * ta.cand_ld;
+        for (int r = i + tid; r < m; r += NT) __stcg(dst + r, src[r]);
+      }
+    }
     const int par = (i & 1) * P;
     if (tid == 0) {
       __stcg(slot_v + par + c, mine.v);
@@ -539,6 +759,10 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
     if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
     const int p = best.i;
     const int phys = inv[p];
+    const int q = phys % P, tq = (phys - q) / P;
+    const int nloc_q = q < k ? (k - q + P - 1) / P : 0;
+    const double* cp = (tq < min(nloc_q, ncap)) ? cand_base + (int64_t)(((i & 1) * P) + q) * ta.cand_ld
+                                                : W + (int64_t)phys * ldw;
     __syncthreads();
     if (tid == 0 && p != i) {   // replay the interchange on the logical permutation
       const int a = inv[i];
@@ -548,7 +772,6 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       pos[phys] = i;
     }
     // (b) reflector of the pivot column (dlarfg), formed by every CTA
-    const double* cp = W + (int64_t)phys * ldw;
     double part = 0.0;
     for (int r = i + 1 + tid; r < m; r += NT) {
       const double x = __ldcg(cp + r);
@@ -556,7 +779,6 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       part += x * x;
     }
     const double xnorm = sqrt(cta_sum(part, sred));   // cta_sum syncs: inv/pos/vs visible
-    TEAM_PHASE(2);
     const double alpha = __ldcg(cp + i);
     double tau = 0.0, beta = alpha, scal = 1.0;
     if (xnorm != 0.0) {
@@ -564,12 +786,12 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
+    TEAM_PHASE(2);
     if (i == 0) cut = cutrel * fabs(beta);
     if (c == 0 && tid == 0) __stcg(diagR + i, beta);
     steps = i + 1;
-    // (c) apply H = I - tau [1; v][1; v]^T (v = scal * x) to owned unpivoted columns, TCH at a time
-    // compact list of owned unpivoted columns (local index t) in shared memory
-    __shared__ int s_nact;
+    // (c) apply H = I - tau [1; v][1; v]^T (v = scal * x) to owned unpivoted columns,
+    //     shared-memory columns first, then streamed ones, TCH at a time
     if (tid == 0) {
       int a = 0;
       for (int t = 0; t < nloc; ++t)
@@ -577,13 +799,23 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       s_nact = a;
     }
     __syncthreads();
-    TEAM_PHASE(3);
     const int nact = s_nact;
     for (int u0 = 0; u0 < nact; u0 += TCH) {
       const int nown = min(TCH, nact - u0);
-      int own[TCH];
+      // chunks never mix residences: cut at the smem/global boundary
+      int nchunk = nown;
+      const bool in_smem = s_own[u0] < ns;
+      for (int u = 1; u < nown; ++u)
+        if ((s_own[u0 + u] < ns) != in_smem) {
+          nchunk = u;
+          break;
+        }
+      double* colp[TCH];
 #pragma unroll
-      for (int u = 0; u < TCH; ++u) own[u] = c + P * s_own[u0 + (u < nown ? u : 0)];
+      for (int u = 0; u < TCH; ++u) {
+        const int t = s_own[u0 + (u < nchunk ? u : 0)];
+        colp[u] = in_smem ? colbuf + (int64_t)t * m : W + (int64_t)(c + P * t) * ldw;
+      }
       if (tau != 0.0) {
         double acc[TCH];
 #pragma unroll
@@ -592,7 +824,7 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
           const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
 #pragma unroll
           for (int u = 0; u < TCH; ++u)
-            if (u < nown) acc[u] += vr * __ldcg(W + (int64_t)own[u] * ldw + r);
+            if (u < nchunk) acc[u] += vr * (in_smem ? colp[u][r] : __ldcg(colp[u] + r));
         }
 #pragma unroll
         for (int u = 0; u < TCH; ++u) {
@@ -602,18 +834,19 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       }
       if (tid == 0) s_nrec = 0;
       __syncthreads();
-      TEAM_PHASE(4);
-      if (tid < nown) {
+      TEAM_PHASE(in_smem ? 3 : 4);
+      if (tid < nchunk) {
         const int t = s_own[u0 + tid];
-        double* cj = W + (int64_t)(c + P * t) * ldw;
-        double rowi = __ldcg(cj + i);
+        double* cj = in_smem ? colbuf + (int64_t)t * m : W + (int64_t)(c + P * t) * ldw;
+        double rowi = in_smem ? cj[i] : __ldcg(cj + i);
         double tw = 0.0;
         if (tau != 0.0) {
           double w = 0.0;
-          for (int q = 0; q < nw; ++q) w += sdot[q * TCH + tid];
+          for (int qq = 0; qq < nw; ++qq) w += sdot[qq * TCH + tid];
           tw = tau * (rowi + scal * w);
           rowi -= tw;
-          __stcg(cj + i, rowi);
+          if (in_smem) cj[i] = rowi;
+          else __stcg(cj + i, rowi);
         }
         sdot[nw * TCH + tid] = tw * scal;
         // partial-norm downdate (dlaqp2 loop 10) on the updated pivot-row entry
@@ -631,31 +864,29 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
         if (rec) atomicAdd(&s_nrec, 1);
       }
       __syncthreads();
-      TEAM_PHASE(5);
       if (tau != 0.0) {
         double tw[TCH];
 #pragma unroll
-        for (int u = 0; u < TCH; ++u) tw[u] = (u < nown) ? sdot[nw * TCH + u] : 0.0;
+        for (int u = 0; u < TCH; ++u) tw[u] = (u < nchunk) ? sdot[nw * TCH + u] : 0.0;
         for (int r = i + 1 + tid; r < m; r += NT) {
           const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
 #pragma unroll
           for (int u = 0; u < TCH; ++u)
-            if (u < nown) {
-              double* q = W + (int64_t)own[u] * ldw + r;
-              __stcg(q, __ldcg(q) - tw[u] * vr);
+            if (u < nchunk) {
+              if (in_smem) colp[u][r] -= tw[u] * vr;
+              else __stcg(colp[u] + r, __ldcg(colp[u] + r) - tw[u] * vr);
             }
         }
       }
-      TEAM_PHASE(6);
       if (s_nrec) {
         __syncthreads();
-        for (int u = warp; u < nown; u += nw) {
+        for (int u = warp; u < nchunk; u += nw) {
           if (!s_rec[u]) continue;
-          const double* cj = W + (int64_t)own[u] * ldw;
+          const double* cj = colp[u];
           double a = 0.0;
           if (i < m - 1) {
             for (int r = i + 1 + lane; r < m; r += 32) {
-              const double x = __ldcg(cj + r);
+              const double x = in_smem ? cj[r] : __ldcg(cj + r);
               a += x * x;
             }
             a = sqrt(warp_sum(a));
@@ -664,13 +895,21 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
         }
       }
       __syncthreads();
-      TEAM_PHASE(7);
+      TEAM_PHASE(in_smem ? 5 : 6);
+      u0 += nchunk - TCH;   // advance by the rows actually processed
     }
     if (prof) ta.prof[8] += 1;
   }
 #undef TEAM_PHASE
+  if (ta.prof && blockIdx.x == 0 && tid == 0) ta.prof[12] += clock64() - t_cp0;
+  const long long t_fin0 = clock64();
+  // write back R rows [0, steps) of shared-memory columns
+  for (int64_t e = tid; e < (int64_t)ns * steps; e += NT) {
+    const int t = (int)(e / steps), r = (int)(e % steps);
+    __stcg(W + (int64_t)(c + P * t) * ldw + r, colbuf[(int64_t)t * m + r]);
+  }
   team_sync(hdr, P);
-  // rank from the diagonal R_ii = W[inv[i]][i] (identical on every CTA); natural-order maps by CTA 0
+  // rank from the diagonal (identical on every CTA); natural-order maps by CTA 0
   __shared__ int s_rank;
   if (tid == 0) {
     const double cutv = cutrel * fabs(__ldcg(diagR));
@@ -684,8 +923,8 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
         perm[j] = inv[j];
       }
       for (int i = r; i < k; ++i) flag[inv[i]] = 1;
-      int ns = 0, nr = 0;
-      for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns++;
+      int ns2 = 0, nr = 0;
+      for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns2++;
     }
   }
   team_sync(hdr, P);
@@ -710,6 +949,8 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
     const int col = __ldcg(sidx + ph);
     for (int l = tid; l < r; l += NT) T[(int64_t)__ldcg(sidx + inv[l]) * kt + col] = __ldcg(W + (int64_t)ph * ldw + l);
   }
+  if (ta.prof && tid == 0) atomicAdd((unsigned long long*)&ta.prof[9 + (c == 0 ? 0 : 1)], (unsigned long long)(clock64() - t_kernel0));
+  if (ta.prof && blockIdx.x == 0 && tid == 0) ta.prof[13] += clock64() - t_fin0;
   if (c == 0) {
     uint8_t* red = sk.red + gof;
     for (int j = tid; j < k; j += NT) {
@@ -1252,11 +1493,18 @@ void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces,
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_skel_gather<<<count, NT, SMEM_BYTES, s>>>(lv, a, faces);
 }
-static size_t team_smem(int vcap, int kmax) { return SMEM_BYTES + (size_t)vcap * sizeof(double) + 2 * sizeof(int) * (size_t)kmax; }
-int team_blocks_per_sm(int vcap, int kmax) {
+static size_t team_smem(int vcap, int kmax, int colcap) {
+  return SMEM_BYTES + ((size_t)vcap + kmax + 1 + colcap) * sizeof(double);
+}
+int team_colcap(int vcap, int kmax) {
+  // fill the CTA's shared memory (one team CTA per SM) with owned columns
+  const long long avail = (227 * 1024 - 14 * 1024) / 8 - SMEM_DOUBLES - vcap - kmax - 1;
+  return avail > 0 ? (int)avail : 0;
+}
+int team_blocks_per_sm(int vcap, int kmax, int colcap) {
   static size_t cached_bytes = 0;
   static int cached = 0;
-  const size_t bytes = team_smem(vcap, kmax);
+  const size_t bytes = team_smem(vcap, kmax, colcap);
   if (bytes == cached_bytes) return cached;
   cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   int nb = 0;
@@ -1268,7 +1516,7 @@ int team_blocks_per_sm(int vcap, int kmax) {
 void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s) {
   if (nblocks == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const size_t bytes = team_smem(t.vcap, t.kmax);
+  const size_t bytes = team_smem(t.vcap, t.kmax, t.colcap);
   cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   LevelDev lv2 = lv;
   SkelArgs a2 = a;

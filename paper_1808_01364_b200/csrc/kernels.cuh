@@ -102,6 +102,9 @@ struct TeamArgs {
   int vcap;              // Householder vector staged in smem when m <= vcap
   int kmax;              // largest separator of the launch (replicated permutation in smem)
   long long* prof;       // optional per-phase clock accumulators (debug)
+  double* cand;          // 2 staging columns per CTA (pivot candidates), ld cand_ld
+  int64_t cand_ld;
+  int colcap;            // doubles of shared memory for resident owned columns
 };
 
 struct RepackArgs {
