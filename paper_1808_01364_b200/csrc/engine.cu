@@ -17,7 +17,8 @@
 
 namespace phif {
 
-constexpr int BIG_N = 192;   // cells with |I| >= BIG_N take the tile-parallel path
+constexpr int BIG_N = 192;       // cells with |I| >= BIG_N take the tile-parallel path
+constexpr int APPLY_BIG = 96;    // groups with |g| >= APPLY_BIG are replayed by batched GEMMs
 
 static std::chrono::steady_clock::time_point g_dbg_t0 = std::chrono::steady_clock::now();
 static double dbg_ms() {
@@ -447,14 +448,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       if (do_prec) {
         L_off[t] = rec;
         Lg_off[g] = rec;
-        rec += (int64_t)k * k;
+        rec += 2 * (int64_t)k * k;   // [L ; L^-T]
       }
       pn[t] = k;
       pI_off[t] = G.off[g];
       pwork[t] = pw;
-      pw += k;
+      pw += (k >= APPLY_BIG ? 2 : 1) * k;
     }
     L.prec_work_unit = pw;
+    L.h_L_off = L_off;
+    L.h_pI_off = pI_off;
+    L.h_pwork = pwork;
+    L.h_pn = pn;
     if (do_prec) {
       for (int t = 0; t < r; ++t) {
         const double k = pn[t];
@@ -479,15 +484,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       T_off[t] = rec;
       rec += (int64_t)k * k;
       SP_off[t] = rec;
-      rec += (int64_t)k * k;
+      rec += 2 * (int64_t)k * k;   // [L~ ; X~^T ; L~^-T]
       work_off[t] = work;
       work += std::max<int64_t>((std::max<int64_t>(rows, 1)) * k + 2 * k, 2 * (int64_t)k * k);
       iwork_off[t] = iwork;
       iwork += 3 * (int64_t)k;
       awork[t] = aw;
-      aw += k;
+      aw += (k >= APPLY_BIG ? 2 : 1) * k;
     }
     L.skel_work_unit = aw;
+    L.h_T_off = T_off;
+    L.h_SP_off = SP_off;
+    L.h_awork = awork;
     L.rec_doubles = rec;
     plan_ms += ms_since(tp);
     // ---------------- device structures ----------------
@@ -647,12 +655,85 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     pa.L_off_of_group = L.p_L_off_of_group.as<int64_t>();
     pa.nscale = do_prec ? (int)P.scale_blk.size() : 0;
     pa.scale_blk = L.p_scale_blk.as<int>();
+    pa.list = nullptr;
+    pa.scale_list = nullptr;
     if (timing) CK(cudaEventRecord(ev[6], s));
     DBG("level %d: precondition r=%d scale=%d", lev, pa.r, pa.nscale);
-    launch_prec_factor(dv, pa, F->status.as<DevStatus>(), s);
-    check_status(*F, lev, ST_PRECONDITION);
-    DBG("level %d: precondition factor done", lev);
-    launch_prec_scale(dv, pa, s);
+    if (do_prec) {
+      // small groups: one CTA each; big groups: tile-parallel panels [A_gg ; I] -> [L ; L^-T]
+      std::vector<int> psmall, pbig;
+      for (int t = 0; t < r; ++t) (pn[t] >= BIG_N ? pbig : psmall).push_back(t);
+      L.h_prec_big = pbig;
+      upload(L.d_prec_small, psmall, s);
+      PrecArgs ps = pa;
+      ps.list = L.d_prec_small.as<int>();
+      ps.r = (int)psmall.size();
+      launch_prec_factor(dv, ps, F->status.as<DevStatus>(), s);
+      if (!pbig.empty()) {
+        DBuf dbig;
+        upload(dbig, pbig, s);
+        launch_prec_build(dv, pa, dbig.as<int>(), (int)pbig.size(), s);
+        std::vector<int> zeros(r, 0);
+        std::vector<int64_t> zoff(r, 0);
+        BigPlan bpp;
+        bpp.build(pbig, pn, zeros, L.rec.as<double>(), L_off, L.rec.as<double>(), zoff, s);
+        bpp.run(F->status.as<DevStatus>(), s);
+      }
+      check_status(*F, lev, ST_PRECONDITION);
+      DBG("level %d: precondition factor done", lev);
+      // two-sided scaling: small blocks by substitution, blocks touching a big group by GEMMs
+      // with the explicit inverses: B <- (L_g^-T)^T B L_h^-T
+      std::vector<int> ssmall;
+      std::vector<GemmDesc> d1, d2;
+      std::vector<int> w1d, w1t, w2d, w2t;
+      int64_t tmp_need = 0;
+      for (size_t q = 0; q < P.scale_blk.size(); ++q) {
+        const int b = P.scale_blk[q];
+        const int kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
+        if (std::max(kg, kh) < BIG_N) ssmall.push_back((int)q);
+        else tmp_need += (int64_t)kg * kh;
+      }
+      upload(L.d_scale_small, ssmall, s);
+      PrecArgs pss = pa;
+      pss.scale_list = L.d_scale_small.as<int>();
+      pss.nscale = (int)ssmall.size();
+      launch_prec_scale(dv, pss, s);
+      if (tmp_need) {
+        DBuf tmp;
+        tmp.alloc(tmp_need * sizeof(double), s);
+        int64_t to = 0;
+        const double* rec0 = L.rec.as<double>();
+        for (size_t q = 0; q < P.scale_blk.size(); ++q) {
+          const int b = P.scale_blk[q];
+          const int gg = P.pat.bg[b], hh = P.pat.bh[b];
+          const int kg = G.size(gg), kh = G.size(hh);
+          if (std::max(kg, kh) < BIG_N) continue;
+          double* blk = L.pool.as<double>() + P.boff[b];
+          double* T = tmp.as<double>() + to;
+          to += (int64_t)kg * kh;
+          GemmDesc a{rec0 + Lg_off[gg] + (int64_t)kg * kg, blk, T, kg, kh, kg, kg, kh, kh, 1, 1.0, 0.0};
+          GemmDesc c{T, rec0 + Lg_off[hh] + (int64_t)kh * kh, blk, kg, kh, kh, kh, kh, kh, 0, 1.0, 0.0};
+          for (int t = 0; t < (kg + 63) / 64; ++t) {
+            w1d.push_back((int)d1.size());
+            w1t.push_back(t);
+            w2d.push_back((int)d2.size());
+            w2t.push_back(t);
+          }
+          d1.push_back(a);
+          d2.push_back(c);
+        }
+        DBuf dd1, dd2, dw1d, dw1t, dw2d, dw2t;
+        upload(dd1, d1, s);
+        upload(dd2, d2, s);
+        upload(dw1d, w1d, s);
+        upload(dw1t, w1t, s);
+        upload(dw2d, w2d, s);
+        upload(dw2t, w2t, s);
+        launch_bgemm(dd1.as<GemmDesc>(), dw1d.as<int>(), dw1t.as<int>(), (int)w1d.size(), s);
+        launch_bgemm(dd2.as<GemmDesc>(), dw2d.as<int>(), dw2t.as<int>(), (int)w2d.size(), s);
+        CK(cudaStreamSynchronize(s));
+      }
+    }
     if (timing) CK(cudaEventRecord(ev[7], s));
     // ---------------- stage 3: skeletonization ----------------
     upload(L.s_groups, P.skeleton, s);
@@ -857,6 +938,21 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     upload(L.s_R, Rd, s);
     upload(L.s_R_off, R_off, s);
     upload(L.s_awork_off, awork, s);
+    L.h_S_off = S_off;
+    L.h_R_off = R_off;
+    L.h_sr = sr;
+    L.h_skt = skt;
+    {
+      std::vector<int> small_sk, small_pr;
+      for (int t = 0; t < nsk; ++t)
+        if (G.size(P.skeleton[t]) < APPLY_BIG) small_sk.push_back(t);
+      for (int t = 0; t < r; ++t)
+        if (pn[t] < APPLY_BIG) small_pr.push_back(t);
+      L.n_apply_small_sk = (int)small_sk.size();
+      L.n_apply_small_pr = (int)small_pr.size();
+      upload(L.d_apply_small_sk, small_sk, s);
+      upload(L.d_apply_small_pr, small_pr, s);
+    }
     plan_ms += ms_since(tp);
     DBG("level %d: next-level inputs ready", lev);
     if (timing) {
@@ -1015,6 +1111,166 @@ static BigApply* big_apply(Factorization& F, LevelRT& L, int k) {
   return &b;
 }
 
+// GEMM replay of the big block-Jacobi and separator records of one level (explicit inverses
+// stored below L and L~). Steps: gather rows -> batched GEMM phases -> scatter rows.
+struct GemmReplay {
+  int k = -1;
+  double* work = nullptr;
+  struct Step {
+    int kind;      // 0 gather, 1 scatter, 2 gemm
+    int64_t off, cnt;
+    int idx;       // gather/scatter index array: 0 members, 1 skeleton DOFs, 2 redundant DOFs
+  };
+  std::vector<Step> steps[4];   // 0 prec up, 1 prec down, 2 skel up, 3 skel down
+  DBuf desc, wd, wt, ss, sd, sl;
+  void build(Factorization& F, LevelRT& L, int kk) {
+    k = kk;
+    work = F.work.as<double>();
+    const LevelPlan& P = L.plan;
+    const Groups& G = P.grp;
+    const double* rec = L.rec.as<double>();
+    std::vector<GemmDesc> d;
+    std::vector<int> wdh, wth;
+    std::vector<int64_t> src, dst;
+    std::vector<int> len;
+    auto seg_begin = [&]() { return (int64_t)src.size(); };
+    auto add_step = [&](int which, int kind, int64_t off, int idx) {
+      const int64_t cnt = (kind == 2 ? (int64_t)wdh.size() : (int64_t)src.size()) - off;
+      if (cnt > 0) steps[which].push_back({kind, off, cnt, idx});
+    };
+    auto gemm = [&](const double* A, int lda, int ta, const double* B, double* C, int M, int K, double al,
+                    double be) {
+      if (M <= 0 || K <= 0) return;
+      GemmDesc g{A, B, C, M, k, K, lda, k, k, ta, al, be};
+      const int id = (int)d.size();
+      d.push_back(g);
+      for (int t = 0; t < (M + 63) / 64; ++t) {
+        wdh.push_back(id);
+        wth.push_back(t);
+      }
+    };
+    // ---- block Jacobi: x_g <- L^-1 x_g (up) / L^-T x_g (down)
+    std::vector<int> bigp;
+    if (F.method != 0 && !P.root)
+      for (size_t t = 0; t < L.h_pn.size(); ++t)
+        if (L.h_pn[t] >= APPLY_BIG) bigp.push_back((int)t);
+    for (int dir = 0; dir < 2; ++dir) {
+      int64_t o = seg_begin();
+      for (int t : bigp) {
+        src.push_back(L.h_pI_off[t]);
+        dst.push_back(L.h_pwork[t]);
+        len.push_back(L.h_pn[t]);
+      }
+      add_step(dir, 0, o, 0);
+      o = (int64_t)wdh.size();
+      for (int t : bigp) {
+        const int n = L.h_pn[t];
+        const double* LiT = rec + L.h_L_off[t] + (int64_t)n * n;
+        double* Y = work + L.h_pwork[t] * k;
+        gemm(LiT, n, dir == 0 ? 1 : 0, Y, Y + (int64_t)n * k, n, n, 1.0, 0.0);
+      }
+      add_step(dir, 2, o, 0);
+      o = seg_begin();
+      for (int t : bigp) {
+        src.push_back(L.h_pI_off[t]);
+        dst.push_back(L.h_pwork[t] + L.h_pn[t]);
+        len.push_back(L.h_pn[t]);
+      }
+      add_step(dir, 1, o, 0);
+    }
+    // ---- separators: records [L~ ; X~^T ; L~^-T] and T
+    std::vector<int> bigs;
+    if (!P.root)
+      for (size_t t = 0; t < P.skeleton.size(); ++t)
+        if (G.size(P.skeleton[t]) >= APPLY_BIG && L.h_skt[t] > 0) bigs.push_back((int)t);
+    for (int dir = 0; dir < 2; ++dir) {
+      const int which = 2 + dir;
+      int64_t o = seg_begin();
+      for (int t : bigs) {
+        src.push_back(L.h_S_off[t]);
+        dst.push_back(L.h_awork[t]);
+        len.push_back(L.h_sr[t]);
+      }
+      add_step(which, 0, o, 1);
+      o = seg_begin();
+      for (int t : bigs) {
+        src.push_back(L.h_R_off[t]);
+        dst.push_back(L.h_awork[t] + L.h_sr[t]);
+        len.push_back(L.h_skt[t]);
+      }
+      add_step(which, 0, o, 2);
+      for (int ph = 0; ph < 3; ++ph) {
+        o = (int64_t)wdh.size();
+        for (int t : bigs) {
+          const int r = L.h_sr[t], kt = L.h_skt[t];
+          const double* T = rec + L.h_T_off[t];
+          const double* Pn = rec + L.h_SP_off[t];
+          const double* PB = Pn + (int64_t)kt * kt;
+          const double* LiT = Pn + (int64_t)(kt + r) * kt;
+          double* Ys = work + L.h_awork[t] * k;
+          double* Yr = Ys + (int64_t)r * k;
+          double* Z = Yr + (int64_t)kt * k;
+          if (dir == 0) {   // up: Yr -= T^T Ys ; Z = L~^-1 Yr ; Ys -= X~^T Z
+            if (ph == 0) gemm(T, kt, 1, Ys, Yr, kt, r, -1.0, 1.0);
+            if (ph == 1) gemm(LiT, kt, 1, Yr, Z, kt, kt, 1.0, 0.0);
+            if (ph == 2) gemm(PB, kt, 0, Z, Ys, r, kt, -1.0, 1.0);
+          } else {          // down: Yr -= X~ Ys ; Z = L~^-T Yr ; Ys -= T Z
+            if (ph == 0) gemm(PB, kt, 1, Ys, Yr, kt, r, -1.0, 1.0);
+            if (ph == 1) gemm(LiT, kt, 0, Yr, Z, kt, kt, 1.0, 0.0);
+            if (ph == 2) gemm(T, kt, 0, Z, Ys, r, kt, -1.0, 1.0);
+          }
+        }
+        add_step(which, 2, o, 0);
+      }
+      o = seg_begin();
+      for (int t : bigs) {
+        src.push_back(L.h_S_off[t]);
+        dst.push_back(L.h_awork[t]);
+        len.push_back(L.h_sr[t]);
+      }
+      add_step(which, 1, o, 1);
+      o = seg_begin();
+      for (int t : bigs) {
+        src.push_back(L.h_R_off[t]);
+        dst.push_back(L.h_awork[t] + L.h_sr[t] + L.h_skt[t]);
+        len.push_back(L.h_skt[t]);
+      }
+      add_step(which, 1, o, 2);
+    }
+    cudaStream_t s = F.stream;
+    upload(desc, d, s);
+    upload(wd, wdh, s);
+    upload(wt, wth, s);
+    upload(ss, src, s);
+    upload(sd, dst, s);
+    upload(sl, len, s);
+  }
+  void run(int which, LevelRT& L, double* x, cudaStream_t s) const {
+    for (const Step& st : steps[which]) {
+      if (st.kind == 2) {
+        launch_bgemm(desc.as<GemmDesc>(), wd.as<int>() + st.off, wt.as<int>() + st.off, (int)st.cnt, s);
+      } else {
+        const int* idx = st.idx == 0 ? L.mem.as<int>() : (st.idx == 1 ? L.s_S.as<int>() : L.s_R.as<int>());
+        launch_rows(work, x, idx, ss.as<int64_t>() + st.off, sd.as<int64_t>() + st.off, sl.as<int>() + st.off,
+                    (int)st.cnt, k, st.kind == 1, s);
+      }
+    }
+  }
+};
+
+static GemmReplay* gemm_replay(Factorization& F, LevelRT& L, int k) {
+  if (!L.replay) L.replay = std::make_shared<GemmReplay>();
+  GemmReplay& r = *L.replay;
+  if (r.k != k || r.work != F.work.as<double>()) {
+    r.steps[0].clear();
+    r.steps[1].clear();
+    r.steps[2].clear();
+    r.steps[3].clear();
+    r.build(F, L, k);
+  }
+  return &r;
+}
+
 static ApplyCellArgs cell_args(Factorization& F, LevelRT& L) {
   ApplyCellArgs a;
   a.list = L.h_small_cells.size() == L.plan.interior.size() ? nullptr : L.d_small_cells.as<int>();
@@ -1035,7 +1291,8 @@ static ApplyCellArgs cell_args(Factorization& F, LevelRT& L) {
 
 static ApplyPrecArgs prec_args(Factorization& F, LevelRT& L) {
   ApplyPrecArgs a;
-  a.r = (F.method != 0 && !L.plan.root) ? (int)L.plan.precond.size() : 0;
+  a.list = L.d_apply_small_pr.as<int>();
+  a.r = (F.method != 0 && !L.plan.root) ? L.n_apply_small_pr : 0;
   a.n = L.p_n.as<int>();
   a.I = L.mem.as<int>();
   a.I_off = L.p_I_off.as<int64_t>();
@@ -1048,7 +1305,8 @@ static ApplyPrecArgs prec_args(Factorization& F, LevelRT& L) {
 
 static ApplySkelArgs skel_args(Factorization& F, LevelRT& L) {
   ApplySkelArgs a;
-  a.nsk = L.plan.root ? 0 : (int)L.plan.skeleton.size();
+  a.list = L.d_apply_small_sk.as<int>();
+  a.nsk = L.plan.root ? 0 : L.n_apply_small_sk;
   a.r = L.s_r.as<int>();
   a.kt = L.s_kt.as<int>();
   a.S = L.s_S.as<int>();
@@ -1074,16 +1332,22 @@ void apply(Factorization& F, double* x, int k, int mode) {
       launch_apply_reduce(L.bd_dof.as<int>(), L.bd_off.as<int64_t>(), L.bd_rows.as<int>(), F.wbuf.as<double>(),
                           L.nbd, x, k, s);
       if (L.plan.root) break;
+      GemmReplay* gr = gemm_replay(F, L, k);
       launch_apply_prec(prec_args(F, L), x, k, true, s);
+      gr->run(0, L, x, s);
       launch_apply_skel(skel_args(F, L), x, k, true, s);
+      gr->run(2, L, x, s);
     }
   }
   if (mode == 0 || mode == 2) {
     for (int li = (int)F.levels.size() - 1; li >= 0; --li) {
       LevelRT& L = *F.levels[li];
       if (!L.plan.root) {
+        GemmReplay* gr = gemm_replay(F, L, k);
         launch_apply_skel(skel_args(F, L), x, k, false, s);
+        gr->run(3, L, x, s);
         launch_apply_prec(prec_args(F, L), x, k, false, s);
+        gr->run(1, L, x, s);
       }
       launch_apply_cell(cell_args(F, L), x, k, false, s);
       if (BigApply* ba = big_apply(F, L, k)) ba->down(L, x, s);

@@ -76,6 +76,13 @@ struct LevelRT {
   int64_t cell_work_unit = 0, wbuf_unit = 0;
   // precondition
   DBuf p_groups, p_L_off, p_L_off_of_group, p_scale_blk, p_n, p_I_off, p_work_off;
+  DBuf d_prec_small, d_scale_small;
+  std::vector<int> h_prec_big;
+  std::vector<int64_t> h_L_off, h_pI_off, h_pwork, h_T_off, h_SP_off, h_awork, h_S_off, h_R_off;
+  std::vector<int> h_pn, h_sr, h_skt;
+  DBuf d_apply_small_sk, d_apply_small_pr;
+  int n_apply_small_sk = 0, n_apply_small_pr = 0;
+  std::shared_ptr<struct GemmReplay> replay;
   int64_t prec_work_unit = 0;
   // skeleton
   DBuf s_groups, s_nbr_off, s_nbr, s_nbr_blk, s_order, s_rank, s_T_off, s_P_off, s_work_off, s_iwork_off;

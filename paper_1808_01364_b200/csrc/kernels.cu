@@ -102,15 +102,19 @@ __global__ void __launch_bounds__(NT) k_schur(LevelDev lv, SchurArgs sa) {
 // ---------------------------------------------------------------------------
 // Stage 2: block Jacobi.
 // ---------------------------------------------------------------------------
+// record [L ; L^-T] (2k x k): the identity rows below A_gg come out of the partial Cholesky as L^-T
 __global__ void __launch_bounds__(NT) k_prec_factor(LevelDev lv, PrecArgs pa, DevStatus* st) {
   extern __shared__ double smem[];
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int t = pa.list ? pa.list[blockIdx.x] : blockIdx.x, tid = threadIdx.x;
   const int g = pa.groups[t], k = lv.gsize[g];
   double* A = lv.pool + lv.boff[lv.diag_blk[g]];
   double* L = pa.rec + pa.L_off[t];
-  for (int64_t e = tid; e < (int64_t)k * k; e += NT) L[e] = A[e];
+  for (int64_t e = tid; e < (int64_t)k * k; e += NT) {
+    L[e] = A[e];
+    L[(int64_t)k * k + e] = (e / k == e % k) ? 1.0 : 0.0;
+  }
   __syncthreads();
-  const int info = cta_potrf_panel(L, k, k, k, smem);
+  const int info = cta_potrf_panel(L, 2 * k, k, k, smem);
   if (info >= 0) {
     if (tid == 0) report_bad(st, t, info);
     return;
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(NT) k_prec_factor(LevelDev lv, PrecArgs pa, De
 
 __global__ void __launch_bounds__(NT) k_prec_scale(LevelDev lv, PrecArgs pa) {
   extern __shared__ double smem[];
-  const int blk = pa.scale_blk[blockIdx.x];
+  const int blk = pa.scale_list ? pa.scale_blk[pa.scale_list[blockIdx.x]] : pa.scale_blk[blockIdx.x];
   const int g = lv.bg[blk], h = lv.bh[blk];
   const int kg = lv.gsize[g], kh = lv.gsize[h];
   double* B = lv.pool + lv.boff[blk];
@@ -1006,6 +1010,8 @@ __global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, De
     Asr[e] = v;
     Ast[e] = v;
   }
+  double* Idr = Pn + (int64_t)(kt + r) * kt;   // identity rows: become L~^-T
+  for (int64_t e = tid; e < (int64_t)kt * kt; e += NT) Idr[e] = (e / kt == e % kt) ? 1.0 : 0.0;
   __syncthreads();
   double* gsm = smem + GEMM_OFF;
   if (r > 0) {
@@ -1013,7 +1019,7 @@ __global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, De
     cta_gemm<true, false>(kt, kt, r, -1.0, T, kt, Ast, kt, 1.0, Pn, kt, false, gsm);      // Att -= T^T Ast
     cta_gemm<true, false>(kt, kt, r, -1.0, Asr, kt, T, kt, 1.0, Pn, kt, false, gsm);      // Att -= Asr^T T
   }
-  const int info = cta_potrf_panel(Pn, kt + r, kt, kt, smem);
+  const int info = cta_potrf_panel(Pn, kt + r + kt, kt, kt, smem);
   if (info >= 0) {
     if (tid == 0) report_bad(st, s, info);
     return;
@@ -1185,6 +1191,23 @@ __global__ void __launch_bounds__(NT) k_big_syrk(BigArgs a) {
                         n, 0.0, U + (int64_t)i0 * b + j0, b, false, smem + GEMM_OFF);
 }
 
+// build panels [A_gg ; I] of big block-Jacobi groups (A_gg <- I afterwards), grid-stride
+__global__ void k_prec_build(LevelDev lv, PrecArgs pa, const int* list, int nbig, int chunks) {
+  const int bc = blockIdx.x / chunks, ch = blockIdx.x % chunks;
+  if (bc >= nbig) return;
+  const int t = list[bc];
+  const int g = pa.groups[t], k = lv.gsize[g];
+  double* A = lv.pool + lv.boff[lv.diag_blk[g]];
+  double* L = pa.rec + pa.L_off[t];
+  const int64_t stride = (int64_t)chunks * blockDim.x;
+  for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)k * k; e += stride) {
+    const double id = (e / k == e % k) ? 1.0 : 0.0;
+    L[e] = A[e];
+    L[(int64_t)k * k + e] = id;
+    A[e] = id;
+  }
+}
+
 // build panels [A_II ; A_BI] of big cells, grid-stride over (cell, chunk)
 __global__ void k_big_build(LevelDev lv, CellArgs ca, const int* big_cells, int nbig, int chunks) {
   const int bc = blockIdx.x / chunks, ch = blockIdx.x % chunks;
@@ -1210,23 +1233,102 @@ __global__ void k_big_build(LevelDev lv, CellArgs ca, const int* big_cells, int 
 }
 
 // ---------------------------------------------------------------------------
-// Batched GEMM: one 64-row output tile (all N columns, 64 at a time) per CTA.
-// work[i] = (descriptor, row tile).
+// Batched skinny GEMM (replay of records, N = nrhs <= 32 per pass):
+// C[64-row tile, 0:N] = beta*C + alpha*op(A)[rows, :] * B[:, 0:N].
+// K is streamed in 32-wide chunks through a 2-stage cp.async pipeline; each warp
+// owns 8 output rows x 32 columns (4 DMMA m8n8k4 tiles).
 // ---------------------------------------------------------------------------
+constexpr int SG_BM = 64, SG_BK = 32, SG_BN = 32;
+constexpr int SG_ALD = SG_BK + 4;   // sA[row][k]   (A rows; +4 pad: conflict-free fragments)
+constexpr int SG_BLD = SG_BN + 4;   // sB[k][col]
+constexpr int SG_STAGE = SG_BM * SG_ALD + SG_BK * SG_BLD;
+
+__device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  const int n = pred ? 8 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gptr), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 __global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile) {
   extern __shared__ double smem[];
   const GemmDesc d = desc[w_desc[blockIdx.x]];
-  const int i0 = 64 * w_tile[blockIdx.x];
-  const int M = min(64, d.M - i0);
+  const int i0 = SG_BM * w_tile[blockIdx.x];
+  const int M = min(SG_BM, d.M - i0);
   if (M <= 0) return;
-  for (int j0 = 0; j0 < d.N; j0 += 64) {
-    const int N = min(64, d.N - j0);
-    if (d.transA)
-      cta_gemm<true, false>(M, N, d.K, d.alpha, d.A + i0, d.lda, d.B + j0, d.ldb, d.beta,
-                            d.C + (int64_t)i0 * d.ldc + j0, d.ldc, false, smem + GEMM_OFF);
-    else
-      cta_gemm<false, false>(M, N, d.K, d.alpha, d.A + (int64_t)i0 * d.lda, d.lda, d.B + j0, d.ldb, d.beta,
-                             d.C + (int64_t)i0 * d.ldc + j0, d.ldc, false, smem + GEMM_OFF);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int j0 = 0; j0 < d.N; j0 += SG_BN) {
+    const int N = min(SG_BN, d.N - j0);
+    auto load_stage = [&](int st, int k0) {
+      double* sA = smem + st * SG_STAGE;
+      double* sB = sA + SG_BM * SG_ALD;
+      // A tile: 64 rows x 32 k
+      for (int e = tid; e < SG_BM * SG_BK; e += NT) {
+        int r, kk;
+        if (d.transA) {   // op(A)(i,k) = A[k*lda + i]: coalesce along i
+          kk = e / SG_BM;
+          r = e % SG_BM;
+        } else {          // A[i*lda + k]: coalesce along k
+          r = e / SG_BK;
+          kk = e % SG_BK;
+        }
+        const int gi = i0 + r, gk = k0 + kk;
+        const bool ok = gi < d.M && gk < d.K;
+        const double* src = d.transA ? d.A + (int64_t)(ok ? gk : 0) * d.lda + (ok ? gi : 0)
+                                     : d.A + (int64_t)(ok ? gi : 0) * d.lda + (ok ? gk : 0);
+        cp_async8(sA + r * SG_ALD + kk, src, ok);
+      }
+      // B tile: 32 k x 32 cols
+      for (int e = tid; e < SG_BK * SG_BN; e += NT) {
+        const int kk = e / SG_BN, c = e % SG_BN;
+        const int gk = k0 + kk;
+        const bool ok = gk < d.K && c < N;
+        const double* src = d.B + (int64_t)(ok ? gk : 0) * d.ldb + j0 + (ok ? c : 0);
+        cp_async8(sB + kk * SG_BLD + c, src, ok);
+      }
+      cp_async_commit();
+    };
+    double acc[4][2];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[y][0] = acc[y][1] = 0.0;
+    const int nk = (d.K + SG_BK - 1) / SG_BK;
+    if (nk > 0) load_stage(0, 0);
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {
+        load_stage((kc + 1) & 1, (kc + 1) * SG_BK);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* sA = smem + (kc & 1) * SG_STAGE;
+      const double* sB = sA + SG_BM * SG_ALD;
+#pragma unroll
+      for (int ks = 0; ks < SG_BK; ks += 4) {
+        const double af = sA[(warp * 8 + g) * SG_ALD + ks + t4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const double bf = sB[(ks + t4) * SG_BLD + y * 8 + g];
+          dmma(acc[y][0], acc[y][1], af, bf);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int r = warp * 8 + g, c = y * 8 + 2 * t4 + z;
+        if (r < M && c < N) {
+          double* p = d.C + (int64_t)(i0 + r) * d.ldc + j0 + c;
+          *p = (d.beta == 0.0 ? 0.0 : d.beta * *p) + d.alpha * acc[y][z];
+        }
+      }
   }
 }
 
@@ -1322,7 +1424,7 @@ __global__ void k_apply_reduce(const int* dof, const int64_t* off, const int* ro
 
 __global__ void __launch_bounds__(NT) k_apply_prec(ApplyPrecArgs a, double* x, int k, int up) {
   extern __shared__ double smem[];
-  const int t = blockIdx.x;
+  const int t = a.list ? a.list[blockIdx.x] : blockIdx.x;
   const int n = a.n[t];
   const int* I = a.I + a.I_off[t];
   double* Y = a.work + a.work_off[t] * k;
@@ -1334,7 +1436,7 @@ __global__ void __launch_bounds__(NT) k_apply_prec(ApplyPrecArgs a, double* x, i
 
 __global__ void __launch_bounds__(NT) k_apply_skel(ApplySkelArgs a, double* x, int k, int up) {
   extern __shared__ double smem[];
-  const int t = blockIdx.x;
+  const int t = a.list ? a.list[blockIdx.x] : blockIdx.x;
   const int r = a.r[t], kt = a.kt[t];
   if (kt == 0) return;
   const int* S = a.S + a.S_off[t];
@@ -1473,6 +1575,11 @@ void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_schur<<<a.ntgt, NT, 0, s>>>(lv, a);
 }
+void launch_prec_build(const LevelDev& lv, const PrecArgs& a, const int* list, int nbig, cudaStream_t s) {
+  if (!nbig) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_prec_build<<<nbig * 32, 256, 0, s>>>(lv, a, list, nbig, 32);
+}
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.r == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1553,7 +1660,7 @@ void launch_big_syrk(const BigArgs& a, cudaStream_t s) {
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
   if (!nwork) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_bgemm<<<nwork, NT, SMEM_BYTES, s>>>(desc, w_desc, w_tile);
+  k_bgemm<<<nwork, NT, 2 * SG_STAGE * sizeof(double), s>>>(desc, w_desc, w_tile);
 }
 void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                  const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s) {
@@ -1651,7 +1758,7 @@ void configure_kernels() {
   cudaFuncSetAttribute(k_big_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
   cudaFuncSetAttribute(k_big_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
   cudaFuncSetAttribute(k_big_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_bgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_bgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SG_STAGE * sizeof(double)));
 }
 
 }  // namespace phif

@@ -57,6 +57,8 @@ struct SchurArgs {
 
 struct PrecArgs {
   int r;
+  const int* list;                // groups factored by the one-CTA kernel (nullptr = all)
+  const int* scale_list;          // blocks scaled by the one-CTA kernel (nullptr = all)
   const int* groups;
   double* rec;
   const int64_t* L_off;           // per precond index

@@ -25,6 +25,7 @@ struct ApplyCellArgs {
 
 struct ApplyPrecArgs {
   int r;
+  const int* list;
   const int* n;
   const int* I;
   const int64_t* I_off;
@@ -36,6 +37,7 @@ struct ApplyPrecArgs {
 
 struct ApplySkelArgs {
   int nsk;
+  const int* list;
   const int* r;
   const int* kt;
   const int* S;
@@ -55,6 +57,7 @@ void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int
                    const double* val, int64_t N, cudaStream_t s);
 void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st, cudaStream_t s);
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s);
+void launch_prec_build(const LevelDev& lv, const PrecArgs& a, const int* list, int nbig, cudaStream_t s);
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s);
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s);
