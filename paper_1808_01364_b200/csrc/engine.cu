@@ -386,14 +386,14 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       const int nn = P.cell_n[t], bb = P.cell_b[t];
       P_off[t] = rec;
       rec += (int64_t)(nn + bb) * nn;
-      if (nn >= BIG_N) rec += (int64_t)nn * nn;   // identity rows -> L^-T for the GEMM apply
+      rec += (int64_t)nn * nn;   // identity rows -> L^-T for the GEMM replay
       U_off[t] = uacc;
       uacc += (int64_t)bb * bb;
       I_off[t] = G.off[P.interior[t]];
       B_off[t] = bacc;
       bacc += bb;
       cwork[t] = wacc;
-      wacc += nn + bb + (nn >= BIG_N ? nn : 0);
+      wacc += 2 * nn + bb;
       for (int64_t j = P.cell_nbr_off[t]; j < P.cell_nbr_off[t + 1]; ++j) {
         const int h = P.cell_nbr[j];
         nbr_w[j] = G.size(h);
@@ -1039,11 +1039,13 @@ struct BigApply {
         wt_h.push_back(t);
       }
     };
-    nbig = (int)L.h_big_cells.size();
+    std::vector<int> cells(P.interior.size());
+    for (size_t t = 0; t < cells.size(); ++t) cells[t] = (int)t;
+    nbig = (int)cells.size();
     // phase 0: Z = (L^-T)^T Y ; phase 1: W = X^T Z ; phase 2: Y -= X Xb ; phase 3: Z = L^-T Y
     for (int ph = 0; ph < 4; ++ph) {
       ph_off[ph] = (int64_t)wd_h.size();
-      for (int t : L.h_big_cells) {
+      for (int t : cells) {
         const int n = P.cell_n[t], b = P.cell_b[t];
         const double* Pp = rec + L.h_P_off[t];
         const double* XT = Pp + (int64_t)n * n;
@@ -1058,7 +1060,7 @@ struct BigApply {
       }
     }
     ph_off[4] = (int64_t)wd_h.size();
-    for (int t : L.h_big_cells) {
+    for (int t : cells) {
       const int n = P.cell_n[t], b = P.cell_b[t];
       isrc.push_back(L.h_I_off[t]);
       idst.push_back(L.h_cwork[t]);
@@ -1104,7 +1106,7 @@ struct BigApply {
 };
 
 static BigApply* big_apply(Factorization& F, LevelRT& L, int k) {
-  if (L.h_big_cells.empty()) return nullptr;
+  if (L.plan.interior.empty()) return nullptr;
   if (!L.bigap) L.bigap = std::make_shared<BigApply>();
   BigApply& b = *L.bigap;
   if (b.k != k || b.work != F.work.as<double>() || b.wbuf != F.wbuf.as<double>()) b.build(F, L, k);
@@ -1273,8 +1275,8 @@ static GemmReplay* gemm_replay(Factorization& F, LevelRT& L, int k) {
 
 static ApplyCellArgs cell_args(Factorization& F, LevelRT& L) {
   ApplyCellArgs a;
-  a.list = L.h_small_cells.size() == L.plan.interior.size() ? nullptr : L.d_small_cells.as<int>();
-  a.p = (int)L.h_small_cells.size();
+  a.list = nullptr;
+  a.p = 0;   // every cell is replayed by batched GEMMs (big_apply)
   a.n = L.c_n.as<int>();
   a.b = L.c_b.as<int>();
   a.I = L.mem.as<int>();

@@ -69,8 +69,10 @@ __global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus
       P[(int64_t)(n + c0 + r) * n + i] = S[e];
     }
   }
+  double* Id = P + (int64_t)(n + b) * n;   // identity rows: become L^-T (GEMM replay)
+  for (int64_t e = tid; e < (int64_t)n * n; e += NT) Id[e] = (e / n == e % n) ? 1.0 : 0.0;
   __syncthreads();
-  const int info = cta_potrf_panel(P, n + b, n, n, smem);
+  const int info = cta_potrf_panel(P, n + b + n, n, n, smem);
   if (info >= 0) {
     if (tid == 0) report_bad(st, t, info);
     return;
@@ -1422,6 +1424,28 @@ __global__ void k_apply_reduce(const int* dof, const int64_t* off, const int* ro
   x[(int64_t)dof[i] * k + c] = s;
 }
 
+// small block-Jacobi records: one warp per group, dense product with the stored L^-T
+__global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up) {
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wg >= a.r) return;
+  const int t = a.list ? a.list[wg] : wg;
+  const int n = a.n[t];
+  const int* I = a.I + a.I_off[t];
+  const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
+  double* Y = a.work + a.work_off[t] * k;
+  for (int e = lane; e < n * k; e += 32) {
+    const int i = e / k, c = e % k;
+    double s = 0.0;
+    if (up)   // y = L^-1 x = (L^-T)^T x, L^-T upper triangular
+      for (int j = 0; j <= i; ++j) s += LiT[(int64_t)j * n + i] * x[(int64_t)I[j] * k + c];
+    else      // y = L^-T x
+      for (int j = i; j < n; ++j) s += LiT[(int64_t)i * n + j] * x[(int64_t)I[j] * k + c];
+    Y[e] = s;
+  }
+  __syncwarp();
+  for (int e = lane; e < n * k; e += 32) x[(int64_t)I[e / k] * k + e % k] = Y[e];
+}
+
 __global__ void __launch_bounds__(NT) k_apply_prec(ApplyPrecArgs a, double* x, int k, int up) {
   extern __shared__ double smem[];
   const int t = a.list ? a.list[blockIdx.x] : blockIdx.x;
@@ -1693,7 +1717,7 @@ void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, co
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.r == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_apply_prec<<<a.r, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
+  k_apply_prec_tiny<<<(a.r * 32 + 255) / 256, 256, 0, s>>>(a, x, k, up ? 1 : 0);
 }
 void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.nsk == 0) return;
