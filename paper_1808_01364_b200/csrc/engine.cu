@@ -995,6 +995,17 @@ static void ensure_work(Factorization& F, int k) {
   }
 }
 
+// gather/scatter segments are split so that one warp moves at most ~1024 values
+static void push_seg(std::vector<int64_t>& src, std::vector<int64_t>& dst, std::vector<int>& len, int64_t s0,
+                     int64_t d0, int n, int k) {
+  const int step = std::max(1, 1024 / std::max(k, 1));
+  for (int r = 0; r < n; r += step) {
+    src.push_back(s0 + r);
+    dst.push_back(d0 + r);
+    len.push_back(std::min(step, n - r));
+  }
+}
+
 // GEMM replay of big cells: L^-T is stored below [L ; X^T] in the panel.
 struct BigApply {
   int k = -1;
@@ -1003,8 +1014,8 @@ struct BigApply {
   DBuf desc;                  // 4 phases of descriptors
   DBuf wd, wt;                // work lists (descriptor, row tile)
   int64_t ph_off[5] = {0, 0, 0, 0, 0};
-  DBuf gi_src, gi_dst, gi_len, sc_dst, gb_src, gb_dst, gb_len;
-  int nbig = 0;
+  DBuf gi_src, gi_dst, gi_len, sc_src, sc_dst, sc_len, gb_src, gb_dst, gb_len;
+  int nbig = 0, nseg_i = 0, nseg_b = 0;
   void build(Factorization& F, LevelRT& L, int kk) {
     k = kk;
     work = F.work.as<double>();
@@ -1060,16 +1071,18 @@ struct BigApply {
       }
     }
     ph_off[4] = (int64_t)wd_h.size();
+    std::vector<int64_t> ssrc;
+    std::vector<int> slen;
     for (int t : cells) {
       const int n = P.cell_n[t], b = P.cell_b[t];
-      isrc.push_back(L.h_I_off[t]);
-      idst.push_back(L.h_cwork[t]);
-      sdst.push_back(L.h_cwork[t] + n);
-      ilen.push_back(n);
-      bsrc.push_back(L.h_B_off[t]);
-      bdst.push_back(L.h_cwork[t] + 2 * n);
-      blen.push_back(b);
+      push_seg(isrc, idst, ilen, L.h_I_off[t], L.h_cwork[t], n, k);
+      push_seg(ssrc, sdst, slen, L.h_I_off[t], L.h_cwork[t] + n, n, k);
+      if (b > 0) push_seg(bsrc, bdst, blen, L.h_B_off[t], L.h_cwork[t] + 2 * n, b, k);
     }
+    nseg_i = (int)isrc.size();
+    nseg_b = (int)bsrc.size();
+    upload(sc_src, ssrc, s);
+    upload(sc_len, slen, s);
     upload(desc, d, s);
     upload(wd, wd_h, s);
     upload(wt, wt_h, s);
@@ -1086,21 +1099,21 @@ struct BigApply {
                  (int)(ph_off[ph + 1] - ph_off[ph]), s);
   }
   void up(LevelRT& L, double* x, cudaStream_t s) const {
-    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nseg_i, k,
                 false, s);
     phase(0, s);
     phase(1, s);
-    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), sc_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+    launch_rows(work, x, L.mem.as<int>(), sc_src.as<int64_t>(), sc_dst.as<int64_t>(), sc_len.as<int>(), nseg_i, k,
                 true, s);
   }
   void down(LevelRT& L, double* x, cudaStream_t s) const {
-    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nseg_i, k,
                 false, s);
-    launch_rows(work, x, L.c_B.as<int>(), gb_src.as<int64_t>(), gb_dst.as<int64_t>(), gb_len.as<int>(), nbig, k,
+    launch_rows(work, x, L.c_B.as<int>(), gb_src.as<int64_t>(), gb_dst.as<int64_t>(), gb_len.as<int>(), nseg_b, k,
                 false, s);
     phase(2, s);
     phase(3, s);
-    launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), sc_dst.as<int64_t>(), gi_len.as<int>(), nbig, k,
+    launch_rows(work, x, L.mem.as<int>(), sc_src.as<int64_t>(), sc_dst.as<int64_t>(), sc_len.as<int>(), nseg_i, k,
                 true, s);
   }
 };
@@ -1158,11 +1171,7 @@ struct GemmReplay {
         if (L.h_pn[t] >= APPLY_BIG) bigp.push_back((int)t);
     for (int dir = 0; dir < 2; ++dir) {
       int64_t o = seg_begin();
-      for (int t : bigp) {
-        src.push_back(L.h_pI_off[t]);
-        dst.push_back(L.h_pwork[t]);
-        len.push_back(L.h_pn[t]);
-      }
+      for (int t : bigp) push_seg(src, dst, len, L.h_pI_off[t], L.h_pwork[t], L.h_pn[t], k);
       add_step(dir, 0, o, 0);
       o = (int64_t)wdh.size();
       for (int t : bigp) {
@@ -1173,11 +1182,7 @@ struct GemmReplay {
       }
       add_step(dir, 2, o, 0);
       o = seg_begin();
-      for (int t : bigp) {
-        src.push_back(L.h_pI_off[t]);
-        dst.push_back(L.h_pwork[t] + L.h_pn[t]);
-        len.push_back(L.h_pn[t]);
-      }
+      for (int t : bigp) push_seg(src, dst, len, L.h_pI_off[t], L.h_pwork[t] + L.h_pn[t], L.h_pn[t], k);
       add_step(dir, 1, o, 0);
     }
     // ---- separators: records [L~ ; X~^T ; L~^-T] and T
@@ -1188,18 +1193,10 @@ struct GemmReplay {
     for (int dir = 0; dir < 2; ++dir) {
       const int which = 2 + dir;
       int64_t o = seg_begin();
-      for (int t : bigs) {
-        src.push_back(L.h_S_off[t]);
-        dst.push_back(L.h_awork[t]);
-        len.push_back(L.h_sr[t]);
-      }
+      for (int t : bigs) push_seg(src, dst, len, L.h_S_off[t], L.h_awork[t], L.h_sr[t], k);
       add_step(which, 0, o, 1);
       o = seg_begin();
-      for (int t : bigs) {
-        src.push_back(L.h_R_off[t]);
-        dst.push_back(L.h_awork[t] + L.h_sr[t]);
-        len.push_back(L.h_skt[t]);
-      }
+      for (int t : bigs) push_seg(src, dst, len, L.h_R_off[t], L.h_awork[t] + L.h_sr[t], L.h_skt[t], k);
       add_step(which, 0, o, 2);
       for (int ph = 0; ph < 3; ++ph) {
         o = (int64_t)wdh.size();
@@ -1225,18 +1222,10 @@ struct GemmReplay {
         add_step(which, 2, o, 0);
       }
       o = seg_begin();
-      for (int t : bigs) {
-        src.push_back(L.h_S_off[t]);
-        dst.push_back(L.h_awork[t]);
-        len.push_back(L.h_sr[t]);
-      }
+      for (int t : bigs) push_seg(src, dst, len, L.h_S_off[t], L.h_awork[t], L.h_sr[t], k);
       add_step(which, 1, o, 1);
       o = seg_begin();
-      for (int t : bigs) {
-        src.push_back(L.h_R_off[t]);
-        dst.push_back(L.h_awork[t] + L.h_sr[t] + L.h_skt[t]);
-        len.push_back(L.h_skt[t]);
-      }
+      for (int t : bigs) push_seg(src, dst, len, L.h_R_off[t], L.h_awork[t] + L.h_sr[t] + L.h_skt[t], L.h_skt[t], k);
       add_step(which, 1, o, 2);
     }
     cudaStream_t s = F.stream;

@@ -2,6 +2,7 @@
 //
 // One CTA per cell / group / block; all dense algebra through dla.cuh
 // (DMMA GEMM core). Reference semantics are cited per kernel.
+#include <algorithm>
 #include <atomic>
 #include <cfloat>
 #include <cstdio>
@@ -1256,14 +1257,16 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile) {
+__global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile,
+                                               int nwork) {
   extern __shared__ double smem[];
-  const GemmDesc d = desc[w_desc[blockIdx.x]];
-  const int i0 = SG_BM * w_tile[blockIdx.x];
-  const int M = min(SG_BM, d.M - i0);
-  if (M <= 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+  const GemmDesc d = desc[w_desc[w]];
+  const int i0 = SG_BM * w_tile[w];
+  const int M = min(SG_BM, d.M - i0);
+  if (M <= 0) continue;
   for (int j0 = 0; j0 < d.N; j0 += SG_BN) {
     const int N = min(SG_BN, d.N - j0);
     auto load_stage = [&](int st, int k0) {
@@ -1331,22 +1334,26 @@ __global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w
           *p = (d.beta == 0.0 ? 0.0 : d.beta * *p) + d.alpha * acc[y][z];
         }
       }
-  }
+  }  }
 }
 
-// gather / scatter of DOF rows for a list of index segments: Y[seg_off + e] <-> x[idx[e]]
+// gather / scatter of DOF rows for a list of index segments: Y[seg_dst + e] <-> x[idx[seg_src + e]]
+// (one warp per segment, grid-stride over segments)
 __global__ void k_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                        const int* seg_len, int nseg, int k, int to_x, int chunks) {
-  const int sgi = blockIdx.x / chunks, ch = blockIdx.x % chunks;
-  if (sgi >= nseg) return;
-  const int* id = idx + seg_src[sgi];
-  double* y = Y + seg_dst[sgi] * k;
-  const int64_t n = (int64_t)seg_len[sgi] * k;
-  for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < n; e += (int64_t)chunks * blockDim.x) {
-    double* px = x + (int64_t)id[e / k] * k + e % k;
-    if (to_x) *px = y[e];
-    else y[e] = *px;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int sgi = blockIdx.x * wpb + (threadIdx.x >> 5); sgi < nseg; sgi += gridDim.x * wpb) {
+    const int* id = idx + seg_src[sgi];
+    double* y = Y + seg_dst[sgi] * k;
+    const int64_t n = (int64_t)seg_len[sgi] * k;
+    for (int64_t e = lane; e < n; e += 32) {
+      double* px = x + (int64_t)id[e / k] * k + e % k;
+      if (to_x) *px = y[e];
+      else y[e] = *px;
+    }
   }
+  (void)chunks;
 }
 
 // ---------------------------------------------------------------------------
@@ -1684,14 +1691,15 @@ void launch_big_syrk(const BigArgs& a, cudaStream_t s) {
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
   if (!nwork) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_bgemm<<<nwork, NT, 2 * SG_STAGE * sizeof(double), s>>>(desc, w_desc, w_tile);
+  const int grid = std::min(nwork, 148 * 32);
+  k_bgemm<<<grid, NT, 2 * SG_STAGE * sizeof(double), s>>>(desc, w_desc, w_tile, nwork);
 }
 void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                  const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s) {
   if (!nseg) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const int chunks = 16;
-  k_rows<<<nseg * chunks, 256, 0, s>>>(Y, x, idx, seg_src, seg_dst, seg_len, nseg, k, to_x ? 1 : 0, chunks);
+  const int grid = std::min((nseg + 7) / 8, 148 * 16);
+  k_rows<<<grid, 256, 0, s>>>(Y, x, idx, seg_src, seg_dst, seg_len, nseg, k, to_x ? 1 : 0, 1);
 }
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s) {
   if (a.nsk == 0) return;
