@@ -857,10 +857,15 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       si.alloc(std::max<int64_t>(2 * slot_off[P.nwaves], 1) * sizeof(int), s);
       for (int w = 0; w < P.nwaves; ++w) {
         ka.order = d_small.as<int>() + small_off[w];
-        launch_skel_id(dv, ka, (int)(small_off[w + 1] - small_off[w]), s);
+        int64_t need = 0;
+        for (int64_t q = small_off[w]; q < small_off[w + 1]; ++q) {
+          const int t = small_list[q];
+          const int64_t kk = G.size(P.skeleton[t]);
+          need = std::max<int64_t>(need, std::max<int64_t>(rows_bound[t], 1) * kk + 4 * kk + 4);
+        }
+        launch_skel_id(dv, ka, (int)(small_off[w + 1] - small_off[w]), need, s);
         const int nl = (int)(large_off[w + 1] - large_off[w]);
         if (nl) {
-          launch_skel_gather(dv, ka, d_large.as<int>() + large_off[w], nl, s);
           TeamArgs ta;
           ta.nface = nl;
           ta.face = d_large.as<int>() + large_off[w];

@@ -350,7 +350,7 @@ __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s
   if (threadIdx.x == 0) sk.rank[s] = 0;
 }
 
-__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
+__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int smem_cap) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
   int* sint = reinterpret_cast<int*>(smem);  // scan scratch (first doubles are free here)
@@ -360,10 +360,12 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk) {
   const int k = lv.gsize[g];
   const int64_t gof = lv.goff[g];
   const int64_t ldw = skel_ldw(lv, sk, s);
-  double* W = sk.work + sk.work_off[s];
+  // A_{R,I} and its CPQR live in shared memory when they fit, else in the global workspace
+  const bool local = ldw * k + 4 * (int64_t)k + 4 <= smem_cap;
+  double* W = local ? smem + SMEM_DOUBLES : sk.work + sk.work_off[s];
   double* vn1 = W + (int64_t)k * ldw;
   double* vn2 = vn1 + k;
-  int* iw = sk.iwork + sk.iwork_off[s];
+  int* iw = local ? reinterpret_cast<int*>(vn2 + k) : sk.iwork + sk.iwork_off[s];
   int* perm = iw;
   int* sidx = iw + k;
   int* flag = iw + 2 * k;
@@ -492,7 +494,86 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
   int* inv = reinterpret_cast<int*>(vs + ta.vcap);   // k ints
   int* pos = inv + k;                                // k ints
   double* colbuf = vs + ta.vcap + k + 1;             // smem-resident owned columns (ld m)
-  const int m0 = __ldcg(sk.rows + s);
+  // ---- gather A_{R,I} across the team: CTA c flags a slice of candidate rows (alive, nonzero),
+  //      a team-wide prefix over the per-CTA counts places the kept rows (neighbour order kept)
+  int m0;
+  {
+    int64_t rows_bound = 0;
+    for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) rows_bound += lv.gsize[sk.nbr[q]];
+    const int64_t chunk = (rows_bound + P - 1) / P;
+    const int64_t r_lo = (int64_t)c * chunk, r_hi = min(rows_bound, r_lo + chunk);
+    int* sint = reinterpret_cast<int*>(smem + GEMM_OFF);
+    // pass 1: count kept rows of my slice
+    int mine = 0;
+    {
+      int64_t base = 0;
+      for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1] && base < r_hi; ++q) {
+        const int h = sk.nbr[q], kh = lv.gsize[h];
+        const int64_t lo = max(r_lo, base), hi = min(r_hi, base + kh);
+        if (lo < hi) {
+          const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+          const bool stored_gh = g < h;
+          const int* hm = lv.mem + lv.goff[h];
+          for (int64_t r0 = lo; r0 < hi; r0 += NT) {
+            const int r = (int)(r0 + tid - base);
+            int keep = 0;
+            if (r0 + tid < hi && sk.alive[hm[r]])
+              for (int cc = 0; cc < k; ++cc)
+                if ((stored_gh ? B[(int64_t)cc * kh + r] : B[(int64_t)r * k + cc]) != 0.0) {
+                  keep = 1;
+                  break;
+                }
+            int total;
+            cta_scan_flag(keep, sint, &total);
+            mine += total;
+          }
+        }
+        base += kh;
+      }
+    }
+    if (tid == 0) __stcg(slot_i + c, mine);
+    team_sync(hdr, P);
+    int before = 0, all = 0;
+    for (int q2 = 0; q2 < P; ++q2) {
+      const int v = __ldcg(slot_i + q2);
+      if (q2 < c) before += v;
+      all += v;
+    }
+    m0 = all;
+    // pass 2: write my kept rows at rows [before, before + mine)
+    {
+      int m = before;
+      int64_t base = 0;
+      for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1] && base < r_hi; ++q) {
+        const int h = sk.nbr[q], kh = lv.gsize[h];
+        const int64_t lo = max(r_lo, base), hi = min(r_hi, base + kh);
+        if (lo < hi) {
+          const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+          const bool stored_gh = g < h;
+          const int* hm = lv.mem + lv.goff[h];
+          for (int64_t r0 = lo; r0 < hi; r0 += NT) {
+            const int r = (int)(r0 + tid - base);
+            int keep = 0;
+            if (r0 + tid < hi && sk.alive[hm[r]])
+              for (int cc = 0; cc < k; ++cc)
+                if ((stored_gh ? B[(int64_t)cc * kh + r] : B[(int64_t)r * k + cc]) != 0.0) {
+                  keep = 1;
+                  break;
+                }
+            int total;
+            const int off = cta_scan_flag(keep, sint, &total);
+            if (keep)
+              for (int cc = 0; cc < k; ++cc)
+                __stcg(W + (int64_t)cc * ldw + m + off, stored_gh ? B[(int64_t)cc * kh + r] : B[(int64_t)r * k + cc]);
+            m += total;
+          }
+        }
+        base += kh;
+      }
+    }
+    if (c == 0 && tid == 0) sk.rows[s] = m0;
+    team_sync(hdr, P);
+  }
   if (m0 == 0) {
     if (c == 0) skel_all_redundant(lv, sk, s);
     return;
@@ -1621,10 +1702,14 @@ void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_prec_scale<<<a.nscale, NT, SMEM_BYTES, s>>>(lv, a);
 }
-void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, cudaStream_t s) {
+void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t need_doubles, cudaStream_t s) {
   if (count == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_skel_id<<<count, NT, SMEM_BYTES, s>>>(lv, a);
+  const int64_t cap_max = (225 * 1024) / 8 - SMEM_DOUBLES;   // leave room for static shared memory
+  const int cap = (int)std::min<int64_t>(need_doubles, cap_max);
+  const size_t bytes = SMEM_BYTES + (size_t)cap * sizeof(double);
+  cudaFuncSetAttribute(k_skel_id, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_skel_id<<<count, NT, bytes, s>>>(lv, a, cap);
 }
 void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces, int count, cudaStream_t s) {
   if (count == 0) return;
