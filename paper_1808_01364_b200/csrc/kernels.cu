@@ -451,6 +451,40 @@ __device__ __forceinline__ void team_sync(TeamHdr* h, int P) {
 
 constexpr int TCH = 16;      // owned columns updated together per pass
 
+// Copy jb (<= 8) columns of n rows between a global column block (ld gld, L1 bypassed: the
+// data is written by other CTAs of the team) and a packed shared-memory panel (ld n).
+// Loads of all columns are issued before any is consumed (16 in flight per thread).
+// VMASK: rows above the diagonal read as 0 and the diagonal as 1 (unit reflectors V).
+template <bool VMASK>
+__device__ __forceinline__ void panel_load(double* dst, const double* src, int64_t gld, int jb, int n) {
+  for (int r0 = 0; r0 < n; r0 += 2 * NT) {
+    double v[8][2];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int rr = r0 + u * NT + threadIdx.x;
+        double x = 0.0;
+        if (jj < jb && rr < n) {
+          if (!VMASK || rr > jj) x = __ldcg(src + (int64_t)jj * gld + rr);
+          else if (rr == jj) x = 1.0;
+        }
+        v[jj][u] = x;
+      }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int rr = r0 + u * NT + threadIdx.x;
+        if (jj < jb && rr < n) dst[(int64_t)jj * n + rr] = v[jj][u];
+      }
+  }
+}
+__device__ __forceinline__ void panel_store(double* dst, int64_t gld, const double* src, int jb, int n) {
+  for (int jj = 0; jj < jb; ++jj)
+    for (int rr = threadIdx.x; rr < n; rr += NT) __stcg(dst + (int64_t)jj * gld + rr, src[(int64_t)jj * n + rr]);
+}
+
 __device__ __forceinline__ int nloc_all(int k, int c, int P) { return c < k ? (k - c + P - 1) / P : 0; }
 constexpr int TOWN = 512;    // max owned columns per CTA (smem norms)
 
@@ -595,10 +629,7 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       const bool qprof = ta.prof && blockIdx.x == 0 && tid == 0;
       long long tq0 = qprof ? clock64() : 0;
       if (c == pi % P) {
-        for (int64_t e = tid; e < (int64_t)jb * ldp; e += NT) {
-          const int jj = (int)(e / ldp), rr = (int)(e % ldp);
-          Pn[e] = __ldcg(W + (int64_t)(j0 + jj) * ldw + j0 + rr);
-        }
+        panel_load<false>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
         __syncthreads();
         __shared__ double s_tau[8];
         for (int jj = 0; jj < jb; ++jj) {
@@ -654,16 +685,39 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
           __syncthreads();
         }
         // compact WY factor T (upper triangular): H_1 ... H_jb = I - V T V^T
+        // G = V^T V (strict upper part) in one pass over the rows: V_a(rr) = 0 above, 1 on the diagonal
         __shared__ double s_G[8][8];
-        for (int ab = warp; ab < jb * jb; ab += nw) {
-          const int a = ab / jb, b = ab % jb;
-          double x = 0.0;
-          if (a < b) {
-            for (int rr = b + lane; rr < ldp; rr += 32)
-              x += (rr == a ? 1.0 : Pn[(int64_t)a * ldp + rr]) * (rr == b ? 1.0 : Pn[(int64_t)b * ldp + rr]);
-            x = warp_sum(x);
+        __shared__ double s_Gp[8][28];
+        {
+          double gp[28];
+#pragma unroll
+          for (int q = 0; q < 28; ++q) gp[q] = 0.0;
+          for (int rr = 1 + tid; rr < ldp; rr += NT) {
+            double va[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+              va[a] = (a < jb && rr >= a) ? (rr == a ? 1.0 : Pn[(int64_t)a * ldp + rr]) : 0.0;
+            int q = 0;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+              for (int b2 = a + 1; b2 < 8; ++b2) gp[q++] += va[a] * va[b2];
           }
-          if (lane == 0) s_G[a][b] = x;
+#pragma unroll
+          for (int q = 0; q < 28; ++q) {
+            const double t2 = warp_sum(gp[q]);
+            if (lane == 0) s_Gp[warp][q] = t2;
+          }
+          __syncthreads();
+          if (tid < 64) {
+            const int a = tid / 8, b2 = tid % 8;
+            double x = 0.0;
+            if (a < b2) {
+              const int q = a * 8 - a * (a + 1) / 2 + (b2 - a - 1);
+              for (int ww = 0; ww < nw; ++ww) x += s_Gp[ww][q];
+            }
+            s_G[a][b2] = x;
+          }
         }
         __syncthreads();
         if (tid == 0) {
@@ -680,10 +734,7 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
           for (int a = 0; a < jb; ++a)
             for (int b = 0; b < jb; ++b) __stcg(qT + a * 8 + b, T[a][b]);
         }
-        for (int64_t e = tid; e < (int64_t)jb * ldp; e += NT) {
-          const int jj = (int)(e / ldp), rr = (int)(e % ldp);
-          __stcg(W + (int64_t)(j0 + jj) * ldw + j0 + rr, Pn[e]);
-        }
+        panel_store(W + (int64_t)j0 * ldw + j0, ldw, Pn, jb, ldp);
       }
       if (qprof) { const long long t1 = clock64(); ta.prof[14] += t1 - tq0; tq0 = t1; }
       team_sync(hdr, P);
@@ -692,10 +743,7 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       const int jstart = j0 + jb;
       const int tfirst = jstart <= c ? 0 : (jstart - c + P - 1) / P;
       if (tfirst < nloc_all(k, c, P)) {
-        for (int64_t e = tid; e < (int64_t)jb * ldp; e += NT) {
-          const int jj = (int)(e / ldp), rr = (int)(e % ldp);
-          Pn[e] = rr < jj ? 0.0 : (rr == jj ? 1.0 : __ldcg(W + (int64_t)(j0 + jj) * ldw + j0 + rr));
-        }
+        panel_load<true>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
         __shared__ double s_T[8][8];
         if (tid < 64) s_T[tid / 8][tid % 8] = (tid / 8 < jb && tid % 8 < jb) ? __ldcg(qT + tid) : 0.0;
         __syncthreads();
@@ -710,15 +758,42 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
           double w0[8], w1[8];
 #pragma unroll
           for (int a = 0; a < 8; ++a) w0[a] = w1[a] = 0.0;
-          for (int rr = tid; rr < ldp; rr += NT) {
-            const double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
+          // all of this thread's rows of both columns are loaded up front (one L2 round trip),
+          // kept in registers for the update below
+          constexpr int QR_NQ = 16;
+          double x0r[QR_NQ], x1r[QR_NQ];
+          const bool regs = ldp <= QR_NQ * NT;
+          if (regs) {
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
-              if (a < jb) {
-                const double va = Pn[(int64_t)a * ldp + rr];
-                w0[a] += va * x0;
-                w1[a] += va * x1;
+            for (int q = 0; q < QR_NQ; ++q) {
+              const int rr = tid + q * NT;
+              x0r[q] = rr < ldp ? __ldcg(cj0 + rr) : 0.0;
+              x1r[q] = rr < ldp ? __ldcg(cj1 + rr) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < QR_NQ; ++q) {
+              const int rr = tid + q * NT;
+              if (rr < ldp) {
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+                  if (a < jb) {
+                    const double va = Pn[(int64_t)a * ldp + rr];
+                    w0[a] += va * x0r[q];
+                    w1[a] += va * x1r[q];
+                  }
               }
+            }
+          } else {
+            for (int rr = tid; rr < ldp; rr += NT) {
+              const double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
+#pragma unroll
+              for (int a = 0; a < 8; ++a)
+                if (a < jb) {
+                  const double va = Pn[(int64_t)a * ldp + rr];
+                  w0[a] += va * x0;
+                  w1[a] += va * x1;
+                }
+            }
           }
 #pragma unroll
           for (int a = 0; a < 8; ++a) {
@@ -741,17 +816,36 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
             s_z[q2][b] = x;
           }
           __syncthreads();
-          for (int rr = tid; rr < ldp; rr += NT) {
-            double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
+          if (regs) {
 #pragma unroll
-            for (int b = 0; b < 8; ++b)
-              if (b < jb) {
-                const double vb = Pn[(int64_t)b * ldp + rr];
-                x0 -= vb * s_z[0][b];
-                x1 -= vb * s_z[1][b];
+            for (int q = 0; q < QR_NQ; ++q) {
+              const int rr = tid + q * NT;
+              if (rr < ldp) {
+                double x0 = x0r[q], x1 = x1r[q];
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                  if (b < jb) {
+                    const double vb = Pn[(int64_t)b * ldp + rr];
+                    x0 -= vb * s_z[0][b];
+                    x1 -= vb * s_z[1][b];
+                  }
+                __stcg(cj0 + rr, x0);
+                if (nt == 2) __stcg(cj1 + rr, x1);
               }
-            __stcg(cj0 + rr, x0);
-            if (nt == 2) __stcg(cj1 + rr, x1);
+            }
+          } else {
+            for (int rr = tid; rr < ldp; rr += NT) {
+              double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
+#pragma unroll
+              for (int b = 0; b < 8; ++b)
+                if (b < jb) {
+                  const double vb = Pn[(int64_t)b * ldp + rr];
+                  x0 -= vb * s_z[0][b];
+                  x1 -= vb * s_z[1][b];
+                }
+              __stcg(cj0 + rr, x0);
+              if (nt == 2) __stcg(cj1 + rr, x1);
+            }
           }
           __syncthreads();
         }
@@ -780,10 +874,8 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
     inv[j] = j;
     pos[j] = j;
   }
-  for (int64_t e = tid; e < (int64_t)ns * m; e += NT) {
-    const int t = (int)(e / m), r = (int)(e % m);
-    colbuf[e] = __ldcg(W + (int64_t)(c + P * t) * ldw + r);
-  }
+  for (int t0 = 0; t0 < ns; t0 += 8)
+    panel_load<false>(colbuf + (int64_t)t0 * m, W + (int64_t)(c + P * t0) * ldw, (int64_t)P * ldw, min(8, ns - t0), m);
   __syncthreads();
   for (int t = warp; t < nloc; t += nw) {
     double a = 0.0;
@@ -1721,7 +1813,13 @@ static size_t team_smem(int vcap, int kmax, int colcap) {
 }
 int team_colcap(int vcap, int kmax) {
   // fill the CTA's shared memory (one team CTA per SM) with owned columns
-  const long long avail = (227 * 1024 - 14 * 1024) / 8 - SMEM_DOUBLES - vcap - kmax - 1;
+  static long long static_bytes = -1;
+  if (static_bytes < 0) {
+    cudaFuncAttributes fa{};
+    static_bytes = cudaFuncGetAttributes(&fa, k_skel_team) == cudaSuccess ? (long long)fa.sharedSizeBytes : 16 * 1024;
+  }
+  // 227 KB per block minus the static arrays and 1 KB the runtime reserves
+  const long long avail = (227 * 1024 - static_bytes - 1024) / 8 - SMEM_DOUBLES - vcap - kmax - 1;
   return avail > 0 ? (int)avail : 0;
 }
 int team_blocks_per_sm(int vcap, int kmax, int colcap) {
