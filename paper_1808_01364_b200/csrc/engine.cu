@@ -360,6 +360,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   std::vector<uint8_t> alive_mem;  // survivors of the previous level, per member position
   for (int lev = 0; lev <= sp.L; ++lev) {
     auto tp = clk::now();
+    const auto t_level0 = tp;
     F->levels.push_back(std::make_unique<LevelRT>());
     LevelRT& L = *F->levels.back();
     LevelRT* prev = lev > 0 ? F->levels[lev - 1].get() : nullptr;
@@ -498,6 +499,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.h_awork = awork;
     L.rec_doubles = rec;
     plan_ms += ms_since(tp);
+    L.t_ms[5] += ms_since(tp);
     // ---------------- device structures ----------------
     DBG("level %d: rec=%lld", lev, (long long)rec);
     upload_structure(L, s);
@@ -531,11 +533,42 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       ra.nbh = L.bh.as<int>();
       ra.nboff = L.boff.as<int64_t>();
       ra.ngoff = L.goff.as<int64_t>();
-      DBuf sg, spos;
+      DBuf sg, spos, sloc, slo, sl, wb, wr, wn;
       upload(sg, G.src_group, s);
       upload(spos, G.src_pos, s);
+      upload(sloc, G.src_local, s);
+      upload(slo, G.srcl_off, s);
+      upload(sl, G.srcl, s);
       ra.nsrc_group = sg.as<int>();
       ra.nsrc_pos = spos.as<int>();
+      ra.nsrc_local = sloc.as<int>();
+      ra.nsrcl_off = slo.as<int64_t>();
+      ra.nsrcl = sl.as<int>();
+      {
+        // row chunks of ~8K elements (at least one row per warp)
+        std::vector<int> wbh, wrh, wnh;
+        int cap = 1;
+        for (size_t b = 0; b < P.pat.bg.size(); ++b) {
+          const int gg = P.pat.bg[b], hh = P.pat.bh[b];
+          const int rows = G.size(gg), cols = G.size(hh);
+          cap = std::max<int>(cap, (int)((G.srcl_off[gg + 1] - G.srcl_off[gg]) * (G.srcl_off[hh + 1] - G.srcl_off[hh])));
+          const int step = std::max(8, 8192 / std::max(cols, 1));
+          for (int r0 = 0; r0 < rows; r0 += step) {
+            wbh.push_back((int)b);
+            wrh.push_back(r0);
+            wnh.push_back(std::min(step, rows - r0));
+          }
+        }
+        upload(wb, wbh, s);
+        upload(wr, wrh, s);
+        upload(wn, wnh, s);
+        if (cap > 12000) throw std::runtime_error("repack: too many source groups per block pair");
+        ra.nwork = (int)wbh.size();
+        ra.tab_cap = cap;
+        ra.w_blk = wb.as<int>();
+        ra.w_row0 = wr.as<int>();
+        ra.w_nrow = wn.as<int>();
+      }
       ra.npool = L.pool.as<double>();
       ra.opool = prev->pool.as<double>();
       ra.oboff = prev->boff.as<int64_t>();
@@ -959,7 +992,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       upload(L.d_apply_small_pr, small_pr, s);
     }
     plan_ms += ms_since(tp);
+    L.t_ms[5] += ms_since(tp);
     DBG("level %d: next-level inputs ready", lev);
+    L.t_wall_ms = ms_since(t_level0);
     if (timing) {
       CK(cudaEventSynchronize(ev[10]));
       float a;
@@ -1530,7 +1565,7 @@ std::string Factorization::stats_json() const {
       << ",\"sep_m_mean\":" << L.sep_m_mean << ",\"sep_m_max\":" << L.sep_m_max << ",\"n_large\":" << L.n_large
       << ",\"team_P_mean\":" << L.team_P_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
       << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
-      << L.t_ms[4] << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]
+      << L.t_ms[4] << ",\"t_plan_ms\":" << L.t_ms[5] << ",\"t_wall_ms\":" << L.t_wall_ms << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]
       << "," << L.fl[2] << "," << L.fl[3] << "," << L.fl[4] << "],\"bytes\":[" << L.by[0] << "," << L.by[1] << ","
       << L.by[2] << "," << L.by[3] << "," << L.by[4] << "]}";
   }

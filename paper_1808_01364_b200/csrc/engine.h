@@ -90,7 +90,8 @@ struct LevelRT {
   std::vector<int> h_rank;
   int64_t skel_work_unit = 0;
   // stats
-  double t_ms[6] = {0, 0, 0, 0, 0, 0};
+  double t_ms[6] = {0, 0, 0, 0, 0, 0};   // repack, eliminate, precondition, id, skel update, host plan
+  double t_wall_ms = 0;
   // algorithmic work per stage (0 repack, 1 eliminate+schur, 2 precondition, 3 id, 4 skel update)
   double fl[6] = {0, 0, 0, 0, 0, 0}, by[6] = {0, 0, 0, 0, 0, 0};
   DBuf s_rows;

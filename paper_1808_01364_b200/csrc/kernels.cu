@@ -1532,25 +1532,47 @@ __global__ void k_rows(double* Y, double* x, const int* idx, const int64_t* seg_
 // ---------------------------------------------------------------------------
 // Level transition: carry the surviving live matrix into the next grouping.
 // ---------------------------------------------------------------------------
+// One CTA per row chunk of a new block. Every (source group of G) x (source group of H) pair
+// resolves to an old block (or none) once, in a shared-memory table; rows then run per warp
+// and columns per lane.
+struct RepackEnt {
+  long long base;   // old block offset, -1: no block (zero)
+  int rs, cs;       // element (pi, pj) at base + pi*rs + pj*cs
+};
 __global__ void __launch_bounds__(NT) k_repack(RepackArgs ra) {
-  const int b = blockIdx.x;
+  extern __shared__ double smem[];
+  RepackEnt* tab = reinterpret_cast<RepackEnt*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  const int b = ra.w_blk[blockIdx.x], row0 = ra.w_row0[blockIdx.x], nrow = ra.w_nrow[blockIdx.x];
   const int G = ra.nbg[b], H = ra.nbh[b];
   const int64_t oG = ra.ngoff[G], oH = ra.ngoff[H];
-  const int rows = (int)(ra.ngoff[G + 1] - oG), cols = (int)(ra.ngoff[H + 1] - oH);
-  double* dst = ra.npool + ra.nboff[b];
-  for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += NT) {
-    const int i = (int)(e / cols), j = (int)(e % cols);
-    const int og = ra.nsrc_group[oG + i], pi = ra.nsrc_pos[oG + i];
-    const int oh = ra.nsrc_group[oH + j], pj = ra.nsrc_pos[oH + j];
-    double v = 0.0;
+  const int cols = (int)(ra.ngoff[H + 1] - oH);
+  const int64_t sG = ra.nsrcl_off[G], sH = ra.nsrcl_off[H];
+  const int nH = (int)(ra.nsrcl_off[H + 1] - sH);
+  const int nt = (int)(ra.nsrcl_off[G + 1] - sG) * nH;
+  for (int e = tid; e < nt; e += NT) {
+    const int og = ra.nsrcl[sG + e / nH], oh = ra.nsrcl[sH + e % nH];
+    RepackEnt t{-1, 0, 0};
     if (og <= oh) {
       const int blk = find_blk(ra.oadj_off, ra.oadj_nbr, ra.oadj_blk, og, oh);
-      if (blk >= 0) v = ra.opool[ra.oboff[blk] + (int64_t)pi * ra.ogsize[oh] + pj];
+      if (blk >= 0) t = RepackEnt{(long long)ra.oboff[blk], ra.ogsize[oh], 1};
     } else {
       const int blk = find_blk(ra.oadj_off, ra.oadj_nbr, ra.oadj_blk, oh, og);
-      if (blk >= 0) v = ra.opool[ra.oboff[blk] + (int64_t)pj * ra.ogsize[og] + pi];
+      if (blk >= 0) t = RepackEnt{(long long)ra.oboff[blk], 1, ra.ogsize[og]};
     }
-    dst[e] = v;
+    tab[e] = t;
+  }
+  __syncthreads();
+  double* dst = ra.npool + ra.nboff[b];
+  for (int i = row0 + warp; i < row0 + nrow; i += nw) {
+    const RepackEnt* trow = tab + ra.nsrc_local[oG + i] * nH;
+    const int64_t pi = ra.nsrc_pos[oG + i];
+    double* drow = dst + (int64_t)i * cols;
+    for (int j = lane; j < cols; j += 32) {
+      const RepackEnt t = trow[ra.nsrc_local[oH + j]];
+      const int64_t pj = ra.nsrc_pos[oH + j];
+      drow[j] = t.base >= 0 ? __ldg(ra.opool + t.base + pi * t.rs + pj * t.cs) : 0.0;
+    }
   }
 }
 
@@ -1892,7 +1914,9 @@ void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cu
 void launch_repack(const RepackArgs& a, cudaStream_t s) {
   if (a.nblk == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_repack<<<a.nblk, NT, 0, s>>>(a);
+  const size_t bytes = (size_t)a.tab_cap * sizeof(RepackEnt);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_repack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_repack<<<a.nwork, NT, bytes, s>>>(a);
 }
 void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.p == 0) return;

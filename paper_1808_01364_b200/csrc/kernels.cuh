@@ -111,6 +111,15 @@ struct TeamArgs {
 
 struct RepackArgs {
   int nblk;
+  // work items: row chunks of new blocks
+  int nwork;
+  const int* w_blk;
+  const int* w_row0;
+  const int* w_nrow;
+  int tab_cap;                  // max (#source groups of G) x (#source groups of H)
+  const int* nsrc_local;        // per new member: index into its group's source list
+  const int64_t* nsrcl_off;     // per new group: range of distinct source groups
+  const int* nsrcl;
   // new level
   const int* nbg;
   const int* nbh;

@@ -209,6 +209,9 @@ Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_
   g.mem.resize(total);
   g.src_group.resize(total);
   g.src_pos.resize(total);
+  g.src_local.resize(total);
+  g.srcl_off.assign(gsrc_off.begin(), gsrc_off.end());
+  g.srcl.assign(order.begin(), order.end());
 #pragma omp parallel
   {
     std::vector<std::tuple<int, int, int>> seg;
@@ -218,13 +221,14 @@ Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_
       for (int64_t q = gsrc_off[G0]; q < gsrc_off[G0 + 1]; ++q) {
         const int pg = order[q];
         for (int64_t p = prev.off[pg]; p < prev.off[pg + 1]; ++p)
-          if (alive[p]) seg.emplace_back(prev.mem[p], pg, (int)(p - prev.off[pg]));
+          if (alive[p]) seg.emplace_back(prev.mem[p], (int)(q - gsrc_off[G0]), (int)(p - prev.off[pg]));
       }
       std::sort(seg.begin(), seg.end());
       int64_t o = g.off[G0];
       for (auto& t : seg) {
         g.mem[o] = std::get<0>(t);
-        g.src_group[o] = std::get<1>(t);
+        g.src_local[o] = std::get<1>(t);
+        g.src_group[o] = order[gsrc_off[G0] + std::get<1>(t)];
         g.src_pos[o] = std::get<2>(t);
         ++o;
       }

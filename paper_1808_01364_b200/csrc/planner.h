@@ -32,6 +32,9 @@ struct Groups {
   // previous level and the member's position inside that source's full member list
   std::vector<int> src_group;
   std::vector<int> src_pos;
+  std::vector<int> src_local;      // index of src_group in the new group's source list
+  std::vector<int64_t> srcl_off;    // G+1: distinct source groups of each new group
+  std::vector<int> srcl;
   int size(int g) const { return (int)(off[g + 1] - off[g]); }
   bool is_sep(int g, int dim) const { return kind[g] == 1; }
 };
