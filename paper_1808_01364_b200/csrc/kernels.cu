@@ -295,42 +295,127 @@ __device__ int cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double*
   return mn;
 }
 
-// Gather A_{R,I} of skeleton s into W (column-major, ld = rows bound): alive rows of every
-// coupled group, only rows with a nonzero entry. Returns m (all threads).
-__device__ int skel_gather(const LevelDev& lv, const SkelArgs& sk, int s, double* W, int64_t ldw, int* sint) {
-  const int tid = threadIdx.x;
-  const int g = sk.groups[s];
-  const int k = lv.gsize[g];
-  int m = 0;
-  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) {
-    const int h = sk.nbr[q], kh = lv.gsize[h];
-    const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
-    const bool stored_gh = g < h;   // block(g,h): |g| x |h|, else block(h,g): |h| x |g|
-    const int* hm = lv.mem + lv.goff[h];
-    for (int r0 = 0; r0 < kh; r0 += NT) {
-      const int r = r0 + tid;
-      int keep = 0;
-      if (r < kh && sk.alive[hm[r]]) {
-        for (int c = 0; c < k; ++c) {
-          const double v = stored_gh ? B[(int64_t)c * kh + r] : B[(int64_t)r * k + c];
-          if (v != 0.0) {
-            keep = 1;
-            break;
-          }
-        }
-      }
-      int total;
-      const int off = cta_scan_flag(keep, sint, &total);
-      if (keep) {
-        const int row = m + off;
-        for (int c = 0; c < k; ++c)
-          W[(int64_t)c * ldw + row] = stored_gh ? B[(int64_t)c * kh + r] : B[(int64_t)r * k + c];
-      }
-      m += total;
+// ---- coupling-row gather in 32-row chunks -------------------------------------------------
+// The candidate rows of A_{R,I} (alive members of every coupled group) are cut into
+// chunks of 32 rows of one neighbour group (neighbours in order, ceil(|h|/32) chunks each).
+// A warp computes a chunk's keep mask (row alive and with a nonzero in A_{h,I}) from independent
+// coalesced loads; a warp scan of the popcounts places the kept rows; a second sweep copies them.
+__device__ __forceinline__ int skel_nchunks(const LevelDev& lv, const SkelArgs& sk, int s) {
+  int n = 0;
+  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) n += (lv.gsize[sk.nbr[q]] + 31) >> 5;
+  return n;
+}
+struct ChunkCursor {
+  int64_t q;
+  int base;   // first chunk of neighbour q
+  __device__ void locate(const LevelDev& lv, const SkelArgs& sk, int ch) {   // ch non-decreasing
+    for (;;) {
+      const int n = (lv.gsize[sk.nbr[q]] + 31) >> 5;
+      if (ch < base + n) return;
+      base += n;
+      ++q;
     }
   }
-  __syncthreads();
-  return m;
+};
+__device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArgs& sk, int g, int k, int64_t q,
+                                               int r0) {
+  const int lane = threadIdx.x & 31;
+  const int h = sk.nbr[q], kh = lv.gsize[h];
+  const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+  const int r = r0 + lane;
+  bool nz = false;
+  if (g < h) {   // block (g,h) is |g| x |h|: column r of it, lanes along rows (coalesced)
+    if (r < kh) {
+      const double* p = B + r;
+      int c = 0;
+      for (; c + 8 <= k; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(c + u) * kh];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nz |= v[u] != 0.0;
+      }
+      for (; c < k; ++c) nz |= p[(int64_t)c * kh] != 0.0;
+    }
+  } else {       // block (h,g) is |h| x |g|: rows r0..r0+31 are contiguous, lanes along columns
+    const int nr = min(32, kh - r0);
+    const double* p = B + (int64_t)r0 * k;
+    for (int rr = 0; rr < nr; ++rr) {
+      bool any = false;
+      for (int c = lane; c < k; c += 32) any |= p[(int64_t)rr * k + c] != 0.0;
+      if (__any_sync(0xffffffffu, any) && lane == rr) nz = true;
+    }
+  }
+  const bool alive = r < kh && sk.alive[lv.mem[lv.goff[h] + r]];
+  return __ballot_sync(0xffffffffu, nz && alive);
+}
+__device__ __forceinline__ void chunk_copy(const LevelDev& lv, const SkelArgs& sk, int g, int k, int64_t q, int r0,
+                                           unsigned mask, double* W, int64_t ldw, int row0) {
+  const int lane = threadIdx.x & 31;
+  const int h = sk.nbr[q], kh = lv.gsize[h];
+  const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+  if (g < h) {
+    if ((mask >> lane) & 1u) {
+      const int row = row0 + __popc(mask & ((1u << lane) - 1u));
+      const double* p = B + r0 + lane;
+      for (int c = 0; c < k; ++c) W[(int64_t)c * ldw + row] = p[(int64_t)c * kh];
+    }
+  } else {
+    int row = row0;
+    while (mask) {
+      const int rr = __ffs(mask) - 1;
+      mask &= mask - 1u;
+      const double* p = B + (int64_t)(r0 + rr) * k;
+      for (int c = lane; c < k; c += 32) W[(int64_t)c * ldw + row] = p[c];
+      ++row;
+    }
+  }
+}
+// Chunks [ch_lo, ch_hi) of separator s: with COPY, kept rows go to W rows base, base+1, ...
+// Returns the number of kept rows (all threads). smem: 2*cap ints.
+template <bool COPY>
+__device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, int s, int ch_lo, int ch_hi, double* W,
+                             int64_t ldw, int base, int* sbuf, int cap) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  const int g = sk.groups[s], k = lv.gsize[g];
+  unsigned* smask = reinterpret_cast<unsigned*>(sbuf);
+  int* spre = sbuf + cap;
+  __shared__ int s_tot;
+  int total = 0;
+  ChunkCursor cur{sk.nbr_off[s], 0}, cur2{sk.nbr_off[s], 0};
+  for (int b0 = ch_lo; b0 < ch_hi; b0 += cap) {
+    const int nb = min(cap, ch_hi - b0);
+    for (int i = warp; i < nb; i += nw) {
+      cur.locate(lv, sk, b0 + i);
+      const unsigned msk = chunk_mask(lv, sk, g, k, cur.q, 32 * (b0 + i - cur.base));
+      if (lane == 0) smask[i] = msk;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int run = 0;
+      for (int i0 = 0; i0 < nb; i0 += 32) {
+        const int v = i0 + lane < nb ? __popc(smask[i0 + lane]) : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (i0 + lane < nb) spre[i0 + lane] = run + inc - v;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) s_tot = run;
+    }
+    __syncthreads();
+    if (COPY)
+      for (int i = warp; i < nb; i += nw) {
+        cur2.locate(lv, sk, b0 + i);
+        chunk_copy(lv, sk, g, k, cur2.q, 32 * (b0 + i - cur2.base), smask[i], W, ldw, base + total + spre[i]);
+      }
+    total += s_tot;
+    __syncthreads();
+  }
+  return total;
 }
 
 __device__ __forceinline__ int64_t skel_ldw(const LevelDev& lv, const SkelArgs& sk, int s) {
@@ -369,7 +454,7 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
   int* perm = iw;
   int* sidx = iw + k;
   int* flag = iw + 2 * k;
-  const int m = skel_gather(lv, sk, s, W, ldw, sint);
+  const int m = gather_chunks<true>(lv, sk, s, 0, skel_nchunks(lv, sk, s), W, ldw, 0, sint, 512);
   if (tid == 0) sk.rows[s] = m;
   uint8_t* red = sk.red + gof;
   if (m == 0) {
@@ -412,16 +497,6 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
     if (flag[j]) sk.alive[lv.mem[gof + j]] = 0;
   }
   if (tid == 0) sk.rank[s] = r;
-}
-
-// Large separators: gather only (one CTA per face); the team kernel does the CPQR.
-__global__ void __launch_bounds__(NT) k_skel_gather(LevelDev lv, SkelArgs sk, const int* faces) {
-  extern __shared__ double smem[];
-  const int s = faces[blockIdx.x];
-  const int64_t ldw = skel_ldw(lv, sk, s);
-  double* W = sk.work + sk.work_off[s];
-  const int m = skel_gather(lv, sk, s, W, ldw, reinterpret_cast<int*>(smem));
-  if (threadIdx.x == 0) sk.rows[s] = m;
 }
 
 // ---------------------------------------------------------------------------
@@ -528,43 +603,15 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
   int* inv = reinterpret_cast<int*>(vs + ta.vcap);   // k ints
   int* pos = inv + k;                                // k ints
   double* colbuf = vs + ta.vcap + k + 1;             // smem-resident owned columns (ld m)
-  // ---- gather A_{R,I} across the team: CTA c flags a slice of candidate rows (alive, nonzero),
-  //      a team-wide prefix over the per-CTA counts places the kept rows (neighbour order kept)
+  // ---- gather A_{R,I} across the team: CTA c takes a contiguous range of 32-row chunks; a
+  //      team-wide prefix over the per-CTA kept counts places its rows (neighbour order kept)
   int m0;
   {
-    int64_t rows_bound = 0;
-    for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) rows_bound += lv.gsize[sk.nbr[q]];
-    const int64_t chunk = (rows_bound + P - 1) / P;
-    const int64_t r_lo = (int64_t)c * chunk, r_hi = min(rows_bound, r_lo + chunk);
     int* sint = reinterpret_cast<int*>(smem + GEMM_OFF);
-    // pass 1: count kept rows of my slice
-    int mine = 0;
-    {
-      int64_t base = 0;
-      for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1] && base < r_hi; ++q) {
-        const int h = sk.nbr[q], kh = lv.gsize[h];
-        const int64_t lo = max(r_lo, base), hi = min(r_hi, base + kh);
-        if (lo < hi) {
-          const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
-          const bool stored_gh = g < h;
-          const int* hm = lv.mem + lv.goff[h];
-          for (int64_t r0 = lo; r0 < hi; r0 += NT) {
-            const int r = (int)(r0 + tid - base);
-            int keep = 0;
-            if (r0 + tid < hi && sk.alive[hm[r]])
-              for (int cc = 0; cc < k; ++cc)
-                if ((stored_gh ? B[(int64_t)cc * kh + r] : B[(int64_t)r * k + cc]) != 0.0) {
-                  keep = 1;
-                  break;
-                }
-            int total;
-            cta_scan_flag(keep, sint, &total);
-            mine += total;
-          }
-        }
-        base += kh;
-      }
-    }
+    const int nch = skel_nchunks(lv, sk, s);
+    const int per = (nch + P - 1) / P;
+    const int ch_lo = min(nch, c * per), ch_hi = min(nch, ch_lo + per);
+    const int mine = gather_chunks<false>(lv, sk, s, ch_lo, ch_hi, W, ldw, 0, sint, 512);
     if (tid == 0) __stcg(slot_i + c, mine);
     team_sync(hdr, P);
     int before = 0, all = 0;
@@ -574,37 +621,7 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
       all += v;
     }
     m0 = all;
-    // pass 2: write my kept rows at rows [before, before + mine)
-    {
-      int m = before;
-      int64_t base = 0;
-      for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1] && base < r_hi; ++q) {
-        const int h = sk.nbr[q], kh = lv.gsize[h];
-        const int64_t lo = max(r_lo, base), hi = min(r_hi, base + kh);
-        if (lo < hi) {
-          const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
-          const bool stored_gh = g < h;
-          const int* hm = lv.mem + lv.goff[h];
-          for (int64_t r0 = lo; r0 < hi; r0 += NT) {
-            const int r = (int)(r0 + tid - base);
-            int keep = 0;
-            if (r0 + tid < hi && sk.alive[hm[r]])
-              for (int cc = 0; cc < k; ++cc)
-                if ((stored_gh ? B[(int64_t)cc * kh + r] : B[(int64_t)r * k + cc]) != 0.0) {
-                  keep = 1;
-                  break;
-                }
-            int total;
-            const int off = cta_scan_flag(keep, sint, &total);
-            if (keep)
-              for (int cc = 0; cc < k; ++cc)
-                __stcg(W + (int64_t)cc * ldw + m + off, stored_gh ? B[(int64_t)cc * kh + r] : B[(int64_t)r * k + cc]);
-            m += total;
-          }
-        }
-        base += kh;
-      }
-    }
+    gather_chunks<true>(lv, sk, s, ch_lo, ch_hi, W, ldw, before, sint, 512);
     if (c == 0 && tid == 0) sk.rows[s] = m0;
     team_sync(hdr, P);
   }
@@ -1550,6 +1567,29 @@ __global__ void __launch_bounds__(NT) k_repack(RepackArgs ra) {
   const int64_t sG = ra.nsrcl_off[G], sH = ra.nsrcl_off[H];
   const int nH = (int)(ra.nsrcl_off[H + 1] - sH);
   const int nt = (int)(ra.nsrcl_off[G + 1] - sG) * nH;
+  double* dst = ra.npool + ra.nboff[b];
+  if ((int64_t)nt * 8 > (int64_t)nrow * cols) {
+    // small chunk: resolve the old block per element
+    for (int i = row0 + warp; i < row0 + nrow; i += nw) {
+      const int og = ra.nsrcl[sG + ra.nsrc_local[oG + i]];
+      const int64_t pi = ra.nsrc_pos[oG + i];
+      double* drow = dst + (int64_t)i * cols;
+      for (int j = lane; j < cols; j += 32) {
+        const int oh = ra.nsrcl[sH + ra.nsrc_local[oH + j]];
+        const int64_t pj = ra.nsrc_pos[oH + j];
+        double v = 0.0;
+        if (og <= oh) {
+          const int blk = find_blk(ra.oadj_off, ra.oadj_nbr, ra.oadj_blk, og, oh);
+          if (blk >= 0) v = __ldg(ra.opool + ra.oboff[blk] + pi * ra.ogsize[oh] + pj);
+        } else {
+          const int blk = find_blk(ra.oadj_off, ra.oadj_nbr, ra.oadj_blk, oh, og);
+          if (blk >= 0) v = __ldg(ra.opool + ra.oboff[blk] + pj * ra.ogsize[og] + pi);
+        }
+        drow[j] = v;
+      }
+    }
+    return;
+  }
   for (int e = tid; e < nt; e += NT) {
     const int og = ra.nsrcl[sG + e / nH], oh = ra.nsrcl[sH + e % nH];
     RepackEnt t{-1, 0, 0};
@@ -1563,7 +1603,6 @@ __global__ void __launch_bounds__(NT) k_repack(RepackArgs ra) {
     tab[e] = t;
   }
   __syncthreads();
-  double* dst = ra.npool + ra.nboff[b];
   for (int i = row0 + warp; i < row0 + nrow; i += nw) {
     const RepackEnt* trow = tab + ra.nsrc_local[oG + i] * nH;
     const int64_t pi = ra.nsrc_pos[oG + i];
@@ -1824,11 +1863,6 @@ void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t ne
   const size_t bytes = SMEM_BYTES + (size_t)cap * sizeof(double);
   cudaFuncSetAttribute(k_skel_id, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_skel_id<<<count, NT, bytes, s>>>(lv, a, cap);
-}
-void launch_skel_gather(const LevelDev& lv, const SkelArgs& a, const int* faces, int count, cudaStream_t s) {
-  if (count == 0) return;
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_skel_gather<<<count, NT, SMEM_BYTES, s>>>(lv, a, faces);
 }
 static size_t team_smem(int vcap, int kmax, int colcap) {
   return SMEM_BYTES + ((size_t)vcap + kmax + 1 + colcap) * sizeof(double);
