@@ -305,12 +305,14 @@ static long long* team_prof_buffer() {
   if (on < 0) {
     on = getenv("PHIF_TEAM_PROF") ? 1 : 0;
     if (on) {
-      cudaMallocManaged(&buf, 16 * sizeof(long long));
-      for (int i = 0; i < 16; ++i) buf[i] = 0;
+      cudaMallocManaged(&buf, 32 * sizeof(long long));
+      for (int i = 0; i < 32; ++i) buf[i] = 0;
       atexit([] {
         cudaDeviceSynchronize();
         fprintf(stderr, "[phif] team phases CTA0 (Mcycles): argmax+publish %.1f sync %.1f reflector %.1f pass1(smem) %.1f pass1(L2) %.1f pass2(smem) %.1f pass2(L2) %.1f | steps %lld | QR %.1f [panel %.1f update %.1f syncs %.1f] CPQR %.1f finish %.1f\n",
                 buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6, buf[8], buf[11] / 1e6, buf[14] / 1e6, buf[7] / 1e6, buf[15] / 1e6, buf[12] / 1e6, buf[13] / 1e6);
+        fprintf(stderr, "[phif] team QR CTA0: update calls %lld [pass1 %.1f Z %.1f pass2 %.1f Mcycles] factor calls %lld waits %lld\n",
+                buf[16], buf[17] / 1e6, buf[18] / 1e6, buf[19] / 1e6, buf[20], buf[21]);
       });
     }
   }
@@ -887,6 +889,11 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       for (int w = 0; w < P.nwaves; ++w) max_blocks = std::max<int64_t>(max_blocks, wave_blocks[w]);
       DBuf cand;
       cand.alloc((size_t)2 * max_blocks * cand_ld * sizeof(double), s);
+      int kmax_lv = 0;
+      for (int w = 0; w < P.nwaves; ++w) kmax_lv = std::max(kmax_lv, wave_kmax[w]);
+      const int64_t qt_ld = 8 * (int64_t)kmax_lv + 64;   // T factors of all QR panels of one face
+      DBuf qtb;
+      qtb.alloc(std::max<size_t>(large_list.size(), 1) * qt_ld * sizeof(double), s);
       si.alloc(std::max<int64_t>(2 * slot_off[P.nwaves], 1) * sizeof(int), s);
       for (int w = 0; w < P.nwaves; ++w) {
         ka.order = d_small.as<int>() + small_off[w];
@@ -911,6 +918,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ta.cand = cand.as<double>();
           ta.cand_ld = cand_ld;
           ta.colcap = team_colcap(wave_vcap[w], wave_kmax[w]);
+          ta.qt = qtb.as<double>() + large_off[w] * qt_ld;
+          ta.qt_ld = qt_ld;
           ta.prof = team_prof_buffer();
           launch_skel_team(dv, ka, ta, wave_blocks[w], s);
         }

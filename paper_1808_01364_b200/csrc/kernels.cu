@@ -444,8 +444,10 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
   const int64_t gof = lv.goff[g];
-  const int64_t ldw = skel_ldw(lv, sk, s);
-  // A_{R,I} and its CPQR live in shared memory when they fit, else in the global workspace
+  // count the kept rows first: A_{R,I} (ld = m) and its CPQR live in shared memory when they
+  // fit, else in the global workspace
+  const int nch = skel_nchunks(lv, sk, s);
+  const int64_t ldw = max(1, gather_chunks<false>(lv, sk, s, 0, nch, nullptr, 1, 0, sint, 512));
   const bool local = ldw * k + 4 * (int64_t)k + 4 <= smem_cap;
   double* W = local ? smem + SMEM_DOUBLES : sk.work + sk.work_off[s];
   double* vn1 = W + (int64_t)k * ldw;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
   int* perm = iw;
   int* sidx = iw + k;
   int* flag = iw + 2 * k;
-  const int m = gather_chunks<true>(lv, sk, s, 0, skel_nchunks(lv, sk, s), W, ldw, 0, sint, 512);
+  const int m = gather_chunks<true>(lv, sk, s, 0, nch, W, ldw, 0, sint, 512);
   if (tid == 0) sk.rows[s] = m;
   uint8_t* red = sk.red + gof;
   if (m == 0) {
@@ -573,7 +575,7 @@ constexpr int TOWN = 512;    // max owned columns per CTA (smem norms)
 //    form the winning Householder reflector right after it.
 //  * Only R's diagonal and strictly-upper part are kept (Q is never needed); the loop stops
 //    once the largest remaining partial norm is below the rank cut (see cta_cpqr).
-__global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, TeamArgs ta) {
+__global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, TeamArgs ta) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
   double* sdot = smem + GEMM_OFF;               // [nw][TCH] partial dots, then [TCH] products
@@ -631,246 +633,299 @@ __global__ void __launch_bounds__(NT) k_skel_team(LevelDev lv, SkelArgs sk, Team
   }
   // ---- row reduction: blocked Householder QR W = Q [R0; 0] (m0 > k) -----------------------
   // CPQR pivots depend only on A^T A, so the CPQR of R0 selects the same columns as the CPQR
-  // of A (up to rounding) while every later step touches k instead of m0 rows. Panels of nbq
-  // columns are factored by one CTA in shared memory; the compact-WY update of the trailing
-  // columns is done by their owners (two team barriers per panel).
+  // of A (up to rounding) while every later step touches k instead of m0 rows.
+  // Panels of nbq columns; block b (its columns) is owned by CTA b % P. The owner of block
+  // pi+1 applies panel pi to it first, factors it at once and publishes it (hdr->qr_done,
+  // look-ahead); everyone else applies published panels to their blocks with DMMA
+  // (X -= V T^T V^T X) and only waits for the panel it needs next. No team barriers.
   int m = m0;
   const long long t_qr0 = clock64();
-  if (m0 > k) {
-    const int nbq = max(1, min(8, ta.colcap / m0));
-    double* qT = cand_base;            // team scratch: T (8 x 8) of the current panel
-    for (int j0 = 0, pi = 0; j0 < k; j0 += nbq, ++pi) {
-      const int jb = min(nbq, k - j0);
-      const int ldp = m0 - j0;
-      double* Pn = colbuf;             // panel (jb x ldp, column-major) / staged V for the update
-      const bool qprof = ta.prof && blockIdx.x == 0 && tid == 0;
+  // shared memory free in this phase: everything (reductions and staging are static here)
+  const int64_t qcap = (int64_t)SMEM_DOUBLES + ta.vcap + ta.kmax + 1 + ta.colcap;
+  if (m0 > k && 2 * (int64_t)m0 <= qcap) {
+    const int nbq = (int)(qcap / (2 * (int64_t)m0) < 8 ? qcap / (2 * (int64_t)m0) : 8);
+    const int npan = (k + nbq - 1) / nbq;
+    double* const vbuf0 = smem;
+    double* const vbuf1 = smem + (int64_t)nbq * m0;
+    __shared__ double s_T[2][64];
+    __shared__ double s_par[20];
+    __shared__ double s_red[8][8];
+    __shared__ double s_Y[8][64];
+    __shared__ double s_Z[64];
+    double* qt = ta.qt + (int64_t)f * ta.qt_ld;
+    const bool qprof = ta.prof && blockIdx.x == 0 && tid == 0;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    // factor panel pi (already updated by panels < pi) in smem, write it back and publish it
+    auto factor = [&](int pi) {
       long long tq0 = qprof ? clock64() : 0;
-      if (c == pi % P) {
-        panel_load<false>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
+      if (qprof) ta.prof[20] += 1;
+      const int j0 = pi * nbq, jb = min(nbq, k - j0), ldp = m0 - j0;
+      double* Pn = (pi & 1) ? vbuf1 : vbuf0;
+      double* Ts = s_T[pi & 1];
+      panel_load<false>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
+      __syncthreads();
+      for (int jj = 0; jj < jb; ++jj) {
+        // one reduction per column: |x|^2 and x . a_u (x = column jj below the diagonal)
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+        const double* xc = Pn + (int64_t)jj * ldp;
+        for (int rr = jj + 1 + tid; rr < ldp; rr += NT) {
+          const double x = xc[rr];
+          acc[0] += x * x;
+#pragma unroll
+          for (int u = 1; u < 8; ++u)
+            if (jj + u < jb) acc[u] += x * Pn[(int64_t)(jj + u) * ldp + rr];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double t2 = warp_sum(acc[u]);
+          if (lane == 0) s_red[warp][u] = t2;
+        }
         __syncthreads();
-        __shared__ double s_tau[8];
-        for (int jj = 0; jj < jb; ++jj) {
-          double* col = Pn + (int64_t)jj * ldp;
-          double part = 0.0;
-          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) part += col[rr] * col[rr];
-          const double xnorm = sqrt(cta_sum(part, sred));
-          const double alpha = col[jj];
+        if (tid == 0) {
+          double sum[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            sum[u] = 0.0;
+            for (int w2 = 0; w2 < nw; ++w2) sum[u] += s_red[w2][u];
+          }
+          const double alpha = xc[jj], xnorm = sqrt(sum[0]);
           double tau = 0.0, beta = alpha, scal = 1.0;
           if (xnorm != 0.0) {
             beta = -copysign(hypot(alpha, xnorm), alpha);
             tau = (beta - alpha) / beta;
             scal = 1.0 / (alpha - beta);
           }
-          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) col[rr] *= scal;
-          __syncthreads();
-          if (tid == 0) {
-            col[jj] = beta;
-            s_tau[jj] = tau;
-          }
-          // apply H_jj to the remaining panel columns: thread row strips, CTA-reduced dots
-          __shared__ double s_pd[8][8];
-          double acc[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) {
-            const double vr = col[rr];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (jj + 1 + u < jb) acc[u] += vr * Pn[(int64_t)(jj + 1 + u) * ldp + rr];
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const double t2 = warp_sum(acc[u]);
-            if (lane == 0) s_pd[warp][u] = t2;
-          }
-          __syncthreads();
-          __shared__ double s_tw[8];
-          if (tid < 8 && jj + 1 + tid < jb) {
-            double a = Pn[(int64_t)(jj + 1 + tid) * ldp + jj];
-            for (int q2 = 0; q2 < nw; ++q2) a += s_pd[q2][tid];
-            const double tw = tau * a;
-            Pn[(int64_t)(jj + 1 + tid) * ldp + jj] -= tw;
-            s_tw[tid] = tw;
-          }
-          __syncthreads();
-          for (int rr = jj + 1 + tid; rr < ldp; rr += NT) {
-            const double vr = col[rr];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (jj + 1 + u < jb) Pn[(int64_t)(jj + 1 + u) * ldp + rr] -= s_tw[u] * vr;
-          }
-          __syncthreads();
-        }
-        // compact WY factor T (upper triangular): H_1 ... H_jb = I - V T V^T
-        // G = V^T V (strict upper part) in one pass over the rows: V_a(rr) = 0 above, 1 on the diagonal
-        __shared__ double s_G[8][8];
-        __shared__ double s_Gp[8][28];
-        {
-          double gp[28];
-#pragma unroll
-          for (int q = 0; q < 28; ++q) gp[q] = 0.0;
-          for (int rr = 1 + tid; rr < ldp; rr += NT) {
-            double va[8];
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-              va[a] = (a < jb && rr >= a) ? (rr == a ? 1.0 : Pn[(int64_t)a * ldp + rr]) : 0.0;
-            int q = 0;
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-              for (int b2 = a + 1; b2 < 8; ++b2) gp[q++] += va[a] * va[b2];
-          }
-#pragma unroll
-          for (int q = 0; q < 28; ++q) {
-            const double t2 = warp_sum(gp[q]);
-            if (lane == 0) s_Gp[warp][q] = t2;
-          }
-          __syncthreads();
-          if (tid < 64) {
-            const int a = tid / 8, b2 = tid % 8;
-            double x = 0.0;
-            if (a < b2) {
-              const int q = a * 8 - a * (a + 1) / 2 + (b2 - a - 1);
-              for (int ww = 0; ww < nw; ++ww) x += s_Gp[ww][q];
+          Pn[(int64_t)jj * ldp + jj] = beta;
+          Ts[jj * 8 + jj] = tau;
+          s_par[0] = scal;
+          for (int u = 1; u < 8; ++u)
+            if (jj + u < jb) {
+              double* au = Pn + (int64_t)(jj + u) * ldp;
+              const double tw = tau * (au[jj] + scal * sum[u]);   // tau * v^T a_u
+              au[jj] -= tw;
+              s_par[u] = tw * scal;                               // a_u -= tw * scal * x (rows > jj)
             }
-            s_G[a][b2] = x;
-          }
+        }
+        __syncthreads();
+        const double scal = s_par[0];
+        double cu[8];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) cu[u] = (jj + u < jb) ? s_par[u] : 0.0;
+        for (int rr = jj + 1 + tid; rr < ldp; rr += NT) {
+          const double x = Pn[(int64_t)jj * ldp + rr];
+#pragma unroll
+          for (int u = 1; u < 8; ++u)
+            if (jj + u < jb) Pn[(int64_t)(jj + u) * ldp + rr] -= cu[u] * x;
+          Pn[(int64_t)jj * ldp + rr] = x * scal;
+        }
+        __syncthreads();
+      }
+      // compact WY factor T (upper triangular): H_1 ... H_jb = I - V T V^T, from G = V^T V
+      {
+        double gp[28];
+#pragma unroll
+        for (int q = 0; q < 28; ++q) gp[q] = 0.0;
+        for (int rr = 1 + tid; rr < ldp; rr += NT) {
+          double va[8];
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+            va[a] = (a < jb && rr >= a) ? (rr == a ? 1.0 : Pn[(int64_t)a * ldp + rr]) : 0.0;
+          int q = 0;
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b2 = a + 1; b2 < 8; ++b2) gp[q++] += va[a] * va[b2];
+        }
+#pragma unroll
+        for (int q = 0; q < 28; ++q) {
+          const double t2 = warp_sum(gp[q]);
+          if (lane == 0) s_Y[warp][q] = t2;
         }
         __syncthreads();
         if (tid == 0) {
-          double T[8][8];
+          double Gm[8][8], T[8][8];
+          for (int a = 0; a < 8; ++a)
+            for (int b2 = a + 1; b2 < 8; ++b2) {
+              const int q = a * 8 - a * (a + 1) / 2 + (b2 - a - 1);
+              double x = 0.0;
+              for (int w2 = 0; w2 < nw; ++w2) x += s_Y[w2][q];
+              Gm[a][b2] = x;
+            }
           for (int i2 = 0; i2 < jb; ++i2) {
+            const double ti = Ts[i2 * 8 + i2];
             for (int a = 0; a < i2; ++a) {
               double x = 0.0;
-              for (int b = a; b < i2; ++b) x += T[a][b] * s_G[b][i2];
-              T[a][i2] = -s_tau[i2] * x;
+              for (int b2 = a; b2 < i2; ++b2) x += T[a][b2] * Gm[b2][i2];
+              T[a][i2] = -ti * x;
             }
-            T[i2][i2] = s_tau[i2];
-            for (int a = i2 + 1; a < jb; ++a) T[a][i2] = 0.0;
+            T[i2][i2] = ti;
+            for (int a = i2 + 1; a < 8; ++a) T[a][i2] = 0.0;
           }
-          for (int a = 0; a < jb; ++a)
-            for (int b = 0; b < jb; ++b) __stcg(qT + a * 8 + b, T[a][b]);
+          for (int a = 0; a < 8; ++a)
+            for (int b2 = 0; b2 < 8; ++b2) {
+              const double v = (a < jb && b2 < jb) ? T[a][b2] : 0.0;
+              Ts[a * 8 + b2] = v;
+              if (a < jb && b2 < jb) __stcg(qt + (int64_t)pi * nbq * nbq + a * nbq + b2, v);
+            }
         }
-        panel_store(W + (int64_t)j0 * ldw + j0, ldw, Pn, jb, ldp);
       }
-      if (qprof) { const long long t1 = clock64(); ta.prof[14] += t1 - tq0; tq0 = t1; }
-      team_sync(hdr, P);
-      if (qprof) { const long long t1 = clock64(); ta.prof[15] += t1 - tq0; tq0 = t1; }
-      // trailing update of owned columns j >= j0 + jb: a <- a - V (T^T (V^T a))
-      const int jstart = j0 + jb;
-      const int tfirst = jstart <= c ? 0 : (jstart - c + P - 1) / P;
-      if (tfirst < nloc_all(k, c, P)) {
-        panel_load<true>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
-        __shared__ double s_T[8][8];
-        if (tid < 64) s_T[tid / 8][tid % 8] = (tid / 8 < jb && tid % 8 < jb) ? __ldcg(qT + tid) : 0.0;
+      panel_store(W + (int64_t)j0 * ldw + j0, ldw, Pn, jb, ldp);
+      __syncthreads();
+      if (tid == 0 && P > 1) {
+        __threadfence();
+        atomicAdd(&hdr->qr_done, 1u);
+      }
+      // the smem copy becomes the unit-lower V of this panel
+      for (int e = tid; e < jb * jb; e += NT) {
+        const int jj = e / jb, rr = e % jb;
+        if (rr <= jj) Pn[(int64_t)jj * ldp + rr] = rr == jj ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      if (qprof) ta.prof[14] += clock64() - tq0;
+    };
+    // X(:, block b) -= V (T^T (V^T X)) for panel pi (V in Vb, T in Ts), rows j0.. of the block.
+    // Rows are split across warps in 8-row tiles; inside a tile the K order of V^T X is
+    // permuted (k-step z takes rows 2t+z) so each lane's B fragments are exactly its C
+    // fragments of the transposed update X^T -= Z^T V^T: the block slice stays in registers
+    // (QR_TPW tiles per warp; all loads issued at once), only the excess is re-read.
+    auto update = [&](int pi, int b, const double* Vb, const double* Ts) {
+      constexpr int QR_TPW = 40;
+      const int j0 = pi * nbq, jb = min(nbq, k - j0), ldp = m0 - j0;
+      const int cb0 = b * nbq, ncol = min(nbq, k - cb0);
+      const int ntile = (ldp + 7) >> 3;
+      const int tpw = (ntile + nw - 1) / nw;
+      const int t_lo = warp * tpw, t_hi = min(ntile, t_lo + tpw);
+      const bool col_ok = g8 < ncol, va_ok = g8 < jb;
+      double* Xc = W + (int64_t)(cb0 + min(g8, ncol - 1)) * ldw + j0;
+      const double* Va = Vb + (int64_t)min(g8, jb - 1) * ldp;
+      long long tp0 = qprof ? clock64() : 0;
+      double xr[QR_TPW][2];
+#pragma unroll
+      for (int u = 0; u < QR_TPW; ++u) {
+        const int rr = (t_lo + u) * 8 + 2 * t4;
+        const bool ok = t_lo + u < t_hi && col_ok;
+        xr[u][0] = (ok && rr < ldp) ? __ldcg(Xc + rr) : 0.0;
+        xr[u][1] = (ok && rr + 1 < ldp) ? __ldcg(Xc + rr + 1) : 0.0;
+      }
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < QR_TPW; ++u) {
+        const int rr = (t_lo + u) * 8 + 2 * t4;
+        if (t_lo + u < t_hi) {
+          const double a0 = (va_ok && rr < ldp) ? Va[rr] : 0.0;
+          const double a1 = (va_ok && rr + 1 < ldp) ? Va[rr + 1] : 0.0;
+          dmma(c0, c1, a0, xr[u][0]);
+          dmma(c0, c1, a1, xr[u][1]);
+        }
+      }
+      for (int tl = t_lo + QR_TPW; tl < t_hi; ++tl) {   // beyond the register slice
+        const int rr = tl * 8 + 2 * t4;
+        const double x0 = (col_ok && rr < ldp) ? __ldcg(Xc + rr) : 0.0;
+        const double x1 = (col_ok && rr + 1 < ldp) ? __ldcg(Xc + rr + 1) : 0.0;
+        dmma(c0, c1, (va_ok && rr < ldp) ? Va[rr] : 0.0, x0);
+        dmma(c0, c1, (va_ok && rr + 1 < ldp) ? Va[rr + 1] : 0.0, x1);
+      }
+      s_Y[warp][g8 * 8 + 2 * t4] = c0;
+      s_Y[warp][g8 * 8 + 2 * t4 + 1] = c1;
+      __syncthreads();
+      if (qprof) {
+        const long long t1 = clock64();
+        ta.prof[16] += 1;
+        ta.prof[17] += t1 - tp0;
+        tp0 = t1;
+      }
+      if (tid < 64) {
+        const int bz = tid >> 3, col = tid & 7;
+        double z = 0.0;
+        for (int a = 0; a <= bz; ++a) {
+          double y = 0.0;
+          for (int w2 = 0; w2 < nw; ++w2) y += s_Y[w2][a * 8 + col];
+          z += Ts[a * 8 + bz] * y;
+        }
+        s_Z[tid] = z;
+      }
+      __syncthreads();
+      if (qprof) {
+        const long long t1 = clock64();
+        ta.prof[18] += t1 - tp0;
+        tp0 = t1;
+      }
+      // X^T -= Z^T V^T: M = columns, N = rows of the tile, K = reflectors (two k-steps)
+      const double za0 = -s_Z[t4 * 8 + g8], za1 = -s_Z[(t4 + 4) * 8 + g8];
+      const double* V0 = Vb + (int64_t)min(t4, jb - 1) * ldp;
+      const double* V1 = Vb + (int64_t)min(t4 + 4, jb - 1) * ldp;
+      const bool b0_ok = t4 < jb, b1_ok = t4 + 4 < jb;
+#pragma unroll
+      for (int u = 0; u < QR_TPW; ++u) {
+        if (t_lo + u < t_hi) {
+          const int rv = (t_lo + u) * 8 + g8;
+          const double vb0 = (b0_ok && rv < ldp) ? V0[rv] : 0.0;
+          const double vb1 = (b1_ok && rv < ldp) ? V1[rv] : 0.0;
+          dmma(xr[u][0], xr[u][1], za0, vb0);
+          dmma(xr[u][0], xr[u][1], za1, vb1);
+          const int rr = (t_lo + u) * 8 + 2 * t4;
+          if (col_ok) {
+            if (rr < ldp) __stcg(Xc + rr, xr[u][0]);
+            if (rr + 1 < ldp) __stcg(Xc + rr + 1, xr[u][1]);
+          }
+        }
+      }
+      for (int tl = t_lo + QR_TPW; tl < t_hi; ++tl) {
+        const int rr = tl * 8 + 2 * t4, rv = tl * 8 + g8;
+        double x0 = (col_ok && rr < ldp) ? __ldcg(Xc + rr) : 0.0;
+        double x1 = (col_ok && rr + 1 < ldp) ? __ldcg(Xc + rr + 1) : 0.0;
+        dmma(x0, x1, za0, (b0_ok && rv < ldp) ? V0[rv] : 0.0);
+        dmma(x0, x1, za1, (b1_ok && rv < ldp) ? V1[rv] : 0.0);
+        if (col_ok) {
+          if (rr < ldp) __stcg(Xc + rr, x0);
+          if (rr + 1 < ldp) __stcg(Xc + rr + 1, x1);
+        }
+      }
+      __syncthreads();
+      if (qprof) ta.prof[19] += clock64() - tp0;
+    };
+    if (c == 0) factor(0);
+    for (int pi = 0; pi < npan; ++pi) {
+      double* Vb = (pi & 1) ? vbuf1 : vbuf0;
+      const double* Ts = s_T[pi & 1];
+      if (pi % P != c) {
+        long long tq0 = qprof ? clock64() : 0;
+        if (qprof) ta.prof[21] += 1;
+        if (tid == 0) {
+          volatile unsigned* done = &hdr->qr_done;
+          while (*done < (unsigned)(pi + 1)) __nanosleep(32);
+          __threadfence();
+        }
         __syncthreads();
-        // owned trailing columns two at a time: thread row strips, CTA-reduced V^T a
-        const int nl = nloc_all(k, c, P);
-        __shared__ double s_w[8][2][8];
-        __shared__ double s_z[2][8];
-        for (int t0 = tfirst; t0 < nl; t0 += 2) {
-          const int nt = min(2, nl - t0);
-          double* cj0 = W + (int64_t)(c + P * t0) * ldw + j0;
-          double* cj1 = W + (int64_t)(c + P * (t0 + nt - 1)) * ldw + j0;
-          double w0[8], w1[8];
-#pragma unroll
-          for (int a = 0; a < 8; ++a) w0[a] = w1[a] = 0.0;
-          // all of this thread's rows of both columns are loaded up front (one L2 round trip),
-          // kept in registers for the update below
-          constexpr int QR_NQ = 16;
-          double x0r[QR_NQ], x1r[QR_NQ];
-          const bool regs = ldp <= QR_NQ * NT;
-          if (regs) {
-#pragma unroll
-            for (int q = 0; q < QR_NQ; ++q) {
-              const int rr = tid + q * NT;
-              x0r[q] = rr < ldp ? __ldcg(cj0 + rr) : 0.0;
-              x1r[q] = rr < ldp ? __ldcg(cj1 + rr) : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < QR_NQ; ++q) {
-              const int rr = tid + q * NT;
-              if (rr < ldp) {
-#pragma unroll
-                for (int a = 0; a < 8; ++a)
-                  if (a < jb) {
-                    const double va = Pn[(int64_t)a * ldp + rr];
-                    w0[a] += va * x0r[q];
-                    w1[a] += va * x1r[q];
-                  }
-              }
-            }
-          } else {
-            for (int rr = tid; rr < ldp; rr += NT) {
-              const double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
-#pragma unroll
-              for (int a = 0; a < 8; ++a)
-                if (a < jb) {
-                  const double va = Pn[(int64_t)a * ldp + rr];
-                  w0[a] += va * x0;
-                  w1[a] += va * x1;
-                }
-            }
-          }
-#pragma unroll
-          for (int a = 0; a < 8; ++a) {
-            const double y0 = warp_sum(w0[a]), y1 = warp_sum(w1[a]);
-            if (lane == 0) {
-              s_w[warp][0][a] = y0;
-              s_w[warp][1][a] = y1;
-            }
-          }
-          __syncthreads();
-          if (tid < 16) {
-            const int q2 = tid >> 3, b = tid & 7;
-            double x = 0.0;
-            if (b < jb)
-              for (int a = 0; a <= b; ++a) {
-                double wa = 0.0;
-                for (int ww = 0; ww < nw; ++ww) wa += s_w[ww][q2][a];
-                x += s_T[a][b] * wa;
-              }
-            s_z[q2][b] = x;
-          }
-          __syncthreads();
-          if (regs) {
-#pragma unroll
-            for (int q = 0; q < QR_NQ; ++q) {
-              const int rr = tid + q * NT;
-              if (rr < ldp) {
-                double x0 = x0r[q], x1 = x1r[q];
-#pragma unroll
-                for (int b = 0; b < 8; ++b)
-                  if (b < jb) {
-                    const double vb = Pn[(int64_t)b * ldp + rr];
-                    x0 -= vb * s_z[0][b];
-                    x1 -= vb * s_z[1][b];
-                  }
-                __stcg(cj0 + rr, x0);
-                if (nt == 2) __stcg(cj1 + rr, x1);
-              }
-            }
-          } else {
-            for (int rr = tid; rr < ldp; rr += NT) {
-              double x0 = __ldcg(cj0 + rr), x1 = __ldcg(cj1 + rr);
-#pragma unroll
-              for (int b = 0; b < 8; ++b)
-                if (b < jb) {
-                  const double vb = Pn[(int64_t)b * ldp + rr];
-                  x0 -= vb * s_z[0][b];
-                  x1 -= vb * s_z[1][b];
-                }
-              __stcg(cj0 + rr, x0);
-              if (nt == 2) __stcg(cj1 + rr, x1);
-            }
-          }
-          __syncthreads();
+        if (qprof) {
+          const long long t1 = clock64();
+          ta.prof[15] += t1 - tq0;
+          tq0 = t1;
         }
+        const int j0 = pi * nbq, jb = min(nbq, k - j0);
+        panel_load<true>(Vb, W + (int64_t)j0 * ldw + j0, ldw, jb, m0 - j0);
+        if (tid < 64) {
+          const int a = tid >> 3, b2 = tid & 7;
+          s_T[pi & 1][tid] = (a < jb && b2 < jb) ? __ldcg(qt + (int64_t)pi * nbq * nbq + a * nbq + b2) : 0.0;
+        }
+        __syncthreads();
+        if (qprof) ta.prof[7] += clock64() - tq0;
       }
-      if (qprof) { const long long t1 = clock64(); ta.prof[7] += t1 - tq0; tq0 = t1; }
-      team_sync(hdr, P);
-      if (qprof) { const long long t1 = clock64(); ta.prof[15] += t1 - tq0; tq0 = t1; }
+      long long tu0 = qprof ? clock64() : 0;
+      int b = pi + 1 + ((c - (pi + 1)) % P + P) % P;   // first owned block > pi
+      if (b == pi + 1 && b < npan) {
+        update(pi, b, Vb, Ts);
+        if (qprof) ta.prof[7] += clock64() - tu0;
+        factor(b);
+        tu0 = qprof ? clock64() : 0;
+        b += P;
+      }
+      for (; b < npan; b += P) update(pi, b, Vb, Ts);
+      if (qprof) ta.prof[7] += clock64() - tu0;
     }
+    team_sync(hdr, P);
     // R0 = rows 0..k-1 of W: clear the reflector entries below the diagonal of owned columns
     for (int t = 0; t < nloc_all(k, c, P); ++t) {
       const int j = c + P * t;

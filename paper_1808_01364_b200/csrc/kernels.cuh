@@ -91,6 +91,7 @@ struct SkelArgs {
 struct TeamHdr {
   unsigned count;
   unsigned gen;
+  unsigned qr_done;   // panels of the row-reduction QR published so far
   double tau;
 };
 
@@ -107,6 +108,8 @@ struct TeamArgs {
   double* cand;          // 2 staging columns per CTA (pivot candidates), ld cand_ld
   int64_t cand_ld;
   int colcap;            // doubles of shared memory for resident owned columns
+  double* qt;            // per team: T factors of the QR panels, qt_ld doubles
+  int64_t qt_ld;
 };
 
 struct RepackArgs {
