@@ -187,13 +187,21 @@ void upload_structure(LevelRT& L, cudaStream_t s) {
 
 // Work lists for the tile-parallel big-cell path (one level).
 struct BigPlan {
-  static constexpr int T = 64;
+  // Right-looking blocked Cholesky of the big panels, all big cells of the level together.
+  // Blocks of KB columns; inside a block, 64-wide steps (diag factor + inverse, panel TRSM as a
+  // GEMM with the inverse, update of the block's own remaining columns); then one KB-deep
+  // update of the whole trailing matrix. Last, U = X^T X (lower tiles, mirrored).
+  static constexpr int T = 64, KB = 256;
   DBuf d_n, d_b, d_rows, d_P, d_U, d_op, d_linv, d_list;
   DBuf d_cell, d_i, d_j;
-  std::vector<int64_t> diag_off, trsm_off, upd_off;   // per step offsets into the work arrays
-  std::vector<int> steps_k0;
-  int64_t syrk_off = 0, syrk_n = 0;
+  struct Phase {
+    int kind;        // 0 diag + trsm + narrow update (one 64-wide step), 1 wide update, 2 U
+    int64_t off[3], cnt[3];
+    int k0, kw;
+  };
+  std::vector<Phase> phases;
   int nbig = 0;
+  int64_t nwork_total = 0;
   void build(const std::vector<int>& big, const std::vector<int>& cn, const std::vector<int>& cb, double* rec,
              const std::vector<int64_t>& P_off, double* U, const std::vector<int64_t>& U_off, cudaStream_t s) {
     nbig = (int)big.size();
@@ -211,53 +219,67 @@ struct BigPlan {
       nmax = std::max(nmax, n[c]);
     }
     std::vector<int> wc, wi, wj;
-    for (int k0 = 0; k0 < nmax; k0 += T) {
-      steps_k0.push_back(k0);
-      diag_off.push_back((int64_t)wc.size());
-      for (int c = 0; c < nbig; ++c)
-        if (n[c] > k0) {
-          wc.push_back(c);
-          wi.push_back(0);
-          wj.push_back(0);
-        }
-      trsm_off.push_back((int64_t)wc.size());
-      for (int c = 0; c < nbig; ++c) {
-        if (n[c] <= k0) continue;
-        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = rws[c];
-        const int ntr = (rows - base + T - 1) / T;
-        for (int it = 0; it < ntr; ++it) {
+    // trailing tiles of cell c for columns [base, cend), rows [base, rows): skip tiles strictly
+    // above the diagonal of the square part
+    auto trailing = [&](int c, int base, int cend) {
+      if (base >= cend) return;
+      const int nr = (rws[c] - base + T - 1) / T, nc = (cend - base + T - 1) / T;
+      for (int it = 0; it < nr; ++it)
+        for (int jt = 0; jt < nc; ++jt) {
+          if (jt > it && base + T * (it + 1) <= n[c]) continue;
           wc.push_back(c);
           wi.push_back(it);
-          wj.push_back(0);
+          wj.push_back(jt);
         }
-      }
-      upd_off.push_back((int64_t)wc.size());
-      for (int c = 0; c < nbig; ++c) {
-        if (n[c] <= k0) continue;
-        const int kb = std::min(T, n[c] - k0), base = k0 + kb, rows = rws[c];
-        if (base >= n[c]) continue;
-        const int nr = (rows - base + T - 1) / T, nc = (n[c] - base + T - 1) / T;
-        for (int it = 0; it < nr; ++it)
-          for (int jt = 0; jt < nc; ++jt) {
-            if (jt > it && base + T * (it + 1) <= n[c]) continue;
+    };
+    for (int kb0 = 0; kb0 < nmax; kb0 += KB) {
+      for (int s0 = kb0; s0 < std::min(nmax, kb0 + KB); s0 += T) {
+        Phase ph{0, {0, 0, 0}, {0, 0, 0}, s0, T};
+        ph.off[0] = (int64_t)wc.size();
+        for (int c = 0; c < nbig; ++c)
+          if (n[c] > s0) {
+            wc.push_back(c);
+            wi.push_back(0);
+            wj.push_back(0);
+          }
+        ph.off[1] = (int64_t)wc.size();
+        for (int c = 0; c < nbig; ++c) {
+          if (n[c] <= s0) continue;
+          const int kb = std::min(T, n[c] - s0), base = s0 + kb;
+          const int ntr = (rws[c] - base + T - 1) / T;
+          for (int it = 0; it < ntr; ++it) {
             wc.push_back(c);
             wi.push_back(it);
-            wj.push_back(jt);
+            wj.push_back(0);
           }
+        }
+        ph.off[2] = (int64_t)wc.size();
+        for (int c = 0; c < nbig; ++c)
+          if (n[c] > s0 + T) trailing(c, s0 + T, std::min(n[c], kb0 + KB));
+        ph.cnt[0] = ph.off[1] - ph.off[0];
+        ph.cnt[1] = ph.off[2] - ph.off[1];
+        ph.cnt[2] = (int64_t)wc.size() - ph.off[2];
+        phases.push_back(ph);
       }
+      Phase wide{1, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
+      for (int c = 0; c < nbig; ++c)
+        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, n[c]);
+      wide.cnt[0] = (int64_t)wc.size() - wide.off[0];
+      if (wide.cnt[0]) phases.push_back(wide);
     }
-    diag_off.push_back((int64_t)wc.size());
-    syrk_off = (int64_t)wc.size();
+    Phase us{2, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, 0, 0};
     for (int c = 0; c < nbig; ++c) {
       const int nb = (b[c] + T - 1) / T;
       for (int it = 0; it < nb; ++it)
-        for (int jt = 0; jt < nb; ++jt) {
+        for (int jt = 0; jt <= it; ++jt) {
           wc.push_back(c);
           wi.push_back(it);
           wj.push_back(jt);
         }
     }
-    syrk_n = (int64_t)wc.size() - syrk_off;
+    us.cnt[0] = (int64_t)wc.size() - us.off[0];
+    if (us.cnt[0]) phases.push_back(us);
+    nwork_total = (int64_t)wc.size();
     upload(d_n, n, s);
     upload(d_b, b, s);
     upload(d_rows, rws, s);
@@ -269,7 +291,7 @@ struct BigPlan {
     upload(d_i, wi, s);
     upload(d_j, wj, s);
   }
-  BigArgs args(int64_t off, int64_t cnt, int k0) const {
+  BigArgs args(int64_t off, int64_t cnt, int k0, int kw) const {
     BigArgs a;
     a.ncell = nbig;
     a.n = d_n.as<int>();
@@ -284,15 +306,17 @@ struct BigPlan {
     a.w_j = d_j.as<int>() + off;
     a.nwork = (int)cnt;
     a.k0 = k0;
+    a.kw = kw;
     return a;
   }
   void run(DevStatus* st, cudaStream_t s) const {
-    for (size_t q = 0; q < steps_k0.size(); ++q) {
-      const int k0 = steps_k0[q];
-      const int64_t d0 = diag_off[q], t0 = trsm_off[q], u0 = upd_off[q], e = diag_off[q + 1];
-      launch_big_step(args(d0, t0 - d0, k0), args(t0, u0 - t0, k0), args(u0, e - u0, k0), st, s);
+    for (const Phase& ph : phases) {
+      if (ph.kind == 0)
+        launch_big_step(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), args(ph.off[1], ph.cnt[1], ph.k0, ph.kw),
+                        args(ph.off[2], ph.cnt[2], ph.k0, ph.kw), st, s);
+      else
+        launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), ph.kind == 1 ? 0 : 1, s);
     }
-    launch_big_syrk(args(syrk_off, syrk_n, 0), s);
   }
 };
 
@@ -628,7 +652,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.h_cwork = cwork;
     BigPlan bp;
     if (!big_cells.empty()) bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
-    DBG("level %d: big plan built (%zu work items)", lev, bp.steps_k0.empty() ? (size_t)0 : (size_t)bp.syrk_off);
+    DBG("level %d: big plan built (%lld work items)", lev, (long long)bp.nwork_total);
     if (timing) CK(cudaEventRecord(ev[2], s));
     if (!small_cells.empty()) {
       ca.list = L.d_small_cells.as<int>();

@@ -1396,49 +1396,6 @@ __global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
       }
 }
 
-// trailing update tile (i, j): C -= A_i A_j^T, K = this step's 64 columns
-__global__ void __launch_bounds__(NT) k_big_update(BigArgs a) {
-  extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + BT * BLD;
-  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
-  const int n = a.n[c], rows = a.rows[c], k0 = a.k0, kb = min(BT, n - k0);
-  const int base = k0 + kb;
-  const int r0 = base + BT * it, c0 = base + BT * jt;
-  double* P = a.P[c];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < BT * BT; e += NT) {
-    const int i = e / BT, j = e % BT;
-    sA[i * BLD + j] = (r0 + i < rows && j < kb) ? P[(int64_t)(r0 + i) * n + k0 + j] : 0.0;
-    sB[i * BLD + j] = (c0 + i < n && j < kb) ? P[(int64_t)(c0 + i) * n + k0 + j] : 0.0;
-  }
-  __syncthreads();
-  double acc[2][4][2] = {};
-  tile_mma_nt(sA, sB, acc);
-  const int lane = tid & 31, warp = tid >> 5, wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int x = 0; x < 2; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y)
-#pragma unroll
-      for (int z = 0; z < 2; ++z) {
-        const int i = r0 + wm * 16 + x * 8 + g, j = c0 + wn * 32 + y * 8 + 2 * t + z;
-        if (i < rows && j < n && (i >= n || j <= i)) P[(int64_t)i * n + j] -= acc[x][y][z];
-      }
-}
-
-// U = X^T X where X^T = P[n:n+b, 0:n]: one 64x64 output tile per CTA, K = n
-__global__ void __launch_bounds__(NT) k_big_syrk(BigArgs a) {
-  extern __shared__ double smem[];
-  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
-  const int n = a.n[c], b = a.b[c];
-  const double* PB = a.P[c] + (int64_t)n * n;
-  double* U = a.U[c];
-  const int i0 = BT * it, j0 = BT * jt;
-  cta_gemm<false, true>(min(BT, b - i0), min(BT, b - j0), n, 1.0, PB + (int64_t)i0 * n, n, PB + (int64_t)j0 * n,
-                        n, 0.0, U + (int64_t)i0 * b + j0, b, false, smem + GEMM_OFF);
-}
-
 // build panels [A_gg ; I] of big block-Jacobi groups (A_gg <- I afterwards), grid-stride
 __global__ void k_prec_build(LevelDev lv, PrecArgs pa, const int* list, int nbig, int chunks) {
   const int bc = blockIdx.x / chunks, ch = blockIdx.x % chunks;
@@ -1879,6 +1836,114 @@ static constexpr size_t SMEM_BYTES = (size_t)SMEM_DOUBLES * sizeof(double);
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+
+// ---------------------------------------------------------------------------
+// Streaming NT tile GEMM for the big cells (64 x 64 output tile per CTA, K streamed in
+// 32-wide chunks through a 3-stage cp.async pipeline, DMMA m8n8k4, 2 CTAs per SM):
+//  MODE 0: trailing update P[r, c] -= sum_{k0 <= k < k0+kw} P[r, k] P[c, k] for rows and
+//          columns >= base = k0 + kw (tile (i, j) of that trailing block)
+//  MODE 1: U = X^T X (X = rows n..n+b of P, K = n), lower tiles only, mirrored on write
+// ---------------------------------------------------------------------------
+constexpr int NTK = 32, NTLD = NTK + 4, NT_STAGES = 3;
+constexpr int NT_STAGE = 2 * BT * NTLD;
+constexpr size_t NT_SMEM = (size_t)NT_STAGES * NT_STAGE * sizeof(double);
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
+  extern __shared__ double smem[];
+  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
+  const int n = a.n[c];
+  double* P = a.P[c];
+  int ar0, br0, kbeg, kend, Mv, Nv;
+  if (MODE == 0) {
+    const int base = a.k0 + a.kw;
+    ar0 = base + BT * it;
+    br0 = base + BT * jt;
+    kbeg = a.k0;
+    kend = a.k0 + a.kw;
+    Mv = min(BT, a.rows[c] - ar0);
+    Nv = min(BT, n - br0);
+  } else {
+    const int nb = n + a.b[c];
+    ar0 = n + BT * it;
+    br0 = n + BT * jt;
+    kbeg = 0;
+    kend = n;
+    Mv = min(BT, nb - ar0);
+    Nv = min(BT, nb - br0);
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+  const double* Ab = P + (int64_t)ar0 * n;
+  const double* Bb = P + (int64_t)br0 * n;
+  auto load = [&](int st, int kc) {
+    double* sA = smem + st * NT_STAGE;
+    double* sB = sA + BT * NTLD;
+#pragma unroll
+    for (int q = 0; q < (BT * NTK) / NT; ++q) {
+      const int e = tid + q * NT, r = e / NTK, kk = e % NTK;
+      const int gk = kc + kk;
+      const bool okA = r < Mv && gk < kend, okB = r < Nv && gk < kend;
+      cp_async8(sA + r * NTLD + kk, Ab + (okA ? (int64_t)r * n + gk : 0), okA);
+      cp_async8(sB + r * NTLD + kk, Bb + (okB ? (int64_t)r * n + gk : 0), okB);
+    }
+    cp_async_commit();
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int nch = (kend - kbeg + NTK - 1) / NTK;
+  load(0, kbeg);
+  if (nch > 1) load(1, kbeg + NTK);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 2 < nch) {
+      load((ch + 2) % NT_STAGES, kbeg + (ch + 2) * NTK);
+      cp_async_wait<2>();
+    } else if (ch + 1 < nch) {
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* sA = smem + (ch % NT_STAGES) * NT_STAGE;
+    const double* sB = sA + BT * NTLD;
+#pragma unroll
+    for (int ks = 0; ks < NTK; ks += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) af[x] = sA[(wm * 16 + x * 8 + g) * NTLD + ks + t];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bf[y] = sB[(wn * 32 + y * 8 + g) * NTLD + ks + t];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
+        if (i < Mv && j < Nv) {
+          if (MODE == 0) {
+            double* p = P + (int64_t)(ar0 + i) * n + br0 + j;
+            *p -= acc[x][y][z];
+          } else {
+            const int b = a.b[c];
+            double* U = a.U[c];
+            U[(int64_t)(BT * it + i) * b + BT * jt + j] = acc[x][y][z];
+            if (it != jt) U[(int64_t)(BT * jt + j) * b + BT * it + i] = acc[x][y][z];
+          }
+        }
+      }
+}
+
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
                    const double* val, int64_t N, cudaStream_t s) {
   if (N == 0) return;
@@ -1972,15 +2037,19 @@ void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& up
     g_launches.fetch_add(1, std::memory_order_relaxed);
     k_big_trsm<<<trsm.nwork, NT, BIG_SMEM, s>>>(trsm);
   }
-  if (upd.nwork) {
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    k_big_update<<<upd.nwork, NT, BIG_SMEM, s>>>(upd);
-  }
+  launch_big_nt(upd, 0, s);
 }
-void launch_big_syrk(const BigArgs& a, cudaStream_t s) {
+void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s) {
   if (!a.nwork) return;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_big_nt<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
+    cudaFuncSetAttribute(k_big_nt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
+    init = true;
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_big_syrk<<<a.nwork, NT, SMEM_BYTES, s>>>(a);
+  if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM, s>>>(a);
+  else k_big_nt<1><<<a.nwork, NT, NT_SMEM, s>>>(a);
 }
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
   if (!nwork) return;
@@ -2084,8 +2153,6 @@ void configure_kernels() {
   cudaFuncSetAttribute(k_apply_skel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_big_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
   cudaFuncSetAttribute(k_big_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
-  cudaFuncSetAttribute(k_big_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
-  cudaFuncSetAttribute(k_big_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_bgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SG_STAGE * sizeof(double)));
 }
 

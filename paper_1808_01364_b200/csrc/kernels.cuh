@@ -161,6 +161,7 @@ struct BigArgs {
   const int* w_j;
   int nwork;
   int k0;                  // current step's panel start
+  int kw;                  // update depth (columns k0 .. k0+kw)
 };
 
 }  // namespace phif
