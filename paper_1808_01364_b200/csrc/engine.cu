@@ -337,6 +337,10 @@ static long long* team_prof_buffer() {
                 buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6, buf[8], buf[11] / 1e6, buf[14] / 1e6, buf[7] / 1e6, buf[15] / 1e6, buf[12] / 1e6, buf[13] / 1e6);
         fprintf(stderr, "[phif] team QR CTA0: update calls %lld [pass1 %.1f Z %.1f pass2 %.1f Mcycles] factor calls %lld waits %lld\n",
                 buf[16], buf[17] / 1e6, buf[18] / 1e6, buf[19] / 1e6, buf[20], buf[21]);
+        fprintf(stderr, "[phif] team QR CTA0 factor: load %.1f columns %.1f G/T %.1f store %.1f Mcycles\n", buf[22] / 1e6,
+                buf[23] / 1e6, buf[24] / 1e6, buf[25] / 1e6);
+        fprintf(stderr, "[phif] team CPQR pass1 CTA0: own-list %.1f chunk-setup %.1f dots %.1f reduce %.1f Mcycles\n",
+                buf[26] / 1e6, buf[27] / 1e6, buf[28] / 1e6, buf[29] / 1e6);
       });
     }
   }
@@ -837,6 +841,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       std::vector<int64_t> small_off(P.nwaves + 1, 0), large_off(P.nwaves + 1, 0), toff_off(P.nwaves + 1, 0),
           slot_off(P.nwaves + 1, 0);
       std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0), wave_kmax(P.nwaves, 0), wave_mmax(P.nwaves, 0);
+      std::vector<int> wave_cluster(P.nwaves, 0);
       for (int w = 0; w < P.nwaves; ++w) {
         std::vector<int> large;
         for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
@@ -884,6 +889,31 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           if (Pv[qm] <= (G.size(P.skeleton[large[qm]]) + 511) / 512) throw std::runtime_error("team CPQR: wave too large");
           --Pv[qm];
           --tot;
+        }
+        // thread-block clusters as teams when every face of the wave gets a co-resident cluster
+        // of comparable size (cluster barriers instead of the global-memory team barrier)
+        if (!large.empty()) {
+          static const char* tmode = getenv("PHIF_TEAM_MODE");   // "coop" | "cluster" | auto
+          const bool force_cl = tmode && !strcmp(tmode, "cluster"), no_cl = tmode && !strcmp(tmode, "coop");
+          const double pmean = (double)tot / large.size();
+          int csel = 0;
+          if (!no_cl)
+            for (int C : {16, 8, 4, 2}) {
+              static std::map<std::pair<size_t, int>, int> cache;
+              const auto key = std::make_pair((size_t)vcap * 100003 + kmax, C);
+              auto itc = cache.find(key);
+              if (itc == cache.end())
+                itc = cache.emplace(key, team_max_clusters(vcap, kmax, team_colcap(vcap, kmax), C)).first;
+              if (itc->second >= (int)large.size()) {
+                if (force_cl || C >= pmean) csel = C;
+                break;
+              }
+            }
+          wave_cluster[w] = csel;
+          if (csel) {
+            for (auto& pv : Pv) pv = csel;
+            tot = csel * (int)large.size();
+          }
         }
         tot = 0;
         for (size_t q = 0; q < large.size(); ++q) {
@@ -944,6 +974,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ta.colcap = team_colcap(wave_vcap[w], wave_kmax[w]);
           ta.qt = qtb.as<double>() + large_off[w] * qt_ld;
           ta.qt_ld = qt_ld;
+          ta.cluster = wave_cluster[w];
           ta.prof = team_prof_buffer();
           launch_skel_team(dv, ka, ta, wave_blocks[w], s);
         }

@@ -526,6 +526,16 @@ __device__ __forceinline__ void team_sync(TeamHdr* h, int P) {
   __syncthreads();
 }
 
+// team barrier: a hardware cluster barrier when the team is a thread-block cluster, else the
+// global-memory barrier above (cooperative launch)
+__device__ __forceinline__ void tsync(TeamHdr* h, int P, bool cl) {
+  if (cl) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    team_sync(h, P);
+  }
+}
+
 constexpr int TCH = 16;      // owned columns updated together per pass
 
 // Copy jb (<= 8) columns of n rows between a global column block (ld gld, L1 bypassed: the
@@ -581,11 +591,16 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
   double* sdot = smem + GEMM_OFF;               // [nw][TCH] partial dots, then [TCH] products
   double* vs = smem + SMEM_DOUBLES;             // reflector (rows > i), vcap doubles
   __shared__ double ovn1[TOWN], ovn2[TOWN];
-  __shared__ int s_rec[TCH], s_nrec, s_nact, s_own[TOWN];
+
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const long long t_kernel0 = clock64();
+  const bool clmode = ta.cluster > 0;
   int f = 0;
-  while (f + 1 < ta.nface && ta.team_off[f + 1] <= (int)blockIdx.x) ++f;
+  if (clmode) {
+    f = blockIdx.x / ta.cluster;
+  } else {
+    while (f + 1 < ta.nface && ta.team_off[f + 1] <= (int)blockIdx.x) ++f;
+  }
   const int c = blockIdx.x - ta.team_off[f];
   const int P = ta.team_off[f + 1] - ta.team_off[f];
   TeamHdr* hdr = ta.hdr + f;
@@ -615,7 +630,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
     const int ch_lo = min(nch, c * per), ch_hi = min(nch, ch_lo + per);
     const int mine = gather_chunks<false>(lv, sk, s, ch_lo, ch_hi, W, ldw, 0, sint, 512);
     if (tid == 0) __stcg(slot_i + c, mine);
-    team_sync(hdr, P);
+    tsync(hdr, P, clmode);
     int before = 0, all = 0;
     for (int q2 = 0; q2 < P; ++q2) {
       const int v = __ldcg(slot_i + q2);
@@ -625,7 +640,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
     m0 = all;
     gather_chunks<true>(lv, sk, s, ch_lo, ch_hi, W, ldw, before, sint, 512);
     if (c == 0 && tid == 0) sk.rows[s] = m0;
-    team_sync(hdr, P);
+    tsync(hdr, P, clmode);
   }
   if (m0 == 0) {
     if (c == 0) skel_all_redundant(lv, sk, s);
@@ -656,14 +671,23 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
     const bool qprof = ta.prof && blockIdx.x == 0 && tid == 0;
     const int g8 = lane >> 2, t4 = lane & 3;
     // factor panel pi (already updated by panels < pi) in smem, write it back and publish it
-    auto factor = [&](int pi) {
+    auto factor = [&](int pi, bool preloaded) {
       long long tq0 = qprof ? clock64() : 0;
       if (qprof) ta.prof[20] += 1;
       const int j0 = pi * nbq, jb = min(nbq, k - j0), ldp = m0 - j0;
       double* Pn = (pi & 1) ? vbuf1 : vbuf0;
       double* Ts = s_T[pi & 1];
-      panel_load<false>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
+      if (!preloaded) panel_load<false>(Pn, W + (int64_t)j0 * ldw + j0, ldw, jb, ldp);
       __syncthreads();
+      long long tf = qprof ? clock64() : 0;
+      auto flap = [&](int slot) {
+        if (qprof) {
+          const long long t1 = clock64();
+          ta.prof[slot] += t1 - tf;
+          tf = t1;
+        }
+      };
+      if (qprof) ta.prof[22] += tf - tq0;
       for (int jj = 0; jj < jb; ++jj) {
         // one reduction per column: |x|^2 and x . a_u (x = column jj below the diagonal)
         double acc[8];
@@ -683,13 +707,16 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
           if (lane == 0) s_red[warp][u] = t2;
         }
         __syncthreads();
-        if (tid == 0) {
+        if (warp == 0) {
+          double mys = 0.0;
+          if (lane < 8) {
+#pragma unroll
+            for (int w2 = 0; w2 < 8; ++w2) mys += s_red[w2][lane];
+          }
           double sum[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            sum[u] = 0.0;
-            for (int w2 = 0; w2 < nw; ++w2) sum[u] += s_red[w2][u];
-          }
+          for (int u = 0; u < 8; ++u) sum[u] = __shfl_sync(0xffffffffu, mys, u);
+          if (lane == 0) {
           const double alpha = xc[jj], xnorm = sqrt(sum[0]);
           double tau = 0.0, beta = alpha, scal = 1.0;
           if (xnorm != 0.0) {
@@ -707,6 +734,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
               au[jj] -= tw;
               s_par[u] = tw * scal;                               // a_u -= tw * scal * x (rows > jj)
             }
+          }
         }
         __syncthreads();
         const double scal = s_par[0];
@@ -722,6 +750,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
         }
         __syncthreads();
       }
+      flap(23);
       // compact WY factor T (upper triangular): H_1 ... H_jb = I - V T V^T, from G = V^T V
       {
         double gp[28];
@@ -744,35 +773,50 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
           if (lane == 0) s_Y[warp][q] = t2;
         }
         __syncthreads();
-        if (tid == 0) {
-          double Gm[8][8], T[8][8];
-          for (int a = 0; a < 8; ++a)
-            for (int b2 = a + 1; b2 < 8; ++b2) {
-              const int q = a * 8 - a * (a + 1) / 2 + (b2 - a - 1);
-              double x = 0.0;
-              for (int w2 = 0; w2 < nw; ++w2) x += s_Y[w2][q];
-              Gm[a][b2] = x;
-            }
-          for (int i2 = 0; i2 < jb; ++i2) {
-            const double ti = Ts[i2 * 8 + i2];
-            for (int a = 0; a < i2; ++a) {
-              double x = 0.0;
-              for (int b2 = a; b2 < i2; ++b2) x += T[a][b2] * Gm[b2][i2];
-              T[a][i2] = -ti * x;
-            }
-            T[i2][i2] = ti;
-            for (int a = i2 + 1; a < 8; ++a) T[a][i2] = 0.0;
+        __shared__ double s_G[8][8];
+        if (tid < 28) {
+          double x = 0.0;
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) x += s_Y[w2][tid];
+          int a = 0, q = tid;
+          while (q >= 7 - a) {
+            q -= 7 - a;
+            ++a;
           }
-          for (int a = 0; a < 8; ++a)
+          s_G[a][a + 1 + q] = x;
+        }
+        __syncthreads();
+        // T(0:i, i) = -tau_i T(0:i, 0:i) G(0:i, i), one column at a time; lane a holds row a
+        if (warp == 0) {
+          const int a = lane;
+          double Trow[8];
+#pragma unroll
+          for (int b2 = 0; b2 < 8; ++b2) Trow[b2] = 0.0;
+#pragma unroll
+          for (int i2 = 0; i2 < 8; ++i2) {
+            if (i2 >= jb) break;
+            const double ti = Ts[i2 * 8 + i2];
+            double x = 0.0;
+#pragma unroll
+            for (int b2 = 0; b2 < 8; ++b2)
+              if (b2 >= a && b2 < i2) x += Trow[b2] * s_G[b2][i2];
+            if (a < i2) Trow[i2] = -ti * x;
+            else if (a == i2) Trow[i2] = ti;
+          }
+          if (a < 8) {
+#pragma unroll
             for (int b2 = 0; b2 < 8; ++b2) {
-              const double v = (a < jb && b2 < jb) ? T[a][b2] : 0.0;
+              const double v = (a < jb && b2 < jb) ? Trow[b2] : 0.0;
               Ts[a * 8 + b2] = v;
               if (a < jb && b2 < jb) __stcg(qt + (int64_t)pi * nbq * nbq + a * nbq + b2, v);
             }
+          }
         }
       }
+      flap(24);
       panel_store(W + (int64_t)j0 * ldw + j0, ldw, Pn, jb, ldp);
       __syncthreads();
+      flap(25);
       if (tid == 0 && P > 1) {
         __threadfence();
         atomicAdd(&hdr->qr_done, 1u);
@@ -790,7 +834,9 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
     // permuted (k-step z takes rows 2t+z) so each lane's B fragments are exactly its C
     // fragments of the transposed update X^T -= Z^T V^T: the block slice stays in registers
     // (QR_TPW tiles per warp; all loads issued at once), only the excess is re-read.
-    auto update = [&](int pi, int b, const double* Vb, const double* Ts) {
+    // Pnext (look-ahead block b = pi+1 of this CTA): rows below the next panel's diagonal go to
+    // the next panel buffer in shared memory instead of global memory (factor() skips its load)
+    auto update = [&](int pi, int b, const double* Vb, const double* Ts, double* Pnext) {
       constexpr int QR_TPW = 40;
       const int j0 = pi * nbq, jb = min(nbq, k - j0), ldp = m0 - j0;
       const int cb0 = b * nbq, ncol = min(nbq, k - cb0);
@@ -867,8 +913,20 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
           dmma(xr[u][0], xr[u][1], za1, vb1);
           const int rr = (t_lo + u) * 8 + 2 * t4;
           if (col_ok) {
-            if (rr < ldp) __stcg(Xc + rr, xr[u][0]);
-            if (rr + 1 < ldp) __stcg(Xc + rr + 1, xr[u][1]);
+            if (Pnext) {
+              const int ldn = ldp - nbq;
+              if (rr < ldp) {
+                if (rr < nbq) __stcg(Xc + rr, xr[u][0]);
+                else Pnext[(int64_t)g8 * ldn + rr - nbq] = xr[u][0];
+              }
+              if (rr + 1 < ldp) {
+                if (rr + 1 < nbq) __stcg(Xc + rr + 1, xr[u][1]);
+                else Pnext[(int64_t)g8 * ldn + rr + 1 - nbq] = xr[u][1];
+              }
+            } else {
+              if (rr < ldp) __stcg(Xc + rr, xr[u][0]);
+              if (rr + 1 < ldp) __stcg(Xc + rr + 1, xr[u][1]);
+            }
           }
         }
       }
@@ -879,14 +937,26 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
         dmma(x0, x1, za0, (b0_ok && rv < ldp) ? V0[rv] : 0.0);
         dmma(x0, x1, za1, (b1_ok && rv < ldp) ? V1[rv] : 0.0);
         if (col_ok) {
-          if (rr < ldp) __stcg(Xc + rr, x0);
-          if (rr + 1 < ldp) __stcg(Xc + rr + 1, x1);
+          if (Pnext) {
+            const int ldn = ldp - nbq;
+            if (rr < ldp) {
+              if (rr < nbq) __stcg(Xc + rr, x0);
+              else Pnext[(int64_t)g8 * ldn + rr - nbq] = x0;
+            }
+            if (rr + 1 < ldp) {
+              if (rr + 1 < nbq) __stcg(Xc + rr + 1, x1);
+              else Pnext[(int64_t)g8 * ldn + rr + 1 - nbq] = x1;
+            }
+          } else {
+            if (rr < ldp) __stcg(Xc + rr, x0);
+            if (rr + 1 < ldp) __stcg(Xc + rr + 1, x1);
+          }
         }
       }
       __syncthreads();
       if (qprof) ta.prof[19] += clock64() - tp0;
     };
-    if (c == 0) factor(0);
+    if (c == 0) factor(0, false);
     for (int pi = 0; pi < npan; ++pi) {
       double* Vb = (pi & 1) ? vbuf1 : vbuf0;
       const double* Ts = s_T[pi & 1];
@@ -916,16 +986,16 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
       long long tu0 = qprof ? clock64() : 0;
       int b = pi + 1 + ((c - (pi + 1)) % P + P) % P;   // first owned block > pi
       if (b == pi + 1 && b < npan) {
-        update(pi, b, Vb, Ts);
+        update(pi, b, Vb, Ts, ((pi + 1) & 1) ? vbuf1 : vbuf0);
         if (qprof) ta.prof[7] += clock64() - tu0;
-        factor(b);
+        factor(b, true);
         tu0 = qprof ? clock64() : 0;
         b += P;
       }
-      for (; b < npan; b += P) update(pi, b, Vb, Ts);
+      for (; b < npan; b += P) update(pi, b, Vb, Ts, nullptr);
       if (qprof) ta.prof[7] += clock64() - tu0;
     }
-    team_sync(hdr, P);
+    tsync(hdr, P, clmode);
     // R0 = rows 0..k-1 of W: clear the reflector entries below the diagonal of owned columns
     for (int t = 0; t < nloc_all(k, c, P); ++t) {
       const int j = c + P * t;
@@ -933,7 +1003,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
       for (int rr = j + 1 + tid; rr < k; rr += NT) __stcg(cj + rr, 0.0);
     }
     m = k;
-    team_sync(hdr, P);
+    tsync(hdr, P, clmode);
   }
   if (ta.prof && blockIdx.x == 0 && tid == 0) ta.prof[11] += clock64() - t_qr0;
   const long long t_cp0 = clock64();
@@ -1001,7 +1071,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
       __stcg(slot_i + par + c, mine.i);
     }
     TEAM_PHASE(0);
-    team_sync(hdr, P);
+    tsync(hdr, P, clmode);
     TEAM_PHASE(1);
     ArgMax cand{-1.0, 0x7fffffff};
     for (int q = tid; q < P; q += NT) cand = better(cand, ArgMax{__ldcg(slot_v + par + q), __ldcg(slot_i + par + q)});
@@ -1042,114 +1112,59 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
     if (i == 0) cut = cutrel * fabs(beta);
     if (c == 0 && tid == 0) __stcg(diagR + i, beta);
     steps = i + 1;
-    // (c) apply H = I - tau [1; v][1; v]^T (v = scal * x) to owned unpivoted columns,
-    //     shared-memory columns first, then streamed ones, TCH at a time
-    if (tid == 0) {
-      int a = 0;
-      for (int t = 0; t < nloc; ++t)
-        if (pos[c + P * t] > i) s_own[a++] = t;
-      s_nact = a;
-    }
-    __syncthreads();
-    const int nact = s_nact;
-    for (int u0 = 0; u0 < nact; u0 += TCH) {
-      const int nown = min(TCH, nact - u0);
-      // chunks never mix residences: cut at the smem/global boundary
-      int nchunk = nown;
-      const bool in_smem = s_own[u0] < ns;
-      for (int u = 1; u < nown; ++u)
-        if ((s_own[u0 + u] < ns) != in_smem) {
-          nchunk = u;
-          break;
-        }
-      double* colp[TCH];
-#pragma unroll
-      for (int u = 0; u < TCH; ++u) {
-        const int t = s_own[u0 + (u < nchunk ? u : 0)];
-        colp[u] = in_smem ? colbuf + (int64_t)t * m : W + (int64_t)(c + P * t) * ldw;
-      }
+    // (c) apply H = I - tau [1; v][1; v]^T (v = scal * x) to the owned unpivoted columns: one
+    //     warp per column (dot, update and the dlaqp2 partial-norm downdate stay in the warp)
+    for (int t = warp; t < nloc; t += nw) {
+      if (pos[c + P * t] <= i) continue;
+      const bool sm = t < ns;
+      double* cj = sm ? colbuf + (int64_t)t * m : W + (int64_t)(c + P * t) * ldw;
+      double rowi = sm ? cj[i] : __ldcg(cj + i);
       if (tau != 0.0) {
-        double acc[TCH];
-#pragma unroll
-        for (int u = 0; u < TCH; ++u) acc[u] = 0.0;
-        for (int r = i + 1 + tid; r < m; r += NT) {
+        double w = 0.0;
+        for (int r = i + 1 + lane; r < m; r += 32) {
           const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
-#pragma unroll
-          for (int u = 0; u < TCH; ++u)
-            if (u < nchunk) acc[u] += vr * (in_smem ? colp[u][r] : __ldcg(colp[u] + r));
+          w += vr * (sm ? cj[r] : __ldcg(cj + r));
         }
-#pragma unroll
-        for (int u = 0; u < TCH; ++u) {
-          const double t2 = warp_sum(acc[u]);
-          if (lane == 0) sdot[warp * TCH + u] = t2;
+        w = warp_sum(w);
+        const double tw = tau * (rowi + scal * w);
+        rowi -= tw;
+        const double tws = tw * scal;
+        for (int r = i + 1 + lane; r < m; r += 32) {
+          const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
+          if (sm) cj[r] -= tws * vr;
+          else __stcg(cj + r, __ldcg(cj + r) - tws * vr);
         }
-      }
-      if (tid == 0) s_nrec = 0;
-      __syncthreads();
-      TEAM_PHASE(in_smem ? 3 : 4);
-      if (tid < nchunk) {
-        const int t = s_own[u0 + tid];
-        double* cj = in_smem ? colbuf + (int64_t)t * m : W + (int64_t)(c + P * t) * ldw;
-        double rowi = in_smem ? cj[i] : __ldcg(cj + i);
-        double tw = 0.0;
-        if (tau != 0.0) {
-          double w = 0.0;
-          for (int qq = 0; qq < nw; ++qq) w += sdot[qq * TCH + tid];
-          tw = tau * (rowi + scal * w);
-          rowi -= tw;
-          if (in_smem) cj[i] = rowi;
+        if (lane == 0) {
+          if (sm) cj[i] = rowi;
           else __stcg(cj + i, rowi);
         }
-        sdot[nw * TCH + tid] = tw * scal;
-        // partial-norm downdate (dlaqp2 loop 10) on the updated pivot-row entry
-        const double v1 = ovn1[t];
-        int rec = 0;
-        if (v1 != 0.0) {
-          double tt = fabs(rowi) / v1;
-          tt = 1.0 - tt * tt;
-          tt = tt < 0.0 ? 0.0 : tt;
-          const double rr = v1 / ovn2[t];
-          if (tt * rr * rr <= tol3z) rec = 1;
-          else ovn1[t] = v1 * sqrt(tt);
-        }
-        s_rec[tid] = rec;
-        if (rec) atomicAdd(&s_nrec, 1);
       }
-      __syncthreads();
-      if (tau != 0.0) {
-        double tw[TCH];
-#pragma unroll
-        for (int u = 0; u < TCH; ++u) tw[u] = (u < nchunk) ? sdot[nw * TCH + u] : 0.0;
-        for (int r = i + 1 + tid; r < m; r += NT) {
-          const double vr = v_in_smem ? vs[r] : __ldcg(cp + r);
-#pragma unroll
-          for (int u = 0; u < TCH; ++u)
-            if (u < nchunk) {
-              if (in_smem) colp[u][r] -= tw[u] * vr;
-              else __stcg(colp[u] + r, __ldcg(colp[u] + r) - tw[u] * vr);
-            }
-        }
+      // partial-norm downdate (dlaqp2 loop 10) on the updated pivot-row entry
+      const double v1 = ovn1[t];
+      bool rec = false;
+      if (v1 != 0.0) {
+        double tt = fabs(rowi) / v1;
+        tt = 1.0 - tt * tt;
+        tt = tt < 0.0 ? 0.0 : tt;
+        const double rr = v1 / ovn2[t];
+        if (tt * rr * rr <= tol3z) rec = true;
+        else if (lane == 0) ovn1[t] = v1 * sqrt(tt);
       }
-      if (s_nrec) {
-        __syncthreads();
-        for (int u = warp; u < nchunk; u += nw) {
-          if (!s_rec[u]) continue;
-          const double* cj = colp[u];
-          double a = 0.0;
-          if (i < m - 1) {
-            for (int r = i + 1 + lane; r < m; r += 32) {
-              const double x = in_smem ? cj[r] : __ldcg(cj + r);
-              a += x * x;
-            }
-            a = sqrt(warp_sum(a));
+      if (rec) {
+        __syncwarp();
+        double a = 0.0;
+        if (i < m - 1) {
+          for (int r = i + 1 + lane; r < m; r += 32) {
+            const double x = sm ? cj[r] : __ldcg(cj + r);
+            a += x * x;
           }
-          if (lane == 0) ovn1[s_own[u0 + u]] = ovn2[s_own[u0 + u]] = a;
+          a = sqrt(warp_sum(a));
         }
+        if (lane == 0) ovn1[t] = ovn2[t] = a;
       }
-      __syncthreads();
-      TEAM_PHASE(in_smem ? 5 : 6);
-      u0 += nchunk - TCH;   // advance by the rows actually processed
     }
+    __syncthreads();
+    TEAM_PHASE(5);
     if (prof) ta.prof[8] += 1;
   }
 #undef TEAM_PHASE
@@ -1160,7 +1175,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
     const int t = (int)(e / steps), r = (int)(e % steps);
     __stcg(W + (int64_t)(c + P * t) * ldw + r, colbuf[(int64_t)t * m + r]);
   }
-  team_sync(hdr, P);
+  tsync(hdr, P, clmode);
   // rank from the diagonal (identical on every CTA); natural-order maps by CTA 0
   __shared__ int s_rank;
   if (tid == 0) {
@@ -1179,7 +1194,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
       for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns2++;
     }
   }
-  team_sync(hdr, P);
+  tsync(hdr, P, clmode);
   const int r = s_rank, kt = k - r;
   // T = R11^-1 R12: owned physical columns at logical positions >= r (warp per column)
   for (int ph = c + P * warp; ph < k; ph += P * nw) {
@@ -2018,8 +2033,48 @@ void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, 
   LevelDev lv2 = lv;
   SkelArgs a2 = a;
   TeamArgs t2 = t;
+  if (t.cluster > 0) {
+    if (t.cluster > 8) cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = t.cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(nblocks);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchKernelEx(&cfg, k_skel_team, lv2, a2, t2);
+    return;
+  }
   void* args[] = {&lv2, &a2, &t2};
   cudaLaunchCooperativeKernel((void*)k_skel_team, dim3(nblocks), dim3(NT), args, bytes, s);
+}
+// co-resident clusters of `csize` team CTAs (0 if the cluster cannot be scheduled)
+int team_max_clusters(int vcap, int kmax, int colcap, int csize) {
+  const size_t bytes = team_smem(vcap, kmax, colcap);
+  cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (csize > 8) cudaFuncSetAttribute(k_skel_team, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(csize * 64);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = bytes;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)k_skel_team, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 static constexpr size_t BIG_SMEM = 2 * BT * BLD * sizeof(double);
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s) {

@@ -110,6 +110,7 @@ struct TeamArgs {
   int colcap;            // doubles of shared memory for resident owned columns
   double* qt;            // per team: T factors of the QR panels, qt_ld doubles
   int64_t qt_ld;
+  int cluster;           // > 0: teams are thread-block clusters of this size (cluster barriers)
 };
 
 struct RepackArgs {

@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // Host-side level planner (see planner.h).
 #include "planner.h"
 
@@ -406,12 +409,21 @@ static void adjacency_from_upper(int G, const std::vector<int64_t>& uoff, const 
 }
 
 void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> pairs) {
+  const bool tdbg = getenv("PHIF_PLAN_TIMING") != nullptr;
+  auto tl = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!tdbg) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "  [plan L%d] %-28s %8.2f ms\n", lp.grp.level, what, std::chrono::duration<double, std::milli>(now - tl).count());
+    tl = now;
+  };
   Groups& g = lp.grp;
   lp.level = g.level;
   lp.root = (g.level == s.L);
   for (int i = 0; i < g.G; ++i) pairs.emplace_back(i, i);
   std::vector<int64_t> uoff;
   std::vector<int> unbr;
+  lap("upper lists (stencil)");
   upper_lists(g.G, pairs, uoff, unbr);
   lp.interior.clear();
   lp.precond.clear();
@@ -430,6 +442,7 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       if (unbr[q] != gi && g.kind[unbr[q]] == 0)
         throw std::runtime_error(g.kind[gi] == 0 ? "planner: two interior groups coupled"
                                                  : "planner: interior group is not first in its closure");
+  lap("classify + checks");
   // elimination fill among each cell's boundary groups
   pairs.clear();
   for (int gi = 0; gi < g.G; ++gi)
@@ -441,8 +454,10 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       for (int64_t b = a; b < a1; ++b) pairs.emplace_back(unbr[a], unbr[b]);
     }
   }
+  lap("fill pairs");
   upper_lists(g.G, pairs, uoff, unbr);
   adjacency_from_upper(g.G, uoff, unbr, lp.pat);
+  lap("adjacency");
   const Pattern& pat = lp.pat;
   const int64_t nblocks = (int64_t)pat.bg.size();
   // pool
@@ -453,6 +468,7 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
     acc += (int64_t)g.size(pat.bg[b]) * g.size(pat.bh[b]);
   }
   lp.pool_doubles = acc;
+  lap("pool");
   // cells: boundary = neighbour groups of I (all after I); Schur targets = pairs of them
   const int p = (int)lp.interior.size();
   lp.cell_nbr_off.assign(p + 1, 0);
@@ -507,6 +523,7 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       }
     }
   }
+  lap("cells + contributions");
   // group contributions by target block (counting sort; stable in cell order)
   std::vector<int64_t> tcnt(nblocks + 1, 0);
   for (int64_t i = 0; i < ncons; ++i) tcnt[ctgt[i] + 1]++;
@@ -531,10 +548,12 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       lp.tgt_off.push_back(tcnt[b + 1]);
     }
   if (lp.tgt_blk.empty()) lp.tgt_off.assign(1, 0);
+  lap("contribution sort");
   // block Jacobi scaling targets
   lp.scale_blk.clear();
   for (size_t b = 0; b < pat.bg.size(); ++b)
     if (pat.bg[b] != pat.bh[b] && g.kind[pat.bg[b]] != 0 && g.kind[pat.bh[b]] != 0) lp.scale_blk.push_back((int)b);
+  lap("scale blocks");
   // skeleton neighbours + dependency waves (sequential semantics)
   const int nsk = (int)lp.skeleton.size();
   std::vector<int> sk_index(g.G, -1);
@@ -566,6 +585,7 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
   lp.wave_off.assign(lp.nwaves + 1, 0);
   for (int i = 0; i < nsk; ++i) lp.wave_off[lp.sk_wave[i] + 1]++;
   for (int w = 0; w < lp.nwaves; ++w) lp.wave_off[w + 1] += lp.wave_off[w];
+  lap("skeleton waves");
 }
 
 std::string level_json(const LevelPlan& lp) {
