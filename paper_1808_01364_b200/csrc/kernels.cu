@@ -1178,26 +1178,76 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
   tsync(hdr, P, clmode);
   // rank from the diagonal (identical on every CTA); natural-order maps by CTA 0
   __shared__ int s_rank;
-  if (tid == 0) {
+  {
     const double cutv = cutrel * fabs(__ldcg(diagR));
-    int r = 0;
-    for (int i = 0; i < steps; ++i)
-      if (fabs(__ldcg(diagR + i)) > cutv) ++r;
-    s_rank = r;
-    if (c == 0) {
-      for (int j = 0; j < k; ++j) {
-        flag[j] = 0;
-        perm[j] = inv[j];
-      }
-      for (int i = r; i < k; ++i) flag[inv[i]] = 1;
-      int ns2 = 0, nr = 0;
-      for (int j = 0; j < k; ++j) sidx[j] = flag[j] ? nr++ : ns2++;
+    int cnt = 0;
+    for (int i = tid; i < steps; i += NT) cnt += fabs(__ldcg(diagR + i)) > cutv ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    __shared__ int s_cnt[NT / 32];
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      int r = 0;
+      for (int w2 = 0; w2 < nw; ++w2) r += s_cnt[w2];
+      s_rank = r;
+    }
+    __syncthreads();
+  }
+  if (c == 0) {
+    // redundant flags, permutation and the natural-order skeleton/redundant indices
+    const int r = s_rank;
+    for (int j = tid; j < k; j += NT) {
+      __stcg(flag + j, 0);
+      __stcg(perm + j, inv[j]);
+    }
+    __syncthreads();
+    for (int i = r + tid; i < k; i += NT) __stcg(flag + inv[i], 1);
+    __syncthreads();
+    int* sint = reinterpret_cast<int*>(sred);
+    int base_s = 0, base_r = 0;
+    for (int j0 = 0; j0 < k; j0 += NT) {
+      const int j = j0 + tid;
+      const int fl = j < k ? __ldcg(flag + j) : 0;
+      int tot;
+      const int off = cta_scan_flag(fl, sint, &tot);
+      if (j < k) __stcg(sidx + j, fl ? base_r + off : base_s + (tid - off));
+      base_r += tot;
+      base_s += min(NT, k - j0) - tot;
     }
   }
   tsync(hdr, P, clmode);
   const int r = s_rank, kt = k - r;
-  // T = R11^-1 R12: owned physical columns at logical positions >= r (warp per column)
-  for (int ph = c + P * warp; ph < k; ph += P * nw) {
+  // T = R11^-1 R12: owned physical columns at logical positions >= r (warp per column).
+  // Column-oriented back substitution: the right-hand side stays in registers (lane holds rows
+  // lane + 32q), x_l is broadcast by a shuffle and R11's column l (contiguous, not written in
+  // this phase, so read through L1 and shared by the CTA's warps) updates the rows above l.
+  constexpr int TQ = 16;
+  for (int ph = c + P * warp; ph < k && r <= 32 * TQ; ph += P * nw) {
+    if (pos[ph] < r) continue;
+    double* cj = W + (int64_t)ph * ldw;
+    double bq[TQ];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) bq[q] = lane + 32 * q < r ? __ldcg(cj + lane + 32 * q) : 0.0;
+    for (int l = r - 1; l >= 0; --l) {
+      const int ql = l >> 5, ll = l & 31;
+      double bl = 0.0;
+#pragma unroll
+      for (int q = 0; q < TQ; ++q)
+        if (q == ql) bl = bq[q];
+      const double xl = __shfl_sync(0xffffffffu, bl, ll) / __ldcg(diagR + l);
+      const double* Rl = W + (int64_t)inv[l] * ldw;
+#pragma unroll
+      for (int q = 0; q < TQ; ++q) {
+        const int row = lane + 32 * q;
+        if (row < l) bq[q] -= xl * __ldg(Rl + row);
+        else if (row == l) bq[q] = xl;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < TQ; ++q)
+      if (lane + 32 * q < r) __stcg(cj + lane + 32 * q, bq[q]);
+  }
+  for (int ph = c + P * warp; ph < k && r > 32 * TQ; ph += P * nw) {
     if (pos[ph] < r) continue;
     double* cj = W + (int64_t)ph * ldw;
     for (int l = r - 1; l >= 0; --l) {
