@@ -833,7 +833,40 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     ka.T_off = L.s_T_off.as<int64_t>();
     ka.P_off = L.s_P_off.as<int64_t>();
     if (timing) CK(cudaEventRecord(ev[8], s));
-    {
+    for (int t = 0; t < nsk; ++t)
+      if (P.sk_nbr_off[t + 1] - P.sk_nbr_off[t] > 256)
+        throw std::runtime_error("skeletonize: a separator couples to more than 256 groups");
+    bool any_large = false;
+    for (int t = 0; t < nsk; ++t) {
+      const int kk = G.size(P.skeleton[t]);
+      if (kk > 48 && rows_bound[t] * kk > 100000) any_large = true;
+    }
+    static const bool no_dyn = getenv("PHIF_NO_DYN") != nullptr;
+    if (nsk && !any_large && !no_dyn) {
+      // only small separators: one persistent dependency-driven launch instead of per-wave launches
+      DBuf nd, so, sc, done, next;
+      upload(nd, P.sk_ndep, s);
+      upload(so, P.sk_succ_off, s);
+      upload(sc, P.sk_succ, s);
+      done.alloc(std::max(nsk, 1) * sizeof(int), s, true);
+      next.alloc(sizeof(int), s, true);
+      DynSched ds;
+      ds.count = nsk;
+      ds.next = next.as<int>();
+      ds.done = done.as<int>();
+      ds.ndep = nd.as<int>();
+      ds.succ_off = so.as<int64_t>();
+      ds.succ = sc.as<int>();
+      ka.order = L.s_order.as<int>();
+      int64_t need = 0;
+      for (int t = 0; t < nsk; ++t) {
+        const int64_t kk = G.size(P.skeleton[t]);
+        need = std::max<int64_t>(need, std::max<int64_t>(rows_bound[t], 1) * kk + 4 * kk + 4);
+      }
+      launch_skel_id_dyn(dv, ka, ds, need, s);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));
+    } else {
       // per wave: small separators -> one CTA each; large ones -> gather + team CPQR
       static int num_sms = 0;
       if (!num_sms) CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0));

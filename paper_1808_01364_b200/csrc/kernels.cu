@@ -300,28 +300,67 @@ __device__ int cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double*
 // chunks of 32 rows of one neighbour group (neighbours in order, ceil(|h|/32) chunks each).
 // A warp computes a chunk's keep mask (row alive and with a nonzero in A_{h,I}) from independent
 // coalesced loads; a warp scan of the popcounts places the kept rows; a second sweep copies them.
-__device__ __forceinline__ int skel_nchunks(const LevelDev& lv, const SkelArgs& sk, int s) {
-  int n = 0;
-  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) n += (lv.gsize[sk.nbr[q]] + 31) >> 5;
-  return n;
-}
-struct ChunkCursor {
-  int64_t q;
-  int base;   // first chunk of neighbour q
-  __device__ void locate(const LevelDev& lv, const SkelArgs& sk, int ch) {   // ch non-decreasing
-    for (;;) {
-      const int n = (lv.gsize[sk.nbr[q]] + 31) >> 5;
-      if (ch < base + n) return;
-      base += n;
-      ++q;
+// Coupled-group metadata of one separator, staged in shared memory once (one thread per
+// neighbour) so the chunk sweeps never walk dependent global loads.
+constexpr int NBMAX = 256;
+struct NbrCache {
+  int n, nch, rows;
+  int h[NBMAX], kh[NBMAX], ch0[NBMAX + 1];
+  long long boff[NBMAX], moff[NBMAX];
+  __device__ int locate(int ch) const {   // neighbour holding chunk ch: last i with ch0[i] <= ch
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ch0[mid] <= ch) lo = mid;
+      else hi = mid - 1;
     }
+    return lo;
   }
 };
-__device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArgs& sk, int g, int k, int64_t q,
-                                               int r0) {
+__device__ void nbr_cache_load(const LevelDev& lv, const SkelArgs& sk, int s, NbrCache& nc) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t q0 = sk.nbr_off[s];
+  const int n = (int)(sk.nbr_off[s + 1] - q0);   // <= NBMAX (checked on the host)
+  for (int i = tid; i < n; i += NT) {
+    const int h = sk.nbr[q0 + i];
+    nc.h[i] = h;
+    nc.kh[i] = lv.gsize[h];
+    nc.boff[i] = lv.boff[sk.nbr_blk[q0 + i]];
+    nc.moff[i] = lv.goff[h];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int run_c = 0, run_r = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const int vc = i < n ? (nc.kh[i] + 31) >> 5 : 0, vr = i < n ? nc.kh[i] : 0;
+      int ic = vc, ir = vr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tc = __shfl_up_sync(0xffffffffu, ic, o), tr = __shfl_up_sync(0xffffffffu, ir, o);
+        if (lane >= o) {
+          ic += tc;
+          ir += tr;
+        }
+      }
+      if (i < n) nc.ch0[i] = run_c + ic - vc;
+      run_c += __shfl_sync(0xffffffffu, ic, 31);
+      run_r += __shfl_sync(0xffffffffu, ir, 31);
+    }
+    if (lane == 0) {
+      nc.n = n;
+      nc.nch = run_c;
+      nc.ch0[n] = run_c;
+      nc.rows = run_r > 0 ? run_r : 1;
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArgs& sk, const NbrCache& nc, int g, int k,
+                                               int i, int r0) {
   const int lane = threadIdx.x & 31;
-  const int h = sk.nbr[q], kh = lv.gsize[h];
-  const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+  const int h = nc.h[i], kh = nc.kh[i];
+  const double* B = lv.pool + nc.boff[i];
   const int r = r0 + lane;
   bool nz = false;
   if (g < h) {   // block (g,h) is |g| x |h|: column r of it, lanes along rows (coalesced)
@@ -340,20 +379,30 @@ __device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArg
   } else {       // block (h,g) is |h| x |g|: rows r0..r0+31 are contiguous, lanes along columns
     const int nr = min(32, kh - r0);
     const double* p = B + (int64_t)r0 * k;
-    for (int rr = 0; rr < nr; ++rr) {
-      bool any = false;
-      for (int c = lane; c < k; c += 32) any |= p[(int64_t)rr * k + c] != 0.0;
-      if (__any_sync(0xffffffffu, any) && lane == rr) nz = true;
+    for (int rb = 0; rb < nr; rb += 8) {
+      bool any[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) any[u] = false;
+      for (int c = lane; c < k; c += 32) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = rb + u < nr ? p[(int64_t)(rb + u) * k + c] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) any[u] |= v[u] != 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (__any_sync(0xffffffffu, any[u]) && lane == rb + u) nz = true;
     }
   }
-  const bool alive = r < kh && sk.alive[lv.mem[lv.goff[h] + r]];
+  const bool alive = r < kh && __ldcg(sk.alive + lv.mem[nc.moff[i] + r]);
   return __ballot_sync(0xffffffffu, nz && alive);
 }
-__device__ __forceinline__ void chunk_copy(const LevelDev& lv, const SkelArgs& sk, int g, int k, int64_t q, int r0,
+__device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& nc, int g, int k, int i, int r0,
                                            unsigned mask, double* W, int64_t ldw, int row0) {
   const int lane = threadIdx.x & 31;
-  const int h = sk.nbr[q], kh = lv.gsize[h];
-  const double* B = lv.pool + lv.boff[sk.nbr_blk[q]];
+  const int h = nc.h[i], kh = nc.kh[i];
+  const double* B = lv.pool + nc.boff[i];
   if (g < h) {
     if ((mask >> lane) & 1u) {
       const int row = row0 + __popc(mask & ((1u << lane) - 1u));
@@ -374,21 +423,20 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const SkelArgs& s
 // Chunks [ch_lo, ch_hi) of separator s: with COPY, kept rows go to W rows base, base+1, ...
 // Returns the number of kept rows (all threads). smem: 2*cap ints.
 template <bool COPY>
-__device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, int s, int ch_lo, int ch_hi, double* W,
-                             int64_t ldw, int base, int* sbuf, int cap) {
+__device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, const NbrCache& nc, int s, int ch_lo, int ch_hi,
+                             double* W, int64_t ldw, int base, int* sbuf, int cap) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const int g = sk.groups[s], k = lv.gsize[g];
   unsigned* smask = reinterpret_cast<unsigned*>(sbuf);
   int* spre = sbuf + cap;
   __shared__ int s_tot;
   int total = 0;
-  ChunkCursor cur{sk.nbr_off[s], 0}, cur2{sk.nbr_off[s], 0};
   for (int b0 = ch_lo; b0 < ch_hi; b0 += cap) {
     const int nb = min(cap, ch_hi - b0);
-    for (int i = warp; i < nb; i += nw) {
-      cur.locate(lv, sk, b0 + i);
-      const unsigned msk = chunk_mask(lv, sk, g, k, cur.q, 32 * (b0 + i - cur.base));
-      if (lane == 0) smask[i] = msk;
+    for (int j = warp; j < nb; j += nw) {
+      const int i = nc.locate(b0 + j);
+      const unsigned msk = chunk_mask(lv, sk, nc, g, k, i, 32 * (b0 + j - nc.ch0[i]));
+      if (lane == 0) smask[j] = msk;
     }
     __syncthreads();
     if (warp == 0) {
@@ -408,9 +456,9 @@ __device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, int s, int 
     }
     __syncthreads();
     if (COPY)
-      for (int i = warp; i < nb; i += nw) {
-        cur2.locate(lv, sk, b0 + i);
-        chunk_copy(lv, sk, g, k, cur2.q, 32 * (b0 + i - cur2.base), smask[i], W, ldw, base + total + spre[i]);
+      for (int j = warp; j < nb; j += nw) {
+        const int i = nc.locate(b0 + j);
+        chunk_copy(lv, nc, g, k, i, 32 * (b0 + j - nc.ch0[i]), smask[j], W, ldw, base + total + spre[j]);
       }
     total += s_tot;
     __syncthreads();
@@ -418,11 +466,6 @@ __device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, int s, int 
   return total;
 }
 
-__device__ __forceinline__ int64_t skel_ldw(const LevelDev& lv, const SkelArgs& sk, int s) {
-  int64_t rows_max = 0;
-  for (int64_t q = sk.nbr_off[s]; q < sk.nbr_off[s + 1]; ++q) rows_max += lv.gsize[sk.nbr[q]];
-  return rows_max > 0 ? rows_max : 1;
-}
 
 // no coupling: every column redundant (kernels.py:95-98)
 __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s) {
@@ -435,19 +478,20 @@ __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s
   if (threadIdx.x == 0) sk.rank[s] = 0;
 }
 
-__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int smem_cap) {
+__device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int smem_cap) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
   int* sint = reinterpret_cast<int*>(smem);  // scan scratch (first doubles are free here)
   const int tid = threadIdx.x;
-  const int s = sk.order[blockIdx.x];
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
   const int64_t gof = lv.goff[g];
   // count the kept rows first: A_{R,I} (ld = m) and its CPQR live in shared memory when they
   // fit, else in the global workspace
-  const int nch = skel_nchunks(lv, sk, s);
-  const int64_t ldw = max(1, gather_chunks<false>(lv, sk, s, 0, nch, nullptr, 1, 0, sint, 512));
+  __shared__ NbrCache nc;
+  nbr_cache_load(lv, sk, s, nc);
+  const int nch = nc.nch;
+  const int64_t ldw = max(1, gather_chunks<false>(lv, sk, nc, s, 0, nch, nullptr, 1, 0, sint, 512));
   const bool local = ldw * k + 4 * (int64_t)k + 4 <= smem_cap;
   double* W = local ? smem + SMEM_DOUBLES : sk.work + sk.work_off[s];
   double* vn1 = W + (int64_t)k * ldw;
@@ -456,7 +500,7 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
   int* perm = iw;
   int* sidx = iw + k;
   int* flag = iw + 2 * k;
-  const int m = gather_chunks<true>(lv, sk, s, 0, nch, W, ldw, 0, sint, 512);
+  const int m = gather_chunks<true>(lv, sk, nc, s, 0, nch, W, ldw, 0, sint, 512);
   if (tid == 0) sk.rows[s] = m;
   uint8_t* red = sk.red + gof;
   if (m == 0) {
@@ -499,6 +543,39 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
     if (flag[j]) sk.alive[lv.mem[gof + j]] = 0;
   }
   if (tid == 0) sk.rank[s] = r;
+}
+
+__global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int smem_cap) {
+  skel_id_one(lv, sk, sk.order[blockIdx.x], smem_cap);
+}
+
+// Persistent, dependency-driven separator IDs (no wave barriers): CTAs take separators in a
+// topological order (the wave order) from a counter, wait until every earlier coupled separator
+// is done, run the ID, then release the later coupled ones. All CTAs are resident, and each
+// waits only for items handed out before its own, so the chain always makes progress.
+__global__ void __launch_bounds__(NT) k_skel_id_dyn(LevelDev lv, SkelArgs sk, int smem_cap, DynSched ds) {
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(ds.next, 1);
+    __syncthreads();
+    const int q = s_item;
+    if (q >= ds.count) break;
+    const int s = sk.order[q];
+    if (threadIdx.x == 0) {
+      volatile int* d = ds.done + s;
+      const int nd = ds.ndep[s];
+      while (*d < nd) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+    skel_id_one(lv, sk, s, smem_cap);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int64_t e = ds.succ_off[s]; e < ds.succ_off[s + 1]; ++e) atomicAdd(ds.done + ds.succ[e], 1);
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -611,7 +688,9 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
   const int64_t gof = lv.goff[g];
-  const int64_t ldw = skel_ldw(lv, sk, s);
+  __shared__ NbrCache nc;
+  nbr_cache_load(lv, sk, s, nc);
+  const int64_t ldw = nc.rows;
   double* W = sk.work + sk.work_off[s];
   int* iw = sk.iwork + sk.iwork_off[s];
   int* perm = iw;
@@ -625,10 +704,10 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
   int m0;
   {
     int* sint = reinterpret_cast<int*>(smem + GEMM_OFF);
-    const int nch = skel_nchunks(lv, sk, s);
+    const int nch = nc.nch;
     const int per = (nch + P - 1) / P;
     const int ch_lo = min(nch, c * per), ch_hi = min(nch, ch_lo + per);
-    const int mine = gather_chunks<false>(lv, sk, s, ch_lo, ch_hi, W, ldw, 0, sint, 512);
+    const int mine = gather_chunks<false>(lv, sk, nc, s, ch_lo, ch_hi, W, ldw, 0, sint, 512);
     if (tid == 0) __stcg(slot_i + c, mine);
     tsync(hdr, P, clmode);
     int before = 0, all = 0;
@@ -638,7 +717,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
       all += v;
     }
     m0 = all;
-    gather_chunks<true>(lv, sk, s, ch_lo, ch_hi, W, ldw, before, sint, 512);
+    gather_chunks<true>(lv, sk, nc, s, ch_lo, ch_hi, W, ldw, before, sint, 512);
     if (c == 0 && tid == 0) sk.rows[s] = m0;
     tsync(hdr, P, clmode);
   }
@@ -2040,10 +2119,28 @@ void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_prec_scale<<<a.nscale, NT, SMEM_BYTES, s>>>(lv, a);
 }
+static long long static_smem(const void* fn) {
+  cudaFuncAttributes fa{};
+  return cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? (long long)fa.sharedSizeBytes : 16 * 1024;
+}
+void launch_skel_id_dyn(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
+                        cudaStream_t s) {
+  if (ds.count == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int64_t cap_max = (227 * 1024 - static_smem((const void*)k_skel_id_dyn) - 1024) / 8 - SMEM_DOUBLES;
+  const int cap = (int)std::min<int64_t>(need_doubles, cap_max);
+  const size_t bytes = SMEM_BYTES + (size_t)cap * sizeof(double);
+  cudaFuncSetAttribute(k_skel_id_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  int per_sm = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_skel_id_dyn, NT, bytes);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = std::max(1, std::min(ds.count, std::max(per_sm, 1) * sms));
+  k_skel_id_dyn<<<grid, NT, bytes, s>>>(lv, a, cap, ds);
+}
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t need_doubles, cudaStream_t s) {
   if (count == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const int64_t cap_max = (225 * 1024) / 8 - SMEM_DOUBLES;   // leave room for static shared memory
+  const int64_t cap_max = (227 * 1024 - static_smem((const void*)k_skel_id) - 1024) / 8 - SMEM_DOUBLES;
   const int cap = (int)std::min<int64_t>(need_doubles, cap_max);
   const size_t bytes = SMEM_BYTES + (size_t)cap * sizeof(double);
   cudaFuncSetAttribute(k_skel_id, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

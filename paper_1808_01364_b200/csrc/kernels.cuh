@@ -88,6 +88,16 @@ struct SkelArgs {
   const int64_t* P_off;      // (kt + r) x kt
 };
 
+// dependency-driven scheduling of separator IDs (k_skel_id_dyn)
+struct DynSched {
+  int count;             // separators (sk.order[0..count) in topological order)
+  int* next;             // work counter (zeroed)
+  int* done;             // per separator: finished earlier coupled separators (zeroed)
+  const int* ndep;       // per separator: earlier coupled separators
+  const int64_t* succ_off;
+  const int* succ;       // later coupled separators
+};
+
 struct TeamHdr {
   unsigned count;
   unsigned gen;

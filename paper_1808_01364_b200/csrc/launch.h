@@ -61,6 +61,8 @@ void launch_prec_build(const LevelDev& lv, const PrecArgs& a, const int* list, i
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s);
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t need_doubles, cudaStream_t s);
+void launch_skel_id_dyn(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
+                        cudaStream_t s);
 int team_colcap(int vcap, int kmax);
 int team_blocks_per_sm(int vcap, int kmax, int colcap);
 void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s);

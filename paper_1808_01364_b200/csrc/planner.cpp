@@ -578,6 +578,26 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
     lp.sk_wave[i] = w;
     lp.nwaves = std::max(lp.nwaves, w + 1);
   }
+  lp.sk_ndep.assign(nsk, 0);
+  lp.sk_succ_off.assign(nsk + 1, 0);
+  for (int i = 0; i < nsk; ++i)
+    for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
+      const int j = sk_index[lp.sk_nbr[q]];
+      if (j >= 0 && j < i) {
+        lp.sk_ndep[i]++;
+        lp.sk_succ_off[j + 1]++;
+      }
+    }
+  for (int i = 0; i < nsk; ++i) lp.sk_succ_off[i + 1] += lp.sk_succ_off[i];
+  lp.sk_succ.assign(lp.sk_succ_off[nsk], 0);
+  {
+    std::vector<int64_t> fill(lp.sk_succ_off.begin(), lp.sk_succ_off.end() - 1);
+    for (int i = 0; i < nsk; ++i)
+      for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
+        const int j = sk_index[lp.sk_nbr[q]];
+        if (j >= 0 && j < i) lp.sk_succ[fill[j]++] = i;
+      }
+  }
   lp.wave_order.resize(nsk);
   std::iota(lp.wave_order.begin(), lp.wave_order.end(), 0);
   std::stable_sort(lp.wave_order.begin(), lp.wave_order.end(),

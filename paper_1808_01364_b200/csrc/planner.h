@@ -73,6 +73,11 @@ struct LevelPlan {
   int nwaves = 0;
   std::vector<int> wave_order;        // skeleton indices sorted by (wave, index)
   std::vector<int64_t> wave_off;      // nwaves+1 into wave_order
+  // dependency graph of the sequential skeletonization: earlier coupled separators (count) and
+  // later coupled separators (lists), for dependency-driven scheduling
+  std::vector<int> sk_ndep;
+  std::vector<int64_t> sk_succ_off;
+  std::vector<int> sk_succ;
 };
 
 // level 0 grouping of all DOFs
