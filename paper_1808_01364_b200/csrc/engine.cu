@@ -724,14 +724,25 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     DBG("level %d: precondition r=%d scale=%d", lev, pa.r, pa.nscale);
     if (do_prec) {
       // small groups: one CTA each; big groups: tile-parallel panels [A_gg ; I] -> [L ; L^-T]
-      std::vector<int> psmall, pbig;
-      for (int t = 0; t < r; ++t) (pn[t] >= BIG_N ? pbig : psmall).push_back(t);
+      std::vector<int> ptiny, psmall, pbig;
+      int tiny_max = 1;
+      for (int t = 0; t < r; ++t) {
+        if (pn[t] <= 32) {
+          ptiny.push_back(t);
+          tiny_max = std::max(tiny_max, pn[t]);
+        } else {
+          (pn[t] >= BIG_N ? pbig : psmall).push_back(t);
+        }
+      }
       L.h_prec_big = pbig;
       upload(L.d_prec_small, psmall, s);
       PrecArgs ps = pa;
       ps.list = L.d_prec_small.as<int>();
       ps.r = (int)psmall.size();
       launch_prec_factor(dv, ps, F->status.as<DevStatus>(), s);
+      DBuf dtiny;
+      upload(dtiny, ptiny, s);
+      launch_prec_factor_warp(dv, pa, dtiny.as<int>(), (int)ptiny.size(), tiny_max, F->status.as<DevStatus>(), s);
       if (!pbig.empty()) {
         DBuf dbig;
         upload(dbig, pbig, s);
@@ -746,21 +757,31 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       DBG("level %d: precondition factor done", lev);
       // two-sided scaling: small blocks by substitution, blocks touching a big group by GEMMs
       // with the explicit inverses: B <- (L_g^-T)^T B L_h^-T
-      std::vector<int> ssmall;
+      std::vector<int> stiny, ssmall;
       std::vector<GemmDesc> d1, d2;
       std::vector<int> w1d, w1t, w2d, w2t;
       int64_t tmp_need = 0;
+      int stiny_max = 1;
       for (size_t q = 0; q < P.scale_blk.size(); ++q) {
         const int b = P.scale_blk[q];
         const int kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
-        if (std::max(kg, kh) < BIG_N) ssmall.push_back((int)q);
-        else tmp_need += (int64_t)kg * kh;
+        if (std::max(kg, kh) <= 32) {
+          stiny.push_back((int)q);
+          stiny_max = std::max(stiny_max, std::max(kg, kh));
+        } else if (std::max(kg, kh) < BIG_N) {
+          ssmall.push_back((int)q);
+        } else {
+          tmp_need += (int64_t)kg * kh;
+        }
       }
       upload(L.d_scale_small, ssmall, s);
       PrecArgs pss = pa;
       pss.scale_list = L.d_scale_small.as<int>();
       pss.nscale = (int)ssmall.size();
       launch_prec_scale(dv, pss, s);
+      DBuf dstiny;
+      upload(dstiny, stiny, s);
+      launch_prec_scale_warp(dv, pa, dstiny.as<int>(), (int)stiny.size(), stiny_max, s);
       if (tmp_need) {
         DBuf tmp;
         tmp.alloc(tmp_need * sizeof(double), s);

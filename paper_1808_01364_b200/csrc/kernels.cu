@@ -137,6 +137,92 @@ __global__ void __launch_bounds__(NT) k_prec_scale(LevelDev lv, PrecArgs pa) {
   cta_trsm_right_lt(Lh, kh, kh, B, kg, kh, smem);
 }
 
+// Small block-Jacobi groups (k <= 32): one warp per group instead of one CTA. Same record
+// as k_prec_factor: [A_gg ; I] -> [L ; L^-T] (row-major, strict upper of L zero), A_gg <- I.
+// Cholesky right-looking in the warp's shared tile (lanes along rows); L^-1 by forward
+// substitution with one right-hand side per lane.
+__global__ void __launch_bounds__(256) k_prec_factor_warp(LevelDev lv, PrecArgs pa, const int* list, int n, int kmax,
+                                                          DevStatus* st) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * 8 + warp;
+  if (idx >= n) return;
+  const int ld = kmax + 1;
+  double* D = smem + (size_t)warp * 2 * kmax * ld;
+  double* X = D + (size_t)kmax * ld;
+  const int t = list[idx];
+  const int g = pa.groups[t], k = lv.gsize[g];
+  double* A = lv.pool + lv.boff[lv.diag_blk[g]];
+  double* L = pa.rec + pa.L_off[t];
+  for (int e = lane; e < k * k; e += 32) D[(e / k) * ld + e % k] = A[e];
+  __syncwarp();
+  for (int j = 0; j < k; ++j) {
+    const double d = D[j * ld + j];
+    if (!(d > 0.0)) {   // same value on every lane: pivot <= 0 or NaN
+      if (lane == 0) report_bad(st, t, j);
+      return;
+    }
+    const double ljj = sqrt(d);
+    __syncwarp();
+    if (lane > j && lane < k) D[lane * ld + j] /= ljj;
+    __syncwarp();
+    if (lane == j) D[j * ld + j] = ljj;
+    if (lane > j && lane < k) {
+      const double lij = D[lane * ld + j];
+      for (int c = j + 1; c <= lane; ++c) D[lane * ld + c] -= lij * D[c * ld + j];
+    }
+    __syncwarp();
+  }
+  // X = L^-1: column `lane`
+  if (lane < k)
+    for (int i = 0; i < k; ++i) {
+      double v = (i == lane) ? 1.0 : 0.0;
+      for (int p = lane; p < i; ++p) v -= D[i * ld + p] * X[p * ld + lane];
+      X[i * ld + lane] = i < lane ? 0.0 : v / D[i * ld + i];
+    }
+  __syncwarp();
+  for (int e = lane; e < k * k; e += 32) {
+    const int i = e / k, c = e % k;
+    L[e] = c <= i ? D[i * ld + c] : 0.0;
+    L[(int64_t)k * k + e] = X[c * ld + i];   // (L^-T)[i][c] = (L^-1)[c][i]
+    A[e] = i == c ? 1.0 : 0.0;
+  }
+}
+
+// Small two-sided scaling B <- L_g^-1 B L_h^-T (kg, kh <= 32), one warp per block, with the
+// explicit inverses U = L^-T stored after each factor: L_g^-1 = U_g^T.
+__global__ void __launch_bounds__(256) k_prec_scale_warp(LevelDev lv, PrecArgs pa, const int* list, int n, int ldmax) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * 8 + warp;
+  if (idx >= n) return;
+  const int ld = ldmax + 1;
+  double* S = smem + (size_t)warp * ldmax * ld;
+  const int blk = pa.scale_blk[list[idx]];
+  const int g = lv.bg[blk], h = lv.bh[blk];
+  const int kg = lv.gsize[g], kh = lv.gsize[h];
+  double* B = lv.pool + lv.boff[blk];
+  const double* UG = pa.rec + pa.L_off_of_group[g] + (int64_t)kg * kg;
+  const double* UH = pa.rec + pa.L_off_of_group[h] + (int64_t)kh * kh;
+  for (int e = lane; e < kg * kh; e += 32) S[(e / kh) * ld + e % kh] = B[e];
+  __syncwarp();
+  if (lane < kh)   // column lane: B[i][j] <- sum_{p <= i} U_g[p][i] B[p][j], rows descending (in place)
+    for (int i = kg - 1; i >= 0; --i) {
+      double v = 0.0;
+      for (int p = 0; p <= i; ++p) v += __ldg(UG + (int64_t)p * kg + i) * S[p * ld + lane];
+      S[i * ld + lane] = v;
+    }
+  __syncwarp();
+  if (lane < kg)   // row lane: B[i][j] <- sum_{p <= j} B[i][p] U_h[p][j], columns descending
+    for (int j = kh - 1; j >= 0; --j) {
+      double v = 0.0;
+      for (int p = 0; p <= j; ++p) v += S[lane * ld + p] * __ldg(UH + (int64_t)p * kh + j);
+      S[lane * ld + j] = v;
+    }
+  __syncwarp();
+  for (int e = lane; e < kg * kh; e += 32) B[e] = S[(e / kh) * ld + e % kh];
+}
+
 // ---------------------------------------------------------------------------
 // Stage 3a: interpolative decomposition of A_{R,I}, one wave of mutually
 // independent separators (kernels.py:84-119).
@@ -2113,6 +2199,21 @@ void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cu
   if (a.r == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_prec_factor<<<a.r, NT, SMEM_BYTES, s>>>(lv, a, st);
+}
+void launch_prec_factor_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int kmax, DevStatus* st,
+                             cudaStream_t s) {
+  if (n == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const size_t bytes = (size_t)8 * 2 * kmax * (kmax + 1) * sizeof(double);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_prec_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_prec_factor_warp<<<(n + 7) / 8, 256, bytes, s>>>(lv, a, list, n, kmax, st);
+}
+void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int ldmax, cudaStream_t s) {
+  if (n == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const size_t bytes = (size_t)8 * ldmax * (ldmax + 1) * sizeof(double);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_prec_scale_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_prec_scale_warp<<<(n + 7) / 8, 256, bytes, s>>>(lv, a, list, n, ldmax);
 }
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
   if (a.nscale == 0) return;

@@ -60,6 +60,9 @@ void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s);
 void launch_prec_build(const LevelDev& lv, const PrecArgs& a, const int* list, int nbig, cudaStream_t s);
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s);
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
+void launch_prec_factor_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int kmax, DevStatus* st,
+                             cudaStream_t s);
+void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int ldmax, cudaStream_t s);
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t need_doubles, cudaStream_t s);
 void launch_skel_id_dyn(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
                         cudaStream_t s);
