@@ -1,3 +1,5 @@
+#include <future>
+#include <numeric>
 // Host driver: per level plan -> device structures -> batched stage launches.
 //
 // factorize() restates SPEC.md:275-283 (level loop, root Cholesky as the level-L
@@ -433,6 +435,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     L.cell_work_unit = wacc;
     L.wbuf_unit = bacc;
+    DBG("level %d: host: cell descriptors", lev);
     for (int t = 0; t < p; ++t) {
       const double nn = P.cell_n[t], bb = P.cell_b[t];
       L.fl[1] += nn * nn * nn / 3.0 + nn * nn * bb + nn * bb * bb;
@@ -443,31 +446,32 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       L.by[1] += 8.0 * 2.0 * G.size(P.pat.bg[blk]) * G.size(P.pat.bh[blk]);
     }
     for (size_t b = 0; b < P.pat.bg.size(); ++b) L.by[0] += 8.0 * 2.0 * G.size(P.pat.bg[b]) * G.size(P.pat.bh[b]);
-    // boundary reduction lists (x_B -= X^T y in fixed cell order)
-    {
-      // counting sort of wbuf rows by boundary DOF (rows of one DOF stay in cell order)
-      std::vector<int> cnt(sp.N + 1, 0);
-      for (int d : Bdofs) cnt[d + 1]++;
-      std::vector<int> dof;
-      std::vector<int64_t> off;
-      int64_t acc2 = 0;
-      std::vector<int64_t> start(sp.N, 0);
-      for (int64_t d = 0; d < sp.N; ++d) {
-        start[d] = acc2;
-        if (cnt[d + 1]) {
-          dof.push_back((int)d);
-          off.push_back(acc2);
-          acc2 += cnt[d + 1];
-        }
+    // boundary reduction lists (x_B -= X^T y in fixed cell order): only the apply needs them,
+    // so they are built on a host thread while the GPU factors and uploaded after the level loop
+    L.bd_task = std::async(std::launch::async, [Bd = Bdofs]() {
+      // rows of every boundary DOF in cell order: counting sort over the DOF range
+      BdLists out;
+      if (Bd.empty()) {
+        out.off.push_back(0);
+        return out;
       }
-      off.push_back(acc2);
-      std::vector<int> rows(Bdofs.size());
-      for (size_t i = 0; i < Bdofs.size(); ++i) rows[start[Bdofs[i]]++] = (int)i;
-      L.nbd = (int)dof.size();
-      upload(L.bd_dof, dof, s);
-      upload(L.bd_off, off, s);
-      upload(L.bd_rows, rows, s);
-    }
+      const auto mm = std::minmax_element(Bd.begin(), Bd.end());
+      const int lo = *mm.first, span = *mm.second - lo + 1;
+      std::vector<int64_t> start(span + 1, 0);
+      for (int d : Bd) start[d - lo + 1]++;
+      for (int d = 0; d < span; ++d) {
+        if (start[d + 1]) {
+          out.dof.push_back(d + lo);
+          out.off.push_back(start[d]);
+        }
+        start[d + 1] += start[d];
+      }
+      out.off.push_back((int64_t)Bd.size());
+      out.rows.resize(Bd.size());
+      for (size_t i = 0; i < Bd.size(); ++i) out.rows[start[Bd[i] - lo]++] = (int)i;
+      return out;
+    });
+    DBG("level %d: host: boundary reduction lists", lev);
     // precondition records
     const int r = P.root ? 0 : (int)P.precond.size();
     const bool do_prec = (method != 0) && !P.root;
@@ -503,6 +507,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         L.by[2] += 8.0 * 2.0 * kg * kh;
       }
     }
+    DBG("level %d: host: precondition records", lev);
     // skeleton records / workspaces (upper bounds; ranks known after the ID)
     const int nsk = P.root ? 0 : (int)P.skeleton.size();
     std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk), rows_bound(nsk);
@@ -1126,6 +1131,16 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   }
   CK(cudaStreamSynchronize(s));
   F->t_factor_ms = ms_since(t_start);
+  for (auto& lvp : F->levels) {
+    LevelRT& L = *lvp;
+    if (!L.bd_task.valid()) continue;
+    BdLists bl = L.bd_task.get();
+    L.nbd = (int)bl.dof.size();
+    upload(L.bd_dof, bl.dof, s);
+    upload(L.bd_off, bl.off, s);
+    upload(L.bd_rows, bl.rows, s);
+  }
+  CK(cudaStreamSynchronize(s));
   F->t_plan_ms = plan_ms;
   if (timing)
     for (auto& e : ev) cudaEventDestroy(e);

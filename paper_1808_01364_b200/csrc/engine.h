@@ -6,6 +6,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <future>
 #include <vector>
 
 #include "launch.h"
@@ -57,6 +58,12 @@ struct Matrix {
 
 struct BigApply;   // GEMM replay of big records (engine.cu)
 
+struct BdLists {
+  std::vector<int> dof;
+  std::vector<int64_t> off;
+  std::vector<int> rows;
+};
+
 struct LevelRT {
   LevelPlan plan;
   // structure on device
@@ -68,6 +75,7 @@ struct LevelRT {
   DBuf c_interior, c_nbr_off, c_nbr_blk, c_nbr_col, c_nbr_w, c_n, c_b, c_P_off, c_U_off;
   DBuf c_I_off, c_B, c_B_off, c_work_off;
   DBuf bd_dof, bd_off, bd_rows;
+  std::future<BdLists> bd_task;   // built on a host thread during the factorization
   std::vector<int> h_small_cells, h_big_cells;
   std::vector<int64_t> h_P_off, h_I_off, h_B_off, h_cwork;
   DBuf d_small_cells;
