@@ -1041,13 +1041,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(s));
     }
-    if (timing) CK(cudaEventRecord(ev[9], s));
-    DBG("level %d: skeleton update nsk=%d waves=%d", lev, nsk, P.nwaves);
-    launch_skel_update(dv, ka, F->status.as<DevStatus>(), s);
-    if (timing) CK(cudaEventRecord(ev[10], s));
-    check_status(*F, lev, ST_SKELETONIZE);
-    DBG("level %d: skeleton update done", lev);
-    // ranks and redundant flags back to the host (planning of the next level)
+    // ranks and redundant flags back to the host (large separator updates, next level planning)
     L.h_rank.resize(nsk);
     std::vector<int> h_rows(nsk);
     std::vector<uint8_t> red(G.mem.size());
@@ -1055,6 +1049,97 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     if (nsk) CK(cudaMemcpyAsync(h_rows.data(), L.s_rows.p, nsk * sizeof(int), cudaMemcpyDeviceToHost, s));
     if (!red.empty()) CK(cudaMemcpyAsync(red.data(), F->red.p, red.size(), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (timing) CK(cudaEventRecord(ev[9], s));
+    DBG("level %d: skeleton update nsk=%d waves=%d", lev, nsk, P.nwaves);
+    {
+      // zeroing + elimination of the redundant DOFs: one CTA per small separator, large ones
+      // (kt >= BIG_N) through gather -> batched GEMMs -> tile Cholesky of the panel -> A_ss -= U
+      std::vector<int> usmall, ubig;
+      for (int t = 0; t < nsk; ++t) {
+        const int kt = G.size(P.skeleton[t]) - L.h_rank[t];
+        if (kt == 0) continue;
+        (kt >= BIG_N ? ubig : usmall).push_back(t);
+      }
+      DBuf dus;
+      upload(dus, usmall, s);
+      launch_skel_update(dv, ka, dus.as<int>(), (int)usmall.size(), F->status.as<DevStatus>(), s);
+      if (!ubig.empty()) {
+        const int nb = (int)ubig.size();
+        std::vector<int> idx, cn(nsk, 0), cb(nsk, 0);
+        std::vector<int64_t> idx_off(nb), U_off_all(nsk, 0), U_off(nb);
+        int64_t uacc = 0;
+        std::vector<GemmDesc> d1, d2, d3;
+        std::vector<int> w1d, w1t, w2d, w2t, w3d, w3t;
+        double* rec0 = L.rec.as<double>();
+        double* wk0 = ka.work;
+        for (int q = 0; q < nb; ++q) {
+          const int t = ubig[q], g = P.skeleton[t], k = G.size(g), r = L.h_rank[t], kt = k - r;
+          idx_off[q] = (int64_t)idx.size();
+          for (int j = 0; j < k; ++j)
+            if (!red[G.off[g] + j]) idx.push_back(j);
+          for (int j = 0; j < k; ++j)
+            if (red[G.off[g] + j]) idx.push_back(j);
+          cn[t] = kt;
+          cb[t] = r;
+          U_off_all[t] = U_off[q] = uacc;
+          uacc += (int64_t)r * r;
+          if (r > 0) {
+            double* Ass = wk0 + work_off[t];
+            double* Asr = Ass + (int64_t)r * r;
+            double* Pn = rec0 + SP_off[t];
+            double* Ast = Pn + (int64_t)kt * kt;
+            const double* T = rec0 + T_off[t];
+            auto add = [&](std::vector<GemmDesc>& d, std::vector<int>& wd, std::vector<int>& wt, GemmDesc gd) {
+              for (int tt = 0; tt < (gd.M + 63) / 64; ++tt) {
+                wd.push_back((int)d.size());
+                wt.push_back(tt);
+              }
+              d.push_back(gd);
+            };
+            add(d1, w1d, w1t, GemmDesc{Ass, T, Ast, r, kt, r, r, kt, kt, 0, -1.0, 1.0});    // A~_st = A_sr - A_ss T
+            add(d2, w2d, w2t, GemmDesc{T, Ast, Pn, kt, kt, r, kt, kt, kt, 1, -1.0, 1.0});   // A_tt -= T^T A~_st
+            add(d3, w3d, w3t, GemmDesc{Asr, T, Pn, kt, kt, r, kt, kt, kt, 1, -1.0, 1.0});   // A_tt -= A_sr^T T
+          }
+        }
+        DBuf dbig, didx, didx_off, dU, dU_off, g1, g2, g3, v1d, v1t, v2d, v2t, v3d, v3t;
+        upload(dbig, ubig, s);
+        upload(didx, idx, s);
+        upload(didx_off, idx_off, s);
+        upload(dU_off, U_off, s);
+        dU.alloc(std::max<int64_t>(uacc, 1) * sizeof(double), s);
+        launch_skel_big_gather(dv, ka, dbig.as<int>(), didx.as<int>(), didx_off.as<int64_t>(), nb, s);
+        upload(g1, d1, s);
+        upload(g2, d2, s);
+        upload(g3, d3, s);
+        upload(v1d, w1d, s);
+        upload(v1t, w1t, s);
+        upload(v2d, w2d, s);
+        upload(v2t, w2t, s);
+        upload(v3d, w3d, s);
+        upload(v3t, w3t, s);
+        launch_bgemm(g1.as<GemmDesc>(), v1d.as<int>(), v1t.as<int>(), (int)w1d.size(), s);
+        launch_bgemm(g2.as<GemmDesc>(), v2d.as<int>(), v2t.as<int>(), (int)w2d.size(), s);
+        launch_bgemm(g3.as<GemmDesc>(), v3d.as<int>(), v3t.as<int>(), (int)w3d.size(), s);
+        BigPlan bps;
+        bps.build(ubig, cn, cb, rec0, SP_off, dU.as<double>(), U_off_all, s);
+        bps.run(F->status.as<DevStatus>(), s);
+        launch_skel_big_post(dv, ka, dbig.as<int>(), didx.as<int>(), didx_off.as<int64_t>(), dU.as<double>(),
+                             dU_off.as<int64_t>(), nb, s);
+        CK(cudaStreamSynchronize(s));
+      }
+    }
+    if (timing) CK(cudaEventRecord(ev[10], s));
+    check_status(*F, lev, ST_SKELETONIZE);
+    DBG("level %d: skeleton update done", lev);
+    CK(cudaStreamSynchronize(s));
+    if (getenv("PHIF_DUMP_SEP")) {
+      FILE* fp = fopen(getenv("PHIF_DUMP_SEP"), lev == 0 ? "w" : "a");
+      if (fp) {
+        for (int t = 0; t < nsk; ++t)
+          fprintf(fp, "%d %d %d %d %d\n", lev, P.sk_wave[t], G.size(P.skeleton[t]), h_rows[t], L.h_rank[t]);
+        fclose(fp);
+      }
+    }
     tp = clk::now();
     alive_mem.assign(G.mem.size(), 0);
     for (int g = 0; g < G.G; ++g)

@@ -1448,10 +1448,10 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
 // Stage 3b: zeroing + elimination of the redundant DOFs.
 // Panel [A~_rr ; A~_sr] ((kt+r) x kt) -> [L~ ; X~^T];  A_ss -= X~^T X~.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, DevStatus* st) {
+__global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, const int* list, DevStatus* st) {
   extern __shared__ double smem[];
   const int tid = threadIdx.x;
-  const int s = blockIdx.x;
+  const int s = list ? list[blockIdx.x] : blockIdx.x;
   const int g = sk.groups[s];
   const int k = lv.gsize[g];
   const int r = sk.rank[s], kt = k - r;
@@ -1509,6 +1509,55 @@ __global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, De
       A[(int64_t)skl[a] * k + skl[b]] = Ass[e];
     }
   }
+}
+
+// Large separators (tile-parallel path): gather [A~_tt ; A~_st ; I] into the record and the
+// work copies A_ss, A_sr (grid-stride over (separator, chunk)); skl/rdl = skeleton and
+// redundant member positions per separator (host-built). The GEMMs, the panel Cholesky and
+// U = X~^T X~ run as batched tile kernels; k_skel_big_post does A_ss -= U.
+__global__ void k_skel_big_gather(LevelDev lv, SkelArgs sk, const int* big, const int* idx, const int64_t* idx_off,
+                                  int nbig, int chunks) {
+  const int bc = blockIdx.x / chunks, ch = blockIdx.x % chunks;
+  if (bc >= nbig) return;
+  const int s = big[bc];
+  const int g = sk.groups[s], k = lv.gsize[g];
+  const int r = sk.rank[s], kt = k - r;
+  const int* skl = idx + idx_off[bc];
+  const int* rdl = skl + r;
+  const double* A = lv.pool + lv.boff[lv.diag_blk[g]];
+  double* Pn = sk.rec + sk.P_off[s];
+  double* Ast = Pn + (int64_t)kt * kt;
+  double* Idr = Ast + (int64_t)r * kt;
+  double* Ass = sk.work + sk.work_off[s];
+  double* Asr = Ass + (int64_t)r * r;
+  const int64_t stride = (int64_t)chunks * blockDim.x;
+  const int64_t e0 = (int64_t)ch * blockDim.x + threadIdx.x;
+  for (int64_t e = e0; e < (int64_t)kt * kt; e += stride) {
+    const int a = (int)(e / kt), b = (int)(e % kt);
+    Pn[e] = A[(int64_t)rdl[a] * k + rdl[b]];
+    Idr[e] = a == b ? 1.0 : 0.0;
+  }
+  for (int64_t e = e0; e < (int64_t)r * r; e += stride) Ass[e] = A[(int64_t)skl[e / r] * k + skl[e % r]];
+  for (int64_t e = e0; e < (int64_t)r * kt; e += stride) {
+    const double v = A[(int64_t)skl[e / kt] * k + rdl[e % kt]];
+    Asr[e] = v;
+    Ast[e] = v;
+  }
+}
+__global__ void k_skel_big_post(LevelDev lv, SkelArgs sk, const int* big, const int* idx, const int64_t* idx_off,
+                                const double* U, const int64_t* U_off, int nbig, int chunks) {
+  const int bc = blockIdx.x / chunks, ch = blockIdx.x % chunks;
+  if (bc >= nbig) return;
+  const int s = big[bc];
+  const int g = sk.groups[s], k = lv.gsize[g];
+  const int r = sk.rank[s];
+  const int* skl = idx + idx_off[bc];
+  double* A = lv.pool + lv.boff[lv.diag_blk[g]];
+  const double* Ass = sk.work + sk.work_off[s];
+  const double* Ub = U + U_off[bc];
+  const int64_t stride = (int64_t)chunks * blockDim.x;
+  for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)r * r; e += stride)
+    A[(int64_t)skl[e / r] * k + skl[e % r]] = Ass[e] - Ub[e];
 }
 
 // ---------------------------------------------------------------------------
@@ -2367,10 +2416,23 @@ void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, c
   const int grid = std::min((nseg + 7) / 8, 148 * 16);
   k_rows<<<grid, 256, 0, s>>>(Y, x, idx, seg_src, seg_dst, seg_len, nseg, k, to_x ? 1 : 0, 1);
 }
-void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s) {
-  if (a.nsk == 0) return;
+void launch_skel_update(const LevelDev& lv, const SkelArgs& a, const int* list, int count, DevStatus* st,
+                        cudaStream_t s) {
+  if (count == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_skel_update<<<a.nsk, NT, SMEM_BYTES, s>>>(lv, a, st);
+  k_skel_update<<<count, NT, SMEM_BYTES, s>>>(lv, a, list, st);
+}
+void launch_skel_big_gather(const LevelDev& lv, const SkelArgs& a, const int* big, const int* idx,
+                            const int64_t* idx_off, int nbig, cudaStream_t s) {
+  if (!nbig) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_skel_big_gather<<<nbig * 64, 256, 0, s>>>(lv, a, big, idx, idx_off, nbig, 64);
+}
+void launch_skel_big_post(const LevelDev& lv, const SkelArgs& a, const int* big, const int* idx, const int64_t* idx_off,
+                          const double* U, const int64_t* U_off, int nbig, cudaStream_t s) {
+  if (!nbig) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_skel_big_post<<<nbig * 32, 256, 0, s>>>(lv, a, big, idx, idx_off, U, U_off, nbig, 32);
 }
 void launch_repack(const RepackArgs& a, cudaStream_t s) {
   if (a.nblk == 0) return;

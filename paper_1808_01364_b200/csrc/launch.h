@@ -76,7 +76,12 @@ void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);   // 0: trailing
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s);
 void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                  const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s);
-void launch_skel_update(const LevelDev& lv, const SkelArgs& a, DevStatus* st, cudaStream_t s);
+void launch_skel_update(const LevelDev& lv, const SkelArgs& a, const int* list, int count, DevStatus* st,
+                        cudaStream_t s);
+void launch_skel_big_gather(const LevelDev& lv, const SkelArgs& a, const int* big, const int* idx,
+                            const int64_t* idx_off, int nbig, cudaStream_t s);
+void launch_skel_big_post(const LevelDev& lv, const SkelArgs& a, const int* big, const int* idx, const int64_t* idx_off,
+                          const double* U, const int64_t* U_off, int nbig, cudaStream_t s);
 void launch_repack(const RepackArgs& a, cudaStream_t s);
 void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s);
 void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd, double* x,

@@ -43,9 +43,12 @@ class DeviceMatrix:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib._lib.phif_matrix_free(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib._lib.phif_matrix_free(h)
+        except (AttributeError, TypeError):   # interpreter shutdown: module globals already gone
+            pass
+        self.handle = None
 
 
 def device_matrix(A, stream=None) -> DeviceMatrix:
@@ -71,9 +74,12 @@ class Factorization:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib._lib is not None:
-            _lib._lib.phif_factor_free(h)
-            self.handle = None
+        try:
+            if h and _lib._lib is not None:
+                _lib._lib.phif_factor_free(h)
+        except (AttributeError, TypeError):   # interpreter shutdown: module globals already gone
+            pass
+        self.handle = None
 
     @property
     def stats(self) -> dict:
