@@ -185,15 +185,27 @@ def dominant_roofline(stats, hbm_peak, fp64_peak):
                 best = (t, lv["level"], si, lv["flops"][si], lv["bytes"][si])
     t_ms, lev, si, fl, by = best
     intensity = fl / by if by else 0.0
+    # measured DRAM traffic per launch of the stage's kernel (ncu --set full, committed profile)
+    traffic, tnote = None, None
+    try:
+        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r01.json")))
+        ent = tj.get(f"level {lev} {names[si]}")
+        if ent:
+            traffic = ent["dram_bytes_per_launch"]
+            tnote = f"dram bytes per {ent['kernel']} launch, {ent['source']}"
+    except (OSError, ValueError, KeyError):
+        pass
     ridge = fp64_peak * 1e12 / (hbm_peak * 1e9)
     if intensity >= ridge:
         ach = fl / (t_ms * 1e-3) / 1e12
         return {"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                "traffic": None, "kernel": f"level {lev} {names[si]}", "time_ms": t_ms, "algorithmic_flops": fl,
+                "traffic": traffic, "traffic_note": tnote, "kernel": f"level {lev} {names[si]}", "time_ms": t_ms,
+                "algorithmic_flops": fl,
                 "algorithmic_bytes": by, "peak_source": "measured cuBLAS DGEMM (profiles/fp64_peak_r01.json)"}
     ach = by / (t_ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-            "traffic": None, "kernel": f"level {lev} {names[si]}", "time_ms": t_ms, "algorithmic_flops": fl,
+            "traffic": traffic, "traffic_note": tnote, "kernel": f"level {lev} {names[si]}", "time_ms": t_ms,
+            "algorithmic_flops": fl,
             "algorithmic_bytes": by, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
 
