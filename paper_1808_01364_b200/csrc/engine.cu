@@ -19,7 +19,15 @@
 
 namespace phif {
 
-constexpr int BIG_N = 192;       // cells with |I| >= BIG_N take the tile-parallel path
+// cells / groups / separators with at least this many DOFs take the tile-parallel paths
+// (PHIF_BIG_CELL / PHIF_BIG_PREC / PHIF_BIG_SEP override, for tuning)
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+static const int BIG_CELL = env_int("PHIF_BIG_CELL", 64);
+static const int BIG_PREC = env_int("PHIF_BIG_PREC", 64);
+static const int BIG_SEP = env_int("PHIF_BIG_SEP", 192);
 constexpr int APPLY_BIG = 96;    // groups with |g| >= APPLY_BIG are replayed by batched GEMMs
 
 static std::chrono::steady_clock::time_point g_dbg_t0 = std::chrono::steady_clock::now();
@@ -650,7 +658,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     CK(cudaMemsetAsync(F->status.p, 0xff, sizeof(DevStatus), s));
     // small cells: one CTA each; big cells (n >= BIG_N): tile-parallel 64-wide steps
     std::vector<int> small_cells, big_cells;
-    for (int t = 0; t < p; ++t) (P.cell_n[t] >= BIG_N ? big_cells : small_cells).push_back(t);
+    for (int t = 0; t < p; ++t) (P.cell_n[t] >= BIG_CELL ? big_cells : small_cells).push_back(t);
     DBG("level %d: cells p=%d (big %zu)", lev, p, big_cells.size());
     upload(L.d_small_cells, small_cells, s);
     L.h_small_cells = small_cells;
@@ -736,7 +744,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ptiny.push_back(t);
           tiny_max = std::max(tiny_max, pn[t]);
         } else {
-          (pn[t] >= BIG_N ? pbig : psmall).push_back(t);
+          (pn[t] >= BIG_PREC ? pbig : psmall).push_back(t);
         }
       }
       L.h_prec_big = pbig;
@@ -773,7 +781,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         if (std::max(kg, kh) <= 32) {
           stiny.push_back((int)q);
           stiny_max = std::max(stiny_max, std::max(kg, kh));
-        } else if (std::max(kg, kh) < BIG_N) {
+        } else if (std::max(kg, kh) < BIG_PREC) {
           ssmall.push_back((int)q);
         } else {
           tmp_need += (int64_t)kg * kh;
@@ -796,7 +804,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           const int b = P.scale_blk[q];
           const int gg = P.pat.bg[b], hh = P.pat.bh[b];
           const int kg = G.size(gg), kh = G.size(hh);
-          if (std::max(kg, kh) < BIG_N) continue;
+          if (std::max(kg, kh) < BIG_PREC) continue;
           double* blk = L.pool.as<double>() + P.boff[b];
           double* T = tmp.as<double>() + to;
           to += (int64_t)kg * kh;
@@ -1058,7 +1066,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       for (int t = 0; t < nsk; ++t) {
         const int kt = G.size(P.skeleton[t]) - L.h_rank[t];
         if (kt == 0) continue;
-        (kt >= BIG_N ? ubig : usmall).push_back(t);
+        (kt >= BIG_SEP ? ubig : usmall).push_back(t);
       }
       DBuf dus;
       upload(dus, usmall, s);
