@@ -12,8 +12,11 @@
  *   apply_inverse(Fz, b)          SPEC.md:293-301    -> phif_apply(mode 0)
  *   apply_ginv(Fz, x)             SPEC.md:302-306    -> phif_apply(mode 1)
  *   apply_ginv_t(Fz, x)           SPEC.md:302-306    -> phif_apply(mode 2)
+ *   apply(Fz, x)  (F x)           SPEC.md:284-292    -> phif_apply(mode 3)
  *   pcg(A, b, precond, tol, maxit) SPEC.md:360-378   -> phif_pcg
  *   estimate_solve_error(A, Fz)   SPEC.md:418-426    -> phif_solve_error
+ *   estimate_apply_error(A, Fz)   SPEC.md:409-417    -> phif_apply_error
+ *   root_condition(Fz)            SPEC.md:311-319    -> phif_root_factor (+ host SVD)
  *   Factorization stats JSON      SPEC.md:341        -> phif_stats_json
  *   skeleton sets of the records  SPEC.md:235        -> phif_skeleton_sets
  *   classify_active(spec, l, S)   hierarchy.py:102   -> phif_classify
@@ -76,7 +79,8 @@ int phif_factorize(const phif_matrix* A, int dim, int n, int m, double eps, int 
                    phif_factor** out, phif_error* err);
 void phif_factor_free(phif_factor* F);
 
-/* x <- op(F) x in place, op: 0 = F^-1, 1 = G^-1, 2 = G^-T. x: N x nrhs. */
+/* x <- op(F) x in place, op: 0 = F^-1 (apply_inverse), 1 = G^-1, 2 = G^-T,
+ * 3 = F (apply), 4 = G^T, 5 = G. x: N x nrhs, host or device. */
 int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err);
 
 /* PCG with F^-1 (F may be NULL for plain CG). b, x: N x nrhs. Per column outputs. */
@@ -86,6 +90,15 @@ int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, i
 /* e_s = ||I - G^-1 A G^-T||_2 by power iteration from host start vector x0 (length N). */
 int phif_solve_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
                      double* value, int* iters, int* converged, double* rel_achieved, phif_error* err);
+
+/* e_a = ||A - F||_2 / ||A||_2 by two power iterations from host start vector x0
+ * (estimate_apply_error). */
+int phif_apply_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
+                     double* value, int* iters, int* converged, double* rel_achieved, phif_error* err);
+
+/* Root Cholesky factor B_L (|S_L| x |S_L| row-major lower) into out (host or device); out = NULL
+ * only sets *n = |S_L|. Used by root_condition. */
+int phif_root_factor(phif_factor* F, double* out, int* n, phif_error* err);
 
 /* Statistics JSON; returns the length needed (excluding NUL), copies at most cap-1 bytes. */
 size_t phif_stats_json(const phif_factor* F, char* buf, size_t cap);

@@ -11,19 +11,19 @@ from .grid import (CONFIGS, CoefficientField, GridSpec, SymSparseMatrix, assembl
                    baseline_field, baseline_problem, baseline_rhs, generate_field)
 
 __all__ = ["GridSpec", "SymSparseMatrix", "CoefficientField", "generate_field", "assemble_operator",
-           "factorize", "apply_inverse", "apply_ginv", "apply_ginv_t", "pcg", "power_norm",
-           "estimate_solve_error", "NotSpdError", "ConfigurationError", "BreakdownError", "EstimationError"]
+           "factorize", "apply_inverse", "apply_ginv", "apply_ginv_t", "apply", "root_condition", "pcg", "power_norm",
+           "estimate_solve_error", "estimate_apply_error", "NotSpdError", "ConfigurationError", "BreakdownError", "EstimationError"]
 
 
 def __getattr__(name):
     # lazy: importing the package must not require the CUDA library (CPU tests)
-    if name in ("factorize", "apply_inverse", "apply_ginv", "apply_ginv_t", "Factorization"):
+    if name in ("factorize", "apply_inverse", "apply_ginv", "apply_ginv_t", "apply", "root_condition", "Factorization"):
         from . import factorization
         return getattr(factorization, name)
     if name in ("pcg", "SolveReport"):
         from . import krylov
         return getattr(krylov, name)
-    if name in ("power_norm", "estimate_solve_error", "NormEstimate"):
+    if name in ("power_norm", "estimate_solve_error", "estimate_apply_error", "NormEstimate"):
         from . import diagnostics
         return getattr(diagnostics, name)
     raise AttributeError(name)

@@ -28,7 +28,8 @@ STAGES = {0: "eliminate", 1: "precondition", 2: "skeletonize", 3: "root"}
 _lib = None
 
 EXPORTS = ("phif_version", "phif_launch_count", "phif_matrix_create", "phif_matrix_free", "phif_factorize", "phif_factor_free",
-           "phif_apply", "phif_pcg", "phif_solve_error", "phif_stats_json", "phif_skeleton_sets",
+           "phif_apply", "phif_pcg", "phif_solve_error", "phif_apply_error", "phif_root_factor", "phif_stats_json",
+           "phif_skeleton_sets",
            "phif_num_levels", "phif_classify", "phif_plan_dryrun")
 
 
@@ -56,6 +57,11 @@ def lib():
     L.phif_solve_error.argtypes = [P, P, P, C.c_double, I, D, C.POINTER(I), C.POINTER(I), D,
                                    C.POINTER(phif_error)]
     L.phif_solve_error.restype = I
+    L.phif_apply_error.argtypes = [P, P, P, C.c_double, I, D, C.POINTER(I), C.POINTER(I), D,
+                                   C.POINTER(phif_error)]
+    L.phif_apply_error.restype = I
+    L.phif_root_factor.argtypes = [P, P, C.POINTER(I), C.POINTER(phif_error)]
+    L.phif_root_factor.restype = I
     L.phif_stats_json.argtypes = [P, C.c_char_p, C.c_size_t]
     L.phif_stats_json.restype = C.c_size_t
     L.phif_skeleton_sets.argtypes = [P, I, P, P, P, P, P]

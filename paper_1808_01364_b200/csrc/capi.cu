@@ -116,6 +116,7 @@ void phif_factor_free(phif_factor* F) { delete F; }
 
 int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err) {
   return guarded(err, [&] {
+    if (mode < 0 || mode > 5) throw std::invalid_argument("phif_apply: mode must be 0..5");
     phif::Factorization& f = *F->f;
     const size_t bytes = (size_t)f.spec.N * nrhs * sizeof(double);
     if (is_device(x)) {
@@ -180,6 +181,21 @@ int phif_solve_error(const phif_matrix* A, phif_factor* F, const double* x0, dou
     *converged = r.converged;
     *rel_achieved = r.rel;
   });
+}
+
+int phif_apply_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
+                     double* value, int* iters, int* converged, double* rel_achieved, phif_error* err) {
+  return guarded(err, [&] {
+    phif::PowerResult r = phif::apply_error(*A->m, *F->f, x0, rel_tol, maxit);
+    *value = r.value;
+    *iters = r.iters;
+    *converged = r.converged;
+    *rel_achieved = r.rel;
+  });
+}
+
+int phif_root_factor(phif_factor* F, double* out, int* n, phif_error* err) {
+  return guarded(err, [&] { *n = phif::root_factor(*F->f, out); });
 }
 
 size_t phif_stats_json(const phif_factor* F, char* buf, size_t cap) {

@@ -1578,9 +1578,58 @@ static ApplySkelArgs skel_args(Factorization& F, LevelRT& L) {
   return a;
 }
 
+// forward replay G^T (up) / G (down) over every record (mode 3: F x = G G^T x, 4: G^T x, 5: G x)
+static void apply_forward(Factorization& F, double* x, int k, int mode) {
+  cudaStream_t s = F.stream;
+  auto fwd_args = [&](LevelRT& L, ApplyCellArgs& c, ApplyPrecArgs& p, ApplySkelArgs& sk) {
+    c = cell_args(F, L);
+    c.p = (int)L.plan.interior.size();
+    p = prec_args(F, L);
+    p.list = nullptr;
+    p.r = (F.method != 0 && !L.plan.root) ? (int)L.plan.precond.size() : 0;
+    sk = skel_args(F, L);
+    sk.list = nullptr;
+    sk.nsk = L.plan.root ? 0 : (int)L.plan.skeleton.size();
+  };
+  if (mode == 3 || mode == 4) {
+    for (auto& lp : F.levels) {
+      LevelRT& L = *lp;
+      ApplyCellArgs c;
+      ApplyPrecArgs p;
+      ApplySkelArgs sk;
+      fwd_args(L, c, p, sk);
+      launch_fwd(&c, nullptr, nullptr, x, k, true, s);
+      if (L.plan.root) break;
+      launch_fwd(nullptr, &p, nullptr, x, k, true, s);
+      launch_fwd(nullptr, nullptr, &sk, x, k, true, s);
+    }
+  }
+  if (mode == 3 || mode == 5) {
+    for (int li = (int)F.levels.size() - 1; li >= 0; --li) {
+      LevelRT& L = *F.levels[li];
+      ApplyCellArgs c;
+      ApplyPrecArgs p;
+      ApplySkelArgs sk;
+      fwd_args(L, c, p, sk);
+      if (!L.plan.root) {
+        launch_fwd(nullptr, nullptr, &sk, x, k, false, s);
+        launch_fwd(nullptr, &p, nullptr, x, k, false, s);
+      }
+      launch_fwd(&c, nullptr, nullptr, x, k, false, s);
+      launch_apply_reduce(L.bd_dof.as<int>(), L.bd_off.as<int64_t>(), L.bd_rows.as<int>(), F.wbuf.as<double>(),
+                          L.nbd, x, k, s);
+    }
+  }
+  CK(cudaGetLastError());
+}
+
 void apply(Factorization& F, double* x, int k, int mode) {
   ensure_work(F, k);
   cudaStream_t s = F.stream;
+  if (mode >= 3) {
+    apply_forward(F, x, k, mode);
+    return;
+  }
   if (mode == 0 || mode == 1) {
     for (auto& lp : F.levels) {
       LevelRT& L = *lp;
@@ -1726,6 +1775,86 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
 // ---------------------------------------------------------------------------
 // e_s = ||I - G^-1 A G^-T||_2 by power iteration
 // ---------------------------------------------------------------------------
+// power iteration ||op||_2 from the host start vector x0 (oracle/diagnostics.py power_norm):
+// est = ||op(x)||, x <- op(x)/est, stop when |est - prev| / est <= rel_tol
+template <typename Op>
+static PowerResult power_norm_dev(int64_t N, cudaStream_t s, const double* x0, double rel_tol, int maxit, Op op) {
+  DBuf X, Y, part, sc;
+  X.alloc(N * sizeof(double), s);
+  Y.alloc(N * sizeof(double), s);
+  part.alloc(dot_part_blocks() * sizeof(double), s);
+  sc.alloc(4 * sizeof(double), s);
+  double* nrm2 = sc.as<double>();
+  CK(cudaMemcpyAsync(X.p, x0, N * sizeof(double), cudaMemcpyHostToDevice, s));
+  launch_dot(X.as<double>(), X.as<double>(), N, 1, part.as<double>(), nrm2, s);
+  launch_scale(X.as<double>(), X.as<double>(), nrm2, N, s);
+  PowerResult pr;
+  double prev = -1.0;
+  for (int it = 1; it <= maxit; ++it) {
+    op(X.as<double>(), Y.as<double>());
+    launch_dot(Y.as<double>(), Y.as<double>(), N, 1, part.as<double>(), nrm2, s);
+    double h;
+    CK(cudaMemcpyAsync(&h, nrm2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double est = std::sqrt(h);
+    pr.iters = it;
+    pr.value = est;
+    if (est == 0.0) {
+      pr.converged = 1;
+      pr.rel = 0.0;
+      return pr;
+    }
+    if (prev >= 0.0) {
+      pr.rel = std::fabs(est - prev) / est;
+      if (pr.rel <= rel_tol) {
+        pr.converged = 1;
+        return pr;
+      }
+    }
+    prev = est;
+    launch_scale(X.as<double>(), Y.as<double>(), nrm2, N, s);
+  }
+  return pr;
+}
+
+// e_a = ||A - F|| / ||A||: two power iterations from the same start vector
+PowerResult apply_error(const Matrix& A, Factorization& F, const double* x0, double rel_tol, int maxit) {
+  cudaStream_t s = F.stream;
+  const int64_t N = A.N;
+  DBuf T;
+  T.alloc(N * sizeof(double), s);
+  const int64_t* rp = A.rowptr.as<int64_t>();
+  const int* ci = A.col.as<int>();
+  const double* va = A.val.as<double>();
+  PowerResult num = power_norm_dev(N, s, x0, rel_tol, maxit, [&](double* X, double* Y) {
+    launch_spmv(rp, ci, va, X, T.as<double>(), N, 1, s);   // T = A x
+    CK(cudaMemcpyAsync(Y, X, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    apply(F, Y, 1, 3);                   // Y = F x
+    launch_xmy(Y, T.as<double>(), N, s);   // Y = A x - F x
+  });
+  PowerResult den = power_norm_dev(N, s, x0, rel_tol, maxit, [&](double* X, double* Y) {
+    launch_spmv(rp, ci, va, X, Y, N, 1, s);
+  });
+  PowerResult r;
+  r.value = den.value > 0.0 ? num.value / den.value : 0.0;
+  r.iters = num.iters + den.iters;
+  r.converged = num.converged && den.converged;
+  r.rel = std::max(num.rel, den.rel);
+  return r;
+}
+
+// root block Cholesky factor B_L (n x n, row-major lower); returns n
+int root_factor(Factorization& F, double* out) {
+  LevelRT& R = *F.levels.back();
+  if (R.plan.interior.empty()) return 0;
+  const int n = R.plan.cell_n[0];
+  if (out)
+    CK(cudaMemcpyAsync(out, R.rec.as<double>() + R.h_P_off[0], (size_t)n * n * sizeof(double), cudaMemcpyDefault,
+                       F.stream));
+  CK(cudaStreamSynchronize(F.stream));
+  return n;
+}
+
 PowerResult solve_error(const Matrix& A, Factorization& F, const double* x0, double rel_tol, int maxit) {
   cudaStream_t s = F.stream;
   const int64_t N = A.N;

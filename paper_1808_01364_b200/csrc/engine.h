@@ -147,5 +147,9 @@ struct PowerResult {
 };
 // e_s: power iteration on x -> x - G^-1 A G^-T x from the start vector x0 (host, length N)
 PowerResult solve_error(const Matrix& A, Factorization& F, const double* x0, double rel_tol, int maxit);
+// e_a = ||A - F|| / ||A|| by two power iterations from x0
+PowerResult apply_error(const Matrix& A, Factorization& F, const double* x0, double rel_tol, int maxit);
+// copy the root Cholesky factor B_L (row-major lower, n x n) to out (host or device; NULL: size only); returns n
+int root_factor(Factorization& F, double* out);
 
 }  // namespace phif

@@ -1907,6 +1907,131 @@ __global__ void __launch_bounds__(NT) k_repack(RepackArgs ra) {
 }
 
 // ---------------------------------------------------------------------------
+// Forward replay: F x = G G^T x (oracle/phif.py _gt/_g). Same records as the
+// inverse replay, multiplied instead of solved. One CTA per record; records of one launch own
+// disjoint DOF sets. Record panels are row-major with a zero strict upper triangle in L, so
+// G^T of a cell is one transposed product P^T [x_I; x_B] and G is P x_I.
+// ---------------------------------------------------------------------------
+// y[col] = sum_rho P[rho][col] * v(rho) over rows [0, nr) of a row-major panel (ld = ncol):
+// threads along columns (coalesced), v(rho) broadcast
+template <typename VF>
+__device__ __forceinline__ double colsum(const double* P, int ld, int nr, int col, VF v) {
+  double a = 0.0;
+  for (int rho = 0; rho < nr; ++rho) a += P[(int64_t)rho * ld + col] * v(rho);
+  return a;
+}
+__device__ __forceinline__ double rowdot(const double* Prow, int n, const double* x, const int* idx, int k, int c) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0;
+  for (int i = lane; i < n; i += 32) a += Prow[i] * x[(int64_t)idx[i] * k + c];
+  return warp_sum(a);
+}
+
+// cells: up = G^T (x_I <- L^T x_I + X x_B), else G (x_B += X^T x_I via wbuf, x_I <- L x_I)
+__global__ void __launch_bounds__(NT) k_fwd_cell(ApplyCellArgs a, double* x, int k, int up) {
+  const int t = blockIdx.x;
+  const int n = a.n[t], b = a.b[t];
+  const int* I = a.I + a.I_off[t];
+  const int* B = a.B + a.B_off[t];
+  const double* P = a.rec + a.P_off[t];
+  double* Y = a.work + a.work_off[t] * k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  for (int c = 0; c < k; ++c) {
+    if (up) {
+      for (int i = tid; i < n; i += NT)
+        Y[i] = colsum(P, n, n + b, i, [&](int rho) {
+          return x[(int64_t)(rho < n ? I[rho] : B[rho - n]) * k + c];
+        });
+      __syncthreads();
+      for (int i = tid; i < n; i += NT) x[(int64_t)I[i] * k + c] = Y[i];
+    } else {
+      for (int rho = warp; rho < n + b; rho += nw) {
+        const double z = rowdot(P + (int64_t)rho * n, n, x, I, k, c);
+        if (lane == 0) {
+          if (rho < n) Y[rho] = z;
+          else a.wbuf[(a.B_off[t] + rho - n) * k + c] = -z;   // the reduction subtracts
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += NT) x[(int64_t)I[i] * k + c] = Y[i];
+    }
+    __syncthreads();
+  }
+}
+
+// block-Jacobi groups: up = G^T (x_I <- L^T x_I), else G (x_I <- L x_I); record [L ; L^-T]
+__global__ void __launch_bounds__(NT) k_fwd_prec(ApplyPrecArgs a, double* x, int k, int up) {
+  const int t = blockIdx.x;
+  const int n = a.n[t];
+  const int* I = a.I + a.I_off[t];
+  const double* L = a.rec + a.L_off[t];
+  double* Y = a.work + a.work_off[t] * k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  for (int c = 0; c < k; ++c) {
+    if (up) {
+      for (int i = tid; i < n; i += NT)
+        Y[i] = colsum(L, n, n, i, [&](int rho) { return x[(int64_t)I[rho] * k + c]; });
+    } else {
+      for (int rho = warp; rho < n; rho += nw) {
+        const double z = rowdot(L + (int64_t)rho * n, n, x, I, k, c);
+        if (lane == 0) Y[rho] = z;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) x[(int64_t)I[i] * k + c] = Y[i];
+    __syncthreads();
+  }
+}
+
+// separators (records T (r x kt) and [L~ ; X~^T ; L~^-T]):
+//  up (G^T): x_S += T x_R ; x_R <- L~^T x_R + X~ x_S
+//  down (G): x_S += X~^T x_R ; x_R <- L~ x_R ; x_R += T^T x_S
+__global__ void __launch_bounds__(NT) k_fwd_skel(ApplySkelArgs a, double* x, int k, int up) {
+  const int t = blockIdx.x;
+  const int r = a.r[t], kt = a.kt[t];
+  if (kt == 0) return;
+  const int* S = a.S + a.S_off[t];
+  const int* R = a.R + a.R_off[t];
+  const double* T = a.rec + a.T_off[t];
+  const double* P = a.rec + a.P_off[t];
+  double* Y = a.work + a.work_off[t] * k;   // r + kt per right-hand side
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  for (int c = 0; c < k; ++c) {
+    if (up) {
+      for (int q = warp; q < r; q += nw) {
+        const double z = rowdot(T + (int64_t)q * kt, kt, x, R, k, c);
+        if (lane == 0) Y[q] = x[(int64_t)S[q] * k + c] + z;
+      }
+      __syncthreads();
+      for (int q = tid; q < r; q += NT) x[(int64_t)S[q] * k + c] = Y[q];
+      __syncthreads();
+      for (int i = tid; i < kt; i += NT)
+        Y[r + i] = colsum(P, kt, kt + r, i, [&](int rho) {
+          return rho < kt ? x[(int64_t)R[rho] * k + c] : Y[rho - kt];
+        });
+      __syncthreads();
+      for (int i = tid; i < kt; i += NT) x[(int64_t)R[i] * k + c] = Y[r + i];
+    } else {
+      for (int rho = warp; rho < kt + r; rho += nw) {
+        const double z = rowdot(P + (int64_t)rho * kt, kt, x, R, k, c);
+        if (lane == 0) {
+          if (rho < kt) Y[r + rho] = z;
+          else Y[rho - kt] = x[(int64_t)S[rho - kt] * k + c] + z;
+        }
+      }
+      __syncthreads();
+      for (int q = tid; q < r; q += NT) x[(int64_t)S[q] * k + c] = Y[q];
+      for (int i = tid; i < kt; i += NT) {
+        double z = Y[r + i];
+        for (int q = 0; q < r; ++q) z += T[(int64_t)q * kt + i] * Y[q];
+        x[(int64_t)R[i] * k + c] = z;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Record replay (apply F^-1, G^-1, G^-T)
 // x is N x k row-major (DOF-major, right-hand sides contiguous).
 // ---------------------------------------------------------------------------
@@ -2456,6 +2581,21 @@ void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaSt
   if (a.r == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_prec_tiny<<<(a.r * 32 + 255) / 256, 256, 0, s>>>(a, x, k, up ? 1 : 0);
+}
+void launch_fwd(const ApplyCellArgs* c, const ApplyPrecArgs* p, const ApplySkelArgs* sk, double* x, int k, bool up,
+                cudaStream_t s) {
+  if (c && c->p) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_fwd_cell<<<c->p, NT, 0, s>>>(*c, x, k, up ? 1 : 0);
+  }
+  if (p && p->r) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_fwd_prec<<<p->r, NT, 0, s>>>(*p, x, k, up ? 1 : 0);
+  }
+  if (sk && sk->nsk) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_fwd_skel<<<sk->nsk, NT, 0, s>>>(*sk, x, k, up ? 1 : 0);
+  }
 }
 void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.nsk == 0) return;

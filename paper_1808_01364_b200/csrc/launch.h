@@ -88,6 +88,9 @@ void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, co
                          int k, cudaStream_t s);
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s);
 void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s);
+// forward replay (F x = G G^T x): one CTA per cell / block-Jacobi group / separator record
+void launch_fwd(const ApplyCellArgs* c, const ApplyPrecArgs* p, const ApplySkelArgs* sk, double* x, int k, bool up,
+                cudaStream_t s);
 void launch_spmv(const int64_t* rowptr, const int* col, const double* val, const double* x, double* y, int64_t N,
                  int k, cudaStream_t s);
 int dot_part_blocks();

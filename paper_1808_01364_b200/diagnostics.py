@@ -60,6 +60,21 @@ def estimate_solve_error(A, Fz: Factorization, rel_tol=1e-2, maxit=200, seed=(0,
     return NormEstimate(val.value, its.value, bool(conv.value), rel.value)
 
 
+def estimate_apply_error(A, Fz: Factorization, rel_tol=1e-2, maxit=200, seed=(0, 12)) -> NormEstimate:
+    """e_a = ||A - F|| / ||A||: two device power iterations from one start vector."""
+    dm = device_matrix(A)
+    x0 = np.ascontiguousarray(np.random.default_rng(list(seed)).standard_normal(dm.N))
+    val = C.c_double()
+    its = C.c_int()
+    conv = C.c_int()
+    rel = C.c_double()
+    err = _lib.phif_error()
+    rc = _lib.lib().phif_apply_error(dm.handle, Fz.handle, _lib.ptr(x0), float(rel_tol), int(maxit),
+                                     C.byref(val), C.byref(its), C.byref(conv), C.byref(rel), C.byref(err))
+    _lib.raise_for(rc, err)
+    return NormEstimate(val.value, its.value, bool(conv.value), rel.value)
+
+
 def estimate_inverse_error(A, Fz: Factorization, rel_tol=1e-2, maxit=200, seed=(0, 14)) -> NormEstimate:
     """||I - A F^-1|| through host callbacks (non-symmetric form; diagnostic only)."""
     csr = getattr(A, "csr", A)

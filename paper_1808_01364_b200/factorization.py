@@ -164,3 +164,51 @@ def apply_ginv(Fz: Factorization, x):
 def apply_ginv_t(Fz: Factorization, x):
     """G^-T x = R_0 ... R_{L-1} B_L^-T x."""
     return _apply(Fz, x, 2)
+
+
+def apply(Fz: Factorization, x):
+    """F x = G G^T x = R_0^-T ... R_{L-1}^-T A_L R_{L-1}^-1 ... R_0^-1 x (PAPER.md eq. eqA):
+    the records replayed in reverse with triangular multiplications."""
+    return _apply(Fz, x, 3)
+
+
+def apply_g(Fz: Factorization, x):
+    """G x (the forward generalized Cholesky factor, F = G G^T)."""
+    return _apply(Fz, x, 5)
+
+
+def apply_g_t(Fz: Factorization, x):
+    """G^T x."""
+    return _apply(Fz, x, 4)
+
+
+ROOT_DENSE_MAX = 5000
+
+
+def root_factor(Fz: Factorization) -> np.ndarray:
+    """The root Cholesky factor B_L (|S_L| x |S_L|, lower), copied to the host."""
+    n = C.c_int()
+    err = _lib.phif_error()
+    L = _lib.lib()
+    rc = L.phif_root_factor(Fz.handle, None, C.byref(n), C.byref(err))
+    _lib.raise_for(rc, err)
+    out = np.zeros((n.value, n.value), dtype=np.float64)
+    if n.value:
+        rc = L.phif_root_factor(Fz.handle, _lib.ptr(out), C.byref(n), C.byref(err))
+        _lib.raise_for(rc, err)
+    return out
+
+
+def root_condition(Fz: Factorization) -> float:
+    """kappa(A_L) of the retained root block: exact, from the singular values of
+    its Cholesky factor (A_L = B_L B_L^T). Refuses |S_L| > 5000 like the reference's size guard."""
+    n = C.c_int()
+    err = _lib.phif_error()
+    rc = _lib.lib().phif_root_factor(Fz.handle, None, C.byref(n), C.byref(err))
+    _lib.raise_for(rc, err)
+    if n.value == 0:
+        return 1.0
+    if n.value > ROOT_DENSE_MAX:
+        raise ConfigurationError(f"root block too large for a dense condition number: |S_L| = {n.value}")
+    s = np.linalg.svd(root_factor(Fz), compute_uv=False)
+    return float((s[0] / s[-1]) ** 2)

@@ -142,3 +142,54 @@ def test_apply_inverse_symmetry_and_ginv_on_gpu():
     assert abs(a - b) <= 1e-12 * abs(a)
     w = gfac.apply_ginv_t(F, gfac.apply_ginv(F, u))
     assert np.linalg.norm(w - gfac.apply_inverse(F, u)) <= 1e-12 * np.linalg.norm(w)
+
+
+# ---- apply (F x), e_a, root_condition --------------------------------
+FWD_CASES = [c for c in CASES if c[0] in ("exact-2d", "phif-2d", "hif-2d", "exact-3d", "phif-3d", "c4-n32")]
+
+
+@pytest.mark.parametrize("name,make,method,eps,tol", FWD_CASES, ids=[c[0] for c in FWD_CASES])
+def test_apply_forward_parity(name, make, method, eps, tol):
+    """F x = G G^T x on the GPU vs the oracle's record replay (oracle/phif.py apply, _g, _gt)."""
+    spec, A = make()
+    Fo = ophif.factorize(A, spec, eps, method)
+    Fg = gfac.factorize(A, spec, eps, method)
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((spec.ndofs, 3))
+    ref = ophif.apply(Fo, X)
+    got = gfac.apply(Fg, X)
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+    gt = ophif._gt(Fo, X.copy())
+    assert np.linalg.norm(gfac.apply_g_t(Fg, X) - gt) <= 1e-10 * np.linalg.norm(gt)
+    g = ophif._g(Fo, X.copy())
+    assert np.linalg.norm(gfac.apply_g(Fg, X) - g) <= 1e-10 * np.linalg.norm(g)
+    # inverse pair and linearity (SPEC.md:288-291,296)
+    x = X[:, 0]
+    back = gfac.apply_inverse(Fg, gfac.apply(Fg, x))
+    assert np.linalg.norm(back - x) <= 1e-9 * np.linalg.norm(x)
+    y = X[:, 1]
+    lin = gfac.apply(Fg, x + y) - gfac.apply(Fg, x) - gfac.apply(Fg, y)
+    assert np.linalg.norm(lin) <= 1e-12 * np.linalg.norm(gfac.apply(Fg, x + y)) * 10
+    if method == "exact":   # SPEC.md:288: ||F x - A x|| / ||A x|| <= 1e-10
+        Ax = A.csr @ x
+        assert np.linalg.norm(gfac.apply(Fg, x) - Ax) <= 1e-10 * np.linalg.norm(Ax)
+
+
+@pytest.mark.parametrize("name,make,method,eps,tol",
+                         [c for c in FWD_CASES if c[0] in ("exact-2d", "phif-2d", "hif-2d", "phif-3d")],
+                         ids=["exact-2d", "phif-2d", "hif-2d", "phif-3d"])
+def test_apply_error_and_root_condition(name, make, method, eps, tol):
+    """e_a = ||A - F|| / ||A|| and kappa(A_L) vs the oracle."""
+    spec, A = make()
+    Fo = ophif.factorize(A, spec, eps, method)
+    Fg = gfac.factorize(A, spec, eps, method)
+    ea_o = odiag.estimate_apply_error(A, Fo)
+    ea_g = gdiag.estimate_apply_error(A, Fg)
+    assert ea_g.converged
+    if method == "exact":
+        assert ea_g.value <= 1e-9
+    else:
+        assert ea_o.value / 2 <= ea_g.value <= 2 * ea_o.value
+    ko = ophif.root_condition(Fo)
+    kg = gfac.root_condition(Fg)
+    assert abs(kg - ko) <= 1e-8 * ko
