@@ -1197,11 +1197,27 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.h_sr = sr;
     L.h_skt = skt;
     {
-      std::vector<int> small_sk, small_pr;
-      for (int t = 0; t < nsk; ++t)
-        if (G.size(P.skeleton[t]) < APPLY_BIG) small_sk.push_back(t);
+      std::vector<int> small_sk, small_pr, tiny_sk;
+      int tiny_rows = 1;
+      for (int t = 0; t < nsk; ++t) {
+        const int kk = G.size(P.skeleton[t]);
+        if (kk <= 64 && sr[t] > 0) {   // warp replay: rows r + 2 k~ staged per warp
+          tiny_sk.push_back(t);
+          tiny_rows = std::max(tiny_rows, sr[t] + 2 * skt[t]);
+        } else if (kk < APPLY_BIG) {
+          small_sk.push_back(t);
+        }
+      }
+      L.n_apply_tiny_sk = (int)tiny_sk.size();
+      L.apply_tiny_rows = tiny_rows;
+      upload(L.d_apply_tiny_sk, tiny_sk, s);
+      int pr_max = 1;
       for (int t = 0; t < r; ++t)
-        if (pn[t] < APPLY_BIG) small_pr.push_back(t);
+        if (pn[t] < APPLY_BIG) {
+          small_pr.push_back(t);
+          pr_max = std::max(pr_max, pn[t]);
+        }
+      L.apply_small_pr_max = pr_max;
       L.n_apply_small_sk = (int)small_sk.size();
       L.n_apply_small_pr = (int)small_pr.size();
       upload(L.d_apply_small_sk, small_sk, s);
@@ -1361,8 +1377,8 @@ struct BigApply {
     upload(gb_len, blen, s);
   }
   void phase(int ph, cudaStream_t s) const {
-    launch_bgemm(desc.as<GemmDesc>(), wd.as<int>() + ph_off[ph], wt.as<int>() + ph_off[ph],
-                 (int)(ph_off[ph + 1] - ph_off[ph]), s);
+    launch_rgemm(desc.as<GemmDesc>(), wd.as<int>() + ph_off[ph], wt.as<int>() + ph_off[ph],
+                 (int)(ph_off[ph + 1] - ph_off[ph]), k, s);
   }
   void up(LevelRT& L, double* x, cudaStream_t s) const {
     launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nseg_i, k,
@@ -1505,7 +1521,7 @@ struct GemmReplay {
   void run(int which, LevelRT& L, double* x, cudaStream_t s) const {
     for (const Step& st : steps[which]) {
       if (st.kind == 2) {
-        launch_bgemm(desc.as<GemmDesc>(), wd.as<int>() + st.off, wt.as<int>() + st.off, (int)st.cnt, s);
+        launch_rgemm(desc.as<GemmDesc>(), wd.as<int>() + st.off, wt.as<int>() + st.off, (int)st.cnt, k, s);
       } else {
         const int* idx = st.idx == 0 ? L.mem.as<int>() : (st.idx == 1 ? L.s_S.as<int>() : L.s_R.as<int>());
         launch_rows(work, x, idx, ss.as<int64_t>() + st.off, sd.as<int64_t>() + st.off, sl.as<int>() + st.off,
@@ -1550,6 +1566,7 @@ static ApplyPrecArgs prec_args(Factorization& F, LevelRT& L) {
   ApplyPrecArgs a;
   a.list = L.d_apply_small_pr.as<int>();
   a.r = (F.method != 0 && !L.plan.root) ? L.n_apply_small_pr : 0;
+  a.ldn = L.apply_small_pr_max;
   a.n = L.p_n.as<int>();
   a.I = L.mem.as<int>();
   a.I_off = L.p_I_off.as<int64_t>();
@@ -1642,6 +1659,8 @@ void apply(Factorization& F, double* x, int k, int mode) {
       launch_apply_prec(prec_args(F, L), x, k, true, s);
       gr->run(0, L, x, s);
       launch_apply_skel(skel_args(F, L), x, k, true, s);
+      launch_apply_skel_warp(skel_args(F, L), L.d_apply_tiny_sk.as<int>(), L.plan.root ? 0 : L.n_apply_tiny_sk, x, k, true,
+                             L.apply_tiny_rows, s);
       gr->run(2, L, x, s);
     }
   }
@@ -1651,6 +1670,8 @@ void apply(Factorization& F, double* x, int k, int mode) {
       if (!L.plan.root) {
         GemmReplay* gr = gemm_replay(F, L, k);
         launch_apply_skel(skel_args(F, L), x, k, false, s);
+        launch_apply_skel_warp(skel_args(F, L), L.d_apply_tiny_sk.as<int>(), L.n_apply_tiny_sk, x, k, false,
+                               L.apply_tiny_rows, s);
         gr->run(3, L, x, s);
         launch_apply_prec(prec_args(F, L), x, k, false, s);
         gr->run(1, L, x, s);

@@ -1738,6 +1738,81 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Replay GEMM for the factor apply (N = nrhs <= 32): C[64-row tile, 0:N] = beta*C + alpha*op(A) B.
+// A (a stored record) is streamed once: each warp's m8n8k4 A fragments are read straight from
+// global memory through the read-only path (8 full 32-byte sectors per load in either storage
+// order); only the small right-hand-side chunk B[kc:kc+64, 0:N] is staged in shared memory.
+// NT8 = ceil(N / 8) output column tiles per warp.
+constexpr int RG_K = 64;
+template <int NT8>
+__global__ void __launch_bounds__(NT) k_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork) {
+  constexpr int LDB = NT8 * 8 + 4;
+  __shared__ double sB[2][RG_K * LDB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const GemmDesc d = desc[w_desc[w]];
+    const int i0 = 64 * w_tile[w];
+    const int row = i0 + warp * 8 + g;
+    const bool rok = row < d.M;
+    const int64_t sr = d.transA ? 1 : d.lda, sk = d.transA ? d.lda : 1;   // A(row, k) = A[row*sr + k*sk]
+    const double* Ar = d.A + (rok ? (int64_t)row * sr : 0);
+    double acc[NT8][2];
+#pragma unroll
+    for (int y = 0; y < NT8; ++y) acc[y][0] = acc[y][1] = 0.0;
+    auto load_a = [&](double* a, int kc) {
+#pragma unroll
+      for (int s = 0; s < RG_K / 4; ++s) {
+        const int kg = kc + 4 * s + t4;
+        a[s] = (rok && kg < d.K) ? __ldg(Ar + (int64_t)kg * sk) : 0.0;
+      }
+    };
+    auto stage_b = [&](int buf, int kc) {
+      for (int e = tid; e < RG_K * NT8 * 8; e += NT) {
+        const int kk = e / (NT8 * 8), c = e % (NT8 * 8);
+        const bool ok = kc + kk < d.K && c < d.N;
+        cp_async8(&sB[buf][kk * LDB + c], d.B + (ok ? (int64_t)(kc + kk) * d.ldb + c : 0), ok);
+      }
+      cp_async_commit();
+    };
+    double a0[RG_K / 4], a1[RG_K / 4];
+    __syncthreads();   // previous work item's reads of sB are done
+    load_a(a0, 0);
+    stage_b(0, 0);
+    int buf = 0;
+    for (int kc = 0; kc < d.K; kc += RG_K) {
+      const bool more = kc + RG_K < d.K;
+      if (more) {
+        load_a(a1, kc + RG_K);
+        stage_b(buf ^ 1, kc + RG_K);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < RG_K / 4; ++s)
+#pragma unroll
+        for (int y = 0; y < NT8; ++y) dmma(acc[y][0], acc[y][1], a0[s], sB[buf][(4 * s + t4) * LDB + y * 8 + g]);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < RG_K / 4; ++s) a0[s] = a1[s];
+      buf ^= 1;
+    }
+    if (rok) {
+#pragma unroll
+      for (int y = 0; y < NT8; ++y)
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+          const int c = y * 8 + 2 * t4 + z;
+          if (c < d.N) {
+            double* p = d.C + (int64_t)row * d.ldc + c;
+            *p = (d.beta == 0.0 ? 0.0 : d.beta * *p) + d.alpha * acc[y][z];
+          }
+        }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile,
                                                int nwork) {
   extern __shared__ double smem[];
@@ -2082,25 +2157,46 @@ __global__ void k_apply_reduce(const int* dof, const int64_t* off, const int* ro
 }
 
 // small block-Jacobi records: one warp per group, dense product with the stored L^-T
-__global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up) {
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int ldn) {
+  // one warp per group (|g| < APPLY_BIG): the group's rows are staged in shared memory, then
+  // y = L^-1 x (up) or L^-T x (down) from the stored L^-T, written straight back to x
+  extern __shared__ double smem[];
+  const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wg = blockIdx.x * wpc + warp;
   if (wg >= a.r) return;
   const int t = a.list ? a.list[wg] : wg;
   const int n = a.n[t];
   const int* I = a.I + a.I_off[t];
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
-  double* Y = a.work + a.work_off[t] * k;
+  if (ldn > 0) {   // few right-hand sides: stage the rows, write straight back
+    double* Y = smem + (size_t)warp * ldn * k;
+    for (int e = lane; e < n * k; e += 32) Y[e] = x[(int64_t)I[e / k] * k + e % k];
+    __syncwarp();
+    for (int e = lane; e < n * k; e += 32) {
+      const int i = e / k, c = e % k;
+      double s = 0.0;
+      if (up)   // y = L^-1 x = (L^-T)^T x, L^-T upper triangular
+        for (int j = 0; j <= i; ++j) s += __ldg(LiT + (int64_t)j * n + i) * Y[j * k + c];
+      else      // y = L^-T x
+        for (int j = i; j < n; ++j) s += __ldg(LiT + (int64_t)i * n + j) * Y[j * k + c];
+      x[(int64_t)I[i] * k + c] = s;
+    }
+    return;
+  }
+  // many right-hand sides: lanes along the right-hand sides read x directly (coalesced),
+  // results buffered in the record's workspace
+  double* Yw = a.work + a.work_off[t] * k;
   for (int e = lane; e < n * k; e += 32) {
     const int i = e / k, c = e % k;
     double s = 0.0;
-    if (up)   // y = L^-1 x = (L^-T)^T x, L^-T upper triangular
-      for (int j = 0; j <= i; ++j) s += LiT[(int64_t)j * n + i] * x[(int64_t)I[j] * k + c];
-    else      // y = L^-T x
-      for (int j = i; j < n; ++j) s += LiT[(int64_t)i * n + j] * x[(int64_t)I[j] * k + c];
-    Y[e] = s;
+    if (up)
+      for (int j = 0; j <= i; ++j) s += __ldg(LiT + (int64_t)j * n + i) * x[(int64_t)I[j] * k + c];
+    else
+      for (int j = i; j < n; ++j) s += __ldg(LiT + (int64_t)i * n + j) * x[(int64_t)I[j] * k + c];
+    Yw[e] = s;
   }
   __syncwarp();
-  for (int e = lane; e < n * k; e += 32) x[(int64_t)I[e / k] * k + e % k] = Y[e];
+  for (int e = lane; e < n * k; e += 32) x[(int64_t)I[e / k] * k + e % k] = Yw[e];
 }
 
 __global__ void __launch_bounds__(NT) k_apply_prec(ApplyPrecArgs a, double* x, int k, int up) {
@@ -2113,6 +2209,78 @@ __global__ void __launch_bounds__(NT) k_apply_prec(ApplyPrecArgs a, double* x, i
   __syncthreads();
   cta_trsm_left(a.rec + a.L_off[t], n, n, Y, k, k, !up, smem);
   scatter_rows(x, Y, I, n, k);
+}
+
+// Small separators (|g| <= 64): one warp per record. The warp stages its rows (skeleton,
+// redundant, and a k~-row temporary) in shared memory, then with the stored L~^-T:
+//   up:   Y_r -= T^T Y_s ; Z = L~^-1 Y_r ; Y_s -= X~^T Z
+//   down: Y_r -= X~ Y_s  ; Z = L~^-T Y_r ; Y_s -= T Z
+// (oracle/phif.py _up/_down, same as k_apply_skel); lanes run over (row, rhs) pairs.
+__global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const int* list, int n, double* x, int k,
+                                                         int up, int ldrows) {
+  extern __shared__ double smem[];
+  const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * wpc + warp;
+  if (idx >= n) return;
+  const int t = list[idx];
+  const int r = a.r[t], kt = a.kt[t];
+  const int* S = a.S + a.S_off[t];
+  const int* R = a.R + a.R_off[t];
+  const double* T = a.rec + a.T_off[t];                     // r x kt
+  const double* PB = a.rec + a.P_off[t] + (int64_t)kt * kt;  // X~^T: r x kt
+  const double* LiT = PB + (int64_t)r * kt;                 // L~^-T: kt x kt (upper)
+  double* Ys = smem + (size_t)warp * ldrows * k;
+  double* Yr = Ys + (size_t)r * k;
+  double* Z = Yr + (size_t)kt * k;
+  for (int e = lane; e < r * k; e += 32) Ys[e] = x[(int64_t)S[e / k] * k + e % k];
+  for (int e = lane; e < kt * k; e += 32) Yr[e] = x[(int64_t)R[e / k] * k + e % k];
+  __syncwarp();
+  if (up) {
+    for (int e = lane; e < kt * k; e += 32) {
+      const int j = e / k, c = e % k;
+      double s = 0.0;
+      for (int q = 0; q < r; ++q) s += __ldg(T + (int64_t)q * kt + j) * Ys[q * k + c];
+      Yr[e] -= s;
+    }
+    __syncwarp();
+    for (int e = lane; e < kt * k; e += 32) {
+      const int i = e / k, c = e % k;
+      double s = 0.0;
+      for (int j = 0; j <= i; ++j) s += __ldg(LiT + (int64_t)j * kt + i) * Yr[j * k + c];
+      Z[e] = s;
+    }
+    __syncwarp();
+    for (int e = lane; e < r * k; e += 32) {
+      const int q = e / k, c = e % k;
+      double s = 0.0;
+      for (int i = 0; i < kt; ++i) s += __ldg(PB + (int64_t)q * kt + i) * Z[i * k + c];
+      Ys[e] -= s;
+    }
+  } else {
+    for (int e = lane; e < kt * k; e += 32) {
+      const int j = e / k, c = e % k;
+      double s = 0.0;
+      for (int q = 0; q < r; ++q) s += __ldg(PB + (int64_t)q * kt + j) * Ys[q * k + c];
+      Yr[e] -= s;
+    }
+    __syncwarp();
+    for (int e = lane; e < kt * k; e += 32) {
+      const int i = e / k, c = e % k;
+      double s = 0.0;
+      for (int j = i; j < kt; ++j) s += __ldg(LiT + (int64_t)i * kt + j) * Yr[j * k + c];
+      Z[e] = s;
+    }
+    __syncwarp();
+    for (int e = lane; e < r * k; e += 32) {
+      const int q = e / k, c = e % k;
+      double s = 0.0;
+      for (int j = 0; j < kt; ++j) s += __ldg(T + (int64_t)q * kt + j) * Z[j * k + c];
+      Ys[e] -= s;
+    }
+  }
+  __syncwarp();
+  for (int e = lane; e < r * k; e += 32) x[(int64_t)S[e / k] * k + e % k] = Ys[e];
+  for (int e = lane; e < kt * k; e += 32) x[(int64_t)R[e / k] * k + e % k] = Z[e];
 }
 
 __global__ void __launch_bounds__(NT) k_apply_skel(ApplySkelArgs a, double* x, int k, int up) {
@@ -2528,6 +2696,18 @@ void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s) {
   if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM, s>>>(a);
   else k_big_nt<1><<<a.nwork, NT, NT_SMEM, s>>>(a);
 }
+void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s) {
+  if (!nwork) return;
+  if (nrhs > 32) {
+    launch_bgemm(desc, w_desc, w_tile, nwork, s);
+    return;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int grid = std::min(nwork, 148 * 16);
+  if (nrhs <= 8) k_rgemm<1><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+  else if (nrhs <= 16) k_rgemm<2><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+  else k_rgemm<4><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+}
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
   if (!nwork) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -2580,7 +2760,16 @@ void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, co
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.r == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_apply_prec_tiny<<<(a.r * 32 + 255) / 256, 256, 0, s>>>(a, x, k, up ? 1 : 0);
+  const int ldn = k <= 4 ? (a.ldn > 0 ? a.ldn : 96) : 0;   // shared-memory staging only for few RHS
+  const size_t per_warp = (size_t)ldn * k * sizeof(double);
+  const int wpc = ldn ? (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp)) : 8;
+  const size_t bytes = per_warp * wpc;
+  static size_t set_bytes = 0;
+  if (bytes > 48 * 1024 && bytes > set_bytes) {
+    cudaFuncSetAttribute(k_apply_prec_tiny, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    set_bytes = bytes;
+  }
+  k_apply_prec_tiny<<<(a.r + wpc - 1) / wpc, 32 * wpc, bytes, s>>>(a, x, k, up ? 1 : 0, ldn);
 }
 void launch_fwd(const ApplyCellArgs* c, const ApplyPrecArgs* p, const ApplySkelArgs* sk, double* x, int k, bool up,
                 cudaStream_t s) {
@@ -2596,6 +2785,20 @@ void launch_fwd(const ApplyCellArgs* c, const ApplyPrecArgs* p, const ApplySkelA
     g_launches.fetch_add(1, std::memory_order_relaxed);
     k_fwd_skel<<<sk->nsk, NT, 0, s>>>(*sk, x, k, up ? 1 : 0);
   }
+}
+void launch_apply_skel_warp(const ApplySkelArgs& a, const int* list, int n, double* x, int k, bool up, int ldrows,
+                            cudaStream_t s) {
+  if (n == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const size_t per_warp = (size_t)ldrows * k * sizeof(double);
+  int wpc = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
+  const size_t bytes = per_warp * wpc;
+  static size_t set_bytes = 0;
+  if (bytes > 48 * 1024 && bytes > set_bytes) {
+    cudaFuncSetAttribute(k_apply_skel_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    set_bytes = bytes;
+  }
+  k_apply_skel_warp<<<(n + wpc - 1) / wpc, 32 * wpc, bytes, s>>>(a, list, n, x, k, up ? 1 : 0, ldrows);
 }
 void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.nsk == 0) return;

@@ -25,6 +25,7 @@ struct ApplyCellArgs {
 
 struct ApplyPrecArgs {
   int r;
+  int ldn;           // largest group of the list (shared-memory staging of the warp kernel)
   const int* list;
   const int* n;
   const int* I;
@@ -74,6 +75,8 @@ void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cel
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
 void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);   // 0: trailing update, 1: U = X^T X
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s);
+// replay GEMM (N = nrhs <= 32, A streamed from global, B chunk in shared memory); falls back to launch_bgemm
+void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s);
 void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                  const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s);
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, const int* list, int count, DevStatus* st,
@@ -88,6 +91,8 @@ void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, co
                          int k, cudaStream_t s);
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s);
 void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaStream_t s);
+void launch_apply_skel_warp(const ApplySkelArgs& a, const int* list, int n, double* x, int k, bool up, int ldrows,
+                            cudaStream_t s);
 // forward replay (F x = G G^T x): one CTA per cell / block-Jacobi group / separator record
 void launch_fwd(const ApplyCellArgs* c, const ApplyPrecArgs* p, const ApplySkelArgs* sk, double* x, int k, bool up,
                 cudaStream_t s);
