@@ -274,7 +274,12 @@ size_t phif_plan_dryrun(int dim, int n, int m, const int64_t* rowptr, const int3
       std::vector<std::pair<int, int>> pairs;
       if (l == 0) {
         P.grp = phif::classify_all(s);
+        auto tc = std::chrono::steady_clock::now();
         pairs = phif::pattern_from_csr(P.grp, s.N, rowptr, col);
+        if (getenv("PHIF_DEBUG"))
+          fprintf(stderr, "level 0: classify %.1f ms pattern %.1f ms\n",
+                  std::chrono::duration<double, std::milli>(tc - t1).count(),
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc).count());
       } else {
         P.grp = phif::classify_next(s, lv[l - 1]->grp, alive);
         pairs = phif::pattern_next(*lv[l - 1], P.grp);

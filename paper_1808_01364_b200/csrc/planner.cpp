@@ -1,4 +1,7 @@
 #include <chrono>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <cstdio>
 #include <cstdlib>
 // Host-side level planner (see planner.h).
@@ -112,12 +115,54 @@ Groups classify_all(const Spec& s) {
       }
       (void)base;
     }
-    for (int64_t i = 0; i < s.N; ++i) cnt[key[i] + 1]++;
+  }
+  // counting sort of the DOFs by key: per-thread histograms over contiguous DOF ranges keep
+  // the members of every key ascending
+  int nth = 1;
+#ifdef _OPENMP
+  nth = omp_get_max_threads();
+#endif
+  std::vector<std::vector<int>> hist(nth);
+  const int64_t chunk = (s.N + nth - 1) / nth;
+#pragma omp parallel num_threads(nth)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    std::vector<int>& h = hist[tid];
+    h.assign(nkeys, 0);
+    const int64_t lo = std::min<int64_t>(s.N, tid * chunk), hi = std::min<int64_t>(s.N, lo + chunk);
+    for (int64_t i = lo; i < hi; ++i) h[key[i]]++;
+  }
+  // cnt[k+1] = total of key k; per-thread starts in place of the histograms
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nkeys; ++k) {
+    int64_t t = 0;
+    for (int q = 0; q < nth; ++q) t += hist[q][k];
+    cnt[k + 1] = t;
   }
   for (int64_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nkeys; ++k) {
+    int64_t o = cnt[k];
+    for (int q = 0; q < nth; ++q) {
+      const int v = hist[q][k];
+      hist[q][k] = (int)o;
+      o += v;
+    }
+  }
   g.mem.resize(s.N);
-  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-  for (int64_t i = 0; i < s.N; ++i) g.mem[fill[key[i]]++] = (int)i;
+#pragma omp parallel num_threads(nth)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    std::vector<int>& h = hist[tid];
+    const int64_t lo = std::min<int64_t>(s.N, tid * chunk), hi = std::min<int64_t>(s.N, lo + chunk);
+    for (int64_t i = lo; i < hi; ++i) g.mem[h[key[i]]++] = (int)i;
+  }
   std::vector<int64_t> gkeys;
   g.off.clear();
   for (int64_t k = 0; k < nkeys; ++k)
@@ -256,26 +301,40 @@ std::vector<std::pair<int, int>> pattern_from_csr(const Groups& g, int64_t N, co
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < g.G; ++i)
     for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) gid[g.mem[p]] = i;
-  std::vector<std::pair<int, int>> pairs;
+  // per group: distinct coupled groups h >= g (a per-thread stamp array dedupes in O(1));
+  // per-thread lists are concatenated in group order
+  int nth = 1;
+#ifdef _OPENMP
+  nth = omp_get_max_threads();
+#endif
+  std::vector<std::vector<std::pair<int, int>>> part(nth);
 #pragma omp parallel
   {
-    std::vector<std::pair<int, int>> mine;
-    std::vector<int> seen;
-#pragma omp for schedule(static) nowait
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    std::vector<std::pair<int, int>>& mine = part[tid];
+    std::vector<int> stamp(g.G, -1);
+#pragma omp for schedule(static)
     for (int i = 0; i < g.G; ++i) {
-      seen.clear();
       for (int64_t p = g.off[i]; p < g.off[i + 1]; ++p) {
         const int r = g.mem[p];
         for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
           const int h = gid[col[e]];
-          if (h >= i && std::find(seen.begin(), seen.end(), h) == seen.end()) seen.push_back(h);
+          if (h >= i && stamp[h] != i) {
+            stamp[h] = i;
+            mine.emplace_back(i, h);
+          }
         }
       }
-      for (int h : seen) mine.emplace_back(i, h);
     }
-#pragma omp critical
-    pairs.insert(pairs.end(), mine.begin(), mine.end());
   }
+  std::vector<std::pair<int, int>> pairs;
+  size_t tot = 0;
+  for (auto& v : part) tot += v.size();
+  pairs.reserve(tot);
+  for (auto& v : part) pairs.insert(pairs.end(), v.begin(), v.end());
   return pairs;
 }
 
@@ -345,16 +404,61 @@ static void build_adjacency(int G, const std::vector<std::pair<int, int>>& pairs
 }
 
 // per-group sorted, de-duplicated "upper" neighbour lists (h >= g) from unsorted pairs
+// Stable parallel counting sort: item i in [0, n) has key(i) in [0, K) (or < 0: dropped). Fills
+// off (K+1) and calls emit(i, pos) with the item's position in key order (stable in i). Per-thread
+// histograms over contiguous item ranges.
+template <class KeyF, class EmitF>
+static void par_bucket(int64_t n, int K, KeyF key, std::vector<int64_t>& off, EmitF emit) {
+  int nth = 1;
+#ifdef _OPENMP
+  nth = omp_get_max_threads();
+#endif
+  const int64_t chunk = (n + nth - 1) / nth;
+  std::vector<std::vector<int64_t>> hist(nth);
+  off.assign((size_t)K + 1, 0);
+#pragma omp parallel num_threads(nth)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    std::vector<int64_t>& h = hist[tid];
+    h.assign(K, 0);
+    const int64_t lo = std::min<int64_t>(n, tid * chunk), hi = std::min<int64_t>(n, lo + chunk);
+    for (int64_t i = lo; i < hi; ++i) {
+      const int k = key(i);
+      if (k >= 0) h[k]++;
+    }
+#pragma omp barrier
+#pragma omp for schedule(static)
+    for (int k = 0; k < K; ++k) {
+      int64_t t = 0;
+      for (int q = 0; q < nth; ++q) t += hist[q][k];
+      off[k + 1] = t;
+    }
+#pragma omp single
+    for (int k = 0; k < K; ++k) off[k + 1] += off[k];
+#pragma omp for schedule(static)
+    for (int k = 0; k < K; ++k) {
+      int64_t o = off[k];
+      for (int q = 0; q < nth; ++q) {
+        const int64_t v = hist[q][k];
+        hist[q][k] = o;
+        o += v;
+      }
+    }
+    for (int64_t i = lo; i < hi; ++i) {
+      const int k = key(i);
+      if (k >= 0) emit(i, h[k]++);
+    }
+  }
+}
+
 static void upper_lists(int G, const std::vector<std::pair<int, int>>& pairs, std::vector<int64_t>& off,
                         std::vector<int>& nbr) {
-  off.assign(G + 1, 0);
-  for (const auto& pr : pairs) off[pr.first + 1]++;
-  for (int i = 0; i < G; ++i) off[i + 1] += off[i];
-  nbr.assign(off[G], 0);
-  {
-    std::vector<int64_t> fill(off.begin(), off.end() - 1);
-    for (const auto& pr : pairs) nbr[fill[pr.first]++] = pr.second;
-  }
+  nbr.assign(pairs.size(), 0);
+  par_bucket((int64_t)pairs.size(), G, [&](int64_t i) { return pairs[i].first; }, off,
+             [&](int64_t i, int64_t pos) { nbr[pos] = pairs[i].second; });
   std::vector<int64_t> keep(G + 1, 0);
 #pragma omp parallel for schedule(dynamic, 256)
   for (int gi = 0; gi < G; ++gi) {
@@ -378,34 +482,48 @@ static void adjacency_from_upper(int G, const std::vector<int64_t>& uoff, const 
   const int64_t nb = uoff[G];
   pat.bg.resize(nb);
   pat.bh.resize(nb);
-  std::vector<int64_t> ndown(G + 1, 0);
+#pragma omp parallel for schedule(static)
   for (int gi = 0; gi < G; ++gi)
     for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) {
       pat.bg[q] = gi;
       pat.bh[q] = unbr[q];
-      if (unbr[q] != gi) ndown[unbr[q] + 1]++;
     }
+  // lower neighbours of h (blocks (g, h), g < h), in increasing g: stable bucket of the blocks by h
+  std::vector<int64_t> loff;
+  std::vector<int64_t> lpos(nb, -1);
+  par_bucket(nb, G, [&](int64_t q) { return unbr[q] != pat.bg[q] ? unbr[q] : -1; }, loff,
+             [&](int64_t q, int64_t pos) { lpos[q] = pos; });
   pat.adj_off.assign(G + 1, 0);
-  for (int gi = 0; gi < G; ++gi) pat.adj_off[gi + 1] = pat.adj_off[gi] + ndown[gi + 1] + (uoff[gi + 1] - uoff[gi]);
+  for (int gi = 0; gi < G; ++gi) pat.adj_off[gi + 1] = loff[gi + 1] + uoff[gi + 1];
   pat.adj_nbr.assign(pat.adj_off[G], 0);
   pat.adj_blk.assign(pat.adj_off[G], 0);
-  std::vector<int64_t> fill(pat.adj_off.begin(), pat.adj_off.end() - 1);
-  // lower neighbours first, in increasing order (outer loop over ascending g)
-  for (int gi = 0; gi < G; ++gi)
-    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) {
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < nb; ++q)
+    if (lpos[q] >= 0) {
       const int h = unbr[q];
-      if (h == gi) continue;
-      pat.adj_nbr[fill[h]] = gi;
-      pat.adj_blk[fill[h]++] = (int)q;
+      const int64_t f = pat.adj_off[h] + (lpos[q] - loff[h]);
+      pat.adj_nbr[f] = pat.bg[q];
+      pat.adj_blk[f] = (int)q;
     }
 #pragma omp parallel for schedule(static)
   for (int gi = 0; gi < G; ++gi) {
-    int64_t f = fill[gi];
+    int64_t f = pat.adj_off[gi] + (loff[gi + 1] - loff[gi]);
     for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) {
       pat.adj_nbr[f] = unbr[q];
       pat.adj_blk[f++] = (int)q;
     }
   }
+}
+
+// exclusive prefix of per-item counts (serial; the counts are computed in parallel)
+static int64_t prefix_counts(std::vector<int64_t>& off) {
+  int64_t acc = 0;
+  for (size_t i = 0; i + 1 < off.size(); ++i) {
+    const int64_t v = off[i + 1];
+    off[i + 1] = acc + v;
+    acc += v;
+  }
+  return acc;
 }
 
 void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> pairs) {
@@ -414,21 +532,24 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
   auto lap = [&](const char* what) {
     if (!tdbg) return;
     const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "  [plan L%d] %-28s %8.2f ms\n", lp.grp.level, what, std::chrono::duration<double, std::milli>(now - tl).count());
+    fprintf(stderr, "  [plan L%d] %-28s %8.2f ms\n", lp.grp.level, what,
+            std::chrono::duration<double, std::milli>(now - tl).count());
     tl = now;
   };
   Groups& g = lp.grp;
+  const int G = g.G;
   lp.level = g.level;
   lp.root = (g.level == s.L);
-  for (int i = 0; i < g.G; ++i) pairs.emplace_back(i, i);
+  for (int i = 0; i < G; ++i) pairs.emplace_back(i, i);
   std::vector<int64_t> uoff;
   std::vector<int> unbr;
-  lap("upper lists (stencil)");
-  upper_lists(g.G, pairs, uoff, unbr);
+  upper_lists(G, pairs, uoff, unbr);
+  std::vector<std::pair<int, int>>().swap(pairs);
+  lap("stencil upper lists");
   lp.interior.clear();
   lp.precond.clear();
   lp.skeleton.clear();
-  for (int i = 0; i < g.G; ++i) {
+  for (int i = 0; i < G; ++i) {
     if (g.kind[i] == 0) {
       lp.interior.push_back(i);
     } else {
@@ -437,40 +558,94 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
     }
   }
   // an interior group is the first group of its cell closure: every coupling of it is an upper entry
-  for (int gi = 0; gi < g.G; ++gi)
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+  for (int gi = 0; gi < G; ++gi)
     for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q)
-      if (unbr[q] != gi && g.kind[unbr[q]] == 0)
-        throw std::runtime_error(g.kind[gi] == 0 ? "planner: two interior groups coupled"
-                                                 : "planner: interior group is not first in its closure");
+      if (unbr[q] != gi && g.kind[unbr[q]] == 0) bad = std::max(bad, g.kind[gi] == 0 ? 2 : 1);
+  if (bad == 2) throw std::runtime_error("planner: two interior groups coupled");
+  if (bad == 1) throw std::runtime_error("planner: interior group is not first in its closure");
   lap("classify + checks");
-  // elimination fill among each cell's boundary groups
-  pairs.clear();
-  for (int gi = 0; gi < g.G; ++gi)
-    for (int64_t q = uoff[gi]; q < uoff[gi + 1]; ++q) pairs.emplace_back(gi, unbr[q]);
-  for (int I : lp.interior) {
-    const int64_t a0 = uoff[I], a1 = uoff[I + 1];
-    for (int64_t a = a0; a < a1; ++a) {
-      if (unbr[a] == I) continue;
-      for (int64_t b = a; b < a1; ++b) pairs.emplace_back(unbr[a], unbr[b]);
+  // cells of every boundary group (interiors in cell order)
+  const int p = (int)lp.interior.size();
+  std::vector<int64_t> roff(G + 1, 0);
+  for (int t = 0; t < p; ++t) {
+    const int I = lp.interior[t];
+    for (int64_t q = uoff[I]; q < uoff[I + 1]; ++q)
+      if (unbr[q] != I) roff[unbr[q] + 1]++;
+  }
+  for (int i = 0; i < G; ++i) roff[i + 1] += roff[i];
+  std::vector<int> rcell(roff[G]);
+  {
+    std::vector<int64_t> fill(roff.begin(), roff.end() - 1);
+    for (int t = 0; t < p; ++t) {
+      const int I = lp.interior[t];
+      for (int64_t q = uoff[I]; q < uoff[I + 1]; ++q)
+        if (unbr[q] != I) rcell[fill[unbr[q]]++] = t;
     }
   }
-  lap("fill pairs");
-  upper_lists(g.G, pairs, uoff, unbr);
-  adjacency_from_upper(g.G, uoff, unbr, lp.pat);
-  lap("adjacency");
+  // block pattern after elimination fill: upper(g) = stencil upper(g) plus every
+  // h >= g sharing a cell with g; two passes (count, fill), groups in parallel
+  std::vector<int64_t> foff(G + 1, 0);
+  std::vector<int> fnbr;
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma omp parallel
+    {
+      std::vector<int> buf;
+#pragma omp for schedule(dynamic, 256)
+      for (int gi = 0; gi < G; ++gi) {
+        buf.assign(unbr.begin() + uoff[gi], unbr.begin() + uoff[gi + 1]);
+        for (int64_t e = roff[gi]; e < roff[gi + 1]; ++e) {
+          const int I = lp.interior[rcell[e]];
+          for (int64_t q = uoff[I]; q < uoff[I + 1]; ++q)
+            if (unbr[q] >= gi && unbr[q] != I) buf.push_back(unbr[q]);
+        }
+        std::sort(buf.begin(), buf.end());
+        const int64_t nu = std::unique(buf.begin(), buf.end()) - buf.begin();
+        if (pass == 0) foff[gi + 1] = nu;
+        else std::copy(buf.begin(), buf.begin() + nu, fnbr.begin() + foff[gi]);
+      }
+    }
+    if (pass == 0) fnbr.assign(prefix_counts(foff), 0);
+  }
+  uoff.swap(foff);
+  unbr.swap(fnbr);
+  lap("fill pattern");
+  adjacency_from_upper(G, uoff, unbr, lp.pat);
   const Pattern& pat = lp.pat;
   const int64_t nblocks = (int64_t)pat.bg.size();
+  lap("adjacency");
   // pool
   lp.boff.resize(nblocks);
-  int64_t acc = 0;
-  for (int64_t b = 0; b < nblocks; ++b) {
-    lp.boff[b] = acc;
-    acc += (int64_t)g.size(pat.bg[b]) * g.size(pat.bh[b]);
+  {
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    std::vector<int64_t> part(nth + 1, 0);
+    const int64_t ch = (nblocks + nth - 1) / nth;
+#pragma omp parallel num_threads(nth)
+    {
+      int tid = 0;
+#ifdef _OPENMP
+      tid = omp_get_thread_num();
+#endif
+      const int64_t lo = std::min<int64_t>(nblocks, tid * ch), hi = std::min<int64_t>(nblocks, lo + ch);
+      int64_t a = 0;
+      for (int64_t b = lo; b < hi; ++b) {
+        lp.boff[b] = a;
+        a += (int64_t)g.size(pat.bg[b]) * g.size(pat.bh[b]);
+      }
+      part[tid + 1] = a;
+#pragma omp barrier
+#pragma omp single
+      for (int q = 0; q < nth; ++q) part[q + 1] += part[q];
+      for (int64_t b = lo; b < hi; ++b) lp.boff[b] += part[tid];
+    }
+    lp.pool_doubles = part[nth];
   }
-  lp.pool_doubles = acc;
   lap("pool");
-  // cells: boundary = neighbour groups of I (all after I); Schur targets = pairs of them
-  const int p = (int)lp.interior.size();
+  // cells: boundary = neighbour groups of I (all after I)
   lp.cell_nbr_off.assign(p + 1, 0);
   lp.cell_n.assign(p, 0);
   lp.cell_b.assign(p, 0);
@@ -482,7 +657,6 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
   lp.cell_nbr.assign(ncn, 0);
   lp.cell_nbr_blk.assign(ncn, 0);
   lp.cell_nbr_col.assign(ncn, 0);
-  std::vector<int64_t> ccount(p + 1, 0);
 #pragma omp parallel for schedule(static)
   for (int t = 0; t < p; ++t) {
     const int I = lp.interior[t];
@@ -499,45 +673,50 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
     }
     lp.cell_n[t] = g.size(I);
     lp.cell_b[t] = bcols;
-    const int64_t w = lp.cell_nbr_off[t + 1] - lp.cell_nbr_off[t];
-    ccount[t + 1] = w * (w + 1) / 2;
   }
-  for (int t = 0; t < p; ++t) ccount[t + 1] += ccount[t];
-  const int64_t ncons = ccount[p];
-  std::vector<int> ctgt(ncons), ccell(ncons), crow(ncons), ccol(ncons);
-#pragma omp parallel for schedule(static)
-  for (int t = 0; t < p; ++t) {
-    int64_t o = ccount[t];
-    const int64_t first = lp.cell_nbr_off[t], last = lp.cell_nbr_off[t + 1];
-    for (int64_t a = first; a < last; ++a) {
-      const int ha = lp.cell_nbr[a];
-      const int* rb = unbr.data() + uoff[ha];
-      const int* re = unbr.data() + uoff[ha + 1];
-      for (int64_t b = a; b < last; ++b) {
-        const int* it = std::lower_bound(rb, re, lp.cell_nbr[b]);
-        ctgt[o] = (int)(it - unbr.data());   // block id = position in the upper lists
-        ccell[o] = t;
-        crow[o] = lp.cell_nbr_col[a];
-        ccol[o] = lp.cell_nbr_col[b];
-        ++o;
-      }
-    }
-  }
-  lap("cells + contributions");
-  // group contributions by target block (counting sort; stable in cell order)
+  // Schur targets: block (a, b), a <= b, receives U_t[a, b] from every cell t holding both a and b
+  // (cells of a intersect cells of b; both lists ascending in cell order = the summation order)
+  auto col_of = [&](int t, int h) {   // first column of group h in cell t's boundary
+    const int* b0 = lp.cell_nbr.data() + lp.cell_nbr_off[t];
+    const int* b1 = lp.cell_nbr.data() + lp.cell_nbr_off[t + 1];
+    return lp.cell_nbr_col[lp.cell_nbr_off[t] + (std::lower_bound(b0, b1, h) - b0)];
+  };
   std::vector<int64_t> tcnt(nblocks + 1, 0);
-  for (int64_t i = 0; i < ncons; ++i) tcnt[ctgt[i] + 1]++;
-  for (int64_t b = 0; b < nblocks; ++b) tcnt[b + 1] += tcnt[b];
-  lp.con_cell.resize(ncons);
-  lp.con_row.resize(ncons);
-  lp.con_col.resize(ncons);
-  {
-    std::vector<int64_t> fill(tcnt.begin(), tcnt.end() - 1);
-    for (int64_t i = 0; i < ncons; ++i) {
-      const int64_t o = fill[ctgt[i]]++;
-      lp.con_cell[o] = ccell[i];
-      lp.con_row[o] = crow[i];
-      lp.con_col[o] = ccol[i];
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t b = 0; b < nblocks; ++b) {
+      const int a0 = pat.bg[b], b0 = pat.bh[b];
+      if (g.kind[a0] == 0 || g.kind[b0] == 0) {
+        if (pass == 0) tcnt[b + 1] = 0;
+        continue;
+      }
+      int64_t o = pass ? tcnt[b] : 0;
+      int64_t ia = roff[a0], ib = roff[b0];
+      const int64_t ea = roff[a0 + 1], eb = roff[b0 + 1];
+      while (ia < ea && ib < eb) {
+        if (rcell[ia] < rcell[ib]) {
+          ++ia;
+        } else if (rcell[ib] < rcell[ia]) {
+          ++ib;
+        } else {
+          if (pass) {
+            const int t = rcell[ia];
+            lp.con_cell[o] = t;
+            lp.con_row[o] = col_of(t, a0);
+            lp.con_col[o] = col_of(t, b0);
+          }
+          ++o;
+          ++ia;
+          ++ib;
+        }
+      }
+      if (pass == 0) tcnt[b + 1] = o;
+    }
+    if (pass == 0) {
+      const int64_t ncons = prefix_counts(tcnt);
+      lp.con_cell.resize(ncons);
+      lp.con_row.resize(ncons);
+      lp.con_col.resize(ncons);
     }
   }
   lp.tgt_blk.clear();
@@ -548,63 +727,77 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       lp.tgt_off.push_back(tcnt[b + 1]);
     }
   if (lp.tgt_blk.empty()) lp.tgt_off.assign(1, 0);
-  lap("contribution sort");
+  lap("cells + Schur targets");
   // block Jacobi scaling targets
   lp.scale_blk.clear();
-  for (size_t b = 0; b < pat.bg.size(); ++b)
+  for (int64_t b = 0; b < nblocks; ++b)
     if (pat.bg[b] != pat.bh[b] && g.kind[pat.bg[b]] != 0 && g.kind[pat.bh[b]] != 0) lp.scale_blk.push_back((int)b);
   lap("scale blocks");
   // skeleton neighbours + dependency waves (sequential semantics)
   const int nsk = (int)lp.skeleton.size();
-  std::vector<int> sk_index(g.G, -1);
+  std::vector<int> sk_index(G, -1);
   for (int i = 0; i < nsk; ++i) sk_index[lp.skeleton[i]] = i;
-  lp.sk_nbr_off.assign(1, 0);
-  lp.sk_nbr.clear();
-  lp.sk_nbr_blk.clear();
-  lp.sk_wave.assign(nsk, 0);
-  lp.nwaves = 0;
+  lp.sk_nbr_off.assign(nsk + 1, 0);
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < nsk; ++i) {
     const int gg = lp.skeleton[i];
-    int w = 0;
+    int64_t cnt = 0;
+    for (int64_t q = pat.adj_off[gg]; q < pat.adj_off[gg + 1]; ++q) {
+      const int h = pat.adj_nbr[q];
+      if (h != gg && g.kind[h] != 0) ++cnt;
+    }
+    lp.sk_nbr_off[i + 1] = cnt;
+  }
+  lp.sk_nbr.assign(prefix_counts(lp.sk_nbr_off), 0);
+  lp.sk_nbr_blk.assign(lp.sk_nbr.size(), 0);
+  lp.sk_ndep.assign(nsk, 0);
+  lp.sk_succ_off.assign(nsk + 1, 0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < nsk; ++i) {
+    const int gg = lp.skeleton[i];
+    int64_t o = lp.sk_nbr_off[i];
+    int nd = 0, ns = 0;
     for (int64_t q = pat.adj_off[gg]; q < pat.adj_off[gg + 1]; ++q) {
       const int h = pat.adj_nbr[q];
       if (h == gg || g.kind[h] == 0) continue;
-      lp.sk_nbr.push_back(h);
-      lp.sk_nbr_blk.push_back(pat.adj_blk[q]);
+      lp.sk_nbr[o] = h;
+      lp.sk_nbr_blk[o++] = pat.adj_blk[q];
       const int j = sk_index[h];
+      if (j >= 0 && j < i) ++nd;
+      if (j > i) ++ns;
+    }
+    lp.sk_ndep[i] = nd;
+    lp.sk_succ_off[i + 1] = ns;
+  }
+  // later coupled separators (the adjacency is symmetric); waves: 1 + latest earlier neighbour
+  lp.sk_succ.assign(prefix_counts(lp.sk_succ_off), 0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < nsk; ++i) {
+    int64_t o = lp.sk_succ_off[i];
+    for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
+      const int j = sk_index[lp.sk_nbr[q]];
+      if (j > i) lp.sk_succ[o++] = j;
+    }
+  }
+  lp.sk_wave.assign(nsk, 0);
+  lp.nwaves = 0;
+  for (int i = 0; i < nsk; ++i) {
+    int w = 0;
+    for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
+      const int j = sk_index[lp.sk_nbr[q]];
       if (j >= 0 && j < i) w = std::max(w, lp.sk_wave[j] + 1);
     }
-    lp.sk_nbr_off.push_back((int64_t)lp.sk_nbr.size());
     lp.sk_wave[i] = w;
     lp.nwaves = std::max(lp.nwaves, w + 1);
   }
-  lp.sk_ndep.assign(nsk, 0);
-  lp.sk_succ_off.assign(nsk + 1, 0);
-  for (int i = 0; i < nsk; ++i)
-    for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
-      const int j = sk_index[lp.sk_nbr[q]];
-      if (j >= 0 && j < i) {
-        lp.sk_ndep[i]++;
-        lp.sk_succ_off[j + 1]++;
-      }
-    }
-  for (int i = 0; i < nsk; ++i) lp.sk_succ_off[i + 1] += lp.sk_succ_off[i];
-  lp.sk_succ.assign(lp.sk_succ_off[nsk], 0);
-  {
-    std::vector<int64_t> fill(lp.sk_succ_off.begin(), lp.sk_succ_off.end() - 1);
-    for (int i = 0; i < nsk; ++i)
-      for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
-        const int j = sk_index[lp.sk_nbr[q]];
-        if (j >= 0 && j < i) lp.sk_succ[fill[j]++] = i;
-      }
-  }
-  lp.wave_order.resize(nsk);
-  std::iota(lp.wave_order.begin(), lp.wave_order.end(), 0);
-  std::stable_sort(lp.wave_order.begin(), lp.wave_order.end(),
-                   [&](int a, int b) { return lp.sk_wave[a] < lp.sk_wave[b]; });
   lp.wave_off.assign(lp.nwaves + 1, 0);
   for (int i = 0; i < nsk; ++i) lp.wave_off[lp.sk_wave[i] + 1]++;
   for (int w = 0; w < lp.nwaves; ++w) lp.wave_off[w + 1] += lp.wave_off[w];
+  lp.wave_order.resize(nsk);
+  {
+    std::vector<int64_t> fill(lp.wave_off.begin(), lp.wave_off.end() - 1);
+    for (int i = 0; i < nsk; ++i) lp.wave_order[fill[lp.sk_wave[i]]++] = i;   // stable: (wave, index)
+  }
   lap("skeleton waves");
 }
 
