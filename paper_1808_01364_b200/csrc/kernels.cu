@@ -853,6 +853,102 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
         }
       };
       if (qprof) ta.prof[22] += tf - tq0;
+      constexpr int PQ = 10;   // panel rows per thread held in registers
+      if (ldp <= PQ * NT) {
+        // register-resident panel: thread tid holds rows tid + q*NT of all (<= 8) columns; the
+        // column loop is unrolled so every register index is static. Row jj < 8 lives in thread jj.
+        double pr[PQ][8];
+#pragma unroll
+        for (int q = 0; q < PQ; ++q) {
+          const int rr = tid + q * NT;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pr[q][u] = (rr < ldp && u < jb) ? Pn[(int64_t)u * ldp + rr] : 0.0;
+        }
+        __shared__ double s_row[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          if (jj < jb) {
+            if (tid == jj) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) s_row[u] = pr[0][u];
+            }
+            double acc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll
+            for (int q = 0; q < PQ; ++q) {
+              const int rr = tid + q * NT;
+              if (rr > jj && rr < ldp) {
+                const double x = pr[q][jj];
+                acc[0] += x * x;
+#pragma unroll
+                for (int u = 1; jj + u < 8; ++u) acc[u] += x * pr[q][jj + u];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const double t2 = warp_sum(acc[u]);
+              if (lane == 0) s_red[warp][u] = t2;
+            }
+            __syncthreads();
+            if (warp == 0) {
+              double mys = 0.0;
+              if (lane < 8) {
+#pragma unroll
+                for (int w2 = 0; w2 < 8; ++w2) mys += s_red[w2][lane];
+              }
+              double sum[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) sum[u] = __shfl_sync(0xffffffffu, mys, u);
+              if (lane == 0) {
+                const double alpha = s_row[jj], xnorm = sqrt(sum[0]);
+                double tau = 0.0, beta = alpha, scal = 1.0;
+                if (xnorm != 0.0) {
+                  beta = -copysign(hypot(alpha, xnorm), alpha);
+                  tau = (beta - alpha) / beta;
+                  scal = 1.0 / (alpha - beta);
+                }
+                Ts[jj * 8 + jj] = tau;
+                s_par[0] = scal;
+                s_par[16] = beta;
+                for (int u = 1; u < 8; ++u) {
+                  const double tw = (jj + u < jb) ? tau * (s_row[jj + u] + scal * sum[u]) : 0.0;   // tau v^T a_u
+                  s_par[u] = tw * scal;
+                  s_par[8 + u] = tw;
+                }
+              }
+            }
+            __syncthreads();
+            const double scal = s_par[0];
+            double cu[8];
+#pragma unroll
+            for (int u = 1; u < 8; ++u) cu[u] = s_par[u];
+#pragma unroll
+            for (int q = 0; q < PQ; ++q) {
+              const int rr = tid + q * NT;
+              if (rr > jj && rr < ldp) {
+                const double x = pr[q][jj];
+#pragma unroll
+                for (int u = 1; jj + u < 8; ++u) pr[q][jj + u] -= cu[u] * x;
+                pr[q][jj] = x * scal;
+              }
+            }
+            if (tid == jj) {
+              pr[0][jj] = s_par[16];
+#pragma unroll
+              for (int u = 1; jj + u < 8; ++u) pr[0][jj + u] -= s_par[8 + u];
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < PQ; ++q) {
+          const int rr = tid + q * NT;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (rr < ldp && u < jb) Pn[(int64_t)u * ldp + rr] = pr[q][u];
+        }
+        __syncthreads();
+      } else
       for (int jj = 0; jj < jb; ++jj) {
         // one reduction per column: |x|^2 and x . a_u (x = column jj below the diagonal)
         double acc[8];
