@@ -909,14 +909,61 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           slot_off(P.nwaves + 1, 0);
       std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0), wave_kmax(P.nwaves, 0), wave_mmax(P.nwaves, 0);
       std::vector<int> wave_cluster(P.nwaves, 0);
+      // Gram-path ID (gram_id.cuh) for the large separators when the ID tolerance leaves room
+      // for the squared conditioning of A^T A (the rank cut sits far above sqrt(k eps_mach))
+      static const bool gid_on = !getenv("PHIF_GID") || atoi(getenv("PHIF_GID")) != 0;
+      static const double gid_eps = getenv("PHIF_GID_EPS") ? atof(getenv("PHIF_GID_EPS")) : 1e-5;
+      const bool use_gid = gid_on && F->eps >= gid_eps;
+      std::vector<int> gid_item, gid_wi, gid_wj, gid_wit;
+      std::vector<int64_t> gid_ld, gid_goff, gid_item_off(P.nwaves + 1, 0), gid_w_off(P.nwaves + 1, 0);
+      std::vector<int> gid_C(P.nwaves, 1), gid_kmax(P.nwaves, 0), gid_P(P.nwaves, 1);
+      std::vector<uint8_t> gid_sg(P.nwaves, 0);
+      int64_t gid_gbuf = 1, gid_cnt = 1;
       for (int w = 0; w < P.nwaves; ++w) {
         std::vector<int> large;
         for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
           const int t = P.wave_order[q];
           const int k = G.size(P.skeleton[t]);
-          if (k > 48 && rows_bound[t] * k > 100000) large.push_back(t);
-          else small_list.push_back(t);
+          if (k > 48 && rows_bound[t] * k > 100000) {
+            if (use_gid) gid_item.push_back(t);
+            else large.push_back(t);
+          } else {
+            small_list.push_back(t);
+          }
         }
+        gid_item_off[w + 1] = (int64_t)gid_item.size();
+        gid_w_off[w] = (int64_t)gid_wi.size();
+        {
+          int kmx = 0;
+          for (int64_t q = gid_item_off[w]; q < gid_item_off[w + 1]; ++q)
+            kmx = std::max(kmx, G.size(P.skeleton[gid_item[q]]));
+          gid_kmax[w] = kmx;
+          const int ni = (int)(gid_item_off[w + 1] - gid_item_off[w]);
+          if (ni) {
+            bool sg = false;
+            gid_C[w] = gid_cluster(kmx, &sg);
+            gid_sg[w] = sg;
+            gid_P[w] = std::max(1, std::min(32, 2 * num_sms / ni));
+            gid_cnt = std::max<int64_t>(gid_cnt, (int64_t)ni * gid_P[w]);
+          }
+          int64_t go = 0;
+          for (int64_t q = gid_item_off[w]; q < gid_item_off[w + 1]; ++q) {
+            const int t = gid_item[q];
+            const int k = G.size(P.skeleton[t]);
+            gid_ld.push_back(std::max<int64_t>(rows_bound[t], 1));
+            gid_goff.push_back(go);
+            go += gid_gbuf_doubles(k, gid_C[w], gid_sg[w]);
+            const int nt = (k + 63) / 64;
+            for (int it = 0; it < nt; ++it)
+              for (int jt = 0; jt <= it; ++jt) {
+                gid_wit.push_back((int)(q - gid_item_off[w]));
+                gid_wi.push_back(it);
+                gid_wj.push_back(jt);
+              }
+          }
+          gid_gbuf = std::max(gid_gbuf, go);
+        }
+        gid_w_off[w + 1] = (int64_t)gid_wi.size();
         small_off[w + 1] = (int64_t)small_list.size();
         int vcap = 0, kmax = 0;
         double wsum = 0.0;
@@ -998,6 +1045,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       }
       L.n_large = (int)large_list.size();
       if (L.n_large) L.team_P_mean /= L.n_large;
+      DBuf d_gitem, d_gld, d_goff, d_gwit, d_gwi, d_gwj, d_gcnt, d_gbuf;
+      if (!gid_item.empty()) {
+        upload(d_gitem, gid_item, s);
+        upload(d_gld, gid_ld, s);
+        upload(d_goff, gid_goff, s);
+        upload(d_gwit, gid_wit, s);
+        upload(d_gwi, gid_wi, s);
+        upload(d_gwj, gid_wj, s);
+        d_gcnt.alloc(gid_cnt * sizeof(int), s);
+        d_gbuf.alloc(gid_gbuf * sizeof(double), s);
+      }
+      L.n_gid = (int)gid_item.size();
       DBuf d_small, d_large, d_toff, hdr, sv, si;
       upload(d_small, small_list, s);
       upload(d_large, large_list, s);
@@ -1025,6 +1084,23 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           need = std::max<int64_t>(need, std::max<int64_t>(rows_bound[t], 1) * kk + 4 * kk + 4);
         }
         launch_skel_id(dv, ka, (int)(small_off[w + 1] - small_off[w]), need, s);
+        const int ng = (int)(gid_item_off[w + 1] - gid_item_off[w]);
+        if (ng) {
+          GramArgs ga;
+          ga.nitem = ng;
+          ga.item_sep = d_gitem.as<int>() + gid_item_off[w];
+          ga.item_ld = d_gld.as<int64_t>() + gid_item_off[w];
+          ga.P = gid_P[w];
+          ga.cnt = d_gcnt.as<int>();
+          ga.gbuf = d_gbuf.as<double>();
+          ga.g_off = d_goff.as<int64_t>() + gid_item_off[w];
+          ga.w_item = d_gwit.as<int>() + gid_w_off[w];
+          ga.w_i = d_gwi.as<int>() + gid_w_off[w];
+          ga.w_j = d_gwj.as<int>() + gid_w_off[w];
+          ga.nwork = (int)(gid_w_off[w + 1] - gid_w_off[w]);
+          ga.C = gid_C[w];
+          launch_gid(dv, ka, ga, gid_kmax[w], gid_sg[w] != 0, s);
+        }
         const int nl = (int)(large_off[w + 1] - large_off[w]);
         if (nl) {
           TeamArgs ta;
@@ -1938,7 +2014,7 @@ std::string Factorization::stats_json() const {
       << ",\"q\":" << (P.root ? 0 : P.skeleton.size()) << ",\"r\":" << (P.root ? 0 : P.precond.size())
       << ",\"blocks\":" << P.pat.bg.size() << ",\"waves\":" << P.nwaves << ",\"rho_max\":" << L.rho_max
       << ",\"rho_mean\":" << L.rho_mean << ",\"sep_k_mean\":" << L.sep_k_mean << ",\"sep_k_max\":" << L.sep_k_max
-      << ",\"sep_m_mean\":" << L.sep_m_mean << ",\"sep_m_max\":" << L.sep_m_max << ",\"n_large\":" << L.n_large
+      << ",\"sep_m_mean\":" << L.sep_m_mean << ",\"sep_m_max\":" << L.sep_m_max << ",\"n_large\":" << L.n_large << ",\"n_gid\":" << L.n_gid
       << ",\"team_P_mean\":" << L.team_P_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
       << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
       << L.t_ms[4] << ",\"t_plan_ms\":" << L.t_ms[5] << ",\"t_wall_ms\":" << L.t_wall_ms << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]

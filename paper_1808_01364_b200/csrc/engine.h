@@ -109,6 +109,7 @@ struct LevelRT {
   double rho_mean = 0.0;
   double sep_k_mean = 0, sep_k_max = 0, sep_m_mean = 0, sep_m_max = 0, team_P_mean = 0;
   int n_large = 0;
+  int n_gid = 0;      // separators on the Gram-path ID
   int64_t S = 0;
   LevelDev dev() const;
 };

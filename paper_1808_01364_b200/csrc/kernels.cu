@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "dla.cuh"
 #include "kernels.cuh"
@@ -2612,6 +2613,8 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
       }
 }
 
+#include "gram_id.cuh"
+
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
                    const double* val, int64_t N, cudaStream_t s) {
   if (N == 0) return;
@@ -2940,6 +2943,66 @@ void launch_xmy(double* y, const double* x, int64_t n, cudaStream_t s) {
 void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_scale<<<nblk(n, 256), 256, 0, s>>>(y, x, nrm2, n);
+}
+
+// ---- Gram-path ID launches (gram_id.cuh) ----
+static constexpr size_t GID_SMEM_CAP = 227 * 1024;
+static int64_t gid_sreg(int k, int C, bool sg) {
+  const int64_t stage = 24 * (int64_t)k;   // back substitution: 16-column R11 block + 1 RHS per warp
+  return sg ? stage : std::max<int64_t>(gid_pack0(k, C), stage);
+}
+int gid_cluster(int kmax, bool* sg) {
+  // smallest cluster whose per-CTA packed Schur share is at most `target` doubles; the Schur
+  // complement moves to global memory when even 16 CTAs cannot hold it in shared memory
+  static const int64_t target = getenv("PHIF_GID_PACK") ? atoll(getenv("PHIF_GID_PACK")) : 6144;
+  static const int force_c = getenv("PHIF_GID_C") ? atoi(getenv("PHIF_GID_C")) : 0;
+  int C = 16;
+  if (force_c) C = force_c;
+  else
+    for (int c : {1, 2, 4, 8, 16})
+      if (gid_pack0(kmax, c) <= target) {
+        C = c;
+        break;
+      }
+  *sg = GidSmem::bytes(gid_sreg(kmax, C, false), kmax) > GID_SMEM_CAP;
+  return C;
+}
+int64_t gid_gbuf_doubles(int k, int C, bool sg) {
+  return (int64_t)k * k + (sg ? (int64_t)C * gid_pack0(k, C) : 0);
+}
+void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int kmax, bool sg, cudaStream_t s) {
+  if (g.nitem == 0) return;
+  LevelDev lv2 = lv;
+  SkelArgs a2 = a;
+  GramArgs g2 = g;
+  g_launches.fetch_add(3, std::memory_order_relaxed);
+  k_gid_count<<<g.nitem * g.P, NT, 0, s>>>(lv, a, g);
+  k_gid_copy<<<g.nitem * g.P, NT, 0, s>>>(lv, a, g);
+  static bool attr = false;
+  if (!attr) {
+    attr = true;
+    cudaFuncSetAttribute(k_gid_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
+    cudaFuncSetAttribute(k_gid_cpqr<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_gid_cpqr<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
+  if (g.nwork) k_gid_gram<<<g.nwork, NT, NT_SMEM, s>>>(lv, a, g);
+  int64_t sreg = gid_sreg(kmax, g.C, sg);
+  const size_t bytes = GidSmem::bytes(sreg, kmax);
+  void (*fn)(LevelDev, SkelArgs, GramArgs, int64_t) = sg ? k_gid_cpqr<true> : k_gid_cpqr<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.nitem * g.C);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  cudaLaunchKernelEx(&cfg, fn, lv2, a2, g2, sreg);
 }
 
 void configure_kernels() {

@@ -123,6 +123,22 @@ struct TeamArgs {
   int cluster;           // > 0: teams are thread-block clusters of this size (cluster barriers)
 };
 
+// Gram-path ID of large separators (gram_id.cuh): one wave's items
+struct GramArgs {
+  int nitem;
+  const int* item_sep;     // skeleton index per item
+  const int64_t* item_ld;  // leading dimension of the gathered A_{R,I} (rows bound)
+  int P;                   // gather CTAs per item
+  int* cnt;                // nitem * P kept-row counts
+  double* gbuf;            // per item: G (k x k, then R) [+ packed Schur complement when global]
+  const int64_t* g_off;
+  const int* w_item;       // Gram tile work list (lower 64x64 tiles)
+  const int* w_i;
+  const int* w_j;
+  int nwork;
+  int C;                   // CPQR cluster size
+};
+
 struct RepackArgs {
   int nblk;
   // work items: row chunks of new blocks
