@@ -357,6 +357,26 @@ static long long* team_prof_buffer() {
   return buf;
 }
 
+// PHIF_GID_PROF=1: per-phase clocks of the Gram-path CPQR (CTA 0 of every launch)
+static long long* gid_prof_buffer() {
+  static long long* buf = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    on = getenv("PHIF_GID_PROF") ? 1 : 0;
+    if (on) {
+      cudaMallocManaged(&buf, 16 * sizeof(long long));
+      for (int i = 0; i < 16; ++i) buf[i] = 0;
+      atexit([] {
+        cudaDeviceSynchronize();
+        fprintf(stderr, "[phif] gid CPQR CTA0 (Mcycles): load %.2f argmax %.2f pieces %.2f barrier %.2f rowread %.2f update %.2f downdate %.2f post %.2f backsub %.2f | steps %lld\n",
+                buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6,
+                buf[7] / 1e6, buf[8] / 1e6, buf[9]);
+      });
+    }
+  }
+  return buf;
+}
+
 static void keep_pool_memory() {
   // freed blocks stay in the stream-ordered pool instead of going back to the driver at every sync
   static bool done = false;
@@ -870,11 +890,16 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     for (int t = 0; t < nsk; ++t)
       if (P.sk_nbr_off[t + 1] - P.sk_nbr_off[t] > 256)
         throw std::runtime_error("skeletonize: a separator couples to more than 256 groups");
-    bool any_large = false;
-    for (int t = 0; t < nsk; ++t) {
+    // large separators: team / Gram-path ID; the rest one CTA each (thresholds env-tunable)
+    static const int large_k = getenv("PHIF_LARGE_K") ? atoi(getenv("PHIF_LARGE_K")) : 48;
+    static const int64_t large_mk = getenv("PHIF_LARGE_MK") ? atoll(getenv("PHIF_LARGE_MK")) : 100000;
+    auto is_large = [&](int t) {
       const int kk = G.size(P.skeleton[t]);
-      if (kk > 48 && rows_bound[t] * kk > 100000) any_large = true;
-    }
+      return kk > large_k && rows_bound[t] * kk > large_mk;
+    };
+    bool any_large = false;
+    for (int t = 0; t < nsk; ++t)
+      if (is_large(t)) any_large = true;
     static const bool no_dyn = getenv("PHIF_NO_DYN") != nullptr;
     if (nsk && !any_large && !no_dyn) {
       // only small separators: one persistent dependency-driven launch instead of per-wave launches
@@ -924,7 +949,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
           const int t = P.wave_order[q];
           const int k = G.size(P.skeleton[t]);
-          if (k > 48 && rows_bound[t] * k > 100000) {
+          if (is_large(t)) {
             if (use_gid) gid_item.push_back(t);
             else large.push_back(t);
           } else {
@@ -1099,6 +1124,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ga.w_j = d_gwj.as<int>() + gid_w_off[w];
           ga.nwork = (int)(gid_w_off[w + 1] - gid_w_off[w]);
           ga.C = gid_C[w];
+          ga.prof = gid_prof_buffer();
           launch_gid(dv, ka, ga, gid_kmax[w], gid_sg[w] != 0, s);
         }
         const int nl = (int)(large_off[w + 1] - large_off[w]);

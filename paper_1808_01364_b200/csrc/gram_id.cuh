@@ -17,18 +17,20 @@
 //                                 T = R11^-1 R12 by blocked back substitution across the cluster.
 //
 // The Schur complement is stored packed-lower and column-cyclic across the cluster's CTAs
-// (column b lives in CTA b % C, rows b..k-1), in shared memory when it fits (SG = false) or in
-// a global workspace (SG = true). Partial norms, Schur diagonal and column positions are
+// (column b lives in CTA b % C, rows b..k-1), in shared memory up to the CTA's budget and the
+// remaining columns in a global spill area. Partial norms, Schur diagonal and column positions are
 // replicated in every CTA and updated with identical arithmetic, so every CTA selects the same
 // pivot without communication; the only exchange per pivot step is row i of R (each CTA
 // computes the entries of the columns it owns, one cluster barrier, then reads the row through
 // distributed shared memory).
 
 struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
-  int64_t sreg;     // Schur region (SG = false) / back-substitution staging
-  __host__ __device__ static int64_t doubles(int64_t sreg, int k) { return sreg + 6 * (int64_t)k + 64; }
-  __host__ __device__ static size_t bytes(int64_t sreg, int k) {
-    return (size_t)doubles(sreg, k) * sizeof(double) + 3 * (size_t)k * sizeof(int);
+  // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][64] doubles, then 3k ints
+  __host__ __device__ static int64_t doubles(int64_t sreg, int k, int nb) {
+    return sreg + (int64_t)(nb + 5) * k + 64;
+  }
+  __host__ __device__ static size_t bytes(int64_t sreg, int k, int nb) {
+    return (size_t)doubles(sreg, k, nb) * sizeof(double) + 3 * (size_t)k * sizeof(int);
   }
 };
 
@@ -48,13 +50,32 @@ __device__ __forceinline__ unsigned cluster_rank() {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ double ld_dsmem(const double* local_ptr, unsigned rank) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(local_ptr);
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
-  return v;
+// generic address of the same shared-memory location in cluster CTA `rank` (plain loads through
+// it stay ordinary memory operations, so the compiler keeps them behind the cluster barrier)
+__device__ __forceinline__ const double* dsmem_map(const double* p, unsigned rank) {
+  uint64_t out;
+  asm("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const double*>(out);
+}
+
+// y[a] -= alpha * x[a] for a in [lo, hi), lanes of one warp; U loads in flight per lane before
+// any store (x and y may alias as far as the compiler knows)
+template <int U>
+__device__ __forceinline__ void warp_axpy(double* y, const double* x, double alpha, int lo, int hi, int lane) {
+  for (int a0 = lo + lane; a0 < hi; a0 += 32 * U) {
+    double xv[U], yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int a = a0 + 32 * u;
+      xv[u] = a < hi ? x[a] : 0.0;
+      yv[u] = a < hi ? y[a] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int a = a0 + 32 * u;
+      if (a < hi) y[a] = __fma_rn(-xv[u], alpha, yv[u]);
+    }
+  }
 }
 
 // ---- 1. gather --------------------------------------------------------------------------
@@ -171,10 +192,14 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
 }
 
 // ---- 3. pivoted Cholesky (dlaqp2 replay) + T on a cluster of C CTAs ------------------------
-template <bool SG>
+// Updates of the Schur complement are deferred over panels of nb pivot steps (the panel's rows
+// of R are replicated in shared memory): a step only forms the entries of row i it needs,
+// S(p, b) - sum_{l in panel} R(l, p) R(l, b), and the owned columns receive the panel's rank-nb
+// update once per panel.
+constexpr int GID_NBMAX = 16;
 __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, GramArgs ga, int64_t sreg) {
   extern __shared__ double smem[];
-  const int C = ga.C;
+  const int C = ga.C, nb = ga.nb;
   const int item = blockIdx.x / C;
   const int c = C > 1 ? (int)cluster_rank() : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
@@ -186,42 +211,67 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     if (c == 0) skel_all_redundant(lv, sk, s);
     return;
   }
-  double* Gm = ga.gbuf + ga.g_off[item];                         // G, then R (R(i, b) at Gm[b*k + i])
-  double* S = SG ? Gm + (int64_t)k * k + (int64_t)c * gid_pack0(k, C) : smem;
-  double* d = smem + sreg;
+  const bool pf = ga.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  long long t0 = pf ? clock64() : 0;
+#define GID_MARK(slot)                                                                                  \
+  if (pf) {                                                                                             \
+    const long long t1 = clock64();                                                                     \
+    atomicAdd(reinterpret_cast<unsigned long long*>(ga.prof + (slot)), (unsigned long long)(t1 - t0)); \
+    t0 = t1;                                                                                            \
+  }
+  double* Gm = ga.gbuf + ga.g_off[item];                              // G, then R (R(i, b) at Gm[b*k + i])
+  double* Sg = Gm + (int64_t)k * k + (int64_t)c * gid_pack0(k, C);   // spill area (when allocated)
+  double* Pn = smem + sreg;                 // nb x k panel rows of R
+  double* d = Pn + (int64_t)nb * k;         // Schur diagonal (replicated)
   double* vn1 = d + k;
   double* vn2 = vn1 + k;
-  double* rowbuf = vn2 + k;   // 2 x k (step parity)
-  double* rowloc = rowbuf + 2 * (int64_t)k;
-  double* sred = rowloc + k;  // 64
+  double* rowbuf = vn2 + k;                 // 2 x k row pieces (step parity), read by the cluster
+  double* sred = rowbuf + 2 * (int64_t)k;   // 64
   int* col_at = reinterpret_cast<int*>(sred + 64);
   int* piv = col_at + k;
   int* sidx = piv + k;
   const int nown = c < k ? (k - c + C - 1) / C : 0;
+  // owned columns 0..nsm-1 in shared memory, the rest spilled to global memory
+  int nsm = 0;
+  while (nsm < nown && gid_coff(nsm + 1, k, c, C) <= sreg) ++nsm;
+  const int64_t split = gid_coff(nsm, k, c, C);
+  auto colp = [&](int lb) -> double* {   // S(., b) - b for owned column b = lb*C + c
+    const int64_t o = gid_coff(lb, k, c, C);
+    return (o < split ? smem + o : Sg + (o - split)) - (lb * C + c);
+  };
   for (int lb = warp; lb < nown; lb += nw) {
     const int b = lb * C + c;
-    double* col = S + gid_coff(lb, k, c, C) - b;
+    double* col = colp(lb);
     const double* src = Gm + (int64_t)b * k;
-    for (int a = b + lane; a < k; a += 32) col[a] = src[a];
+    for (int a0 = b + lane; a0 < k; a0 += 32 * 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = a0 + 32 * u < k ? src[a0 + 32 * u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (a0 + 32 * u < k) col[a0 + 32 * u] = v[u];
+    }
   }
+  ArgMax loc{-1.0, 0x7fffffff};
   for (int j = tid; j < k; j += NT) {
     const double dj = Gm[(int64_t)j * k + j];
+    const double nj = sqrt(fmax(dj, 0.0));
     d[j] = dj;
-    vn1[j] = vn2[j] = sqrt(fmax(dj, 0.0));
+    vn1[j] = vn2[j] = nj;
     col_at[j] = j;
     piv[j] = 0;
+    loc = better(loc, ArgMax{nj, j});
   }
+  ArgMax best = cta_argmax(loc, sred);
   if (C > 1) cluster_barrier();   // G fully read before it is overwritten by R
   else __syncthreads();
+  GID_MARK(0)
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
   const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
   const int mn = min(m, k);
   double cut = 0.0;
-  int r = 0, i = 0;
+  int r = 0, i = 0, np = 0;
   for (; i < mn; ++i) {
-    ArgMax loc{-1.0, 0x7fffffff};
-    for (int j = i + tid; j < k; j += NT) loc = better(loc, ArgMax{vn1[j], j});
-    const ArgMax best = cta_argmax(loc, sred);
     if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
     if (tid == 0 && best.i != i) {
       const int pp = best.i, tcol = col_at[pp];
@@ -236,69 +286,127 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     if (i == 0) cut = cutrel * rd;
     if (rd > cut) ++r;
     const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
-    double* buf = rowbuf + (int64_t)(i & 1) * k;
-    // entries of row i in the columns this CTA owns: R(i, b) = S(p, b) / R(i, i)
+    double* row = Pn + (int64_t)np * k;                       // this step's row of R
+    double* buf = C > 1 ? rowbuf + (int64_t)(i & 1) * k : row;
+    // entries of row i in the owned columns: (S(p, b) - sum_l R(l, p) R(l, b)) / R(i, i)
     for (int lb = tid; lb < nown; lb += NT) {
       const int b = lb * C + c;
-      if (b < p && !piv[b]) buf[b] = S[gid_coff(lb, k, c, C) + (p - b)] * inv;
+      if (b < p && !piv[b]) {
+        double v0 = colp(lb)[p], v1 = 0.0;
+        int l = 0;
+        for (; l + 1 < np; l += 2) {
+          v0 = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v0);
+          v1 = __fma_rn(-Pn[(l + 1) * k + p], Pn[(l + 1) * k + b], v1);
+        }
+        if (l < np) v0 = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v0);
+        buf[b] = (v0 + v1) * inv;
+      }
     }
     const unsigned owner = (unsigned)(p % C);
     if (owner == (unsigned)c) {
-      const double* colp = S + gid_coff(p / C, k, c, C) - p;
-      for (int a = p + 1 + tid; a < k; a += NT) buf[a] = piv[a] ? 0.0 : colp[a] * inv;
-    }
-    __syncthreads();
-    if (tid == 0) piv[p] = 1;
-    if (C > 1) cluster_barrier();
-    else __syncthreads();
-    for (int a = tid; a < k; a += NT) {
-      double v;
-      if (a == p) v = rd;
-      else if (piv[a]) v = 0.0;
-      else {
-        const unsigned src = a < p ? (unsigned)(a % C) : owner;
-        v = src == (unsigned)c ? buf[a] : ld_dsmem(buf + a, src);
+      const double* cp = colp(p / C);
+      for (int a = p + 1 + tid; a < k; a += NT) {
+        double v = 0.0;
+        if (!piv[a]) {
+          double v0 = cp[a], v1 = 0.0;
+          int l = 0;
+          for (; l + 1 < np; l += 2) {
+            v0 = __fma_rn(-Pn[l * k + a], Pn[l * k + p], v0);
+            v1 = __fma_rn(-Pn[(l + 1) * k + a], Pn[(l + 1) * k + p], v1);
+          }
+          if (l < np) v0 = __fma_rn(-Pn[l * k + a], Pn[l * k + p], v0);
+          v = (v0 + v1) * inv;
+        }
+        buf[a] = v;
       }
-      rowloc[a] = v;
     }
-    __syncthreads();
-    for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
-      const int b = lb * C + c;
-      Gm[(int64_t)b * k + i] = rowloc[b];
-    }
-    // rank-1 update of the owned (unpivoted) columns below the diagonal
-    for (int lb = warp; lb < nown; lb += nw) {
-      const int b = lb * C + c;
-      if (piv[b]) continue;
-      const double rb = rowloc[b];
-      if (rb == 0.0) continue;
-      double* col = S + gid_coff(lb, k, c, C) - b;
-      for (int a = b + 1 + lane; a < k; a += 32) col[a] = __fma_rn(-rowloc[a], rb, col[a]);
-    }
-    // replicated Schur diagonal, then the dlaqp2 partial-norm downdate (positions > i)
-    for (int j = tid; j < k; j += NT)
-      if (!piv[j]) d[j] = __fma_rn(-rowloc[j], rowloc[j], d[j]);
-    __syncthreads();
-    for (int j = i + 1 + tid; j < k; j += NT) {
-      const double v1 = vn1[j];
-      if (v1 != 0.0) {
-        const int col = col_at[j];
-        double tt = fabs(rowloc[col]) / v1;
-        tt = 1.0 - tt * tt;
-        tt = tt < 0.0 ? 0.0 : tt;
-        const double rr = v1 / vn2[j];
-        const double t2 = tt * rr * rr;
-        if (t2 <= tol3z) {
-          const double nv = i < m - 1 ? sqrt(fmax(d[col], 0.0)) : 0.0;
-          vn1[j] = nv;
-          vn2[j] = nv;
-        } else {
-          vn1[j] = v1 * sqrt(tt);
+    GID_MARK(2)
+    if (C > 1) {
+      __syncthreads();
+      if (tid == 0) piv[p] = 1;
+      cluster_barrier();
+      GID_MARK(3)
+      for (int a0 = tid; a0 < k; a0 += 4 * NT) {   // 4 remote loads in flight per thread
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int a = a0 + u * NT;
+          v[u] = 0.0;
+          if (a < k && a != p && !piv[a]) v[u] = *dsmem_map(buf + a, a < p ? (unsigned)(a % C) : owner);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int a = a0 + u * NT;
+          if (a < k) row[a] = a == p ? rd : v[u];
         }
       }
+    } else {
+      for (int a = tid; a < k; a += NT)   // pivoted columns (other than p) read as 0
+        if (piv[a] && a != p) row[a] = 0.0;
+      if (tid == 0) {
+        row[p] = rd;
+        piv[p] = 1;
+      }
     }
     __syncthreads();
+    GID_MARK(4)
+    for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
+      const int b = lb * C + c;
+      Gm[(int64_t)b * k + i] = row[b];
+    }
+    // fused: Schur diagonal, dlaqp2 partial-norm downdate and the next pivot's argmax over the
+    // positions > i (identical arithmetic in every CTA)
+    loc = ArgMax{-1.0, 0x7fffffff};
+    for (int j = i + 1 + tid; j < k; j += NT) {
+      const int col = col_at[j];
+      const double rv = row[col];
+      const double dn = __fma_rn(-rv, rv, d[col]);
+      d[col] = dn;
+      double v1 = vn1[j];
+      if (v1 != 0.0) {
+        // dlaqp2: temp = max(0, 1 - (|R(i,j)|/vn1)^2); recompute when temp (vn1/vn2)^2 <= tol3z,
+        // else vn1 *= sqrt(temp) -- in division-free form: w = vn1^2 - R(i,j)^2
+        const double w = fmax(__fma_rn(-rv, rv, v1 * v1), 0.0);
+        const double v2 = vn2[j];
+        if (w <= tol3z * v2 * v2) {
+          v1 = i < m - 1 ? sqrt(fmax(dn, 0.0)) : 0.0;
+          vn2[j] = v1;
+        } else {
+          v1 = sqrt(w);
+        }
+        vn1[j] = v1;
+      }
+      loc = better(loc, ArgMax{v1, j});
+    }
+    best = cta_argmax(loc, sred);
+    GID_MARK(6)
+    if (++np == nb) {   // rank-nb update of the owned, unpivoted columns
+      for (int lb = warp; lb < nown; lb += nw) {
+        const int b = lb * C + c;
+        if (piv[b]) continue;
+        double rb[GID_NBMAX];
+#pragma unroll
+        for (int l = 0; l < GID_NBMAX; ++l) rb[l] = l < np ? Pn[l * k + b] : 0.0;
+        double* col = colp(lb);
+        for (int a0 = b + 1 + lane; a0 < k; a0 += 64) {
+          const int a1 = a0 + 32;
+          double v0 = col[a0], v1 = a1 < k ? col[a1] : 0.0;
+#pragma unroll
+          for (int l = 0; l < GID_NBMAX; ++l)
+            if (l < np) {
+              v0 = __fma_rn(-Pn[l * k + a0], rb[l], v0);
+              if (a1 < k) v1 = __fma_rn(-Pn[l * k + a1], rb[l], v1);
+            }
+          col[a0] = v0;
+          if (a1 < k) col[a1] = v1;
+        }
+      }
+      np = 0;
+      __syncthreads();
+      GID_MARK(5)
+    }
   }
+  if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(ga.prof + 9), (unsigned long long)i);
   const int kt = k - r;
   // redundant flags by column (positions r..k-1) and the sorted-list index of every column
   for (int j = tid; j < k; j += NT) piv[col_at[j]] = j >= r ? 1 : 0;
@@ -319,14 +427,16 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   __threadfence();
   if (C > 1) cluster_barrier();   // all rows of R in global memory; no more remote reads
   else __syncthreads();
+  GID_MARK(7)
   // T = R11^-1 R12 (pivot order) by column back substitution; RHS columns spread over the
-  // cluster's warps, 16/32-column blocks of R11 staged in shared memory (the Schur region is free)
+  // cluster's warps, 16/32-column blocks of R11 staged in shared memory (Schur region + panel)
   if (kt > 0 && r > 0) {
     double* T = sk.rec + sk.T_off[s];
-    double* stage = SG ? smem : S;
-    // staging: BW columns of R11 + NR right-hand sides per warp (host guarantees 24 r <= sreg)
-    const int BW = sreg >= (int64_t)(32 + nw) * r ? 32 : 16;
-    const int NR = max(1, min(4, (int)((sreg / r - BW) / nw)));
+    double* stage = smem;
+    const int64_t sreg2 = sreg + (int64_t)nb * k;
+    // staging: BW columns of R11 + NR right-hand sides per warp (host guarantees 24 k <= sreg2)
+    const int BW = sreg2 >= (int64_t)(32 + nw) * r ? 32 : 16;
+    const int NR = max(1, min(4, (int)((sreg2 / r - BW) / nw)));
     double* Rs = stage;
     double* xs = stage + (int64_t)BW * r + (int64_t)warp * NR * r;
     const int gw = c * nw + warp, nwarps = nw * C;
@@ -344,9 +454,18 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       for (int i0 = ((r - 1) / BW) * BW; i0 >= 0; i0 -= BW) {
         const int ib = min(BW, r - i0), h = i0 + ib;
         __syncthreads();
-        for (int e = tid; e < ib * h; e += NT) {
-          const int qq = e / h, l = e % h;
-          Rs[qq * r + l] = __ldcg(Gm + (int64_t)col_at[i0 + qq] * k + l);
+        for (int e0 = tid; e0 < ib * h; e0 += 4 * NT) {
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * NT;
+            v[u] = e < ib * h ? __ldcg(Gm + (int64_t)col_at[i0 + e / h] * k + e % h) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * NT;
+            if (e < ib * h) Rs[(e / h) * r + e % h] = v[u];
+          }
         }
         __syncthreads();
         for (int ii = ib - 1; ii >= 0 && nj > 0; --ii) {
@@ -358,7 +477,7 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
             const double xi = x[ia] / dg;
             __syncwarp();
             if (lane == 0) x[ia] = xi;
-            for (int l = lane; l < ia; l += 32) x[l] = __fma_rn(-Rc[l], xi, x[l]);
+            warp_axpy<4>(x, Rc, xi, 0, ia, lane);
           }
           __syncwarp();
         }
@@ -370,6 +489,8 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       __syncwarp();
     }
   }
+  GID_MARK(8)
+#undef GID_MARK
   if (c == 0) {
     uint8_t* redp = sk.red + gof;
     for (int j = tid; j < k; j += NT) {

@@ -7,6 +7,7 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <stdexcept>
 
 #include "dla.cuh"
 #include "kernels.cuh"
@@ -490,11 +491,21 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& n
   const int lane = threadIdx.x & 31;
   const int h = nc.h[i], kh = nc.kh[i];
   const double* B = lv.pool + nc.boff[i];
+  // loads are batched ahead of the stores (W and B may alias as far as the compiler knows, so an
+  // unbatched copy loop would pay one full memory latency per element)
+  constexpr int U = 8;
   if (g < h) {
     if ((mask >> lane) & 1u) {
       const int row = row0 + __popc(mask & ((1u << lane) - 1u));
       const double* p = B + r0 + lane;
-      for (int c = 0; c < k; ++c) W[(int64_t)c * ldw + row] = p[(int64_t)c * kh];
+      for (int c0 = 0; c0 < k; c0 += U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = c0 + u < k ? p[(int64_t)(c0 + u) * kh] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u < k) W[(int64_t)(c0 + u) * ldw + row] = v[u];
+      }
     }
   } else {
     int row = row0;
@@ -502,7 +513,14 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& n
       const int rr = __ffs(mask) - 1;
       mask &= mask - 1u;
       const double* p = B + (int64_t)(r0 + rr) * k;
-      for (int c = lane; c < k; c += 32) W[(int64_t)c * ldw + row] = p[c];
+      for (int c0 = lane; c0 < k; c0 += 32 * U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = c0 + 32 * u < k ? p[c0 + 32 * u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + 32 * u < k) W[(int64_t)(c0 + 32 * u) * ldw + row] = v[u];
+      }
       ++row;
     }
   }
@@ -2947,24 +2965,33 @@ void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cud
 
 // ---- Gram-path ID launches (gram_id.cuh) ----
 static constexpr size_t GID_SMEM_CAP = 227 * 1024;
-static int64_t gid_sreg(int k, int C, bool sg) {
-  const int64_t stage = 24 * (int64_t)k;   // back substitution: 16-column R11 block + 1 RHS per warp
-  return sg ? stage : std::max<int64_t>(gid_pack0(k, C), stage);
+int gid_panel(int k) { return k <= 600 ? 16 : 8; }
+static int64_t gid_sreg(int k, int C) {
+  // shared-memory Schur region: the packed share when it fits the CTA budget, else what is left
+  // (columns beyond it spill to global memory); the back substitution stages in region + panel
+  const int nb = gid_panel(k);
+  const int64_t avail = ((int64_t)GID_SMEM_CAP - (int64_t)GidSmem::bytes(0, k, nb)) / (int64_t)sizeof(double);
+  return std::min(avail, std::max<int64_t>(gid_pack0(k, C), std::max<int64_t>(0, (24 - nb) * (int64_t)k)));
 }
 int gid_cluster(int kmax, bool* sg) {
-  // smallest cluster whose per-CTA packed Schur share is at most `target` doubles; the Schur
-  // complement moves to global memory when even 16 CTAs cannot hold it in shared memory
+  // smallest cluster whose per-CTA packed Schur share is at most `target` doubles
   static const int64_t target = getenv("PHIF_GID_PACK") ? atoll(getenv("PHIF_GID_PACK")) : 6144;
   static const int force_c = getenv("PHIF_GID_C") ? atoi(getenv("PHIF_GID_C")) : 0;
+  // one CTA (no per-step cluster exchange) up to c1k columns, the Schur complement spilling
+  // to global memory beyond the shared-memory budget
+  static const int c1k = getenv("PHIF_GID_C1K") ? atoi(getenv("PHIF_GID_C1K")) : 0;
   int C = 16;
   if (force_c) C = force_c;
+  else if (kmax <= c1k) C = 1;
   else
     for (int c : {1, 2, 4, 8, 16})
       if (gid_pack0(kmax, c) <= target) {
         C = c;
         break;
       }
-  *sg = GidSmem::bytes(gid_sreg(kmax, C, false), kmax) > GID_SMEM_CAP;
+  *sg = gid_pack0(kmax, C) > gid_sreg(kmax, C);
+  if (24 * (int64_t)kmax > gid_sreg(kmax, C) + (int64_t)gid_panel(kmax) * kmax)
+    throw std::runtime_error("gram ID: separator too large");
   return C;
 }
 int64_t gid_gbuf_doubles(int k, int C, bool sg) {
@@ -2982,13 +3009,15 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
   if (!attr) {
     attr = true;
     cudaFuncSetAttribute(k_gid_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
-    cudaFuncSetAttribute(k_gid_cpqr<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_gid_cpqr<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_gid_cpqr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   if (g.nwork) k_gid_gram<<<g.nwork, NT, NT_SMEM, s>>>(lv, a, g);
-  int64_t sreg = gid_sreg(kmax, g.C, sg);
-  const size_t bytes = GidSmem::bytes(sreg, kmax);
-  void (*fn)(LevelDev, SkelArgs, GramArgs, int64_t) = sg ? k_gid_cpqr<true> : k_gid_cpqr<false>;
+  int64_t sreg = gid_sreg(kmax, g.C);
+  (void)sg;
+  GramArgs g3 = g;
+  g3.nb = gid_panel(kmax);
+  const size_t bytes = GidSmem::bytes(sreg, kmax, g3.nb);
+  void (*fn)(LevelDev, SkelArgs, GramArgs, int64_t) = k_gid_cpqr;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -3002,7 +3031,7 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
-  cudaLaunchKernelEx(&cfg, fn, lv2, a2, g2, sreg);
+  cudaLaunchKernelEx(&cfg, fn, lv2, a2, g3, sreg);
 }
 
 void configure_kernels() {

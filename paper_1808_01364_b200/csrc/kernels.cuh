@@ -137,6 +137,8 @@ struct GramArgs {
   const int* w_j;
   int nwork;
   int C;                   // CPQR cluster size
+  int nb;                  // deferred-update panel width (<= 16)
+  long long* prof;         // optional phase clocks of CTA 0 (PHIF_GID_PROF)
 };
 
 struct RepackArgs {
