@@ -879,6 +879,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     ka.rank = L.s_rank.as<int>();
     ka.rows = L.s_rows.as<int>();
     ka.eps = F->eps;
+    {
+      // Gram-path ID when the ID tolerance leaves room for the squared conditioning of A^T A
+      // (the rank cut sits far above sqrt(k eps_mach)); PHIF_GID=0 keeps Householder CPQR
+      static const bool gid_on = !getenv("PHIF_GID") || atoi(getenv("PHIF_GID")) != 0;
+      static const double gid_eps = getenv("PHIF_GID_EPS") ? atof(getenv("PHIF_GID_EPS")) : 1e-5;
+      ka.gram = (gid_on && F->eps >= gid_eps) ? 1 : 0;
+    }
     ka.work = wk.as<double>();
     ka.work_off = L.s_work_off.as<int64_t>();
     ka.iwork = iwk.as<int>();
@@ -934,11 +941,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           slot_off(P.nwaves + 1, 0);
       std::vector<int> wave_blocks(P.nwaves, 0), wave_vcap(P.nwaves, 0), wave_kmax(P.nwaves, 0), wave_mmax(P.nwaves, 0);
       std::vector<int> wave_cluster(P.nwaves, 0);
-      // Gram-path ID (gram_id.cuh) for the large separators when the ID tolerance leaves room
-      // for the squared conditioning of A^T A (the rank cut sits far above sqrt(k eps_mach))
-      static const bool gid_on = !getenv("PHIF_GID") || atoi(getenv("PHIF_GID")) != 0;
-      static const double gid_eps = getenv("PHIF_GID_EPS") ? atof(getenv("PHIF_GID_EPS")) : 1e-5;
-      const bool use_gid = gid_on && F->eps >= gid_eps;
+      // Gram-path ID (gram_id.cuh) for the large separators under the same rule
+      const bool use_gid = ka.gram != 0;
       std::vector<int> gid_item, gid_wi, gid_wj, gid_wit;
       std::vector<int64_t> gid_ld, gid_goff, gid_item_off(P.nwaves + 1, 0), gid_w_off(P.nwaves + 1, 0);
       std::vector<int> gid_C(P.nwaves, 1), gid_kmax(P.nwaves, 0), gid_P(P.nwaves, 1);

@@ -583,6 +583,178 @@ __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s
   if (threadIdx.x == 0) sk.rank[s] = 0;
 }
 
+// Gram-path ID of one small separator (k <= 57) on one CTA: G = A^T A by DMMA into smem[0, k^2),
+// then the pivoted Cholesky replay of dlaqp2 (see gram_id.cuh) with the full symmetric Schur
+// complement updated in place, then T = R11^-1 R12 (4 threads per right-hand side). The
+// workspace after G reuses the gathered matrix's region (base = smem + SMEM_DOUBLES).
+// Returns false (nothing written) when the shapes do not fit; the caller then runs cta_cpqr.
+__device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int k, const double* W, int64_t ldw,
+                             int m, double* smem, int cap) {
+  if (k > 57 || k * k > RED_OFF || (int64_t)k * k + 5 * k + 8 > cap) return false;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  const int g = sk.groups[s];
+  const int64_t gof = lv.goff[g];
+  double* S = smem;                        // k x k (G, then the Schur complement; then R permuted)
+  double* sred = smem + RED_OFF;
+  double* base = smem + SMEM_DOUBLES;
+  double* Rsm = base;                      // k x k: row i of R at Rsm[i*k + column]
+  double* d = Rsm + k * k;
+  double* vn1 = d + k;
+  double* vn2 = vn1 + k;
+  int* col_at = reinterpret_cast<int*>(vn2 + k);
+  int* piv = col_at + k;
+  int* sidx = piv + k;
+  // G = W^T W: lower 8x8 tiles, one DMMA chain per tile (K = m in steps of 4), mirrored
+  {
+    const int gq = lane >> 2, t4 = lane & 3;
+    const int nt = (k + 7) / 8, ntl = nt * (nt + 1) / 2;
+    for (int tix = warp; tix < ntl; tix += nw) {
+      int it = 0;
+      while ((it + 1) * (it + 2) / 2 <= tix) ++it;
+      const int jt = tix - it * (it + 1) / 2;
+      const int a = it * 8 + gq, b = jt * 8 + gq;
+      const double* Wa = W + (int64_t)min(a, k - 1) * ldw;
+      const double* Wb = W + (int64_t)min(b, k - 1) * ldw;
+      const bool oka = a < k, okb = b < k;
+      double c0 = 0.0, c1 = 0.0;
+      for (int r0 = 0; r0 < m; r0 += 4) {
+        const int r = r0 + t4;
+        const double av = (oka && r < m) ? Wa[r] : 0.0;
+        const double bv = (okb && r < m) ? Wb[r] : 0.0;
+        dmma(c0, c1, av, bv);
+      }
+      const int row = it * 8 + gq, col = jt * 8 + 2 * t4;
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const double v = z ? c1 : c0;
+        if (row < k && col + z < k) {
+          S[row * k + col + z] = v;
+          S[(col + z) * k + row] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  ArgMax loc{-1.0, 0x7fffffff};
+  for (int j = tid; j < k; j += NT) {
+    const double dj = S[j * k + j];
+    const double nj = sqrt(fmax(dj, 0.0));
+    d[j] = dj;
+    vn1[j] = vn2[j] = nj;
+    col_at[j] = j;
+    piv[j] = 0;
+    loc = better(loc, ArgMax{nj, j});
+  }
+  ArgMax best = cta_argmax(loc, sred);
+  const double tol3z = sqrt(DBL_EPSILON * 0.5);
+  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
+  const int mn = min(m, k);
+  double cut = 0.0;
+  int r = 0, i = 0;
+  for (; i < mn; ++i) {
+    if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
+    if (tid == 0 && best.i != i) {
+      const int pp = best.i, tcol = col_at[pp];
+      col_at[pp] = col_at[i];
+      col_at[i] = tcol;
+      vn1[pp] = vn1[i];
+      vn2[pp] = vn2[i];
+    }
+    __syncthreads();
+    const int p = col_at[i];
+    const double rd = sqrt(fmax(d[p], 0.0));
+    if (i == 0) cut = cutrel * rd;
+    if (rd > cut) ++r;
+    const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
+    double* row = Rsm + i * k;
+    for (int a = tid; a < k; a += NT) row[a] = a == p ? rd : (piv[a] ? 0.0 : S[p * k + a] * inv);
+    __syncthreads();
+    if (tid == 0) piv[p] = 1;
+    // rank-1 update (rows of pivoted columns have R(i, a) = 0; row/column p become garbage and
+    // are never read again)
+    for (int a = warp; a < k; a += nw) {
+      const double ra = row[a];
+      if (ra == 0.0 || a == p) continue;
+      for (int b = lane; b < k; b += 32) S[a * k + b] = __fma_rn(-ra, row[b], S[a * k + b]);
+    }
+    loc = ArgMax{-1.0, 0x7fffffff};
+    for (int j = i + 1 + tid; j < k; j += NT) {
+      const int col = col_at[j];
+      const double rv = row[col];
+      const double dn = __fma_rn(-rv, rv, d[col]);
+      d[col] = dn;
+      double v1 = vn1[j];
+      if (v1 != 0.0) {
+        const double w = fmax(__fma_rn(-rv, rv, v1 * v1), 0.0);
+        const double v2 = vn2[j];
+        if (w <= tol3z * v2 * v2) {
+          v1 = i < m - 1 ? sqrt(fmax(dn, 0.0)) : 0.0;
+          vn2[j] = v1;
+        } else {
+          v1 = sqrt(w);
+        }
+        vn1[j] = v1;
+      }
+      loc = better(loc, ArgMax{v1, j});
+    }
+    best = cta_argmax(loc, sred);
+  }
+  const int kt = k - r;
+  for (int j = tid; j < k; j += NT) piv[col_at[j]] = j >= r ? 1 : 0;
+  __syncthreads();
+  if (warp == 0) {
+    int ns = 0, nr = 0;
+    for (int j0 = 0; j0 < k; j0 += 32) {
+      const int j = j0 + lane;
+      const bool ok = j < k;
+      const int f = ok ? piv[j] : 0;
+      const unsigned bf = __ballot_sync(0xffffffffu, ok && f), bs = __ballot_sync(0xffffffffu, ok && !f);
+      const unsigned below = (1u << lane) - 1u;
+      if (ok) sidx[j] = f ? nr + __popc(bf & below) : ns + __popc(bs & below);
+      nr += __popc(bf);
+      ns += __popc(bs);
+    }
+  }
+  // R in pivot order (rows < r): Rp[i*k + l] = R(i, col_at[l]), in the Schur region
+  double* Rp = S;
+  for (int e = tid; e < r * k; e += NT) Rp[e] = Rsm[(e / k) * k + col_at[e % k]];
+  __syncthreads();
+  if (kt > 0 && r > 0) {
+    // X = R11^-1 R12: thread (j, q) = (tid / 4, tid % 4) sums the terms l = q mod 4
+    double* X = Rsm;   // r x kt
+    for (int e = tid; e < r * kt; e += NT) X[e] = Rp[(e / kt) * k + r + e % kt];
+    __syncthreads();
+    const int q = tid & 3;
+    for (int j0 = 0; j0 < kt; j0 += NT / 4) {
+      const int j = j0 + (tid >> 2);
+      const bool act = j < kt;
+      for (int ii = r - 1; ii >= 0; --ii) {
+        double sacc = 0.0;
+        if (act)
+          for (int l = ii + 1 + q; l < r; l += 4) sacc = __fma_rn(Rp[ii * k + l], X[l * kt + j], sacc);
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+        if (act && q == 0) X[ii * kt + j] = (X[ii * kt + j] - sacc) / Rp[ii * k + ii];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    double* T = sk.rec + sk.T_off[s];
+    for (int e = tid; e < r * kt; e += NT) {
+      const int ii = e / kt, j = e % kt;
+      T[(int64_t)sidx[col_at[ii]] * kt + sidx[col_at[r + j]]] = X[e];
+    }
+  }
+  uint8_t* red = sk.red + gof;
+  for (int j = tid; j < k; j += NT) {
+    const int f = piv[j];
+    red[j] = (uint8_t)f;
+    if (f) sk.alive[lv.mem[gof + j]] = 0;
+  }
+  if (tid == 0) sk.rank[s] = r;
+  return true;
+}
+
 __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int smem_cap) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
@@ -611,6 +783,10 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
   if (m == 0) {
     skel_all_redundant(lv, sk, s);
     return;
+  }
+  if (sk.gram) {
+    __syncthreads();   // gathered rows visible to every warp
+    if (skel_id_gram(lv, sk, s, k, W, ldw, m, smem, smem_cap)) return;
   }
   const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
   const int steps = cta_cpqr(W, m, k, ldw, perm, vn1, vn2, sred, cutrel);

@@ -79,6 +79,7 @@ struct SkelArgs {
   int* rank;                 // per skeleton
   int* rows;                 // per skeleton: rows of A_{R,I} after filtering
   double eps;
+  int gram;                  // 1: separators of <= 57 columns take the Gram-path ID (skel_id_gram)
   double* work;              // per skeleton workspace
   const int64_t* work_off;
   int* iwork;
