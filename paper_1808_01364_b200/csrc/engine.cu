@@ -231,12 +231,17 @@ struct BigPlan {
     std::vector<int> wc, wi, wj;
     // trailing tiles of cell c for columns [base, cend), rows [base, rows): skip tiles strictly
     // above the diagonal of the square part
-    auto trailing = [&](int c, int base, int cend) {
+    // Identity row i (panel row n+b+i) holds nonzeros only in columns >= i (it becomes row i of
+    // L^-T), so its update from the K range [.., kend) vanishes when i >= kend: such tiles are
+    // skipped (zero_tile).
+    auto zero_tile = [&](int c, int r0, int kend) { return r0 - (n[c] + b[c]) >= kend; };
+    auto trailing = [&](int c, int base, int cend, int kend) {
       if (base >= cend) return;
       const int nr = (rws[c] - base + T - 1) / T, nc = (cend - base + T - 1) / T;
       for (int it = 0; it < nr; ++it)
         for (int jt = 0; jt < nc; ++jt) {
           if (jt > it && base + T * (it + 1) <= n[c]) continue;
+          if (zero_tile(c, base + T * it, kend)) continue;
           wc.push_back(c);
           wi.push_back(it);
           wj.push_back(jt);
@@ -258,6 +263,7 @@ struct BigPlan {
           const int kb = std::min(T, n[c] - s0), base = s0 + kb;
           const int ntr = (rws[c] - base + T - 1) / T;
           for (int it = 0; it < ntr; ++it) {
+            if (zero_tile(c, base + T * it, s0 + kb)) continue;
             wc.push_back(c);
             wi.push_back(it);
             wj.push_back(0);
@@ -265,7 +271,7 @@ struct BigPlan {
         }
         ph.off[2] = (int64_t)wc.size();
         for (int c = 0; c < nbig; ++c)
-          if (n[c] > s0 + T) trailing(c, s0 + T, std::min(n[c], kb0 + KB));
+          if (n[c] > s0 + T) trailing(c, s0 + T, std::min(n[c], kb0 + KB), s0 + T);
         ph.cnt[0] = ph.off[1] - ph.off[0];
         ph.cnt[1] = ph.off[2] - ph.off[1];
         ph.cnt[2] = (int64_t)wc.size() - ph.off[2];
@@ -273,7 +279,7 @@ struct BigPlan {
       }
       Phase wide{1, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
       for (int c = 0; c < nbig; ++c)
-        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, n[c]);
+        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, n[c], kb0 + KB);
       wide.cnt[0] = (int64_t)wc.size() - wide.off[0];
       if (wide.cnt[0]) phases.push_back(wide);
     }
@@ -327,6 +333,7 @@ struct BigPlan {
       else
         launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), ph.kind == 1 ? 0 : 1, s);
     }
+    if (nbig) launch_big_zero_upper(args(0, 0, 0, 0), s);
   }
 };
 
@@ -2045,6 +2052,8 @@ std::string Factorization::stats_json() const {
       << ",\"blocks\":" << P.pat.bg.size() << ",\"waves\":" << P.nwaves << ",\"rho_max\":" << L.rho_max
       << ",\"rho_mean\":" << L.rho_mean << ",\"sep_k_mean\":" << L.sep_k_mean << ",\"sep_k_max\":" << L.sep_k_max
       << ",\"sep_m_mean\":" << L.sep_m_mean << ",\"sep_m_max\":" << L.sep_m_max << ",\"n_large\":" << L.n_large << ",\"n_gid\":" << L.n_gid
+      << ",\"cell_n_max\":" << (P.cell_n.empty() ? 0 : *std::max_element(P.cell_n.begin(), P.cell_n.end()))
+      << ",\"cell_b_max\":" << (P.cell_b.empty() ? 0 : *std::max_element(P.cell_b.begin(), P.cell_b.end()))
       << ",\"team_P_mean\":" << L.team_P_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
       << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
       << L.t_ms[4] << ",\"t_plan_ms\":" << L.t_ms[5] << ",\"t_wall_ms\":" << L.t_wall_ms << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]

@@ -16,13 +16,12 @@
 //                                 the early stop of cta_cpqr, count-based rank; then
 //                                 T = R11^-1 R12 by blocked back substitution across the cluster.
 //
-// The Schur complement is stored packed-lower and column-cyclic across the cluster's CTAs
-// (column b lives in CTA b % C, rows b..k-1), in shared memory up to the CTA's budget and the
-// remaining columns in a global spill area. Partial norms, Schur diagonal and column positions are
-// replicated in every CTA and updated with identical arithmetic, so every CTA selects the same
-// pivot without communication; the only exchange per pivot step is row i of R (each CTA
-// computes the entries of the columns it owns, one cluster barrier, then reads the row through
-// distributed shared memory).
+// The Schur complement is stored column-cyclic across the cluster's CTAs (full column b lives in
+// CTA b % C), in shared memory up to the CTA's budget and the remaining columns in a global spill
+// area. Partial norms, Schur diagonal and column positions are replicated in every CTA and
+// updated with identical arithmetic, so every CTA selects the same pivot without communication;
+// the only exchange per pivot step is row i of R (each CTA computes the entries of the columns
+// it owns and pushes them to every CTA through distributed shared memory).
 
 struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
   // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][64] doubles, then 3k ints
@@ -34,13 +33,8 @@ struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
   }
 };
 
-// packed-lower offset of CTA c's local column lb (global column b = lb*C + c, rows b..k-1)
-__host__ __device__ __forceinline__ int64_t gid_coff(int lb, int k, int c, int C) {
-  return (int64_t)lb * (k - c) - (int64_t)C * lb * (lb - 1) / 2;
-}
-__host__ __device__ __forceinline__ int64_t gid_pack0(int k, int C) {   // largest per-CTA packed size (c = 0)
-  return gid_coff((k + C - 1) / C, k, 0, C);
-}
+// largest per-CTA share of the Schur complement (full owned columns)
+__host__ __device__ __forceinline__ int64_t gid_pack0(int k, int C) { return (int64_t)((k + C - 1) / C) * k; }
 
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
@@ -187,16 +181,50 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
         const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
-        if (i < Mv && j < Nv) Gm[(int64_t)(br0 + j) * k + ar0 + i] = acc[x][y][z];
+        if (i < Mv && j < Nv) {
+          Gm[(int64_t)(br0 + j) * k + ar0 + i] = acc[x][y][z];
+          if (it != jt) Gm[(int64_t)(ar0 + i) * k + br0 + j] = acc[x][y][z];   // mirror: full G
+        }
       }
 }
 
 // ---- 3. pivoted Cholesky (dlaqp2 replay) + T on a cluster of C CTAs ------------------------
-// Updates of the Schur complement are deferred over panels of nb pivot steps (the panel's rows
-// of R are replicated in shared memory): a step only forms the entries of row i it needs,
-// S(p, b) - sum_{l in panel} R(l, p) R(l, b), and the owned columns receive the panel's rank-nb
-// update once per panel.
+// CTA c owns the full columns b = c, c+C, ... of the Schur complement (shared memory up to its
+// budget, the rest in a global spill area). Updates are deferred over panels of nb pivot steps
+// (the panel's rows of R are replicated in shared memory): step i forms only row i,
+// R(i, b) = (S(p, b) - sum_{l in panel} R(l, p) R(l, b)) / R(i, i), each CTA for its own columns,
+// and pushes those entries into every CTA's row buffer with st.async, completing bytes on the
+// receiver's mbarrier (no cluster-wide barrier per step). The owned columns receive the
+// panel's rank-nb update once per panel.
 constexpr int GID_NBMAX = 16;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const uint32_t a = smem_addr(bar);
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, GramArgs ga, int64_t sreg) {
   extern __shared__ double smem[];
   const int C = ga.C, nb = ga.nb;
@@ -219,31 +247,27 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     atomicAdd(reinterpret_cast<unsigned long long*>(ga.prof + (slot)), (unsigned long long)(t1 - t0)); \
     t0 = t1;                                                                                            \
   }
-  double* Gm = ga.gbuf + ga.g_off[item];                              // G, then R (R(i, b) at Gm[b*k + i])
-  double* Sg = Gm + (int64_t)k * k + (int64_t)c * gid_pack0(k, C);   // spill area (when allocated)
+  const int nown0 = (k + C - 1) / C;
+  double* Gm = ga.gbuf + ga.g_off[item];                              // G (full), then R (R(i, b) at Gm[b*k + i])
+  double* Sg = Gm + (int64_t)k * k + (int64_t)c * nown0 * k;         // spill area (when allocated)
   double* Pn = smem + sreg;                 // nb x k panel rows of R
   double* d = Pn + (int64_t)nb * k;         // Schur diagonal (replicated)
   double* vn1 = d + k;
   double* vn2 = vn1 + k;
-  double* rowbuf = vn2 + k;                 // 2 x k row pieces (step parity), read by the cluster
-  double* sred = rowbuf + 2 * (int64_t)k;   // 64
+  double* rowbuf = vn2 + k;                 // 2 x k receive buffers (step parity)
+  double* sred = rowbuf + 2 * (int64_t)k;   // 64 (sred[48..49]: the two mbarriers)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sred + 48);
   int* col_at = reinterpret_cast<int*>(sred + 64);
   int* piv = col_at + k;
   int* sidx = piv + k;
   const int nown = c < k ? (k - c + C - 1) / C : 0;
-  // owned columns 0..nsm-1 in shared memory, the rest spilled to global memory
-  int nsm = 0;
-  while (nsm < nown && gid_coff(nsm + 1, k, c, C) <= sreg) ++nsm;
-  const int64_t split = gid_coff(nsm, k, c, C);
-  auto colp = [&](int lb) -> double* {   // S(., b) - b for owned column b = lb*C + c
-    const int64_t o = gid_coff(lb, k, c, C);
-    return (o < split ? smem + o : Sg + (o - split)) - (lb * C + c);
-  };
+  const int nsm = (int)(sreg / k < nown ? sreg / k : nown);   // owned columns resident in shared memory
+  auto colf = [&](int lb) -> double* { return lb < nsm ? smem + (int64_t)lb * k : Sg + (int64_t)(lb - nsm) * k; };
   for (int lb = warp; lb < nown; lb += nw) {
     const int b = lb * C + c;
-    double* col = colp(lb);
+    double* col = colf(lb);
     const double* src = Gm + (int64_t)b * k;
-    for (int a0 = b + lane; a0 < k; a0 += 32 * 4) {
+    for (int a0 = lane; a0 < k; a0 += 32 * 4) {
       double v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = a0 + 32 * u < k ? src[a0 + 32 * u] : 0.0;
@@ -262,10 +286,16 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     piv[j] = 0;
     loc = better(loc, ArgMax{nj, j});
   }
+  if (C > 1 && tid == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(mbar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   ArgMax best = cta_argmax(loc, sred);
-  if (C > 1) cluster_barrier();   // G fully read before it is overwritten by R
+  if (C > 1) cluster_barrier();   // G read, mbarriers initialised cluster-wide
   else __syncthreads();
   GID_MARK(0)
+  const uint32_t rb_addr = smem_addr(rowbuf), bar_addr = smem_addr(mbar);
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
   const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
   const int mn = min(m, k);
@@ -273,6 +303,8 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   int r = 0, i = 0, np = 0;
   for (; i < mn; ++i) {
     if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
+    const int q = i & 1;
+    if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1));
     if (tid == 0 && best.i != i) {
       const int pp = best.i, tcol = col_at[pp];
       col_at[pp] = col_at[i];
@@ -286,69 +318,45 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     if (i == 0) cut = cutrel * rd;
     if (rd > cut) ++r;
     const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
-    double* row = Pn + (int64_t)np * k;                       // this step's row of R
-    double* buf = C > 1 ? rowbuf + (int64_t)(i & 1) * k : row;
-    // entries of row i in the owned columns: (S(p, b) - sum_l R(l, p) R(l, b)) / R(i, i)
-    for (int lb = tid; lb < nown; lb += NT) {
+    double* row = Pn + (int64_t)np * k;   // this step's row of R
+    // entries of row i in the owned columns, 8 threads per column (panel terms split 8 ways)
+    for (int cb0 = 0; cb0 < nown; cb0 += NT / 8) {
+      const int lb = cb0 + (tid >> 3), part = tid & 7;
       const int b = lb * C + c;
-      if (b < p && !piv[b]) {
-        double v0 = colp(lb)[p], v1 = 0.0;
-        int l = 0;
-        for (; l + 1 < np; l += 2) {
-          v0 = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v0);
-          v1 = __fma_rn(-Pn[(l + 1) * k + p], Pn[(l + 1) * k + b], v1);
-        }
-        if (l < np) v0 = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v0);
-        buf[b] = (v0 + v1) * inv;
+      const bool act = lb < nown && b != p && !piv[b];
+      double v = 0.0;
+      if (act) {
+        for (int l = part; l < np; l += 8) v = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v);
+        if (part == 0) v += colf(lb)[p];
       }
-    }
-    const unsigned owner = (unsigned)(p % C);
-    if (owner == (unsigned)c) {
-      const double* cp = colp(p / C);
-      for (int a = p + 1 + tid; a < k; a += NT) {
-        double v = 0.0;
-        if (!piv[a]) {
-          double v0 = cp[a], v1 = 0.0;
-          int l = 0;
-          for (; l + 1 < np; l += 2) {
-            v0 = __fma_rn(-Pn[l * k + a], Pn[l * k + p], v0);
-            v1 = __fma_rn(-Pn[(l + 1) * k + a], Pn[(l + 1) * k + p], v1);
-          }
-          if (l < np) v0 = __fma_rn(-Pn[l * k + a], Pn[l * k + p], v0);
-          v = (v0 + v1) * inv;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      if (act) {
+        v *= inv;
+        if (C > 1) {
+          for (int dst = part; dst < C; dst += 8)
+            st_async_f64(mapa_u32(rb_addr + (uint32_t)(q * k + b) * 8u, (unsigned)dst), v,
+                         mapa_u32(bar_addr + 8u * q, (unsigned)dst));
+        } else if (part == 0) {
+          row[b] = v;
         }
-        buf[a] = v;
       }
     }
     GID_MARK(2)
     if (C > 1) {
-      __syncthreads();
-      if (tid == 0) piv[p] = 1;
-      cluster_barrier();
+      mbar_wait(mbar + q, (unsigned)((i >> 1) & 1));
       GID_MARK(3)
-      for (int a0 = tid; a0 < k; a0 += 4 * NT) {   // 4 remote loads in flight per thread
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int a = a0 + u * NT;
-          v[u] = 0.0;
-          if (a < k && a != p && !piv[a]) v[u] = *dsmem_map(buf + a, a < p ? (unsigned)(a % C) : owner);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int a = a0 + u * NT;
-          if (a < k) row[a] = a == p ? rd : v[u];
-        }
-      }
+      const double* rb = rowbuf + (int64_t)q * k;
+      for (int a = tid; a < k; a += NT) row[a] = a == p ? rd : (piv[a] ? 0.0 : rb[a]);
     } else {
-      for (int a = tid; a < k; a += NT)   // pivoted columns (other than p) read as 0
-        if (piv[a] && a != p) row[a] = 0.0;
-      if (tid == 0) {
-        row[p] = rd;
-        piv[p] = 1;
-      }
+      __syncthreads();
+      for (int a = tid; a < k; a += NT)
+        if (a == p) row[a] = rd;
+        else if (piv[a]) row[a] = 0.0;
     }
     __syncthreads();
+    if (tid == 0) piv[p] = 1;
     GID_MARK(4)
     for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
       const int b = lb * C + c;
@@ -380,25 +388,42 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     }
     best = cta_argmax(loc, sred);
     GID_MARK(6)
-    if (++np == nb) {   // rank-nb update of the owned, unpivoted columns
-      for (int lb = warp; lb < nown; lb += nw) {
-        const int b = lb * C + c;
-        if (piv[b]) continue;
-        double rb[GID_NBMAX];
+    if (++np == nb) {   // rank-nb update of the owned, unpivoted columns (all rows)
+      // one warp per pair of owned columns, two rows per lane: each panel value loaded from shared
+      // memory feeds two FMAs, four independent accumulation chains per lane
+      for (int lp = warp; 2 * lp < nown; lp += nw) {
+        const int lb1 = 2 * lp, lb2 = 2 * lp + 1;
+        const bool u1 = !piv[lb1 * C + c], u2 = lb2 < nown && !piv[lb2 * C + c];
+        if (!u1 && !u2) continue;
+        double r1[GID_NBMAX], r2[GID_NBMAX];
 #pragma unroll
-        for (int l = 0; l < GID_NBMAX; ++l) rb[l] = l < np ? Pn[l * k + b] : 0.0;
-        double* col = colp(lb);
-        for (int a0 = b + 1 + lane; a0 < k; a0 += 64) {
+        for (int l = 0; l < GID_NBMAX; ++l) {
+          r1[l] = (u1 && l < np) ? Pn[l * k + lb1 * C + c] : 0.0;
+          r2[l] = (u2 && l < np) ? Pn[l * k + lb2 * C + c] : 0.0;
+        }
+        double* c1 = colf(lb1);
+        double* c2 = u2 ? colf(lb2) : c1;
+        for (int a0 = lane; a0 < k; a0 += 64) {
           const int a1 = a0 + 32;
-          double v0 = col[a0], v1 = a1 < k ? col[a1] : 0.0;
+          const bool ok1 = a1 < k;
+          double x00 = c1[a0], x01 = ok1 ? c1[a1] : 0.0, x10 = c2[a0], x11 = ok1 ? c2[a1] : 0.0;
 #pragma unroll
           for (int l = 0; l < GID_NBMAX; ++l)
             if (l < np) {
-              v0 = __fma_rn(-Pn[l * k + a0], rb[l], v0);
-              if (a1 < k) v1 = __fma_rn(-Pn[l * k + a1], rb[l], v1);
+              const double pa = Pn[l * k + a0], pb = ok1 ? Pn[l * k + a1] : 0.0;
+              x00 = __fma_rn(-pa, r1[l], x00);
+              x01 = __fma_rn(-pb, r1[l], x01);
+              x10 = __fma_rn(-pa, r2[l], x10);
+              x11 = __fma_rn(-pb, r2[l], x11);
             }
-          col[a0] = v0;
-          if (a1 < k) col[a1] = v1;
+          if (u1) {
+            c1[a0] = x00;
+            if (ok1) c1[a1] = x01;
+          }
+          if (u2) {
+            c2[a0] = x10;
+            if (ok1) c2[a1] = x11;
+          }
         }
       }
       np = 0;

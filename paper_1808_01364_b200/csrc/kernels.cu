@@ -1913,8 +1913,17 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
     Lo[e] = Li[i * BLD + j];
     if (i < kb && j < kb) P[(int64_t)(k0 + i) * n + k0 + j] = (j <= i) ? D[i * BLD + j] : 0.0;
   }
-  // zero the strict upper part above this diagonal block (rows < k0, cols k0..k0+kb)
-  for (int64_t e = tid; e < (int64_t)k0 * kb; e += NT) P[(e / kb) * n + k0 + e % kb] = 0.0;
+  // (the strict upper part of the square block is zeroed once at the end: k_big_zero_upper)
+}
+
+// zero the strict upper triangle of every big panel's square part (never read by the steps)
+__global__ void k_big_zero_upper(BigArgs a, int chunks) {
+  const int c = blockIdx.x / chunks, ch = blockIdx.x % chunks;
+  if (c >= a.ncell) return;
+  const int n = a.n[c];
+  double* P = a.P[c];
+  for (int r = ch; r < n - 1; r += chunks)
+    for (int j = r + 1 + (int)threadIdx.x; j < n; j += blockDim.x) P[(int64_t)r * n + j] = 0.0;
 }
 
 // acc += A (64 x 64) * B^T (64 x 64) on DMMA, both tiles row-major in smem (ld BLD)
@@ -2977,6 +2986,12 @@ void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& up
   }
   launch_big_nt(upd, 0, s);
 }
+void launch_big_zero_upper(const BigArgs& a, cudaStream_t s) {
+  if (!a.ncell) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int chunks = 64;
+  k_big_zero_upper<<<a.ncell * chunks, 256, 0, s>>>(a, chunks);
+}
 void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s) {
   if (!a.nwork) return;
   static bool init = false;
@@ -3141,7 +3156,11 @@ void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cud
 
 // ---- Gram-path ID launches (gram_id.cuh) ----
 static constexpr size_t GID_SMEM_CAP = 227 * 1024;
-int gid_panel(int k) { return k <= 600 ? 16 : 8; }
+int gid_panel(int k) {
+  static const int nb = getenv("PHIF_GID_NB") ? atoi(getenv("PHIF_GID_NB")) : 0;
+  if (nb > 0) return std::min(nb, 16);
+  return k <= 600 ? 16 : 8;
+}
 static int64_t gid_sreg(int k, int C) {
   // shared-memory Schur region: the packed share when it fits the CTA budget, else what is left
   // (columns beyond it spill to global memory); the back substitution stages in region + panel
@@ -3151,7 +3170,7 @@ static int64_t gid_sreg(int k, int C) {
 }
 int gid_cluster(int kmax, bool* sg) {
   // smallest cluster whose per-CTA packed Schur share is at most `target` doubles
-  static const int64_t target = getenv("PHIF_GID_PACK") ? atoll(getenv("PHIF_GID_PACK")) : 6144;
+  static const int64_t target = getenv("PHIF_GID_PACK") ? atoll(getenv("PHIF_GID_PACK")) : 12288;
   static const int force_c = getenv("PHIF_GID_C") ? atoi(getenv("PHIF_GID_C")) : 0;
   // one CTA (no per-step cluster exchange) up to c1k columns, the Schur complement spilling
   // to global memory beyond the shared-memory budget

@@ -78,7 +78,8 @@ int64_t gid_gbuf_doubles(int k, int C, bool sg);
 void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int kmax, bool sg, cudaStream_t s);
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s);
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
-void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);   // 0: trailing update, 1: U = X^T X
+void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);
+void launch_big_zero_upper(const BigArgs& a, cudaStream_t s);   // 0: trailing update, 1: U = X^T X
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s);
 // replay GEMM (N = nrhs <= 32, A streamed from global, B chunk in shared memory); falls back to launch_bgemm
 void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s);
