@@ -584,15 +584,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     LevelDev dv = L.dev();
     if (timing) CK(cudaEventRecord(ev[0], s));
     if (lev == 0) {
-      std::vector<int> gid(sp.N), pos(sp.N);
-      for (int g = 0; g < G.G; ++g)
-        for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) {
-          gid[G.mem[q]] = g;
-          pos[G.mem[q]] = (int)(q - G.off[g]);
-        }
       DBuf dgid, dpos;
-      upload(dgid, gid, s);
-      upload(dpos, pos, s);
+      dgid.alloc(sp.N * sizeof(int), s);
+      dpos.alloc(sp.N * sizeof(int), s);
+      launch_group_pos(dv, dgid.as<int>(), dpos.as<int>(), s);
       launch_ingest(dv, dgid.as<int>(), dpos.as<int>(), A.rowptr.as<int64_t>(), A.col.as<int>(),
                     A.val.as<double>(), sp.N, s);
       CK(cudaStreamSynchronize(s));

@@ -53,6 +53,18 @@ __global__ void k_ingest(LevelDev lv, const int* gid, const int* pos, const int6
   }
 }
 
+// group and position of every member DOF (one warp per group)
+__global__ void k_group_pos(LevelDev lv, int* gid, int* pos) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= lv.G) return;
+  const int64_t q0 = lv.goff[w], q1 = lv.goff[w + 1];
+  for (int64_t q = q0 + lane; q < q1; q += 32) {
+    const int d = lv.mem[q];
+    gid[d] = w;
+    pos[d] = (int)(q - q0);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Stage 1: cell elimination.
 // Panel P = [A_II ; A_BI] ((n+b) x n) -> partial Cholesky -> [L ; X^T]; U = X^T X.
@@ -2823,6 +2835,11 @@ void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int
   if (N == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_ingest<<<nblk(N, 256), 256, 0, s>>>(lv, gid, pos, rowptr, col, val, N);
+}
+void launch_group_pos(const LevelDev& lv, int* gid, int* pos, cudaStream_t s) {
+  if (lv.G == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_group_pos<<<nblk((int64_t)lv.G * 32, 256), 256, 0, s>>>(lv, gid, pos);
 }
 void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st, cudaStream_t s) {
   if (count == 0) return;
