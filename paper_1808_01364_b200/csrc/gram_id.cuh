@@ -276,10 +276,11 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
         if (a0 + 32 * u < k) col[a0 + 32 * u] = v[u];
     }
   }
+  // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
   ArgMax loc{-1.0, 0x7fffffff};
   for (int j = tid; j < k; j += NT) {
     const double dj = Gm[(int64_t)j * k + j];
-    const double nj = sqrt(fmax(dj, 0.0));
+    const double nj = fmax(dj, 0.0);
     d[j] = dj;
     vn1[j] = vn2[j] = nj;
     col_at[j] = j;
@@ -291,31 +292,38 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     mbar_init(mbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  ArgMax best = cta_argmax(loc, sred);
+  ArgMax best = cta_argmax1(loc, sred);
   if (C > 1) cluster_barrier();   // G read, mbarriers initialised cluster-wide
   else __syncthreads();
   GID_MARK(0)
   const uint32_t rb_addr = smem_addr(rowbuf), bar_addr = smem_addr(mbar);
+  // remote row-buffer / mbarrier addresses of the (at most two) destinations this thread pushes to
+  uint32_t rb_dst[2] = {0u, 0u}, bar_dst[2] = {0u, 0u};
+  if (C > 1)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int dst = (tid & 7) + 8 * u;
+      if (dst < C) {
+        rb_dst[u] = mapa_u32(rb_addr, (unsigned)dst);
+        bar_dst[u] = mapa_u32(bar_addr, (unsigned)dst);
+      }
+    }
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
   const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
   const int mn = min(m, k);
-  double cut = 0.0;
+  double cut = 0.0, cut2 = 0.0;
   int r = 0, i = 0, np = 0;
   for (; i < mn; ++i) {
-    if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
+    if (i > 0 && best.v < cut2) break;
     const int q = i & 1;
     if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1));
-    if (tid == 0 && best.i != i) {
-      const int pp = best.i, tcol = col_at[pp];
-      col_at[pp] = col_at[i];
-      col_at[i] = tcol;
-      vn1[pp] = vn1[i];
-      vn2[pp] = vn2[i];
-    }
-    __syncthreads();
-    const int p = col_at[i];
+    // pivot column (position best.i); the position swap is applied after the row exchange
+    const int p = col_at[best.i];
     const double rd = sqrt(fmax(d[p], 0.0));
-    if (i == 0) cut = cutrel * rd;
+    if (i == 0) {
+      cut = cutrel * rd;
+      cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
+    }
     if (rd > cut) ++r;
     const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
     double* row = Pn + (int64_t)np * k;   // this step's row of R
@@ -335,9 +343,9 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       if (act) {
         v *= inv;
         if (C > 1) {
-          for (int dst = part; dst < C; dst += 8)
-            st_async_f64(mapa_u32(rb_addr + (uint32_t)(q * k + b) * 8u, (unsigned)dst), v,
-                         mapa_u32(bar_addr + 8u * q, (unsigned)dst));
+          const uint32_t off = (uint32_t)(q * k + b) * 8u;
+          if (part < C) st_async_f64(rb_dst[0] + off, v, bar_dst[0] + 8u * q);
+          if (part + 8 < C) st_async_f64(rb_dst[1] + off, v, bar_dst[1] + 8u * q);
         } else if (part == 0) {
           row[b] = v;
         }
@@ -356,7 +364,17 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
         else if (piv[a]) row[a] = 0.0;
     }
     __syncthreads();
-    if (tid == 0) piv[p] = 1;
+    if (tid == 0) {
+      piv[p] = 1;
+      if (best.i != i) {   // dlaqp2 swap of positions i and best.i
+        const int pp = best.i;
+        col_at[pp] = col_at[i];
+        col_at[i] = p;
+        vn1[pp] = vn1[i];
+        vn2[pp] = vn2[i];
+      }
+    }
+    __syncthreads();
     GID_MARK(4)
     for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
       const int b = lb * C + c;
@@ -370,23 +388,22 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       const double rv = row[col];
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;
-      double v1 = vn1[j];
-      if (v1 != 0.0) {
+      double w1 = vn1[j];
+      if (w1 != 0.0) {
         // dlaqp2: temp = max(0, 1 - (|R(i,j)|/vn1)^2); recompute when temp (vn1/vn2)^2 <= tol3z,
-        // else vn1 *= sqrt(temp) -- in division-free form: w = vn1^2 - R(i,j)^2
-        const double w = fmax(__fma_rn(-rv, rv, v1 * v1), 0.0);
-        const double v2 = vn2[j];
-        if (w <= tol3z * v2 * v2) {
-          v1 = i < m - 1 ? sqrt(fmax(dn, 0.0)) : 0.0;
-          vn2[j] = v1;
+        // else vn1 *= sqrt(temp) -- here on squared norms: w = vn1^2 - R(i,j)^2
+        const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
+        if (w <= tol3z * vn2[j]) {
+          w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
+          vn2[j] = w1;
         } else {
-          v1 = sqrt(w);
+          w1 = w;
         }
-        vn1[j] = v1;
+        vn1[j] = w1;
       }
-      loc = better(loc, ArgMax{v1, j});
+      loc = better(loc, ArgMax{w1, j});
     }
-    best = cta_argmax(loc, sred);
+    best = cta_argmax1(loc, sred);
     GID_MARK(6)
     if (++np == nb) {   // rank-nb update of the owned, unpivoted columns (all rows)
       // one warp per pair of owned columns, two rows per lane: each panel value loaded from shared
@@ -493,16 +510,36 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
           }
         }
         __syncthreads();
+        // all (up to 4) right-hand sides of the warp advance together: one staged R value feeds
+        // nj FMAs, 4 rows per lane in flight
         for (int ii = ib - 1; ii >= 0 && nj > 0; --ii) {
           const int ia = i0 + ii;
           const double* Rc = Rs + ii * r;
-          const double dg = Rc[ia];
-          for (int n = 0; n < nj; ++n) {
-            double* x = xs + n * r;
-            const double xi = x[ia] / dg;
-            __syncwarp();
-            if (lane == 0) x[ia] = xi;
-            warp_axpy<4>(x, Rc, xi, 0, ia, lane);
+          const double dinv = 1.0 / Rc[ia];
+          double xi[4];
+#pragma unroll
+          for (int n = 0; n < 4; ++n) xi[n] = n < nj ? xs[n * r + ia] * dinv : 0.0;
+          __syncwarp();
+          if (lane == 0)
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+              if (n < nj) xs[n * r + ia] = xi[n];
+          for (int a0 = lane; a0 < ia; a0 += 128) {
+            double rc[4], xv[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int a = a0 + 32 * u;
+              rc[u] = a < ia ? Rc[a] : 0.0;
+#pragma unroll
+              for (int n = 0; n < 4; ++n) xv[n][u] = (a < ia && n < nj) ? xs[n * r + a] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int a = a0 + 32 * u;
+#pragma unroll
+              for (int n = 0; n < 4; ++n)
+                if (a < ia && n < nj) xs[n * r + a] = __fma_rn(-rc[u], xi[n], xv[n][u]);
+            }
           }
           __syncwarp();
         }

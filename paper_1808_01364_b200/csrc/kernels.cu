@@ -275,6 +275,38 @@ __device__ ArgMax cta_argmax(ArgMax x, double* sred) {
   return r;
 }
 
+// CTA argmax without the trailing barrier: warp shuffles, one __syncthreads, then every warp
+// reduces the 8 warp winners with 3 shuffle levels. The caller guarantees a __syncthreads
+// between two calls sharing `sred`.
+__device__ ArgMax cta_argmax1(ArgMax x, double* sred) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = better(x, y);
+  }
+  int* sidx = reinterpret_cast<int*>(sred + 16);
+  if (lane == 0) {
+    sred[w] = x.v;
+    sidx[w] = x.i;
+  }
+  __syncthreads();
+  ArgMax r{-1.0, 0x7fffffff};
+  if (lane < NT / 32) r = ArgMax{sred[lane], sidx[lane]};
+#pragma unroll
+  for (int o = NT / 64; o > 0; o >>= 1) {
+    ArgMax y;
+    y.v = __shfl_xor_sync(0xffffffffu, r.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, r.i, o);
+    r = better(r, y);
+  }
+  r.v = __shfl_sync(0xffffffffu, r.v, 0);
+  r.i = __shfl_sync(0xffffffffu, r.i, 0);
+  return r;
+}
+
 // Exclusive CTA scan of 0/1 flags; returns this thread's offset, *total = count.
 __device__ int cta_scan_flag(int f, int* sint, int* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -647,24 +679,25 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     }
   }
   __syncthreads();
+  // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
   ArgMax loc{-1.0, 0x7fffffff};
   for (int j = tid; j < k; j += NT) {
     const double dj = S[j * k + j];
-    const double nj = sqrt(fmax(dj, 0.0));
+    const double nj = fmax(dj, 0.0);
     d[j] = dj;
     vn1[j] = vn2[j] = nj;
     col_at[j] = j;
     piv[j] = 0;
     loc = better(loc, ArgMax{nj, j});
   }
-  ArgMax best = cta_argmax(loc, sred);
+  ArgMax best = cta_argmax1(loc, sred);
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
   const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
   const int mn = min(m, k);
-  double cut = 0.0;
+  double cut = 0.0, cut2 = 0.0;
   int r = 0, i = 0;
   for (; i < mn; ++i) {
-    if (i > 0 && best.v < cut * (1.0 - 1e-4)) break;
+    if (i > 0 && best.v < cut2) break;
     if (tid == 0 && best.i != i) {
       const int pp = best.i, tcol = col_at[pp];
       col_at[pp] = col_at[i];
@@ -675,7 +708,10 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     __syncthreads();
     const int p = col_at[i];
     const double rd = sqrt(fmax(d[p], 0.0));
-    if (i == 0) cut = cutrel * rd;
+    if (i == 0) {
+      cut = cutrel * rd;
+      cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
+    }
     if (rd > cut) ++r;
     const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
     double* row = Rsm + i * k;
@@ -695,21 +731,20 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
       const double rv = row[col];
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;
-      double v1 = vn1[j];
-      if (v1 != 0.0) {
-        const double w = fmax(__fma_rn(-rv, rv, v1 * v1), 0.0);
-        const double v2 = vn2[j];
-        if (w <= tol3z * v2 * v2) {
-          v1 = i < m - 1 ? sqrt(fmax(dn, 0.0)) : 0.0;
-          vn2[j] = v1;
+      double w1 = vn1[j];
+      if (w1 != 0.0) {
+        const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
+        if (w <= tol3z * vn2[j]) {
+          w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
+          vn2[j] = w1;
         } else {
-          v1 = sqrt(w);
+          w1 = w;
         }
-        vn1[j] = v1;
+        vn1[j] = w1;
       }
-      loc = better(loc, ArgMax{v1, j});
+      loc = better(loc, ArgMax{w1, j});
     }
-    best = cta_argmax(loc, sred);
+    best = cta_argmax1(loc, sred);
   }
   const int kt = k - r;
   for (int j = tid; j < k; j += NT) piv[col_at[j]] = j >= r ? 1 : 0;
