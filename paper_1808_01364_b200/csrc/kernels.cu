@@ -2766,6 +2766,8 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 constexpr int NTK = 32, NTLD = NTK + 4, NT_STAGES = 3;
 constexpr int NT_STAGE = 2 * BT * NTLD;
 constexpr size_t NT_SMEM = (size_t)NT_STAGES * NT_STAGE * sizeof(double);
+constexpr int NT_CLD = BT + 1;   // C tile of the trailing update (MODE 0)
+constexpr size_t NT_SMEM0 = (size_t)(2 * NT_STAGE + BT * NT_CLD) * sizeof(double);
 
 template <int MODE>
 __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
@@ -2808,25 +2810,40 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
     }
     cp_async_commit();
   };
+  // MODE 0 (trailing update C -= A B^T): the C tile is fetched into shared memory by cp.async
+  // ahead of the K loop (2 stages, so two CTAs still fit per SM); its read-modify-write latency
+  // no longer sits behind the last DMMA
+  constexpr int STG = MODE == 0 ? 2 : NT_STAGES;
+  double* sC = smem + STG * NT_STAGE;
+  if (MODE == 0) {
+#pragma unroll
+    for (int q = 0; q < (BT * BT) / NT; ++q) {
+      const int e = tid + q * NT, r = e / BT, j = e % BT;
+      const bool ok = r < Mv && j < Nv;
+      cp_async8(sC + r * NT_CLD + j, P + (ok ? (int64_t)(ar0 + r) * n + br0 + j : 0), ok);
+    }
+    cp_async_commit();
+  }
   double acc[2][4][2];
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const int nch = (kend - kbeg + NTK - 1) / NTK;
-  load(0, kbeg);
-  if (nch > 1) load(1, kbeg + NTK);
+#pragma unroll
+  for (int st = 0; st < STG - 1; ++st)
+    if (st < nch) load(st, kbeg + st * NTK);
   for (int ch = 0; ch < nch; ++ch) {
-    if (ch + 2 < nch) {
-      load((ch + 2) % NT_STAGES, kbeg + (ch + 2) * NTK);
-      cp_async_wait<2>();
-    } else if (ch + 1 < nch) {
+    if (ch + STG - 1 < nch) {
+      load((ch + STG - 1) % STG, kbeg + (ch + STG - 1) * NTK);
+      cp_async_wait<STG - 1>();
+    } else if (STG == 3 && ch + 1 < nch) {
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* sA = smem + (ch % NT_STAGES) * NT_STAGE;
+    const double* sA = smem + (ch % STG) * NT_STAGE;
     const double* sB = sA + BT * NTLD;
 #pragma unroll
     for (int ks = 0; ks < NTK; ks += 4) {
@@ -2851,8 +2868,7 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
         const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
         if (i < Mv && j < Nv) {
           if (MODE == 0) {
-            double* p = P + (int64_t)(ar0 + i) * n + br0 + j;
-            *p -= acc[x][y][z];
+            P[(int64_t)(ar0 + i) * n + br0 + j] = sC[i * NT_CLD + j] - acc[x][y][z];
           } else {
             const int b = a.b[c];
             double* U = a.U[c];
@@ -3048,12 +3064,12 @@ void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s) {
   if (!a.nwork) return;
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_big_nt<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
+    cudaFuncSetAttribute(k_big_nt<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM0);
     cudaFuncSetAttribute(k_big_nt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
     init = true;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM, s>>>(a);
+  if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM0, s>>>(a);
   else k_big_nt<1><<<a.nwork, NT, NT_SMEM, s>>>(a);
 }
 void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s) {
