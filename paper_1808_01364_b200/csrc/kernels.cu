@@ -2049,12 +2049,28 @@ __global__ void k_big_build(LevelDev lv, CellArgs ca, const int* big_cells, int 
   const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
   const int64_t stride = (int64_t)chunks * blockDim.x;
   for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)n * n; e += stride) P[e] = A[e];
+  // A_BI rows: the block (I, h) is |I| x w row-major; its transpose lands in panel rows
+  // n + c0 .. n + c0 + w. 32 x 32 tiles through shared memory (coalesced reads and writes).
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
   for (int64_t j = ca.nbr_off[t]; j < ca.nbr_off[t + 1]; ++j) {
     const int w = ca.nbr_w[j], c0 = ca.nbr_col[j];
     const double* S = lv.pool + lv.boff[ca.nbr_blk[j]];
-    for (int64_t e = (int64_t)ch * blockDim.x + threadIdx.x; e < (int64_t)n * w; e += stride) {
-      const int i = (int)(e / w), r = (int)(e % w);
-      P[(int64_t)(n + c0 + r) * n + i] = S[e];
+    const int ti = (n + 31) / 32, tr = (w + 31) / 32;
+    for (int tt = ch; tt < ti * tr; tt += chunks) {
+      const int i0 = 32 * (tt / tr), r0 = 32 * (tt % tr);
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + ty + 8 * u, r = r0 + tx;
+        if (i < n && r < w) tile[ty + 8 * u][tx] = S[(int64_t)i * w + r];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + ty + 8 * u, i = i0 + tx;
+        if (i < n && r < w) P[(int64_t)(n + c0 + r) * n + i] = tile[tx][ty + 8 * u];
+      }
     }
   }
   // identity rows below [A_II; A_BI]: the partial Cholesky turns them into L^-T (apply by GEMM)
@@ -2160,84 +2176,102 @@ __global__ void __launch_bounds__(NT) k_rgemm(const GemmDesc* desc, const int* w
   }
 }
 
-__global__ void __launch_bounds__(NT) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile,
-                                               int nwork) {
+// Batched GEMM, C[64-row tile, :] = beta*C + alpha*op(A)[rows, :] B: the N columns in 64-wide
+// chunks (one 64 x 64 output tile at a time), K streamed in 16-wide chunks through a 3-stage
+// cp.async pipeline, each warp a 16 x 32 DMMA tile (2 x 4 m8n8k4 fragments).
+constexpr int BG_BK = 16, BG_ALD = BG_BK + 4, BG_BLD = 64 + 4, BG_STAGES = 3;
+constexpr int BG_STAGE = 64 * BG_ALD + BG_BK * BG_BLD;
+constexpr size_t BG_SMEM = (size_t)BG_STAGES * BG_STAGE * sizeof(double);
+__global__ void __launch_bounds__(NT, 2) k_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile,
+                                                  int nwork) {
   extern __shared__ double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-  const GemmDesc d = desc[w_desc[w]];
-  const int i0 = SG_BM * w_tile[w];
-  const int M = min(SG_BM, d.M - i0);
-  if (M <= 0) continue;
-  for (int j0 = 0; j0 < d.N; j0 += SG_BN) {
-    const int N = min(SG_BN, d.N - j0);
-    auto load_stage = [&](int st, int k0) {
-      double* sA = smem + st * SG_STAGE;
-      double* sB = sA + SG_BM * SG_ALD;
-      // A tile: 64 rows x 32 k
-      for (int e = tid; e < SG_BM * SG_BK; e += NT) {
-        int r, kk;
-        if (d.transA) {   // op(A)(i,k) = A[k*lda + i]: coalesce along i
-          kk = e / SG_BM;
-          r = e % SG_BM;
-        } else {          // A[i*lda + k]: coalesce along k
-          r = e / SG_BK;
-          kk = e % SG_BK;
+    const GemmDesc d = desc[w_desc[w]];
+    const int i0 = 64 * w_tile[w];
+    const int M = min(64, d.M - i0);
+    if (M <= 0) continue;
+    for (int j0 = 0; j0 < d.N; j0 += 64) {
+      const int N = min(64, d.N - j0);
+      auto load = [&](int st, int k0) {
+        double* sA = smem + st * BG_STAGE;
+        double* sB = sA + 64 * BG_ALD;
+#pragma unroll
+        for (int q = 0; q < (64 * BG_BK) / NT; ++q) {
+          const int e = tid + q * NT;
+          int r, kk;
+          if (d.transA) {   // op(A)(i,k) = A[k*lda + i]: coalesce along i
+            kk = e / 64;
+            r = e % 64;
+          } else {          // A[i*lda + k]
+            r = e / BG_BK;
+            kk = e % BG_BK;
+          }
+          const int gi = i0 + r, gk = k0 + kk;
+          const bool ok = r < M && gk < d.K;
+          const double* src = d.transA ? d.A + (ok ? (int64_t)gk * d.lda + gi : 0)
+                                       : d.A + (ok ? (int64_t)gi * d.lda + gk : 0);
+          cp_async8(sA + r * BG_ALD + kk, src, ok);
         }
-        const int gi = i0 + r, gk = k0 + kk;
-        const bool ok = gi < d.M && gk < d.K;
-        const double* src = d.transA ? d.A + (int64_t)(ok ? gk : 0) * d.lda + (ok ? gi : 0)
-                                     : d.A + (int64_t)(ok ? gi : 0) * d.lda + (ok ? gk : 0);
-        cp_async8(sA + r * SG_ALD + kk, src, ok);
-      }
-      // B tile: 32 k x 32 cols
-      for (int e = tid; e < SG_BK * SG_BN; e += NT) {
-        const int kk = e / SG_BN, c = e % SG_BN;
-        const int gk = k0 + kk;
-        const bool ok = gk < d.K && c < N;
-        const double* src = d.B + (int64_t)(ok ? gk : 0) * d.ldb + j0 + (ok ? c : 0);
-        cp_async8(sB + kk * SG_BLD + c, src, ok);
-      }
-      cp_async_commit();
-    };
-    double acc[4][2];
 #pragma unroll
-    for (int y = 0; y < 4; ++y) acc[y][0] = acc[y][1] = 0.0;
-    const int nk = (d.K + SG_BK - 1) / SG_BK;
-    if (nk > 0) load_stage(0, 0);
-    for (int kc = 0; kc < nk; ++kc) {
-      if (kc + 1 < nk) {
-        load_stage((kc + 1) & 1, (kc + 1) * SG_BK);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* sA = smem + (kc & 1) * SG_STAGE;
-      const double* sB = sA + SG_BM * SG_ALD;
-#pragma unroll
-      for (int ks = 0; ks < SG_BK; ks += 4) {
-        const double af = sA[(warp * 8 + g) * SG_ALD + ks + t4];
-#pragma unroll
-        for (int y = 0; y < 4; ++y) {
-          const double bf = sB[(ks + t4) * SG_BLD + y * 8 + g];
-          dmma(acc[y][0], acc[y][1], af, bf);
+        for (int q = 0; q < (BG_BK * 64) / NT; ++q) {
+          const int e = tid + q * NT, kk = e / 64, c = e % 64;
+          const int gk = k0 + kk;
+          const bool ok = gk < d.K && c < N;
+          cp_async8(sB + kk * BG_BLD + c, d.B + (ok ? (int64_t)gk * d.ldb + j0 + c : 0), ok);
         }
+        cp_async_commit();
+      };
+      double acc[2][4][2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+      const int nk = (d.K + BG_BK - 1) / BG_BK;
+      __syncthreads();   // previous tile's readers of the stage buffers are done
+      if (nk > 0) load(0, 0);
+      if (nk > 1) load(1, BG_BK);
+      for (int kc = 0; kc < nk; ++kc) {
+        if (kc + 2 < nk) {
+          load((kc + 2) % BG_STAGES, (kc + 2) * BG_BK);
+          cp_async_wait<2>();
+        } else if (kc + 1 < nk) {
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* sA = smem + (kc % BG_STAGES) * BG_STAGE;
+        const double* sB = sA + 64 * BG_ALD;
+#pragma unroll
+        for (int ks = 0; ks < BG_BK; ks += 4) {
+          double af[2], bf[4];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) af[x] = sA[(wm * 16 + x * 8 + g) * BG_ALD + ks + t];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) bf[y] = sB[(ks + t) * BG_BLD + wn * 32 + y * 8 + g];
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+        }
+        __syncthreads();
       }
-      __syncthreads();
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int z = 0; z < 2; ++z) {
+            const int r = wm * 16 + x * 8 + g, c = wn * 32 + y * 8 + 2 * t + z;
+            if (r < M && c < N) {
+              double* p = d.C + (int64_t)(i0 + r) * d.ldc + j0 + c;
+              *p = (d.beta == 0.0 ? 0.0 : d.beta * *p) + d.alpha * acc[x][y][z];
+            }
+          }
     }
-#pragma unroll
-    for (int y = 0; y < 4; ++y)
-#pragma unroll
-      for (int z = 0; z < 2; ++z) {
-        const int r = warp * 8 + g, c = y * 8 + 2 * t4 + z;
-        if (r < M && c < N) {
-          double* p = d.C + (int64_t)(i0 + r) * d.ldc + j0 + c;
-          *p = (d.beta == 0.0 ? 0.0 : d.beta * *p) + d.alpha * acc[y][z];
-        }
-      }
-  }  }
+  }
 }
 
 // gather / scatter of DOF rows for a list of index segments: Y[seg_dst + e] <-> x[idx[seg_src + e]]
@@ -3087,8 +3121,8 @@ void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, in
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
   if (!nwork) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const int grid = std::min(nwork, 148 * 32);
-  k_bgemm<<<grid, NT, 2 * SG_STAGE * sizeof(double), s>>>(desc, w_desc, w_tile, nwork);
+  const int grid = std::min(nwork, 148 * 16);
+  k_bgemm<<<grid, NT, BG_SMEM, s>>>(desc, w_desc, w_tile, nwork);
 }
 void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                  const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s) {
@@ -3312,7 +3346,7 @@ void configure_kernels() {
   cudaFuncSetAttribute(k_apply_skel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_big_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
   cudaFuncSetAttribute(k_big_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BIG_SMEM);
-  cudaFuncSetAttribute(k_bgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * SG_STAGE * sizeof(double)));
+  cudaFuncSetAttribute(k_bgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BG_SMEM);
 }
 
 }  // namespace phif
