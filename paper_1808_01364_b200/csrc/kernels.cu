@@ -1920,23 +1920,27 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
     D[i * BLD + j] = (i < kb && j <= i) ? P[(int64_t)(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
     Li[i * BLD + j] = 0.0;
   }
+  __shared__ double dinv[BT];
   if (tid == 0) sflag = -1;
   __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
   for (int j = 0; j < kb; ++j) {
     const double d = D[j * BLD + j];
     if (!(d > 0.0)) {
       if (tid == 0) sflag = j;
       break;
     }
-    const double ljj = sqrt(d);
+    const double ljj = sqrt(d), rj = 1.0 / ljj;
+    // column j scaled (each thread scales the entries it needs itself: no barrier in between)
+    for (int i = j + 1 + warp; i < kb; i += NT / 32) {
+      const double lij = D[i * BLD + j] * rj;
+      for (int k = j + 1 + lane; k <= i; k += 32) D[i * BLD + k] -= lij * (D[k * BLD + j] * rj);
+    }
     __syncthreads();
-    if (tid == 0) D[j * BLD + j] = ljj;
-    for (int i = j + 1 + tid; i < kb; i += NT) D[i * BLD + j] /= ljj;
-    __syncthreads();
-    const int m = kb - j - 1;
-    for (int e = tid; e < m * m; e += NT) {
-      const int i = j + 1 + e / m, k = j + 1 + e % m;
-      if (k <= i) D[i * BLD + k] -= D[i * BLD + j] * D[k * BLD + j];
+    for (int i = j + 1 + tid; i < kb; i += NT) D[i * BLD + j] *= rj;
+    if (tid == 0) {
+      D[j * BLD + j] = ljj;
+      dinv[j] = rj;
     }
     __syncthreads();
   }
@@ -1945,12 +1949,20 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
     if (tid == 0) report_bad(st, a.op[c], k0 + sflag);
     return;
   }
-  // inverse of the lower factor: column `col` of Li solves D x = e_col (thread per column)
-  for (int col = tid; col < BT; col += NT) {
-    for (int i = col; i < BT; ++i) {
-      double v = (i == col) ? 1.0 : 0.0;
-      for (int l = col; l < i; ++l) v -= D[i * BLD + l] * Li[l * BLD + col];
-      Li[i * BLD + col] = v / D[i * BLD + i];
+  for (int i = kb + tid; i < BT; i += NT) dinv[i] = 1.0;   // identity padding
+  __syncthreads();
+  // inverse of the lower factor, column col = tid / 4 by forward substitution; the 4 threads
+  // of a column split every dot product (2 shuffles), so all 64 columns advance together
+  {
+    const int col = tid >> 2, part = tid & 3;
+    for (int i = 0; i < BT; ++i) {
+      double v = 0.0;
+      if (i > col)
+        for (int l = col + part; l < i; l += 4) v = __fma_rn(D[i * BLD + l], Li[l * BLD + col], v);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (part == 0 && i >= col) Li[i * BLD + col] = ((i == col ? 1.0 : 0.0) - v) * dinv[i];
+      __syncwarp();
     }
   }
   __syncthreads();
