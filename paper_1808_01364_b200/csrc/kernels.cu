@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(NT) k_prec_factor(LevelDev lv, PrecArgs pa, De
   for (int64_t e = tid; e < (int64_t)k * k; e += NT) A[e] = (e / k == e % k) ? 1.0 : 0.0;
 }
 
+constexpr int PREC_SCALE_T = 64 * 64;   // doubles of the scaling intermediate (after SMEM_DOUBLES)
 __global__ void __launch_bounds__(NT) k_prec_scale(LevelDev lv, PrecArgs pa) {
   extern __shared__ double smem[];
   const int blk = pa.scale_list ? pa.scale_blk[pa.scale_list[blockIdx.x]] : pa.scale_blk[blockIdx.x];
@@ -147,6 +148,15 @@ __global__ void __launch_bounds__(NT) k_prec_scale(LevelDev lv, PrecArgs pa) {
   double* B = lv.pool + lv.boff[blk];
   const double* Lg = pa.rec + pa.L_off_of_group[g];
   const double* Lh = pa.rec + pa.L_off_of_group[h];
+  if (kg * kh <= PREC_SCALE_T) {
+    // two DMMA GEMMs with the explicit inverses stored after each factor ([L ; L^-T] record):
+    // T = (L_g^-T)^T B in shared memory, then B = T L_h^-T
+    double* T = smem + SMEM_DOUBLES;
+    double* gsm = smem + GEMM_OFF;
+    cta_gemm<true, false>(kg, kh, kg, 1.0, Lg + (int64_t)kg * kg, kg, B, kh, 0.0, T, kh, false, gsm);
+    cta_gemm<false, false>(kg, kh, kh, 1.0, T, kh, Lh + (int64_t)kh * kh, kh, 0.0, B, kh, false, gsm);
+    return;
+  }
   cta_trsm_left(Lg, kg, kg, B, kh, kh, false, smem);
   cta_trsm_right_lt(Lh, kh, kh, B, kg, kh, smem);
 }
@@ -2976,7 +2986,7 @@ void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* li
 void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
   if (a.nscale == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_prec_scale<<<a.nscale, NT, SMEM_BYTES, s>>>(lv, a);
+  k_prec_scale<<<a.nscale, NT, SMEM_BYTES + PREC_SCALE_T * sizeof(double), s>>>(lv, a);
 }
 static long long static_smem(const void* fn) {
   cudaFuncAttributes fa{};
@@ -3350,7 +3360,8 @@ void configure_kernels() {
   const int bytes = (int)SMEM_BYTES;
   cudaFuncSetAttribute(k_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_prec_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_prec_scale, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_prec_scale, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       bytes + (int)(PREC_SCALE_T * sizeof(double)));
   cudaFuncSetAttribute(k_skel_id, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_skel_update, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_apply_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
