@@ -956,7 +956,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           const int t = P.wave_order[q];
           const int k = G.size(P.skeleton[t]);
           if (is_large(t)) {
-            if (use_gid) gid_item.push_back(t);
+            if (use_gid && gid_fits(k)) gid_item.push_back(t);
             else large.push_back(t);
           } else {
             small_list.push_back(t);

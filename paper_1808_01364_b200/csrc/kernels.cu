@@ -3313,6 +3313,11 @@ int gid_cluster(int kmax, bool* sg) {
     throw std::runtime_error("gram ID: separator too large");
   return C;
 }
+// separators the Gram path can stage (back-substitution buffers in shared memory)
+bool gid_fits(int k) {
+  const int64_t sreg = gid_sreg(k, 16);
+  return 24 * (int64_t)k <= sreg + (int64_t)gid_panel(k) * k;
+}
 int64_t gid_gbuf_doubles(int k, int C, bool sg) {
   return (int64_t)k * k + (sg ? (int64_t)C * gid_pack0(k, C) : 0);
 }
