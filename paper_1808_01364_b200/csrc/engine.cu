@@ -1,4 +1,5 @@
 #include <future>
+#include <mutex>
 #include <numeric>
 // Host driver: per level plan -> device structures -> batched stage launches.
 //
@@ -151,9 +152,9 @@ std::unique_ptr<Matrix> matrix_create(const int64_t* rowptr, const int* col, con
   A->rowptr.alloc((N + 1) * sizeof(int64_t), s);
   A->col.alloc(A->nnz * sizeof(int), s);
   A->val.alloc(A->nnz * sizeof(double), s);
-  CK(cudaMemcpyAsync(A->rowptr.p, rowptr, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(A->col.p, col, A->nnz * sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(A->val.p, val, A->nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  upload_bytes(A->rowptr.p, rowptr, (N + 1) * sizeof(int64_t), s);
+  upload_bytes(A->col.p, col, A->nnz * sizeof(int), s);
+  upload_bytes(A->val.p, val, A->nnz * sizeof(double), s);
   return A;
 }
 
@@ -384,6 +385,59 @@ static long long* gid_prof_buffer() {
   return buf;
 }
 
+// Pinned staging ring for host -> device uploads: two halves, each guarded by the event of the
+// last copy issued from it; the host fills the staging area with a parallel memcpy, so the DMA
+// engine copies at pinned-memory speed instead of the driver's pageable staging.
+void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  static constexpr size_t HALF = (size_t)96 << 20, MIN_STAGED = (size_t)1 << 20;
+  static char* ring = nullptr;
+  static bool ok = true;
+  static cudaEvent_t ev[2];
+  static int cur = 0;
+  static size_t pos = 0;
+  static std::mutex mu;
+  if (bytes < MIN_STAGED || !ok) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ring) {
+    if (cudaHostAlloc((void**)&ring, 2 * HALF, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+      return;
+    }
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    CK(cudaEventRecord(ev[0], s));
+    CK(cudaEventRecord(ev[1], s));
+  }
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  while (bytes > 0) {
+    if (pos == HALF) {   // switch halves; wait until the other half's last copy has drained
+      cur ^= 1;
+      pos = 0;
+      CK(cudaEventSynchronize(ev[cur]));
+    }
+    const size_t len = std::min(bytes, HALF - pos);
+    char* stage = ring + (size_t)cur * HALF + pos;
+    const int64_t nchunk = (int64_t)std::max<size_t>(1, len >> 20);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nchunk; ++c) {
+      const size_t a = len * c / nchunk, e = len * (c + 1) / nchunk;
+      memcpy(stage + a, sp + a, e - a);
+    }
+    CK(cudaMemcpyAsync(dp, stage, len, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ev[cur], s));
+    pos += len;
+    sp += len;
+    dp += len;
+    bytes -= len;
+  }
+}
+
 static void keep_pool_memory() {
   // freed blocks stay in the stream-ordered pool instead of going back to the driver at every sync
   static bool done = false;
@@ -413,11 +467,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   auto t_start = clk::now();
   double plan_ms = 0.0;
   F->alive.alloc(sp.N * sizeof(int), s);
-  {
-    std::vector<int> ones(sp.N, 1);
-    CK(cudaMemcpyAsync(F->alive.p, ones.data(), sp.N * sizeof(int), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  }
+  launch_fill_int(F->alive.as<int>(), 1, sp.N, s);
+  DBG("alive initialised");
   F->status.alloc(sizeof(DevStatus), s);
   cudaEvent_t ev[16];
   if (timing)
@@ -433,6 +484,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     LevelRT* prev = lev > 0 ? F->levels[lev - 1].get() : nullptr;
     if (lev == 0) {
       L.plan.grp = classify_all(sp);
+      DBG("level 0: classified");
       pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.data(), A.h_col.data());
     } else {
       L.plan.grp = classify_next(sp, prev->plan.grp, alive_mem);
@@ -448,7 +500,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     const int p = (int)P.interior.size();
     std::vector<int64_t> P_off(p), U_off(p), I_off(p), B_off(p), cwork(p);
     std::vector<int> nbr_w(P.cell_nbr.size());
-    std::vector<int> Bdofs;
+    auto Bdofs_p = std::make_shared<std::vector<int>>();   // shared with the reduction-list task
+    std::vector<int>& Bdofs = *Bdofs_p;
     int64_t rec = 0, uacc = 0, bacc = 0, wacc = 0;
     for (int t = 0; t < p; ++t) {
       const int nn = P.cell_n[t], bb = P.cell_b[t];
@@ -462,50 +515,41 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       bacc += bb;
       cwork[t] = wacc;
       wacc += 2 * nn + bb;
+    }
+    // boundary DOFs of every cell (cell order, neighbour order, members ascending), in parallel
+    Bdofs.resize(bacc);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int t = 0; t < p; ++t) {
+      int64_t o = B_off[t];
       for (int64_t j = P.cell_nbr_off[t]; j < P.cell_nbr_off[t + 1]; ++j) {
         const int h = P.cell_nbr[j];
         nbr_w[j] = G.size(h);
-        for (int64_t q = G.off[h]; q < G.off[h + 1]; ++q) Bdofs.push_back(G.mem[q]);
+        for (int64_t q = G.off[h]; q < G.off[h + 1]; ++q) Bdofs[o++] = G.mem[q];
       }
     }
     L.cell_work_unit = wacc;
     L.wbuf_unit = bacc;
     DBG("level %d: host: cell descriptors", lev);
-    for (int t = 0; t < p; ++t) {
-      const double nn = P.cell_n[t], bb = P.cell_b[t];
-      L.fl[1] += nn * nn * nn / 3.0 + nn * nn * bb + nn * bb * bb;
-      L.by[1] += 8.0 * (nn * nn + nn * bb + (nn + bb) * nn + bb * bb);
-    }
-    for (size_t q = 0; q < P.tgt_blk.size(); ++q) {
-      const int blk = P.tgt_blk[q];
-      L.by[1] += 8.0 * 2.0 * G.size(P.pat.bg[blk]) * G.size(P.pat.bh[blk]);
-    }
-    for (size_t b = 0; b < P.pat.bg.size(); ++b) L.by[0] += 8.0 * 2.0 * G.size(P.pat.bg[b]) * G.size(P.pat.bh[b]);
-    // boundary reduction lists (x_B -= X^T y in fixed cell order): only the apply needs them,
-    // so they are built on a host thread while the GPU factors and uploaded after the level loop
-    L.bd_task = std::async(std::launch::async, [Bd = Bdofs]() {
-      // rows of every boundary DOF in cell order: counting sort over the DOF range
-      BdLists out;
-      if (Bd.empty()) {
-        out.off.push_back(0);
-        return out;
+    {
+      double f1 = 0.0, b1 = 0.0, b0 = 0.0;
+#pragma omp parallel for reduction(+ : f1, b1)
+      for (int t = 0; t < p; ++t) {
+        const double nn = P.cell_n[t], bb = P.cell_b[t];
+        f1 += nn * nn * nn / 3.0 + nn * nn * bb + nn * bb * bb;
+        b1 += 8.0 * (nn * nn + nn * bb + (nn + bb) * nn + bb * bb);
       }
-      const auto mm = std::minmax_element(Bd.begin(), Bd.end());
-      const int lo = *mm.first, span = *mm.second - lo + 1;
-      std::vector<int64_t> start(span + 1, 0);
-      for (int d : Bd) start[d - lo + 1]++;
-      for (int d = 0; d < span; ++d) {
-        if (start[d + 1]) {
-          out.dof.push_back(d + lo);
-          out.off.push_back(start[d]);
-        }
-        start[d + 1] += start[d];
+      const int64_t ntgt = (int64_t)P.tgt_blk.size(), nblkp = (int64_t)P.pat.bg.size();
+#pragma omp parallel for reduction(+ : b1)
+      for (int64_t q = 0; q < ntgt; ++q) {
+        const int blk = P.tgt_blk[q];
+        b1 += 8.0 * 2.0 * G.size(P.pat.bg[blk]) * G.size(P.pat.bh[blk]);
       }
-      out.off.push_back((int64_t)Bd.size());
-      out.rows.resize(Bd.size());
-      for (size_t i = 0; i < Bd.size(); ++i) out.rows[start[Bd[i] - lo]++] = (int)i;
-      return out;
-    });
+#pragma omp parallel for reduction(+ : b0)
+      for (int64_t b = 0; b < nblkp; ++b) b0 += 8.0 * 2.0 * G.size(P.pat.bg[b]) * G.size(P.pat.bh[b]);
+      L.fl[1] += f1;
+      L.by[1] += b1;
+      L.by[0] += b0;
+    }
     DBG("level %d: host: boundary reduction lists", lev);
     // precondition records
     const int r = P.root ? 0 : (int)P.precond.size();
@@ -531,16 +575,23 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.h_pwork = pwork;
     L.h_pn = pn;
     if (do_prec) {
+      double f2 = 0.0, b2 = 0.0;
+#pragma omp parallel for reduction(+ : f2, b2)
       for (int t = 0; t < r; ++t) {
         const double k = pn[t];
-        L.fl[2] += k * k * k / 3.0;
-        L.by[2] += 8.0 * 3.0 * k * k;
+        f2 += k * k * k / 3.0;
+        b2 += 8.0 * 3.0 * k * k;
       }
-      for (int b : P.scale_blk) {
+      const int64_t nsc = (int64_t)P.scale_blk.size();
+#pragma omp parallel for reduction(+ : f2, b2)
+      for (int64_t q = 0; q < nsc; ++q) {
+        const int b = P.scale_blk[q];
         const double kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
-        L.fl[2] += kg * kg * kh + kg * kh * kh;
-        L.by[2] += 8.0 * 2.0 * kg * kh;
+        f2 += kg * kg * kh + kg * kh * kh;
+        b2 += 8.0 * 2.0 * kg * kh;
       }
+      L.fl[2] += f2;
+      L.by[2] += b2;
     }
     DBG("level %d: host: precondition records", lev);
     // skeleton records / workspaces (upper bounds; ranks known after the ID)
@@ -570,6 +621,33 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.rec_doubles = rec;
     plan_ms += ms_since(tp);
     L.t_ms[5] += ms_since(tp);
+    // boundary reduction lists (x_B -= X^T y in fixed cell order): only the apply needs them,
+    // so they are built on a host thread (started after the OpenMP planning loops) while the GPU
+    // factors, and uploaded after the level loop
+    L.bd_task = std::async(std::launch::async, [Bdp = std::shared_ptr<const std::vector<int>>(Bdofs_p)]() {
+      const std::vector<int>& Bd = *Bdp;
+      // rows of every boundary DOF in cell order: counting sort over the DOF range
+      BdLists out;
+      if (Bd.empty()) {
+        out.off.push_back(0);
+        return out;
+      }
+      const auto mm = std::minmax_element(Bd.begin(), Bd.end());
+      const int lo = *mm.first, span = *mm.second - lo + 1;
+      std::vector<int64_t> start(span + 1, 0);
+      for (int d : Bd) start[d - lo + 1]++;
+      for (int d = 0; d < span; ++d) {
+        if (start[d + 1]) {
+          out.dof.push_back(d + lo);
+          out.off.push_back(start[d]);
+        }
+        start[d + 1] += start[d];
+      }
+      out.off.push_back((int64_t)Bd.size());
+      out.rows.resize(Bd.size());
+      for (size_t i = 0; i < Bd.size(); ++i) out.rows[start[Bd[i] - lo]++] = (int)i;
+      return out;
+    });
     // ---------------- device structures ----------------
     DBG("level %d: rec=%lld", lev, (long long)rec);
     upload_structure(L, s);

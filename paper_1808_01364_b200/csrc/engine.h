@@ -43,10 +43,12 @@ struct DBuf {
   T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// host -> device copy on stream s; large copies go through a pinned staging ring (engine.cu)
+void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s);
 template <class T>
 void upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
   b.alloc(std::max<size_t>(1, v.size()) * sizeof(T), s);
-  if (!v.empty()) cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+  if (!v.empty()) upload_bytes(b.p, v.data(), v.size() * sizeof(T), s);
 }
 
 struct Matrix {

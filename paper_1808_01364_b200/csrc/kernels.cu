@@ -2943,6 +2943,14 @@ void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_ingest<<<nblk(N, 256), 256, 0, s>>>(lv, gid, pos, rowptr, col, val, N);
 }
+__global__ void k_fill_int(int* p, int v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+void launch_fill_int(int* p, int v, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_fill_int<<<std::min<int64_t>(nblk(n, 256), 148 * 8), 256, 0, s>>>(p, v, n);
+}
 void launch_group_pos(const LevelDev& lv, int* gid, int* pos, cudaStream_t s) {
   if (lv.G == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);

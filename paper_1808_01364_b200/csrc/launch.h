@@ -56,6 +56,7 @@ void configure_kernels();
 long long launch_count();   // kernel launches issued so far (all streams)
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
                    const double* val, int64_t N, cudaStream_t s);
+void launch_fill_int(int* p, int v, int64_t n, cudaStream_t s);
 void launch_group_pos(const LevelDev& lv, int* gid, int* pos, cudaStream_t s);
 void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st, cudaStream_t s);
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s);
