@@ -13,7 +13,7 @@ echo "launch list rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gid_cpqr --launch-skip 75 --launch-count 1 \
   -o gpurun_out/gidcpqr_l3_$R python tools/one_factor.py c5 1e-2 - 1 > gpurun_out/ncu_gid.log 2>&1
 echo "gid full rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_big_nt<1>" --launch-skip 2 --launch-count 1 \
+timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:k_big_nt<.int.1>" --launch-skip 2 --launch-count 1 \
   -o gpurun_out/bignt1_l3_$R python tools/one_factor.py c5 1e-2 - 1 > gpurun_out/ncu_bignt.log 2>&1
 echo "big_nt full rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gid_gram --launch-skip 75 --launch-count 1 \
