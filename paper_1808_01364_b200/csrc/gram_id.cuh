@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(NT) k_gid_copy(LevelDev lv, SkelArgs sk, GramA
   const int nch = nc.nch;
   const int lo = (int)((int64_t)nch * part / ga.P), hi = (int)((int64_t)nch * (part + 1) / ga.P);
   double* W = sk.work + sk.work_off[s];
-  gather_chunks<true>(lv, sk, nc, s, lo, hi, W, ga.item_ld[item], s_base, sbuf, 512);
+  gather_chunks<true, 16>(lv, sk, nc, s, lo, hi, W, ga.item_ld[item], s_base, sbuf, 512);
   if (part == 0 && threadIdx.x == 0) sk.rows[s] = s_tot;
 }
 

@@ -506,17 +506,15 @@ __device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArg
   const int r = r0 + lane;
   bool nz = false;
   if (g < h) {   // block (g,h) is |g| x |h|: column r of it, lanes along rows (coalesced)
-    if (r < kh) {
-      const double* p = B + r;
-      int c = 0;
-      for (; c + 8 <= k; c += 8) {
-        double v[8];
+    const double* p = B + (r < kh ? r : 0);
+    // stop as soon as every lane has seen a nonzero (the usual case: after the first batch)
+    for (int c = 0; c < k; c += 8) {
+      double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(c + u) * kh];
+      for (int u = 0; u < 8; ++u) v[u] = (r < kh && c + u < k) ? p[(int64_t)(c + u) * kh] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) nz |= v[u] != 0.0;
-      }
-      for (; c < k; ++c) nz |= p[(int64_t)c * kh] != 0.0;
+      for (int u = 0; u < 8; ++u) nz |= v[u] != 0.0;
+      if (c + 8 < k && __all_sync(0xffffffffu, nz || r >= kh)) break;
     }
   } else {       // block (h,g) is |h| x |g|: rows r0..r0+31 are contiguous, lanes along columns
     const int nr = min(32, kh - r0);
@@ -525,12 +523,19 @@ __device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArg
       bool any[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) any[u] = false;
-      for (int c = lane; c < k; c += 32) {
+      for (int c0 = 0; c0 < k; c0 += 32) {
+        const int c = c0 + lane;
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = rb + u < nr ? p[(int64_t)(rb + u) * k + c] : 0.0;
+        for (int u = 0; u < 8; ++u) v[u] = (rb + u < nr && c < k) ? p[(int64_t)(rb + u) * k + c] : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) any[u] |= v[u] != 0.0;
+        if (c0 + 32 < k) {   // more columns left: stop once every row of the group has a nonzero
+          bool all = true;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) all = all && (__any_sync(0xffffffffu, any[u]) || rb + u >= nr);
+          if (all) break;
+        }
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -540,6 +545,7 @@ __device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArg
   const bool alive = r < kh && __ldcg(sk.alive + lv.mem[nc.moff[i] + r]);
   return __ballot_sync(0xffffffffu, nz && alive);
 }
+template <int U>
 __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& nc, int g, int k, int i, int r0,
                                            unsigned mask, double* W, int64_t ldw, int row0) {
   const int lane = threadIdx.x & 31;
@@ -547,7 +553,6 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& n
   const double* B = lv.pool + nc.boff[i];
   // loads are batched ahead of the stores (W and B may alias as far as the compiler knows, so an
   // unbatched copy loop would pay one full memory latency per element)
-  constexpr int U = 8;
   if (g < h) {
     if ((mask >> lane) & 1u) {
       const int row = row0 + __popc(mask & ((1u << lane) - 1u));
@@ -581,7 +586,7 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& n
 }
 // Chunks [ch_lo, ch_hi) of separator s: with COPY, kept rows go to W rows base, base+1, ...
 // Returns the number of kept rows (all threads). smem: 2*cap ints.
-template <bool COPY>
+template <bool COPY, int U = 8>
 __device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, const NbrCache& nc, int s, int ch_lo, int ch_hi,
                              double* W, int64_t ldw, int base, int* sbuf, int cap) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
@@ -617,7 +622,7 @@ __device__ int gather_chunks(const LevelDev& lv, const SkelArgs& sk, const NbrCa
     if (COPY)
       for (int j = warp; j < nb; j += nw) {
         const int i = nc.locate(b0 + j);
-        chunk_copy(lv, nc, g, k, i, 32 * (b0 + j - nc.ch0[i]), smask[j], W, ldw, base + total + spre[j]);
+        chunk_copy<U>(lv, nc, g, k, i, 32 * (b0 + j - nc.ch0[i]), smask[j], W, ldw, base + total + spre[j]);
       }
     total += s_tot;
     __syncthreads();
