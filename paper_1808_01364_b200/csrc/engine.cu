@@ -1025,7 +1025,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       const bool use_gid = ka.gram != 0;
       std::vector<int> gid_item, gid_wi, gid_wj, gid_wit;
       std::vector<int64_t> gid_ld, gid_goff, gid_item_off(P.nwaves + 1, 0), gid_w_off(P.nwaves + 1, 0);
-      std::vector<int> gid_C(P.nwaves, 1), gid_kmax(P.nwaves, 0), gid_P(P.nwaves, 1);
+      std::vector<int> gid_C(P.nwaves, 1), gid_kmax(P.nwaves, 0), gid_P(P.nwaves, 1), gid_S(P.nwaves, 1);
       std::vector<uint8_t> gid_sg(P.nwaves, 0);
       int64_t gid_gbuf = 1, gid_cnt = 1;
       for (int w = 0; w < P.nwaves; ++w) {
@@ -1055,20 +1055,32 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
             gid_P[w] = std::max(1, std::min(32, 2 * num_sms / ni));
             gid_cnt = std::max<int64_t>(gid_cnt, (int64_t)ni * gid_P[w]);
           }
+          // split-K of the Gram tiles so that a wave fills the GPU (partial blocks, fixed-order sum)
+          int64_t ntiles = 0, rmin = INT64_MAX;
+          for (int64_t q = gid_item_off[w]; q < gid_item_off[w + 1]; ++q) {
+            const int t = gid_item[q], nt = (G.size(P.skeleton[t]) + 63) / 64;
+            ntiles += (int64_t)nt * (nt + 1) / 2;
+            rmin = std::min<int64_t>(rmin, rows_bound[t]);
+          }
+          static const int smax = env_int("PHIF_GID_SPLITK", 4);
+          int S = 1;
+          while (S < smax && ntiles * S < 2 * num_sms && rmin / (2 * S) >= 256) S *= 2;
+          gid_S[w] = S;
           int64_t go = 0;
           for (int64_t q = gid_item_off[w]; q < gid_item_off[w + 1]; ++q) {
             const int t = gid_item[q];
             const int k = G.size(P.skeleton[t]);
             gid_ld.push_back(std::max<int64_t>(rows_bound[t], 1));
             gid_goff.push_back(go);
-            go += gid_gbuf_doubles(k, gid_C[w], gid_sg[w]);
+            go += gid_gbuf_doubles(k, gid_C[w], gid_sg[w], S);
             const int nt = (k + 63) / 64;
-            for (int it = 0; it < nt; ++it)
-              for (int jt = 0; jt <= it; ++jt) {
-                gid_wit.push_back((int)(q - gid_item_off[w]));
-                gid_wi.push_back(it);
-                gid_wj.push_back(jt);
-              }
+            for (int ks = 0; ks < S; ++ks)
+              for (int it = 0; it < nt; ++it)
+                for (int jt = 0; jt <= it; ++jt) {
+                  gid_wit.push_back((int)(q - gid_item_off[w]));
+                  gid_wi.push_back(it);
+                  gid_wj.push_back(jt | (ks << 16));
+                }
           }
           gid_gbuf = std::max(gid_gbuf, go);
         }
@@ -1208,6 +1220,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ga.w_j = d_gwj.as<int>() + gid_w_off[w];
           ga.nwork = (int)(gid_w_off[w + 1] - gid_w_off[w]);
           ga.C = gid_C[w];
+          ga.S = gid_S[w];
           ga.prof = gid_prof_buffer();
           launch_gid(dv, ka, ga, gid_kmax[w], gid_sg[w] != 0, s);
         }

@@ -114,13 +114,16 @@ __global__ void __launch_bounds__(NT) k_gid_copy(LevelDev lv, SkelArgs sk, GramA
 // column a of A (contiguous over r) is the "row" a of the NT product. G is column-major (ld k).
 __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, GramArgs ga) {
   extern __shared__ double smem[];
-  const int item = ga.w_item[blockIdx.x], it = ga.w_i[blockIdx.x], jt = ga.w_j[blockIdx.x];
+  const int item = ga.w_item[blockIdx.x], it = ga.w_i[blockIdx.x], jt = ga.w_j[blockIdx.x] & 0xffff;
+  const int ks = ga.w_j[blockIdx.x] >> 16;   // split-K part: rows [kbeg, kend) into partial block ks
   const int s = ga.item_sep[item];
   const int k = lv.gsize[sk.groups[s]];
-  const int m = sk.rows[s];
+  const int mrows = sk.rows[s];
+  const int kchunk = ((mrows + ga.S - 1) / ga.S + NTK - 1) / NTK * NTK;
+  const int kbeg = min(mrows, ks * kchunk), m = min(mrows, kbeg + kchunk);
   const int64_t ld = ga.item_ld[item];
   const double* W = sk.work + sk.work_off[s];
-  double* Gm = ga.gbuf + ga.g_off[item];
+  double* Gm = ga.gbuf + ga.g_off[item] + (int64_t)ks * k * k;
   const int ar0 = BT * it, br0 = BT * jt;
   const int Mv = min(BT, k - ar0), Nv = min(BT, k - br0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -145,12 +148,12 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
   for (int x = 0; x < 2; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-  const int nch = (m + NTK - 1) / NTK;
-  if (nch > 0) load(0, 0);
-  if (nch > 1) load(1, NTK);
+  const int nch = (m - kbeg + NTK - 1) / NTK;
+  if (nch > 0) load(0, kbeg);
+  if (nch > 1) load(1, kbeg + NTK);
   for (int ch = 0; ch < nch; ++ch) {
     if (ch + 2 < nch) {
-      load((ch + 2) % NT_STAGES, (ch + 2) * NTK);
+      load((ch + 2) % NT_STAGES, kbeg + (ch + 2) * NTK);
       cp_async_wait<2>();
     } else if (ch + 1 < nch) {
       cp_async_wait<1>();
@@ -249,7 +252,8 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   }
   const int nown0 = (k + C - 1) / C;
   double* Gm = ga.gbuf + ga.g_off[item];                              // G (full), then R (R(i, b) at Gm[b*k + i])
-  double* Sg = Gm + (int64_t)k * k + (int64_t)c * nown0 * k;         // spill area (when allocated)
+  const int64_t kk2 = (int64_t)k * k;
+  double* Sg = Gm + ga.S * kk2 + (int64_t)c * nown0 * k;            // spill area (when allocated)
   double* Pn = smem + sreg;                 // nb x k panel rows of R
   double* d = Pn + (int64_t)nb * k;         // Schur diagonal (replicated)
   double* vn1 = d + k;
@@ -271,6 +275,9 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       double v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = a0 + 32 * u < k ? src[a0 + 32 * u] : 0.0;
+      for (int q = 1; q < ga.S; ++q)   // split-K partial blocks, fixed order
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] += a0 + 32 * u < k ? src[q * kk2 + a0 + 32 * u] : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (a0 + 32 * u < k) col[a0 + 32 * u] = v[u];
@@ -279,7 +286,8 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
   ArgMax loc{-1.0, 0x7fffffff};
   for (int j = tid; j < k; j += NT) {
-    const double dj = Gm[(int64_t)j * k + j];
+    double dj = Gm[(int64_t)j * k + j];
+    for (int q = 1; q < ga.S; ++q) dj += Gm[q * kk2 + (int64_t)j * k + j];
     const double nj = fmax(dj, 0.0);
     d[j] = dj;
     vn1[j] = vn2[j] = nj;

@@ -3331,8 +3331,8 @@ bool gid_fits(int k) {
   const int64_t sreg = gid_sreg(k, 16);
   return 24 * (int64_t)k <= sreg + (int64_t)gid_panel(k) * k;
 }
-int64_t gid_gbuf_doubles(int k, int C, bool sg) {
-  return (int64_t)k * k + (sg ? (int64_t)C * gid_pack0(k, C) : 0);
+int64_t gid_gbuf_doubles(int k, int C, bool sg, int S) {
+  return (int64_t)S * k * k + (sg ? (int64_t)C * gid_pack0(k, C) : 0);
 }
 void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int kmax, bool sg, cudaStream_t s) {
   if (g.nitem == 0) return;

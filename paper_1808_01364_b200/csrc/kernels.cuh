@@ -138,6 +138,7 @@ struct GramArgs {
   const int* w_j;
   int nwork;
   int C;                   // CPQR cluster size
+  int S;                   // split-K factor of the Gram tiles (partial G blocks summed by the CPQR)
   int nb;                  // deferred-update panel width (<= 16)
   long long* prof;         // optional phase clocks of CTA 0 (PHIF_GID_PROF)
 };
