@@ -305,12 +305,17 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   else __syncthreads();
   GID_MARK(0)
   const uint32_t rb_addr = smem_addr(rowbuf), bar_addr = smem_addr(mbar);
-  // remote row-buffer / mbarrier addresses of the (at most two) destinations this thread pushes to
-  uint32_t rb_dst[2] = {0u, 0u}, bar_dst[2] = {0u, 0u};
+  // threads per owned column in the row-entry step (power of two, nown <= NT / tpc when possible;
+  // tpc >= C / 4 so every thread pushes to at most 4 destinations)
+  int tpc = 8;
+  while (tpc > 1 && nown > NT / tpc) tpc >>= 1;
+  while (tpc * 4 < C) tpc <<= 1;
+  // remote row-buffer / mbarrier addresses of the destinations this thread pushes to
+  uint32_t rb_dst[4] = {0u, 0u, 0u, 0u}, bar_dst[4] = {0u, 0u, 0u, 0u};
   if (C > 1)
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int dst = (tid & 7) + 8 * u;
+    for (int u = 0; u < 4; ++u) {
+      const int dst = (tid & (tpc - 1)) + tpc * u;
       if (dst < C) {
         rb_dst[u] = mapa_u32(rb_addr, (unsigned)dst);
         bar_dst[u] = mapa_u32(bar_addr, (unsigned)dst);
@@ -335,25 +340,25 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     if (rd > cut) ++r;
     const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
     double* row = Pn + (int64_t)np * k;   // this step's row of R
-    // entries of row i in the owned columns, 8 threads per column (panel terms split 8 ways)
-    for (int cb0 = 0; cb0 < nown; cb0 += NT / 8) {
-      const int lb = cb0 + (tid >> 3), part = tid & 7;
+    // entries of row i in the owned columns, tpc threads per column (panel terms split tpc ways;
+    // one round over the owned columns whenever nown <= 256)
+    for (int cb0 = 0; cb0 < nown; cb0 += NT / tpc) {
+      const int lb = cb0 + tid / tpc, part = tid & (tpc - 1);
       const int b = lb * C + c;
       const bool act = lb < nown && b != p && !piv[b];
       double v = 0.0;
       if (act) {
-        for (int l = part; l < np; l += 8) v = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v);
+        for (int l = part; l < np; l += tpc) v = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v);
         if (part == 0) v += colf(lb)[p];
       }
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      for (int o = 1; o < tpc; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (act) {
         v *= inv;
         if (C > 1) {
           const uint32_t off = (uint32_t)(q * k + b) * 8u;
-          if (part < C) st_async_f64(rb_dst[0] + off, v, bar_dst[0] + 8u * q);
-          if (part + 8 < C) st_async_f64(rb_dst[1] + off, v, bar_dst[1] + 8u * q);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (part + u * tpc < C) st_async_f64(rb_dst[u] + off, v, bar_dst[u] + 8u * q);
         } else if (part == 0) {
           row[b] = v;
         }
