@@ -24,9 +24,9 @@
 // it owns and pushes them to every CTA through distributed shared memory).
 
 struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
-  // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][64] doubles, then 3k ints
+  // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][rdv, invv: 2k][64] doubles, then 3k ints
   __host__ __device__ static int64_t doubles(int64_t sreg, int k, int nb) {
-    return sreg + (int64_t)(nb + 5) * k + 64;
+    return sreg + (int64_t)(nb + 7) * k + 64;
   }
   __host__ __device__ static size_t bytes(int64_t sreg, int k, int nb) {
     return (size_t)doubles(sreg, k, nb) * sizeof(double) + 3 * (size_t)k * sizeof(int);
@@ -259,7 +259,9 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   double* vn1 = d + k;
   double* vn2 = vn1 + k;
   double* rowbuf = vn2 + k;                 // 2 x k receive buffers (step parity)
-  double* sred = rowbuf + 2 * (int64_t)k;   // 64 (sred[48..49]: the two mbarriers)
+  double* rdv = rowbuf + 2 * (int64_t)k;    // sqrt(Schur diagonal) and its reciprocal per column,
+  double* invv = rdv + k;                   // formed off the pivot chain in the downdate loop
+  double* sred = invv + k;                  // 64 (sred[48..49]: the two mbarriers)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sred + 48);
   int* col_at = reinterpret_cast<int*>(sred + 64);
   int* piv = col_at + k;
@@ -290,6 +292,8 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     for (int q = 1; q < ga.S; ++q) dj += Gm[q * kk2 + (int64_t)j * k + j];
     const double nj = fmax(dj, 0.0);
     d[j] = dj;
+    rdv[j] = sqrt(nj);
+    invv[j] = nj > 0.0 ? 1.0 / rdv[j] : 0.0;
     vn1[j] = vn2[j] = nj;
     col_at[j] = j;
     piv[j] = 0;
@@ -332,13 +336,13 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1));
     // pivot column (position best.i); the position swap is applied after the row exchange
     const int p = col_at[best.i];
-    const double rd = sqrt(fmax(d[p], 0.0));
+    const double rd = rdv[p];
     if (i == 0) {
       cut = cutrel * rd;
       cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
     }
     if (rd > cut) ++r;
-    const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
+    const double inv = invv[p];
     double* row = Pn + (int64_t)np * k;   // this step's row of R
     // entries of row i in the owned columns, tpc threads per column (panel terms split tpc ways;
     // one round over the owned columns whenever nown <= 256)
@@ -401,6 +405,11 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       const double rv = row[col];
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;
+      {
+        const double rdn = sqrt(fmax(dn, 0.0));
+        rdv[col] = rdn;
+        invv[col] = rdn > 0.0 ? 1.0 / rdn : 0.0;
+      }
       double w1 = vn1[j];
       if (w1 != 0.0) {
         // dlaqp2: temp = max(0, 1 - (|R(i,j)|/vn1)^2); recompute when temp (vn1/vn2)^2 <= tol3z,
