@@ -1922,71 +1922,112 @@ constexpr int BT = 64, BLD = 65;
 
 // one CTA per big cell still active at this step
 __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
-  extern __shared__ double smem[];
-  double* D = smem;                 // BT x BLD
-  double* Li = smem + BT * BLD;     // BT x BLD (inverse)
+  // Register-resident 64 x 64 Cholesky and triangular inverse: warp w owns rows w, w+8, ...,
+  // lane l owns columns l and l+32 (16 entries per thread). Each step publishes one column
+  // (factor) or one row (inverse) in shared memory, double-buffered: one barrier per step.
+  __shared__ double colbuf[2][BT];
+  __shared__ double dinv[BT];
   __shared__ int sflag;
   const int c = a.w_cell[blockIdx.x];
   const int n = a.n[c], k0 = a.k0, kb = min(BT, n - k0);
   double* P = a.P[c];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < BT * BT; e += NT) {
-    const int i = e / BT, j = e % BT;
-    D[i * BLD + j] = (i < kb && j <= i) ? P[(int64_t)(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
-    Li[i * BLD + j] = 0.0;
-  }
-  __shared__ double dinv[BT];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double Dr[8][2];
+#pragma unroll
+  for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci) {
+      const int i = w + 8 * ri, cc = lane + 32 * ci;
+      Dr[ri][ci] = (i < kb && cc <= i) ? P[(int64_t)(k0 + i) * n + k0 + cc] : (i == cc ? 1.0 : 0.0);
+    }
   if (tid == 0) sflag = -1;
-  __syncthreads();
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int j = 0; j < kb; ++j) {
-    const double d = D[j * BLD + j];
-    if (!(d > 0.0)) {
+  for (int j = 0; j < BT; ++j) {
+    const int par = j & 1, cj = j >> 5, lj = j & 31;
+    if (lane == lj)
+#pragma unroll
+      for (int ri = 0; ri < 8; ++ri) {
+        const int i = w + 8 * ri;
+        if (i >= j) colbuf[par][i] = cj ? Dr[ri][1] : Dr[ri][0];   // (selects keep Dr in registers)
+      }
+    __syncthreads();
+    const double djj = colbuf[par][j];
+    if (!(djj > 0.0)) {
       if (tid == 0) sflag = j;
       break;
     }
-    const double ljj = sqrt(d), rj = 1.0 / ljj;
-    // column j scaled (each thread scales the entries it needs itself: no barrier in between)
-    for (int i = j + 1 + warp; i < kb; i += NT / 32) {
-      const double lij = D[i * BLD + j] * rj;
-      for (int k = j + 1 + lane; k <= i; k += 32) D[i * BLD + k] -= lij * (D[k * BLD + j] * rj);
+    const double ljj = sqrt(djj), rj = 1.0 / ljj;
+    double lc[2];
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci) {
+      const int cc = lane + 32 * ci;
+      lc[ci] = cc > j ? colbuf[par][cc] * rj : 0.0;
     }
-    __syncthreads();
-    for (int i = j + 1 + tid; i < kb; i += NT) D[i * BLD + j] *= rj;
-    if (tid == 0) {
-      D[j * BLD + j] = ljj;
-      dinv[j] = rj;
+#pragma unroll
+    for (int ri = 0; ri < 8; ++ri) {
+      const int i = w + 8 * ri;
+      if (i > j) {
+        const double li = colbuf[par][i] * rj;
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+          const int cc = lane + 32 * ci;
+          if (cc > j && cc <= i) Dr[ri][ci] = __fma_rn(-li, lc[ci], Dr[ri][ci]);
+        }
+        if (lane == lj) {
+          if (cj) Dr[ri][1] = li;
+          else Dr[ri][0] = li;
+        }
+      } else if (i == j && lane == lj) {
+        if (cj) Dr[ri][1] = ljj;
+        else Dr[ri][0] = ljj;
+      }
     }
-    __syncthreads();
+    if (tid == 0) dinv[j] = rj;
   }
   __syncthreads();
   if (sflag >= 0) {
-    if (tid == 0) report_bad(st, a.op[c], k0 + sflag);
+    if (tid == 0 && sflag < kb) report_bad(st, a.op[c], k0 + sflag);
     return;
   }
-  for (int i = kb + tid; i < BT; i += NT) dinv[i] = 1.0;   // identity padding
-  __syncthreads();
-  // inverse of the lower factor, column col = tid / 4 by forward substitution; the 4 threads
-  // of a column split every dot product (2 shuffles), so all 64 columns advance together
-  {
-    const int col = tid >> 2, part = tid & 3;
-    for (int i = 0; i < BT; ++i) {
-      double v = 0.0;
-      if (i > col)
-        for (int l = col + part; l < i; l += 4) v = __fma_rn(D[i * BLD + l], Li[l * BLD + col], v);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      if (part == 0 && i >= col) Li[i * BLD + col] = ((i == col ? 1.0 : 0.0) - v) * dinv[i];
-      __syncwarp();
+  // X = L^-1, right-looking: row j of X is final after scaling by 1/L(j,j); rows i > j then
+  // subtract L(i,j) X(j,:) (L(i,j) from the owning lane of the row's warp by shuffle)
+  double Xr[8][2];
+#pragma unroll
+  for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci) Xr[ri][ci] = (w + 8 * ri == lane + 32 * ci) ? 1.0 : 0.0;
+  for (int j = 0; j < BT; ++j) {
+    const int par = j & 1, rj_i = j >> 3, wj = j & 7;
+    if (w == wj) {
+#pragma unroll
+      for (int ri = 0; ri < 8; ++ri)
+        if (ri == rj_i)
+#pragma unroll
+          for (int ci = 0; ci < 2; ++ci) {
+            Xr[ri][ci] *= dinv[j];
+            colbuf[par][lane + 32 * ci] = Xr[ri][ci];
+          }
+    }
+    __syncthreads();
+    const double x0 = colbuf[par][lane], x1 = colbuf[par][lane + 32];
+#pragma unroll
+    for (int ri = 0; ri < 8; ++ri) {
+      const int i = w + 8 * ri;
+      const double lij = __shfl_sync(0xffffffffu, (j >> 5) ? Dr[ri][1] : Dr[ri][0], j & 31);
+      if (i > j) {
+        Xr[ri][0] = __fma_rn(-lij, x0, Xr[ri][0]);
+        Xr[ri][1] = __fma_rn(-lij, x1, Xr[ri][1]);
+      }
     }
   }
-  __syncthreads();
   double* Lo = a.Linv + (int64_t)c * BT * BT;
-  for (int e = tid; e < BT * BT; e += NT) {
-    const int i = e / BT, j = e % BT;
-    Lo[e] = Li[i * BLD + j];
-    if (i < kb && j < kb) P[(int64_t)(k0 + i) * n + k0 + j] = (j <= i) ? D[i * BLD + j] : 0.0;
-  }
+#pragma unroll
+  for (int ri = 0; ri < 8; ++ri)
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci) {
+      const int i = w + 8 * ri, cc = lane + 32 * ci;
+      Lo[i * BT + cc] = Xr[ri][ci];
+      if (i < kb && cc < kb) P[(int64_t)(k0 + i) * n + k0 + cc] = (cc <= i) ? Dr[ri][ci] : 0.0;
+    }
   // (the strict upper part of the square block is zeroed once at the end: k_big_zero_upper)
 }
 
@@ -3115,7 +3156,7 @@ void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cel
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s) {
   if (diag.nwork) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    k_big_diag<<<diag.nwork, NT, BIG_SMEM, s>>>(diag, st);
+    k_big_diag<<<diag.nwork, NT, 0, s>>>(diag, st);
   }
   if (trsm.nwork) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
