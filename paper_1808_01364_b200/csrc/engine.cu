@@ -424,7 +424,9 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     const size_t len = std::min(bytes, HALF - pos);
     char* stage = ring + (size_t)cur * HALF + pos;
     const int64_t nchunk = (int64_t)std::max<size_t>(1, len >> 20);
-#pragma omp parallel for schedule(static)
+    // a few threads saturate the host memory bandwidth; the rest of the cores stay free for the
+    // planner's helper threads (a statically scheduled team waiting on a preempted thread stalls)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(std::min<int64_t>(nchunk, 6))
     for (int64_t c = 0; c < nchunk; ++c) {
       const size_t a = len * c / nchunk, e = len * (c + 1) / nchunk;
       memcpy(stage + a, sp + a, e - a);
