@@ -147,8 +147,20 @@ std::unique_ptr<Matrix> matrix_create(const int64_t* rowptr, const int* col, con
   auto A = std::make_unique<Matrix>();
   A->N = N;
   A->nnz = rowptr[N];
-  A->h_rowptr.assign(rowptr, rowptr + N + 1);
-  A->h_col.assign(col, col + A->nnz);
+  // host copies of the pattern for the planner (parallel chunked copies; a few threads saturate
+  // the host memory bandwidth)
+  A->h_rowptr.resize(N + 1);
+  A->h_col.resize(A->nnz);
+  auto pcopy = [](void* dst, const void* src, size_t bytes) {
+    const int64_t nchunk = (int64_t)std::max<size_t>(1, bytes >> 22);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(std::min<int64_t>(nchunk, 6))
+    for (int64_t c = 0; c < nchunk; ++c) {
+      const size_t a = bytes * c / nchunk, e = bytes * (c + 1) / nchunk;
+      memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, e - a);
+    }
+  };
+  pcopy(A->h_rowptr.data(), rowptr, (N + 1) * sizeof(int64_t));
+  pcopy(A->h_col.data(), col, A->nnz * sizeof(int));
   A->rowptr.alloc((N + 1) * sizeof(int64_t), s);
   A->col.alloc(A->nnz * sizeof(int), s);
   A->val.alloc(A->nnz * sizeof(double), s);
