@@ -922,8 +922,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           double* blk = L.pool.as<double>() + P.boff[b];
           double* T = tmp.as<double>() + to;
           to += (int64_t)kg * kh;
-          GemmDesc a{rec0 + Lg_off[gg] + (int64_t)kg * kg, blk, T, kg, kh, kg, kg, kh, kh, 1, 1.0, 0.0};
-          GemmDesc c{T, rec0 + Lg_off[hh] + (int64_t)kh * kh, blk, kg, kh, kh, kh, kh, kh, 0, 1.0, 0.0};
+          // L_g^-1 (op of the stored L_g^-T) is lower triangular, L_h^-T upper triangular
+          GemmDesc a{rec0 + Lg_off[gg] + (int64_t)kg * kg, blk, T, kg, kh, kg, kg, kh, kh, 1, 1.0, 0.0, 1};
+          GemmDesc c{T, rec0 + Lg_off[hh] + (int64_t)kh * kh, blk, kg, kh, kh, kh, kh, kh, 0, 1.0, 0.0, 2};
           for (int t = 0; t < (kg + 63) / 64; ++t) {
             w1d.push_back((int)d1.size());
             w1t.push_back(t);

@@ -2262,6 +2262,9 @@ __global__ void __launch_bounds__(NT, 2) k_bgemm(const GemmDesc* desc, const int
     if (M <= 0) continue;
     for (int j0 = 0; j0 < d.N; j0 += 64) {
       const int N = min(64, d.N - j0);
+      // triangular operands: the K range ends at the tile's last row (op(A) lower) or column
+      // (B upper); the terms beyond are structural zeros
+      const int Kt = d.tri == 1 ? min(d.K, i0 + 64) : (d.tri == 2 ? min(d.K, j0 + 64) : d.K);
       auto load = [&](int st, int k0) {
         double* sA = smem + st * BG_STAGE;
         double* sB = sA + 64 * BG_ALD;
@@ -2277,7 +2280,7 @@ __global__ void __launch_bounds__(NT, 2) k_bgemm(const GemmDesc* desc, const int
             kk = e % BG_BK;
           }
           const int gi = i0 + r, gk = k0 + kk;
-          const bool ok = r < M && gk < d.K;
+          const bool ok = r < M && gk < Kt;
           const double* src = d.transA ? d.A + (ok ? (int64_t)gk * d.lda + gi : 0)
                                        : d.A + (ok ? (int64_t)gi * d.lda + gk : 0);
           cp_async8(sA + r * BG_ALD + kk, src, ok);
@@ -2286,7 +2289,7 @@ __global__ void __launch_bounds__(NT, 2) k_bgemm(const GemmDesc* desc, const int
         for (int q = 0; q < (BG_BK * 64) / NT; ++q) {
           const int e = tid + q * NT, kk = e / 64, c = e % 64;
           const int gk = k0 + kk;
-          const bool ok = gk < d.K && c < N;
+          const bool ok = gk < Kt && c < N;
           cp_async8(sB + kk * BG_BLD + c, d.B + (ok ? (int64_t)gk * d.ldb + j0 + c : 0), ok);
         }
         cp_async_commit();
@@ -2296,7 +2299,7 @@ __global__ void __launch_bounds__(NT, 2) k_bgemm(const GemmDesc* desc, const int
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-      const int nk = (d.K + BG_BK - 1) / BG_BK;
+      const int nk = (Kt + BG_BK - 1) / BG_BK;
       __syncthreads();   // previous tile's readers of the stage buffers are done
       if (nk > 0) load(0, 0);
       if (nk > 1) load(1, BG_BK);
