@@ -384,13 +384,15 @@ static long long* gid_prof_buffer() {
   if (on < 0) {
     on = getenv("PHIF_GID_PROF") ? 1 : 0;
     if (on) {
-      cudaMallocManaged(&buf, 16 * sizeof(long long));
-      for (int i = 0; i < 16; ++i) buf[i] = 0;
+      cudaMallocManaged(&buf, 32 * sizeof(long long));
+      for (int i = 0; i < 32; ++i) buf[i] = 0;
       atexit([] {
         cudaDeviceSynchronize();
         fprintf(stderr, "[phif] gid CPQR CTA0 (Mcycles): load %.2f argmax %.2f pieces %.2f barrier %.2f rowread %.2f update %.2f downdate %.2f post %.2f backsub %.2f | steps %lld\n",
                 buf[0] / 1e6, buf[1] / 1e6, buf[2] / 1e6, buf[3] / 1e6, buf[4] / 1e6, buf[5] / 1e6, buf[6] / 1e6,
                 buf[7] / 1e6, buf[8] / 1e6, buf[9]);
+        fprintf(stderr, "[phif] small-separator ID CTA0 (Mcycles): dependency wait %.2f gather-count %.2f copy %.2f gram+cpqr+T %.2f | separators %lld\n",
+                buf[19] / 1e6, buf[16] / 1e6, buf[17] / 1e6, buf[18] / 1e6, buf[23]);
       });
     }
   }
@@ -980,6 +982,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       static const bool gid_on = !getenv("PHIF_GID") || atoi(getenv("PHIF_GID")) != 0;
       static const double gid_eps = getenv("PHIF_GID_EPS") ? atof(getenv("PHIF_GID_EPS")) : 1e-5;
       ka.gram = (gid_on && F->eps >= gid_eps) ? 1 : 0;
+      ka.prof = gid_prof_buffer();
     }
     ka.work = wk.as<double>();
     ka.work_off = L.s_work_off.as<int64_t>();

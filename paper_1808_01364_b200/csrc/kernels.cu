@@ -447,7 +447,7 @@ __device__ int cta_cpqr(double* W, int m, int k, int64_t ldw, int* perm, double*
 constexpr int NBMAX = 256;
 struct NbrCache {
   int n, nch, rows;
-  int h[NBMAX], kh[NBMAX], ch0[NBMAX + 1];
+  int h[NBMAX], kh[NBMAX], ch0[NBMAX + 1], r0[NBMAX];   // r0: first row of neighbour i in A_{R,I}
   long long boff[NBMAX], moff[NBMAX];
   __device__ int locate(int ch) const {   // neighbour holding chunk ch: last i with ch0[i] <= ch
     int lo = 0, hi = n - 1;
@@ -485,7 +485,10 @@ __device__ void nbr_cache_load(const LevelDev& lv, const SkelArgs& sk, int s, Nb
           ir += tr;
         }
       }
-      if (i < n) nc.ch0[i] = run_c + ic - vc;
+      if (i < n) {
+        nc.ch0[i] = run_c + ic - vc;
+        nc.r0[i] = run_r + ir - vr;
+      }
       run_c += __shfl_sync(0xffffffffu, ic, 31);
       run_r += __shfl_sync(0xffffffffu, ir, 31);
     }
@@ -553,6 +556,32 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& n
   const double* B = lv.pool + nc.boff[i];
   // loads are batched ahead of the stores (W and B may alias as far as the compiler knows, so an
   // unbatched copy loop would pay one full memory latency per element)
+  if (row0 < 0) {   // fixed positions: row (-1 - row0) + r0 + lane, rejected rows written as zeros
+    const int rbase = -1 - row0 + r0;
+    if (g < h) {
+      const int r = r0 + lane;
+      if (r < kh) {
+        const bool keep = (mask >> lane) & 1u;
+        const double* p = B + r;
+        for (int c0 = 0; c0 < k; c0 += U) {
+          double v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = (keep && c0 + u < k) ? p[(int64_t)(c0 + u) * kh] : 0.0;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (c0 + u < k) W[(int64_t)(c0 + u) * ldw + rbase + lane] = v[u];
+        }
+      }
+    } else {
+      const int nr = min(32, kh - r0);
+      for (int rr = 0; rr < nr; ++rr) {
+        const bool keep = (mask >> rr) & 1u;
+        const double* p = B + (int64_t)(r0 + rr) * k;
+        for (int c = lane; c < k; c += 32) W[(int64_t)c * ldw + rbase + rr] = keep ? p[c] : 0.0;
+      }
+    }
+    return;
+  }
   if (g < h) {
     if ((mask >> lane) & 1u) {
       const int row = row0 + __popc(mask & ((1u << lane) - 1u));
@@ -647,9 +676,13 @@ __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s
 // complement updated in place, then T = R11^-1 R12 (4 threads per right-hand side). The
 // workspace after G reuses the gathered matrix's region (base = smem + SMEM_DOUBLES).
 // Returns false (nothing written) when the shapes do not fit; the caller then runs cta_cpqr.
+__device__ __forceinline__ bool skel_id_gram_fits(int k, int cap) {
+  return k <= 57 && k * k <= RED_OFF && (int64_t)k * k + 5 * k + 8 <= cap;
+}
+// W holds mrows rows (kept rows and zero rows), m of them kept
 __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int k, const double* W, int64_t ldw,
-                             int m, double* smem, int cap) {
-  if (k > 57 || k * k > RED_OFF || (int64_t)k * k + 5 * k + 8 > cap) return false;
+                             int mrows, int m, double* smem, int cap) {
+  if (!skel_id_gram_fits(k, cap)) return false;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const int g = sk.groups[s];
   const int64_t gof = lv.goff[g];
@@ -676,10 +709,10 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
       const double* Wb = W + (int64_t)min(b, k - 1) * ldw;
       const bool oka = a < k, okb = b < k;
       double c0 = 0.0, c1 = 0.0;
-      for (int r0 = 0; r0 < m; r0 += 4) {
+      for (int r0 = 0; r0 < mrows; r0 += 4) {
         const int r = r0 + t4;
-        const double av = (oka && r < m) ? Wa[r] : 0.0;
-        const double bv = (okb && r < m) ? Wb[r] : 0.0;
+        const double av = (oka && r < mrows) ? Wa[r] : 0.0;
+        const double bv = (okb && r < mrows) ? Wb[r] : 0.0;
         dmma(c0, c1, av, bv);
       }
       const int row = it * 8 + gq, col = jt * 8 + 2 * t4;
@@ -827,10 +860,50 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
   const int64_t gof = lv.goff[g];
   // count the kept rows first: A_{R,I} (ld = m) and its CPQR live in shared memory when they
   // fit, else in the global workspace
+  const bool pf = sk.prof != nullptr && blockIdx.x == 0 && tid == 0;
+  long long t0 = pf ? clock64() : 0;
+#define SID_MARK(slot)                                                                                  \
+  if (pf) {                                                                                             \
+    const long long t1 = clock64();                                                                     \
+    atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + (slot)), (unsigned long long)(t1 - t0)); \
+    t0 = t1;                                                                                            \
+  }
   __shared__ NbrCache nc;
   nbr_cache_load(lv, sk, s, nc);
   const int nch = nc.nch;
+  if (sk.gram && skel_id_gram_fits(k, smem_cap) && (int64_t)max(1, nc.rows) * k <= smem_cap) {
+    // Gram path: A^T A does not depend on the row order and zero rows add nothing, so one pass
+    // places every candidate row at its natural position (rejected rows as zeros): no count
+    // pass, no prefix scan; the kept-row count m only enters the rank cut floor
+    const int64_t ldw = max(1, nc.rows);
+    double* W = smem + SMEM_DOUBLES;
+    __shared__ int s_m;
+    if (tid == 0) s_m = 0;
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5, g0 = sk.groups[s];
+    int mine = 0;
+    for (int ch = warp; ch < nch; ch += NT / 32) {
+      const int i = nc.locate(ch), r0 = 32 * (ch - nc.ch0[i]);
+      const unsigned msk = chunk_mask(lv, sk, nc, g0, k, i, r0);
+      chunk_copy<8>(lv, nc, g0, k, i, r0, msk, W, ldw, -1 - nc.r0[i]);
+      mine += __popc(msk);
+    }
+    if (lane == 0 && mine) atomicAdd(&s_m, mine);
+    __syncthreads();
+    const int m = s_m;
+    if (tid == 0) sk.rows[s] = m;
+    SID_MARK(17)
+    if (m == 0) {
+      skel_all_redundant(lv, sk, s);
+      return;
+    }
+    skel_id_gram(lv, sk, s, k, W, ldw, (int)ldw, m, smem, smem_cap);
+    SID_MARK(18)
+    if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + 23), 1ull);
+    return;
+  }
   const int64_t ldw = max(1, gather_chunks<false>(lv, sk, nc, s, 0, nch, nullptr, 1, 0, sint, 512));
+  SID_MARK(16)
   const bool local = ldw * k + 4 * (int64_t)k + 4 <= smem_cap;
   double* W = local ? smem + SMEM_DOUBLES : sk.work + sk.work_off[s];
   double* vn1 = W + (int64_t)k * ldw;
@@ -841,6 +914,7 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
   int* flag = iw + 2 * k;
   const int m = gather_chunks<true>(lv, sk, nc, s, 0, nch, W, ldw, 0, sint, 512);
   if (tid == 0) sk.rows[s] = m;
+  SID_MARK(17)
   uint8_t* red = sk.red + gof;
   if (m == 0) {
     skel_all_redundant(lv, sk, s);
@@ -848,8 +922,13 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
   }
   if (sk.gram) {
     __syncthreads();   // gathered rows visible to every warp
-    if (skel_id_gram(lv, sk, s, k, W, ldw, m, smem, smem_cap)) return;
+    if (skel_id_gram(lv, sk, s, k, W, ldw, m, m, smem, smem_cap)) {
+      SID_MARK(18)
+      if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + 23), 1ull);
+      return;
+    }
   }
+#undef SID_MARK
   const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
   const int steps = cta_cpqr(W, m, k, ldw, perm, vn1, vn2, sred, cutrel);
   __shared__ int s_rank;
@@ -904,6 +983,7 @@ __global__ void __launch_bounds__(NT) k_skel_id_dyn(LevelDev lv, SkelArgs sk, in
     const int q = s_item;
     if (q >= ds.count) break;
     const int s = sk.order[q];
+    const long long tw0 = (sk.prof && blockIdx.x == 0 && threadIdx.x == 0) ? clock64() : 0;
     if (threadIdx.x == 0) {
       volatile int* d = ds.done + s;
       const int nd = ds.ndep[s];
@@ -911,6 +991,8 @@ __global__ void __launch_bounds__(NT) k_skel_id_dyn(LevelDev lv, SkelArgs sk, in
       __threadfence();
     }
     __syncthreads();
+    if (sk.prof && blockIdx.x == 0 && threadIdx.x == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + 19), (unsigned long long)(clock64() - tw0));
     skel_id_one(lv, sk, s, smem_cap);
     __syncthreads();
     if (threadIdx.x == 0) {

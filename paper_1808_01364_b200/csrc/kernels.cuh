@@ -80,6 +80,7 @@ struct SkelArgs {
   int* rows;                 // per skeleton: rows of A_{R,I} after filtering
   double eps;
   int gram;                  // 1: separators of <= 57 columns take the Gram-path ID (skel_id_gram)
+  long long* prof;           // optional phase clocks (PHIF_GID_PROF), slots 16..23
   double* work;              // per skeleton workspace
   const int64_t* work_off;
   int* iwork;
