@@ -1367,21 +1367,33 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     tp = clk::now();
     alive_mem.assign(G.mem.size(), 0);
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int g = 0; g < G.G; ++g)
       if (G.kind[g] != 0)
         for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) alive_mem[q] = red[q] ? 0 : 1;
-    // skeleton apply descriptors
+    // skeleton apply descriptors (offsets by prefix sums, members filled in parallel)
     std::vector<int> sr(nsk), skt(nsk), Sd, Rd;
     std::vector<int64_t> S_off(nsk), R_off(nsk);
-    int64_t rsum = 0;
+    int64_t rsum = 0, ktsum = 0;
     for (int t = 0; t < nsk; ++t) {
       const int g = P.skeleton[t];
       sr[t] = L.h_rank[t];
       skt[t] = G.size(g) - L.h_rank[t];
+      S_off[t] = rsum;
+      R_off[t] = ktsum;
       rsum += sr[t];
-      S_off[t] = (int64_t)Sd.size();
-      R_off[t] = (int64_t)Rd.size();
-      for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) (red[q] ? Rd : Sd).push_back(G.mem[q]);
+      ktsum += skt[t];
+    }
+    Sd.resize(rsum);
+    Rd.resize(ktsum);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int t = 0; t < nsk; ++t) {
+      const int g = P.skeleton[t];
+      int64_t a = S_off[t], b = R_off[t];
+      for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) {
+        if (red[q]) Rd[b++] = G.mem[q];
+        else Sd[a++] = G.mem[q];
+      }
     }
     for (int t = 0; t < nsk; ++t) {
       const double mm = h_rows[t], kk = sr[t] + skt[t], rr = sr[t], kt = skt[t];

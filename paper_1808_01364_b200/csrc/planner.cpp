@@ -347,15 +347,35 @@ std::vector<std::pair<int, int>> pattern_next(const LevelPlan& prev, const Group
         throw std::runtime_error("planner: an old group split across new groups");
       old2new[og] = G;
     }
-  std::vector<std::pair<int, int>> pairs;
-  pairs.reserve(prev.pat.bg.size());
-  for (size_t b = 0; b < prev.pat.bg.size(); ++b) {
-    const int og = prev.pat.bg[b], oh = prev.pat.bh[b];
-    if (prev.grp.kind[og] == 0 || prev.grp.kind[oh] == 0) continue;
-    const int G = old2new[og], H = old2new[oh];
-    if (G < 0 || H < 0) continue;
-    pairs.emplace_back(std::min(G, H), std::max(G, H));
+  // per-thread lists over block ranges, concatenated (build_level sorts and dedups per group)
+  const int64_t nb = (int64_t)prev.pat.bg.size();
+  int nth = 1;
+#ifdef _OPENMP
+  nth = omp_get_max_threads();
+#endif
+  std::vector<std::vector<std::pair<int, int>>> part(nth);
+#pragma omp parallel num_threads(nth)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    std::vector<std::pair<int, int>>& mine = part[tid];
+    const int64_t lo = nb * tid / nth, hi = nb * (tid + 1) / nth;
+    mine.reserve(hi - lo);
+    for (int64_t b = lo; b < hi; ++b) {
+      const int og = prev.pat.bg[b], oh = prev.pat.bh[b];
+      if (prev.grp.kind[og] == 0 || prev.grp.kind[oh] == 0) continue;
+      const int G = old2new[og], H = old2new[oh];
+      if (G < 0 || H < 0) continue;
+      mine.emplace_back(std::min(G, H), std::max(G, H));
+    }
   }
+  std::vector<std::pair<int, int>> pairs;
+  size_t tot = 0;
+  for (auto& v : part) tot += v.size();
+  pairs.reserve(tot);
+  for (auto& v : part) pairs.insert(pairs.end(), v.begin(), v.end());
   return pairs;
 }
 
