@@ -133,6 +133,17 @@ def test_multi_rhs_block_equals_single_solves():
         assert np.linalg.norm(x - X[:, c]) <= 1e-12 * np.linalg.norm(x)
 
 
+@pytest.mark.parametrize("nrhs", [33, 48])
+def test_wide_rhs_block_apply_matches_oracle(nrhs):
+    # more than 32 right-hand sides take the generic batched-GEMM replay (k_bgemm)
+    spec, A = baseline_problem("c4", 0, 32)[:2]
+    Fo = ophif.factorize(A, spec, 1e-3, "phif")
+    Fg = gfac.factorize(A, spec, 1e-3, "phif")
+    B = np.random.default_rng(11).standard_normal((A.n, nrhs))
+    yo, yg = ophif.apply_inverse(Fo, B), gfac.apply_inverse(Fg, B)
+    assert np.linalg.norm(yg - yo) <= APPLY_TOL * np.linalg.norm(yo)
+
+
 def test_apply_inverse_symmetry_and_ginv_on_gpu():
     spec, A = baseline_problem("c4", 0, 32)[:2]
     F = gfac.factorize(A, spec, 1e-3, "phif")
