@@ -214,7 +214,8 @@ struct BigPlan {
   // Blocks of KB columns; inside a block, 64-wide steps (diag factor + inverse, panel TRSM as a
   // GEMM with the inverse, update of the block's own remaining columns); then one KB-deep
   // update of the whole trailing matrix. Last, U = X^T X (lower tiles, mirrored).
-  static constexpr int T = 64, KB = 256;
+  static constexpr int T = 64;
+  const int KB = env_int("PHIF_BIG_KB", 256);   // multiple of T
   DBuf d_n, d_b, d_rows, d_P, d_U, d_op, d_linv, d_list;
   DBuf d_cell, d_i, d_j;
   struct Phase {
