@@ -2702,6 +2702,19 @@ __global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int
   const int n = a.n[t];
   const int* I = a.I + a.I_off[t];
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
+  if (k == 32 && ldn > 0) {   // 32 right-hand sides: lane = right-hand side, no index division
+    double* Y = smem + (size_t)warp * ldn * 32;
+    for (int i = 0; i < n; ++i) Y[i * 32 + lane] = x[(int64_t)I[i] * 32 + lane];
+    for (int i = 0; i < n; ++i) {
+      double s = 0.0;
+      if (up)
+        for (int j = 0; j <= i; ++j) s = __fma_rn(__ldg(LiT + (int64_t)j * n + i), Y[j * 32 + lane], s);
+      else
+        for (int j = i; j < n; ++j) s = __fma_rn(__ldg(LiT + (int64_t)i * n + j), Y[j * 32 + lane], s);
+      x[(int64_t)I[i] * 32 + lane] = s;
+    }
+    return;
+  }
   if (ldn > 0) {   // few right-hand sides: stage the rows, write straight back
     double* Y = smem + (size_t)warp * ldn * k;
     for (int e = lane; e < n * k; e += 32) Y[e] = x[(int64_t)I[e / k] * k + e % k];
@@ -2766,6 +2779,32 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
   double* Ys = smem + (size_t)warp * ldrows * k;
   double* Yr = Ys + (size_t)r * k;
   double* Z = Yr + (size_t)kt * k;
+  if (k == 32) {   // lane = right-hand side: every lane works on its own column (no warp sync)
+    for (int q = 0; q < r; ++q) Ys[q * 32 + lane] = x[(int64_t)S[q] * 32 + lane];
+    for (int j = 0; j < kt; ++j) Yr[j * 32 + lane] = x[(int64_t)R[j] * 32 + lane];
+    const double* M1 = up ? T : PB;    // b_R -= M1^T b_S
+    const double* M3 = up ? PB : T;    // b_S -= M3 z
+    for (int j = 0; j < kt; ++j) {
+      double sacc = 0.0;
+      for (int q = 0; q < r; ++q) sacc = __fma_rn(__ldg(M1 + (int64_t)q * kt + j), Ys[q * 32 + lane], sacc);
+      Yr[j * 32 + lane] -= sacc;
+    }
+    for (int i = 0; i < kt; ++i) {
+      double sacc = 0.0;
+      if (up)
+        for (int j = 0; j <= i; ++j) sacc = __fma_rn(__ldg(LiT + (int64_t)j * kt + i), Yr[j * 32 + lane], sacc);
+      else
+        for (int j = i; j < kt; ++j) sacc = __fma_rn(__ldg(LiT + (int64_t)i * kt + j), Yr[j * 32 + lane], sacc);
+      Z[i * 32 + lane] = sacc;
+    }
+    for (int q = 0; q < r; ++q) {
+      double sacc = 0.0;
+      for (int i = 0; i < kt; ++i) sacc = __fma_rn(__ldg(M3 + (int64_t)q * kt + i), Z[i * 32 + lane], sacc);
+      x[(int64_t)S[q] * 32 + lane] = Ys[q * 32 + lane] - sacc;
+    }
+    for (int i = 0; i < kt; ++i) x[(int64_t)R[i] * 32 + lane] = Z[i * 32 + lane];
+    return;
+  }
   for (int e = lane; e < r * k; e += 32) Ys[e] = x[(int64_t)S[e / k] * k + e % k];
   for (int e = lane; e < kt * k; e += 32) Yr[e] = x[(int64_t)R[e / k] * k + e % k];
   __syncwarp();

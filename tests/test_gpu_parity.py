@@ -133,9 +133,9 @@ def test_multi_rhs_block_equals_single_solves():
         assert np.linalg.norm(x - X[:, c]) <= 1e-12 * np.linalg.norm(x)
 
 
-@pytest.mark.parametrize("nrhs", [33, 48])
+@pytest.mark.parametrize("nrhs", [32, 33, 48])
 def test_wide_rhs_block_apply_matches_oracle(nrhs):
-    # more than 32 right-hand sides take the generic batched-GEMM replay (k_bgemm)
+    # 32 right-hand sides: lane-per-RHS replay kernels; more than 32: the generic batched GEMM
     spec, A = baseline_problem("c4", 0, 32)[:2]
     Fo = ophif.factorize(A, spec, 1e-3, "phif")
     Fg = gfac.factorize(A, spec, 1e-3, "phif")
