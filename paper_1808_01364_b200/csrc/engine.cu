@@ -1431,6 +1431,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       int tiny_rows = 1;
       for (int t = 0; t < nsk; ++t) {
         const int kk = G.size(P.skeleton[t]);
+        if (skt[t] == 0 && kk < APPLY_BIG) continue;   // full rank: the record is the identity
         if (kk <= 64 && sr[t] > 0) {   // warp replay: rows r + 2 k~ staged per warp
           tiny_sk.push_back(t);
           tiny_rows = std::max(tiny_rows, sr[t] + 2 * skt[t]);

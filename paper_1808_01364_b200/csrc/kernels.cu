@@ -2702,8 +2702,8 @@ __global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int
   const int n = a.n[t];
   const int* I = a.I + a.I_off[t];
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
-  if (k == 32 && ldn > 0) {   // 32 right-hand sides: lane = right-hand side, no index division
-    double* Y = smem + (size_t)warp * ldn * 32;
+  if (k == 32) {   // 32 right-hand sides: lane = right-hand side, no index division
+    double* Y = ldn > 0 ? smem + (size_t)warp * ldn * 32 : a.work + a.work_off[t] * 32;
     for (int i = 0; i < n; ++i) Y[i * 32 + lane] = x[(int64_t)I[i] * 32 + lane];
     for (int i = 0; i < n; ++i) {
       double s = 0.0;
