@@ -2784,10 +2784,17 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
     for (int j = 0; j < kt; ++j) Yr[j * 32 + lane] = x[(int64_t)R[j] * 32 + lane];
     const double* M1 = up ? T : PB;    // b_R -= M1^T b_S
     const double* M3 = up ? PB : T;    // b_S -= M3 z
-    for (int j = 0; j < kt; ++j) {
-      double sacc = 0.0;
-      for (int q = 0; q < r; ++q) sacc = __fma_rn(__ldg(M1 + (int64_t)q * kt + j), Ys[q * 32 + lane], sacc);
-      Yr[j * 32 + lane] -= sacc;
+    for (int j0 = 0; j0 < kt; j0 += 4) {   // four outputs per pass: independent FMA chains
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int q = 0; q < r; ++q) {
+        const double y = Ys[q * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u < kt) acc[u] = __fma_rn(__ldg(M1 + (int64_t)q * kt + j0 + u), y, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < kt) Yr[(j0 + u) * 32 + lane] -= acc[u];
     }
     for (int i = 0; i < kt; ++i) {
       double sacc = 0.0;
@@ -2797,10 +2804,17 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
         for (int j = i; j < kt; ++j) sacc = __fma_rn(__ldg(LiT + (int64_t)i * kt + j), Yr[j * 32 + lane], sacc);
       Z[i * 32 + lane] = sacc;
     }
-    for (int q = 0; q < r; ++q) {
-      double sacc = 0.0;
-      for (int i = 0; i < kt; ++i) sacc = __fma_rn(__ldg(M3 + (int64_t)q * kt + i), Z[i * 32 + lane], sacc);
-      x[(int64_t)S[q] * 32 + lane] = Ys[q * 32 + lane] - sacc;
+    for (int q0 = 0; q0 < r; q0 += 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int i = 0; i < kt; ++i) {
+        const double z = Z[i * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u < r) acc[u] = __fma_rn(__ldg(M3 + (int64_t)(q0 + u) * kt + i), z, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u < r) x[(int64_t)S[q0 + u] * 32 + lane] = Ys[(q0 + u) * 32 + lane] - acc[u];
     }
     for (int i = 0; i < kt; ++i) x[(int64_t)R[i] * 32 + lane] = Z[i * 32 + lane];
     return;
