@@ -64,6 +64,7 @@ void finalize_groups(const Spec& s, Groups& g, const std::vector<int64_t>& keys_
   g.q.assign(3 * (size_t)g.G, 0);
   g.bits.assign(g.G, 0);
   g.kind.assign(g.G, 0);
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < g.G; ++i) {
     int q[3] = {0, 0, 0}, b = 0;
     key_of(s, g.level, g.mem[g.off[i]], q, b);
@@ -315,6 +316,7 @@ std::vector<std::pair<int, int>> pattern_from_csr(const Groups& g, int64_t N, co
     tid = omp_get_thread_num();
 #endif
     std::vector<std::pair<int, int>>& mine = part[tid];
+    mine.reserve((size_t)(N / nth + 1) * 4);
     std::vector<int> stamp(g.G, -1);
 #pragma omp for schedule(static)
     for (int i = 0; i < g.G; ++i) {
