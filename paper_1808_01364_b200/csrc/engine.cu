@@ -1541,9 +1541,10 @@ struct BigApply {
     std::vector<int64_t> isrc, idst, sdst, bsrc, bdst;
     std::vector<int> ilen, blen;
     auto add = [&](const double* A, int lda, int ta, const double* B, double* C, int M, int K, double al,
-                   double be) {
+                   double be, int tri) {
       if (M <= 0) return;
       GemmDesc g;
+      g.tri = tri;
       g.A = A;
       g.B = B;
       g.C = C;
@@ -1577,10 +1578,10 @@ struct BigApply {
         double* Y = work + L.h_cwork[t] * k;
         double* Z = Y + (int64_t)n * k;
         double* Xb = Z + (int64_t)n * k;
-        if (ph == 0) add(LiT, n, 1, Y, Z, n, n, 1.0, 0.0);
-        if (ph == 1 && b > 0) add(XT, n, 0, Z, wbuf + L.h_B_off[t] * k, b, n, 1.0, 0.0);
-        if (ph == 2 && b > 0) add(XT, n, 1, Xb, Y, n, b, -1.0, 1.0);
-        if (ph == 3) add(LiT, n, 0, Y, Z, n, n, 1.0, 0.0);
+        if (ph == 0) add(LiT, n, 1, Y, Z, n, n, 1.0, 0.0, 1);   // L^-1 = (L^-T)^T: lower
+        if (ph == 1 && b > 0) add(XT, n, 0, Z, wbuf + L.h_B_off[t] * k, b, n, 1.0, 0.0, 0);
+        if (ph == 2 && b > 0) add(XT, n, 1, Xb, Y, n, b, -1.0, 1.0, 0);
+        if (ph == 3) add(LiT, n, 0, Y, Z, n, n, 1.0, 0.0, 3);   // L^-T: upper
       }
     }
     ph_off[4] = (int64_t)wd_h.size();

@@ -2288,12 +2288,16 @@ __global__ void __launch_bounds__(NT) k_rgemm(const GemmDesc* desc, const int* w
       cp_async_commit();
     };
     double a0[RG_K / 4], a1[RG_K / 4];
+    // triangular records: op(A) lower (tri 1) ends the K range at the tile's last row, op(A)
+    // upper (tri 3) starts it at the tile's first row; the skipped terms are structural zeros
+    const int kbeg = d.tri == 3 ? (i0 / RG_K) * RG_K : 0;
+    const int kend = d.tri == 1 ? min(d.K, i0 + 64) : d.K;
     __syncthreads();   // previous work item's reads of sB are done
-    load_a(a0, 0);
-    stage_b(0, 0);
+    load_a(a0, kbeg);
+    stage_b(0, kbeg);
     int buf = 0;
-    for (int kc = 0; kc < d.K; kc += RG_K) {
-      const bool more = kc + RG_K < d.K;
+    for (int kc = kbeg; kc < kend; kc += RG_K) {
+      const bool more = kc + RG_K < kend;
       if (more) {
         load_a(a1, kc + RG_K);
         stage_b(buf ^ 1, kc + RG_K);
@@ -2381,13 +2385,14 @@ __global__ void __launch_bounds__(NT, 2) k_bgemm(const GemmDesc* desc, const int
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-      const int nk = (Kt + BG_BK - 1) / BG_BK;
+      const int Kb = d.tri == 3 ? (i0 / BG_BK) * BG_BK : 0;
+      const int nk = (Kt - Kb + BG_BK - 1) / BG_BK;
       __syncthreads();   // previous tile's readers of the stage buffers are done
-      if (nk > 0) load(0, 0);
-      if (nk > 1) load(1, BG_BK);
+      if (nk > 0) load(0, Kb);
+      if (nk > 1) load(1, Kb + BG_BK);
       for (int kc = 0; kc < nk; ++kc) {
         if (kc + 2 < nk) {
-          load((kc + 2) % BG_STAGES, (kc + 2) * BG_BK);
+          load((kc + 2) % BG_STAGES, Kb + (kc + 2) * BG_BK);
           cp_async_wait<2>();
         } else if (kc + 1 < nk) {
           cp_async_wait<1>();

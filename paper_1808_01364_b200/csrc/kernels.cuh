@@ -208,7 +208,8 @@ struct GemmDesc {
   int M, N, K, lda, ldb, ldc;
   int transA;
   double alpha, beta;
-  int tri = 0;   // 0 dense; 1: op(A) lower triangular (K range < row tile end); 2: B upper triangular
+  int tri = 0;   // 0 dense; 1: op(A) lower (K < tile's last row); 2: B upper (K < tile's last column);
+                 // 3: op(A) upper (K >= tile's first row)
 };
 
 }  // namespace phif
