@@ -381,17 +381,7 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
         else if (piv[a]) row[a] = 0.0;
     }
     __syncthreads();
-    if (tid == 0) {
-      piv[p] = 1;
-      if (best.i != i) {   // dlaqp2 swap of positions i and best.i
-        const int pp = best.i;
-        col_at[pp] = col_at[i];
-        col_at[i] = p;
-        vn1[pp] = vn1[i];
-        vn2[pp] = vn2[i];
-      }
-    }
-    __syncthreads();
+    if (tid == 0) piv[p] = 1;   // (read again only after the argmax barrier)
     GID_MARK(4)
     for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
       const int b = lb * C + c;
@@ -399,9 +389,21 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     }
     // fused: Schur diagonal, dlaqp2 partial-norm downdate and the next pivot's argmax over the
     // positions > i (identical arithmetic in every CTA)
+    // the dlaqp2 swap of positions i and best.i is done by the thread owning position best.i
+    // (it takes over position i's column and norms; position i is final)
     loc = ArgMax{-1.0, 0x7fffffff};
+    const int pb = best.i;
     for (int j = i + 1 + tid; j < k; j += NT) {
-      const int col = col_at[j];
+      int col;
+      if (j == pb) {
+        col = col_at[i];
+        col_at[j] = col;
+        col_at[i] = p;
+        vn1[j] = vn1[i];
+        vn2[j] = vn2[i];
+      } else {
+        col = col_at[j];
+      }
       const double rv = row[col];
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;

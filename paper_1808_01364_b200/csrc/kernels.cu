@@ -677,7 +677,7 @@ __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s
 // workspace after G reuses the gathered matrix's region (base = smem + SMEM_DOUBLES).
 // Returns false (nothing written) when the shapes do not fit; the caller then runs cta_cpqr.
 __device__ __forceinline__ bool skel_id_gram_fits(int k, int cap) {
-  return k <= 57 && k * k <= RED_OFF && (int64_t)k * k + 5 * k + 8 <= cap;
+  return k <= 57 && k * k <= RED_OFF && (int64_t)k * k + 7 * k + 8 <= cap;
 }
 // W holds mrows rows (kept rows and zero rows), m of them kept
 __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int k, const double* W, int64_t ldw,
@@ -693,7 +693,9 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
   double* d = Rsm + k * k;
   double* vn1 = d + k;
   double* vn2 = vn1 + k;
-  int* col_at = reinterpret_cast<int*>(vn2 + k);
+  double* rdv = vn2 + k;    // sqrt(Schur diagonal) and its reciprocal per column
+  double* invv = rdv + k;
+  int* col_at = reinterpret_cast<int*>(invv + k);
   int* piv = col_at + k;
   int* sidx = piv + k;
   // G = W^T W: lower 8x8 tiles, one DMMA chain per tile (K = m in steps of 4), mirrored
@@ -734,6 +736,8 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     const double nj = fmax(dj, 0.0);
     d[j] = dj;
     vn1[j] = vn2[j] = nj;
+    rdv[j] = sqrt(nj);
+    invv[j] = nj > 0.0 ? 1.0 / rdv[j] : 0.0;
     col_at[j] = j;
     piv[j] = 0;
     loc = better(loc, ArgMax{nj, j});
@@ -746,22 +750,14 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
   int r = 0, i = 0;
   for (; i < mn; ++i) {
     if (i > 0 && best.v < cut2) break;
-    if (tid == 0 && best.i != i) {
-      const int pp = best.i, tcol = col_at[pp];
-      col_at[pp] = col_at[i];
-      col_at[i] = tcol;
-      vn1[pp] = vn1[i];
-      vn2[pp] = vn2[i];
-    }
-    __syncthreads();
-    const int p = col_at[i];
-    const double rd = sqrt(fmax(d[p], 0.0));
+    const int pb = best.i, p = col_at[pb];   // (the position swap happens in the downdate loop)
+    const double rd = rdv[p];
     if (i == 0) {
       cut = cutrel * rd;
       cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
     }
     if (rd > cut) ++r;
-    const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
+    const double inv = invv[p];
     double* row = Rsm + i * k;
     for (int a = tid; a < k; a += NT) row[a] = a == p ? rd : (piv[a] ? 0.0 : S[p * k + a] * inv);
     __syncthreads();
@@ -775,10 +771,24 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     }
     loc = ArgMax{-1.0, 0x7fffffff};
     for (int j = i + 1 + tid; j < k; j += NT) {
-      const int col = col_at[j];
+      int col;
+      if (j == pb) {   // dlaqp2 swap of positions i and pb, by the owner of position pb
+        col = col_at[i];
+        col_at[j] = col;
+        col_at[i] = p;
+        vn1[j] = vn1[i];
+        vn2[j] = vn2[i];
+      } else {
+        col = col_at[j];
+      }
       const double rv = row[col];
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;
+      {
+        const double rdn = sqrt(fmax(dn, 0.0));
+        rdv[col] = rdn;
+        invv[col] = rdn > 0.0 ? 1.0 / rdn : 0.0;
+      }
       double w1 = vn1[j];
       if (w1 != 0.0) {
         const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
