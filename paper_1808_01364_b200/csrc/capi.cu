@@ -125,10 +125,9 @@ int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err) {
     } else {
       phif::DBuf d;
       d.alloc(bytes, f.stream);
-      cudaMemcpyAsync(d.p, x, bytes, cudaMemcpyHostToDevice, f.stream);
+      phif::upload_bytes(d.p, x, bytes, f.stream);
       phif::apply(f, d.as<double>(), nrhs, mode);
-      cudaMemcpyAsync(x, d.p, bytes, cudaMemcpyDeviceToHost, f.stream);
-      cudaStreamSynchronize(f.stream);
+      phif::download_bytes(x, d.p, bytes, f.stream);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw phif::CudaError(cudaGetErrorString(e));
@@ -147,7 +146,7 @@ int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, i
     const bool xdev = is_device(x);
     if (!is_device(b)) {
       db.alloc(bytes, s);
-      cudaMemcpyAsync(db.p, b, bytes, cudaMemcpyHostToDevice, s);
+      phif::upload_bytes(db.p, b, bytes, s);
       bd = db.as<double>();
     }
     if (!xdev) {
@@ -155,7 +154,7 @@ int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, i
       xd = dx.as<double>();
     }
     phif::PcgResult r = phif::pcg(*A->m, F ? F->f.get() : nullptr, bd, xd, nrhs, tol, maxit, s);
-    if (!xdev) cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, s);
+    if (!xdev) phif::download_bytes(x, xd, bytes, s);
     cudaStreamSynchronize(s);
     for (int c = 0; c < nrhs; ++c) {
       if (iters) iters[c] = r.iters[c];

@@ -455,6 +455,54 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   }
 }
 
+// device -> host copy through a pinned staging buffer (DMA into pinned memory, then a parallel
+// host memcpy out); synchronises the stream
+void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  static constexpr size_t CH = (size_t)64 << 20;
+  static char* stage = nullptr;
+  static bool ok = true;
+  static std::mutex mu;
+  if (bytes < ((size_t)1 << 20) || !ok) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (!stage && cudaHostAlloc((void**)&stage, 2 * CH, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    ok = false;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  // double-buffered: the DMA of chunk c+1 overlaps the host copy of chunk c
+  const size_t nch = (bytes + CH - 1) / CH;
+  cudaEvent_t ev[2];
+  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto issue = [&](size_t c) {
+    const size_t a = c * CH, len = std::min(CH, bytes - a);
+    CK(cudaMemcpyAsync(stage + (c & 1) * CH, static_cast<const char*>(src) + a, len, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ev[c & 1], s));
+  };
+  issue(0);
+  for (size_t c = 0; c < nch; ++c) {
+    if (c + 1 < nch) issue(c + 1);
+    CK(cudaEventSynchronize(ev[c & 1]));
+    const size_t a = c * CH, len = std::min(CH, bytes - a);
+    const char* from = stage + (c & 1) * CH;
+    char* to = static_cast<char*>(dst) + a;
+    const int64_t np = (int64_t)std::max<size_t>(1, len >> 22);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(std::min<int64_t>(np, 6))
+    for (int64_t q = 0; q < np; ++q) {
+      const size_t u = len * q / np, e = len * (q + 1) / np;
+      memcpy(to + u, from + u, e - u);
+    }
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+}
+
 static void keep_pool_memory() {
   // freed blocks stay in the stream-ordered pool instead of going back to the driver at every sync
   static bool done = false;

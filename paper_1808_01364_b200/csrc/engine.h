@@ -45,6 +45,8 @@ struct DBuf {
 
 // host -> device copy on stream s; large copies go through a pinned staging ring (engine.cu)
 void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// device -> host copy through pinned staging (synchronises the stream)
+void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s);
 template <class T>
 void upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
   b.alloc(std::max<size_t>(1, v.size()) * sizeof(T), s);
