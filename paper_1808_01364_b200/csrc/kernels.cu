@@ -922,7 +922,22 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
   int* perm = iw;
   int* sidx = iw + k;
   int* flag = iw + 2 * k;
-  const int m = gather_chunks<true>(lv, sk, nc, s, 0, nch, W, ldw, 0, sint, 512);
+  int m;
+  if (nch <= 512) {
+    // the count pass left every chunk's keep mask and row prefix in sint: copy without
+    // recomputing them (nothing has written sint since)
+    const unsigned* smask = reinterpret_cast<const unsigned*>(sint);
+    const int* spre = sint + 512;
+    const int g0 = sk.groups[s], warp = tid >> 5;
+    for (int j = warp; j < nch; j += NT / 32) {
+      const int i = nc.locate(j);
+      chunk_copy<8>(lv, nc, g0, k, i, 32 * (j - nc.ch0[i]), smask[j], W, ldw, spre[j]);
+    }
+    m = nch > 0 ? spre[nch - 1] + __popc(smask[nch - 1]) : 0;
+    __syncthreads();
+  } else {
+    m = gather_chunks<true>(lv, sk, nc, s, 0, nch, W, ldw, 0, sint, 512);
+  }
   if (tid == 0) sk.rows[s] = m;
   SID_MARK(17)
   uint8_t* red = sk.red + gof;
