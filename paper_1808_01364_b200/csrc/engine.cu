@@ -149,8 +149,8 @@ std::unique_ptr<Matrix> matrix_create(const int64_t* rowptr, const int* col, con
   A->nnz = rowptr[N];
   // host copies of the pattern for the planner (parallel chunked copies; a few threads saturate
   // the host memory bandwidth)
-  A->h_rowptr.resize(N + 1);
-  A->h_col.resize(A->nnz);
+  A->h_rowptr.reset(new int64_t[N + 1]);
+  A->h_col.reset(new int[std::max<int64_t>(A->nnz, 1)]);
   auto pcopy = [](void* dst, const void* src, size_t bytes) {
     const int64_t nchunk = (int64_t)std::max<size_t>(1, bytes >> 22);
 #pragma omp parallel for schedule(dynamic, 1) num_threads(std::min<int64_t>(nchunk, 6))
@@ -159,8 +159,8 @@ std::unique_ptr<Matrix> matrix_create(const int64_t* rowptr, const int* col, con
       memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, e - a);
     }
   };
-  pcopy(A->h_rowptr.data(), rowptr, (N + 1) * sizeof(int64_t));
-  pcopy(A->h_col.data(), col, A->nnz * sizeof(int));
+  pcopy(A->h_rowptr.get(), rowptr, (N + 1) * sizeof(int64_t));
+  pcopy(A->h_col.get(), col, A->nnz * sizeof(int));
   A->rowptr.alloc((N + 1) * sizeof(int64_t), s);
   A->col.alloc(A->nnz * sizeof(int), s);
   A->val.alloc(A->nnz * sizeof(double), s);
@@ -550,7 +550,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     if (lev == 0) {
       L.plan.grp = classify_all(sp);
       DBG("level 0: classified");
-      pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.data(), A.h_col.data());
+      pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.get(), A.h_col.get());
     } else {
       L.plan.grp = classify_next(sp, prev->plan.grp, alive_mem);
       pairs = pattern_next(prev->plan, L.plan.grp);

@@ -55,8 +55,8 @@ void upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
 
 struct Matrix {
   int64_t N = 0, nnz = 0;
-  std::vector<int64_t> h_rowptr;
-  std::vector<int> h_col;
+  std::unique_ptr<int64_t[]> h_rowptr;   // host copy of the pattern for the planner
+  std::unique_ptr<int[]> h_col;           // (uninitialised allocations: filled by parallel copies)
   DBuf rowptr, col, val;
 };
 
