@@ -733,7 +733,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       launch_group_pos(dv, dgid.as<int>(), dpos.as<int>(), s);
       launch_ingest(dv, dgid.as<int>(), dpos.as<int>(), A.rowptr.as<int64_t>(), A.col.as<int>(),
                     A.val.as<double>(), sp.N, s);
-      CK(cudaStreamSynchronize(s));
+      // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     } else {
       RepackArgs ra;
       ra.nblk = (int)P.pat.bg.size();
@@ -785,7 +785,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       ra.oadj_blk = prev->adj_blk.as<int>();
       ra.ogsize = prev->gsize.as<int>();
       launch_repack(ra, s);
-      CK(cudaStreamSynchronize(s));
+      // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
       prev->pool.release();
     }
     if (timing) CK(cudaEventRecord(ev[1], s));
@@ -994,7 +994,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         upload(dw2t, w2t, s);
         launch_bgemm(dd1.as<GemmDesc>(), dw1d.as<int>(), dw1t.as<int>(), (int)w1d.size(), s);
         launch_bgemm(dd2.as<GemmDesc>(), dw2d.as<int>(), dw2t.as<int>(), (int)w2d.size(), s);
-        CK(cudaStreamSynchronize(s));
+        // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
       }
     }
     if (timing) CK(cudaEventRecord(ev[7], s));
@@ -1078,7 +1078,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       }
       launch_skel_id_dyn(dv, ka, ds, need, s);
       CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(s));
+      // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     } else {
       // per wave: small separators -> one CTA each; large ones -> gather + team CPQR
       static int num_sms = 0;
@@ -1313,7 +1313,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         }
       }
       CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(s));
+      // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     }
     // ranks and redundant flags back to the host (large separator updates, next level planning)
     L.h_rank.resize(nsk);
