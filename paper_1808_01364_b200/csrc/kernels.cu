@@ -2466,6 +2466,29 @@ __global__ void k_rows(double* Y, double* x, const int* idx, const int64_t* seg_
   for (int sgi = blockIdx.x * wpb + (threadIdx.x >> 5); sgi < nseg; sgi += gridDim.x * wpb) {
     const int* id = idx + seg_src[sgi];
     double* y = Y + seg_dst[sgi] * k;
+    if (k == 32) {   // lane = right-hand side, 8 rows in flight (no index division)
+      const int nr = seg_len[sgi];
+      for (int r0 = 0; r0 < nr; r0 += 8) {
+        int rid[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rid[u] = r0 + u < nr ? __ldg(id + r0 + u) : 0;
+        if (to_x) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = r0 + u < nr ? y[(int64_t)(r0 + u) * 32 + lane] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (r0 + u < nr) x[(int64_t)rid[u] * 32 + lane] = v[u];
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = r0 + u < nr ? x[(int64_t)rid[u] * 32 + lane] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (r0 + u < nr) y[(int64_t)(r0 + u) * 32 + lane] = v[u];
+        }
+      }
+      continue;
+    }
     const int64_t n = (int64_t)seg_len[sgi] * k;
     for (int64_t e = lane; e < n; e += 32) {
       double* px = x + (int64_t)id[e / k] * k + e % k;
