@@ -213,6 +213,43 @@ def dominant_roofline(stats, hbm_peak, fp64_peak):
             "algorithmic_bytes": by, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
 
+STAGES = ["repack", "eliminate", "precondition", "id", "skel_update"]
+STAGE_KEYS = ["t_repack_ms", "t_eliminate_ms", "t_precondition_ms", "t_id_ms", "t_skel_update_ms"]
+
+
+def roofline_levels(stats, hbm_peak, fp64_peak):
+    """Per (level, stage): algorithmic flops and bytes (SURVEY.md 8(d) counts accumulated by the
+    engine from the actual shapes) over the stage's CUDA-event time on the launch stream, as
+    fractions of the measured FP64 (DGEMM) and HBM (copy) peaks. `bound` is the roofline the
+    stage's arithmetic intensity puts it under (ridge = fp64_peak / hbm_peak)."""
+    ridge = fp64_peak * 1e12 / (hbm_peak * 1e9)
+    out = []
+    for lv in stats["levels"]:
+        for si, key in enumerate(STAGE_KEYS):
+            t = float(lv.get(key, 0.0))
+            fl, by = float(lv["flops"][si]), float(lv["bytes"][si])
+            if t <= 0.0 or (fl == 0.0 and by == 0.0):
+                continue
+            tf = fl / (t * 1e-3) / 1e12
+            gb = by / (t * 1e-3) / 1e9
+            root = lv["level"] == stats["levels"][-1]["level"] and si == 1
+            out.append({"level": lv["level"], "stage": "root" if root else STAGES[si], "t_ms": round(t, 4), "flops": fl, "bytes": by,
+                        "tflops": round(tf, 3), "gbs": round(gb, 1), "frac_fp64": round(tf / fp64_peak, 4),
+                        "frac_hbm": round(gb / hbm_peak, 4),
+                        "bound": "tensor" if by and fl / by >= ridge else "hbm"})
+    return out
+
+
+def cpu_fullsize(workload):
+    """Committed full-size CPU-oracle timing of the workload, measured on the GPU box host
+    (profiles/cpu_fullsize_<workload>_r02.json, written by tools/cpu_fullsize.py)."""
+    path = os.path.join(ROOT, "profiles", f"cpu_fullsize_{workload}_r02.json")
+    try:
+        return json.load(open(path))
+    except (OSError, ValueError):
+        return None
+
+
 def run_b200(args, world, rank, local, pg):
     import torch
 
@@ -268,7 +305,7 @@ def run_b200(args, world, rank, local, pg):
     # untimed warm-up solve (apply workspaces for this nrhs are allocated on the first call)
     rc = L.phif_pcg(dm.handle, F.handle, C.c_void_p(Bd.data_ptr()), C.c_void_p(Xd.data_ptr()), B.shape[1],
                     cfg.tol, 2, C.c_void_p(stream), _lib.ptr(iters), _lib.ptr(relres), _lib.ptr(conv),
-                    C.byref(err))
+                    None, None, C.byref(err))
     _lib.raise_for(rc, err)
     Xd.zero_()
     torch.cuda.synchronize(dev)
@@ -277,11 +314,17 @@ def run_b200(args, world, rank, local, pg):
     e0.record()
     rc = L.phif_pcg(dm.handle, F.handle, C.c_void_p(Bd.data_ptr()), C.c_void_p(Xd.data_ptr()), B.shape[1],
                     cfg.tol, 500, C.c_void_p(stream), _lib.ptr(iters), _lib.ptr(relres), _lib.ptr(conv),
-                    C.byref(err))
+                    None, None, C.byref(err))
     e1.record()
     torch.cuda.synchronize(dev)
     _lib.raise_for(rc, err)
     t_solve = e0.elapsed_time(e1)
+
+    # e_s = ||I - G^-1 A G^-T|| (power iteration on the device)
+    from paper_1808_01364_b200 import diagnostics
+    t0 = time.perf_counter()
+    es = diagnostics.estimate_solve_error(A, F)
+    t_es = time.perf_counter() - t0
 
     # e2e: public API with host buffers (CSR upload + factorize + stats read-back)
     h2d = A.csr.indptr.size * 8 + A.csr.indices.size * 4 + A.csr.data.size * 8
@@ -308,9 +351,20 @@ def run_b200(args, world, rank, local, pg):
     cpu = None
     if world == 1 and not args.no_cpu:
         dofs, dt, sspec, _ = cpu_sample(args.workload)
-        cpu = {"value": dofs, "unit": "DOF/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"oracle factorize of the {cfg_name} recipe on a {sn}-grid (N={sspec.ndofs}), "
-                         f"{dt:.1f} s; numpy/scipy OpenBLAS using all host threads"}
+        sampled = {"value": dofs, "unit": "DOF/s", "cores": os.cpu_count(), "N": sspec.ndofs, "seconds": dt,
+                   "sample": f"oracle factorize of the {cfg_name} recipe on a {sn}-grid (N={sspec.ndofs}), "
+                             f"timed live in this run; numpy/scipy OpenBLAS using all host threads"}
+        full = cpu_fullsize(args.workload)
+        if full and full.get("N") == N:
+            cpu = {"value": full["dofs_per_s"], "unit": "DOF/s", "cores": full["cores"], "kind": "port",
+                   "N": N, "seconds": full["t_factor_s"],
+                   "sample": f"full-size oracle factorization of {cfg_name} (N={N}) on the GPU box host "
+                             f"({full['cpu_model']}, {full['cores']} cores), committed in "
+                             f"profiles/cpu_fullsize_{args.workload}_r02.json; the live bounded sample of this "
+                             f"run is under 'sampled'",
+                   "sampled": sampled}
+        else:
+            cpu = dict(sampled, kind="port")
     line = {
         "metric": METRIC,
         "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -327,6 +381,8 @@ def run_b200(args, world, rank, local, pg):
                 "solve_ms_per_rhs": 1e3 * t_e2e_solve / B.shape[1],
                 "solve_h2d_bytes": int(B.nbytes), "solve_d2h_bytes": int(Xh.nbytes)},
         "roofline": roof,
+        "roofline_levels": roofline_levels(stats, hbm_peak, fp64_peak),
+        "e_s": es.value, "e_s_iters": es.iterations, "e_s_ms": 1e3 * t_es,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,

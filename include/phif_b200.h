@@ -83,9 +83,13 @@ void phif_factor_free(phif_factor* F);
  * 3 = F (apply), 4 = G^T, 5 = G. x: N x nrhs, host or device. */
 int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err);
 
-/* PCG with F^-1 (F may be NULL for plain CG). b, x: N x nrhs. Per column outputs. */
+/* PCG with F^-1 (F may be NULL for plain CG). b, x: N x nrhs. Per column outputs. history (may be
+ * NULL) receives the relative residual of every column after every iteration (row-major,
+ * iteration x nrhs, room for maxit rows: SolveReport residual history) and
+ * *history_len the number of rows written. */
 int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, int nrhs, double tol, int maxit,
-             void* stream, int* iters, double* relres, int* converged, phif_error* err);
+             void* stream, int* iters, double* relres, int* converged, double* history, int* history_len,
+             phif_error* err);
 
 /* e_s = ||I - G^-1 A G^-T||_2 by power iteration from host start vector x0 (length N). */
 int phif_solve_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
@@ -111,11 +115,21 @@ int phif_skeleton_sets(const phif_factor* F, int level, int64_t* counts, int32_t
                        int32_t* skel_dofs, int32_t* red_dofs);
 int phif_num_levels(const phif_factor* F);
 
+/* Statistics JSON of the levels a factorization completed before its last PHIF_NOT_SPD failure on
+ * this thread (NotSpdError.partial_stats, errors.py:21-30 / SPEC.md:279); same contract as
+ * phif_stats_json. */
+size_t phif_last_partial_stats(char* buf, size_t cap);
+
 /* Planner check (CPU only): group the active DOFs of `level` like classify_active.
  * group_of[i] = group index (classify order) of active[i]; kind_of_group[g] = number of
  * on-line axes. Returns the number of groups (or -1); kind_of_group may be NULL. */
 int64_t phif_classify(int dim, int n, int m, int level, const int32_t* active, int64_t nactive, int32_t* group_of,
                       int32_t* kind_of_group, int64_t kind_cap);
+
+/* Device planner check (GPU): plan level 0 of A's pattern on the host (planner.cpp) and on the
+ * device (gpu_plan.cu, the level-0 planner factorize uses) and compare every plan array.
+ * Returns the number of differing arrays (0 = identical, -1 = error); names them in `report`. */
+int phif_plan_check(const phif_matrix* A, int dim, int n, int m, char* report, size_t cap);
 
 /* Planner dry run (CPU only): plan every level of a factorization of the CSR pattern,
  * assuming the first `keep` DOFs of every separator group survive (keep < 0: all survive).

@@ -3,9 +3,9 @@
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 power_norm: power iteration from a unit start vector drawn from
-default_rng(seed).standard_normal(dim); each step y = op(x), estimate ||y||,
-x <- y / ||y||; converged when two successive estimates agree to rel_tol
-(SPEC.md:400-404). e_s = power_norm(x -> x - G^-1 A G^-T x),
+default_rng(seed).standard_normal(dim); each step y = op(x), estimate |x^T y|
+(the Rayleigh quotient of the unit iterate), x <- y / ||y||; converged when two
+successive Rayleigh quotients agree to rel_tol. e_s = power_norm(x -> x - G^-1 A G^-T x),
 e_a = power_norm(x -> A x - F x) / power_norm(A).
 """
 
@@ -33,16 +33,17 @@ def power_norm(op, dim, rel_tol=1e-2, maxit=200, seed=0):
     est = 0.0
     for it in range(1, maxit + 1):
         y = np.asarray(op(x), dtype=np.float64)
-        est = float(np.linalg.norm(y))
-        if est == 0.0:
+        est = abs(float(x @ y))              # Rayleigh quotient of the unit iterate
+        ny = float(np.linalg.norm(y))
+        if ny == 0.0:
             return NormEstimate(0.0, it, True, 0.0)
         if prev is not None:
-            rel = abs(est - prev) / est
+            rel = abs(est - prev) / est if est > 0.0 else abs(est - prev)
             if rel <= rel_tol:
                 return NormEstimate(est, it, True, rel)
         prev = est
-        x = y / est
-    rel = abs(est - prev) / est if prev else np.inf
+        x = y / ny
+    rel = (abs(est - prev) / est if est > 0.0 else abs(est - prev)) if prev is not None else np.inf
     return NormEstimate(est, maxit, False, rel)
 
 

@@ -30,7 +30,7 @@ _lib = None
 EXPORTS = ("phif_version", "phif_launch_count", "phif_matrix_create", "phif_matrix_free", "phif_factorize", "phif_factor_free",
            "phif_apply", "phif_pcg", "phif_solve_error", "phif_apply_error", "phif_root_factor", "phif_stats_json",
            "phif_skeleton_sets",
-           "phif_num_levels", "phif_classify", "phif_plan_dryrun")
+           "phif_num_levels", "phif_last_partial_stats", "phif_plan_check", "phif_classify", "phif_plan_dryrun")
 
 
 def lib():
@@ -52,7 +52,7 @@ def lib():
     L.phif_factor_free.argtypes = [P]
     L.phif_apply.argtypes = [P, P, I, I, C.POINTER(phif_error)]
     L.phif_apply.restype = I
-    L.phif_pcg.argtypes = [P, P, P, P, I, C.c_double, I, P, P, P, P, C.POINTER(phif_error)]
+    L.phif_pcg.argtypes = [P, P, P, P, I, C.c_double, I, P, P, P, P, P, C.POINTER(I), C.POINTER(phif_error)]
     L.phif_pcg.restype = I
     L.phif_solve_error.argtypes = [P, P, P, C.c_double, I, D, C.POINTER(I), C.POINTER(I), D,
                                    C.POINTER(phif_error)]
@@ -68,6 +68,10 @@ def lib():
     L.phif_skeleton_sets.restype = I
     L.phif_num_levels.argtypes = [P]
     L.phif_num_levels.restype = I
+    L.phif_last_partial_stats.argtypes = [C.c_char_p, C.c_size_t]
+    L.phif_last_partial_stats.restype = C.c_size_t
+    L.phif_plan_check.argtypes = [P, I, I, I, C.c_char_p, C.c_size_t]
+    L.phif_plan_check.restype = I
     L.phif_classify.argtypes = [I, I, I, I, P, I64, P, P, I64]
     L.phif_classify.restype = I64
     L.phif_plan_dryrun.argtypes = [I, I, I, P, P, I, C.c_char_p, C.c_size_t]
@@ -80,11 +84,28 @@ def ptr(a: np.ndarray):
     return C.c_void_p(a.ctypes.data)
 
 
+def last_partial_stats():
+    """Statistics of the levels completed before the last NotSpd failure (None if unavailable)."""
+    import json
+    L = lib()
+    n = L.phif_last_partial_stats(None, 0)
+    if n == 0:
+        return None
+    buf = C.create_string_buffer(n + 1)
+    L.phif_last_partial_stats(buf, n + 1)
+    try:
+        return json.loads(buf.value.decode())
+    except ValueError:
+        return None
+
+
 def raise_for(rc: int, err: phif_error, partial_stats=None):
     from .errors import BreakdownError, NotSpdError
     if rc == OK:
         return
     if rc == NOT_SPD:
+        if partial_stats is None:
+            partial_stats = last_partial_stats()
         raise NotSpdError(err.pivot, err.level, STAGES.get(err.stage, err.stage), err.group, partial_stats)
     if rc == BREAKDOWN:
         raise BreakdownError(f"non-finite PCG recurrence value at iteration {err.group}")

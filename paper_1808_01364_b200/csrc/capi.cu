@@ -9,6 +9,7 @@
 
 #include "../../include/phif_b200.h"
 #include "engine.h"
+#include "gpu_plan.h"
 
 struct phif_matrix {
   std::unique_ptr<phif::Matrix> m;
@@ -43,6 +44,8 @@ void set_err(phif_error* e, int code, const char* msg) {
   std::snprintf(e->message, sizeof(e->message), "%s", msg);
 }
 
+thread_local std::string g_partial_stats;   // stats of the levels done before the last NotSpd
+
 template <class Fn>
 int guarded(phif_error* err, Fn&& fn) {
   try {
@@ -50,6 +53,7 @@ int guarded(phif_error* err, Fn&& fn) {
     if (err) err->code = PHIF_OK;
     return PHIF_OK;
   } catch (const phif::NotSpd& e) {
+    g_partial_stats = e.partial;
     if (err) {
       err->code = PHIF_NOT_SPD;
       err->pivot = e.pivot;
@@ -135,7 +139,8 @@ int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err) {
 }
 
 int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, int nrhs, double tol, int maxit,
-             void* stream, int* iters, double* relres, int* converged, phif_error* err) {
+             void* stream, int* iters, double* relres, int* converged, double* history, int* history_len,
+             phif_error* err) {
   int brk = 0;
   int rc = guarded(err, [&] {
     cudaStream_t s = F ? F->f->stream : (cudaStream_t)stream;
@@ -153,7 +158,9 @@ int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, i
       dx.alloc(bytes, s);
       xd = dx.as<double>();
     }
-    phif::PcgResult r = phif::pcg(*A->m, F ? F->f.get() : nullptr, bd, xd, nrhs, tol, maxit, s);
+    phif::PcgResult r = phif::pcg(*A->m, F ? F->f.get() : nullptr, bd, xd, nrhs, tol, maxit, s, history != nullptr);
+    if (history_len) *history_len = r.history_len;
+    if (history && r.history_len) std::memcpy(history, r.history.data(), r.history.size() * sizeof(double));
     if (!xdev) phif::download_bytes(x, xd, bytes, s);
     cudaStreamSynchronize(s);
     for (int c = 0; c < nrhs; ++c) {
@@ -199,6 +206,97 @@ int phif_root_factor(phif_factor* F, double* out, int* n, phif_error* err) {
 
 size_t phif_stats_json(const phif_factor* F, char* buf, size_t cap) {
   const std::string s = F->f->stats_json();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return s.size();
+}
+
+int phif_plan_check(const phif_matrix* A, int dim, int n, int m, char* report, size_t cap) {
+  std::string rep;
+  int bad = 0;
+  try {
+    phif::Spec s;
+    s.init(dim, n, m);
+    const phif::Matrix& M = *A->m;
+    phif::LevelPlan h, d;
+    h.grp = phif::classify_all(s);
+    phif::build_level(s, h, phif::pattern_from_csr(h.grp, s.N, M.h_rowptr.get(), M.h_col.get()));
+    phif::DevPlan0 dp;
+    phif::plan_level0_device(s, M.rowptr.as<int64_t>(), M.col.as<int>(), M.nnz, d, dp, A->stream);
+    phif::download_plan0(dp, d, A->stream);
+    cudaStreamSynchronize(A->stream);
+    auto cmp = [&](const char* name, const auto& a, const auto& b) {
+      if (a.size() != b.size() || !std::equal(a.begin(), a.end(), b.begin())) {
+        ++bad;
+        rep += std::string(name) + " ";
+      }
+    };
+    if (h.grp.G != d.grp.G) {
+      ++bad;
+      rep += "G ";
+    }
+    cmp("off", h.grp.off, d.grp.off);
+    cmp("mem", h.grp.mem, d.grp.mem);
+    cmp("kind", h.grp.kind, d.grp.kind);
+    cmp("q", h.grp.q, d.grp.q);
+    cmp("bits", h.grp.bits, d.grp.bits);
+    cmp("bg", h.pat.bg, d.pat.bg);
+    cmp("bh", h.pat.bh, d.pat.bh);
+    cmp("adj_off", h.pat.adj_off, d.pat.adj_off);
+    cmp("adj_nbr", h.pat.adj_nbr, d.pat.adj_nbr);
+    cmp("adj_blk", h.pat.adj_blk, d.pat.adj_blk);
+    cmp("boff", h.boff, d.boff);
+    if (h.pool_doubles != d.pool_doubles) {
+      ++bad;
+      rep += "pool_doubles ";
+    }
+    cmp("interior", h.interior, d.interior);
+    cmp("precond", h.precond, d.precond);
+    cmp("skeleton", h.skeleton, d.skeleton);
+    cmp("cell_nbr_off", h.cell_nbr_off, d.cell_nbr_off);
+    cmp("cell_nbr", h.cell_nbr, d.cell_nbr);
+    cmp("cell_nbr_blk", h.cell_nbr_blk, d.cell_nbr_blk);
+    cmp("cell_nbr_col", h.cell_nbr_col, d.cell_nbr_col);
+    cmp("cell_n", h.cell_n, d.cell_n);
+    cmp("cell_b", h.cell_b, d.cell_b);
+    cmp("tgt_blk", h.tgt_blk, d.tgt_blk);
+    cmp("tgt_off", h.tgt_off, d.tgt_off);
+    cmp("con_cell", h.con_cell, d.con_cell);
+    cmp("con_row", h.con_row, d.con_row);
+    cmp("con_col", h.con_col, d.con_col);
+    cmp("scale_blk", h.scale_blk, d.scale_blk);
+    cmp("sk_nbr_off", h.sk_nbr_off, d.sk_nbr_off);
+    cmp("sk_nbr", h.sk_nbr, d.sk_nbr);
+    cmp("sk_nbr_blk", h.sk_nbr_blk, d.sk_nbr_blk);
+    cmp("sk_ndep", h.sk_ndep, d.sk_ndep);
+    cmp("sk_succ_off", h.sk_succ_off, d.sk_succ_off);
+    cmp("sk_succ", h.sk_succ, d.sk_succ);
+    cmp("sk_wave", h.sk_wave, d.sk_wave);
+    cmp("wave_off", h.wave_off, d.wave_off);
+    cmp("wave_order", h.wave_order, d.wave_order);
+    if (h.nwaves != d.nwaves) {
+      ++bad;
+      rep += "nwaves ";
+    }
+    rep += "| G=" + std::to_string(d.grp.G) + " blocks=" + std::to_string(d.pat.bg.size()) +
+           " schur_contributions=" + std::to_string(d.con_cell.size());
+  } catch (const std::exception& e) {
+    rep = std::string("error: ") + e.what();
+    bad = -1;
+  }
+  if (report && cap) {
+    const size_t k = std::min(cap - 1, rep.size());
+    std::memcpy(report, rep.data(), k);
+    report[k] = 0;
+  }
+  return bad;
+}
+
+size_t phif_last_partial_stats(char* buf, size_t cap) {
+  const std::string& s = g_partial_stats;
   if (buf && cap) {
     const size_t n = std::min(cap - 1, s.size());
     std::memcpy(buf, s.data(), n);

@@ -17,6 +17,7 @@
 #include <sstream>
 
 #include "engine.h"
+#include "gpu_plan.h"
 
 namespace phif {
 
@@ -69,39 +70,87 @@ DBuf& DBuf::operator=(DBuf&& o) noexcept {
 }
 
 // Caching device allocator: blocks come from cudaMalloc once and are recycled by size class
-// (never returned to the driver). Safe because every engine buffer is used on one stream in
-// order, so a block released here is only handed out again to later work on that stream.
+// (never returned to the driver). Thread-safe (one mutex) and stream-ordered: a block released on
+// stream s carries an event recorded on s at release; a later request from the same stream reuses
+// it directly (stream order already serialises the old and the new user), a request from another
+// stream first makes that stream wait on the event (no host synchronisation either way).
 namespace {
 struct DeviceCache {
-  std::multimap<size_t, void*> free_blocks;
+  struct Blk {
+    void* p;
+    cudaStream_t s;
+    cudaEvent_t ev;
+    int dev;
+  };
+  std::multimap<size_t, Blk> free_blocks;
+  std::vector<cudaEvent_t> events;   // recycled release events
   size_t cached = 0;
+  std::mutex mu;
   static size_t round(size_t b) {
     if (b <= (1u << 20)) return (b + 511) & ~size_t(511);
     return (b + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
   }
-  void* get(size_t& b) {
+  void* get(size_t& b, cudaStream_t st) {
     b = round(b);
-    auto it = free_blocks.lower_bound(b);
-    if (it != free_blocks.end() && it->first <= b + b / 4) {
-      void* p = it->second;
-      b = it->first;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    // best fit within +25%, preferring a block released on the requesting stream
+    auto lo = free_blocks.lower_bound(b), hi = free_blocks.upper_bound(b + b / 4);
+    auto pick = free_blocks.end();
+    for (auto it = lo; it != hi; ++it) {
+      if (it->second.dev != dev) continue;
+      if (it->second.s == st) {
+        pick = it;
+        break;
+      }
+      if (pick == free_blocks.end()) pick = it;
+    }
+    if (pick != free_blocks.end()) {
+      Blk k = pick->second;
+      b = pick->first;
       cached -= b;
-      free_blocks.erase(it);
-      return p;
+      free_blocks.erase(pick);
+      if (k.s != st) CK(cudaStreamWaitEvent(st, k.ev, 0));
+      events.push_back(k.ev);
+      return k.p;
     }
     void* p = nullptr;
     if (cudaMalloc(&p, b) != cudaSuccess) {
       cudaGetLastError();
-      // release cached blocks and retry once
-      for (auto& kv : free_blocks) cudaFree(kv.second);
-      free_blocks.clear();
-      cached = 0;
+      // release the cached blocks of this device (after their last users) and retry once
+      for (auto it = free_blocks.begin(); it != free_blocks.end();) {
+        if (it->second.dev == dev) {
+          cudaEventSynchronize(it->second.ev);
+          cudaFree(it->second.p);
+          events.push_back(it->second.ev);
+          cached -= it->first;
+          it = free_blocks.erase(it);
+        } else {
+          ++it;
+        }
+      }
       CK(cudaMalloc(&p, b));
     }
     return p;
   }
-  void put(void* p, size_t b) {
-    free_blocks.emplace(b, p);
+  void put(void* p, size_t b, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    cudaEvent_t ev;
+    if (events.empty()) {
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    } else {
+      ev = events.back();
+      events.pop_back();
+    }
+    if (cudaEventRecord(ev, st) != cudaSuccess) {   // (stream already destroyed: order on the device)
+      cudaGetLastError();
+      cudaDeviceSynchronize();
+      CK(cudaEventRecord(ev, 0));
+    }
+    free_blocks.emplace(b, Blk{p, st, ev, dev});
     cached += b;
   }
 };
@@ -115,12 +164,12 @@ void DBuf::alloc(size_t nbytes, cudaStream_t st, bool zero) {
   release();
   s = st;
   bytes = std::max<size_t>(nbytes, 8);
-  p = dcache().get(bytes);
+  p = dcache().get(bytes, st);
   if (zero) CK(cudaMemsetAsync(p, 0, bytes, st));
 }
 
 void DBuf::release() {
-  if (p) dcache().put(p, bytes);
+  if (p) dcache().put(p, bytes, s);
   p = nullptr;
   bytes = 0;
 }
@@ -400,14 +449,15 @@ static long long* gid_prof_buffer() {
   return buf;
 }
 
-// Pinned staging ring for host -> device uploads: two halves, each guarded by the event of the
-// last copy issued from it; the host fills the staging area with a parallel memcpy, so the DMA
+// Pinned staging ring for host -> device uploads: two halves; every copy issued from a half
+// records its own event (on whichever stream issued it), and a half is refilled only after all
+// of its copies have drained. The host fills the staging area with a parallel memcpy, so the DMA
 // engine copies at pinned-memory speed instead of the driver's pageable staging.
 void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   static constexpr size_t HALF = (size_t)96 << 20, MIN_STAGED = (size_t)1 << 20;
   static char* ring = nullptr;
   static bool ok = true;
-  static cudaEvent_t ev[2];
+  static std::vector<cudaEvent_t> pending[2], spare;
   static int cur = 0;
   static size_t pos = 0;
   static std::mutex mu;
@@ -423,18 +473,18 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
       return;
     }
-    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-    CK(cudaEventRecord(ev[0], s));
-    CK(cudaEventRecord(ev[1], s));
   }
   const char* sp = static_cast<const char*>(src);
   char* dp = static_cast<char*>(dst);
   while (bytes > 0) {
-    if (pos == HALF) {   // switch halves; wait until the other half's last copy has drained
+    if (pos == HALF) {   // switch halves; wait until every copy from the other half has drained
       cur ^= 1;
       pos = 0;
-      CK(cudaEventSynchronize(ev[cur]));
+      for (cudaEvent_t e : pending[cur]) {
+        CK(cudaEventSynchronize(e));
+        spare.push_back(e);
+      }
+      pending[cur].clear();
     }
     const size_t len = std::min(bytes, HALF - pos);
     char* stage = ring + (size_t)cur * HALF + pos;
@@ -447,7 +497,15 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
       memcpy(stage + a, sp + a, e - a);
     }
     CK(cudaMemcpyAsync(dp, stage, len, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(ev[cur], s));
+    cudaEvent_t e;
+    if (spare.empty()) {
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    } else {
+      e = spare.back();
+      spare.pop_back();
+    }
+    CK(cudaEventRecord(e, s));
+    pending[cur].push_back(e);
     pos += len;
     sp += len;
     dp += len;
@@ -541,22 +599,37 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
 
   std::vector<std::pair<int, int>> pairs;
   std::vector<uint8_t> alive_mem;  // survivors of the previous level, per member position
+  try {
   for (int lev = 0; lev <= sp.L; ++lev) {
     auto tp = clk::now();
     const auto t_level0 = tp;
     F->levels.push_back(std::make_unique<LevelRT>());
     LevelRT& L = *F->levels.back();
     LevelRT* prev = lev > 0 ? F->levels[lev - 1].get() : nullptr;
-    if (lev == 0) {
-      L.plan.grp = classify_all(sp);
-      DBG("level 0: classified");
-      pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.get(), A.h_col.get());
+    // level 0 is planned on the device when its cells take the one-CTA path (gpu_plan.cu;
+    // PHIF_HOST_PLAN=1 forces the host planner)
+    static const bool host_plan = getenv("PHIF_HOST_PLAN") != nullptr;
+    DevPlan0 dp;
+    if (lev == 0 && !host_plan && gpu_plan0_applicable(sp, BIG_CELL)) {
+      plan_level0_device(sp, A.rowptr.as<int64_t>(), A.col.as<int>(), A.nnz, L.plan, dp, s);
+      DBG("level 0: planned on the device G=%d blocks=%lld", L.plan.grp.G, (long long)dp.nblocks);
     } else {
-      L.plan.grp = classify_next(sp, prev->plan.grp, alive_mem);
-      pairs = pattern_next(prev->plan, L.plan.grp);
+      if (lev == 0) {
+        L.plan.grp = classify_all(sp);
+        DBG("level 0: classified");
+        pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.get(), A.h_col.get());
+      } else {
+        L.plan.grp = classify_next(sp, prev->plan.grp, alive_mem);
+        pairs = pattern_next(prev->plan, L.plan.grp);
+      }
+      DBG("level %d: grouped G=%d", lev, L.plan.grp.G);
+      build_level(sp, L.plan, std::move(pairs));
     }
-    DBG("level %d: grouped G=%d", lev, L.plan.grp.G);
-    build_level(sp, L.plan, std::move(pairs));
+    // device copy of a plan array: taken over from the device planner, else uploaded
+    auto dev_arr = [&](DBuf& dst, DBuf& from, const auto& host) {
+      if (dp.valid) dst = std::move(from);
+      else upload(dst, host, s);
+    };
     DBG("level %d: planned blocks=%zu pool=%lld", lev, L.plan.pat.bg.size(), (long long)L.plan.pool_doubles);
     const LevelPlan& P = L.plan;
     const Groups& G = P.grp;
@@ -715,7 +788,20 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     });
     // ---------------- device structures ----------------
     DBG("level %d: rec=%lld", lev, (long long)rec);
-    upload_structure(L, s);
+    if (dp.valid) {
+      L.goff = std::move(dp.goff);
+      L.mem = std::move(dp.mem);
+      L.gsize = std::move(dp.gsize);
+      L.boff = std::move(dp.boff);
+      L.bg = std::move(dp.bg);
+      L.bh = std::move(dp.bh);
+      L.adj_off = std::move(dp.adj_off);
+      L.adj_nbr = std::move(dp.adj_nbr);
+      L.adj_blk = std::move(dp.adj_blk);
+      L.diag_blk = std::move(dp.diag_blk);
+    } else {
+      upload_structure(L, s);
+    }
     DBG("level %d: structure uploaded", lev);
     L.pool.alloc(std::max<int64_t>(P.pool_doubles, 1) * sizeof(double), s, /*zero=*/true);
     if (debug_on()) cudaStreamSynchronize(s);
@@ -791,13 +877,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     if (timing) CK(cudaEventRecord(ev[1], s));
     DBG("level %d: ingest/repack done", lev);
     // ---------------- stage 1: cell elimination ----------------
-    upload(L.c_interior, P.interior, s);
-    upload(L.c_nbr_off, P.cell_nbr_off, s);
-    upload(L.c_nbr_blk, P.cell_nbr_blk, s);
-    upload(L.c_nbr_col, P.cell_nbr_col, s);
-    upload(L.c_nbr_w, nbr_w, s);
-    upload(L.c_n, P.cell_n, s);
-    upload(L.c_b, P.cell_b, s);
+    dev_arr(L.c_interior, dp.interior, P.interior);
+    dev_arr(L.c_nbr_off, dp.cell_nbr_off, P.cell_nbr_off);
+    dev_arr(L.c_nbr_blk, dp.cell_nbr_blk, P.cell_nbr_blk);
+    dev_arr(L.c_nbr_col, dp.cell_nbr_col, P.cell_nbr_col);
+    dev_arr(L.c_nbr_w, dp.cell_nbr_w, nbr_w);
+    dev_arr(L.c_n, dp.cell_n, P.cell_n);
+    dev_arr(L.c_b, dp.cell_b, P.cell_b);
     upload(L.c_P_off, P_off, s);
     upload(L.c_U_off, U_off, s);
     upload(L.c_I_off, I_off, s);
@@ -849,11 +935,11 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     check_status(*F, lev, P.root ? ST_ROOT : ST_ELIMINATE);
     DBG("level %d: cells done", lev);
     DBuf tb, to, cc, cr, ccol;
-    upload(tb, P.tgt_blk, s);
-    upload(to, P.tgt_off, s);
-    upload(cc, P.con_cell, s);
-    upload(cr, P.con_row, s);
-    upload(ccol, P.con_col, s);
+    dev_arr(tb, dp.tgt_blk, P.tgt_blk);
+    dev_arr(to, dp.tgt_off, P.tgt_off);
+    dev_arr(cc, dp.con_cell, P.con_cell);
+    dev_arr(cr, dp.con_row, P.con_row);
+    dev_arr(ccol, dp.con_col, P.con_col);
     SchurArgs sa;
     sa.ntgt = (int)P.tgt_blk.size();
     sa.tgt_blk = tb.as<int>();
@@ -881,10 +967,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       break;
     }
     // ---------------- stage 2: block Jacobi ----------------
-    upload(L.p_groups, P.precond, s);
+    dev_arr(L.p_groups, dp.precond, P.precond);
     upload(L.p_L_off, L_off, s);
     upload(L.p_L_off_of_group, Lg_off, s);
-    upload(L.p_scale_blk, P.scale_blk, s);
+    dev_arr(L.p_scale_blk, dp.scale_blk, P.scale_blk);
     upload(L.p_n, pn, s);
     upload(L.p_I_off, pI_off, s);
     upload(L.p_work_off, pwork, s);
@@ -999,10 +1085,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     if (timing) CK(cudaEventRecord(ev[7], s));
     // ---------------- stage 3: skeletonization ----------------
-    upload(L.s_groups, P.skeleton, s);
-    upload(L.s_nbr_off, P.sk_nbr_off, s);
-    upload(L.s_nbr, P.sk_nbr, s);
-    upload(L.s_nbr_blk, P.sk_nbr_blk, s);
+    dev_arr(L.s_groups, dp.skeleton, P.skeleton);
+    dev_arr(L.s_nbr_off, dp.sk_nbr_off, P.sk_nbr_off);
+    dev_arr(L.s_nbr, dp.sk_nbr, P.sk_nbr);
+    dev_arr(L.s_nbr_blk, dp.sk_nbr_blk, P.sk_nbr_blk);
     upload(L.s_order, P.wave_order, s);
     L.s_rank.alloc(std::max(nsk, 1) * sizeof(int), s, true);
     L.s_rows.alloc(std::max(nsk, 1) * sizeof(int), s, true);
@@ -1058,9 +1144,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     if (nsk && !any_large && !no_dyn) {
       // only small separators: one persistent dependency-driven launch instead of per-wave launches
       DBuf nd, so, sc, done, next;
-      upload(nd, P.sk_ndep, s);
-      upload(so, P.sk_succ_off, s);
-      upload(sc, P.sk_succ, s);
+      dev_arr(nd, dp.sk_ndep, P.sk_ndep);
+      dev_arr(so, dp.sk_succ_off, P.sk_succ_off);
+      dev_arr(sc, dp.sk_succ, P.sk_succ);
       done.alloc(std::max(nsk, 1) * sizeof(int), s, true);
       next.alloc(sizeof(int), s, true);
       DynSched ds;
@@ -1517,6 +1603,17 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       cudaEventElapsedTime(&a, ev[9], ev[10]); L.t_ms[4] = a;
     }
   }
+  } catch (NotSpd& e) {
+    // partial statistics: the levels completed before the failing one (errors.py:21-30)
+    cudaStreamSynchronize(s);
+    while ((int)F->levels.size() > e.level) F->levels.pop_back();
+    F->t_factor_ms = ms_since(t_start);
+    F->t_plan_ms = plan_ms;
+    e.partial = F->stats_json();
+    if (timing)
+      for (auto& ev1 : ev) cudaEventDestroy(ev1);
+    throw;
+  }
   CK(cudaStreamSynchronize(s));
   F->t_factor_ms = ms_since(t_start);
   for (auto& lvp : F->levels) {
@@ -1968,16 +2065,18 @@ void apply(Factorization& F, double* x, int k, int mode) {
 // true residual every 50 iterations, BreakdownError on non-finite values.
 // ---------------------------------------------------------------------------
 PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int k, double tol, int maxit,
-              cudaStream_t s) {
+              cudaStream_t s, bool want_history) {
+  // The per-column scalars, convergence flags and the residual history stay on the device; the
+  // host reads two integers per iteration (active columns, breakdown) to stop the loop.
   const int64_t N = A.N;
   const size_t vb = (size_t)N * k * sizeof(double);
-  DBuf R, Z, Pv, Q, part, sc;
+  DBuf R, Z, Pv, Q, part, sc, ctlb, hist;
   R.alloc(vb, s);
   Z.alloc(vb, s);
   Pv.alloc(vb, s);
   Q.alloc(vb, s);
   part.alloc((size_t)dot_part_blocks() * k * sizeof(double), s);
-  sc.alloc(8 * (size_t)k * sizeof(double), s);
+  sc.alloc(10 * (size_t)k * sizeof(double), s);
   double* rz = sc.as<double>();
   double* pq = rz + k;
   double* alpha = pq + k;
@@ -1985,30 +2084,28 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
   double* rn2 = beta + k;
   double* rzn = rn2 + k;
   double* bn2 = rzn + k;
-  DBuf act;
-  act.alloc(k * sizeof(int), s);
+  double* bn = bn2 + k;
+  double* relres = bn + k;
+  ctlb.alloc((3 * (size_t)k + 2) * sizeof(int), s);
+  int* ctl = ctlb.as<int>();
+  int* act = ctl + 2;
+  int* iters = act + k;
+  int* conv = iters + k;
+  if (want_history && maxit > 0) hist.alloc((size_t)maxit * k * sizeof(double), s);
+  double* hp = want_history && maxit > 0 ? hist.as<double>() : nullptr;
   const int64_t* rp = A.rowptr.as<int64_t>();
   const int* ci = A.col.as<int>();
   const double* va = A.val.as<double>();
   PcgResult res;
-  res.iters.assign(k, 0);
-  res.relres.assign(k, 1.0);
-  res.converged.assign(k, 0);
-  std::vector<int> active(k, 1);
-  std::vector<double> h_bn(k), h_rn(k), h_al(k), h_be(k);
+  int hctl[2] = {0, 0};
+  auto read_ctl = [&]() {
+    CK(cudaMemcpyAsync(hctl, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  };
   CK(cudaMemsetAsync(x, 0, vb, s));
   CK(cudaMemcpyAsync(R.p, b, vb, cudaMemcpyDeviceToDevice, s));
   launch_dot(b, b, N, k, part.as<double>(), bn2, s);
-  CK(cudaMemcpyAsync(h_bn.data(), bn2, k * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  for (int c = 0; c < k; ++c) {
-    h_bn[c] = std::sqrt(h_bn[c]);
-    if (h_bn[c] == 0.0) {
-      active[c] = 0;
-      res.relres[c] = 0.0;
-      res.converged[c] = 1;
-    }
-  }
+  launch_pcg_init(bn2, bn, act, relres, iters, conv, ctl, k, s);
   auto precond = [&](double* dst, const double* src) {
     CK(cudaMemcpyAsync(dst, src, vb, cudaMemcpyDeviceToDevice, s));
     if (F) apply(*F, dst, k, 0);
@@ -2016,58 +2113,42 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
   precond(Z.as<double>(), R.as<double>());
   CK(cudaMemcpyAsync(Pv.p, Z.p, vb, cudaMemcpyDeviceToDevice, s));
   launch_dot(R.as<double>(), Z.as<double>(), N, k, part.as<double>(), rz, s);
+  read_ctl();
   int it = 0;
-  auto all_done = [&]() {
-    for (int c = 0; c < k; ++c)
-      if (active[c]) return false;
-    return true;
-  };
-  while (!all_done() && it < maxit) {
+  while (hctl[0] > 0 && it < maxit) {
     ++it;
-    CK(cudaMemcpyAsync(act.p, active.data(), k * sizeof(int), cudaMemcpyHostToDevice, s));
     launch_spmv(rp, ci, va, Pv.as<double>(), Q.as<double>(), N, k, s);
     launch_dot(Pv.as<double>(), Q.as<double>(), N, k, part.as<double>(), pq, s);
-    launch_ratio(rz, pq, act.as<int>(), alpha, k, s);
-    launch_axpy(x, Pv.as<double>(), alpha, 1.0, act.as<int>(), N, k, s);
-    if (it % 50 == 0) {
+    launch_pcg_alpha(rz, pq, act, alpha, ctl, it, k, s);
+    launch_axpy(x, Pv.as<double>(), alpha, 1.0, act, N, k, s);
+    if (it % 50 == 0) {   // true residual
       launch_spmv(rp, ci, va, x, Q.as<double>(), N, k, s);
-      launch_sub(R.as<double>(), b, Q.as<double>(), act.as<int>(), N, k, s);
+      launch_sub(R.as<double>(), b, Q.as<double>(), act, N, k, s);
     } else {
-      launch_axpy(R.as<double>(), Q.as<double>(), alpha, -1.0, act.as<int>(), N, k, s);
+      launch_axpy(R.as<double>(), Q.as<double>(), alpha, -1.0, act, N, k, s);
     }
     launch_dot(R.as<double>(), R.as<double>(), N, k, part.as<double>(), rn2, s);
-    CK(cudaMemcpyAsync(h_rn.data(), rn2, k * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(h_al.data(), alpha, k * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (int c = 0; c < k; ++c) {
-      if (!active[c]) continue;
-      const double rr = std::sqrt(h_rn[c]) / h_bn[c];
-      if (!std::isfinite(h_al[c]) || !std::isfinite(rr)) {
-        res.breakdown = it;
-        return res;
-      }
-      res.relres[c] = rr;
-      res.iters[c] = it;
-      if (rr <= tol) {
-        active[c] = 0;
-        res.converged[c] = 1;
-      }
-    }
-    if (all_done()) break;
-    CK(cudaMemcpyAsync(act.p, active.data(), k * sizeof(int), cudaMemcpyHostToDevice, s));
+    launch_pcg_check(rn2, bn, act, relres, iters, conv, hp, it, tol, ctl, k, s);
+    read_ctl();
+    if (hctl[1]) break;
+    if (hctl[0] == 0) break;
     precond(Z.as<double>(), R.as<double>());
     launch_dot(R.as<double>(), Z.as<double>(), N, k, part.as<double>(), rzn, s);
-    launch_ratio(rzn, rz, act.as<int>(), beta, k, s);
-    CK(cudaMemcpyAsync(h_be.data(), beta, k * sizeof(double), cudaMemcpyDeviceToHost, s));
-    launch_xpby(Pv.as<double>(), Z.as<double>(), beta, act.as<int>(), N, k, s);
-    // rz <- rzn for active columns (inactive columns keep rz; unused afterwards)
-    CK(cudaMemcpyAsync(rz, rzn, k * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(cudaStreamSynchronize(s));
-    for (int c = 0; c < k; ++c)
-      if (active[c] && !std::isfinite(h_be[c])) {
-        res.breakdown = it;
-        return res;
-      }
+    launch_pcg_beta(rzn, rz, act, beta, ctl, it, k, s);
+    launch_xpby(Pv.as<double>(), Z.as<double>(), beta, act, N, k, s);
+  }
+  if (!hctl[1] && it > 0) read_ctl();   // (a breakdown flagged by the last beta)
+  res.breakdown = hctl[1];
+  res.iters.resize(k);
+  res.relres.resize(k);
+  res.converged.resize(k);
+  CK(cudaMemcpyAsync(res.iters.data(), iters, k * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(res.relres.data(), relres, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(res.converged.data(), conv, k * sizeof(int), cudaMemcpyDeviceToHost, s));
+  res.history_len = hp ? it : 0;
+  if (hp && it > 0) {
+    res.history.resize((size_t)it * k);
+    CK(cudaMemcpyAsync(res.history.data(), hp, (size_t)it * k * sizeof(double), cudaMemcpyDeviceToHost, s));
   }
   CK(cudaStreamSynchronize(s));
   return res;
@@ -2076,8 +2157,9 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
 // ---------------------------------------------------------------------------
 // e_s = ||I - G^-1 A G^-T||_2 by power iteration
 // ---------------------------------------------------------------------------
-// power iteration ||op||_2 from the host start vector x0 (oracle/diagnostics.py power_norm):
-// est = ||op(x)||, x <- op(x)/est, stop when |est - prev| / est <= rel_tol
+// power iteration ||op||_2 of a symmetric op from the host start vector x0 (oracle/diagnostics.py
+// power_norm): x unit, y = op(x), estimate = |x^T y| (Rayleigh quotient),
+// x <- y / ||y||; converged when successive Rayleigh quotients agree to rel_tol
 template <typename Op>
 static PowerResult power_norm_dev(int64_t N, cudaStream_t s, const double* x0, double rel_tol, int maxit, Op op) {
   DBuf X, Y, part, sc;
@@ -2086,6 +2168,7 @@ static PowerResult power_norm_dev(int64_t N, cudaStream_t s, const double* x0, d
   part.alloc(dot_part_blocks() * sizeof(double), s);
   sc.alloc(4 * sizeof(double), s);
   double* nrm2 = sc.as<double>();
+  double* rq = nrm2 + 1;
   CK(cudaMemcpyAsync(X.p, x0, N * sizeof(double), cudaMemcpyHostToDevice, s));
   launch_dot(X.as<double>(), X.as<double>(), N, 1, part.as<double>(), nrm2, s);
   launch_scale(X.as<double>(), X.as<double>(), nrm2, N, s);
@@ -2093,20 +2176,22 @@ static PowerResult power_norm_dev(int64_t N, cudaStream_t s, const double* x0, d
   double prev = -1.0;
   for (int it = 1; it <= maxit; ++it) {
     op(X.as<double>(), Y.as<double>());
+    launch_dot(X.as<double>(), Y.as<double>(), N, 1, part.as<double>(), rq, s);   // Rayleigh quotient x^T op x
     launch_dot(Y.as<double>(), Y.as<double>(), N, 1, part.as<double>(), nrm2, s);
-    double h;
-    CK(cudaMemcpyAsync(&h, nrm2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    double h[2];
+    CK(cudaMemcpyAsync(h, nrm2, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const double est = std::sqrt(h);
+    const double est = std::fabs(h[1]);
     pr.iters = it;
     pr.value = est;
-    if (est == 0.0) {
+    if (h[0] == 0.0) {
+      pr.value = 0.0;
       pr.converged = 1;
       pr.rel = 0.0;
       return pr;
     }
     if (prev >= 0.0) {
-      pr.rel = std::fabs(est - prev) / est;
+      pr.rel = est > 0.0 ? std::fabs(est - prev) / est : std::fabs(est - prev);
       if (pr.rel <= rel_tol) {
         pr.converged = 1;
         return pr;
@@ -2159,49 +2244,15 @@ int root_factor(Factorization& F, double* out) {
 PowerResult solve_error(const Matrix& A, Factorization& F, const double* x0, double rel_tol, int maxit) {
   cudaStream_t s = F.stream;
   const int64_t N = A.N;
-  DBuf X, Y, T, part, sc;
-  X.alloc(N * sizeof(double), s);
-  Y.alloc(N * sizeof(double), s);
+  DBuf T;
   T.alloc(N * sizeof(double), s);
-  part.alloc(dot_part_blocks() * sizeof(double), s);
-  sc.alloc(4 * sizeof(double), s);
-  double* nrm2 = sc.as<double>();
-  CK(cudaMemcpyAsync(X.p, x0, N * sizeof(double), cudaMemcpyHostToDevice, s));
-  launch_dot(X.as<double>(), X.as<double>(), N, 1, part.as<double>(), nrm2, s);
-  launch_scale(X.as<double>(), X.as<double>(), nrm2, N, s);
-  PowerResult pr;
-  double prev = -1.0, est = 0.0;
-  for (int it = 1; it <= maxit; ++it) {
-    CK(cudaMemcpyAsync(T.p, X.p, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return power_norm_dev(N, s, x0, rel_tol, maxit, [&](double* X, double* Y) {
+    CK(cudaMemcpyAsync(T.p, X, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     apply(F, T.as<double>(), 1, 2);   // G^-T x
-    launch_spmv(A.rowptr.as<int64_t>(), A.col.as<int>(), A.val.as<double>(), T.as<double>(), Y.as<double>(), N,
-                1, s);
-    apply(F, Y.as<double>(), 1, 1);   // G^-1 A G^-T x
-    launch_xmy(Y.as<double>(), X.as<double>(), N, s);
-    launch_dot(Y.as<double>(), Y.as<double>(), N, 1, part.as<double>(), nrm2, s);
-    double h;
-    CK(cudaMemcpyAsync(&h, nrm2, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    est = std::sqrt(h);
-    pr.iters = it;
-    pr.value = est;
-    if (est == 0.0) {
-      pr.converged = 1;
-      pr.rel = 0.0;
-      return pr;
-    }
-    if (prev >= 0.0) {
-      const double rel = std::fabs(est - prev) / est;
-      pr.rel = rel;
-      if (rel <= rel_tol) {
-        pr.converged = 1;
-        return pr;
-      }
-    }
-    prev = est;
-    launch_scale(X.as<double>(), Y.as<double>(), nrm2, N, s);
-  }
-  return pr;
+    launch_spmv(A.rowptr.as<int64_t>(), A.col.as<int>(), A.val.as<double>(), T.as<double>(), Y, N, 1, s);
+    apply(F, Y, 1, 1);                // G^-1 A G^-T x
+    launch_xmy(Y, X, N, s);           // x - G^-1 A G^-T x
+  });
 }
 
 std::string Factorization::stats_json() const {
@@ -2227,8 +2278,9 @@ std::string Factorization::stats_json() const {
       << "," << L.fl[2] << "," << L.fl[3] << "," << L.fl[4] << "],\"bytes\":[" << L.by[0] << "," << L.by[1] << ","
       << L.by[2] << "," << L.by[3] << "," << L.by[4] << "]}";
   }
-  const LevelRT& R = *levels.back();
-  o << "],\"SL\":" << (R.plan.interior.empty() ? 0 : R.plan.cell_n[0]) << "}";
+  const bool done = !levels.empty() && levels.back()->plan.root;
+  o << "],\"SL\":" << (done && !levels.back()->plan.interior.empty() ? levels.back()->plan.cell_n[0] : 0)
+    << ",\"complete\":" << (done ? "true" : "false") << "}";
   return o.str();
 }
 

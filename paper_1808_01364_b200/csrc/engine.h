@@ -20,6 +20,7 @@ struct CudaError : std::runtime_error {
 
 struct NotSpd : std::runtime_error {
   int pivot, level, stage, group;
+  std::string partial;   // stats JSON of the levels completed before the failure
   NotSpd(int p, int l, int s, int g)
       : std::runtime_error("not SPD"), pivot(p), level(l), stage(s), group(g) {}
 };
@@ -142,10 +143,12 @@ struct PcgResult {
   std::vector<int> iters;
   std::vector<double> relres;
   std::vector<int> converged;
+  std::vector<double> history;   // history_len x k relative residuals (row per iteration)
+  int history_len = 0;
   int breakdown = 0;
 };
 PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int k, double tol, int maxit,
-              cudaStream_t s);
+              cudaStream_t s, bool want_history = false);
 struct PowerResult {
   double value = 0.0;
   int iters = 0;

@@ -24,9 +24,10 @@
 // it owns and pushes them to every CTA through distributed shared memory).
 
 struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
-  // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][rdv, invv: 2k][64] doubles, then 3k ints
+  // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][rdv, invv: 2k][96] doubles, then 3k ints
+  // (the 96: argmax scratch, two mbarriers, and 2 x 16 step-token slots of the row exchange)
   __host__ __device__ static int64_t doubles(int64_t sreg, int k, int nb) {
-    return sreg + (int64_t)(nb + 7) * k + 64;
+    return sreg + (int64_t)(nb + 7) * k + 96;
   }
   __host__ __device__ static size_t bytes(int64_t sreg, int k, int nb) {
     return (size_t)doubles(sreg, k, nb) * sizeof(double) + 3 * (size_t)k * sizeof(int);
@@ -261,9 +262,10 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   double* rowbuf = vn2 + k;                 // 2 x k receive buffers (step parity)
   double* rdv = rowbuf + 2 * (int64_t)k;    // sqrt(Schur diagonal) and its reciprocal per column,
   double* invv = rdv + k;                   // formed off the pivot chain in the downdate loop
-  double* sred = invv + k;                  // 64 (sred[48..49]: the two mbarriers)
+  double* sred = invv + k;                  // 96 (sred[48..49]: the two mbarriers, [64..95] tokens)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sred + 48);
-  int* col_at = reinterpret_cast<int*>(sred + 64);
+  double* tok = sred + 64;                  // tok[q * 16 + src]: step tokens (never read)
+  int* col_at = reinterpret_cast<int*>(sred + 96);
   int* piv = col_at + k;
   int* sidx = piv + k;
   const int nown = c < k ? (k - c + C - 1) / C : 0;
@@ -308,7 +310,15 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   if (C > 1) cluster_barrier();   // G read, mbarriers initialised cluster-wide
   else __syncthreads();
   GID_MARK(0)
-  const uint32_t rb_addr = smem_addr(rowbuf), bar_addr = smem_addr(mbar);
+  const uint32_t rb_addr = smem_addr(rowbuf), bar_addr = smem_addr(mbar), tok_addr = smem_addr(tok);
+  // Back-pressure of the row exchange: besides its row entries, every CTA pushes one 8-byte token
+  // per step to every CTA (also when none of its columns is still active), and every receiver
+  // expects 8 (k - i - 1) + 8 C bytes. A CTA therefore completes step i + 1 only after every
+  // peer has issued its step-(i + 1) pushes, i.e. after every peer has finished reading its own
+  // step-i row buffer, so no CTA runs more than one step ahead: the step-(i + 2) pushes into
+  // buffer parity q can never land while a peer still reads that buffer for step i.
+  const uint32_t tok_dst = (C > 1 && tid < C) ? mapa_u32(tok_addr, (unsigned)tid) : 0u;
+  const uint32_t tokbar_dst = (C > 1 && tid < C) ? mapa_u32(bar_addr, (unsigned)tid) : 0u;
   // threads per owned column in the row-entry step (power of two, nown <= NT / tpc when possible;
   // tpc >= C / 4 so every thread pushes to at most 4 destinations)
   int tpc = 8;
@@ -333,7 +343,7 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   for (; i < mn; ++i) {
     if (i > 0 && best.v < cut2) break;
     const int q = i & 1;
-    if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1));
+    if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1 + C));
     // pivot column (position best.i); the position swap is applied after the row exchange
     const int p = col_at[best.i];
     const double rd = rdv[p];
@@ -368,6 +378,7 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
         }
       }
     }
+    if (C > 1 && tid < C) st_async_f64(tok_dst + 8u * (uint32_t)(q * 16 + c), 0.0, tokbar_dst + 8u * q);
     GID_MARK(2)
     if (C > 1) {
       mbar_wait(mbar + q, (unsigned)((i >> 1) & 1));

@@ -3027,6 +3027,75 @@ __global__ void k_ratio(const double* num, const double* den, const int* active,
   out[c] = (active == nullptr || active[c]) ? num[c] / den[c] : 0.0;
 }
 
+// ---- PCG control on the device (one block; columns c < k) ----------------------------------
+// ctl[0] = number of still-active columns, ctl[1] = first breakdown iteration (0 = none)
+__global__ void k_pcg_init(const double* bn2, double* bn, int* active, double* relres, int* iters, int* conv,
+                           int* ctl, int k) {
+  if (threadIdx.x == 0) {
+    ctl[0] = 0;
+    ctl[1] = 0;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    const double b = sqrt(bn2[c]);
+    bn[c] = b;
+    iters[c] = 0;
+    const bool a = b != 0.0;
+    active[c] = a;
+    relres[c] = a ? 1.0 : 0.0;
+    conv[c] = a ? 0 : 1;
+    if (a) atomicAdd(ctl, 1);
+  }
+}
+
+__device__ __forceinline__ void pcg_flag_breakdown(int* ctl, int it) { atomicCAS(ctl + 1, 0, it); }
+
+// alpha = rz / pq for active columns (0 otherwise)
+__global__ void k_pcg_alpha(const double* rz, const double* pq, const int* active, double* alpha, int* ctl, int it,
+                            int k) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    const double a = active[c] ? rz[c] / pq[c] : 0.0;
+    if (!isfinite(a)) pcg_flag_breakdown(ctl, it);
+    alpha[c] = a;
+  }
+}
+
+// relative residuals, convergence, history row it-1 (every column, frozen ones keep their value)
+__global__ void k_pcg_check(const double* rn2, const double* bn, int* active, double* relres, int* iters, int* conv,
+                            double* hist, int it, double tol, int* ctl, int k) {
+  if (threadIdx.x == 0) ctl[0] = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    if (active[c]) {
+      const double rr = sqrt(rn2[c]) / bn[c];
+      if (!isfinite(rr)) pcg_flag_breakdown(ctl, it);
+      relres[c] = rr;
+      iters[c] = it;
+      if (rr <= tol) {
+        active[c] = 0;
+        conv[c] = 1;
+      } else {
+        atomicAdd(ctl, 1);
+      }
+    }
+    if (hist) hist[(int64_t)(it - 1) * k + c] = relres[c];
+  }
+}
+
+// beta = rzn / rz and rz <- rzn for active columns
+__global__ void k_pcg_beta(const double* rzn, double* rz, const int* active, double* beta, int* ctl, int it, int k) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    if (active[c]) {
+      const double b = rzn[c] / rz[c];
+      if (!isfinite(b)) pcg_flag_breakdown(ctl, it);
+      beta[c] = b;
+      rz[c] = rzn[c];
+    } else {
+      beta[c] = 0.0;
+    }
+  }
+}
+
 // y = x - y (power iteration residual), y /= scale handled by k_scale
 __global__ void k_xmy(double* y, const double* x, int64_t n) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -3509,6 +3578,27 @@ void launch_xpby(double* p, const double* z, const double* coef, const int* acti
 void launch_sub(double* r, const double* b, const double* q, const int* active, int64_t N, int k, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_sub<<<nblk(N * k, 256), 256, 0, s>>>(r, b, q, active, N, k);
+}
+static int ctl_threads(int k) { return std::min(1024, 32 * ((k + 31) / 32)); }
+void launch_pcg_init(const double* bn2, double* bn, int* active, double* relres, int* iters, int* conv, int* ctl,
+                     int k, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_pcg_init<<<1, ctl_threads(k), 0, s>>>(bn2, bn, active, relres, iters, conv, ctl, k);
+}
+void launch_pcg_alpha(const double* rz, const double* pq, const int* active, double* alpha, int* ctl, int it, int k,
+                      cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_pcg_alpha<<<1, ctl_threads(k), 0, s>>>(rz, pq, active, alpha, ctl, it, k);
+}
+void launch_pcg_check(const double* rn2, const double* bn, int* active, double* relres, int* iters, int* conv,
+                      double* hist, int it, double tol, int* ctl, int k, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_pcg_check<<<1, ctl_threads(k), 0, s>>>(rn2, bn, active, relres, iters, conv, hist, it, tol, ctl, k);
+}
+void launch_pcg_beta(const double* rzn, double* rz, const int* active, double* beta, int* ctl, int it, int k,
+                     cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_pcg_beta<<<1, ctl_threads(k), 0, s>>>(rzn, rz, active, beta, ctl, it, k);
 }
 void launch_ratio(const double* num, const double* den, const int* active, double* out, int k, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);

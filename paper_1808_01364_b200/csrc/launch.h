@@ -114,6 +114,14 @@ void launch_axpy(double* y, const double* x, const double* coef, double sgn, con
 void launch_xpby(double* p, const double* z, const double* coef, const int* active, int64_t N, int k,
                  cudaStream_t s);
 void launch_sub(double* r, const double* b, const double* q, const int* active, int64_t N, int k, cudaStream_t s);
+void launch_pcg_init(const double* bn2, double* bn, int* active, double* relres, int* iters, int* conv, int* ctl,
+                     int k, cudaStream_t s);
+void launch_pcg_alpha(const double* rz, const double* pq, const int* active, double* alpha, int* ctl, int it, int k,
+                      cudaStream_t s);
+void launch_pcg_check(const double* rn2, const double* bn, int* active, double* relres, int* iters, int* conv,
+                      double* hist, int it, double tol, int* ctl, int k, cudaStream_t s);
+void launch_pcg_beta(const double* rzn, double* rz, const int* active, double* beta, int* ctl, int it, int k,
+                     cudaStream_t s);
 void launch_ratio(const double* num, const double* den, const int* active, double* out, int k, cudaStream_t s);
 void launch_xmy(double* y, const double* x, int64_t n, cudaStream_t s);
 void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cudaStream_t s);

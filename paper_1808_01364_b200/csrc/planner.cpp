@@ -202,6 +202,15 @@ Groups classify_set(const Spec& s, int level, const std::vector<int>& active) {
 }
 
 Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_t>& alive) {
+  const bool tdbg = getenv("PHIF_PLAN_TIMING") != nullptr;
+  auto tl = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!tdbg) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "  [classify_next L%d] %-20s %8.2f ms\n", prev.level + 1, what,
+            std::chrono::duration<double, std::milli>(now - tl).count());
+    tl = now;
+  };
   // Every surviving DOF of an old group lands in the same new group (the old group's
   // on-line axes stay on-line iff their line index is even; free coordinates stay inside
   // the same cell), so the new grouping is a bucket sort of old groups by their new key
@@ -229,6 +238,7 @@ Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_
       okey[pg] = key_of(s, g.level, prev.mem[first], q, b);
     }
   }
+  lap("survivors + keys");
   // bucket old groups by new key (stable: ascending old group index)
   std::vector<int64_t> kcnt(nkeys + 1, 0);
   for (int pg = 0; pg < prev.G; ++pg)
@@ -253,6 +263,7 @@ Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_
     }
   gsrc_off.push_back(kcnt[nkeys]);
   moff.push_back(total);
+  lap("bucket");
   const int G = (int)gkeys.size();
   g.off = moff;
   g.mem.resize(total);
@@ -283,7 +294,9 @@ Groups classify_next(const Spec& s, const Groups& prev, const std::vector<uint8_
       }
     }
   }
+  lap("merge members");
   finalize_groups(s, g, {}, gkeys);
+  lap("finalize");
   return g;
 }
 

@@ -2,7 +2,8 @@
 
 * power_norm(op, dim, rel_tol=1e-2, maxit=200, seed)  generic host-callback power iteration
   (SPEC.md:400-404): unit start vector from default_rng(seed).standard_normal(dim),
-  estimate ||op(x)||, converged when two successive estimates agree to rel_tol.
+  estimate |x^T op(x)| (Rayleigh quotient), converged when two successive Rayleigh
+  quotients agree to rel_tol.
 * estimate_solve_error(A, Fz)   e_s = ||I - G^-1 A G^-T||, run
   entirely on the device: G^-T, SpMV, G^-1 per iteration through the C-ABI, with the
   same start vector and stopping rule as power_norm.
@@ -34,16 +35,18 @@ def power_norm(op, dim, rel_tol=1e-2, maxit=200, seed=0) -> NormEstimate:
     prev, est = None, 0.0
     for it in range(1, maxit + 1):
         y = np.asarray(op(x), dtype=np.float64)
-        est = float(np.linalg.norm(y))
-        if est == 0.0:
+        est = abs(float(x @ y))              # Rayleigh quotient of the unit iterate
+        ny = float(np.linalg.norm(y))
+        if ny == 0.0:
             return NormEstimate(0.0, it, True, 0.0)
         if prev is not None:
-            rel = abs(est - prev) / est
+            rel = abs(est - prev) / est if est > 0.0 else abs(est - prev)
             if rel <= rel_tol:
                 return NormEstimate(est, it, True, rel)
         prev = est
-        x = y / est
-    return NormEstimate(est, maxit, False, abs(est - prev) / est if prev else float("inf"))
+        x = y / ny
+    rel = (abs(est - prev) / est if est > 0.0 else abs(est - prev)) if prev is not None else float("inf")
+    return NormEstimate(est, maxit, False, rel)
 
 
 def estimate_solve_error(A, Fz: Factorization, rel_tol=1e-2, maxit=200, seed=(0, 13)) -> NormEstimate:

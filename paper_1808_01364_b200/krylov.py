@@ -5,7 +5,9 @@ grid.py:288-292. Standard PCG per right-hand-side column with F^-1 from the B200
 factorization, stop on ||r||/||b|| <= tol, true residual every 50 iterations,
 BreakdownError on a non-finite recurrence value, maxit flagged in the report with
 the partial x returned. Converged columns are frozen so a block of right-hand
-sides behaves like independent single-RHS solves.
+sides behaves like independent single-RHS solves. SolveReport.history holds the
+relative residual after every iteration (a float per iteration for
+one right-hand side, an array per iteration for a block).
 """
 
 from __future__ import annotations
@@ -44,12 +46,15 @@ def pcg(A, b, precond: Factorization | None = None, tol: float = 1e-12, maxit: i
     iters = np.zeros(k, dtype=np.int32)
     relres = np.zeros(k, dtype=np.float64)
     conv = np.zeros(k, dtype=np.int32)
+    hist = np.zeros((max(int(maxit), 1), k), dtype=np.float64)
+    nh = C.c_int(0)
     err = _lib.phif_error()
     rc = _lib.lib().phif_pcg(dm.handle, precond.handle if precond is not None else None, _lib.ptr(B),
                              _lib.ptr(X), k, float(tol), int(maxit), C.c_void_p(stream or 0), _lib.ptr(iters),
-                             _lib.ptr(relres), _lib.ptr(conv), C.byref(err))
+                             _lib.ptr(relres), _lib.ptr(conv), _lib.ptr(hist), C.byref(nh), C.byref(err))
     _lib.raise_for(rc, err)
+    history = [float(h[0]) if flat else h.copy() for h in hist[:nh.value]]
     rep = SolveReport(int(iters[0]) if flat else iters.astype(np.int64),
                       float(relres[0]) if flat else relres,
-                      bool(conv[0]) if flat else conv.astype(bool), [], time.perf_counter() - t0)
+                      bool(conv[0]) if flat else conv.astype(bool), history, time.perf_counter() - t0)
     return (X[:, 0] if flat else X), rep

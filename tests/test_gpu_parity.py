@@ -204,3 +204,62 @@ def test_apply_error_and_root_condition(name, make, method, eps, tol):
     ko = ophif.root_condition(Fo)
     kg = gfac.root_condition(Fg)
     assert abs(kg - ko) <= 1e-8 * ko
+
+
+_GID_DUMP = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+from paper_1808_01364_b200 import factorization as gfac
+from paper_1808_01364_b200.grid import baseline_problem
+spec, A, _ = baseline_problem("c5", 0, 64)
+F = gfac.factorize(A, spec, 1e-2, "phif")
+print(json.dumps({"SL": F.SL, "n_gid": sum(lv.get("n_gid", 0) for lv in F.stats["levels"]),
+                  "red": [[sorted(int(v) for v in r) for _, r in F.skeleton_sets(l)] for l in range(spec.levels)]}))
+"""
+
+
+@pytest.mark.parametrize("clusters", ["16", "2"])
+def test_gram_id_forced_cluster_matches_oracle(clusters):
+    """Gram-path ID with a forced cluster size (mixed-k waves, C=16 leaves CTAs with no
+    active columns while their peers run on): skeleton sets still equal the oracle's at c5 n=64."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PHIF_GID_C=clusters)
+    res = subprocess.run([sys.executable, "-c", _GID_DUMP, root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    assert got["n_gid"] > 0
+    spec, A = baseline_problem("c5", 0, 64)[:2]
+    Fo = ophif.factorize(A, spec, 1e-2, "phif")
+    assert got["SL"] == Fo.SL
+    for lev in range(spec.levels):
+        g = {tuple(r) for r in got["red"][lev] if r}
+        assert g == _redundant_sets(Fo, lev), f"level {lev}"
+
+
+def test_pcg_residual_history_and_partial_stats():
+    """SolveReport.history: one relative residual per iteration, matching the
+    oracle's history to the PCG tolerance scale; NotSpdError.partial_stats (errors.py:21-30) holds
+    the statistics of the levels completed before the failure."""
+    spec, A = baseline_problem("c4", 0, 32)[:2]
+    Fo = ophif.factorize(A, spec, 1e-3, "phif")
+    Fg = gfac.factorize(A, spec, 1e-3, "phif")
+    b = np.random.default_rng([0, 1]).standard_normal(A.n)
+    xo, ro = okry.pcg(A, b, precond=Fo, tol=1e-12)
+    xg, rg = gkry.pcg(A, b, precond=Fg, tol=1e-12)
+    assert len(rg.history) == rg.n_i and rg.history[-1] == pytest.approx(rg.relres)
+    m = min(len(rg.history), len(ro.history))
+    ho = np.array([float(h[0]) for h in ro.history[:m]])
+    assert np.allclose(np.array(rg.history[:m]), ho, rtol=1e-6, atol=1e-13)
+    B = np.random.default_rng([0, 2]).standard_normal((A.n, 3))
+    Xg, rb = gkry.pcg(A, B, precond=Fg, tol=1e-12)
+    assert len(rb.history) == int(np.max(rb.n_i)) and rb.history[-1].shape == (3,)
+    spec2, A2 = baseline_problem("c3", 1, 256)[:2]
+    with pytest.raises(NotSpdError) as g:
+        gfac.factorize(A2, spec2, 1e-2, "phif")
+    ps = g.value.partial_stats
+    assert ps is not None and len(ps["levels"]) == g.value.level and ps["complete"] is False
