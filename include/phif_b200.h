@@ -74,6 +74,24 @@ int phif_matrix_create(const int64_t* rowptr, const int32_t* col, const double* 
                        phif_matrix** out, phif_error* err);
 void phif_matrix_free(phif_matrix* A);
 
+/* On-device problem generation and assembly (grid.py:182-260): the nodal
+ * coefficient lattice a ((n-1)^dim values, x fastest; host or device pointer) is Gaussian-smoothed
+ * on the device with the given symmetric weights (scipy.ndimage.gaussian_filter order, reflect
+ * boundary; nweights = 0: none), thresholded to a > 0 ? hi : lo (lo = hi = 0: none), and A =
+ * -div(a grad u) + b u is assembled on the device (bh2 = b h^2) bit-identically to
+ * assemble_operator. The matrix keeps the field for the matrix-free stencil SpMV that phif_pcg and
+ * the estimators then use. */
+int phif_matrix_from_field(int dim, int n, const double* a, const double* weights, int nweights, double lo, double hi,
+                           double bh2, void* stream, phif_matrix** out, phif_error* err);
+
+/* Copy A to host arrays (any output may be NULL): *nnz, rowptr (N+1), col, val (nnz), and the
+ * coefficient field (N) of a matrix built by phif_matrix_from_field. */
+int phif_matrix_csr(const phif_matrix* A, int64_t* nnz, int64_t* rowptr, int32_t* col, double* val, double* field);
+
+/* y = A x for host arrays (N x nrhs): the engine's SpMV (matrix-free stencil when A carries its
+ * field, unless force_csr). */
+int phif_matrix_apply(const phif_matrix* A, const double* x, double* y, int nrhs, int force_csr, phif_error* err);
+
 /* factorize(A, GridSpec(dim, n, m), eps, method); timing != 0 records per-stage CUDA events. */
 int phif_factorize(const phif_matrix* A, int dim, int n, int m, double eps, int method, void* stream, int timing,
                    phif_factor** out, phif_error* err);

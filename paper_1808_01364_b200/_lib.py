@@ -27,7 +27,8 @@ STAGES = {0: "eliminate", 1: "precondition", 2: "skeletonize", 3: "root"}
 
 _lib = None
 
-EXPORTS = ("phif_version", "phif_launch_count", "phif_matrix_create", "phif_matrix_free", "phif_factorize", "phif_factor_free",
+EXPORTS = ("phif_version", "phif_launch_count", "phif_matrix_create", "phif_matrix_free", "phif_matrix_from_field",
+           "phif_matrix_csr", "phif_matrix_apply", "phif_factorize", "phif_factor_free",
            "phif_apply", "phif_pcg", "phif_solve_error", "phif_apply_error", "phif_root_factor", "phif_stats_json",
            "phif_skeleton_sets",
            "phif_num_levels", "phif_last_partial_stats", "phif_plan_check", "phif_classify", "phif_plan_dryrun")
@@ -47,6 +48,13 @@ def lib():
     L.phif_matrix_create.argtypes = [P, P, P, I64, P, C.POINTER(P), C.POINTER(phif_error)]
     L.phif_matrix_create.restype = I
     L.phif_matrix_free.argtypes = [P]
+    L.phif_matrix_from_field.argtypes = [I, I, P, P, I, C.c_double, C.c_double, C.c_double, P, C.POINTER(P),
+                                         C.POINTER(phif_error)]
+    L.phif_matrix_from_field.restype = I
+    L.phif_matrix_csr.argtypes = [P, C.POINTER(C.c_int64), P, P, P, P]
+    L.phif_matrix_csr.restype = I
+    L.phif_matrix_apply.argtypes = [P, P, P, I, I, C.POINTER(phif_error)]
+    L.phif_matrix_apply.restype = I
     L.phif_factorize.argtypes = [P, I, I, I, C.c_double, I, P, I, C.POINTER(P), C.POINTER(phif_error)]
     L.phif_factorize.restype = I
     L.phif_factor_free.argtypes = [P]

@@ -10,6 +10,7 @@ $NVCC $FLAGS -c planner.cpp -o build/planner.o
 $NVCC $FLAGS -c kernels.cu -o build/kernels.o ${PTXAS_V:+-Xptxas -v}
 $NVCC $FLAGS -c engine.cu -o build/engine.o
 $NVCC $FLAGS -c gpu_plan.cu -o build/gpu_plan.o
+$NVCC $FLAGS -c problem.cu -o build/problem.o
 $NVCC $FLAGS -c capi.cu -o build/capi.o
-$NVCC -shared -gencode arch=compute_100a,code=sm_100a -o $OUT build/planner.o build/kernels.o build/engine.o build/gpu_plan.o build/capi.o -lcudart -lgomp -Xlinker -export-dynamic
+$NVCC -shared -gencode arch=compute_100a,code=sm_100a -o $OUT build/planner.o build/kernels.o build/engine.o build/gpu_plan.o build/problem.o build/capi.o -lcudart -lgomp -Xlinker -export-dynamic
 echo "built $(realpath $OUT)"

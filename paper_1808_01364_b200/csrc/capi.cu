@@ -10,6 +10,7 @@
 #include "../../include/phif_b200.h"
 #include "engine.h"
 #include "gpu_plan.h"
+#include "problem.h"
 
 struct phif_matrix {
   std::unique_ptr<phif::Matrix> m;
@@ -101,6 +102,65 @@ int phif_matrix_create(const int64_t* rowptr, const int32_t* col, const double* 
 }
 
 void phif_matrix_free(phif_matrix* A) { delete A; }
+
+int phif_matrix_from_field(int dim, int n, const double* a, const double* weights, int nweights, double lo, double hi,
+                           double bh2, void* stream, phif_matrix** out, phif_error* err) {
+  return guarded(err, [&] {
+    if (dim < 2 || dim > 3 || n < 2) throw std::invalid_argument("phif_matrix_from_field: bad grid");
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t N = 1;
+    for (int d = 0; d < dim; ++d) N *= (n - 1);
+    phif::DBuf f;
+    f.alloc(N * sizeof(double), s);
+    if (is_device(a)) cudaMemcpyAsync(f.p, a, N * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    else phif::upload_bytes(f.p, a, N * sizeof(double), s);
+    if (nweights > 0) {
+      if (nweights % 2 != 1) throw std::invalid_argument("phif_matrix_from_field: odd number of weights expected");
+      phif::smooth_field(dim, n - 1, f.as<double>(), std::vector<double>(weights, weights + nweights), s);
+    }
+    if (lo != 0.0 || hi != 0.0) phif::threshold_field(f.as<double>(), N, lo, hi, s);
+    auto* A = new phif_matrix;
+    A->stream = s;
+    try {
+      A->m = phif::matrix_from_field(dim, n, f.as<double>(), bh2, s, false);
+    } catch (...) {
+      delete A;
+      throw;
+    }
+    *out = A;
+  });
+}
+
+int phif_matrix_csr(const phif_matrix* A, int64_t* nnz, int64_t* rowptr, int32_t* col, double* val, double* field) {
+  const phif::Matrix& M = *A->m;
+  *nnz = M.nnz;
+  if (rowptr) cudaMemcpy(rowptr, M.rowptr.p, (M.N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (col) cudaMemcpy(col, M.col.p, M.nnz * sizeof(int), cudaMemcpyDeviceToHost);
+  if (val) cudaMemcpy(val, M.val.p, M.nnz * sizeof(double), cudaMemcpyDeviceToHost);
+  if (field && M.stencil) cudaMemcpy(field, M.field.p, M.N * sizeof(double), cudaMemcpyDeviceToHost);
+  return cudaGetLastError() == cudaSuccess ? PHIF_OK : PHIF_ERROR;
+}
+
+int phif_matrix_apply(const phif_matrix* A, const double* x, double* y, int nrhs, int force_csr, phif_error* err) {
+  return guarded(err, [&] {
+    const phif::Matrix& M = *A->m;
+    cudaStream_t s = A->stream;
+    const size_t bytes = (size_t)M.N * nrhs * sizeof(double);
+    phif::DBuf dx, dy;
+    dx.alloc(bytes, s);
+    dy.alloc(bytes, s);
+    phif::upload_bytes(dx.p, x, bytes, s);
+    if (force_csr)
+      phif::launch_spmv(M.rowptr.as<int64_t>(), M.col.as<int>(), M.val.as<double>(), dx.as<double>(), dy.as<double>(),
+                        M.N, nrhs, s);
+    else
+      phif::spmv(M, dx.as<double>(), dy.as<double>(), nrhs, s);
+    phif::download_bytes(y, dy.p, bytes, s);
+    cudaStreamSynchronize(s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw phif::CudaError(cudaGetErrorString(e));
+  });
+}
 
 int phif_factorize(const phif_matrix* A, int dim, int n, int m, double eps, int method, void* stream, int timing,
                    phif_factor** out, phif_error* err) {
@@ -221,6 +281,7 @@ int phif_plan_check(const phif_matrix* A, int dim, int n, int m, char* report, s
     phif::Spec s;
     s.init(dim, n, m);
     const phif::Matrix& M = *A->m;
+    M.ensure_host_pattern(A->stream);
     phif::LevelPlan h, d;
     h.grp = phif::classify_all(s);
     phif::build_level(s, h, phif::pattern_from_csr(h.grp, s.N, M.h_rowptr.get(), M.h_col.get()));

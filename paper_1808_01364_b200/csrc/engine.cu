@@ -1,4 +1,5 @@
 #include <future>
+#include <omp.h>
 #include <mutex>
 #include <numeric>
 // Host driver: per level plan -> device structures -> batched stage launches.
@@ -18,6 +19,7 @@
 
 #include "engine.h"
 #include "gpu_plan.h"
+#include "problem.h"
 
 namespace phif {
 
@@ -219,6 +221,14 @@ std::unique_ptr<Matrix> matrix_create(const int64_t* rowptr, const int* col, con
   return A;
 }
 
+void Matrix::ensure_host_pattern(cudaStream_t s) const {
+  if (h_rowptr) return;
+  h_rowptr.reset(new int64_t[N + 1]);
+  h_col.reset(new int[std::max<int64_t>(nnz, 1)]);
+  download_bytes(h_rowptr.get(), rowptr.p, (N + 1) * sizeof(int64_t), s);
+  download_bytes(h_col.get(), col.p, nnz * sizeof(int), s);
+}
+
 namespace {
 
 using clk = std::chrono::steady_clock;
@@ -268,7 +278,8 @@ struct BigPlan {
   DBuf d_n, d_b, d_rows, d_P, d_U, d_op, d_linv, d_list;
   DBuf d_cell, d_i, d_j;
   struct Phase {
-    int kind;        // 0 diag + trsm + narrow update (one 64-wide step), 1 wide update, 2 U
+    int kind;        // 0 diag + trsm + narrow update (one 64-wide step), 1 wide update of the next
+                     // block's columns, 3 wide update beyond the next block (side stream), 2 U
     int64_t off[3], cnt[3];
     int k0, kw;
   };
@@ -340,11 +351,31 @@ struct BigPlan {
         ph.cnt[2] = (int64_t)wc.size() - ph.off[2];
         phases.push_back(ph);
       }
-      Phase wide{1, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
+      // KB-deep update of the trailing matrix, split for look-ahead: W1 = the next block's
+      // columns (stays on the main stream, the next block's steps need it), W2 = the columns
+      // beyond the next block (side stream, overlapping the next block's 64-wide chain)
+      Phase w1{1, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
       for (int c = 0; c < nbig; ++c)
-        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, n[c], kb0 + KB);
-      wide.cnt[0] = (int64_t)wc.size() - wide.off[0];
-      if (wide.cnt[0]) phases.push_back(wide);
+        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, std::min(n[c], kb0 + 2 * KB), kb0 + KB);
+      w1.cnt[0] = (int64_t)wc.size() - w1.off[0];
+      if (w1.cnt[0]) phases.push_back(w1);
+      Phase w2{3, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
+      for (int c = 0; c < nbig; ++c)
+        if (n[c] > kb0 + 2 * KB) {
+          // tiles of trailing(c, kb0 + KB, n, ..) with column tile index >= KB / T
+          const int base = kb0 + KB, kend = kb0 + KB;
+          const int nr = (rws[c] - base + T - 1) / T, nc = (n[c] - base + T - 1) / T;
+          for (int it = 0; it < nr; ++it)
+            for (int jt = KB / T; jt < nc; ++jt) {
+              if (jt > it && base + T * (it + 1) <= n[c]) continue;
+              if (zero_tile(c, base + T * it, kend)) continue;
+              wc.push_back(c);
+              wi.push_back(it);
+              wj.push_back(jt);
+            }
+        }
+      w2.cnt[0] = (int64_t)wc.size() - w2.off[0];
+      if (w2.cnt[0]) phases.push_back(w2);
     }
     Phase us{2, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, 0, 0};
     for (int c = 0; c < nbig; ++c) {
@@ -389,14 +420,51 @@ struct BigPlan {
     return a;
   }
   void run(DevStatus* st, cudaStream_t s) const {
+    // Look-ahead: the 64-wide chain (diag, trsm, narrow updates) and W1 (the next block's
+    // columns) run on a high-priority stream, W2 (the trailing columns beyond the next block) on
+    // the caller's stream; so the chain of block b+1 takes SMs as soon as W2(b)'s CTAs retire
+    // instead of queueing behind them. W1(b+1) waits for W2(b) (same C tiles).
+    static const bool lookahead = !getenv("PHIF_NO_LOOKAHEAD");
+    cudaStream_t hp = lookahead ? prio_stream() : s;
+    std::vector<cudaEvent_t> evs;
+    auto mark = [&](cudaStream_t from, cudaStream_t to) {   // `to` waits for the work issued on `from`
+      if (from == to) return;
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      CK(cudaEventRecord(e, from));
+      CK(cudaStreamWaitEvent(to, e, 0));
+    };
+    mark(s, hp);
+    bool w2_pending = false;
     for (const Phase& ph : phases) {
-      if (ph.kind == 0)
+      if (ph.kind == 0) {
         launch_big_step(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), args(ph.off[1], ph.cnt[1], ph.k0, ph.kw),
-                        args(ph.off[2], ph.cnt[2], ph.k0, ph.kw), st, s);
-      else
-        launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), ph.kind == 1 ? 0 : 1, s);
+                        args(ph.off[2], ph.cnt[2], ph.k0, ph.kw), st, hp);
+      } else if (ph.kind == 3) {
+        mark(hp, s);
+        launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), 0, s);
+        w2_pending = true;
+      } else {
+        if (w2_pending) mark(s, hp);
+        w2_pending = false;
+        launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), ph.kind == 1 ? 0 : 1, hp);
+      }
     }
+    mark(hp, s);
     if (nbig) launch_big_zero_upper(args(0, 0, 0, 0), s);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);   // (destruction is deferred until they complete)
+  }
+  static cudaStream_t prio_stream() {
+    static cudaStream_t st[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!st[dev & 15]) {
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&st[dev & 15], cudaStreamNonBlocking, hi));
+    }
+    return st[dev & 15];
   }
 };
 
@@ -579,6 +647,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
                                          cudaStream_t s, bool timing) {
   configure_kernels();
   keep_pool_memory();
+  // the planner's OpenMP teams leave two cores to the helper threads (boundary reduction lists,
+  // staging copies): a statically scheduled team waiting on a preempted thread stalls
+  static const int omp_once = [] {
+    if (!getenv("OMP_NUM_THREADS")) omp_set_num_threads(std::max(1, omp_get_num_procs() - 2));
+    return 0;
+  }();
+  (void)omp_once;
   g_dbg_t0 = std::chrono::steady_clock::now();
   auto F = std::make_unique<Factorization>();
   F->spec.init(dim, n, m);
@@ -615,6 +690,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       DBG("level 0: planned on the device G=%d blocks=%lld", L.plan.grp.G, (long long)dp.nblocks);
     } else {
       if (lev == 0) {
+        A.ensure_host_pattern(s);
         L.plan.grp = classify_all(sp);
         DBG("level 0: classified");
         pairs = pattern_from_csr(L.plan.grp, sp.N, A.h_rowptr.get(), A.h_col.get());
@@ -2093,9 +2169,6 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
   int* conv = iters + k;
   if (want_history && maxit > 0) hist.alloc((size_t)maxit * k * sizeof(double), s);
   double* hp = want_history && maxit > 0 ? hist.as<double>() : nullptr;
-  const int64_t* rp = A.rowptr.as<int64_t>();
-  const int* ci = A.col.as<int>();
-  const double* va = A.val.as<double>();
   PcgResult res;
   int hctl[2] = {0, 0};
   auto read_ctl = [&]() {
@@ -2117,12 +2190,12 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
   int it = 0;
   while (hctl[0] > 0 && it < maxit) {
     ++it;
-    launch_spmv(rp, ci, va, Pv.as<double>(), Q.as<double>(), N, k, s);
+    spmv(A, Pv.as<double>(), Q.as<double>(), k, s);
     launch_dot(Pv.as<double>(), Q.as<double>(), N, k, part.as<double>(), pq, s);
     launch_pcg_alpha(rz, pq, act, alpha, ctl, it, k, s);
     launch_axpy(x, Pv.as<double>(), alpha, 1.0, act, N, k, s);
     if (it % 50 == 0) {   // true residual
-      launch_spmv(rp, ci, va, x, Q.as<double>(), N, k, s);
+      spmv(A, x, Q.as<double>(), k, s);
       launch_sub(R.as<double>(), b, Q.as<double>(), act, N, k, s);
     } else {
       launch_axpy(R.as<double>(), Q.as<double>(), alpha, -1.0, act, N, k, s);
@@ -2209,17 +2282,14 @@ PowerResult apply_error(const Matrix& A, Factorization& F, const double* x0, dou
   const int64_t N = A.N;
   DBuf T;
   T.alloc(N * sizeof(double), s);
-  const int64_t* rp = A.rowptr.as<int64_t>();
-  const int* ci = A.col.as<int>();
-  const double* va = A.val.as<double>();
   PowerResult num = power_norm_dev(N, s, x0, rel_tol, maxit, [&](double* X, double* Y) {
-    launch_spmv(rp, ci, va, X, T.as<double>(), N, 1, s);   // T = A x
+    spmv(A, X, T.as<double>(), 1, s);   // T = A x
     CK(cudaMemcpyAsync(Y, X, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     apply(F, Y, 1, 3);                   // Y = F x
     launch_xmy(Y, T.as<double>(), N, s);   // Y = A x - F x
   });
   PowerResult den = power_norm_dev(N, s, x0, rel_tol, maxit, [&](double* X, double* Y) {
-    launch_spmv(rp, ci, va, X, Y, N, 1, s);
+    spmv(A, X, Y, 1, s);
   });
   PowerResult r;
   r.value = den.value > 0.0 ? num.value / den.value : 0.0;
@@ -2249,7 +2319,7 @@ PowerResult solve_error(const Matrix& A, Factorization& F, const double* x0, dou
   return power_norm_dev(N, s, x0, rel_tol, maxit, [&](double* X, double* Y) {
     CK(cudaMemcpyAsync(T.p, X, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     apply(F, T.as<double>(), 1, 2);   // G^-T x
-    launch_spmv(A.rowptr.as<int64_t>(), A.col.as<int>(), A.val.as<double>(), T.as<double>(), Y, N, 1, s);
+    spmv(A, T.as<double>(), Y, 1, s);
     apply(F, Y, 1, 1);                // G^-1 A G^-T x
     launch_xmy(Y, X, N, s);           // x - G^-1 A G^-T x
   });

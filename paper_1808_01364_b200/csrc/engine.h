@@ -56,8 +56,17 @@ void upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
 
 struct Matrix {
   int64_t N = 0, nnz = 0;
-  std::unique_ptr<int64_t[]> h_rowptr;   // host copy of the pattern for the planner
-  std::unique_ptr<int[]> h_col;           // (uninitialised allocations: filled by parallel copies)
+  // assembled on the device from a coefficient field (problem.cu): the field and the diagonal
+  // are kept for the matrix-free stencil SpMV
+  bool stencil = false;
+  int dim = 0;
+  int64_t side = 0;
+  DBuf field, diag;
+  // host copy of the pattern for the host planner (uninitialised allocations filled by parallel
+  // copies; downloaded on first use for a matrix assembled on the device)
+  mutable std::unique_ptr<int64_t[]> h_rowptr;
+  mutable std::unique_ptr<int[]> h_col;
+  void ensure_host_pattern(cudaStream_t s) const;
   DBuf rowptr, col, val;
 };
 
@@ -71,6 +80,7 @@ struct BdLists {
 
 struct LevelRT {
   LevelPlan plan;
+  ~LevelRT() { recycle_plan(plan); }
   // structure on device
   DBuf goff, mem, gsize, boff, bg, bh, adj_off, adj_nbr, adj_blk, diag_blk;
   DBuf pool;   // live matrix blocks (freed after the level transition)

@@ -70,9 +70,12 @@ T read1(const T* d, cudaStream_t s) {
   return h;
 }
 
+inline void pool_take(std::vector<int>& h, int64_t n) { h = pool_take_int((size_t)n); }
+inline void pool_take(std::vector<int64_t>& h, int64_t n) { h = pool_take_i64((size_t)n); }
+
 template <class T>
 void down(std::vector<T>& h, const DBuf& d, int64_t n, cudaStream_t s) {
-  h.resize(n);
+  pool_take(h, n);   // recycled host allocation (no page faults once warm)
   if (n) download_bytes(h.data(), d.p, (size_t)n * sizeof(T), s);
 }
 

@@ -2962,7 +2962,7 @@ __global__ void k_spmv(const int64_t* rowptr, const int* col, const double* val,
   const int64_t r = e / k;
   const int c = (int)(e % k);
   double s = 0.0;
-  for (int64_t q = rowptr[r]; q < rowptr[r + 1]; ++q) s += val[q] * x[(int64_t)col[q] * k + c];
+  for (int64_t q = rowptr[r]; q < rowptr[r + 1]; ++q) s = __fma_rn(val[q], x[(int64_t)col[q] * k + c], s);
   y[e] = s;
 }
 

@@ -13,6 +13,8 @@
 #include <sstream>
 #include <stdexcept>
 #include <tuple>
+#include <map>
+#include <mutex>
 
 namespace phif {
 
@@ -834,6 +836,63 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
     for (int i = 0; i < nsk; ++i) lp.wave_order[fill[lp.sk_wave[i]]++] = i;   // stable: (wave, index)
   }
   lap("skeleton waves");
+}
+
+namespace {
+template <class T>
+struct VecPool {
+  std::mutex mu;
+  std::multimap<size_t, std::vector<T>> free;   // by capacity
+  size_t bytes = 0;
+  static constexpr size_t CAP = (size_t)2 << 30;   // keep at most 2 GB of host plan arrays
+  std::vector<T> take(size_t n) {
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto it = free.lower_bound(n);
+      if (it != free.end() && it->first <= 2 * n + 4096) {
+        std::vector<T> v = std::move(it->second);
+        bytes -= it->first * sizeof(T);
+        free.erase(it);
+        v.resize(n);   // truncation, or a short zero tail
+        return v;
+      }
+    }
+    return std::vector<T>(n);
+  }
+  void give(std::vector<T>& v) {
+    if (v.capacity() < 4096) return;
+    std::vector<T> w;
+    w.swap(v);
+    std::lock_guard<std::mutex> lock(mu);
+    if (bytes + w.capacity() * sizeof(T) > CAP) return;
+    bytes += w.capacity() * sizeof(T);
+    free.emplace(w.capacity(), std::move(w));
+  }
+};
+VecPool<int>& ipool() {
+  static VecPool<int>* p = new VecPool<int>();
+  return *p;
+}
+VecPool<int64_t>& lpool() {
+  static VecPool<int64_t>* p = new VecPool<int64_t>();
+  return *p;
+}
+}  // namespace
+
+std::vector<int> pool_take_int(size_t n) { return ipool().take(n); }
+std::vector<int64_t> pool_take_i64(size_t n) { return lpool().take(n); }
+
+void recycle_plan(LevelPlan& lp) {
+  for (std::vector<int>* v : {&lp.grp.q, &lp.grp.bits, &lp.grp.kind, &lp.grp.mem, &lp.grp.src_group, &lp.grp.src_pos,
+                              &lp.grp.src_local, &lp.grp.srcl, &lp.pat.bg, &lp.pat.bh, &lp.pat.adj_nbr,
+                              &lp.pat.adj_blk, &lp.interior, &lp.precond, &lp.skeleton, &lp.cell_nbr,
+                              &lp.cell_nbr_blk, &lp.cell_nbr_col, &lp.cell_n, &lp.cell_b, &lp.tgt_blk, &lp.con_cell,
+                              &lp.con_row, &lp.con_col, &lp.scale_blk, &lp.sk_nbr, &lp.sk_nbr_blk, &lp.sk_wave,
+                              &lp.wave_order, &lp.sk_ndep, &lp.sk_succ})
+    ipool().give(*v);
+  for (std::vector<int64_t>* v : {&lp.grp.off, &lp.grp.srcl_off, &lp.pat.adj_off, &lp.boff, &lp.cell_nbr_off,
+                                  &lp.tgt_off, &lp.sk_nbr_off, &lp.wave_off, &lp.sk_succ_off})
+    lpool().give(*v);
 }
 
 std::string level_json(const LevelPlan& lp) {

@@ -96,4 +96,12 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
 
 std::string level_json(const LevelPlan& lp);
 
+// Host vector pool for plan arrays: vectors taken from it are reused allocations (already
+// faulted in), so large per-factorization plan arrays cost a copy, not fresh page faults.
+// pool_take returns a vector of size n with unspecified contents; recycle_plan gives every
+// array of a finished plan back.
+std::vector<int> pool_take_int(size_t n);
+std::vector<int64_t> pool_take_i64(size_t n);
+void recycle_plan(LevelPlan& lp);
+
 }  // namespace phif
