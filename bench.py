@@ -148,6 +148,16 @@ def cpu_sample(workload, seed=0):
     return A.n / dt, dt, spec, F
 
 
+def _fullsize_note(workload):
+    full = cpu_fullsize(workload)
+    if not full:
+        return None
+    return {"value": full["dofs_per_s"], "unit": "DOF/s", "N": full["N"], "seconds": full["t_factor_s"],
+            "cores": full["cores"], "cpu_model": full["cpu_model"],
+            "source": f"profiles/cpu_fullsize_{workload}_r02.json (the oracle's full-size factorization timed on "
+                      f"the GPU box host; too long to repeat per step)"}
+
+
 def run_reference(args, world, rank, pg):
     if rank != 0:
         return
@@ -170,6 +180,7 @@ def run_reference(args, world, rank, pg):
             "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": f"oracle factorize of the {cfg} recipe on a {sn}-grid (N={N}), "
                                        f"numpy/scipy OpenBLAS with all host threads"},
+            "fullsize": _fullsize_note(args.workload),
             "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 

@@ -26,7 +26,9 @@
  * (pivot 0-based as kernels.py:32, level, stage, group) like errors.py:21-30.
  * Vector arguments may be host or device pointers (detected); vectors with
  * nrhs columns are N x nrhs row-major (DOF-major). `stream` is a cudaStream_t.
- * A finished factor is read-only; apply/pcg calls on one stream at a time.
+ * A finished factor is read-only and safe for concurrent callers: apply / pcg /
+ * estimator calls on one factor from several host threads are serialised per factor (each call
+ * is synchronous), calls on different factors run concurrently.
  */
 #ifndef PHIF_B200_H
 #define PHIF_B200_H

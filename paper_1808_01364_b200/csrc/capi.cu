@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <execinfo.h>
 #include <unistd.h>
 
@@ -18,6 +19,9 @@ struct phif_matrix {
 };
 struct phif_factor {
   std::unique_ptr<phif::Factorization> f;
+  // A finished factor is read-only, but its apply workspaces and lazily built replay plans are
+  // per factor: concurrent callers are serialised here, each call synchronous.
+  std::mutex mu;
 };
 
 namespace {
@@ -180,6 +184,7 @@ void phif_factor_free(phif_factor* F) { delete F; }
 
 int phif_apply(phif_factor* F, double* x, int nrhs, int mode, phif_error* err) {
   return guarded(err, [&] {
+    std::lock_guard<std::mutex> lock(F->mu);
     if (mode < 0 || mode > 5) throw std::invalid_argument("phif_apply: mode must be 0..5");
     phif::Factorization& f = *F->f;
     const size_t bytes = (size_t)f.spec.N * nrhs * sizeof(double);
@@ -203,6 +208,8 @@ int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, i
              phif_error* err) {
   int brk = 0;
   int rc = guarded(err, [&] {
+    std::unique_lock<std::mutex> lock;
+    if (F) lock = std::unique_lock<std::mutex>(F->mu);
     cudaStream_t s = F ? F->f->stream : (cudaStream_t)stream;
     const size_t bytes = (size_t)A->m->N * nrhs * sizeof(double);
     phif::DBuf db, dx;
@@ -241,6 +248,7 @@ int phif_pcg(const phif_matrix* A, phif_factor* F, const double* b, double* x, i
 int phif_solve_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
                      double* value, int* iters, int* converged, double* rel_achieved, phif_error* err) {
   return guarded(err, [&] {
+    std::lock_guard<std::mutex> lock(F->mu);
     phif::PowerResult r = phif::solve_error(*A->m, *F->f, x0, rel_tol, maxit);
     *value = r.value;
     *iters = r.iters;
@@ -252,6 +260,7 @@ int phif_solve_error(const phif_matrix* A, phif_factor* F, const double* x0, dou
 int phif_apply_error(const phif_matrix* A, phif_factor* F, const double* x0, double rel_tol, int maxit,
                      double* value, int* iters, int* converged, double* rel_achieved, phif_error* err) {
   return guarded(err, [&] {
+    std::lock_guard<std::mutex> lock(F->mu);
     phif::PowerResult r = phif::apply_error(*A->m, *F->f, x0, rel_tol, maxit);
     *value = r.value;
     *iters = r.iters;
@@ -261,7 +270,10 @@ int phif_apply_error(const phif_matrix* A, phif_factor* F, const double* x0, dou
 }
 
 int phif_root_factor(phif_factor* F, double* out, int* n, phif_error* err) {
-  return guarded(err, [&] { *n = phif::root_factor(*F->f, out); });
+  return guarded(err, [&] {
+    std::lock_guard<std::mutex> lock(F->mu);
+    *n = phif::root_factor(*F->f, out);
+  });
 }
 
 size_t phif_stats_json(const phif_factor* F, char* buf, size_t cap) {

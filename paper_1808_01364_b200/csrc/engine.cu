@@ -1066,7 +1066,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       // small groups: one CTA each; big groups: tile-parallel panels [A_gg ; I] -> [L ; L^-T]
       std::vector<int> ptiny, psmall, pbig;
       int tiny_max = 1;
-      for (int t = 0; t < r; ++t) {
+      const int kmax_pr = r ? *std::max_element(pn.begin(), pn.end()) : 1;
+      const bool all_tiny = kmax_pr <= 32;   // (level 0: no host lists, the warp kernels take all)
+      if (all_tiny) tiny_max = std::max(1, kmax_pr);
+      for (int t = 0; t < r && !all_tiny; ++t) {
         if (pn[t] <= 32) {
           ptiny.push_back(t);
           tiny_max = std::max(tiny_max, pn[t]);
@@ -1081,8 +1084,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       ps.r = (int)psmall.size();
       launch_prec_factor(dv, ps, F->status.as<DevStatus>(), s);
       DBuf dtiny;
-      upload(dtiny, ptiny, s);
-      launch_prec_factor_warp(dv, pa, dtiny.as<int>(), (int)ptiny.size(), tiny_max, F->status.as<DevStatus>(), s);
+      if (!all_tiny) upload(dtiny, ptiny, s);
+      launch_prec_factor_warp(dv, pa, all_tiny ? nullptr : dtiny.as<int>(), all_tiny ? r : (int)ptiny.size(), tiny_max,
+                              F->status.as<DevStatus>(), s);
       if (!pbig.empty()) {
         DBuf dbig;
         upload(dbig, pbig, s);
@@ -1102,7 +1106,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       std::vector<int> w1d, w1t, w2d, w2t;
       int64_t tmp_need = 0;
       int stiny_max = 1;
-      for (size_t q = 0; q < P.scale_blk.size(); ++q) {
+      if (all_tiny) stiny_max = tiny_max;   // (every scaled block couples two tiny groups)
+      for (size_t q = 0; q < P.scale_blk.size() && !all_tiny; ++q) {
         const int b = P.scale_blk[q];
         const int kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
         if (std::max(kg, kh) <= 32) {
@@ -1120,8 +1125,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       pss.nscale = (int)ssmall.size();
       launch_prec_scale(dv, pss, s);
       DBuf dstiny;
-      upload(dstiny, stiny, s);
-      launch_prec_scale_warp(dv, pa, dstiny.as<int>(), (int)stiny.size(), stiny_max, s);
+      if (!all_tiny) upload(dstiny, stiny, s);
+      launch_prec_scale_warp(dv, pa, all_tiny ? nullptr : dstiny.as<int>(),
+                             all_tiny ? (int)P.scale_blk.size() : (int)stiny.size(), stiny_max, s);
       if (tmp_need) {
         DBuf tmp;
         tmp.alloc(tmp_need * sizeof(double), s);

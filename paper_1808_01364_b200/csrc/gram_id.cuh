@@ -178,6 +178,11 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
     }
     __syncthreads();
   }
+  // epilogue staged in the drained pipeline buffers, then coalesced column-major stores of the
+  // tile and of its mirror (full G)
+  double* sT = smem;
+  constexpr int LD = BT + 1;
+  if (nch == 0) __syncthreads();
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -185,11 +190,18 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
         const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
-        if (i < Mv && j < Nv) {
-          Gm[(int64_t)(br0 + j) * k + ar0 + i] = acc[x][y][z];
-          if (it != jt) Gm[(int64_t)(ar0 + i) * k + br0 + j] = acc[x][y][z];   // mirror: full G
-        }
+        sT[j * LD + i] = acc[x][y][z];
       }
+  __syncthreads();
+  for (int e = tid; e < BT * BT; e += NT) {
+    const int j = e / BT, i = e % BT;   // G(ar0 + i, br0 + j) at column br0 + j
+    if (i < Mv && j < Nv) Gm[(int64_t)(br0 + j) * k + ar0 + i] = sT[j * LD + i];
+  }
+  if (it != jt)
+    for (int e = tid; e < BT * BT; e += NT) {
+      const int i = e / BT, j = e % BT;   // mirror G(br0 + j, ar0 + i) at column ar0 + i
+      if (i < Mv && j < Nv) Gm[(int64_t)(ar0 + i) * k + br0 + j] = sT[j * LD + i];
+    }
 }
 
 // ---- 3. pivoted Cholesky (dlaqp2 replay) + T on a cluster of C CTAs ------------------------

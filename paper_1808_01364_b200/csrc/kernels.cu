@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) k_prec_factor_warp(LevelDev lv, PrecArgs 
   const int ld = kmax + 1;
   double* D = smem + (size_t)warp * 2 * kmax * ld;
   double* X = D + (size_t)kmax * ld;
-  const int t = list[idx];
+  const int t = list ? list[idx] : idx;   // (no list: every group)
   const int g = pa.groups[t], k = lv.gsize[g];
   double* A = lv.pool + lv.boff[lv.diag_blk[g]];
   double* L = pa.rec + pa.L_off[t];
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) k_prec_scale_warp(LevelDev lv, PrecArgs p
   if (idx >= n) return;
   const int ld = ldmax + 1;
   double* S = smem + (size_t)warp * ldmax * ld;
-  const int blk = pa.scale_blk[list[idx]];
+  const int blk = pa.scale_blk[list ? list[idx] : idx];   // (no list: every scaling block)
   const int g = lv.bg[blk], h = lv.bh[blk];
   const int kg = lv.gsize[g], kh = lv.gsize[h];
   double* B = lv.pool + lv.boff[blk];
@@ -3221,6 +3221,14 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
     }
     __syncthreads();
   }
+  // epilogue through shared memory: the fragments land in the (padded) C tile, then whole rows
+  // leave with coalesced stores (a warp writes 32 consecutive doubles of one row); the mirror
+  // tile of U reads the staged tile by columns (conflict-free thanks to the padding)
+  if (nch == 0) {   // (no K chunk: the C prefetch is still in flight)
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  double* sT = MODE == 0 ? sC : smem;   // (MODE 1: the drained pipeline stages hold the tile)
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -3228,17 +3236,28 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
         const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
-        if (i < Mv && j < Nv) {
-          if (MODE == 0) {
-            P[(int64_t)(ar0 + i) * n + br0 + j] = sC[i * NT_CLD + j] - acc[x][y][z];
-          } else {
-            const int b = a.b[c];
-            double* U = a.U[c];
-            U[(int64_t)(BT * it + i) * b + BT * jt + j] = acc[x][y][z];
-            if (it != jt) U[(int64_t)(BT * jt + j) * b + BT * it + i] = acc[x][y][z];
-          }
-        }
+        if (MODE == 0) sT[i * NT_CLD + j] -= acc[x][y][z];
+        else sT[i * NT_CLD + j] = acc[x][y][z];
       }
+  __syncthreads();
+  if (MODE == 0) {
+    for (int e = tid; e < BT * BT; e += NT) {
+      const int i = e / BT, j = e % BT;
+      if (i < Mv && j < Nv) P[(int64_t)(ar0 + i) * n + br0 + j] = sT[i * NT_CLD + j];
+    }
+  } else {
+    const int b = a.b[c];
+    double* U = a.U[c];
+    for (int e = tid; e < BT * BT; e += NT) {
+      const int i = e / BT, j = e % BT;
+      if (i < Mv && j < Nv) U[(int64_t)(BT * it + i) * b + BT * jt + j] = sT[i * NT_CLD + j];
+    }
+    if (it != jt)
+      for (int e = tid; e < BT * BT; e += NT) {
+        const int jj = e / BT, ii = e % BT;   // mirror row BT*jt + jj, column BT*it + ii
+        if (ii < Mv && jj < Nv) U[(int64_t)(BT * jt + jj) * b + BT * it + ii] = sT[ii * NT_CLD + jj];
+      }
+  }
 }
 
 #include "gram_id.cuh"

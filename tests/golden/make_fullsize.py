@@ -69,6 +69,23 @@ def cpu_model():
     return platform.processor()
 
 
+def _progress():
+    """Print every oracle stage as it finishes (the full-size runs take tens of minutes)."""
+    t_start = time.perf_counter()
+    for name in ("eliminate_cells", "precondition_blocks", "skeletonize_separators"):
+        fn = getattr(ophif, name)
+
+        def wrap(*a, _fn=fn, _name=name, **k):
+            t0 = time.perf_counter()
+            out = _fn(*a, **k)
+            li = 3 if _name == "skeletonize_separators" else 2
+            lev = k.get("level", a[li] if len(a) > li else None)
+            print(f"  [{time.perf_counter() - t_start:8.1f} s] level {lev} {_name} {time.perf_counter() - t0:.1f} s",
+                  flush=True)
+            return out
+        setattr(ophif, name, wrap)
+
+
 def main():
     name, eps, method = sys.argv[1], float(sys.argv[2]), sys.argv[3]
     nrhs = int(sys.argv[4]) if len(sys.argv) > 4 else None
@@ -84,6 +101,7 @@ def main():
             "generator": "tests/golden/make_fullsize.py"}
     print(json.dumps(meta), flush=True)
     arrays = {}
+    _progress()
     t0 = time.perf_counter()
     try:
         F = ophif.factorize(A, spec, eps, method)

@@ -263,3 +263,26 @@ def test_pcg_residual_history_and_partial_stats():
         gfac.factorize(A2, spec2, 1e-2, "phif")
     ps = g.value.partial_stats
     assert ps is not None and len(ps["levels"]) == g.value.level and ps["complete"] is False
+
+
+def test_concurrent_apply_on_one_factor():
+    """a completed Factorization is safe for concurrent callers (the C-ABI serialises
+    per factor; ctypes releases the GIL, so the threads really overlap on the host)."""
+    import threading
+    spec, A = baseline_problem("c4", 0, 32)[:2]
+    F = gfac.factorize(A, spec, 1e-3, "phif")
+    rhs = [np.random.default_rng([9, i]).standard_normal((A.n, 1 + i % 3)) for i in range(8)]
+    ref = [gfac.apply_inverse(F, b) for b in rhs]
+    out = [None] * len(rhs)
+
+    def work(i):
+        for _ in range(3):
+            out[i] = gfac.apply_inverse(F, rhs[i])
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(rhs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r, o in zip(ref, out):
+        assert np.array_equal(r, o)
