@@ -674,6 +674,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
 
   std::vector<std::pair<int, int>> pairs;
   std::vector<uint8_t> alive_mem;  // survivors of the previous level, per member position
+  std::future<LevelPlan> preplan;  // structure of the next level, planned while the IDs run
+  static const bool no_preplan = getenv("PHIF_NO_PREPLAN") != nullptr;
   try {
   for (int lev = 0; lev <= sp.L; ++lev) {
     auto tp = clk::now();
@@ -689,6 +691,16 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       plan_level0_device(sp, A.rowptr.as<int64_t>(), A.col.as<int>(), A.nnz, L.plan, dp, s);
       DBG("level 0: planned on the device G=%d blocks=%lld", L.plan.grp.G, (long long)dp.nblocks);
     } else {
+      bool done = false;
+      if (lev > 0 && preplan.valid()) {
+        LevelPlan pp = preplan.get();
+        if (finish_preplan(sp, pp, prev->plan, alive_mem)) {
+          L.plan = std::move(pp);
+          done = true;
+          DBG("level %d: pre-plan finished G=%d", lev, L.plan.grp.G);
+        }
+      }
+      if (!done) {
       if (lev == 0) {
         A.ensure_host_pattern(s);
         L.plan.grp = classify_all(sp);
@@ -700,6 +712,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       }
       DBG("level %d: grouped G=%d", lev, L.plan.grp.G);
       build_level(sp, L.plan, std::move(pairs));
+      }
     }
     // device copy of a plan array: taken over from the device planner, else uploaded
     auto dev_arr = [&](DBuf& dst, DBuf& from, const auto& host) {
@@ -1483,6 +1496,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       CK(cudaGetLastError());
       // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     }
+    // the next level's structure is planned on a host thread while the IDs run on the device
+    if (!P.root && !no_preplan)
+      preplan = std::async(std::launch::async, [&sp, &L]() {
+        // a smaller OpenMP team: the main thread keeps its own team for the level's host work
+        omp_set_num_threads(std::max(2, omp_get_num_procs() / 2 - 1));
+        return preplan_next(sp, L.plan);
+      });
     // ranks and redundant flags back to the host (large separator updates, next level planning)
     L.h_rank.resize(nsk);
     std::vector<int> h_rows(nsk);
@@ -1687,6 +1707,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   }
   } catch (NotSpd& e) {
     // partial statistics: the levels completed before the failing one (errors.py:21-30)
+    if (preplan.valid()) preplan.wait();   // (it reads the plan of the level being dropped)
     cudaStreamSynchronize(s);
     while ((int)F->levels.size() > e.level) F->levels.pop_back();
     F->t_factor_ms = ms_since(t_start);

@@ -729,81 +729,111 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     }
   }
   __syncthreads();
-  // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
-  ArgMax loc{-1.0, 0x7fffffff};
-  for (int j = tid; j < k; j += NT) {
-    const double dj = S[j * k + j];
-    const double nj = fmax(dj, 0.0);
-    d[j] = dj;
-    vn1[j] = vn2[j] = nj;
-    rdv[j] = sqrt(nj);
-    invv[j] = nj > 0.0 ? 1.0 / rdv[j] : 0.0;
-    col_at[j] = j;
-    piv[j] = 0;
-    loc = better(loc, ArgMax{nj, j});
-  }
-  ArgMax best = cta_argmax1(loc, sred);
-  const double tol3z = sqrt(DBL_EPSILON * 0.5);
-  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
-  const int mn = min(m, k);
-  double cut = 0.0, cut2 = 0.0;
-  int r = 0, i = 0;
-  for (; i < mn; ++i) {
-    if (i > 0 && best.v < cut2) break;
-    const int pb = best.i, p = col_at[pb];   // (the position swap happens in the downdate loop)
-    const double rd = rdv[p];
-    if (i == 0) {
-      cut = cutrel * rd;
-      cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
+  // Pivoted Cholesky of G replaying dlaqp2, by warp 0 alone (no CTA barriers on the pivot chain;
+  // k <= 57, two positions per lane). Left-looking: row i of R is formed from row p of G and the
+  // earlier rows of R, acc = fma(-R(l, p), R(l, b), acc) for l = 0 .. i-1 -- the same operations
+  // in the same order as the right-looking rank-1 updates of the Schur complement, so R, the
+  // pivots and the rank are bit-identical to that formulation (and to cta_cpqr's dlaqp2 rules).
+  __shared__ int s_rank;
+  if (warp == 0) {
+    // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
+    ArgMax loc{-1.0, 0x7fffffff};
+    for (int j = lane; j < k; j += 32) {
+      const double dj = S[j * k + j];
+      const double nj = fmax(dj, 0.0);
+      d[j] = dj;
+      vn1[j] = vn2[j] = nj;
+      rdv[j] = sqrt(nj);
+      invv[j] = nj > 0.0 ? 1.0 / rdv[j] : 0.0;
+      col_at[j] = j;
+      piv[j] = 0;
+      loc = better(loc, ArgMax{nj, j});
     }
-    if (rd > cut) ++r;
-    const double inv = invv[p];
-    double* row = Rsm + i * k;
-    for (int a = tid; a < k; a += NT) row[a] = a == p ? rd : (piv[a] ? 0.0 : S[p * k + a] * inv);
-    __syncthreads();
-    if (tid == 0) piv[p] = 1;
-    // rank-1 update (rows of pivoted columns have R(i, a) = 0; row/column p become garbage and
-    // are never read again)
-    for (int a = warp; a < k; a += nw) {
-      const double ra = row[a];
-      if (ra == 0.0 || a == p) continue;
-      for (int b = lane; b < k; b += 32) S[a * k + b] = __fma_rn(-ra, row[b], S[a * k + b]);
-    }
-    loc = ArgMax{-1.0, 0x7fffffff};
-    for (int j = i + 1 + tid; j < k; j += NT) {
-      int col;
-      if (j == pb) {   // dlaqp2 swap of positions i and pb, by the owner of position pb
-        col = col_at[i];
-        col_at[j] = col;
-        col_at[i] = p;
-        vn1[j] = vn1[i];
-        vn2[j] = vn2[i];
-      } else {
-        col = col_at[j];
+    auto warp_best = [&](ArgMax x) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ArgMax y;
+        y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+        y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+        x = better(x, y);
       }
-      const double rv = row[col];
-      const double dn = __fma_rn(-rv, rv, d[col]);
-      d[col] = dn;
-      {
-        const double rdn = sqrt(fmax(dn, 0.0));
-        rdv[col] = rdn;
-        invv[col] = rdn > 0.0 ? 1.0 / rdn : 0.0;
+      return x;
+    };
+    ArgMax best = warp_best(loc);
+    __syncwarp();
+    const double tol3z = sqrt(DBL_EPSILON * 0.5);
+    const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
+    const int mn = min(m, k);
+    double cut = 0.0, cut2 = 0.0;
+    int r = 0, i = 0;
+    for (; i < mn; ++i) {
+      if (i > 0 && best.v < cut2) break;
+      const int pb = best.i, p = col_at[pb];
+      const double rd = rdv[p];
+      if (i == 0) {
+        cut = cutrel * rd;
+        cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
       }
-      double w1 = vn1[j];
-      if (w1 != 0.0) {
-        const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
-        if (w <= tol3z * vn2[j]) {
-          w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
-          vn2[j] = w1;
+      if (rd > cut) ++r;
+      const double inv = invv[p];
+      double* row = Rsm + i * k;
+      for (int b = lane; b < k; b += 32) {
+        double v;
+        if (b == p) {
+          v = rd;
+        } else if (piv[b]) {
+          v = 0.0;
         } else {
-          w1 = w;
+          double acc = S[p * k + b];
+          for (int l = 0; l < i; ++l) acc = __fma_rn(-Rsm[l * k + p], Rsm[l * k + b], acc);
+          v = acc * inv;
         }
-        vn1[j] = w1;
+        row[b] = v;
       }
-      loc = better(loc, ArgMax{w1, j});
+      __syncwarp();
+      if (lane == 0) piv[p] = 1;
+      loc = ArgMax{-1.0, 0x7fffffff};
+      // positions j > i: the dlaqp2 swap of i and pb is done by the lane owning pb (it takes over
+      // position i's column and norms); position i is final
+      for (int j = i + 1 + lane; j < k; j += 32) {
+        int col;
+        if (j == pb) {
+          col = col_at[i];
+          col_at[j] = col;
+          col_at[i] = p;
+          vn1[j] = vn1[i];
+          vn2[j] = vn2[i];
+        } else {
+          col = col_at[j];
+        }
+        const double rv = row[col];
+        const double dn = __fma_rn(-rv, rv, d[col]);
+        d[col] = dn;
+        {
+          const double rdn = sqrt(fmax(dn, 0.0));
+          rdv[col] = rdn;
+          invv[col] = rdn > 0.0 ? 1.0 / rdn : 0.0;
+        }
+        double w1 = vn1[j];
+        if (w1 != 0.0) {
+          const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
+          if (w <= tol3z * vn2[j]) {
+            w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
+            vn2[j] = w1;
+          } else {
+            w1 = w;
+          }
+          vn1[j] = w1;
+        }
+        loc = better(loc, ArgMax{w1, j});
+      }
+      best = warp_best(loc);
+      __syncwarp();
     }
-    best = cta_argmax1(loc, sred);
+    if (lane == 0) s_rank = r;
   }
+  __syncthreads();
+  const int r = s_rank;
   const int kt = k - r;
   for (int j = tid; j < k; j += NT) piv[col_at[j]] = j >= r ? 1 : 0;
   __syncthreads();

@@ -713,6 +713,11 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
   }
   // Schur targets: block (a, b), a <= b, receives U_t[a, b] from every cell t holding both a and b
   // (cells of a intersect cells of b; both lists ascending in cell order = the summation order)
+  auto pos_in_cell = [&](int t, int h) {   // index of group h in cell t's neighbour list
+    const int* b0 = lp.cell_nbr.data() + lp.cell_nbr_off[t];
+    const int* b1 = lp.cell_nbr.data() + lp.cell_nbr_off[t + 1];
+    return (int)(std::lower_bound(b0, b1, h) - b0);
+  };
   auto col_of = [&](int t, int h) {   // first column of group h in cell t's boundary
     const int* b0 = lp.cell_nbr.data() + lp.cell_nbr_off[t];
     const int* b1 = lp.cell_nbr.data() + lp.cell_nbr_off[t + 1];
@@ -741,6 +746,8 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
             lp.con_cell[o] = t;
             lp.con_row[o] = col_of(t, a0);
             lp.con_col[o] = col_of(t, b0);
+            lp.con_ri[o] = pos_in_cell(t, a0);
+            lp.con_ci[o] = pos_in_cell(t, b0);
           }
           ++o;
           ++ia;
@@ -754,6 +761,8 @@ void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> 
       lp.con_cell.resize(ncons);
       lp.con_row.resize(ncons);
       lp.con_col.resize(ncons);
+      lp.con_ri.resize(ncons);
+      lp.con_ci.resize(ncons);
     }
   }
   lp.tgt_blk.clear();
@@ -887,12 +896,99 @@ void recycle_plan(LevelPlan& lp) {
                               &lp.grp.src_local, &lp.grp.srcl, &lp.pat.bg, &lp.pat.bh, &lp.pat.adj_nbr,
                               &lp.pat.adj_blk, &lp.interior, &lp.precond, &lp.skeleton, &lp.cell_nbr,
                               &lp.cell_nbr_blk, &lp.cell_nbr_col, &lp.cell_n, &lp.cell_b, &lp.tgt_blk, &lp.con_cell,
-                              &lp.con_row, &lp.con_col, &lp.scale_blk, &lp.sk_nbr, &lp.sk_nbr_blk, &lp.sk_wave,
+                              &lp.con_row, &lp.con_col, &lp.con_ri, &lp.con_ci, &lp.scale_blk, &lp.sk_nbr, &lp.sk_nbr_blk, &lp.sk_wave,
                               &lp.wave_order, &lp.sk_ndep, &lp.sk_succ})
     ipool().give(*v);
   for (std::vector<int64_t>* v : {&lp.grp.off, &lp.grp.srcl_off, &lp.pat.adj_off, &lp.boff, &lp.cell_nbr_off,
                                   &lp.tgt_off, &lp.sk_nbr_off, &lp.wave_off, &lp.sk_succ_off})
     lpool().give(*v);
+}
+
+LevelPlan preplan_next(const Spec& s, const LevelPlan& prev) {
+  const Groups& pg = prev.grp;
+  std::vector<uint8_t> alive(pg.mem.size(), 0);
+#pragma omp parallel for schedule(static)
+  for (int g = 0; g < pg.G; ++g)
+    if (pg.kind[g] != 0)
+      for (int64_t q = pg.off[g]; q < pg.off[g + 1]; ++q) alive[q] = 1;
+  LevelPlan lp;
+  lp.grp = classify_next(s, pg, alive);
+  build_level(s, lp, pattern_next(prev, lp.grp));
+  return lp;
+}
+
+bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const std::vector<uint8_t>& alive) {
+  (void)s;
+  Groups& g = lp.grp;
+  const Groups& pg = prev.grp;
+  const int G = g.G;
+  // every non-interior old group must keep a DOF (else the grouping differs)
+  int lost = 0;
+#pragma omp parallel for schedule(static) reduction(max : lost)
+  for (int og = 0; og < pg.G; ++og) {
+    if (pg.kind[og] == 0) continue;
+    bool any = false;
+    for (int64_t q = pg.off[og]; q < pg.off[og + 1] && !any; ++q) any = alive[q] != 0;
+    if (!any) lost = 1;
+  }
+  if (lost) return false;
+  // filtered member lists (survivors keep their ascending order and provenance)
+  std::vector<int64_t> cnt(G + 1, 0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int i = 0; i < G; ++i) {
+    int64_t c = 0;
+    for (int64_t q = g.off[i]; q < g.off[i + 1]; ++q) c += alive[pg.off[g.src_group[q]] + g.src_pos[q]] != 0;
+    cnt[i + 1] = c;
+  }
+  for (int i = 0; i < G; ++i) cnt[i + 1] += cnt[i];
+  const int64_t tot = cnt[G];
+  std::vector<int> mem(tot), sg(tot), sp(tot), sl(tot);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int i = 0; i < G; ++i) {
+    int64_t o = cnt[i];
+    for (int64_t q = g.off[i]; q < g.off[i + 1]; ++q)
+      if (alive[pg.off[g.src_group[q]] + g.src_pos[q]]) {
+        mem[o] = g.mem[q];
+        sg[o] = g.src_group[q];
+        sp[o] = g.src_pos[q];
+        sl[o] = g.src_local[q];
+        ++o;
+      }
+  }
+  g.off.swap(cnt);
+  g.mem.swap(mem);
+  g.src_group.swap(sg);
+  g.src_pos.swap(sp);
+  g.src_local.swap(sl);
+  // size-dependent parts of the plan
+  const int64_t nb = (int64_t)lp.pat.bg.size();
+  {
+    int64_t acc = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+      lp.boff[b] = acc;
+      acc += (int64_t)g.size(lp.pat.bg[b]) * g.size(lp.pat.bh[b]);
+    }
+    lp.pool_doubles = acc;
+  }
+  const int p = (int)lp.interior.size();
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < p; ++t) {
+    int bc = 0;
+    for (int64_t j = lp.cell_nbr_off[t]; j < lp.cell_nbr_off[t + 1]; ++j) {
+      lp.cell_nbr_col[j] = bc;
+      bc += g.size(lp.cell_nbr[j]);
+    }
+    lp.cell_n[t] = g.size(lp.interior[t]);
+    lp.cell_b[t] = bc;
+  }
+  const int64_t ncon = (int64_t)lp.con_cell.size();
+#pragma omp parallel for schedule(static)
+  for (int64_t o = 0; o < ncon; ++o) {
+    const int64_t base = lp.cell_nbr_off[lp.con_cell[o]];
+    lp.con_row[o] = lp.cell_nbr_col[base + lp.con_ri[o]];
+    lp.con_col[o] = lp.cell_nbr_col[base + lp.con_ci[o]];
+  }
+  return true;
 }
 
 std::string level_json(const LevelPlan& lp) {

@@ -64,6 +64,7 @@ struct LevelPlan {
   std::vector<int> tgt_blk;
   std::vector<int64_t> tgt_off;       // per target (size ntargets+1)
   std::vector<int> con_cell, con_row, con_col;
+  std::vector<int> con_ri, con_ci;    // (host only) neighbour index of the row / column group in its cell
   // off-diagonal blocks scaled by block Jacobi (both ends preconditioned)
   std::vector<int> scale_blk;
   // skeletonization: per skeleton s: neighbour (h, blk) lists excluding self, wave index
@@ -93,6 +94,17 @@ std::vector<std::pair<int, int>> pattern_from_csr(const Groups& g, int64_t N, co
 std::vector<std::pair<int, int>> pattern_next(const LevelPlan& prev, const Groups& next);
 // complete a level plan from its groups and input pattern
 void build_level(const Spec& s, LevelPlan& lp, std::vector<std::pair<int, int>> pairs);
+
+// Pre-plan of level l+1 computed while level l's IDs run: the grouping and every structural list
+// of the next level assuming each non-interior group of level l keeps all its DOFs (group pairs,
+// adjacency, cells, Schur targets, scaling blocks, skeleton lists and wavefronts depend only on
+// which groups exist, not on their sizes).
+LevelPlan preplan_next(const Spec& s, const LevelPlan& prev);
+// Finish a pre-plan with the real survivors: drop the redundant members (ascending order and
+// provenance kept) and recompute what depends on group sizes (pool offsets, cell sizes and
+// boundary columns, Schur contribution columns). Returns false if some non-interior group of the
+// previous level lost every DOF (the grouping changes; re-plan from scratch).
+bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const std::vector<uint8_t>& alive);
 
 std::string level_json(const LevelPlan& lp);
 
