@@ -392,24 +392,33 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     }
     if (C > 1 && tid < C) st_async_f64(tok_dst + 8u * (uint32_t)(q * 16 + c), 0.0, tokbar_dst + 8u * q);
     GID_MARK(2)
+    // C > 1: no CTA barrier here -- after the mbarrier wait every thread reads the received row
+    // entries of its own downdate positions straight from the receive buffer and files them into
+    // the panel row and (owned columns) into R; thread 0 files the diagonal. Entries of already
+    // pivoted columns are never read again (row formation and downdates touch unpivoted columns
+    // only; the back substitution reads R on and above the diagonal).
+    const double* rb = rowbuf + (int64_t)q * k;
     if (C > 1) {
       mbar_wait(mbar + q, (unsigned)((i >> 1) & 1));
       GID_MARK(3)
-      const double* rb = rowbuf + (int64_t)q * k;
-      for (int a = tid; a < k; a += NT) row[a] = a == p ? rd : (piv[a] ? 0.0 : rb[a]);
+      if (tid == 0) {
+        row[p] = rd;
+        piv[p] = 1;   // (read again only after the argmax barrier)
+        if (p % C == c) Gm[(int64_t)p * k + i] = rd;
+      }
     } else {
       __syncthreads();
       for (int a = tid; a < k; a += NT)
         if (a == p) row[a] = rd;
         else if (piv[a]) row[a] = 0.0;
+      __syncthreads();
+      if (tid == 0) piv[p] = 1;   // (read again only after the argmax barrier)
+      for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
+        const int b = lb * C + c;
+        Gm[(int64_t)b * k + i] = row[b];
+      }
     }
-    __syncthreads();
-    if (tid == 0) piv[p] = 1;   // (read again only after the argmax barrier)
     GID_MARK(4)
-    for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
-      const int b = lb * C + c;
-      Gm[(int64_t)b * k + i] = row[b];
-    }
     // fused: Schur diagonal, dlaqp2 partial-norm downdate and the next pivot's argmax over the
     // positions > i (identical arithmetic in every CTA)
     // the dlaqp2 swap of positions i and best.i is done by the thread owning position best.i
@@ -427,7 +436,14 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       } else {
         col = col_at[j];
       }
-      const double rv = row[col];
+      double rv;
+      if (C > 1) {
+        rv = rb[col];
+        row[col] = rv;
+        if (col % C == c) Gm[(int64_t)col * k + i] = rv;
+      } else {
+        rv = row[col];
+      }
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;
       {

@@ -573,11 +573,35 @@ __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& n
         }
       }
     } else {
+      // rows r0.. of block (h, g) are contiguous: lanes along columns, 8 rows x 2 column strips
+      // of loads in flight before their stores
       const int nr = min(32, kh - r0);
-      for (int rr = 0; rr < nr; ++rr) {
-        const bool keep = (mask >> rr) & 1u;
-        const double* p = B + (int64_t)(r0 + rr) * k;
-        for (int c = lane; c < k; c += 32) W[(int64_t)c * ldw + rbase + rr] = keep ? p[c] : 0.0;
+      for (int rr0 = 0; rr0 < nr; rr0 += 8) {
+        double v[8][2];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int rr = rr0 + u;
+          const bool keep = rr < nr && ((mask >> rr) & 1u);
+          const double* p = B + (int64_t)(r0 + rr) * k;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const int c = lane + 32 * w;
+            v[u][w] = (keep && c < k) ? p[c] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int rr = rr0 + u;
+          if (rr >= nr) break;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const int c = lane + 32 * w;
+            if (c < k) W[(int64_t)c * ldw + rbase + rr] = v[u][w];
+          }
+        }
+        for (int c = lane + 64; c < k; c += 32)   // (k > 64: remaining columns, unbatched)
+          for (int rr = rr0; rr < min(nr, rr0 + 8); ++rr)
+            W[(int64_t)c * ldw + rbase + rr] = ((mask >> rr) & 1u) ? B[(int64_t)(r0 + rr) * k + c] : 0.0;
       }
     }
     return;
@@ -785,6 +809,7 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
           v = 0.0;
         } else {
           double acc = S[p * k + b];
+#pragma unroll 8
           for (int l = 0; l < i; ++l) acc = __fma_rn(-Rsm[l * k + p], Rsm[l * k + b], acc);
           v = acc * inv;
         }
