@@ -900,6 +900,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     DBG("level %d: records allocated", lev);
     F->rec_bytes += rec * (int64_t)sizeof(double);
     LevelDev dv = L.dev();
+    int band_w = 0, band_nmax = 0, band_bmax = 0;   // banded level-0 cells (2D), set below
     if (timing) CK(cudaEventRecord(ev[0], s));
     if (lev == 0) {
       DBuf dgid, dpos;
@@ -908,6 +909,29 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       launch_group_pos(dv, dgid.as<int>(), dpos.as<int>(), s);
       launch_ingest(dv, dgid.as<int>(), dpos.as<int>(), A.rowptr.as<int64_t>(), A.col.as<int>(),
                     A.val.as<double>(), sp.N, s);
+      // 2D level-0 cells too big for the one-CTA kernel: banded path when every interior group's
+      // couplings stay within w = m-1 positions (natural order; checked on the device)
+      static const bool no_band = getenv("PHIF_NO_BAND") != nullptr;
+      int nmax = 0, bmax = 0;
+      for (int t = 0; t < p; ++t) {
+        nmax = std::max(nmax, P.cell_n[t]);
+        bmax = std::max(bmax, P.cell_b[t]);
+      }
+      if (!no_band && sp.dim == 2 && nmax >= BIG_CELL && band_cells_fit(nmax, bmax, sp.m - 1)) {
+        std::vector<uint8_t> isint(G.G);
+        for (int gi = 0; gi < G.G; ++gi) isint[gi] = G.kind[gi] == 0;
+        DBuf dint, dflag;
+        upload(dint, isint, s);
+        dflag.alloc(sizeof(int), s, true);
+        launch_band_check(A.rowptr.as<int64_t>(), A.col.as<int>(), dgid.as<int>(), dpos.as<int>(),
+                          dint.as<uint8_t>(), sp.N, sp.m - 1, dflag.as<int>(), s);
+        int flag = 1;
+        CK(cudaMemcpyAsync(&flag, dflag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        band_w = flag ? 0 : sp.m - 1;
+        band_nmax = nmax;
+        band_bmax = bmax;
+      }
       // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     } else {
       RepackArgs ra;
@@ -1008,14 +1032,29 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.h_B_off = B_off;
     L.h_cwork = cwork;
     BigPlan bp;
-    if (!big_cells.empty()) bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
+    const bool banded = band_w > 0 && !big_cells.empty();
+    if (banded) {   // algorithmic work of the banded cells: POTRF n w^2, TRSM 2 n w b, SYRK n b^2
+      double fd = 0.0, fb = 0.0;
+      for (int t : big_cells) {
+        const double nn = P.cell_n[t], bb = P.cell_b[t], ww = band_w;
+        fd += nn * nn * nn / 3.0 + nn * nn * bb + nn * bb * bb;
+        fb += nn * ww * ww + 2.0 * nn * ww * bb + nn * bb * bb;
+      }
+      L.fl[1] += fb - fd;
+    }
+    if (!big_cells.empty() && !banded)
+      bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
     DBG("level %d: big plan built (%lld work items)", lev, (long long)bp.nwork_total);
     if (timing) CK(cudaEventRecord(ev[2], s));
     if (!small_cells.empty()) {
       ca.list = L.d_small_cells.as<int>();
       launch_cell(dv, ca, (int)small_cells.size(), F->status.as<DevStatus>(), s);
     }
-    if (!big_cells.empty()) {
+    if (banded) {
+      upload(bp.d_list, big_cells, s);
+      launch_cell_band(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), band_nmax, band_bmax, band_w,
+                       F->status.as<DevStatus>(), s);
+    } else if (!big_cells.empty()) {
       upload(bp.d_list, big_cells, s);
       launch_big_build(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), s);
       bp.run(F->status.as<DevStatus>(), s);

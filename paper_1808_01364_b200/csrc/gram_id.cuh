@@ -358,13 +358,13 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1 + C));
     // pivot column (position best.i); the position swap is applied after the row exchange
     const int p = col_at[best.i];
-    const double rd = rdv[p];
+    const double rd = i == 0 ? rdv[p] : sqrt(fmax(d[p], 0.0));   // (only the pivot needs it)
     if (i == 0) {
       cut = cutrel * rd;
       cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
     }
     if (rd > cut) ++r;
-    const double inv = invv[p];
+    const double inv = i == 0 ? invv[p] : (rd > 0.0 ? 1.0 / rd : 0.0);
     double* row = Pn + (int64_t)np * k;   // this step's row of R
     // entries of row i in the owned columns, tpc threads per column (panel terms split tpc ways;
     // one round over the owned columns whenever nown <= 256)
@@ -446,11 +446,6 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       }
       const double dn = __fma_rn(-rv, rv, d[col]);
       d[col] = dn;
-      {
-        const double rdn = sqrt(fmax(dn, 0.0));
-        rdv[col] = rdn;
-        invv[col] = rdn > 0.0 ? 1.0 / rdn : 0.0;
-      }
       double w1 = vn1[j];
       if (w1 != 0.0) {
         // dlaqp2: temp = max(0, 1 - (|R(i,j)|/vn1)^2); recompute when temp (vn1/vn2)^2 <= tol3z,

@@ -97,6 +97,177 @@ __global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus
                           false, smem + GEMM_OFF);
 }
 
+// ---------------------------------------------------------------------------
+// Banded cells (2D level 0, n = (m-1)^2 interior DOFs in natural order): A_II is the 5-point
+// stencil restricted to the cell, banded with half-bandwidth w = m-1 (checked on the device by
+// k_band_check before this path is taken), so its Cholesky factor has the same band
+// (POTRF n w^2, TRSM 2 n w b). One CTA per cell:
+//   1. band of A_II -> shared memory; banded Cholesky by one warp (right-looking, no CTA
+//      barriers on the column chain); NotSpd reported like the dense path (cell, 0-based pivot);
+//   2. X = L^-1 A_BI^T: one thread per boundary DOF, forward substitution with the last w
+//      values in registers, written straight into the panel rows [n, n+b) as X^T;
+//   3. U = X^T X from 64-column chunks of X^T staged in shared memory;
+//   4. the record rows: L (dense rows, zeros outside the band) and L^-T (row j = L^-1 e_j, one
+//      thread per column of the identity), the layout the big-cell replay reads.
+// ---------------------------------------------------------------------------
+constexpr int BAND_WMAX = 31;   // w <= 31: one lane per band entry of a column
+__global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, const int* list, int w, DevStatus* st) {
+  extern __shared__ double smem[];
+  const int t = list[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int I = ca.interior[t], n = ca.n[t], b = ca.b[t];
+  const int W1 = w + 1;
+  double* Lb = smem;                  // n x (w+1): Lb[i*W1 + d] = L(i, i-d)
+  double* dinv = Lb + (int64_t)n * W1;   // n
+  double* Xs = dinv + n;              // b x 64 staging of X^T chunks (U)
+  __shared__ int s_bad;
+  double* P = ca.rec + ca.P_off[t];
+  const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
+  for (int e = tid; e < n * W1; e += NT) {
+    const int i = e / W1, d = e % W1;
+    Lb[e] = i - d >= 0 ? A[(int64_t)i * n + i - d] : 0.0;
+  }
+  if (tid == 0) s_bad = -1;
+  __syncthreads();
+  if (warp == 0) {
+    for (int j = 0; j < n; ++j) {
+      const double djj = Lb[(int64_t)j * W1];
+      if (!(djj > 0.0)) {
+        if (lane == 0) s_bad = j;
+        break;
+      }
+      const double ljj = sqrt(djj), rinv = 1.0 / ljj;
+      const int d = lane + 1;   // column j, row j + d
+      double c = 0.0;
+      if (d <= w && j + d < n) {
+        c = Lb[(int64_t)(j + d) * W1 + d] * rinv;
+        Lb[(int64_t)(j + d) * W1 + d] = c;
+      }
+      if (lane == 0) {
+        Lb[(int64_t)j * W1] = ljj;
+        dinv[j] = rinv;
+      }
+      // trailing update of the band: L(j+d, j+e) -= c_d c_e, 1 <= e <= d <= w
+      for (int e = 1; e <= w; ++e) {
+        const double ce = __shfl_sync(0xffffffffu, c, e - 1);
+        if (d <= w && d >= e && j + d < n) Lb[(int64_t)(j + d) * W1 + (d - e)] -= c * ce;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (s_bad >= 0) {
+    if (tid == 0) report_bad(st, t, s_bad);
+    return;
+  }
+  // L rows of the record (dense, zeros outside the band)
+  for (int64_t e = tid; e < (int64_t)n * n; e += NT) {
+    const int i = (int)(e / n), c = (int)(e % n), d = i - c;
+    P[e] = (d >= 0 && d <= w) ? Lb[(int64_t)i * W1 + d] : 0.0;
+  }
+  // X = L^-1 A_BI^T, one boundary DOF per thread (its A_BI row from the neighbour block)
+  if (tid < b) {
+    const int r = tid;
+    int64_t jn = ca.nbr_off[t];
+    while (jn + 1 < ca.nbr_off[t + 1] && ca.nbr_col[jn + 1] <= r) ++jn;
+    const int wn = ca.nbr_w[jn], rc = r - ca.nbr_col[jn];
+    const double* S = lv.pool + lv.boff[ca.nbr_blk[jn]];   // block (I, h): |I| x wn row-major
+    double h[BAND_WMAX];
+#pragma unroll
+    for (int q = 0; q < BAND_WMAX; ++q) h[q] = 0.0;
+    double* Xr = P + (int64_t)(n + r) * n;
+    for (int i = 0; i < n; ++i) {
+      double acc = S[(int64_t)i * wn + rc];
+      const double* Li = Lb + (int64_t)i * W1;
+#pragma unroll
+      for (int q = 0; q < BAND_WMAX; ++q)
+        if (q < w) acc = __fma_rn(-Li[q + 1], h[q], acc);
+      const double x = acc * dinv[i];
+#pragma unroll
+      for (int q = BAND_WMAX - 1; q > 0; --q) h[q] = h[q - 1];
+      h[0] = x;
+      Xr[i] = x;
+    }
+  }
+  // L^-T rows: row j = L^-1 e_j (zeros before j)
+  if (tid < n) {
+    const int j = tid;
+    double* Zr = P + (int64_t)(n + b + j) * n;
+    for (int i = 0; i < j; ++i) Zr[i] = 0.0;
+    double h[BAND_WMAX];
+#pragma unroll
+    for (int q = 0; q < BAND_WMAX; ++q) h[q] = 0.0;
+    for (int i = j; i < n; ++i) {
+      double acc = i == j ? 1.0 : 0.0;
+      const double* Li = Lb + (int64_t)i * W1;
+#pragma unroll
+      for (int q = 0; q < BAND_WMAX; ++q)
+        if (q < w) acc = __fma_rn(-Li[q + 1], h[q], acc);
+      const double z = acc * dinv[i];
+#pragma unroll
+      for (int q = BAND_WMAX - 1; q > 0; --q) h[q] = h[q - 1];
+      h[0] = z;
+      Zr[i] = z;
+    }
+  }
+  __syncthreads();   // X^T rows written (global, read back through L2 below)
+  // U = X^T X (b x b): 64-column chunks of X^T in shared memory, a 4 x 4 output block per thread
+  if (b > 0) {
+    double acc[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+    const int ti = tid / 16, tj = tid % 16;   // rows 4ti.., columns 4tj.. (b <= 64)
+    for (int c0 = 0; c0 < n; c0 += 64) {
+      const int cw = min(64, n - c0);
+      __syncthreads();
+      for (int e = tid; e < b * 64; e += NT) {
+        const int r = e / 64, c = e % 64;
+        Xs[e] = c < cw ? __ldcg(P + (int64_t)(n + r) * n + c0 + c) : 0.0;
+      }
+      __syncthreads();
+      for (int c = 0; c < cw; ++c) {
+        double xa[4], xb[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int ra = 4 * ti + x, rb = 4 * tj + x;
+          xa[x] = ra < b ? Xs[ra * 64 + c] : 0.0;
+          xb[x] = rb < b ? Xs[rb * 64 + c] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = __fma_rn(xa[x], xb[y], acc[x][y]);
+      }
+    }
+    double* U = ca.U + ca.U_off[t];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int ra = 4 * ti + x, rb = 4 * tj + y;
+        if (ra < b && rb < b) U[(int64_t)ra * b + rb] = acc[x][y];
+      }
+  }
+}
+
+// flag = 1 if some interior DOF couples, inside its own group, to a member more than w positions
+// away (the banded cell path is then not applicable)
+__global__ void k_band_check(const int64_t* rowptr, const int* col, const int* gid, const int* pos,
+                             const uint8_t* is_int, int64_t N, int w, int* flag) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const int g = gid[r];
+  if (!is_int[g]) return;
+  for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+    const int c = col[e];
+    if (gid[c] == g && abs(pos[c] - pos[r]) > w) {
+      atomicExch(flag, 1);
+      return;
+    }
+  }
+}
+
 // A_BB -= sum_c X_c^T X_c, owner-computes per target block, contributions in cell order.
 __global__ void __launch_bounds__(NT) k_schur(LevelDev lv, SchurArgs sa) {
   const int tau = blockIdx.x;
@@ -793,13 +964,13 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     for (; i < mn; ++i) {
       if (i > 0 && best.v < cut2) break;
       const int pb = best.i, p = col_at[pb];
-      const double rd = rdv[p];
+      const double rd = i == 0 ? rdv[p] : sqrt(fmax(d[p], 0.0));   // (only the pivot needs it)
       if (i == 0) {
         cut = cutrel * rd;
         cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
       }
       if (rd > cut) ++r;
-      const double inv = invv[p];
+      const double inv = i == 0 ? invv[p] : (rd > 0.0 ? 1.0 / rd : 0.0);
       double* row = Rsm + i * k;
       for (int b = lane; b < k; b += 32) {
         double v;
@@ -834,11 +1005,6 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
         const double rv = row[col];
         const double dn = __fma_rn(-rv, rv, d[col]);
         d[col] = dn;
-        {
-          const double rdn = sqrt(fmax(dn, 0.0));
-          rdv[col] = rdn;
-          invv[col] = rdn > 0.0 ? 1.0 / rdn : 0.0;
-        }
         double w1 = vn1[j];
         if (w1 != 0.0) {
           const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
@@ -3497,6 +3663,23 @@ void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& up
     k_big_trsm<<<trsm.nwork, NT, BIG_SMEM, s>>>(trsm);
   }
   launch_big_nt(upd, 0, s);
+}
+bool band_cells_fit(int nmax, int bmax, int w) {
+  const size_t bytes = ((size_t)nmax * (w + 1) + nmax + (size_t)bmax * 64) * sizeof(double);
+  return w <= BAND_WMAX && nmax <= NT && bmax <= 64 && bytes <= 200 * 1024;
+}
+void launch_cell_band(const LevelDev& lv, const CellArgs& ca, const int* list, int count, int nmax, int bmax, int w,
+                      DevStatus* st, cudaStream_t s) {
+  if (count == 0) return;
+  const size_t bytes = ((size_t)nmax * (w + 1) + nmax + (size_t)bmax * 64) * sizeof(double);
+  cudaFuncSetAttribute(k_cell_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_cell_band<<<count, NT, bytes, s>>>(lv, ca, list, w, st);
+}
+void launch_band_check(const int64_t* rowptr, const int* col, const int* gid, const int* pos, const uint8_t* is_int,
+                       int64_t N, int w, int* flag, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_band_check<<<nblk(N, 256), 256, 0, s>>>(rowptr, col, gid, pos, is_int, N, w, flag);
 }
 void launch_big_zero_upper(const BigArgs& a, cudaStream_t s) {
   if (!a.ncell) return;

@@ -82,6 +82,12 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s);
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
 void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);
+// banded level-0 cells (2D): shared-memory fit, the kernel, and the device band check
+bool band_cells_fit(int nmax, int bmax, int w);
+void launch_cell_band(const LevelDev& lv, const CellArgs& ca, const int* list, int count, int nmax, int bmax, int w,
+                      DevStatus* st, cudaStream_t s);
+void launch_band_check(const int64_t* rowptr, const int* col, const int* gid, const int* pos, const uint8_t* is_int,
+                       int64_t N, int w, int* flag, cudaStream_t s);
 void launch_big_zero_upper(const BigArgs& a, cudaStream_t s);   // 0: trailing update, 1: U = X^T X
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s);
 // replay GEMM (N = nrhs <= 32, A streamed from global, B chunk in shared memory); falls back to launch_bgemm
