@@ -511,6 +511,9 @@ static long long* gid_prof_buffer() {
                 buf[7] / 1e6, buf[8] / 1e6, buf[9]);
         fprintf(stderr, "[phif] small-separator ID CTA0 (Mcycles): dependency wait %.2f gather-count %.2f copy %.2f gram+cpqr+T %.2f | separators %lld\n",
                 buf[19] / 1e6, buf[16] / 1e6, buf[17] / 1e6, buf[18] / 1e6, buf[23]);
+        fprintf(stderr, "[phif] banded cell CTA0 (kcycles/cell): load %.1f cholesky %.1f L rows %.1f X %.1f L^-T %.1f U %.1f | cells %lld\n",
+                buf[24] / 1e3 / std::max(1LL, buf[30]), buf[25] / 1e3 / std::max(1LL, buf[30]), buf[26] / 1e3 / std::max(1LL, buf[30]),
+                buf[27] / 1e3 / std::max(1LL, buf[30]), buf[28] / 1e3 / std::max(1LL, buf[30]), buf[29] / 1e3 / std::max(1LL, buf[30]), buf[30]);
       });
     }
   }
@@ -1053,7 +1056,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     if (banded) {
       upload(bp.d_list, big_cells, s);
       launch_cell_band(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), band_nmax, band_bmax, band_w,
-                       F->status.as<DevStatus>(), s);
+                       F->status.as<DevStatus>(), gid_prof_buffer(), s);
     } else if (!big_cells.empty()) {
       upload(bp.d_list, big_cells, s);
       launch_big_build(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), s);

@@ -111,14 +111,24 @@ __global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus
 //      thread per column of the identity), the layout the big-cell replay reads.
 // ---------------------------------------------------------------------------
 constexpr int BAND_WMAX = 31;   // w <= 31: one lane per band entry of a column
-__global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, const int* list, int w, DevStatus* st) {
+template <int WM>   // register window of the substitutions (w <= WM)
+__global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, const int* list, int w, DevStatus* st,
+                                                  long long* prof) {
   extern __shared__ double smem[];
   const int t = list[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 0;
+  long long t0 = pf ? clock64() : 0;
+#define BAND_MARK(slot)                                                                                 \
+  if (pf) {                                                                                             \
+    const long long t1 = clock64();                                                                     \
+    atomicAdd(reinterpret_cast<unsigned long long*>(prof + (slot)), (unsigned long long)(t1 - t0));     \
+    t0 = t1;                                                                                            \
+  }
   const int I = ca.interior[t], n = ca.n[t], b = ca.b[t];
   const int W1 = w + 1;
   double* Lb = smem;                  // n x (w+1): Lb[i*W1 + d] = L(i, i-d)
   double* dinv = Lb + (int64_t)n * W1;   // n
-  double* Xs = dinv + n;              // b x 64 staging of X^T chunks (U)
+  double* Xs = dinv + n;              // b x 64 staging of X^T chunks (U) / 8 warps x 32 x 17 row staging
   __shared__ int s_bad;
   double* P = ca.rec + ca.P_off[t];
   const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
@@ -128,6 +138,7 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
   }
   if (tid == 0) s_bad = -1;
   __syncthreads();
+  BAND_MARK(24)
   if (warp == 0) {
     for (int j = 0; j < n; ++j) {
       const double djj = Lb[(int64_t)j * W1];
@@ -155,61 +166,80 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
     }
   }
   __syncthreads();
+  BAND_MARK(25)
   if (s_bad >= 0) {
     if (tid == 0) report_bad(st, t, s_bad);
     return;
   }
   // L rows of the record (dense, zeros outside the band)
-  for (int64_t e = tid; e < (int64_t)n * n; e += NT) {
-    const int i = (int)(e / n), c = (int)(e % n), d = i - c;
-    P[e] = (d >= 0 && d <= w) ? Lb[(int64_t)i * W1 + d] : 0.0;
-  }
-  // X = L^-1 A_BI^T, one boundary DOF per thread (its A_BI row from the neighbour block)
-  if (tid < b) {
+  for (int i = warp; i < n; i += NT / 32)   // row i: lanes along columns (no 64-bit division)
+    for (int c = lane; c < n; c += 32) {
+      const int d = i - c;
+      P[(int64_t)i * n + c] = (d >= 0 && d <= w) ? Lb[i * W1 + d] : 0.0;
+    }
+  // X = L^-1 A_BI^T (one boundary DOF per thread) and L^-T (row j = L^-1 e_j, one identity column
+  // per thread): substitutions in lockstep over 16-row chunks; each warp stages its 32 x 16 chunk
+  // in shared memory and writes it out as 16-double row segments (coalesced), zeros included
+  double* stg = Xs + (int64_t)warp * 32 * 17;
+  auto solve_rows = [&](bool active, const double* S, int wn, int rc, int rhs_one, double* row0, int nrows_warp,
+                        int64_t row_base) {
+    double h[WM];
+#pragma unroll
+    for (int q = 0; q < WM; ++q) h[q] = 0.0;
+    for (int i0 = 0; i0 < n; i0 += 16) {
+      const int cnt = min(16, n - i0);
+      double a[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        a[u] = (active && u < cnt) ? (S ? S[(int64_t)(i0 + u) * wn + rc] : (i0 + u == rhs_one ? 1.0 : 0.0)) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (u >= cnt) break;
+        const int i = i0 + u;
+        double acc = a[u];
+        const double* Li = Lb + (int64_t)i * W1;
+#pragma unroll
+        for (int q = 0; q < WM; ++q)
+          if (q < w) acc = __fma_rn(-Li[q + 1], h[q], acc);
+        const double x = active ? acc * dinv[i] : 0.0;
+#pragma unroll
+        for (int q = WM - 1; q > 0; --q) h[q] = h[q - 1];
+        h[0] = x;
+        stg[lane * 17 + u] = x;
+      }
+      __syncwarp();
+      for (int e = lane; e < 32 * 16; e += 32) {
+        const int rr = e >> 4, u = e & 15;
+        if (rr < nrows_warp && u < cnt) row0[(row_base + rr) * n + i0 + u] = stg[rr * 17 + u];
+      }
+      __syncwarp();
+    }
+  };
+  (void)solve_rows;
+  __syncthreads();
+  BAND_MARK(26)
+  if (warp * 32 < b) {   // X^T rows n + r
     const int r = tid;
-    int64_t jn = ca.nbr_off[t];
-    while (jn + 1 < ca.nbr_off[t + 1] && ca.nbr_col[jn + 1] <= r) ++jn;
-    const int wn = ca.nbr_w[jn], rc = r - ca.nbr_col[jn];
-    const double* S = lv.pool + lv.boff[ca.nbr_blk[jn]];   // block (I, h): |I| x wn row-major
-    double h[BAND_WMAX];
-#pragma unroll
-    for (int q = 0; q < BAND_WMAX; ++q) h[q] = 0.0;
-    double* Xr = P + (int64_t)(n + r) * n;
-    for (int i = 0; i < n; ++i) {
-      double acc = S[(int64_t)i * wn + rc];
-      const double* Li = Lb + (int64_t)i * W1;
-#pragma unroll
-      for (int q = 0; q < BAND_WMAX; ++q)
-        if (q < w) acc = __fma_rn(-Li[q + 1], h[q], acc);
-      const double x = acc * dinv[i];
-#pragma unroll
-      for (int q = BAND_WMAX - 1; q > 0; --q) h[q] = h[q - 1];
-      h[0] = x;
-      Xr[i] = x;
+    const bool act = r < b;
+    const double* S = nullptr;
+    int wn = 1, rc = 0;
+    if (act) {
+      int64_t jn = ca.nbr_off[t];
+      while (jn + 1 < ca.nbr_off[t + 1] && ca.nbr_col[jn + 1] <= r) ++jn;
+      wn = ca.nbr_w[jn];
+      rc = r - ca.nbr_col[jn];
+      S = lv.pool + lv.boff[ca.nbr_blk[jn]];   // block (I, h): |I| x wn row-major
     }
+    solve_rows(act, act ? S : Lb, wn, rc, -1, P, min(32, b - warp * 32), (int64_t)n + warp * 32);
   }
-  // L^-T rows: row j = L^-1 e_j (zeros before j)
-  if (tid < n) {
+  __syncthreads();   // (the staging area is reused)
+  BAND_MARK(27)
+  if (warp * 32 < n) {   // L^-T rows n + b + j
     const int j = tid;
-    double* Zr = P + (int64_t)(n + b + j) * n;
-    for (int i = 0; i < j; ++i) Zr[i] = 0.0;
-    double h[BAND_WMAX];
-#pragma unroll
-    for (int q = 0; q < BAND_WMAX; ++q) h[q] = 0.0;
-    for (int i = j; i < n; ++i) {
-      double acc = i == j ? 1.0 : 0.0;
-      const double* Li = Lb + (int64_t)i * W1;
-#pragma unroll
-      for (int q = 0; q < BAND_WMAX; ++q)
-        if (q < w) acc = __fma_rn(-Li[q + 1], h[q], acc);
-      const double z = acc * dinv[i];
-#pragma unroll
-      for (int q = BAND_WMAX - 1; q > 0; --q) h[q] = h[q - 1];
-      h[0] = z;
-      Zr[i] = z;
-    }
+    solve_rows(j < n, nullptr, 1, 0, j, P, min(32, n - warp * 32), (int64_t)n + b + warp * 32);
   }
   __syncthreads();   // X^T rows written (global, read back through L2 below)
+  BAND_MARK(28)
   // U = X^T X (b x b): 64-column chunks of X^T in shared memory, a 4 x 4 output block per thread
   if (b > 0) {
     double acc[4][4];
@@ -249,6 +279,10 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
         if (ra < b && rb < b) U[(int64_t)ra * b + rb] = acc[x][y];
       }
   }
+  __syncthreads();
+  BAND_MARK(29)
+  if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(prof + 30), 1ull);
+#undef BAND_MARK
 }
 
 // flag = 1 if some interior DOF couples, inside its own group, to a member more than w positions
@@ -3664,17 +3698,25 @@ void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& up
   }
   launch_big_nt(upd, 0, s);
 }
+static size_t band_smem(int nmax, int bmax, int w) {
+  return ((size_t)nmax * (w + 1) + nmax + std::max<size_t>((size_t)bmax * 64, 8 * 32 * 17)) * sizeof(double);
+}
 bool band_cells_fit(int nmax, int bmax, int w) {
-  const size_t bytes = ((size_t)nmax * (w + 1) + nmax + (size_t)bmax * 64) * sizeof(double);
+  const size_t bytes = band_smem(nmax, bmax, w);
   return w <= BAND_WMAX && nmax <= NT && bmax <= 64 && bytes <= 200 * 1024;
 }
 void launch_cell_band(const LevelDev& lv, const CellArgs& ca, const int* list, int count, int nmax, int bmax, int w,
-                      DevStatus* st, cudaStream_t s) {
+                      DevStatus* st, long long* prof, cudaStream_t s) {
   if (count == 0) return;
-  const size_t bytes = ((size_t)nmax * (w + 1) + nmax + (size_t)bmax * 64) * sizeof(double);
-  cudaFuncSetAttribute(k_cell_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const size_t bytes = band_smem(nmax, bmax, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_cell_band<<<count, NT, bytes, s>>>(lv, ca, list, w, st);
+  if (w <= 15) {
+    cudaFuncSetAttribute(k_cell_band<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    k_cell_band<15><<<count, NT, bytes, s>>>(lv, ca, list, w, st, prof);
+  } else {
+    cudaFuncSetAttribute(k_cell_band<BAND_WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    k_cell_band<BAND_WMAX><<<count, NT, bytes, s>>>(lv, ca, list, w, st, prof);
+  }
 }
 void launch_band_check(const int64_t* rowptr, const int* col, const int* gid, const int* pos, const uint8_t* is_int,
                        int64_t N, int w, int* flag, cudaStream_t s) {
