@@ -1055,8 +1055,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     if (banded) {
       upload(bp.d_list, big_cells, s);
+      DBuf scratch;   // band of L + reciprocals per cell, from the one-warp Cholesky
+      scratch.alloc((size_t)big_cells.size() * band_scratch_stride(band_nmax, band_w) * sizeof(double), s);
       launch_cell_band(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), band_nmax, band_bmax, band_w,
-                       F->status.as<DevStatus>(), gid_prof_buffer(), s);
+                       scratch.as<double>(), F->status.as<DevStatus>(), gid_prof_buffer(), s);
     } else if (!big_cells.empty()) {
       upload(bp.d_list, big_cells, s);
       launch_big_build(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), s);

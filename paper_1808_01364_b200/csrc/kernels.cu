@@ -111,9 +111,65 @@ __global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus
 //      thread per column of the identity), the layout the big-cell replay reads.
 // ---------------------------------------------------------------------------
 constexpr int BAND_WMAX = 31;   // w <= 31: one lane per band entry of a column
+// Banded Cholesky of the level-0 cells, one warp per cell (many cells in flight per SM hide the
+// per-column dependency chain): register window of w+1 rows, band of L and 1/diag to a scratch
+// area read by k_cell_band; NotSpd reported like the dense path (cell, 0-based pivot).
+template <int WM>
+__global__ void __launch_bounds__(256) k_band_chol(LevelDev lv, CellArgs ca, const int* list, int count, int w,
+                                                   double* scratch, int64_t stride, DevStatus* st) {
+  const int wid = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (wid >= count) return;
+  const int t = list[wid], I = ca.interior[t], n = ca.n[t];
+  const int W1 = w + 1;
+  const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
+  double* Lb = scratch + (int64_t)wid * stride;   // n x (w+1) band, then n reciprocals
+  double* dinv = Lb + (int64_t)n * W1;
+  // lane d <= w holds row j+d of the active band, R[c] = A(j+d, j+c) (c <= d); per column:
+  // broadcast the pivot, scale the column, rank-1 update of the window (shuffles), shift the
+  // window one row/column down and bring the next row in
+  double R[WM + 1], nxt[WM + 1];
+#pragma unroll
+  for (int c = 0; c <= WM; ++c) R[c] = (lane <= w && c <= lane && lane < n) ? A[(int64_t)lane * n + c] : 0.0;
+#pragma unroll
+  for (int c = 0; c <= WM; ++c)   // the row entering after column 0 (loaded one column ahead)
+    nxt[c] = (lane == w && 1 + w < n && c <= w) ? A[(int64_t)(1 + w) * n + 1 + c] : 0.0;
+  for (int j = 0; j < n; ++j) {
+    const double djj = __shfl_sync(0xffffffffu, R[0], 0);
+    if (!(djj > 0.0)) {
+      if (lane == 0) report_bad(st, t, j);
+      return;
+    }
+    const double ljj = sqrt(djj), rinv = 1.0 / ljj;
+    const bool row_ok = lane >= 1 && lane <= w && j + lane < n;
+    const double cd = row_ok ? R[0] * rinv : 0.0;   // L(j+lane, j)
+    if (lane == 0) {
+      Lb[(int64_t)j * W1] = ljj;
+      dinv[j] = rinv;
+    } else if (row_ok) {
+      Lb[(int64_t)(j + lane) * W1 + lane] = cd;
+    }
+#pragma unroll
+    for (int e = 1; e <= WM; ++e) {   // L(j+d, j+e) -= c_d c_e, 1 <= e <= d
+      const double ce = __shfl_sync(0xffffffffu, cd, e);
+      if (e <= lane) R[e] = __fma_rn(-cd, ce, R[e]);
+    }
+#pragma unroll
+    for (int c = 0; c < WM; ++c) R[c] = __shfl_down_sync(0xffffffffu, R[c + 1], 1);
+    R[WM] = 0.0;
+    if (lane == w) {   // row j+1+w enters (prefetched); prefetch row j+2+w
+      const int r = j + 2 + w;
+#pragma unroll
+      for (int c = 0; c <= WM; ++c) {
+        R[c] = nxt[c];
+        nxt[c] = (r < n && c <= w) ? A[(int64_t)r * n + j + 2 + c] : 0.0;
+      }
+    }
+  }
+}
+
 template <int WM>   // register window of the substitutions (w <= WM)
 __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, const int* list, int w, DevStatus* st,
-                                                  long long* prof) {
+                                                  long long* prof, const double* scratch, int64_t stride) {
   extern __shared__ double smem[];
   const int t = list[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool pf = prof != nullptr && blockIdx.x == 0 && tid == 0;
@@ -131,46 +187,14 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
   double* Xs = dinv + n;              // b x 64 staging of X^T chunks (U) / 8 warps x 32 x 17 row staging
   __shared__ int s_bad;
   double* P = ca.rec + ca.P_off[t];
-  const double* A = lv.pool + lv.boff[lv.diag_blk[I]];
-  for (int e = tid; e < n * W1; e += NT) {
-    const int i = e / W1, d = e % W1;
-    Lb[e] = i - d >= 0 ? A[(int64_t)i * n + i - d] : 0.0;
-  }
-  if (tid == 0) s_bad = -1;
+  // band of L and 1/diag from the one-warp Cholesky (k_band_chol)
+  const double* Sc = scratch + (int64_t)blockIdx.x * stride;
+  for (int e = tid; e < n * W1 + n; e += NT) Lb[e] = Sc[e];
+  if (tid == 0) s_bad = st->first_bad == ~0ull ? -1 : 0;   // (a failed cell anywhere: results unused)
   __syncthreads();
   BAND_MARK(24)
-  if (warp == 0) {
-    for (int j = 0; j < n; ++j) {
-      const double djj = Lb[(int64_t)j * W1];
-      if (!(djj > 0.0)) {
-        if (lane == 0) s_bad = j;
-        break;
-      }
-      const double ljj = sqrt(djj), rinv = 1.0 / ljj;
-      const int d = lane + 1;   // column j, row j + d
-      double c = 0.0;
-      if (d <= w && j + d < n) {
-        c = Lb[(int64_t)(j + d) * W1 + d] * rinv;
-        Lb[(int64_t)(j + d) * W1 + d] = c;
-      }
-      if (lane == 0) {
-        Lb[(int64_t)j * W1] = ljj;
-        dinv[j] = rinv;
-      }
-      // trailing update of the band: L(j+d, j+e) -= c_d c_e, 1 <= e <= d <= w
-      for (int e = 1; e <= w; ++e) {
-        const double ce = __shfl_sync(0xffffffffu, c, e - 1);
-        if (d <= w && d >= e && j + d < n) Lb[(int64_t)(j + d) * W1 + (d - e)] -= c * ce;
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
   BAND_MARK(25)
-  if (s_bad >= 0) {
-    if (tid == 0) report_bad(st, t, s_bad);
-    return;
-  }
+  if (s_bad >= 0) return;   // (NotSpd: reported by k_band_chol; the factorization stops)
   // L rows of the record (dense, zeros outside the band)
   for (int i = warp; i < n; i += NT / 32)   // row i: lanes along columns (no 64-bit division)
     for (int c = lane; c < n; c += 32) {
@@ -196,12 +220,15 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
       for (int u = 0; u < 16; ++u) {
         if (u >= cnt) break;
         const int i = i0 + u;
-        double acc = a[u];
+        double acc = a[u], acc2 = 0.0;   // two chains: even / odd band offsets
         const double* Li = Lb + (int64_t)i * W1;
 #pragma unroll
         for (int q = 0; q < WM; ++q)
-          if (q < w) acc = __fma_rn(-Li[q + 1], h[q], acc);
-        const double x = active ? acc * dinv[i] : 0.0;
+          if (q < w) {
+            if (q & 1) acc2 = __fma_rn(-Li[q + 1], h[q], acc2);
+            else acc = __fma_rn(-Li[q + 1], h[q], acc);
+          }
+        const double x = active ? (acc + acc2) * dinv[i] : 0.0;
 #pragma unroll
         for (int q = WM - 1; q > 0; --q) h[q] = h[q - 1];
         h[0] = x;
@@ -3705,17 +3732,22 @@ bool band_cells_fit(int nmax, int bmax, int w) {
   const size_t bytes = band_smem(nmax, bmax, w);
   return w <= BAND_WMAX && nmax <= NT && bmax <= 64 && bytes <= 200 * 1024;
 }
+int64_t band_scratch_stride(int nmax, int w) { return (int64_t)nmax * (w + 2); }
 void launch_cell_band(const LevelDev& lv, const CellArgs& ca, const int* list, int count, int nmax, int bmax, int w,
-                      DevStatus* st, long long* prof, cudaStream_t s) {
+                      double* scratch, DevStatus* st, long long* prof, cudaStream_t s) {
   if (count == 0) return;
   const size_t bytes = band_smem(nmax, bmax, w);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  const int64_t stride = band_scratch_stride(nmax, w);
+  const int cb = (count + 7) / 8;
   if (w <= 15) {
+    k_band_chol<15><<<cb, 256, 0, s>>>(lv, ca, list, count, w, scratch, stride, st);
     cudaFuncSetAttribute(k_cell_band<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    k_cell_band<15><<<count, NT, bytes, s>>>(lv, ca, list, w, st, prof);
+    k_cell_band<15><<<count, NT, bytes, s>>>(lv, ca, list, w, st, prof, scratch, stride);
   } else {
+    k_band_chol<BAND_WMAX><<<cb, 256, 0, s>>>(lv, ca, list, count, w, scratch, stride, st);
     cudaFuncSetAttribute(k_cell_band<BAND_WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    k_cell_band<BAND_WMAX><<<count, NT, bytes, s>>>(lv, ca, list, w, st, prof);
+    k_cell_band<BAND_WMAX><<<count, NT, bytes, s>>>(lv, ca, list, w, st, prof, scratch, stride);
   }
 }
 void launch_band_check(const int64_t* rowptr, const int* col, const int* gid, const int* pos, const uint8_t* is_int,

@@ -84,8 +84,9 @@ void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& up
 void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);
 // banded level-0 cells (2D): shared-memory fit, the kernel, and the device band check
 bool band_cells_fit(int nmax, int bmax, int w);
+int64_t band_scratch_stride(int nmax, int w);   // doubles of one cell's band + reciprocals
 void launch_cell_band(const LevelDev& lv, const CellArgs& ca, const int* list, int count, int nmax, int bmax, int w,
-                      DevStatus* st, long long* prof, cudaStream_t s);
+                      double* scratch, DevStatus* st, long long* prof, cudaStream_t s);
 void launch_band_check(const int64_t* rowptr, const int* col, const int* gid, const int* pos, const uint8_t* is_int,
                        int64_t N, int w, int* flag, cudaStream_t s);
 void launch_big_zero_upper(const BigArgs& a, cudaStream_t s);   // 0: trailing update, 1: U = X^T X
