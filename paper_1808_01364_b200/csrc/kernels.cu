@@ -3037,6 +3037,37 @@ __global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int
   const int n = a.n[t];
   const int* I = a.I + a.I_off[t];
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
+  if (k == 32 && n <= 16) {   // lane = right-hand side, the group's rows in registers
+    // indices first (one per lane, then shuffled), every row load in flight before the solve
+    const int myI = lane < n ? I[lane] : 0;
+    double y[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int gi = __shfl_sync(0xffffffffu, myI, i);
+      y[i] = i < n ? x[(int64_t)gi * 32 + lane] : 0.0;
+    }
+    double z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      double acc = 0.0;
+      if (up) {
+#pragma unroll
+        for (int j = 0; j <= i; ++j)
+          if (i < n) acc = __fma_rn(__ldg(LiT + (int64_t)j * n + i), y[j], acc);
+      } else {
+#pragma unroll
+        for (int j = i; j < 16; ++j)
+          if (j < n) acc = __fma_rn(__ldg(LiT + (int64_t)i * n + j), y[j], acc);
+      }
+      z[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int gi = __shfl_sync(0xffffffffu, myI, i);
+      if (i < n) x[(int64_t)gi * 32 + lane] = z[i];
+    }
+    return;
+  }
   if (k == 32) {   // 32 right-hand sides: lane = right-hand side, no index division
     double* Y = ldn > 0 ? smem + (size_t)warp * ldn * 32 : a.work + a.work_off[t] * 32;
     for (int i = 0; i < n; ++i) Y[i * 32 + lane] = x[(int64_t)I[i] * 32 + lane];
@@ -3115,8 +3146,35 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
   double* Yr = Ys + (size_t)r * k;
   double* Z = Yr + (size_t)kt * k;
   if (k == 32) {   // lane = right-hand side: every lane works on its own column (no warp sync)
-    for (int q = 0; q < r; ++q) Ys[q * 32 + lane] = x[(int64_t)S[q] * 32 + lane];
-    for (int j = 0; j < kt; ++j) Yr[j * 32 + lane] = x[(int64_t)R[j] * 32 + lane];
+    // gathers: indices one per lane (shuffled), 8 row loads in flight before their stores
+    for (int q0 = 0; q0 < r; q0 += 32) {
+      const int myS = q0 + lane < r ? S[q0 + lane] : 0;
+      for (int q1 = 0; q1 < min(32, r - q0); q1 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int gi = __shfl_sync(0xffffffffu, myS, (q1 + u) & 31);
+          v[u] = q0 + q1 + u < r ? x[(int64_t)gi * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + q1 + u < r) Ys[(q0 + q1 + u) * 32 + lane] = v[u];
+      }
+    }
+    for (int j0 = 0; j0 < kt; j0 += 32) {
+      const int myR = j0 + lane < kt ? R[j0 + lane] : 0;
+      for (int j1 = 0; j1 < min(32, kt - j0); j1 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int gi = __shfl_sync(0xffffffffu, myR, (j1 + u) & 31);
+          v[u] = j0 + j1 + u < kt ? x[(int64_t)gi * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + j1 + u < kt) Yr[(j0 + j1 + u) * 32 + lane] = v[u];
+      }
+    }
     const double* M1 = up ? T : PB;    // b_R -= M1^T b_S
     const double* M3 = up ? PB : T;    // b_S -= M3 z
     for (int j0 = 0; j0 < kt; j0 += 4) {   // four outputs per pass: independent FMA chains
