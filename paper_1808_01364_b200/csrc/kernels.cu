@@ -3037,37 +3037,6 @@ __global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int
   const int n = a.n[t];
   const int* I = a.I + a.I_off[t];
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
-  if (k == 32 && n <= 16) {   // lane = right-hand side, the group's rows in registers
-    // indices first (one per lane, then shuffled), every row load in flight before the solve
-    const int myI = lane < n ? I[lane] : 0;
-    double y[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int gi = __shfl_sync(0xffffffffu, myI, i);
-      y[i] = i < n ? x[(int64_t)gi * 32 + lane] : 0.0;
-    }
-    double z[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      double acc = 0.0;
-      if (up) {
-#pragma unroll
-        for (int j = 0; j <= i; ++j)
-          if (i < n) acc = __fma_rn(__ldg(LiT + (int64_t)j * n + i), y[j], acc);
-      } else {
-#pragma unroll
-        for (int j = i; j < 16; ++j)
-          if (j < n) acc = __fma_rn(__ldg(LiT + (int64_t)i * n + j), y[j], acc);
-      }
-      z[i] = acc;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int gi = __shfl_sync(0xffffffffu, myI, i);
-      if (i < n) x[(int64_t)gi * 32 + lane] = z[i];
-    }
-    return;
-  }
   if (k == 32) {   // 32 right-hand sides: lane = right-hand side, no index division
     double* Y = ldn > 0 ? smem + (size_t)warp * ldn * 32 : a.work + a.work_off[t] * 32;
     for (int i = 0; i < n; ++i) Y[i * 32 + lane] = x[(int64_t)I[i] * 32 + lane];
