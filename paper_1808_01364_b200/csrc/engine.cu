@@ -828,11 +828,15 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     const int nsk = P.root ? 0 : (int)P.skeleton.size();
     std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk), rows_bound(nsk);
     int64_t work = 0, iwork = 0, aw = 0;
-    for (int t = 0; t < nsk; ++t) {
-      const int g = P.skeleton[t], k = G.size(g);
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < nsk; ++t) {   // coupled rows per separator (the prefix sums follow)
       int64_t rows = 0;
       for (int64_t q = P.sk_nbr_off[t]; q < P.sk_nbr_off[t + 1]; ++q) rows += G.size(P.sk_nbr[q]);
       rows_bound[t] = rows;
+    }
+    for (int t = 0; t < nsk; ++t) {
+      const int g = P.skeleton[t], k = G.size(g);
+      const int64_t rows = rows_bound[t];
       T_off[t] = rec;
       rec += (int64_t)k * k;
       SP_off[t] = rec;

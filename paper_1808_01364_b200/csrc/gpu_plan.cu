@@ -26,6 +26,9 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <mutex>
+#include <tuple>
+#include <cstring>
 
 #include "engine.h"
 #include "gpu_plan.h"
@@ -621,14 +624,83 @@ void plan_level0_device(const Spec& s, const int64_t* rowptr, const int* col, in
   g_launches.fetch_add(nlaunch, std::memory_order_relaxed);
   lap("skeleton lists");
   // ---- host copies of what the level loop reads ------------------------------------------------
+  // one batched transfer: every array into one pinned staging buffer (one synchronisation), then a
+  // single parallel copy-out into recycled (already faulted-in) host vectors
   Groups& g = lp.grp;
   g.level = 0;
   g.G = G;
-  down(g.off, dp.goff, G + 1, st);
-  down(g.mem, dp.mem, N, st);
-  down(g.kind, dp.kind, G, st);
   std::vector<int> hkey;
-  down(hkey, gkey, G, st);
+  {
+    struct Item {
+      void* host;
+      const void* dev;
+      size_t bytes;
+    };
+    std::vector<Item> items;
+    auto want_i = [&](std::vector<int>& h, const DBuf& d, int64_t n) {
+      pool_take(h, n);
+      if (n) items.push_back({h.data(), d.p, (size_t)n * sizeof(int)});
+    };
+    auto want_l = [&](std::vector<int64_t>& h, const DBuf& d, int64_t n) {
+      pool_take(h, n);
+      if (n) items.push_back({h.data(), d.p, (size_t)n * sizeof(int64_t)});
+    };
+    want_l(g.off, dp.goff, G + 1);
+    want_i(g.mem, dp.mem, N);
+    want_i(g.kind, dp.kind, G);
+    want_i(hkey, gkey, G);
+    want_i(lp.pat.bg, dp.bg, nb);
+    want_i(lp.pat.bh, dp.bh, nb);
+    want_i(lp.interior, dp.interior, p);
+    want_i(lp.precond, dp.precond, r);
+    want_i(lp.skeleton, dp.skeleton, nsk);
+    want_l(lp.cell_nbr_off, dp.cell_nbr_off, p + 1);
+    want_i(lp.cell_nbr, dp.cell_nbr, ncn);
+    want_i(lp.cell_n, dp.cell_n, p);
+    want_i(lp.cell_b, dp.cell_b, p);
+    want_i(lp.tgt_blk, dp.tgt_blk, dp.ntgt);
+    want_i(lp.scale_blk, dp.scale_blk, nscale);
+    want_l(lp.sk_nbr_off, dp.sk_nbr_off, nsk + 1);
+    want_i(lp.sk_nbr, dp.sk_nbr, nskn);
+    size_t tot = 0;
+    for (auto& it : items) tot += (it.bytes + 255) & ~size_t(255);
+    static char* pin = nullptr;
+    static size_t pin_cap = 0;
+    static std::mutex pin_mu;
+    std::lock_guard<std::mutex> lock(pin_mu);
+    if (tot > pin_cap) {
+      if (pin) cudaFreeHost(pin);
+      pin_cap = tot + (tot >> 2);
+      if (cudaHostAlloc((void**)&pin, pin_cap, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        pin = nullptr;
+        pin_cap = 0;
+      }
+    }
+    if (pin) {
+      size_t o = 0;
+      std::vector<size_t> at(items.size());
+      for (size_t q = 0; q < items.size(); ++q) {
+        at[q] = o;
+        GCK(cudaMemcpyAsync(pin + o, items[q].dev, items[q].bytes, cudaMemcpyDeviceToHost, st));
+        o += (items[q].bytes + 255) & ~size_t(255);
+      }
+      GCK(cudaStreamSynchronize(st));
+      // chunks of <= 1 MB over all arrays, copied out in parallel
+      std::vector<std::tuple<size_t, size_t, size_t>> chunks;   // (item, offset, length)
+      for (size_t q = 0; q < items.size(); ++q)
+        for (size_t a0 = 0; a0 < items[q].bytes; a0 += (size_t)1 << 20)
+          chunks.emplace_back(q, a0, std::min<size_t>((size_t)1 << 20, items[q].bytes - a0));
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int64_t c = 0; c < (int64_t)chunks.size(); ++c) {
+        const auto& ck = chunks[c];
+        const size_t q = std::get<0>(ck), a0 = std::get<1>(ck), len = std::get<2>(ck);
+        memcpy(static_cast<char*>(items[q].host) + a0, pin + at[q] + a0, len);
+      }
+    } else {
+      for (auto& it : items) download_bytes(it.host, it.dev, it.bytes, st);
+    }
+  }
   g.q.assign(3 * (size_t)G, 0);
   g.bits.assign(G, 0);
   for (int i = 0; i < G; ++i) {
@@ -641,19 +713,6 @@ void plan_level0_device(const Spec& s, const int64_t* rowptr, const int* col, in
   }
   lp.level = 0;
   lp.root = s.L == 0;
-  down(lp.pat.bg, dp.bg, nb, st);
-  down(lp.pat.bh, dp.bh, nb, st);
-  down(lp.interior, dp.interior, p, st);
-  down(lp.precond, dp.precond, r, st);
-  down(lp.skeleton, dp.skeleton, nsk, st);
-  down(lp.cell_nbr_off, dp.cell_nbr_off, p + 1, st);
-  down(lp.cell_nbr, dp.cell_nbr, ncn, st);
-  down(lp.cell_n, dp.cell_n, p, st);
-  down(lp.cell_b, dp.cell_b, p, st);
-  down(lp.tgt_blk, dp.tgt_blk, dp.ntgt, st);
-  down(lp.scale_blk, dp.scale_blk, nscale, st);
-  down(lp.sk_nbr_off, dp.sk_nbr_off, nsk + 1, st);
-  down(lp.sk_nbr, dp.sk_nbr, nskn, st);
   lap("downloads");
   dp.nblocks = nb;
   dp.ncon = nfill;

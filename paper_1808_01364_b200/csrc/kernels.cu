@@ -3440,8 +3440,11 @@ constexpr size_t NT_SMEM = (size_t)NT_STAGES * NT_STAGE * sizeof(double);
 constexpr int NT_CLD = BT + 1;   // C tile of the trailing update (MODE 0)
 constexpr size_t NT_SMEM0 = (size_t)(2 * NT_STAGE + BT * NT_CLD) * sizeof(double);
 
-template <int MODE>
+// MODE 2 = MODE 0 without the C-tile prefetch: three K stages, C read (coalesced) in the epilogue
+template <int MODE_>
 __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
+  constexpr int MODE = MODE_ == 2 ? 0 : MODE_;
+  constexpr bool CPRE = MODE_ == 0;
   extern __shared__ double smem[];
   const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
   const int n = a.n[c];
@@ -3484,9 +3487,9 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
   // MODE 0 (trailing update C -= A B^T): the C tile is fetched into shared memory by cp.async
   // ahead of the K loop (2 stages, so two CTAs still fit per SM); its read-modify-write latency
   // no longer sits behind the last DMMA
-  constexpr int STG = MODE == 0 ? 2 : NT_STAGES;
+  constexpr int STG = CPRE ? 2 : NT_STAGES;
   double* sC = smem + STG * NT_STAGE;
-  if (MODE == 0) {
+  if (CPRE) {
 #pragma unroll
     for (int q = 0; q < (BT * BT) / NT; ++q) {
       const int e = tid + q * NT, r = e / BT, j = e % BT;
@@ -3537,7 +3540,7 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
     cp_async_wait<0>();
     __syncthreads();
   }
-  double* sT = MODE == 0 ? sC : smem;   // (MODE 1: the drained pipeline stages hold the tile)
+  double* sT = CPRE ? sC : smem;   // (otherwise the drained pipeline stages hold the tile)
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -3545,14 +3548,17 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
         const int i = wm * 16 + x * 8 + g, j = wn * 32 + y * 8 + 2 * t + z;
-        if (MODE == 0) sT[i * NT_CLD + j] -= acc[x][y][z];
+        if (CPRE) sT[i * NT_CLD + j] -= acc[x][y][z];
         else sT[i * NT_CLD + j] = acc[x][y][z];
       }
   __syncthreads();
   if (MODE == 0) {
     for (int e = tid; e < BT * BT; e += NT) {
       const int i = e / BT, j = e % BT;
-      if (i < Mv && j < Nv) P[(int64_t)(ar0 + i) * n + br0 + j] = sT[i * NT_CLD + j];
+      if (i < Mv && j < Nv) {
+        double* pc = P + (int64_t)(ar0 + i) * n + br0 + j;
+        *pc = CPRE ? sT[i * NT_CLD + j] : *pc - sT[i * NT_CLD + j];
+      }
     }
   } else {
     const int b = a.b[c];
@@ -3794,10 +3800,13 @@ void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s) {
   if (!init) {
     cudaFuncSetAttribute(k_big_nt<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM0);
     cudaFuncSetAttribute(k_big_nt<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
+    cudaFuncSetAttribute(k_big_nt<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
     init = true;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM0, s>>>(a);
+  static const bool no_cpre = getenv("PHIF_NT_NOCPRE") != nullptr;
+  if (mode == 0 && no_cpre) k_big_nt<2><<<a.nwork, NT, NT_SMEM, s>>>(a);
+  else if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM0, s>>>(a);
   else k_big_nt<1><<<a.nwork, NT, NT_SMEM, s>>>(a);
 }
 void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s) {
