@@ -653,7 +653,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   // the planner's OpenMP teams leave two cores to the helper threads (boundary reduction lists,
   // staging copies): a statically scheduled team waiting on a preempted thread stalls
   static const int omp_once = [] {
-    if (!getenv("OMP_NUM_THREADS")) omp_set_num_threads(std::max(1, omp_get_num_procs() - 2));
+    // main team + pre-plan team + the reduction-list helper stay within the host's cores
+    if (!getenv("OMP_NUM_THREADS"))
+      omp_set_num_threads(std::max(1, omp_get_num_procs() - std::max(2, omp_get_num_procs() / 4) - 2));
     return 0;
   }();
   (void)omp_once;
@@ -717,6 +719,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       build_level(sp, L.plan, std::move(pairs));
       }
     }
+    // the next level's structure only depends on this level's plan: it is planned on a host
+    // thread while this level's host descriptors are built and its kernels run
+    if (!L.plan.root && !no_preplan)
+      preplan = std::async(std::launch::async, [&sp, &L]() {
+        omp_set_num_threads(std::max(2, omp_get_num_procs() / 4));   // (small team; see below)
+        return preplan_next(sp, L.plan);
+      });
     // device copy of a plan array: taken over from the device planner, else uploaded
     auto dev_arr = [&](DBuf& dst, DBuf& from, const auto& host) {
       if (dp.valid) dst = std::move(from);
@@ -1544,13 +1553,6 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       CK(cudaGetLastError());
       // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     }
-    // the next level's structure is planned on a host thread while the IDs run on the device
-    if (!P.root && !no_preplan)
-      preplan = std::async(std::launch::async, [&sp, &L]() {
-        // a smaller OpenMP team: the main thread keeps its own team for the level's host work
-        omp_set_num_threads(std::max(2, omp_get_num_procs() / 2 - 1));
-        return preplan_next(sp, L.plan);
-      });
     // ranks and redundant flags back to the host (large separator updates, next level planning)
     L.h_rank.resize(nsk);
     std::vector<int> h_rows(nsk);

@@ -3039,13 +3039,24 @@ __global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
   if (k == 32) {   // 32 right-hand sides: lane = right-hand side, no index division
     double* Y = ldn > 0 ? smem + (size_t)warp * ldn * 32 : a.work + a.work_off[t] * 32;
+#pragma unroll 8
     for (int i = 0; i < n; ++i) Y[i * 32 + lane] = x[(int64_t)I[i] * 32 + lane];
+    __syncwarp();
+    // the record loads of each 8-term block are issued together (same sequential FMA order)
     for (int i = 0; i < n; ++i) {
       double s = 0.0;
-      if (up)
-        for (int j = 0; j <= i; ++j) s = __fma_rn(__ldg(LiT + (int64_t)j * n + i), Y[j * 32 + lane], s);
-      else
-        for (int j = i; j < n; ++j) s = __fma_rn(__ldg(LiT + (int64_t)i * n + j), Y[j * 32 + lane], s);
+      const int j0 = up ? 0 : i, j1 = up ? i + 1 : n;
+      int j = j0;
+      for (; j + 8 <= j1; j += 8) {
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          l[u] = up ? __ldg(LiT + (int64_t)(j + u) * n + i) : __ldg(LiT + (int64_t)i * n + j + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = __fma_rn(l[u], Y[(j + u) * 32 + lane], s);
+      }
+      for (; j < j1; ++j) s = __fma_rn(up ? __ldg(LiT + (int64_t)j * n + i) : __ldg(LiT + (int64_t)i * n + j),
+                                       Y[j * 32 + lane], s);
       x[(int64_t)I[i] * 32 + lane] = s;
     }
     return;
@@ -3148,6 +3159,7 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
     const double* M3 = up ? PB : T;    // b_S -= M3 z
     for (int j0 = 0; j0 < kt; j0 += 4) {   // four outputs per pass: independent FMA chains
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
       for (int q = 0; q < r; ++q) {
         const double y = Ys[q * 32 + lane];
 #pragma unroll
@@ -3160,14 +3172,18 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
     }
     for (int i = 0; i < kt; ++i) {
       double sacc = 0.0;
-      if (up)
+      if (up) {
+#pragma unroll 8
         for (int j = 0; j <= i; ++j) sacc = __fma_rn(__ldg(LiT + (int64_t)j * kt + i), Yr[j * 32 + lane], sacc);
-      else
+      } else {
+#pragma unroll 8
         for (int j = i; j < kt; ++j) sacc = __fma_rn(__ldg(LiT + (int64_t)i * kt + j), Yr[j * 32 + lane], sacc);
+      }
       Z[i * 32 + lane] = sacc;
     }
     for (int q0 = 0; q0 < r; q0 += 4) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
       for (int i = 0; i < kt; ++i) {
         const double z = Z[i * 32 + lane];
 #pragma unroll
