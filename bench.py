@@ -223,7 +223,9 @@ def dominant_roofline(stats, hbm_peak, fp64_peak):
     # measured DRAM traffic per launch of the stage's kernel (ncu --set full, committed profile)
     traffic, tnote = None, None
     try:
-        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r01.json")))
+        pdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+        tpath = os.path.join(pdir, "traffic_r02.json")
+        tj = json.load(open(tpath if os.path.exists(tpath) else os.path.join(pdir, "traffic_r01.json")))
         ent = tj.get(f"level {lev} {names[si]}")
         if ent:
             traffic = ent["dram_bytes_per_launch"]

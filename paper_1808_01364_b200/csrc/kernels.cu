@@ -3039,24 +3039,13 @@ __global__ void k_apply_prec_tiny(ApplyPrecArgs a, double* x, int k, int up, int
   const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
   if (k == 32) {   // 32 right-hand sides: lane = right-hand side, no index division
     double* Y = ldn > 0 ? smem + (size_t)warp * ldn * 32 : a.work + a.work_off[t] * 32;
-#pragma unroll 8
     for (int i = 0; i < n; ++i) Y[i * 32 + lane] = x[(int64_t)I[i] * 32 + lane];
-    __syncwarp();
-    // the record loads of each 8-term block are issued together (same sequential FMA order)
     for (int i = 0; i < n; ++i) {
       double s = 0.0;
-      const int j0 = up ? 0 : i, j1 = up ? i + 1 : n;
-      int j = j0;
-      for (; j + 8 <= j1; j += 8) {
-        double l[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          l[u] = up ? __ldg(LiT + (int64_t)(j + u) * n + i) : __ldg(LiT + (int64_t)i * n + j + u);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s = __fma_rn(l[u], Y[(j + u) * 32 + lane], s);
-      }
-      for (; j < j1; ++j) s = __fma_rn(up ? __ldg(LiT + (int64_t)j * n + i) : __ldg(LiT + (int64_t)i * n + j),
-                                       Y[j * 32 + lane], s);
+      if (up)
+        for (int j = 0; j <= i; ++j) s = __fma_rn(__ldg(LiT + (int64_t)j * n + i), Y[j * 32 + lane], s);
+      else
+        for (int j = i; j < n; ++j) s = __fma_rn(__ldg(LiT + (int64_t)i * n + j), Y[j * 32 + lane], s);
       x[(int64_t)I[i] * 32 + lane] = s;
     }
     return;
