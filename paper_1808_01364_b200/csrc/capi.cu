@@ -300,6 +300,7 @@ int phif_plan_check(const phif_matrix* A, int dim, int n, int m, char* report, s
     phif::DevPlan0 dp;
     phif::plan_level0_device(s, M.rowptr.as<int64_t>(), M.col.as<int>(), M.nnz, d, dp, A->stream);
     phif::download_plan0(dp, d, A->stream);
+    phif::compute_waves(d, d.grp.G);
     cudaStreamSynchronize(A->stream);
     auto cmp = [&](const char* name, const auto& a, const auto& b) {
       if (a.size() != b.size() || !std::equal(a.begin(), a.end(), b.begin())) {

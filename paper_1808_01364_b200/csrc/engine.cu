@@ -790,78 +790,24 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       L.by[0] += b0;
     }
     DBG("level %d: host: boundary reduction lists", lev);
-    // precondition records
+    // record sizes of the block-Jacobi groups and separators (their offsets are formed later,
+    // while the GPU eliminates the cells): the pool is allocated for the total now
     const int r = P.root ? 0 : (int)P.precond.size();
     const bool do_prec = (method != 0) && !P.root;
-    std::vector<int64_t> L_off(r), Lg_off(G.G, -1), pI_off(r), pwork(r);
-    std::vector<int> pn(r);
-    int64_t pw = 0;
-    for (int t = 0; t < r; ++t) {
-      const int g = P.precond[t], k = G.size(g);
-      if (do_prec) {
-        L_off[t] = rec;
-        Lg_off[g] = rec;
-        rec += 2 * (int64_t)k * k;   // [L ; L^-T]
-      }
-      pn[t] = k;
-      pI_off[t] = G.off[g];
-      pwork[t] = pw;
-      pw += (k >= APPLY_BIG ? 2 : 1) * k;
-    }
-    L.prec_work_unit = pw;
-    L.h_L_off = L_off;
-    L.h_pI_off = pI_off;
-    L.h_pwork = pwork;
-    L.h_pn = pn;
-    if (do_prec) {
-      double f2 = 0.0, b2 = 0.0;
-#pragma omp parallel for reduction(+ : f2, b2)
-      for (int t = 0; t < r; ++t) {
-        const double k = pn[t];
-        f2 += k * k * k / 3.0;
-        b2 += 8.0 * 3.0 * k * k;
-      }
-      const int64_t nsc = (int64_t)P.scale_blk.size();
-#pragma omp parallel for reduction(+ : f2, b2)
-      for (int64_t q = 0; q < nsc; ++q) {
-        const int b = P.scale_blk[q];
-        const double kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
-        f2 += kg * kg * kh + kg * kh * kh;
-        b2 += 8.0 * 2.0 * kg * kh;
-      }
-      L.fl[2] += f2;
-      L.by[2] += b2;
-    }
-    DBG("level %d: host: precondition records", lev);
-    // skeleton records / workspaces (upper bounds; ranks known after the ID)
     const int nsk = P.root ? 0 : (int)P.skeleton.size();
-    std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk), rows_bound(nsk);
-    int64_t work = 0, iwork = 0, aw = 0;
-#pragma omp parallel for schedule(static)
-    for (int t = 0; t < nsk; ++t) {   // coupled rows per separator (the prefix sums follow)
-      int64_t rows = 0;
-      for (int64_t q = P.sk_nbr_off[t]; q < P.sk_nbr_off[t + 1]; ++q) rows += G.size(P.sk_nbr[q]);
-      rows_bound[t] = rows;
+    int64_t rec_prec = 0, rec_skel = 0;
+#pragma omp parallel for reduction(+ : rec_prec)
+    for (int t = 0; t < r; ++t) {
+      const int64_t k = G.size(P.precond[t]);
+      rec_prec += do_prec ? 2 * k * k : 0;
     }
+#pragma omp parallel for reduction(+ : rec_skel)
     for (int t = 0; t < nsk; ++t) {
-      const int g = P.skeleton[t], k = G.size(g);
-      const int64_t rows = rows_bound[t];
-      T_off[t] = rec;
-      rec += (int64_t)k * k;
-      SP_off[t] = rec;
-      rec += 2 * (int64_t)k * k;   // [L~ ; X~^T ; L~^-T]
-      work_off[t] = work;
-      work += std::max<int64_t>((std::max<int64_t>(rows, 1)) * k + 2 * k, 2 * (int64_t)k * k);
-      iwork_off[t] = iwork;
-      iwork += 3 * (int64_t)k;
-      awork[t] = aw;
-      aw += (k >= APPLY_BIG ? 2 : 1) * k;
+      const int64_t k = G.size(P.skeleton[t]);
+      rec_skel += 3 * k * k;
     }
-    L.skel_work_unit = aw;
-    L.h_T_off = T_off;
-    L.h_SP_off = SP_off;
-    L.h_awork = awork;
-    L.rec_doubles = rec;
+    const int64_t rec_total = rec + rec_prec + rec_skel;
+    L.rec_doubles = rec_total;
     plan_ms += ms_since(tp);
     L.t_ms[5] += ms_since(tp);
     // boundary reduction lists (x_B -= X^T y in fixed cell order): only the apply needs them,
@@ -911,10 +857,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     L.pool.alloc(std::max<int64_t>(P.pool_doubles, 1) * sizeof(double), s, /*zero=*/true);
     if (debug_on()) cudaStreamSynchronize(s);
     DBG("level %d: pool allocated", lev);
-    L.rec.alloc(std::max<int64_t>(rec, 1) * sizeof(double), s);
+    L.rec.alloc(std::max<int64_t>(rec_total, 1) * sizeof(double), s);
     if (debug_on()) cudaStreamSynchronize(s);
     DBG("level %d: records allocated", lev);
-    F->rec_bytes += rec * (int64_t)sizeof(double);
+    F->rec_bytes += rec_total * (int64_t)sizeof(double);
     LevelDev dv = L.dev();
     int band_w = 0, band_nmax = 0, band_bmax = 0;   // banded level-0 cells (2D), set below
     if (timing) CK(cudaEventRecord(ev[0], s));
@@ -1078,7 +1024,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       bp.run(F->status.as<DevStatus>(), s);
     }
     if (timing) CK(cudaEventRecord(ev[3], s));
-    check_status(*F, lev, P.root ? ST_ROOT : ST_ELIMINATE);
+    // (below the root the cell-stage status is read after the block-Jacobi descriptors are built,
+    // so that host work overlaps the elimination; nothing reads the factor before that check)
+    if (P.root) check_status(*F, lev, ST_ROOT);
     DBG("level %d: cells done", lev);
     DBuf tb, to, cc, cr, ccol;
     dev_arr(tb, dp.tgt_blk, P.tgt_blk);
@@ -1113,6 +1061,50 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       break;
     }
     // ---------------- stage 2: block Jacobi ----------------
+    auto t_ov = clk::now();   // (host work overlapped with the GPU's cell elimination)
+    // precondition records
+    std::vector<int64_t> L_off(r), Lg_off(G.G, -1), pI_off(r), pwork(r);
+    std::vector<int> pn(r);
+    int64_t pw = 0;
+    for (int t = 0; t < r; ++t) {
+      const int g = P.precond[t], k = G.size(g);
+      if (do_prec) {
+        L_off[t] = rec;
+        Lg_off[g] = rec;
+        rec += 2 * (int64_t)k * k;   // [L ; L^-T]
+      }
+      pn[t] = k;
+      pI_off[t] = G.off[g];
+      pwork[t] = pw;
+      pw += (k >= APPLY_BIG ? 2 : 1) * k;
+    }
+    L.prec_work_unit = pw;
+    L.h_L_off = L_off;
+    L.h_pI_off = pI_off;
+    L.h_pwork = pwork;
+    L.h_pn = pn;
+    if (do_prec) {
+      double f2 = 0.0, b2 = 0.0;
+#pragma omp parallel for reduction(+ : f2, b2)
+      for (int t = 0; t < r; ++t) {
+        const double k = pn[t];
+        f2 += k * k * k / 3.0;
+        b2 += 8.0 * 3.0 * k * k;
+      }
+      const int64_t nsc = (int64_t)P.scale_blk.size();
+#pragma omp parallel for reduction(+ : f2, b2)
+      for (int64_t q = 0; q < nsc; ++q) {
+        const int b = P.scale_blk[q];
+        const double kg = G.size(P.pat.bg[b]), kh = G.size(P.pat.bh[b]);
+        f2 += kg * kg * kh + kg * kh * kh;
+        b2 += 8.0 * 2.0 * kg * kh;
+      }
+      L.fl[2] += f2;
+      L.by[2] += b2;
+    }
+    DBG("level %d: host: precondition records", lev);
+    L.t_host_overlap_ms += ms_since(t_ov);
+    check_status(*F, lev, ST_ELIMINATE);
     dev_arr(L.p_groups, dp.precond, P.precond);
     upload(L.p_L_off, L_off, s);
     upload(L.p_L_off_of_group, Lg_off, s);
@@ -1167,8 +1159,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
         bpp.build(pbig, pn, zeros, L.rec.as<double>(), L_off, L.rec.as<double>(), zoff, s);
         bpp.run(F->status.as<DevStatus>(), s);
       }
-      check_status(*F, lev, ST_PRECONDITION);
-      DBG("level %d: precondition factor done", lev);
+      DBG("level %d: precondition factor launched", lev);   // (status read before the IDs)
       // two-sided scaling: small blocks by substitution, blocks touching a big group by GEMMs
       // with the explicit inverses: B <- (L_g^-T)^T B L_h^-T
       std::vector<int> stiny, ssmall;
@@ -1237,6 +1228,38 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     if (timing) CK(cudaEventRecord(ev[7], s));
     // ---------------- stage 3: skeletonization ----------------
+    t_ov = clk::now();   // (overlapped with the block-Jacobi stage)
+    if (nsk && L.plan.wave_order.empty()) compute_waves(L.plan, G.G);   // (device-planned level 0)
+    // skeleton records / workspaces (upper bounds; ranks known after the ID)
+    std::vector<int64_t> T_off(nsk), SP_off(nsk), work_off(nsk), iwork_off(nsk), awork(nsk), rows_bound(nsk);
+    int64_t work = 0, iwork = 0, aw = 0;
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < nsk; ++t) {   // coupled rows per separator (the prefix sums follow)
+      int64_t rows = 0;
+      for (int64_t q = P.sk_nbr_off[t]; q < P.sk_nbr_off[t + 1]; ++q) rows += G.size(P.sk_nbr[q]);
+      rows_bound[t] = rows;
+    }
+    for (int t = 0; t < nsk; ++t) {
+      const int g = P.skeleton[t], k = G.size(g);
+      const int64_t rows = rows_bound[t];
+      T_off[t] = rec;
+      rec += (int64_t)k * k;
+      SP_off[t] = rec;
+      rec += 2 * (int64_t)k * k;   // [L~ ; X~^T ; L~^-T]
+      work_off[t] = work;
+      work += std::max<int64_t>((std::max<int64_t>(rows, 1)) * k + 2 * k, 2 * (int64_t)k * k);
+      iwork_off[t] = iwork;
+      iwork += 3 * (int64_t)k;
+      awork[t] = aw;
+      aw += (k >= APPLY_BIG ? 2 : 1) * k;
+    }
+    L.skel_work_unit = aw;
+    L.h_T_off = T_off;
+    L.h_SP_off = SP_off;
+    L.h_awork = awork;
+    if (rec != rec_total) throw std::runtime_error("record pool layout mismatch");
+    L.t_host_overlap_ms += ms_since(t_ov);
+    if (do_prec) check_status(*F, lev, ST_PRECONDITION);
     dev_arr(L.s_groups, dp.skeleton, P.skeleton);
     dev_arr(L.s_nbr_off, dp.sk_nbr_off, P.sk_nbr_off);
     dev_arr(L.s_nbr, dp.sk_nbr, P.sk_nbr);
@@ -2421,7 +2444,7 @@ std::string Factorization::stats_json() const {
       << ",\"cell_b_max\":" << (P.cell_b.empty() ? 0 : *std::max_element(P.cell_b.begin(), P.cell_b.end()))
       << ",\"team_P_mean\":" << L.team_P_mean << ",\"t_repack_ms\":" << L.t_ms[0] << ",\"t_eliminate_ms\":" << L.t_ms[1]
       << ",\"t_precondition_ms\":" << L.t_ms[2] << ",\"t_id_ms\":" << L.t_ms[3] << ",\"t_skel_update_ms\":"
-      << L.t_ms[4] << ",\"t_plan_ms\":" << L.t_ms[5] << ",\"t_wall_ms\":" << L.t_wall_ms << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]
+      << L.t_ms[4] << ",\"t_plan_ms\":" << L.t_ms[5] << ",\"t_wall_ms\":" << L.t_wall_ms << ",\"t_host_overlap_ms\":" << L.t_host_overlap_ms << ",\"record_bytes\":" << L.rec_doubles * 8 << ",\"flops\":[" << L.fl[0] << "," << L.fl[1]
       << "," << L.fl[2] << "," << L.fl[3] << "," << L.fl[4] << "],\"bytes\":[" << L.by[0] << "," << L.by[1] << ","
       << L.by[2] << "," << L.by[3] << "," << L.by[4] << "]}";
   }

@@ -117,6 +117,7 @@ struct LevelRT {
   // stats
   double t_ms[6] = {0, 0, 0, 0, 0, 0};   // repack, eliminate, precondition, id, skel update, host plan
   double t_wall_ms = 0;
+  double t_host_overlap_ms = 0;   // host descriptor work done while the GPU runs this level
   // algorithmic work per stage (0 repack, 1 eliminate+schur, 2 precondition, 3 id, 4 skel update)
   double fl[6] = {0, 0, 0, 0, 0, 0}, by[6] = {0, 0, 0, 0, 0, 0};
   DBuf s_rows;

@@ -719,30 +719,9 @@ void plan_level0_device(const Spec& s, const int64_t* rowptr, const int* col, in
   dp.nscale = nscale;
   dp.nsk_nbr = nskn;
   dp.nsucc = nsucc;
-  // dependency wavefronts (sequential longest path over the coupled earlier separators)
-  std::vector<int> ski(G, -1);
-  for (int i = 0; i < nsk; ++i) ski[lp.skeleton[i]] = i;
-  lp.sk_wave.assign(nsk, 0);
-  lp.nwaves = 0;
-  for (int i = 0; i < nsk; ++i) {
-    int w = 0;
-    for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
-      const int j = ski[lp.sk_nbr[q]];
-      if (j >= 0 && j < i) w = std::max(w, lp.sk_wave[j] + 1);
-    }
-    lp.sk_wave[i] = w;
-    lp.nwaves = std::max(lp.nwaves, w + 1);
-  }
-  lp.wave_off.assign(lp.nwaves + 1, 0);
-  for (int i = 0; i < nsk; ++i) lp.wave_off[lp.sk_wave[i] + 1]++;
-  for (int w = 0; w < lp.nwaves; ++w) lp.wave_off[w + 1] += lp.wave_off[w];
-  lp.wave_order.resize(nsk);
-  {
-    std::vector<int64_t> fill(lp.wave_off.begin(), lp.wave_off.end() - 1);
-    for (int i = 0; i < nsk; ++i) lp.wave_order[fill[lp.sk_wave[i]]++] = i;
-  }
+  // (the dependency wavefronts are formed later by the engine, off the critical path:
+  // compute_waves, while the GPU eliminates the level's cells)
   dp.valid = true;
-  lap("waves");
 }
 
 // full download (for the planner check): every array the host planner produces

@@ -991,6 +991,29 @@ bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const s
   return true;
 }
 
+void compute_waves(LevelPlan& lp, int G) {
+  const int nsk = (int)lp.skeleton.size();
+  std::vector<int> ski(G, -1);
+  for (int i = 0; i < nsk; ++i) ski[lp.skeleton[i]] = i;
+  lp.sk_wave.assign(nsk, 0);
+  lp.nwaves = 0;
+  for (int i = 0; i < nsk; ++i) {
+    int w = 0;
+    for (int64_t q = lp.sk_nbr_off[i]; q < lp.sk_nbr_off[i + 1]; ++q) {
+      const int j = ski[lp.sk_nbr[q]];
+      if (j >= 0 && j < i) w = std::max(w, lp.sk_wave[j] + 1);
+    }
+    lp.sk_wave[i] = w;
+    lp.nwaves = std::max(lp.nwaves, w + 1);
+  }
+  lp.wave_off.assign(lp.nwaves + 1, 0);
+  for (int i = 0; i < nsk; ++i) lp.wave_off[lp.sk_wave[i] + 1]++;
+  for (int w = 0; w < lp.nwaves; ++w) lp.wave_off[w + 1] += lp.wave_off[w];
+  lp.wave_order.resize(nsk);
+  std::vector<int64_t> fill(lp.wave_off.begin(), lp.wave_off.end() - 1);
+  for (int i = 0; i < nsk; ++i) lp.wave_order[fill[lp.sk_wave[i]]++] = i;   // stable: (wave, index)
+}
+
 std::string level_json(const LevelPlan& lp) {
   std::ostringstream o;
   o << "{\"level\":" << lp.level << ",\"G\":" << lp.grp.G << ",\"S\":" << lp.grp.mem.size()

@@ -108,6 +108,10 @@ bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const s
 
 std::string level_json(const LevelPlan& lp);
 
+// dependency wavefronts of the sequential skeletonization (sk_wave, nwaves, wave_off, wave_order)
+// from the skeleton neighbour lists (build_level does this itself; the device planner leaves it)
+void compute_waves(LevelPlan& lp, int G);
+
 // Host vector pool for plan arrays: vectors taken from it are reused allocations (already
 // faulted in), so large per-factorization plan arrays cost a copy, not fresh page faults.
 // pool_take returns a vector of size n with unspecified contents; recycle_plan gives every
