@@ -274,7 +274,8 @@ struct BigPlan {
   // GEMM with the inverse, update of the block's own remaining columns); then one KB-deep
   // update of the whole trailing matrix. Last, U = X^T X (lower tiles, mirrored).
   static constexpr int T = 64;
-  const int KB = env_int("PHIF_BIG_KB", 256);   // multiple of T
+  const int KB = env_int("PHIF_BIG_KB", 256);   // multiple of 128
+  const bool wide128 = env_int("PHIF_WIDE128", 1) != 0;
   DBuf d_n, d_b, d_rows, d_P, d_U, d_op, d_linv, d_list;
   DBuf d_cell, d_i, d_j;
   struct Phase {
@@ -309,7 +310,7 @@ struct BigPlan {
     // L^-T), so its update from the K range [.., kend) vanishes when i >= kend: such tiles are
     // skipped (zero_tile).
     auto zero_tile = [&](int c, int r0, int kend) { return r0 - (n[c] + b[c]) >= kend; };
-    auto trailing = [&](int c, int base, int cend, int kend) {
+    auto trailing = [&](int c, int base, int cend, int kend, int T = BigPlan::T) {
       if (base >= cend) return;
       const int nr = (rws[c] - base + T - 1) / T, nc = (cend - base + T - 1) / T;
       for (int it = 0; it < nr; ++it)
@@ -321,6 +322,8 @@ struct BigPlan {
           wj.push_back(jt);
         }
     };
+    // tile size of the KB-deep updates and of U: 128 (k_big_wide) unless PHIF_WIDE128=0
+    const int TW = wide128 ? 128 : T;
     for (int kb0 = 0; kb0 < nmax; kb0 += KB) {
       for (int s0 = kb0; s0 < std::min(nmax, kb0 + KB); s0 += T) {
         Phase ph{0, {0, 0, 0}, {0, 0, 0}, s0, T};
@@ -356,7 +359,7 @@ struct BigPlan {
       // beyond the next block (side stream, overlapping the next block's 64-wide chain)
       Phase w1{1, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
       for (int c = 0; c < nbig; ++c)
-        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, std::min(n[c], kb0 + 2 * KB), kb0 + KB);
+        if (n[c] > kb0 + KB) trailing(c, kb0 + KB, std::min(n[c], kb0 + 2 * KB), kb0 + KB, TW);
       w1.cnt[0] = (int64_t)wc.size() - w1.off[0];
       if (w1.cnt[0]) phases.push_back(w1);
       Phase w2{3, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, kb0, KB};
@@ -364,11 +367,11 @@ struct BigPlan {
         if (n[c] > kb0 + 2 * KB) {
           // tiles of trailing(c, kb0 + KB, n, ..) with column tile index >= KB / T
           const int base = kb0 + KB, kend = kb0 + KB;
-          const int nr = (rws[c] - base + T - 1) / T, nc = (n[c] - base + T - 1) / T;
+          const int nr = (rws[c] - base + TW - 1) / TW, nc = (n[c] - base + TW - 1) / TW;
           for (int it = 0; it < nr; ++it)
-            for (int jt = KB / T; jt < nc; ++jt) {
-              if (jt > it && base + T * (it + 1) <= n[c]) continue;
-              if (zero_tile(c, base + T * it, kend)) continue;
+            for (int jt = KB / TW; jt < nc; ++jt) {
+              if (jt > it && base + TW * (it + 1) <= n[c]) continue;
+              if (zero_tile(c, base + TW * it, kend)) continue;
               wc.push_back(c);
               wi.push_back(it);
               wj.push_back(jt);
@@ -379,7 +382,7 @@ struct BigPlan {
     }
     Phase us{2, {(int64_t)wc.size(), 0, 0}, {0, 0, 0}, 0, 0};
     for (int c = 0; c < nbig; ++c) {
-      const int nb = (b[c] + T - 1) / T;
+      const int nb = (b[c] + TW - 1) / TW;
       for (int it = 0; it < nb; ++it)
         for (int jt = 0; jt <= it; ++jt) {
           wc.push_back(c);
@@ -435,6 +438,10 @@ struct BigPlan {
       CK(cudaEventRecord(e, from));
       CK(cudaStreamWaitEvent(to, e, 0));
     };
+    auto wide = [&](const BigArgs& a, int mode, cudaStream_t st) {
+      if (wide128) launch_big_wide(a, mode, st);
+      else launch_big_nt(a, mode, st);
+    };
     mark(s, hp);
     bool w2_pending = false;
     for (const Phase& ph : phases) {
@@ -443,12 +450,12 @@ struct BigPlan {
                         args(ph.off[2], ph.cnt[2], ph.k0, ph.kw), st, hp);
       } else if (ph.kind == 3) {
         mark(hp, s);
-        launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), 0, s);
+        wide(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), 0, s);
         w2_pending = true;
       } else {
         if (w2_pending) mark(s, hp);
         w2_pending = false;
-        launch_big_nt(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), ph.kind == 1 ? 0 : 1, hp);
+        wide(args(ph.off[0], ph.cnt[0], ph.k0, ph.kw), ph.kind == 1 ? 0 : 1, hp);
       }
     }
     mark(hp, s);

@@ -3580,6 +3580,156 @@ __global__ void __launch_bounds__(NT, 2) k_big_nt(BigArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// 128 x 128 output tile variant of the streaming NT GEMM for the deep updates of the big cells
+// (the KB-deep trailing updates and U = X^T X): one CTA per SM, 8 warps of 32 x 64, K streamed in
+// 16-wide chunks through a 4-stage cp.async pipeline with one barrier per chunk. Twice the
+// flops per byte fetched from L2 and half the cp.async / LDS instructions per DMMA of the
+// 64 x 64 kernel. Tiles are counted in units of 128 from the same bases as k_big_nt.
+//  MODE 0: P[r, c] -= sum_{k0 <= k < k0+kw} P[r, k] P[c, k]   (rows, columns >= k0 + kw)
+//  MODE 1: U = X^T X (lower tiles; the mirror tile is written from the staged tile)
+// Diagonal tiles skip the two warps whose 32 x 64 part lies strictly above the diagonal; identity
+// rows (row n+b+i holds nonzeros in columns >= i only) start their K range at their first column.
+// ---------------------------------------------------------------------------
+constexpr int WT = 128, WTK = 16, WLD = WTK + 4, W_STAGES = 4;
+constexpr int W_STAGE = 2 * WT * WLD;
+constexpr int W_CLD = WT + 1;
+constexpr size_t W_SMEM = (size_t)(W_STAGES * W_STAGE > WT * W_CLD ? W_STAGES * W_STAGE : WT * W_CLD) * sizeof(double);
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 1) k_big_wide(BigArgs a) {
+  extern __shared__ double smem[];
+  const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x], jt = a.w_j[blockIdx.x];
+  const int n = a.n[c];
+  double* P = a.P[c];
+  int ar0, br0, kbeg, kend, Mv, Nv;
+  if (MODE == 0) {
+    const int base = a.k0 + a.kw;
+    ar0 = base + WT * it;
+    br0 = base + WT * jt;
+    kbeg = a.k0;
+    kend = a.k0 + a.kw;
+    Mv = min(WT, a.rows[c] - ar0);
+    Nv = min(WT, n - br0);
+    const int id0 = ar0 - (n + a.b[c]);   // first identity row of the tile (if >= 0)
+    if (id0 > kbeg) kbeg = min(kend, id0 / WTK * WTK);
+  } else {
+    const int nb = n + a.b[c];
+    ar0 = n + WT * it;
+    br0 = n + WT * jt;
+    kbeg = 0;
+    kend = n;
+    Mv = min(WT, nb - ar0);
+    Nv = min(WT, nb - br0);
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+  const bool diag = it == jt;
+  const bool skip = diag && wn == 1 && wm < 2;   // rows < 64, columns >= 64 of a diagonal tile
+  const double* Ab = P + (int64_t)ar0 * n;
+  const double* Bb = P + (int64_t)br0 * n;
+  auto load = [&](int st, int kc) {
+    double* sA = smem + st * W_STAGE;
+    double* sB = sA + WT * WLD;
+#pragma unroll
+    for (int q = 0; q < (WT * WTK) / NT; ++q) {
+      const int e = tid + q * NT, r = e / WTK, kk = e % WTK;
+      const int gk = kc + kk;
+      const bool okA = r < Mv && gk < kend, okB = r < Nv && gk < kend;
+      cp_async8(sA + r * WLD + kk, Ab + (okA ? (int64_t)r * n + gk : 0), okA);
+      cp_async8(sB + r * WLD + kk, Bb + (okB ? (int64_t)r * n + gk : 0), okB);
+    }
+  };
+  double acc[4][8][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int nch = (kend - kbeg + WTK - 1) / WTK;
+#pragma unroll
+  for (int st = 0; st < W_STAGES - 1; ++st) {
+    if (st < nch) load(st, kbeg + st * WTK);
+    cp_async_commit();
+  }
+  if (MODE == 0) {   // C tile -> L2 (one 128-byte line per 16 columns of a row)
+    for (int e = tid; e < WT * (WT / 16); e += NT) {
+      const int i = e / (WT / 16), j = (e % (WT / 16)) * 16;
+      if (i < Mv && j < Nv)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P + (int64_t)(ar0 + i) * n + br0 + j));
+    }
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait<W_STAGES - 2>();   // chunk ch has landed (one group is committed per iteration)
+    __syncthreads();                 // ... for every thread; stage (ch - 1) % STAGES is drained
+    if (ch + W_STAGES - 1 < nch) load((ch + W_STAGES - 1) % W_STAGES, kbeg + (ch + W_STAGES - 1) * WTK);
+    cp_async_commit();
+    if (skip) continue;
+    const double* sA = smem + (ch % W_STAGES) * W_STAGE + (wm * 32 + g) * WLD + t;
+    const double* sB = smem + (ch % W_STAGES) * W_STAGE + WT * WLD + (wn * 64 + g) * WLD + t;
+#pragma unroll
+    for (int ks = 0; ks < WTK; ks += 4) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) af[x] = sA[x * 8 * WLD + ks];
+#pragma unroll
+      for (int y = 0; y < 8; ++y) bf[y] = sB[y * 8 * WLD + ks];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // epilogue through shared memory (the drained pipeline stages): fragments -> padded tile,
+  // then whole rows leave with coalesced accesses
+  double* sT = smem;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int i = wm * 32 + x * 8 + g, j = wn * 64 + y * 8 + 2 * t + z;
+        sT[i * W_CLD + j] = acc[x][y][z];
+      }
+  __syncthreads();
+  if (MODE == 0) {
+    // read-modify-write of the C tile, 32 independent rows in flight per thread (the accumulator
+    // registers are free by now); the tile was prefetched into L2 ahead of the K loop
+    const int j = tid & (WT - 1), i0 = tid >> 7;   // NT = 256: two rows per pass
+    if (j < Nv) {
+      double* pc = P + (int64_t)ar0 * n + br0 + j;
+      for (int ib = i0; ib < Mv; ib += 64) {
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int i = ib + 2 * u;
+          v[u] = i < Mv ? pc[(int64_t)i * n] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int i = ib + 2 * u;
+          if (i < Mv) pc[(int64_t)i * n] = v[u] - sT[i * W_CLD + j];
+        }
+      }
+    }
+  } else {
+    const int b = a.b[c];
+    double* U = a.U[c];
+    for (int e = tid; e < WT * WT; e += NT) {
+      const int i = e / WT, j = e % WT;
+      if (i < Mv && j < Nv)
+        U[(int64_t)(WT * it + i) * b + WT * jt + j] = (diag && j > i) ? sT[j * W_CLD + i] : sT[i * W_CLD + j];
+    }
+    if (!diag)
+      for (int e = tid; e < WT * WT; e += NT) {
+        const int jj = e / WT, ii = e % WT;   // mirror row WT*jt + jj, column WT*it + ii
+        if (ii < Mv && jj < Nv) U[(int64_t)(WT * jt + jj) * b + WT * it + ii] = sT[ii * W_CLD + jj];
+      }
+  }
+}
+
 #include "gram_id.cuh"
 
 void launch_ingest(const LevelDev& lv, const int* gid, const int* pos, const int64_t* rowptr, const int* col,
@@ -3813,6 +3963,18 @@ void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s) {
   if (mode == 0 && no_cpre) k_big_nt<2><<<a.nwork, NT, NT_SMEM, s>>>(a);
   else if (mode == 0) k_big_nt<0><<<a.nwork, NT, NT_SMEM0, s>>>(a);
   else k_big_nt<1><<<a.nwork, NT, NT_SMEM, s>>>(a);
+}
+void launch_big_wide(const BigArgs& a, int mode, cudaStream_t s) {
+  if (!a.nwork) return;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_big_wide<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
+    cudaFuncSetAttribute(k_big_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
+    init = true;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (mode == 0) k_big_wide<0><<<a.nwork, NT, W_SMEM, s>>>(a);
+  else k_big_wide<1><<<a.nwork, NT, W_SMEM, s>>>(a);
 }
 void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s) {
   if (!nwork) return;

@@ -82,6 +82,7 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s);
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
 void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);
+void launch_big_wide(const BigArgs& a, int mode, cudaStream_t s);   // 128 x 128 tiles
 // banded level-0 cells (2D): shared-memory fit, the kernel, and the device band check
 bool band_cells_fit(int nmax, int bmax, int w);
 int64_t band_scratch_stride(int nmax, int w);   // doubles of one cell's band + reciprocals
