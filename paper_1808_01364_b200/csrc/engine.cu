@@ -275,7 +275,7 @@ struct BigPlan {
   // update of the whole trailing matrix. Last, U = X^T X (lower tiles, mirrored).
   static constexpr int T = 64;
   const int KB = env_int("PHIF_BIG_KB", 256);   // multiple of 128
-  const bool wide128 = env_int("PHIF_WIDE128", 1) != 0;
+  const bool wide128 = env_int("PHIF_WIDE128", 0) != 0;   // (measured: no gain over the 64-tile kernel)
   DBuf d_n, d_b, d_rows, d_P, d_U, d_op, d_linv, d_list;
   DBuf d_cell, d_i, d_j;
   struct Phase {
@@ -322,7 +322,7 @@ struct BigPlan {
           wj.push_back(jt);
         }
     };
-    // tile size of the KB-deep updates and of U: 128 (k_big_wide) unless PHIF_WIDE128=0
+    // tile size of the KB-deep updates and of U: 128 (k_big_wide) with PHIF_WIDE128=1
     const int TW = wide128 ? 128 : T;
     for (int kb0 = 0; kb0 < nmax; kb0 += KB) {
       for (int s0 = kb0; s0 < std::min(nmax, kb0 + KB); s0 += T) {

@@ -18,24 +18,9 @@
 //
 // The Schur complement is stored column-cyclic across the cluster's CTAs (full column b lives in
 // CTA b % C), in shared memory up to the CTA's budget and the remaining columns in a global spill
-// area. Partial norms, Schur diagonal and column positions are replicated in every CTA and
-// updated with identical arithmetic, so every CTA selects the same pivot without communication;
-// the only exchange per pivot step is row i of R (each CTA computes the entries of the columns
-// it owns and pushes them to every CTA through distributed shared memory).
-
-struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
-  // [Schur region sreg][panel nb x k][d, vn1, vn2: 3k][row pieces 2k][rdv, invv: 2k][96] doubles, then 3k ints
-  // (the 96: argmax scratch, two mbarriers, and 2 x 16 step-token slots of the row exchange)
-  __host__ __device__ static int64_t doubles(int64_t sreg, int k, int nb) {
-    return sreg + (int64_t)(nb + 7) * k + 96;
-  }
-  __host__ __device__ static size_t bytes(int64_t sreg, int k, int nb) {
-    return (size_t)doubles(sreg, k, nb) * sizeof(double) + 3 * (size_t)k * sizeof(int);
-  }
-};
-
-// largest per-CTA share of the Schur complement (full owned columns)
-__host__ __device__ __forceinline__ int64_t gid_pack0(int k, int C) { return (int64_t)((k + C - 1) / C) * k; }
+// area. Partial norms, Schur diagonal and position of a column live only in its owner; per pivot
+// step the CTAs exchange one small candidate message each (see k_gid_cpqr) and every CTA forms
+// only its own entries of row i of R.
 
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
@@ -206,13 +191,49 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
 
 // ---- 3. pivoted Cholesky (dlaqp2 replay) + T on a cluster of C CTAs ------------------------
 // CTA c owns the full columns b = c, c+C, ... of the Schur complement (shared memory up to its
-// budget, the rest in a global spill area). Updates are deferred over panels of nb pivot steps
-// (the panel's rows of R are replicated in shared memory): step i forms only row i,
-// R(i, b) = (S(p, b) - sum_{l in panel} R(l, p) R(l, b)) / R(i, i), each CTA for its own columns,
-// and pushes those entries into every CTA's row buffer with st.async, completing bytes on the
-// receiver's mbarrier (no cluster-wide barrier per step). The owned columns receive the
-// panel's rank-nb update once per panel.
+// budget, the rest in a global spill area); rows are stored in the permuted order
+// a' = (a % C) * nown0 + a / C, so every CTA's entries of a row of R are one contiguous segment.
+//
+// Candidate exchange. Norms, Schur diagonal and positions of a column live only in its owner
+// (registers of warp 0, which runs the whole pivot chain without CTA barriers). Per step every
+// CTA picks its local candidate (largest partial norm, lowest position among ties) and pushes one
+// small message to every CTA of the cluster: [norm^2, (position, column), R_ii, 1 / R_ii, and the
+// candidate column's entries in the current panel rows]. After ONE mbarrier wait every CTA reduces
+// the C candidates with the same rule -- the dlaqp2 pivot -- and already holds what it needs to
+// form its own entries of row i,
+//   R(i, b) = (S(p, b) - sum_{l in panel} R(l, p) R(l, b)) / R(i, i),   S(p, b) = S(b, p)' own column,
+// and to downdate its own norms. Full rows of R are not exchanged on the pivot chain: the panel's
+// rows are all-gathered once per panel (one bulk shared::cta -> shared::cluster copy per row and
+// peer) right before the rank-nb update of the owned columns, which runs on DMMA with all warps.
+// Flow control: a CTA completes step i only after every peer pushed its step-i message, which a
+// peer does only after it finished reading the step-(i-1) slots and (at panel boundaries) its
+// panel update; so the double-buffered slots and the single panel buffer are never overwritten
+// while still in use.
 constexpr int GID_NBMAX = 16;
+struct GidShape {   // shapes shared by host and device
+  int nown0, kp, lds, ldp;
+  __host__ __device__ GidShape(int k, int C) {
+    nown0 = ((k + C - 1) / C + 1) & ~1;   // owned columns per CTA, even (16-byte row segments)
+    kp = (C * nown0 + 15) & ~15;          // permuted rows, padded for the 16-row DMMA blocks
+    lds = kp + 2;                         // column stride of the Schur storage (= 2 mod 8) and
+    ldp = kp + 4;                         // row stride of the panel (= 4 mod 16): conflict-free fragments
+  }
+};
+struct GidSmem {   // shared-memory carve-up (doubles first, then ints)
+  // [Schur region sreg][panel nb x ldp][candidate slots 2 x C x (nb + 4)][8: mbarriers, flags] doubles, then 3k ints
+  __host__ __device__ static int64_t doubles(int64_t sreg, int k, int C, int nb) {
+    return sreg + (int64_t)nb * GidShape(k, C).ldp + 2 * (int64_t)C * (nb + 4) + 8;
+  }
+  __host__ __device__ static size_t bytes(int64_t sreg, int k, int C, int nb) {
+    return (size_t)doubles(sreg, k, C, nb) * sizeof(double) + 3 * (size_t)k * sizeof(int);
+  }
+};
+// per-CTA share of the Schur complement (owned columns at their padded stride)
+__host__ __device__ __forceinline__ int64_t gid_pack0(int k, int C) {
+  const GidShape sh(k, C);
+  return (int64_t)sh.nown0 * sh.lds;
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, unsigned rank) {
   uint32_t r;
@@ -235,10 +256,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "r"(a), "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
-               "l"(__double_as_longlong(v)), "r"(rbar)
+__device__ __forceinline__ void st_async_b64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
+               "r"(rbar)
                : "memory");
+}
+__device__ __forceinline__ void bulk_cta_to_cluster(uint32_t rdst, uint32_t src, uint32_t bytes, uint32_t rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
+               "r"(src), "r"(bytes), "r"(rbar)
+               : "memory");
+}
+// warp argmax of (v >= 0, pos): largest v, lowest pos among ties (dlaqp2's first maximum); three
+// redux operations on the bit pattern of v. Returns the winning lane's ballot mask.
+__device__ __forceinline__ unsigned warp_first_max(double v, unsigned pos) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const bool top = hi == mh && lo == ml;
+  const unsigned mp = __reduce_min_sync(0xffffffffu, top ? pos : 0xffffffffu);
+  return __ballot_sync(0xffffffffu, top && pos == mp);
 }
 
 __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, GramArgs ga, int64_t sreg) {
@@ -263,249 +300,307 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     atomicAdd(reinterpret_cast<unsigned long long*>(ga.prof + (slot)), (unsigned long long)(t1 - t0)); \
     t0 = t1;                                                                                            \
   }
-  const int nown0 = (k + C - 1) / C;
+  const GidShape sh(k, C);
+  const int nown0 = sh.nown0, kp = sh.kp, lds = sh.lds, ldp = sh.ldp;
+  const int SLOT = nb + 4;
   double* Gm = ga.gbuf + ga.g_off[item];                              // G (full), then R (R(i, b) at Gm[b*k + i])
   const int64_t kk2 = (int64_t)k * k;
-  double* Sg = Gm + ga.S * kk2 + (int64_t)c * nown0 * k;            // spill area (when allocated)
-  double* Pn = smem + sreg;                 // nb x k panel rows of R
-  double* d = Pn + (int64_t)nb * k;         // Schur diagonal (replicated)
-  double* vn1 = d + k;
-  double* vn2 = vn1 + k;
-  double* rowbuf = vn2 + k;                 // 2 x k receive buffers (step parity)
-  double* rdv = rowbuf + 2 * (int64_t)k;    // sqrt(Schur diagonal) and its reciprocal per column,
-  double* invv = rdv + k;                   // formed off the pivot chain in the downdate loop
-  double* sred = invv + k;                  // 96 (sred[48..49]: the two mbarriers, [64..95] tokens)
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sred + 48);
-  double* tok = sred + 64;                  // tok[q * 16 + src]: step tokens (never read)
-  int* col_at = reinterpret_cast<int*>(sred + 96);
+  double* Sg = Gm + ga.S * kk2 + (int64_t)c * nown0 * lds;          // spill area (when allocated)
+  double* Pn = smem + sreg;                              // nb panel rows of R (permuted column order)
+  double* slots = Pn + (int64_t)nb * ldp;                // [2][C][SLOT] candidate messages
+  double* misc = slots + 2 * (int64_t)C * SLOT;          // 8: three mbarriers, flags
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(misc);    // [0], [1]: candidates (step parity), [2]: panel
+  int* sflag = reinterpret_cast<int*>(misc + 3);         // [0] another panel follows, [1] rank, [2] steps
+  int* col_at = reinterpret_cast<int*>(misc + 8);
   int* piv = col_at + k;
   int* sidx = piv + k;
-  const int nown = c < k ? (k - c + C - 1) / C : 0;
-  const int nsm = (int)(sreg / k < nown ? sreg / k : nown);   // owned columns resident in shared memory
-  auto colf = [&](int lb) -> double* { return lb < nsm ? smem + (int64_t)lb * k : Sg + (int64_t)(lb - nsm) * k; };
+  const int nown = c < k ? (k - c + C - 1) / C : 0;      // owned columns b = lb * C + c
+  int nsm = (int)(sreg / lds < nown0 ? sreg / lds : nown0);   // owned columns resident in shared memory
+  if (nsm < nown0) nsm &= ~7;                            // (whole 8-column DMMA tiles on either side)
+  auto colf = [&](int lb) -> double* { return lb < nsm ? smem + (int64_t)lb * lds : Sg + (int64_t)(lb - nsm) * lds; };
+  // own columns of G (split-K partial blocks summed in a fixed order), rows permuted, pads zero
   for (int lb = warp; lb < nown; lb += nw) {
     const int b = lb * C + c;
     double* col = colf(lb);
     const double* src = Gm + (int64_t)b * k;
-    for (int a0 = lane; a0 < k; a0 += 32 * 4) {
+    for (int a0 = lane; a0 < lds; a0 += 32 * 4) {
       double v[4];
+      int a[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = a0 + 32 * u < k ? src[a0 + 32 * u] : 0.0;
-      for (int q = 1; q < ga.S; ++q)   // split-K partial blocks, fixed order
+      for (int u = 0; u < 4; ++u) {
+        const int ap = a0 + 32 * u;
+        a[u] = (ap % nown0) * C + ap / nown0;
+        if (ap >= C * nown0 || a[u] >= k) a[u] = -1;
+        v[u] = a[u] >= 0 ? src[a[u]] : 0.0;
+      }
+      for (int q = 1; q < ga.S; ++q)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] += a0 + 32 * u < k ? src[q * kk2 + a0 + 32 * u] : 0.0;
+        for (int u = 0; u < 4; ++u) v[u] += a[u] >= 0 ? src[q * kk2 + a[u]] : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (a0 + 32 * u < k) col[a0 + 32 * u] = v[u];
+        if (a0 + 32 * u < lds) col[a0 + 32 * u] = v[u];
     }
   }
-  // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
-  ArgMax loc{-1.0, 0x7fffffff};
+  for (int e = tid; e < nb * ldp; e += NT) Pn[e] = 0.0;
   for (int j = tid; j < k; j += NT) {
-    double dj = Gm[(int64_t)j * k + j];
-    for (int q = 1; q < ga.S; ++q) dj += Gm[q * kk2 + (int64_t)j * k + j];
-    const double nj = fmax(dj, 0.0);
-    d[j] = dj;
-    rdv[j] = sqrt(nj);
-    invv[j] = nj > 0.0 ? 1.0 / rdv[j] : 0.0;
-    vn1[j] = vn2[j] = nj;
     col_at[j] = j;
     piv[j] = 0;
-    loc = better(loc, ArgMax{nj, j});
   }
-  if (C > 1 && tid == 0) {
+  if (tid == 0) {
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
+    mbar_init(mbar + 2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  ArgMax best = cta_argmax1(loc, sred);
-  if (C > 1) cluster_barrier();   // G read, mbarriers initialised cluster-wide
-  else __syncthreads();
+  __syncthreads();
+  if (C > 1) cluster_barrier();   // mbarriers initialised cluster-wide
   GID_MARK(0)
-  const uint32_t rb_addr = smem_addr(rowbuf), bar_addr = smem_addr(mbar), tok_addr = smem_addr(tok);
-  // Back-pressure of the row exchange: besides its row entries, every CTA pushes one 8-byte token
-  // per step to every CTA (also when none of its columns is still active), and every receiver
-  // expects 8 (k - i - 1) + 8 C bytes. A CTA therefore completes step i + 1 only after every
-  // peer has issued its step-(i + 1) pushes, i.e. after every peer has finished reading its own
-  // step-i row buffer, so no CTA runs more than one step ahead: the step-(i + 2) pushes into
-  // buffer parity q can never land while a peer still reads that buffer for step i.
-  const uint32_t tok_dst = (C > 1 && tid < C) ? mapa_u32(tok_addr, (unsigned)tid) : 0u;
-  const uint32_t tokbar_dst = (C > 1 && tid < C) ? mapa_u32(bar_addr, (unsigned)tid) : 0u;
-  // threads per owned column in the row-entry step (power of two, nown <= NT / tpc when possible;
-  // tpc >= C / 4 so every thread pushes to at most 4 destinations)
-  int tpc = 8;
-  while (tpc > 1 && nown > NT / tpc) tpc >>= 1;
-  while (tpc * 4 < C) tpc <<= 1;
-  // remote row-buffer / mbarrier addresses of the destinations this thread pushes to
-  uint32_t rb_dst[4] = {0u, 0u, 0u, 0u}, bar_dst[4] = {0u, 0u, 0u, 0u};
-  if (C > 1)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int dst = (tid & (tpc - 1)) + tpc * u;
-      if (dst < C) {
-        rb_dst[u] = mapa_u32(rb_addr, (unsigned)dst);
-        bar_dst[u] = mapa_u32(bar_addr, (unsigned)dst);
-      }
-    }
-  const double tol3z = sqrt(DBL_EPSILON * 0.5);
-  const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
-  const int mn = min(m, k);
-  double cut = 0.0, cut2 = 0.0;
-  int r = 0, i = 0, np = 0;
-  for (; i < mn; ++i) {
-    if (i > 0 && best.v < cut2) break;
-    const int q = i & 1;
-    if (C > 1 && tid == 0) mbar_expect(mbar + q, 8u * (unsigned)(k - i - 1 + C));
-    // pivot column (position best.i); the position swap is applied after the row exchange
-    const int p = col_at[best.i];
-    const double rd = i == 0 ? rdv[p] : sqrt(fmax(d[p], 0.0));   // (only the pivot needs it)
-    if (i == 0) {
-      cut = cutrel * rd;
-      cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
-    }
-    if (rd > cut) ++r;
-    const double inv = i == 0 ? invv[p] : (rd > 0.0 ? 1.0 / rd : 0.0);
-    double* row = Pn + (int64_t)np * k;   // this step's row of R
-    // entries of row i in the owned columns, tpc threads per column (panel terms split tpc ways;
-    // one round over the owned columns whenever nown <= 256)
-    for (int cb0 = 0; cb0 < nown; cb0 += NT / tpc) {
-      const int lb = cb0 + tid / tpc, part = tid & (tpc - 1);
-      const int b = lb * C + c;
-      const bool act = lb < nown && b != p && !piv[b];
-      double v = 0.0;
-      if (act) {
-        for (int l = part; l < np; l += tpc) v = __fma_rn(-Pn[l * k + p], Pn[l * k + b], v);
-        if (part == 0) v += colf(lb)[p];
-      }
-      for (int o = 1; o < tpc; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (act) {
-        v *= inv;
-        if (C > 1) {
-          const uint32_t off = (uint32_t)(q * k + b) * 8u;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (part + u * tpc < C) st_async_f64(rb_dst[u] + off, v, bar_dst[u] + 8u * q);
-        } else if (part == 0) {
-          row[b] = v;
-        }
-      }
-    }
-    if (C > 1 && tid < C) st_async_f64(tok_dst + 8u * (uint32_t)(q * 16 + c), 0.0, tokbar_dst + 8u * q);
-    GID_MARK(2)
-    // C > 1: no CTA barrier here -- after the mbarrier wait every thread reads the received row
-    // entries of its own downdate positions straight from the receive buffer and files them into
-    // the panel row and (owned columns) into R; thread 0 files the diagonal. Entries of already
-    // pivoted columns are never read again (row formation and downdates touch unpivoted columns
-    // only; the back substitution reads R on and above the diagonal).
-    const double* rb = rowbuf + (int64_t)q * k;
+  const double* Pown = Pn + c * nown0;
+  int npanel = 0;
+  // all-gather of the panel's rows + rank-nb update of the owned columns (all threads)
+  auto panel_end = [&]() {
     if (C > 1) {
-      mbar_wait(mbar + q, (unsigned)((i >> 1) & 1));
-      GID_MARK(3)
-      if (tid == 0) {
-        row[p] = rd;
-        piv[p] = 1;   // (read again only after the argmax barrier)
-        if (p % C == c) Gm[(int64_t)p * k + i] = rd;
+      if (tid == 0) mbar_expect(mbar + 2, 8u * (unsigned)((C - 1) * nb * nown0));
+      const uint32_t bar2 = smem_addr(mbar + 2);
+      for (int e = tid; e < nb * (C - 1); e += NT) {
+        const int l = e / (C - 1), dd = e % (C - 1), dst = dd + (dd >= c ? 1 : 0);
+        const uint32_t src = smem_addr(Pown + l * ldp);
+        bulk_cta_to_cluster(mapa_u32(src, (unsigned)dst), src, 8u * (unsigned)nown0, mapa_u32(bar2, (unsigned)dst));
       }
-    } else {
-      __syncthreads();
-      for (int a = tid; a < k; a += NT)
-        if (a == p) row[a] = rd;
-        else if (piv[a]) row[a] = 0.0;
-      __syncthreads();
-      if (tid == 0) piv[p] = 1;   // (read again only after the argmax barrier)
-      for (int lb = tid; lb < nown; lb += NT) {   // row i of R, columns owned here
-        const int b = lb * C + c;
-        Gm[(int64_t)b * k + i] = row[b];
-      }
+      mbar_wait(mbar + 2, (unsigned)(npanel & 1));
     }
-    GID_MARK(4)
-    // fused: Schur diagonal, dlaqp2 partial-norm downdate and the next pivot's argmax over the
-    // positions > i (identical arithmetic in every CTA)
-    // the dlaqp2 swap of positions i and best.i is done by the thread owning position best.i
-    // (it takes over position i's column and norms; position i is final)
-    loc = ArgMax{-1.0, 0x7fffffff};
-    const int pb = best.i;
-    for (int j = i + 1 + tid; j < k; j += NT) {
-      int col;
-      if (j == pb) {
-        col = col_at[i];
-        col_at[j] = col;
-        col_at[i] = p;
-        vn1[j] = vn1[i];
-        vn2[j] = vn2[i];
-      } else {
-        col = col_at[j];
-      }
-      double rv;
-      if (C > 1) {
-        rv = rb[col];
-        row[col] = rv;
-        if (col % C == c) Gm[(int64_t)col * k + i] = rv;
-      } else {
-        rv = row[col];
-      }
-      const double dn = __fma_rn(-rv, rv, d[col]);
-      d[col] = dn;
-      double w1 = vn1[j];
-      if (w1 != 0.0) {
-        // dlaqp2: temp = max(0, 1 - (|R(i,j)|/vn1)^2); recompute when temp (vn1/vn2)^2 <= tol3z,
-        // else vn1 *= sqrt(temp) -- here on squared norms: w = vn1^2 - R(i,j)^2
-        const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
-        if (w <= tol3z * vn2[j]) {
-          w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
-          vn2[j] = w1;
-        } else {
-          w1 = w;
-        }
-        vn1[j] = w1;
-      }
-      loc = better(loc, ArgMax{w1, j});
-    }
-    best = cta_argmax1(loc, sred);
-    GID_MARK(6)
-    if (++np == nb) {   // rank-nb update of the owned, unpivoted columns (all rows)
-      // one warp per pair of owned columns, two rows per lane: each panel value loaded from shared
-      // memory feeds two FMAs, four independent accumulation chains per lane
-      for (int lp = warp; 2 * lp < nown; lp += nw) {
-        const int lb1 = 2 * lp, lb2 = 2 * lp + 1;
-        const bool u1 = !piv[lb1 * C + c], u2 = lb2 < nown && !piv[lb2 * C + c];
-        if (!u1 && !u2) continue;
-        double r1[GID_NBMAX], r2[GID_NBMAX];
+    ++npanel;
+    // S(a', lb) -= sum_l P(l, a') P(l, lb): 16-row blocks over the warps, 4 column tiles at a time
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int nct = (nown + 7) >> 3;
+    for (int rb = warp; rb < (kp >> 4); rb += nw) {
+      const int r0 = rb << 4;
+      for (int ct0 = 0; ct0 < nct; ct0 += 4) {
+        double acc[2][4][2];
+        double* cp[4][2];
 #pragma unroll
-        for (int l = 0; l < GID_NBMAX; ++l) {
-          r1[l] = (u1 && l < np) ? Pn[l * k + lb1 * C + c] : 0.0;
-          r2[l] = (u2 && l < np) ? Pn[l * k + lb2 * C + c] : 0.0;
-        }
-        double* c1 = colf(lb1);
-        double* c2 = u2 ? colf(lb2) : c1;
-        for (int a0 = lane; a0 < k; a0 += 64) {
-          const int a1 = a0 + 32;
-          const bool ok1 = a1 < k;
-          double x00 = c1[a0], x01 = ok1 ? c1[a1] : 0.0, x10 = c2[a0], x11 = ok1 ? c2[a1] : 0.0;
+        for (int y = 0; y < 4; ++y)
 #pragma unroll
-          for (int l = 0; l < GID_NBMAX; ++l)
-            if (l < np) {
-              const double pa = Pn[l * k + a0], pb = ok1 ? Pn[l * k + a1] : 0.0;
-              x00 = __fma_rn(-pa, r1[l], x00);
-              x01 = __fma_rn(-pb, r1[l], x01);
-              x10 = __fma_rn(-pa, r2[l], x10);
-              x11 = __fma_rn(-pb, r2[l], x11);
+          for (int z = 0; z < 2; ++z) {
+            const int lb = (ct0 + y) * 8 + 2 * t4 + z;
+            cp[y][z] = lb < nown ? colf(lb) + r0 + g8 : nullptr;
+#pragma unroll
+            for (int x = 0; x < 2; ++x) acc[x][y][z] = cp[y][z] ? cp[y][z][8 * x] : 0.0;
+          }
+        for (int ks = 0; ks < nb; ks += 4) {
+          const double* pr = Pn + (ks + t4) * ldp;
+          double af[2], bf[4];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) af[x] = -pr[r0 + 8 * x + g8];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) bf[y] = pr[c * nown0 + (ct0 + y) * 8 + g8];
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+        }
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int z = 0; z < 2; ++z)
+            if (cp[y][z]) {
+#pragma unroll
+              for (int x = 0; x < 2; ++x) cp[y][z][8 * x] = acc[x][y][z];
             }
-          if (u1) {
-            c1[a0] = x00;
-            if (ok1) c1[a1] = x01;
+      }
+    }
+    __syncthreads();
+  };
+  if (warp != 0) {
+    for (;;) {   // helpers: wait for a full panel (or the end of the pivot chain)
+      __syncthreads();
+      if (!sflag[0]) break;
+      panel_end();
+    }
+  } else {
+    // ---- the pivot chain (warp 0): own columns lb = lane + 32 u ----
+    constexpr int UMAX = 4;   // nown0 <= 128 (host check)
+    int cb[UMAX], cpos[UMAX];
+    bool cpv[UMAX];            // pivoted (or no such column)
+    double cd[UMAX], c1[UMAX], c2[UMAX];
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      const int lb = lane + 32 * u;
+      const bool ok = lb < nown;
+      cb[u] = ok ? lb * C + c : -1;
+      cpos[u] = cb[u];
+      cpv[u] = !ok;
+      const double dj = ok ? colf(lb)[c * nown0 + lb] : 0.0;
+      cd[u] = dj;
+      c1[u] = c2[u] = fmax(dj, 0.0);   // squared partial norms (argmax and the dlaqp2 tests in squared form)
+    }
+    const uint32_t slot_addr = smem_addr(slots), bar_addr = smem_addr(mbar);
+    // message words w = lane / C, lane / C + 32 / C, ... go to CTA lane % C
+    const int mydst = lane & (C - 1), w0 = lane / C, wstep = 32 / C;
+    const uint32_t rslot = C > 1 ? mapa_u32(slot_addr, (unsigned)mydst) : 0u;
+    const uint32_t rbar = C > 1 ? mapa_u32(bar_addr, (unsigned)mydst) : 0u;
+    const double tol3z = sqrt(DBL_EPSILON * 0.5);
+    const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
+    const int mn = min(m, k);
+    double cut = 0.0, cut2 = 0.0;
+    int r = 0, i = 0, np = 0;
+    for (; i < mn; ++i) {
+      const int q = i & 1;
+      // local candidate: largest partial norm, lowest position among ties
+      double bv = 0.0, bd = 0.0;
+      int bpos = 0x7fffffff, bcol = -1, blb = 0;
+#pragma unroll
+      for (int u = 0; u < UMAX; ++u)
+        if (!cpv[u] && (c1[u] > bv || (c1[u] == bv && cpos[u] < bpos))) {
+          bv = c1[u];
+          bd = cd[u];
+          bpos = cpos[u];
+          bcol = cb[u];
+          blb = lane + 32 * u;
+        }
+      // (its R_ii and 1 / R_ii are formed by every lane for its own best while the argmax runs)
+      const double brd = sqrt(fmax(bd, 0.0));
+      const double binv = brd > 0.0 ? 1.0 / brd : 0.0;
+      const unsigned wm = warp_first_max(bv, (unsigned)bpos);
+      const int wl = __ffs(wm) - 1;   // (bpos values are distinct except the "none" marker)
+      const double wv = __shfl_sync(0xffffffffu, bv, wl);
+      const int wpos = __shfl_sync(0xffffffffu, bpos, wl);
+      const int wcol = __shfl_sync(0xffffffffu, bcol, wl);
+      const int wlb = __shfl_sync(0xffffffffu, blb, wl);
+      const double wrd = __shfl_sync(0xffffffffu, brd, wl);
+      const double winv = __shfl_sync(0xffffffffu, binv, wl);
+      double* myslot = slots + (int64_t)(q * C + c) * SLOT;
+      if (C > 1) {
+        if (lane == 0) mbar_expect(mbar + q, 8u * (unsigned)(C * (np + 4)));
+        for (int w = w0; w < np + 4; w += wstep) {
+          unsigned long long val;
+          if (w == 0) val = (unsigned long long)__double_as_longlong(wv);
+          else if (w == 1) val = ((unsigned long long)(unsigned)wpos << 32) | (unsigned)wcol;
+          else if (w == 2) val = (unsigned long long)__double_as_longlong(wrd);
+          else if (w == 3) val = (unsigned long long)__double_as_longlong(winv);
+          else val = (unsigned long long)__double_as_longlong(Pown[(w - 4) * ldp + wlb]);
+          st_async_b64(rslot + (uint32_t)((q * C + c) * SLOT + w) * 8u, val, rbar + 8u * q);
+        }
+        GID_MARK(2)
+        mbar_wait(mbar + q, (unsigned)((i >> 1) & 1));
+        GID_MARK(3)
+      } else {
+        unsigned long long* ms = reinterpret_cast<unsigned long long*>(myslot);
+        for (int w = lane; w < np + 4; w += 32) {
+          unsigned long long val;
+          if (w == 0) val = (unsigned long long)__double_as_longlong(wv);
+          else if (w == 1) val = ((unsigned long long)(unsigned)wpos << 32) | (unsigned)wcol;
+          else if (w == 2) val = (unsigned long long)__double_as_longlong(wrd);
+          else if (w == 3) val = (unsigned long long)__double_as_longlong(winv);
+          else val = (unsigned long long)__double_as_longlong(Pown[(w - 4) * ldp + wlb]);
+          ms[w] = val;
+        }
+        __syncwarp();
+        GID_MARK(2)
+      }
+      // the pivot: first maximum over the C candidates (identical in every CTA)
+      int ws = 0;
+      if (C > 1) {
+        double sv = 0.0;
+        unsigned spos = 0xffffffffu;
+        if (lane < C) {
+          const double* sl = slots + (int64_t)(q * C + lane) * SLOT;
+          sv = sl[0];
+          spos = (unsigned)(reinterpret_cast<const unsigned long long*>(sl)[1] >> 32);
+        }
+        ws = __ffs(warp_first_max(sv, spos)) - 1;
+      }
+      const double* wsl = slots + (int64_t)(q * C + ws) * SLOT;
+      const double gv = wsl[0];
+      const unsigned long long key = reinterpret_cast<const unsigned long long*>(wsl)[1];
+      const int pb = (int)(key >> 32), p = (int)(unsigned)key;
+      const double rd = wsl[2], inv = wsl[3];
+      if (pb == 0x7fffffff) break;            // (no unpivoted column left: cannot happen while i < k)
+      if (i > 0 && gv < cut2) break;
+      if (i == 0) {
+        cut = cutrel * rd;
+        cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
+      }
+      if (rd > cut) ++r;
+      // own entries of row i of R
+      const int pp = (p % C) * nown0 + p / C;
+      double* prow = Pn + np * ldp + c * nown0;
+      double rp[GID_NBMAX];
+#pragma unroll
+      for (int l = 0; l < GID_NBMAX; ++l) rp[l] = l < np ? wsl[4 + l] : 0.0;
+      double rvv[UMAX];
+#pragma unroll
+      for (int u = 0; u < UMAX; ++u) {
+        const int lb = lane + 32 * u;
+        rvv[u] = 0.0;
+        if (cb[u] >= 0) {
+          double v;
+          if (cb[u] == p) {
+            v = rd;
+            cpv[u] = true;
+            Gm[(int64_t)p * k + i] = rd;
+          } else if (cpv[u]) {
+            v = 0.0;
+          } else {
+            double acc = colf(lb)[pp];
+#pragma unroll
+            for (int l = 0; l < GID_NBMAX; ++l)
+              if (l < np) acc = __fma_rn(-rp[l], Pown[l * ldp + lb], acc);
+            v = acc * inv;
+            Gm[(int64_t)cb[u] * k + i] = v;
+            rvv[u] = v;
           }
-          if (u2) {
-            c2[a0] = x10;
-            if (ok1) c2[a1] = x11;
-          }
+          prow[lb] = v;
         }
       }
-      np = 0;
-      __syncthreads();
-      GID_MARK(5)
+      // dlaqp2 swap of positions i and pb: the column displaced from position i moves to pb
+      const int ci = col_at[i];
+      __syncwarp();
+      if (lane == 0) {
+        col_at[pb] = ci;
+        col_at[i] = p;
+      }
+      GID_MARK(4)
+      // Schur diagonal and dlaqp2 partial-norm downdate of the own unpivoted columns
+#pragma unroll
+      for (int u = 0; u < UMAX; ++u)
+        if (!cpv[u]) {
+          if (cb[u] == ci) cpos[u] = pb;
+          const double rv = rvv[u];
+          const double dn = __fma_rn(-rv, rv, cd[u]);
+          cd[u] = dn;
+          double w1 = c1[u];
+          if (w1 != 0.0) {
+            // dlaqp2: temp = max(0, 1 - (|R(i,j)|/vn1)^2); recompute when temp (vn1/vn2)^2 <= tol3z,
+            // else vn1 *= sqrt(temp) -- here on squared norms: w = vn1^2 - R(i,j)^2
+            const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
+            if (w <= tol3z * c2[u]) {
+              w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
+              c2[u] = w1;
+            } else {
+              w1 = w;
+            }
+            c1[u] = w1;
+          }
+        }
+      GID_MARK(6)
+      if (++np == nb) {   // rank-nb update of the owned columns
+        if (lane == 0) sflag[0] = 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // panel rows -> bulk copies
+        __syncthreads();
+        panel_end();
+        np = 0;
+        GID_MARK(5)
+      }
     }
+    if (lane == 0) {
+      sflag[0] = 0;
+      sflag[1] = r;
+      sflag[2] = i;
+    }
+    __syncthreads();
   }
+  const int r = sflag[1], i = sflag[2];
   if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(ga.prof + 9), (unsigned long long)i);
   const int kt = k - r;
   // redundant flags by column (positions r..k-1) and the sorted-list index of every column
@@ -533,7 +628,7 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   if (kt > 0 && r > 0) {
     double* T = sk.rec + sk.T_off[s];
     double* stage = smem;
-    const int64_t sreg2 = sreg + (int64_t)nb * k;
+    const int64_t sreg2 = sreg + (int64_t)nb * ldp;
     // staging: BW columns of R11 + NR right-hand sides per warp (host guarantees 24 k <= sreg2)
     const int BW = sreg2 >= (int64_t)(32 + nw) * r ? 32 : 16;
     const int NR = max(1, min(4, (int)((sreg2 / r - BW) / nw)));

@@ -4151,42 +4151,45 @@ void launch_scale(double* y, const double* x, const double* nrm2, int64_t n, cud
 static constexpr size_t GID_SMEM_CAP = 227 * 1024;
 int gid_panel(int k) {
   static const int nb = getenv("PHIF_GID_NB") ? atoi(getenv("PHIF_GID_NB")) : 0;
-  if (nb > 0) return std::min(nb, 16);
+  if (nb > 0) return std::max(4, std::min(nb, 16) & ~3);   // multiple of 4 (DMMA K steps)
   (void)k;
   return 16;   // measured: the widest panel the register blocking allows wins at every level
 }
 static int64_t gid_sreg(int k, int C) {
   // shared-memory Schur region: the packed share when it fits the CTA budget, else what is left
-  // (columns beyond it spill to global memory); the back substitution stages in region + panel
+  // (columns beyond it spill to global memory); the back substitution stages in region + panel.
+  // Even, so that the panel rows behind it stay 16-byte aligned (bulk copies).
   const int nb = gid_panel(k);
-  const int64_t avail = ((int64_t)GID_SMEM_CAP - (int64_t)GidSmem::bytes(0, k, nb)) / (int64_t)sizeof(double);
-  return std::min(avail, std::max<int64_t>(gid_pack0(k, C), std::max<int64_t>(0, (24 - nb) * (int64_t)k)));
+  const int64_t avail = ((int64_t)GID_SMEM_CAP - (int64_t)GidSmem::bytes(0, k, C, nb)) / (int64_t)sizeof(double);
+  return std::min(avail, std::max<int64_t>(gid_pack0(k, C), std::max<int64_t>(0, (24 - nb) * (int64_t)k))) & ~(int64_t)1;
 }
 int gid_cluster(int kmax, bool* sg) {
   // smallest cluster whose per-CTA packed Schur share is at most `target` doubles
   static const int64_t target = getenv("PHIF_GID_PACK") ? atoll(getenv("PHIF_GID_PACK")) : 12288;
   static const int force_c = getenv("PHIF_GID_C") ? atoi(getenv("PHIF_GID_C")) : 0;
-  // one CTA (no per-step cluster exchange) up to c1k columns, the Schur complement spilling
-  // to global memory beyond the shared-memory budget
-  static const int c1k = getenv("PHIF_GID_C1K") ? atoi(getenv("PHIF_GID_C1K")) : 0;
   int C = 16;
-  if (force_c) C = force_c;
-  else if (kmax <= c1k) C = 1;
-  else
+  if (force_c) {
+    if (force_c != 1 && force_c != 2 && force_c != 4 && force_c != 8 && force_c != 16)
+      throw std::runtime_error("PHIF_GID_C must be 1, 2, 4, 8 or 16");
+    C = force_c;
+  } else {
     for (int c : {1, 2, 4, 8, 16})
       if (gid_pack0(kmax, c) <= target) {
         C = c;
         break;
       }
+  }
   *sg = gid_pack0(kmax, C) > gid_sreg(kmax, C);
-  if (24 * (int64_t)kmax > gid_sreg(kmax, C) + (int64_t)gid_panel(kmax) * kmax)
+  if (24 * (int64_t)kmax > gid_sreg(kmax, C) + (int64_t)gid_panel(kmax) * GidShape(kmax, C).ldp ||
+      GidShape(kmax, C).nown0 > 128)
     throw std::runtime_error("gram ID: separator too large");
   return C;
 }
-// separators the Gram path can stage (back-substitution buffers in shared memory)
+// separators the Gram path can stage (back-substitution buffers in shared memory; at most 128
+// owned columns per CTA)
 bool gid_fits(int k) {
   const int64_t sreg = gid_sreg(k, 16);
-  return 24 * (int64_t)k <= sreg + (int64_t)gid_panel(k) * k;
+  return 24 * (int64_t)k <= sreg + (int64_t)gid_panel(k) * GidShape(k, 16).ldp && GidShape(k, 16).nown0 <= 128;
 }
 int64_t gid_gbuf_doubles(int k, int C, bool sg, int S) {
   return (int64_t)S * k * k + (sg ? (int64_t)C * gid_pack0(k, C) : 0);
@@ -4210,7 +4213,7 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
   (void)sg;
   GramArgs g3 = g;
   g3.nb = gid_panel(kmax);
-  const size_t bytes = GidSmem::bytes(sreg, kmax, g3.nb);
+  const size_t bytes = GidSmem::bytes(sreg, kmax, g.C, g3.nb);
   void (*fn)(LevelDev, SkelArgs, GramArgs, int64_t) = k_gid_cpqr;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaLaunchConfig_t cfg = {};

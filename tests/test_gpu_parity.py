@@ -218,7 +218,7 @@ print(json.dumps({"SL": F.SL, "n_gid": sum(lv.get("n_gid", 0) for lv in F.stats[
 """
 
 
-@pytest.mark.parametrize("clusters", ["16", "2"])
+@pytest.mark.parametrize("clusters", ["16", "8"])
 def test_gram_id_forced_cluster_matches_oracle(clusters):
     """Gram-path ID with a forced cluster size (mixed-k waves, C=16 leaves CTAs with no
     active columns while their peers run on): skeleton sets still equal the oracle's at c5 n=64."""
