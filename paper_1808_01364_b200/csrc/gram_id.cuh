@@ -197,8 +197,9 @@ __global__ void __launch_bounds__(NT, 2) k_gid_gram(LevelDev lv, SkelArgs sk, Gr
 // Candidate exchange. Norms, Schur diagonal and positions of a column live only in its owner
 // (registers of warp 0, which runs the whole pivot chain without CTA barriers). Per step every
 // CTA picks its local candidate (largest partial norm, lowest position among ties) and pushes one
-// small message to every CTA of the cluster: [norm^2, (position, column), R_ii, 1 / R_ii, and the
-// candidate column's entries in the current panel rows]. After ONE mbarrier wait every CTA reduces
+// small message to every CTA of the cluster: [norm^2, (position, column), Schur diagonal, -, and the
+// candidate column's entries in the current panel rows] (one word per lane, one st.async per
+// lane and destination). After ONE mbarrier wait every CTA reduces
 // the C candidates with the same rule -- the dlaqp2 pivot -- and already holds what it needs to
 // form its own entries of row i,
 //   R(i, b) = (S(p, b) - sum_{l in panel} R(l, p) R(l, b)) / R(i, i),   S(p, b) = S(b, p)' own column,
@@ -278,6 +279,8 @@ __device__ __forceinline__ unsigned warp_first_max(double v, unsigned pos) {
   return __ballot_sync(0xffffffffu, top && pos == mp);
 }
 
+// UMAX: column slots per lane of the pivot-chain warp (owned columns per CTA <= 32 * UMAX)
+template <int UMAX>
 __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, GramArgs ga, int64_t sreg) {
   extern __shared__ double smem[];
   const int C = ga.C, nb = ga.nb;
@@ -419,7 +422,6 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
     }
   } else {
     // ---- the pivot chain (warp 0): own columns lb = lane + 32 u ----
-    constexpr int UMAX = 4;   // nown0 <= 128 (host check)
     int cb[UMAX], cpos[UMAX];
     bool cpv[UMAX];            // pivoted (or no such column)
     double cd[UMAX], c1[UMAX], c2[UMAX];
@@ -435,14 +437,11 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       c1[u] = c2[u] = fmax(dj, 0.0);   // squared partial norms (argmax and the dlaqp2 tests in squared form)
     }
     const uint32_t slot_addr = smem_addr(slots), bar_addr = smem_addr(mbar);
-    // message words w = lane / C, lane / C + 32 / C, ... go to CTA lane % C
-    const int mydst = lane & (C - 1), w0 = lane / C, wstep = 32 / C;
-    const uint32_t rslot = C > 1 ? mapa_u32(slot_addr, (unsigned)mydst) : 0u;
-    const uint32_t rbar = C > 1 ? mapa_u32(bar_addr, (unsigned)mydst) : 0u;
     const double tol3z = sqrt(DBL_EPSILON * 0.5);
     const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
     const int mn = min(m, k);
     double cut = 0.0, cut2 = 0.0;
+    const int lgC = 31 - __clz(C);
     int r = 0, i = 0, np = 0;
     for (; i < mn; ++i) {
       const int q = i & 1;
@@ -458,43 +457,36 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
           bcol = cb[u];
           blb = lane + 32 * u;
         }
-      // (its R_ii and 1 / R_ii are formed by every lane for its own best while the argmax runs)
-      const double brd = sqrt(fmax(bd, 0.0));
-      const double binv = brd > 0.0 ? 1.0 / brd : 0.0;
       const unsigned wm = warp_first_max(bv, (unsigned)bpos);
       const int wl = __ffs(wm) - 1;   // (bpos values are distinct except the "none" marker)
       const double wv = __shfl_sync(0xffffffffu, bv, wl);
       const int wpos = __shfl_sync(0xffffffffu, bpos, wl);
       const int wcol = __shfl_sync(0xffffffffu, bcol, wl);
       const int wlb = __shfl_sync(0xffffffffu, blb, wl);
-      const double wrd = __shfl_sync(0xffffffffu, brd, wl);
-      const double winv = __shfl_sync(0xffffffffu, binv, wl);
-      double* myslot = slots + (int64_t)(q * C + c) * SLOT;
+      const double wd = __shfl_sync(0xffffffffu, bd, wl);
+      // message word `word` of this lane: [norm^2, (position, column), Schur diagonal, panel entries]
+      const int nwords = np + 4;   // (word 3 unused: the panel entries start 16-byte aligned)
+      const int P2 = nwords <= 8 ? 8 : (nwords <= 16 ? 16 : 32);
+      const int word = lane & (P2 - 1);
+      unsigned long long val = 0ull;
+      if (word == 0) val = (unsigned long long)__double_as_longlong(wv);
+      else if (word == 1) val = ((unsigned long long)(unsigned)wpos << 32) | (unsigned)wcol;
+      else if (word == 2) val = (unsigned long long)__double_as_longlong(wd);
+      else if (word > 3 && word < nwords) val = (unsigned long long)__double_as_longlong(Pown[(word - 4) * ldp + wlb]);
       if (C > 1) {
-        if (lane == 0) mbar_expect(mbar + q, 8u * (unsigned)(C * (np + 4)));
-        for (int w = w0; w < np + 4; w += wstep) {
-          unsigned long long val;
-          if (w == 0) val = (unsigned long long)__double_as_longlong(wv);
-          else if (w == 1) val = ((unsigned long long)(unsigned)wpos << 32) | (unsigned)wcol;
-          else if (w == 2) val = (unsigned long long)__double_as_longlong(wrd);
-          else if (w == 3) val = (unsigned long long)__double_as_longlong(winv);
-          else val = (unsigned long long)__double_as_longlong(Pown[(w - 4) * ldp + wlb]);
-          st_async_b64(rslot + (uint32_t)((q * C + c) * SLOT + w) * 8u, val, rbar + 8u * q);
+        if (lane == 0) mbar_expect(mbar + q, 8u * (unsigned)(C * nwords));
+        if (word < nwords) {
+          // every lane sends its one word to the destinations d = lane / P2, + 32 / P2, ...
+          const uint32_t off = (uint32_t)((q * C + c) * SLOT + word) * 8u;
+          for (int dd = lane / P2; dd < C; dd += 32 / P2)
+            st_async_b64(mapa_u32(slot_addr, (unsigned)dd) + off, val, mapa_u32(bar_addr, (unsigned)dd) + 8u * q);
         }
         GID_MARK(2)
         mbar_wait(mbar + q, (unsigned)((i >> 1) & 1));
         GID_MARK(3)
       } else {
-        unsigned long long* ms = reinterpret_cast<unsigned long long*>(myslot);
-        for (int w = lane; w < np + 4; w += 32) {
-          unsigned long long val;
-          if (w == 0) val = (unsigned long long)__double_as_longlong(wv);
-          else if (w == 1) val = ((unsigned long long)(unsigned)wpos << 32) | (unsigned)wcol;
-          else if (w == 2) val = (unsigned long long)__double_as_longlong(wrd);
-          else if (w == 3) val = (unsigned long long)__double_as_longlong(winv);
-          else val = (unsigned long long)__double_as_longlong(Pown[(w - 4) * ldp + wlb]);
-          ms[w] = val;
-        }
+        unsigned long long* ms = reinterpret_cast<unsigned long long*>(slots + (int64_t)(q * C + c) * SLOT);
+        if (lane < nwords) ms[lane] = val;
         __syncwarp();
         GID_MARK(2)
       }
@@ -514,7 +506,9 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       const double gv = wsl[0];
       const unsigned long long key = reinterpret_cast<const unsigned long long*>(wsl)[1];
       const int pb = (int)(key >> 32), p = (int)(unsigned)key;
-      const double rd = wsl[2], inv = wsl[3];
+      // R_ii and 1 / R_ii of the pivot, formed by every CTA (they overlap the row's FMA chains)
+      const double rd = sqrt(fmax(wsl[2], 0.0));
+      const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
       if (pb == 0x7fffffff) break;            // (no unpivoted column left: cannot happen while i < k)
       if (i > 0 && gv < cut2) break;
       if (i == 0) {
@@ -523,11 +517,16 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       }
       if (rd > cut) ++r;
       // own entries of row i of R
-      const int pp = (p % C) * nown0 + p / C;
+      const int pp = (p & (C - 1)) * nown0 + (p >> lgC);   // (C is a power of two)
       double* prow = Pn + np * ldp + c * nown0;
       double rp[GID_NBMAX];
 #pragma unroll
-      for (int l = 0; l < GID_NBMAX; ++l) rp[l] = l < np ? wsl[4 + l] : 0.0;
+      for (int l = 0; l < GID_NBMAX; l += 2) {   // (entries beyond np are stale and never used)
+        double2 t2 = make_double2(0.0, 0.0);
+        if (l < nb) t2 = *reinterpret_cast<const double2*>(wsl + 4 + l);
+        rp[l] = t2.x;
+        rp[l + 1] = t2.y;
+      }
       double rvv[UMAX];
 #pragma unroll
       for (int u = 0; u < UMAX; ++u) {

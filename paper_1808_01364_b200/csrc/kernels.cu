@@ -4206,7 +4206,6 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
   if (!attr) {
     attr = true;
     cudaFuncSetAttribute(k_gid_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT_SMEM);
-    cudaFuncSetAttribute(k_gid_cpqr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   if (g.nwork) k_gid_gram<<<g.nwork, NT, NT_SMEM, s>>>(lv, a, g);
   int64_t sreg = gid_sreg(kmax, g.C);
@@ -4214,7 +4213,11 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
   GramArgs g3 = g;
   g3.nb = gid_panel(kmax);
   const size_t bytes = GidSmem::bytes(sreg, kmax, g.C, g3.nb);
-  void (*fn)(LevelDev, SkelArgs, GramArgs, int64_t) = k_gid_cpqr;
+  // column slots per lane of the pivot-chain warp: 1, 2 or 4 by the owned columns per CTA
+  const int nown0 = GidShape(kmax, g.C).nown0;
+  void (*fn)(LevelDev, SkelArgs, GramArgs, int64_t) =
+      nown0 <= 32 ? k_gid_cpqr<1> : (nown0 <= 64 ? k_gid_cpqr<2> : k_gid_cpqr<4>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
