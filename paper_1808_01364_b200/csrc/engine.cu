@@ -1688,87 +1688,107 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     for (int g = 0; g < G.G; ++g)
       if (G.kind[g] != 0)
         for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) alive_mem[q] = red[q] ? 0 : 1;
-    // skeleton apply descriptors (offsets by prefix sums, members filled in parallel)
-    std::vector<int> sr(nsk), skt(nsk), Sd, Rd;
-    std::vector<int64_t> S_off(nsk), R_off(nsk);
-    int64_t rsum = 0, ktsum = 0;
-    for (int t = 0; t < nsk; ++t) {
-      const int g = P.skeleton[t];
-      sr[t] = L.h_rank[t];
-      skt[t] = G.size(g) - L.h_rank[t];
-      S_off[t] = rsum;
-      R_off[t] = ktsum;
-      rsum += sr[t];
-      ktsum += skt[t];
-    }
-    Sd.resize(rsum);
-    Rd.resize(ktsum);
-#pragma omp parallel for schedule(dynamic, 256)
-    for (int t = 0; t < nsk; ++t) {
-      const int g = P.skeleton[t];
-      int64_t a = S_off[t], b = R_off[t];
-      for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) {
-        if (red[q]) Rd[b++] = G.mem[q];
-        else Sd[a++] = G.mem[q];
-      }
-    }
-    for (int t = 0; t < nsk; ++t) {
-      const double mm = h_rows[t], kk = sr[t] + skt[t], rr = sr[t], kt = skt[t];
-      const double a = std::max(mm, kk), b = std::min(mm, kk);
-      L.fl[3] += 2.0 * a * b * b - 2.0 * b * b * b / 3.0 + rr * rr * kt;   // GEQP3 + T solve
-      L.by[3] += 8.0 * (mm * kk + rr * kt) + 4.0 * kk;
-      if (kt > 0) {
-        L.fl[4] += 2.0 * rr * rr * kt + 4.0 * rr * kt * kt + kt * kt * kt / 3.0 + kt * kt * rr + kt * rr * rr;
-        L.by[4] += 8.0 * (kk * kk + rr * rr + (kt + rr) * kt + rr * kt);
-      }
-    }
-    for (int t = 0; t < nsk; ++t) {
-      const double kk = sr[t] + skt[t];
-      L.sep_k_mean += kk / nsk;
-      L.sep_m_mean += (double)h_rows[t] / nsk;
-      L.sep_k_max = std::max(L.sep_k_max, kk);
-      L.sep_m_max = std::max(L.sep_m_max, (double)h_rows[t]);
-    }
-    L.rho_max = nsk ? *std::max_element(sr.begin(), sr.end()) : 0;
-    L.rho_mean = nsk ? (double)rsum / nsk : 0.0;
-    upload(L.s_r, sr, s);
-    upload(L.s_kt, skt, s);
-    upload(L.s_S, Sd, s);
-    upload(L.s_S_off, S_off, s);
-    upload(L.s_R, Rd, s);
-    upload(L.s_R_off, R_off, s);
-    upload(L.s_awork_off, awork, s);
-    L.h_S_off = S_off;
-    L.h_R_off = R_off;
-    L.h_sr = sr;
-    L.h_skt = skt;
+    // skeleton apply descriptors and the ID statistics: only the apply and the stats need them,
+    // so they are built (and uploaded) on a host thread while the next level is planned and
+    // factored; joined after the level loop (and before a level is dropped on NotSpd)
     {
-      std::vector<int> small_sk, small_pr, tiny_sk;
-      int tiny_rows = 1;
-      for (int t = 0; t < nsk; ++t) {
-        const int kk = G.size(P.skeleton[t]);
-        if (skt[t] == 0 && kk < APPLY_BIG) continue;   // full rank: the record is the identity
-        if (kk <= 64 && sr[t] > 0) {   // warp replay: rows r + 2 k~ staged per warp
-          tiny_sk.push_back(t);
-          tiny_rows = std::max(tiny_rows, sr[t] + 2 * skt[t]);
-        } else if (kk < APPLY_BIG) {
-          small_sk.push_back(t);
+      auto redp = std::make_shared<std::vector<uint8_t>>(std::move(red));
+      auto rowsp = std::make_shared<std::vector<int>>(std::move(h_rows));
+      auto pnp = std::make_shared<std::vector<int>>(std::move(pn));
+      LevelRT* Lp = &L;
+      int cur_dev = 0;
+      CK(cudaGetDevice(&cur_dev));
+      L.ap_task = std::async(std::launch::async, [Lp, redp, rowsp, pnp, nsk, r, s, cur_dev]() {
+        CK(cudaSetDevice(cur_dev));   // (a new host thread starts on device 0)
+        LevelRT& L = *Lp;
+        const LevelPlan& P = L.plan;
+        const Groups& G = P.grp;
+        const std::vector<uint8_t>& red_t = *redp;
+        const std::vector<int>& rows_t = *rowsp;
+        const std::vector<int>& pn_t = *pnp;
+        const std::vector<int64_t>& awork = L.h_awork;
+        // skeleton apply descriptors (offsets by prefix sums, members filled in parallel)
+        std::vector<int> sr(nsk), skt(nsk), Sd, Rd;
+        std::vector<int64_t> S_off(nsk), R_off(nsk);
+        int64_t rsum = 0, ktsum = 0;
+        for (int t = 0; t < nsk; ++t) {
+          const int g = P.skeleton[t];
+          sr[t] = L.h_rank[t];
+          skt[t] = G.size(g) - L.h_rank[t];
+          S_off[t] = rsum;
+          R_off[t] = ktsum;
+          rsum += sr[t];
+          ktsum += skt[t];
         }
-      }
-      L.n_apply_tiny_sk = (int)tiny_sk.size();
-      L.apply_tiny_rows = tiny_rows;
-      upload(L.d_apply_tiny_sk, tiny_sk, s);
-      int pr_max = 1;
-      for (int t = 0; t < r; ++t)
-        if (pn[t] < APPLY_BIG) {
-          small_pr.push_back(t);
-          pr_max = std::max(pr_max, pn[t]);
+        Sd.resize(rsum);
+        Rd.resize(ktsum);
+        for (int t = 0; t < nsk; ++t) {
+          const int g = P.skeleton[t];
+          int64_t a = S_off[t], b = R_off[t];
+          for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) {
+            if (red_t[q]) Rd[b++] = G.mem[q];
+            else Sd[a++] = G.mem[q];
+          }
         }
-      L.apply_small_pr_max = pr_max;
-      L.n_apply_small_sk = (int)small_sk.size();
-      L.n_apply_small_pr = (int)small_pr.size();
-      upload(L.d_apply_small_sk, small_sk, s);
-      upload(L.d_apply_small_pr, small_pr, s);
+        for (int t = 0; t < nsk; ++t) {
+          const double mm = rows_t[t], kk = sr[t] + skt[t], rr = sr[t], kt = skt[t];
+          const double a = std::max(mm, kk), b = std::min(mm, kk);
+          L.fl[3] += 2.0 * a * b * b - 2.0 * b * b * b / 3.0 + rr * rr * kt;   // GEQP3 + T solve
+          L.by[3] += 8.0 * (mm * kk + rr * kt) + 4.0 * kk;
+          if (kt > 0) {
+            L.fl[4] += 2.0 * rr * rr * kt + 4.0 * rr * kt * kt + kt * kt * kt / 3.0 + kt * kt * rr + kt * rr * rr;
+            L.by[4] += 8.0 * (kk * kk + rr * rr + (kt + rr) * kt + rr * kt);
+          }
+        }
+        for (int t = 0; t < nsk; ++t) {
+          const double kk = sr[t] + skt[t];
+          L.sep_k_mean += kk / nsk;
+          L.sep_m_mean += (double)rows_t[t] / nsk;
+          L.sep_k_max = std::max(L.sep_k_max, kk);
+          L.sep_m_max = std::max(L.sep_m_max, (double)rows_t[t]);
+        }
+        L.rho_max = nsk ? *std::max_element(sr.begin(), sr.end()) : 0;
+        L.rho_mean = nsk ? (double)rsum / nsk : 0.0;
+        upload(L.s_r, sr, s);
+        upload(L.s_kt, skt, s);
+        upload(L.s_S, Sd, s);
+        upload(L.s_S_off, S_off, s);
+        upload(L.s_R, Rd, s);
+        upload(L.s_R_off, R_off, s);
+        upload(L.s_awork_off, awork, s);
+        L.h_S_off = S_off;
+        L.h_R_off = R_off;
+        L.h_sr = sr;
+        L.h_skt = skt;
+        {
+          std::vector<int> small_sk, small_pr, tiny_sk;
+          int tiny_rows = 1;
+          for (int t = 0; t < nsk; ++t) {
+            const int kk = G.size(P.skeleton[t]);
+            if (skt[t] == 0 && kk < APPLY_BIG) continue;   // full rank: the record is the identity
+            if (kk <= 64 && sr[t] > 0) {   // warp replay: rows r + 2 k~ staged per warp
+              tiny_sk.push_back(t);
+              tiny_rows = std::max(tiny_rows, sr[t] + 2 * skt[t]);
+            } else if (kk < APPLY_BIG) {
+              small_sk.push_back(t);
+            }
+          }
+          L.n_apply_tiny_sk = (int)tiny_sk.size();
+          L.apply_tiny_rows = tiny_rows;
+          upload(L.d_apply_tiny_sk, tiny_sk, s);
+          int pr_max = 1;
+          for (int t = 0; t < r; ++t)
+            if (pn_t[t] < APPLY_BIG) {
+              small_pr.push_back(t);
+              pr_max = std::max(pr_max, pn_t[t]);
+            }
+          L.apply_small_pr_max = pr_max;
+          L.n_apply_small_sk = (int)small_sk.size();
+          L.n_apply_small_pr = (int)small_pr.size();
+          upload(L.d_apply_small_sk, small_sk, s);
+          upload(L.d_apply_small_pr, small_pr, s);
+        }
+      });
     }
     plan_ms += ms_since(tp);
     L.t_ms[5] += ms_since(tp);
@@ -1788,6 +1808,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   } catch (NotSpd& e) {
     // partial statistics: the levels completed before the failing one (errors.py:21-30)
     if (preplan.valid()) preplan.wait();   // (it reads the plan of the level being dropped)
+    for (auto& lvp : F->levels)
+      if (lvp->ap_task.valid()) lvp->ap_task.wait();
     cudaStreamSynchronize(s);
     while ((int)F->levels.size() > e.level) F->levels.pop_back();
     F->t_factor_ms = ms_since(t_start);
@@ -1797,6 +1819,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       for (auto& ev1 : ev) cudaEventDestroy(ev1);
     throw;
   }
+  for (auto& lvp : F->levels)
+    if (lvp->ap_task.valid()) lvp->ap_task.get();
   CK(cudaStreamSynchronize(s));
   F->t_factor_ms = ms_since(t_start);
   for (auto& lvp : F->levels) {

@@ -128,6 +128,9 @@ struct LevelRT {
   int n_gid = 0;      // separators on the Gram-path ID
   int64_t S = 0;
   LevelDev dev() const;
+  // apply descriptors of the separators (built on a host thread; declared last so that it is
+  // joined before the members it fills are destroyed)
+  std::future<void> ap_task;
 };
 
 struct Factorization {
