@@ -687,6 +687,9 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   std::vector<std::pair<int, int>> pairs;
   std::vector<uint8_t> alive_mem;  // survivors of the previous level, per member position
   std::future<LevelPlan> preplan;  // structure of the next level, planned while the IDs run
+  // the pre-plan completed with the survivors (sizes, offsets), on a host thread while the GPU
+  // runs the skeleton updates
+  std::future<std::pair<LevelPlan, bool>> fin_task;
   static const bool no_preplan = getenv("PHIF_NO_PREPLAN") != nullptr;
   try {
   for (int lev = 0; lev <= sp.L; ++lev) {
@@ -704,10 +707,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       DBG("level 0: planned on the device G=%d blocks=%lld", L.plan.grp.G, (long long)dp.nblocks);
     } else {
       bool done = false;
-      if (lev > 0 && preplan.valid()) {
-        LevelPlan pp = preplan.get();
-        if (finish_preplan(sp, pp, prev->plan, alive_mem)) {
-          L.plan = std::move(pp);
+      if (lev > 0 && fin_task.valid()) {
+        auto res = fin_task.get();
+        if (res.second) {
+          L.plan = std::move(res.first);
           done = true;
           DBG("level %d: pre-plan finished G=%d", lev, L.plan.grp.G);
         }
@@ -1593,6 +1596,20 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     CK(cudaStreamSynchronize(s));
     if (timing) CK(cudaEventRecord(ev[9], s));
     DBG("level %d: skeleton update nsk=%d waves=%d", lev, nsk, P.nwaves);
+    // survivors per member position, and the next level's plan completed with them on a host
+    // thread while the skeleton updates are launched and run
+    alive_mem.assign(G.mem.size(), 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int g = 0; g < G.G; ++g)
+      if (G.kind[g] != 0)
+        for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) alive_mem[q] = red[q] ? 0 : 1;
+    if (preplan.valid())
+      fin_task = std::async(std::launch::async, [&sp, &L, &alive_mem, pf = std::move(preplan)]() mutable {
+        omp_set_num_threads(std::max(2, omp_get_num_procs() / 2));
+        LevelPlan pp = pf.get();
+        const bool ok = finish_preplan(sp, pp, L.plan, alive_mem);
+        return std::make_pair(std::move(pp), ok);
+      });
     {
       // zeroing + elimination of the redundant DOFs: one CTA per small separator, large ones
       // (kt >= BIG_N) through gather -> batched GEMMs -> tile Cholesky of the panel -> A_ss -= U
@@ -1683,11 +1700,6 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       }
     }
     tp = clk::now();
-    alive_mem.assign(G.mem.size(), 0);
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int g = 0; g < G.G; ++g)
-      if (G.kind[g] != 0)
-        for (int64_t q = G.off[g]; q < G.off[g + 1]; ++q) alive_mem[q] = red[q] ? 0 : 1;
     // skeleton apply descriptors and the ID statistics: only the apply and the stats need them,
     // so they are built (and uploaded) on a host thread while the next level is planned and
     // factored; joined after the level loop (and before a level is dropped on NotSpd)
@@ -1807,7 +1819,8 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
   }
   } catch (NotSpd& e) {
     // partial statistics: the levels completed before the failing one (errors.py:21-30)
-    if (preplan.valid()) preplan.wait();   // (it reads the plan of the level being dropped)
+    if (fin_task.valid()) fin_task.wait();   // (they read the plan of the level being dropped)
+    if (preplan.valid()) preplan.wait();
     for (auto& lvp : F->levels)
       if (lvp->ap_task.valid()) lvp->ap_task.wait();
     cudaStreamSynchronize(s);

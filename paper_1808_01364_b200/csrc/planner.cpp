@@ -933,7 +933,9 @@ bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const s
   }
   if (lost) return false;
   // filtered member lists (survivors keep their ascending order and provenance)
-  std::vector<int64_t> cnt(G + 1, 0);
+  // (arrays from the host pool: recycled allocations, no fresh page faults on this path)
+  std::vector<int64_t> cnt = pool_take_i64((size_t)G + 1);
+  cnt[0] = 0;
 #pragma omp parallel for schedule(dynamic, 256)
   for (int i = 0; i < G; ++i) {
     int64_t c = 0;
@@ -942,7 +944,7 @@ bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const s
   }
   for (int i = 0; i < G; ++i) cnt[i + 1] += cnt[i];
   const int64_t tot = cnt[G];
-  std::vector<int> mem(tot), sg(tot), sp(tot), sl(tot);
+  std::vector<int> mem = pool_take_int(tot), sg = pool_take_int(tot), sp = pool_take_int(tot), sl = pool_take_int(tot);
 #pragma omp parallel for schedule(dynamic, 256)
   for (int i = 0; i < G; ++i) {
     int64_t o = cnt[i];
@@ -960,6 +962,11 @@ bool finish_preplan(const Spec& s, LevelPlan& lp, const LevelPlan& prev, const s
   g.src_group.swap(sg);
   g.src_pos.swap(sp);
   g.src_local.swap(sl);
+  lpool().give(cnt);
+  ipool().give(mem);
+  ipool().give(sg);
+  ipool().give(sp);
+  ipool().give(sl);
   // size-dependent parts of the plan
   const int64_t nb = (int64_t)lp.pat.bg.size();
   {
