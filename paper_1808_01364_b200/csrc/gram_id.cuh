@@ -267,18 +267,6 @@ __device__ __forceinline__ void bulk_cta_to_cluster(uint32_t rdst, uint32_t src,
                "r"(src), "r"(bytes), "r"(rbar)
                : "memory");
 }
-// warp argmax of (v >= 0, pos): largest v, lowest pos among ties (dlaqp2's first maximum); three
-// redux operations on the bit pattern of v. Returns the winning lane's ballot mask.
-__device__ __forceinline__ unsigned warp_first_max(double v, unsigned pos) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
-  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-  const bool top = hi == mh && lo == ml;
-  const unsigned mp = __reduce_min_sync(0xffffffffu, top ? pos : 0xffffffffu);
-  return __ballot_sync(0xffffffffu, top && pos == mp);
-}
-
 // UMAX: column slots per lane of the pivot-chain warp (owned columns per CTA <= 32 * UMAX)
 template <int UMAX>
 __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, GramArgs ga, int64_t sreg) {

@@ -733,8 +733,8 @@ __device__ void nbr_cache_load(const LevelDev& lv, const SkelArgs& sk, int s, Nb
   }
   __syncthreads();
 }
-__device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArgs& sk, const NbrCache& nc, int g, int k,
-                                               int i, int r0) {
+// rows r0 .. r0+31 of neighbour i with a nonzero in A_{h,I} (independent of the alive flags)
+__device__ __forceinline__ unsigned chunk_nz(const LevelDev& lv, const NbrCache& nc, int g, int k, int i, int r0) {
   const int lane = threadIdx.x & 31;
   const int h = nc.h[i], kh = nc.kh[i];
   const double* B = lv.pool + nc.boff[i];
@@ -777,8 +777,14 @@ __device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArg
         if (__any_sync(0xffffffffu, any[u]) && lane == rb + u) nz = true;
     }
   }
-  const bool alive = r < kh && __ldcg(sk.alive + lv.mem[nc.moff[i] + r]);
-  return __ballot_sync(0xffffffffu, nz && alive);
+  return __ballot_sync(0xffffffffu, nz);
+}
+__device__ __forceinline__ unsigned chunk_mask(const LevelDev& lv, const SkelArgs& sk, const NbrCache& nc, int g, int k,
+                                               int i, int r0) {
+  const unsigned nzm = chunk_nz(lv, nc, g, k, i, r0);
+  const int r = r0 + (threadIdx.x & 31);
+  const bool alive = r < nc.kh[i] && __ldcg(sk.alive + lv.mem[nc.moff[i] + r]);
+  return __ballot_sync(0xffffffffu, alive) & nzm;
 }
 template <int U>
 __device__ __forceinline__ void chunk_copy(const LevelDev& lv, const NbrCache& nc, int g, int k, int i, int r0,
@@ -927,6 +933,18 @@ __device__ void skel_all_redundant(const LevelDev& lv, const SkelArgs& sk, int s
   if (threadIdx.x == 0) sk.rank[s] = 0;
 }
 
+// warp argmax of (v >= 0, pos): largest v, lowest pos among ties (dlaqp2's first maximum); three
+// redux operations on the bit pattern of v. Returns the winning lane's ballot mask.
+__device__ __forceinline__ unsigned warp_first_max(double v, unsigned pos) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const bool top = hi == mh && lo == ml;
+  const unsigned mp = __reduce_min_sync(0xffffffffu, top ? pos : 0xffffffffu);
+  return __ballot_sync(0xffffffffu, top && pos == mp);
+}
+
 // Gram-path ID of one small separator (k <= 57) on one CTA: G = A^T A by DMMA into smem[0, k^2),
 // then the pivoted Cholesky replay of dlaqp2 (see gram_id.cuh) with the full symmetric Schur
 // complement updated in place, then T = R11^-1 R12 (4 threads per right-hand side). The
@@ -936,8 +954,10 @@ __device__ __forceinline__ bool skel_id_gram_fits(int k, int cap) {
   return k <= 57 && k * k <= RED_OFF && (int64_t)k * k + 7 * k + 8 <= cap;
 }
 // W holds mrows rows (kept rows and zero rows), m of them kept
+// With ds != nullptr (dependency-driven launch) the redundant flags are published and the
+// dependent separators released right after the pivot chain, before T is formed.
 __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int k, const double* W, int64_t ldw,
-                             int mrows, int m, double* smem, int cap) {
+                             int mrows, int m, double* smem, int cap, const DynSched* ds = nullptr) {
   if (!skel_id_gram_fits(k, cap)) return false;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   const int g = sk.groups[s];
@@ -1005,15 +1025,16 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
       piv[j] = 0;
       loc = better(loc, ArgMax{nj, j});
     }
+    // (values are >= 0 or the -1 "none" marker: compared through max(v, 0) bit patterns, the
+    // marker loses every tie by its index 0x7fffffff; three redux operations instead of a
+    // five-level shuffle tree)
     auto warp_best = [&](ArgMax x) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ArgMax y;
-        y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
-        y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
-        x = better(x, y);
-      }
-      return x;
+      const double xv = x.v < 0.0 ? 0.0 : x.v;
+      const int wl = __ffs(warp_first_max(xv, (unsigned)x.i)) - 1;
+      ArgMax y;
+      y.v = __shfl_sync(0xffffffffu, xv, wl);
+      y.i = __shfl_sync(0xffffffffu, x.i, wl);
+      return y;
     };
     ArgMax best = warp_best(loc);
     __syncwarp();
@@ -1102,6 +1123,23 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
       ns += __popc(bs);
     }
   }
+  // redundant flags and rank out first: the later separators only wait for these
+  {
+    uint8_t* red = sk.red + gof;
+    for (int j = tid; j < k; j += NT) {
+      const int f = piv[j];
+      red[j] = (uint8_t)f;
+      if (f) sk.alive[lv.mem[gof + j]] = 0;
+    }
+    if (tid == 0) sk.rank[s] = r;
+    if (ds) {
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        for (int64_t e = ds->succ_off[s]; e < ds->succ_off[s + 1]; ++e) atomicAdd(ds->done + ds->succ[e], 1);
+      }
+    }
+  }
   // R in pivot order (rows < r): Rp[i*k + l] = R(i, col_at[l]), in the Schur region
   double* Rp = S;
   for (int e = tid; e < r * k; e += NT) Rp[e] = Rsm[(e / k) * k + col_at[e % k]];
@@ -1132,17 +1170,41 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
       T[(int64_t)sidx[col_at[ii]] * kt + sidx[col_at[r + j]]] = X[e];
     }
   }
-  uint8_t* red = sk.red + gof;
-  for (int j = tid; j < k; j += NT) {
-    const int f = piv[j];
-    red[j] = (uint8_t)f;
-    if (f) sk.alive[lv.mem[gof + j]] = 0;
-  }
-  if (tid == 0) sk.rank[s] = r;
   return true;
 }
 
-__device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int smem_cap) {
+// Part of a small separator's ID that does not depend on the earlier separators (the alive
+// flags): coupled-group metadata and, on the Gram path, every candidate row of A_{R,I} copied to
+// its natural position in shared memory (all-zero rows as zeros), with the row's DOF index kept
+// for the alive test. In the dependency-driven launch this runs before the wait.
+// Returns true when the Gram path's shared-memory staging was taken.
+__device__ bool skel_id_pre(const LevelDev& lv, const SkelArgs& sk, int s, int smem_cap, NbrCache& nc) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g0 = sk.groups[s], k = lv.gsize[g0];
+  nbr_cache_load(lv, sk, s, nc);
+  const int nch = nc.nch;
+  if (!(sk.gram && skel_id_gram_fits(k, smem_cap) && (int64_t)max(1, nc.rows) * k <= smem_cap &&
+        nc.rows <= 2 * RED_OFF))
+    return false;
+  const int64_t ldw = max(1, nc.rows);
+  double* W = smem + SMEM_DOUBLES;
+  int* rowdof = reinterpret_cast<int*>(smem);   // (the Gram matrix takes this region later)
+  for (int ch = warp; ch < nch; ch += NT / 32) {
+    const int i = nc.locate(ch), r0 = 32 * (ch - nc.ch0[i]);
+    const unsigned nzm = chunk_nz(lv, nc, g0, k, i, r0);
+    chunk_copy<8>(lv, nc, g0, k, i, r0, nzm, W, ldw, -1 - nc.r0[i]);
+    const int r = r0 + lane;
+    if (r < nc.kh[i]) rowdof[nc.r0[i] + r] = ((nzm >> lane) & 1u) ? lv.mem[nc.moff[i] + r] : -1;
+  }
+  __syncthreads();
+  return true;
+}
+
+// pre: result of skel_id_pre for this separator (same nc). Returns true when the dependent
+// separators were already released (ds given and the early-release path taken).
+__device__ bool skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int smem_cap, NbrCache& nc, bool pre,
+                            const DynSched* ds) {
   extern __shared__ double smem[];
   double* sred = smem + RED_OFF;
   int* sint = reinterpret_cast<int*>(smem);  // scan scratch (first doubles are free here)
@@ -1160,25 +1222,31 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
     atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + (slot)), (unsigned long long)(t1 - t0)); \
     t0 = t1;                                                                                            \
   }
-  __shared__ NbrCache nc;
-  nbr_cache_load(lv, sk, s, nc);
   const int nch = nc.nch;
-  if (sk.gram && skel_id_gram_fits(k, smem_cap) && (int64_t)max(1, nc.rows) * k <= smem_cap) {
-    // Gram path: A^T A does not depend on the row order and zero rows add nothing, so one pass
-    // places every candidate row at its natural position (rejected rows as zeros): no count
-    // pass, no prefix scan; the kept-row count m only enters the rank cut floor
+  if (pre) {
+    // Gram path: A^T A does not depend on the row order and zero rows add nothing, so every
+    // candidate row sits at its natural position (skel_id_pre); the rows whose DOF an earlier
+    // separator made redundant are zeroed here, and the kept-row count m only enters the rank
+    // cut floor
     const int64_t ldw = max(1, nc.rows);
     double* W = smem + SMEM_DOUBLES;
+    const int* rowdof = reinterpret_cast<const int*>(smem);
     __shared__ int s_m;
     if (tid == 0) s_m = 0;
     __syncthreads();
-    const int lane = tid & 31, warp = tid >> 5, g0 = sk.groups[s];
+    const int lane = tid & 31, warp = tid >> 5;
     int mine = 0;
-    for (int ch = warp; ch < nch; ch += NT / 32) {
-      const int i = nc.locate(ch), r0 = 32 * (ch - nc.ch0[i]);
-      const unsigned msk = chunk_mask(lv, sk, nc, g0, k, i, r0);
-      chunk_copy<8>(lv, nc, g0, k, i, r0, msk, W, ldw, -1 - nc.r0[i]);
-      mine += __popc(msk);
+    for (int rb = 32 * warp; rb < nc.rows; rb += NT) {
+      const int rr = rb + lane;
+      const int dof = rr < nc.rows ? rowdof[rr] : -1;
+      const bool alive = dof >= 0 && __ldcg(sk.alive + dof);
+      const unsigned dead = __ballot_sync(0xffffffffu, dof >= 0 && !alive);
+      mine += __popc(__ballot_sync(0xffffffffu, alive));
+      if (dead) {
+        const bool mydead = (dead >> lane) & 1u;
+        for (int c = 0; c < k; ++c)
+          if (mydead) W[(int64_t)c * ldw + rr] = 0.0;
+      }
     }
     if (lane == 0 && mine) atomicAdd(&s_m, mine);
     __syncthreads();
@@ -1187,12 +1255,12 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
     SID_MARK(17)
     if (m == 0) {
       skel_all_redundant(lv, sk, s);
-      return;
+      return false;
     }
-    skel_id_gram(lv, sk, s, k, W, ldw, (int)ldw, m, smem, smem_cap);
+    skel_id_gram(lv, sk, s, k, W, ldw, (int)ldw, m, smem, smem_cap, ds);
     SID_MARK(18)
     if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + 23), 1ull);
-    return;
+    return ds != nullptr;
   }
   const int64_t ldw = max(1, gather_chunks<false>(lv, sk, nc, s, 0, nch, nullptr, 1, 0, sint, 512));
   SID_MARK(16)
@@ -1225,14 +1293,14 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
   uint8_t* red = sk.red + gof;
   if (m == 0) {
     skel_all_redundant(lv, sk, s);
-    return;
+    return false;
   }
   if (sk.gram) {
     __syncthreads();   // gathered rows visible to every warp
-    if (skel_id_gram(lv, sk, s, k, W, ldw, m, m, smem, smem_cap)) {
+    if (skel_id_gram(lv, sk, s, k, W, ldw, m, m, smem, smem_cap, ds)) {
       SID_MARK(18)
       if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + 23), 1ull);
-      return;
+      return ds != nullptr;
     }
   }
 #undef SID_MARK
@@ -1272,10 +1340,14 @@ __device__ void skel_id_one(const LevelDev& lv, const SkelArgs& sk, int s, int s
     if (flag[j]) sk.alive[lv.mem[gof + j]] = 0;
   }
   if (tid == 0) sk.rank[s] = r;
+  return false;
 }
 
 __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int smem_cap) {
-  skel_id_one(lv, sk, sk.order[blockIdx.x], smem_cap);
+  __shared__ NbrCache nc;
+  const int s = sk.order[blockIdx.x];
+  const bool pre = skel_id_pre(lv, sk, s, smem_cap, nc);
+  skel_id_one(lv, sk, s, smem_cap, nc, pre, nullptr);
 }
 
 // Persistent, dependency-driven separator IDs (no wave barriers): CTAs take separators in a
@@ -1284,12 +1356,15 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
 // waits only for items handed out before its own, so the chain always makes progress.
 __global__ void __launch_bounds__(NT) k_skel_id_dyn(LevelDev lv, SkelArgs sk, int smem_cap, DynSched ds) {
   __shared__ int s_item;
+  __shared__ NbrCache nc;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(ds.next, 1);
     __syncthreads();
     const int q = s_item;
     if (q >= ds.count) break;
     const int s = sk.order[q];
+    // everything that does not depend on the earlier separators first (metadata, row staging)
+    const bool pre = skel_id_pre(lv, sk, s, smem_cap, nc);
     const long long tw0 = (sk.prof && blockIdx.x == 0 && threadIdx.x == 0) ? clock64() : 0;
     if (threadIdx.x == 0) {
       volatile int* d = ds.done + s;
@@ -1300,9 +1375,9 @@ __global__ void __launch_bounds__(NT) k_skel_id_dyn(LevelDev lv, SkelArgs sk, in
     __syncthreads();
     if (sk.prof && blockIdx.x == 0 && threadIdx.x == 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(sk.prof + 19), (unsigned long long)(clock64() - tw0));
-    skel_id_one(lv, sk, s, smem_cap);
+    const bool released = skel_id_one(lv, sk, s, smem_cap, nc, pre, &ds);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !released) {
       __threadfence();
       for (int64_t e = ds.succ_off[s]; e < ds.succ_off[s + 1]; ++e) atomicAdd(ds.done + ds.succ[e], 1);
     }
