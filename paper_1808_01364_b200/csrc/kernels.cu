@@ -1012,31 +1012,25 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
   // pivots and the rank are bit-identical to that formulation (and to cta_cpqr's dlaqp2 rules).
   __shared__ int s_rank;
   if (warp == 0) {
-    // vn1 / vn2 hold squared partial norms (argmax and the dlaqp2 tests in squared form)
-    ArgMax loc{-1.0, 0x7fffffff};
+    // Column state in registers (k <= 57: columns lane and lane + 32): Schur diagonal, squared
+    // partial norms vn1 / vn2 (argmax and the dlaqp2 tests in squared form), position, pivoted.
+    double cd[2], c1[2], c2[2];
+    int cpos[2];
+    bool cpv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int b = lane + 32 * u;
+      const bool ok = b < k;
+      const double dj = ok ? S[b * k + b] : 0.0;
+      cd[u] = dj;
+      c1[u] = c2[u] = fmax(dj, 0.0);
+      cpos[u] = ok ? b : 0x7fffffff;
+      cpv[u] = !ok;
+    }
     for (int j = lane; j < k; j += 32) {
-      const double dj = S[j * k + j];
-      const double nj = fmax(dj, 0.0);
-      d[j] = dj;
-      vn1[j] = vn2[j] = nj;
-      rdv[j] = sqrt(nj);
-      invv[j] = nj > 0.0 ? 1.0 / rdv[j] : 0.0;
       col_at[j] = j;
       piv[j] = 0;
-      loc = better(loc, ArgMax{nj, j});
     }
-    // (values are >= 0 or the -1 "none" marker: compared through max(v, 0) bit patterns, the
-    // marker loses every tie by its index 0x7fffffff; three redux operations instead of a
-    // five-level shuffle tree)
-    auto warp_best = [&](ArgMax x) {
-      const double xv = x.v < 0.0 ? 0.0 : x.v;
-      const int wl = __ffs(warp_first_max(xv, (unsigned)x.i)) - 1;
-      ArgMax y;
-      y.v = __shfl_sync(0xffffffffu, xv, wl);
-      y.i = __shfl_sync(0xffffffffu, x.i, wl);
-      return y;
-    };
-    ArgMax best = warp_best(loc);
     __syncwarp();
     const double tol3z = sqrt(DBL_EPSILON * 0.5);
     const double cutrel = fmax(sk.eps, DBL_EPSILON * (double)max(m, k));
@@ -1044,63 +1038,82 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
     double cut = 0.0, cut2 = 0.0;
     int r = 0, i = 0;
     for (; i < mn; ++i) {
-      if (i > 0 && best.v < cut2) break;
-      const int pb = best.i, p = col_at[pb];
-      const double rd = i == 0 ? rdv[p] : sqrt(fmax(d[p], 0.0));   // (only the pivot needs it)
+      // local candidate: largest partial norm, lowest position among ties (dlaqp2's first maximum)
+      double bv = 0.0, bd = 0.0;
+      int bpos = 0x7fffffff, bu = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (!cpv[u] && (c1[u] > bv || (c1[u] == bv && cpos[u] < bpos))) {
+          bv = c1[u];
+          bd = cd[u];
+          bpos = cpos[u];
+          bu = u;
+        }
+      const int ci = col_at[i];   // the column leaving position i (read early: off the argmax chain)
+      const int wl = __ffs(warp_first_max(bv, (unsigned)bpos)) - 1;
+      const double wv = __shfl_sync(0xffffffffu, bv, wl);
+      const int pb = __shfl_sync(0xffffffffu, bpos, wl);
+      const int wu = __shfl_sync(0xffffffffu, bu, wl);
+      const double wd = __shfl_sync(0xffffffffu, bd, wl);
+      if (pb == 0x7fffffff) break;   // (no unpivoted column left: cannot happen while i < k)
+      if (i > 0 && wv < cut2) break;
+      const int p = wl + 32 * wu;
+      const double rd = sqrt(fmax(wd, 0.0));   // (only the pivot needs it)
+      const double inv = rd > 0.0 ? 1.0 / rd : 0.0;
       if (i == 0) {
         cut = cutrel * rd;
         cut2 = cut * (1.0 - 1e-4) * (cut * (1.0 - 1e-4));
       }
       if (rd > cut) ++r;
-      const double inv = i == 0 ? invv[p] : (rd > 0.0 ? 1.0 / rd : 0.0);
+      // row i of R, left-looking (the same FMAs in the same order as the right-looking updates)
       double* row = Rsm + i * k;
-      for (int b = lane; b < k; b += 32) {
-        double v;
-        if (b == p) {
-          v = rd;
-        } else if (piv[b]) {
-          v = 0.0;
-        } else {
-          double acc = S[p * k + b];
-#pragma unroll 8
-          for (int l = 0; l < i; ++l) acc = __fma_rn(-Rsm[l * k + p], Rsm[l * k + b], acc);
-          v = acc * inv;
-        }
-        row[b] = v;
-      }
-      __syncwarp();
-      if (lane == 0) piv[p] = 1;
-      loc = ArgMax{-1.0, 0x7fffffff};
-      // positions j > i: the dlaqp2 swap of i and pb is done by the lane owning pb (it takes over
-      // position i's column and norms); position i is final
-      for (int j = i + 1 + lane; j < k; j += 32) {
-        int col;
-        if (j == pb) {
-          col = col_at[i];
-          col_at[j] = col;
-          col_at[i] = p;
-          vn1[j] = vn1[i];
-          vn2[j] = vn2[i];
-        } else {
-          col = col_at[j];
-        }
-        const double rv = row[col];
-        const double dn = __fma_rn(-rv, rv, d[col]);
-        d[col] = dn;
-        double w1 = vn1[j];
-        if (w1 != 0.0) {
-          const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
-          if (w <= tol3z * vn2[j]) {
-            w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
-            vn2[j] = w1;
+      double rvv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int b = lane + 32 * u;
+        rvv[u] = 0.0;
+        if (b < k) {
+          double v;
+          if (b == p) {
+            v = rd;
+            cpv[u] = true;
+          } else if (cpv[u]) {
+            v = 0.0;
           } else {
-            w1 = w;
+            double acc = S[p * k + b];
+#pragma unroll 8
+            for (int l = 0; l < i; ++l) acc = __fma_rn(-Rsm[l * k + p], Rsm[l * k + b], acc);
+            v = acc * inv;
+            rvv[u] = v;
           }
-          vn1[j] = w1;
+          row[b] = v;
         }
-        loc = better(loc, ArgMax{w1, j});
       }
-      best = warp_best(loc);
+      // dlaqp2 swap of positions i and pb: the column displaced from position i moves to pb
+      if (lane == 0) {
+        col_at[pb] = ci;
+        col_at[i] = p;
+      }
+      // Schur diagonal and partial-norm downdate of the unpivoted columns
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (!cpv[u]) {
+          if (lane + 32 * u == ci) cpos[u] = pb;
+          const double rv = rvv[u];
+          const double dn = __fma_rn(-rv, rv, cd[u]);
+          cd[u] = dn;
+          double w1 = c1[u];
+          if (w1 != 0.0) {
+            const double w = fmax(__fma_rn(-rv, rv, w1), 0.0);
+            if (w <= tol3z * c2[u]) {
+              w1 = i < m - 1 ? fmax(dn, 0.0) : 0.0;
+              c2[u] = w1;
+            } else {
+              w1 = w;
+            }
+            c1[u] = w1;
+          }
+        }
       __syncwarp();
     }
     if (lane == 0) s_rank = r;
