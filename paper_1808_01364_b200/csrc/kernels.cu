@@ -1067,26 +1067,42 @@ __device__ bool skel_id_gram(const LevelDev& lv, const SkelArgs& sk, int s, int 
       if (rd > cut) ++r;
       // row i of R, left-looking (the same FMAs in the same order as the right-looking updates)
       double* row = Rsm + i * k;
-      double rvv[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int b = lane + 32 * u;
-        rvv[u] = 0.0;
-        if (b < k) {
-          double v;
-          if (b == p) {
-            v = rd;
-            cpv[u] = true;
-          } else if (cpv[u]) {
-            v = 0.0;
-          } else {
-            double acc = S[p * k + b];
+      double rvv[2] = {0.0, 0.0};
+      {
+        // both column slots advance together: two independent FMA chains per lane
+        const int b0 = lane, b1 = lane + 32;
+        const bool f0 = b0 < k && b0 != p && !cpv[0], f1 = b1 < k && b1 != p && !cpv[1];
+        double acc0 = f0 ? S[p * k + b0] : 0.0, acc1 = f1 ? S[p * k + b1] : 0.0;
+        const double* Rp0 = Rsm + p;
+        const double* Rb0 = Rsm + (f0 ? b0 : p);
+        const double* Rb1 = Rsm + (f1 ? b1 : p);
 #pragma unroll 8
-            for (int l = 0; l < i; ++l) acc = __fma_rn(-Rsm[l * k + p], Rsm[l * k + b], acc);
-            v = acc * inv;
-            rvv[u] = v;
+        for (int l = 0; l < i; ++l) {
+          const double rlp = -Rp0[l * k];
+          acc0 = __fma_rn(rlp, Rb0[l * k], acc0);
+          acc1 = __fma_rn(rlp, Rb1[l * k], acc1);
+        }
+        if (b0 < k) {
+          double v = 0.0;
+          if (b0 == p) {
+            v = rd;
+            cpv[0] = true;
+          } else if (f0) {
+            v = acc0 * inv;
+            rvv[0] = v;
           }
-          row[b] = v;
+          row[b0] = v;
+        }
+        if (b1 < k) {
+          double v = 0.0;
+          if (b1 == p) {
+            v = rd;
+            cpv[1] = true;
+          } else if (f1) {
+            v = acc1 * inv;
+            rvv[1] = v;
+          }
+          row[b1] = v;
         }
       }
       // dlaqp2 swap of positions i and pb: the column displaced from position i moves to pb
