@@ -1362,10 +1362,11 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       // Gram-path ID (gram_id.cuh) for the large separators under the same rule
       const bool use_gid = ka.gram != 0;
       std::vector<int> gid_item, gid_wi, gid_wj, gid_wit;
-      std::vector<int64_t> gid_ld, gid_goff, gid_item_off(P.nwaves + 1, 0), gid_w_off(P.nwaves + 1, 0);
+      std::vector<int64_t> gid_ld, gid_goff, gid_coff, gid_item_off(P.nwaves + 1, 0), gid_w_off(P.nwaves + 1, 0);
       std::vector<int> gid_C(P.nwaves, 1), gid_kmax(P.nwaves, 0), gid_P(P.nwaves, 1), gid_S(P.nwaves, 1);
       std::vector<uint8_t> gid_sg(P.nwaves, 0);
-      int64_t gid_gbuf = 1, gid_cnt = 1;
+      int64_t gid_gbuf = 1, gid_cnt = 1, gid_go = 0, gid_co = 0;   // (R of every item persists until k_gid_T)
+      int gid_kmax_lv = 0, gid_C_lv = 1;
       for (int w = 0; w < P.nwaves; ++w) {
         std::vector<int> large;
         for (int64_t q = P.wave_off[w]; q < P.wave_off[w + 1]; ++q) {
@@ -1404,12 +1405,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           int S = 1;
           while (S < smax && ntiles * S < 2 * num_sms && rmin / (2 * S) >= 256) S *= 2;
           gid_S[w] = S;
-          int64_t go = 0;
+          int64_t& go = gid_go;
+          if (ni) {
+            gid_kmax_lv = std::max(gid_kmax_lv, kmx);
+            gid_C_lv = std::max(gid_C_lv, gid_C[w]);
+          }
           for (int64_t q = gid_item_off[w]; q < gid_item_off[w + 1]; ++q) {
             const int t = gid_item[q];
             const int k = G.size(P.skeleton[t]);
             gid_ld.push_back(std::max<int64_t>(rows_bound[t], 1));
             gid_goff.push_back(go);
+            gid_coff.push_back(gid_co);
+            gid_co += k;
             go += gid_gbuf_doubles(k, gid_C[w], gid_sg[w], S);
             const int nt = (k + 63) / 64;
             for (int ks = 0; ks < S; ++ks)
@@ -1504,11 +1511,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       }
       L.n_large = (int)large_list.size();
       if (L.n_large) L.team_P_mean /= L.n_large;
-      DBuf d_gitem, d_gld, d_goff, d_gwit, d_gwi, d_gwj, d_gcnt, d_gbuf;
+      DBuf d_gitem, d_gld, d_goff, d_gcoff, d_gcol, d_gwit, d_gwi, d_gwj, d_gcnt, d_gbuf;
       if (!gid_item.empty()) {
         upload(d_gitem, gid_item, s);
         upload(d_gld, gid_ld, s);
         upload(d_goff, gid_goff, s);
+        upload(d_gcoff, gid_coff, s);
+        d_gcol.alloc(std::max<int64_t>(gid_co, 1) * sizeof(int), s);
         upload(d_gwit, gid_wit, s);
         upload(d_gwi, gid_wi, s);
         upload(d_gwj, gid_wj, s);
@@ -1553,6 +1562,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ga.cnt = d_gcnt.as<int>();
           ga.gbuf = d_gbuf.as<double>();
           ga.g_off = d_goff.as<int64_t>() + gid_item_off[w];
+          ga.col = d_gcol.as<int>();
+          ga.c_off = d_gcoff.as<int64_t>() + gid_item_off[w];
+          ga.CT = 1;
+          ga.tcap = 0;
           ga.w_item = d_gwit.as<int>() + gid_w_off[w];
           ga.w_i = d_gwi.as<int>() + gid_w_off[w];
           ga.w_j = d_gwj.as<int>() + gid_w_off[w];
@@ -1582,6 +1595,19 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           ta.prof = team_prof_buffer();
           launch_skel_team(dv, ka, ta, wave_blocks[w], s);
         }
+      }
+      if (!gid_item.empty()) {
+        // T = R11^-1 R12 of every Gram-path separator of the level, off the wave chain
+        GramArgs ga{};
+        ga.nitem = (int)gid_item.size();
+        ga.item_sep = d_gitem.as<int>();
+        ga.gbuf = d_gbuf.as<double>();
+        ga.g_off = d_goff.as<int64_t>();
+        ga.col = d_gcol.as<int>();
+        ga.c_off = d_gcoff.as<int64_t>();
+        ga.CT = gid_C_lv;
+        ga.tcap = gid_T_cap(gid_kmax_lv);
+        launch_gid_T(dv, ka, ga, gid_kmax_lv, s);
       }
       CK(cudaGetLastError());
       // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)

@@ -589,16 +589,51 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
   }
   const int r = sflag[1], i = sflag[2];
   if (pf) atomicAdd(reinterpret_cast<unsigned long long*>(ga.prof + 9), (unsigned long long)i);
-  const int kt = k - r;
-  // redundant flags by column (positions r..k-1) and the sorted-list index of every column
-  for (int j = tid; j < k; j += NT) piv[col_at[j]] = j >= r ? 1 : 0;
-  __syncthreads();
-  if (warp == 0) {
+  // redundant flags by column (positions r..k-1), the rank and the pivot order go out; T is formed
+  // for all waves at once by k_gid_T after the last wave
+  if (c == 0) {
+    uint8_t* redp = sk.red + gof;
+    int* colg = ga.col + ga.c_off[item];
+    for (int j = tid; j < k; j += NT) {
+      const int cj = col_at[j];
+      const int f = j >= r ? 1 : 0;
+      colg[j] = cj;
+      redp[cj] = (uint8_t)f;
+      if (f) sk.alive[lv.mem[gof + cj]] = 0;
+    }
+    if (tid == 0) sk.rank[s] = r;
+  }
+  __threadfence();
+  if (C > 1) cluster_barrier();   // no CTA leaves while a peer's bulk copy may still read its panel
+  GID_MARK(7)
+#undef GID_MARK
+}
+
+// ---- 4. T = R11^-1 R12 of every Gram-path separator of the level (after the last wave) -------
+// R(i, b) sits at Gm[b*k + i] (written by k_gid_cpqr), the pivot order in ga.col. CT CTAs per
+// item; RHS columns spread over their warps, 16/32-column blocks of R11 staged in shared memory.
+__global__ void __launch_bounds__(NT, 1) k_gid_T(LevelDev lv, SkelArgs sk, GramArgs ga) {
+  extern __shared__ double smem[];
+  const int C = ga.CT;
+  const int item = blockIdx.x / C, c = blockIdx.x % C;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  const int s = ga.item_sep[item];
+  const int g = sk.groups[s], k = lv.gsize[g];
+  const int64_t gof = lv.goff[g];
+  const int r = sk.rank[s], kt = k - r;
+  if (kt == 0 || r == 0 || sk.rows[s] == 0) return;
+  double* Gm = ga.gbuf + ga.g_off[item];
+  int* col_at = reinterpret_cast<int*>(smem + ga.tcap);
+  int* sidx = col_at + k;
+  const uint8_t* redp = sk.red + gof;
+  const int* colg = ga.col + ga.c_off[item];
+  for (int j = tid; j < k; j += NT) col_at[j] = colg[j];
+  if (warp == 0) {   // sorted-list index of every column inside its (skeleton / redundant) set
     int ns = 0, nr = 0;
     for (int j0 = 0; j0 < k; j0 += 32) {
       const int j = j0 + lane;
       const bool ok = j < k;
-      const int f = ok ? piv[j] : 0;
+      const int f = ok ? redp[j] : 0;
       const unsigned bf = __ballot_sync(0xffffffffu, ok && f), bs = __ballot_sync(0xffffffffu, ok && !f);
       const unsigned below = (1u << lane) - 1u;
       if (ok) sidx[j] = f ? nr + __popc(bf & below) : ns + __popc(bs & below);
@@ -606,17 +641,11 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       ns += __popc(bs);
     }
   }
-  __threadfence();
-  if (C > 1) cluster_barrier();   // all rows of R in global memory; no more remote reads
-  else __syncthreads();
-  GID_MARK(7)
-  // T = R11^-1 R12 (pivot order) by column back substitution; RHS columns spread over the
-  // cluster's warps, 16/32-column blocks of R11 staged in shared memory (Schur region + panel)
-  if (kt > 0 && r > 0) {
+  __syncthreads();
+  {
     double* T = sk.rec + sk.T_off[s];
     double* stage = smem;
-    const int64_t sreg2 = sreg + (int64_t)nb * ldp;
-    // staging: BW columns of R11 + NR right-hand sides per warp (host guarantees 24 k <= sreg2)
+    const int64_t sreg2 = ga.tcap;
     const int BW = sreg2 >= (int64_t)(32 + nw) * r ? 32 : 16;
     const int NR = max(1, min(4, (int)((sreg2 / r - BW) / nw)));
     double* Rs = stage;
@@ -690,16 +719,5 @@ __global__ void __launch_bounds__(NT, 1) k_gid_cpqr(LevelDev lv, SkelArgs sk, Gr
       }
       __syncwarp();
     }
-  }
-  GID_MARK(8)
-#undef GID_MARK
-  if (c == 0) {
-    uint8_t* redp = sk.red + gof;
-    for (int j = tid; j < k; j += NT) {
-      const int f = piv[j];
-      redp[j] = (uint8_t)f;
-      if (f) sk.alive[lv.mem[gof + j]] = 0;
-    }
-    if (tid == 0) sk.rank[s] = r;
   }
 }

@@ -4338,6 +4338,19 @@ void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int km
   cudaLaunchKernelEx(&cfg, fn, lv2, a2, g3, sreg);
 }
 
+// T of every Gram-path separator of the level in one launch (g.nitem items, g.CT CTAs each)
+int64_t gid_T_cap(int kmax) {
+  // staging doubles per CTA: what the CPQR kernel offered its back substitution (>= 24 kmax)
+  return std::max<int64_t>(24 * (int64_t)kmax, std::min<int64_t>(25000, 64 * (int64_t)kmax));
+}
+void launch_gid_T(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int kmax, cudaStream_t s) {
+  if (g.nitem == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const size_t bytes = (size_t)g.tcap * sizeof(double) + 2 * (size_t)kmax * sizeof(int);
+  cudaFuncSetAttribute(k_gid_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_gid_T<<<g.nitem * g.CT, NT, bytes, s>>>(lv, a, g);
+}
+
 void configure_kernels() {
   static bool done = false;
   if (done) return;

@@ -141,6 +141,10 @@ struct GramArgs {
   int C;                   // CPQR cluster size
   int S;                   // split-K factor of the Gram tiles (partial G blocks summed by the CPQR)
   int nb;                  // deferred-update panel width (<= 16)
+  int* col;                // per item: column at every pivot position (read by k_gid_T)
+  const int64_t* c_off;
+  int CT;                  // k_gid_T: CTAs per item
+  int64_t tcap;            // k_gid_T: staging doubles per CTA
   long long* prof;         // optional phase clocks of CTA 0 (PHIF_GID_PROF)
 };
 

@@ -79,6 +79,8 @@ int gid_cluster(int kmax, bool* sg);
 bool gid_fits(int k);
 int64_t gid_gbuf_doubles(int k, int C, bool sg, int S);
 void launch_gid(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int kmax, bool sg, cudaStream_t s);
+int64_t gid_T_cap(int kmax);
+void launch_gid_T(const LevelDev& lv, const SkelArgs& a, const GramArgs& g, int kmax, cudaStream_t s);
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s);
 void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& upd, DevStatus* st, cudaStream_t s);
 void launch_big_nt(const BigArgs& a, int mode, cudaStream_t s);
