@@ -2415,11 +2415,14 @@ constexpr int BT = 64, BLD = 65;
 
 // one CTA per big cell still active at this step
 __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
-  // Register-resident 64 x 64 Cholesky and triangular inverse: warp w owns rows w, w+8, ...,
-  // lane l owns columns l and l+32 (16 entries per thread). Each step publishes one column
-  // (factor) or one row (inverse) in shared memory, double-buffered: one barrier per step.
+  // 64 x 64 Cholesky and triangular inverse. The trailing block lives in registers: warp w owns
+  // rows w, w+8, ..., lane l owns columns l and l+32 (16 entries per thread). Each step publishes
+  // one column (factor) or one row (inverse) in shared memory, double-buffered: one barrier per
+  // step. The finished columns of L go to shared memory (Ls), from where the inverse reads its
+  // multipliers as warp-wide broadcasts (issued before the step's barrier).
   __shared__ double colbuf[2][BT];
   __shared__ double dinv[BT];
+  __shared__ double Ls[BT * BLD];
   __shared__ int sflag;
   const int c = a.w_cell[blockIdx.x];
   const int n = a.n[c], k0 = a.k0, kb = min(BT, n - k0);
@@ -2449,29 +2452,19 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
       break;
     }
     const double ljj = sqrt(djj), rj = 1.0 / ljj;
-    double lc[2];
-#pragma unroll
-    for (int ci = 0; ci < 2; ++ci) {
-      const int cc = lane + 32 * ci;
-      lc[ci] = cc > j ? colbuf[par][cc] * rj : 0.0;
-    }
+    // (column slot 0 holds columns <= 31: nothing left to update there once j >= 31)
+    const double lc0 = (cj == 0 && lane > j) ? colbuf[par][lane] * rj : 0.0;
+    const double lc1 = (lane + 32 > j) ? colbuf[par][lane + 32] * rj : 0.0;
 #pragma unroll
     for (int ri = 0; ri < 8; ++ri) {
       const int i = w + 8 * ri;
       if (i > j) {
         const double li = colbuf[par][i] * rj;
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
-          const int cc = lane + 32 * ci;
-          if (cc > j && cc <= i) Dr[ri][ci] = __fma_rn(-li, lc[ci], Dr[ri][ci]);
-        }
-        if (lane == lj) {
-          if (cj) Dr[ri][1] = li;
-          else Dr[ri][0] = li;
-        }
-      } else if (i == j && lane == lj) {
-        if (cj) Dr[ri][1] = ljj;
-        else Dr[ri][0] = ljj;
+        if (cj == 0 && lane > j && lane <= i) Dr[ri][0] = __fma_rn(-li, lc0, Dr[ri][0]);
+        if (lane + 32 > j && lane + 32 <= i) Dr[ri][1] = __fma_rn(-li, lc1, Dr[ri][1]);
+        if (lane == 0) Ls[i * BLD + j] = li;
+      } else if (i == j) {
+        if (lane == 0) Ls[i * BLD + j] = ljj;
       }
     }
     if (tid == 0) dinv[j] = rj;
@@ -2482,7 +2475,7 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
     return;
   }
   // X = L^-1, right-looking: row j of X is final after scaling by 1/L(j,j); rows i > j then
-  // subtract L(i,j) X(j,:) (L(i,j) from the owning lane of the row's warp by shuffle)
+  // subtract L(i,j) X(j,:). X(j, c) = 0 for c > j, so column slot 1 only takes part from j = 32.
   double Xr[8][2];
 #pragma unroll
   for (int ri = 0; ri < 8; ++ri)
@@ -2490,6 +2483,9 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
     for (int ci = 0; ci < 2; ++ci) Xr[ri][ci] = (w + 8 * ri == lane + 32 * ci) ? 1.0 : 0.0;
   for (int j = 0; j < BT; ++j) {
     const int par = j & 1, rj_i = j >> 3, wj = j & 7;
+    double lij[8];
+#pragma unroll
+    for (int ri = 0; ri < 8; ++ri) lij[ri] = Ls[(w + 8 * ri) * BLD + j];   // (rows <= j: never used)
     if (w == wj) {
 #pragma unroll
       for (int ri = 0; ri < 8; ++ri)
@@ -2501,15 +2497,19 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
           }
     }
     __syncthreads();
-    const double x0 = colbuf[par][lane], x1 = colbuf[par][lane + 32];
+    const double x0 = colbuf[par][lane];
+    if (j < 32) {
 #pragma unroll
-    for (int ri = 0; ri < 8; ++ri) {
-      const int i = w + 8 * ri;
-      const double lij = __shfl_sync(0xffffffffu, (j >> 5) ? Dr[ri][1] : Dr[ri][0], j & 31);
-      if (i > j) {
-        Xr[ri][0] = __fma_rn(-lij, x0, Xr[ri][0]);
-        Xr[ri][1] = __fma_rn(-lij, x1, Xr[ri][1]);
-      }
+      for (int ri = 0; ri < 8; ++ri)
+        if (w + 8 * ri > j) Xr[ri][0] = __fma_rn(-lij[ri], x0, Xr[ri][0]);
+    } else {
+      const double x1 = colbuf[par][lane + 32];
+#pragma unroll
+      for (int ri = 0; ri < 8; ++ri)
+        if (w + 8 * ri > j) {
+          Xr[ri][0] = __fma_rn(-lij[ri], x0, Xr[ri][0]);
+          Xr[ri][1] = __fma_rn(-lij[ri], x1, Xr[ri][1]);
+        }
     }
   }
   double* Lo = a.Linv + (int64_t)c * BT * BT;
@@ -2519,7 +2519,7 @@ __global__ void __launch_bounds__(NT) k_big_diag(BigArgs a, DevStatus* st) {
     for (int ci = 0; ci < 2; ++ci) {
       const int i = w + 8 * ri, cc = lane + 32 * ci;
       Lo[i * BT + cc] = Xr[ri][ci];
-      if (i < kb && cc < kb) P[(int64_t)(k0 + i) * n + k0 + cc] = (cc <= i) ? Dr[ri][ci] : 0.0;
+      if (i < kb && cc < kb) P[(int64_t)(k0 + i) * n + k0 + cc] = (cc <= i) ? Ls[i * BLD + cc] : 0.0;
     }
   // (the strict upper part of the square block is zeroed once at the end: k_big_zero_upper)
 }
