@@ -1910,6 +1910,31 @@ static void push_seg(std::vector<int64_t>& src, std::vector<int64_t>& dst, std::
   }
 }
 
+// Order the work items [begin, end) of one replay-GEMM launch by decreasing K depth (stable): the
+// persistent CTAs of k_rgemm take items w, w + G, w + 2G, ..., so every CTA gets one item of each
+// depth tier (imbalance at most one item) and the shortest items fill the tail.
+static void balance_items(std::vector<int>& wd, std::vector<int>& wt, size_t begin, size_t end,
+                          const std::vector<GemmDesc>& d) {
+  if (end - begin < 2) return;
+  auto depth = [&](size_t i) {
+    const GemmDesc& g = d[wd[i]];
+    const int i0 = 64 * wt[i];
+    if (g.tri == 1) return std::min(g.K, i0 + 64);
+    if (g.tri == 3) return g.K - i0;
+    return g.K;
+  };
+  std::vector<std::pair<int, size_t>> key(end - begin);
+  for (size_t i = begin; i < end; ++i) key[i - begin] = {-depth(i), i};
+  std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<int> nd(end - begin), nt(end - begin);
+  for (size_t j = 0; j < key.size(); ++j) {
+    nd[j] = wd[key[j].second];
+    nt[j] = wt[key[j].second];
+  }
+  std::copy(nd.begin(), nd.end(), wd.begin() + begin);
+  std::copy(nt.begin(), nt.end(), wt.begin() + begin);
+}
+
 // GEMM replay of big cells: L^-T is stored below [L ; X^T] in the panel.
 struct BigApply {
   int k = -1;
@@ -1918,6 +1943,7 @@ struct BigApply {
   DBuf desc;                  // 4 phases of descriptors
   DBuf wd, wt;                // work lists (descriptor, row tile)
   int64_t ph_off[5] = {0, 0, 0, 0, 0};
+  int ph_kmean[4] = {0, 0, 0, 0};   // mean K depth per work item of each phase
   DBuf gi_src, gi_dst, gi_len, sc_src, sc_dst, sc_len, gb_src, gb_dst, gb_len;
   int nbig = 0, nseg_i = 0, nseg_b = 0;
   void build(Factorization& F, LevelRT& L, int kk) {
@@ -1931,9 +1957,11 @@ struct BigApply {
     std::vector<int> wd_h, wt_h;
     std::vector<int64_t> isrc, idst, sdst, bsrc, bdst;
     std::vector<int> ilen, blen;
+    int64_t ksum = 0;
     auto add = [&](const double* A, int lda, int ta, const double* B, double* C, int M, int K, double al,
                    double be, int tri) {
       if (M <= 0) return;
+      ksum += (int64_t)((M + 63) / 64) * (tri ? (K + 1) / 2 : K);
       GemmDesc g;
       g.tri = tri;
       g.A = A;
@@ -1961,6 +1989,7 @@ struct BigApply {
     // phase 0: Z = (L^-T)^T Y ; phase 1: W = X^T Z ; phase 2: Y -= X Xb ; phase 3: Z = L^-T Y
     for (int ph = 0; ph < 4; ++ph) {
       ph_off[ph] = (int64_t)wd_h.size();
+      ksum = 0;
       for (int t : cells) {
         const int n = P.cell_n[t], b = P.cell_b[t];
         const double* Pp = rec + L.h_P_off[t];
@@ -1974,6 +2003,8 @@ struct BigApply {
         if (ph == 2 && b > 0) add(XT, n, 1, Xb, Y, n, b, -1.0, 1.0, 0);
         if (ph == 3) add(LiT, n, 0, Y, Z, n, n, 1.0, 0.0, 3);   // L^-T: upper
       }
+      ph_kmean[ph] = (int)(ksum / std::max<int64_t>(1, (int64_t)wd_h.size() - ph_off[ph]));
+      balance_items(wd_h, wt_h, (size_t)ph_off[ph], wd_h.size(), d);
     }
     ph_off[4] = (int64_t)wd_h.size();
     std::vector<int64_t> ssrc;
@@ -2001,7 +2032,7 @@ struct BigApply {
   }
   void phase(int ph, cudaStream_t s) const {
     launch_rgemm(desc.as<GemmDesc>(), wd.as<int>() + ph_off[ph], wt.as<int>() + ph_off[ph],
-                 (int)(ph_off[ph + 1] - ph_off[ph]), k, s);
+                 (int)(ph_off[ph + 1] - ph_off[ph]), k, s, ph_kmean[ph]);
   }
   void up(LevelRT& L, double* x, cudaStream_t s) const {
     launch_rows(work, x, L.mem.as<int>(), gi_src.as<int64_t>(), gi_dst.as<int64_t>(), gi_len.as<int>(), nseg_i, k,
@@ -2040,6 +2071,7 @@ struct GemmReplay {
     int kind;      // 0 gather, 1 scatter, 2 gemm
     int64_t off, cnt;
     int idx;       // gather/scatter index array: 0 members, 1 skeleton DOFs, 2 redundant DOFs
+                   // (GEMM steps: mean K depth per work item)
   };
   std::vector<Step> steps[4];   // 0 prec up, 1 prec down, 2 skel up, 3 skel down
   DBuf desc, wd, wt, ss, sd, sl;
@@ -2054,13 +2086,17 @@ struct GemmReplay {
     std::vector<int64_t> src, dst;
     std::vector<int> len;
     auto seg_begin = [&]() { return (int64_t)src.size(); };
+    int64_t ksum = 0;
     auto add_step = [&](int which, int kind, int64_t off, int idx) {
       const int64_t cnt = (kind == 2 ? (int64_t)wdh.size() : (int64_t)src.size()) - off;
-      if (cnt > 0) steps[which].push_back({kind, off, cnt, idx});
+      if (cnt > 0) steps[which].push_back({kind, off, cnt, kind == 2 ? (int)(ksum / cnt) : idx});
+      if (kind == 2) balance_items(wdh, wth, (size_t)off, wdh.size(), d);
+      ksum = 0;
     };
     auto gemm = [&](const double* A, int lda, int ta, const double* B, double* C, int M, int K, double al,
                     double be) {
       if (M <= 0 || K <= 0) return;
+      ksum += (int64_t)((M + 63) / 64) * K;
       GemmDesc g{A, B, C, M, k, K, lda, k, k, ta, al, be};
       const int id = (int)d.size();
       d.push_back(g);
@@ -2144,7 +2180,7 @@ struct GemmReplay {
   void run(int which, LevelRT& L, double* x, cudaStream_t s) const {
     for (const Step& st : steps[which]) {
       if (st.kind == 2) {
-        launch_rgemm(desc.as<GemmDesc>(), wd.as<int>() + st.off, wt.as<int>() + st.off, (int)st.cnt, k, s);
+        launch_rgemm(desc.as<GemmDesc>(), wd.as<int>() + st.off, wt.as<int>() + st.off, (int)st.cnt, k, s, st.idx);
       } else {
         const int* idx = st.idx == 0 ? L.mem.as<int>() : (st.idx == 1 ? L.s_S.as<int>() : L.s_R.as<int>());
         launch_rows(work, x, idx, ss.as<int64_t>() + st.off, sd.as<int64_t>() + st.off, sl.as<int>() + st.off,
@@ -2363,14 +2399,15 @@ PcgResult pcg(const Matrix& A, Factorization* F, const double* b, double* x, int
     spmv(A, Pv.as<double>(), Q.as<double>(), k, s);
     launch_dot(Pv.as<double>(), Q.as<double>(), N, k, part.as<double>(), pq, s);
     launch_pcg_alpha(rz, pq, act, alpha, ctl, it, k, s);
-    launch_axpy(x, Pv.as<double>(), alpha, 1.0, act, N, k, s);
     if (it % 50 == 0) {   // true residual
+      launch_axpy(x, Pv.as<double>(), alpha, 1.0, act, N, k, s);
       spmv(A, x, Q.as<double>(), k, s);
       launch_sub(R.as<double>(), b, Q.as<double>(), act, N, k, s);
-    } else {
-      launch_axpy(R.as<double>(), Q.as<double>(), alpha, -1.0, act, N, k, s);
+      launch_dot(R.as<double>(), R.as<double>(), N, k, part.as<double>(), rn2, s);
+    } else {   // x += alpha p ; r -= alpha q ; ||r||^2 in one pass
+      launch_pcg_update(x, Pv.as<double>(), R.as<double>(), Q.as<double>(), alpha, act, N, k, part.as<double>(), rn2,
+                        s);
     }
-    launch_dot(R.as<double>(), R.as<double>(), N, k, part.as<double>(), rn2, s);
     launch_pcg_check(rn2, bn, act, relres, iters, conv, hp, it, tol, ctl, k, s);
     read_ctl();
     if (hctl[1]) break;

@@ -330,21 +330,54 @@ __global__ void k_band_check(const int64_t* rowptr, const int* col, const int* g
 }
 
 // A_BB -= sum_c X_c^T X_c, owner-computes per target block, contributions in cell order.
+// blockIdx.y splits the rows of a target block (deep levels have few, large blocks); a warp owns
+// a row, lanes run along the columns (coalesced, no index division). The per-element summation
+// order is the cell order whatever the split.
 __global__ void __launch_bounds__(NT) k_schur(LevelDev lv, SchurArgs sa) {
   const int tau = blockIdx.x;
   const int blk = sa.tgt_blk[tau];
   const int rows = lv.gsize[lv.bg[blk]], cols = lv.gsize[lv.bh[blk]];
   double* dst = lv.pool + lv.boff[blk];
   const int64_t c0 = sa.tgt_off[tau], c1 = sa.tgt_off[tau + 1];
-  for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += NT) {
-    const int i = (int)(e / cols), j = (int)(e % cols);
-    double s = dst[e];
-    for (int64_t c = c0; c < c1; ++c) {
-      const int cell = sa.con_cell[c];
-      const int bb = sa.cell_b[cell];
-      s -= sa.U[sa.U_off[cell] + (int64_t)(sa.con_row[c] + i) * bb + sa.con_col[c] + j];
+  if (rows * cols <= 2048) {   // small block: one pass of the CTA over the elements
+    if (blockIdx.y) return;
+    for (int e = threadIdx.x; e < rows * cols; e += NT) {
+      const int i = e / cols, j = e - i * cols;
+      double s = dst[e];
+      for (int64_t c = c0; c < c1; ++c) {
+        const int cell = sa.con_cell[c];
+        s -= sa.U[sa.U_off[cell] + (int64_t)(sa.con_row[c] + i) * sa.cell_b[cell] + sa.con_col[c] + j];
+      }
+      dst[e] = s;
     }
-    dst[e] = s;
+    return;
+  }
+  const int lane = threadIdx.x & 31, wpb = NT / 32;
+  for (int i = blockIdx.y * wpb + (threadIdx.x >> 5); i < rows; i += gridDim.y * wpb) {
+    double* drow = dst + (int64_t)i * cols;
+    for (int j0 = 0; j0 < cols; j0 += 128) {   // four columns per lane in flight
+      double s[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + 32 * u + lane;
+        s[u] = j < cols ? drow[j] : 0.0;
+      }
+      for (int64_t c = c0; c < c1; ++c) {
+        const int cell = sa.con_cell[c];
+        const int bb = sa.cell_b[cell];
+        const double* urow = sa.U + sa.U_off[cell] + (int64_t)(sa.con_row[c] + i) * bb + sa.con_col[c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + 32 * u + lane;
+          if (j < cols) s[u] -= urow[j];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + 32 * u + lane;
+        if (j < cols) drow[j] = s[u];
+      }
+    }
   }
 }
 
@@ -2667,11 +2700,150 @@ __device__ __forceinline__ void cp_async_wait() {
 // global memory through the read-only path (8 full 32-byte sectors per load in either storage
 // order); only the small right-hand-side chunk B[kc:kc+64, 0:N] is staged in shared memory.
 // NT8 = ceil(N / 8) output column tiles per warp.
-constexpr int RG_K = 64;
-template <int NT8>
-__global__ void __launch_bounds__(NT) k_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork) {
+// The CTA walks its work items as one stream of 64-deep K chunks, pipelined ACROSS items: while
+// chunk s is multiplied, the operands of chunk s+1 (possibly the first chunk of the next item)
+// are in flight, and the descriptor of the item after that and the list entry of the one after
+// that are prefetched. Records with K <= 64 (level-0/1 cells and separators) therefore cost one
+// hidden round trip instead of four exposed ones. Arithmetic order per item is unchanged.
+// RG_K = K depth of a chunk: 32 (3 CTAs per SM) for launches of shallow records, 64 (2 CTAs per SM,
+// half the barriers and exposed steps) for deep ones; the host picks per launch from the mean K.
+template <int NT8, int RG_K>
+__global__ void __launch_bounds__(NT, RG_K == 32 ? 3 : 2) k_rgemm(const GemmDesc* __restrict__ desc, const int* __restrict__ w_desc,
+                                                  const int* __restrict__ w_tile, int nwork, int N) {   // N = columns of every item (nrhs)
   constexpr int LDB = NT8 * 8 + 4;
   __shared__ double sB[2][RG_K * LDB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int G = gridDim.x;
+  // stage I: list entry (descriptor id, row tile) of the item three ahead
+  int wI = blockIdx.x, pdI = -1, ptI = 0;
+  auto fetchI = [&]() {
+    pdI = -1;
+    if (wI < nwork) {
+      pdI = __ldg(w_desc + wI);
+      ptI = __ldg(w_tile + wI);
+    }
+    wI += G;
+  };
+  // stage D: raw descriptor of the item two ahead
+  const double *dA = nullptr, *dB = nullptr;
+  int dM = 0, dK = 0, dlda = 0, dldb = 0, dtA = 0, dtri = 0, ddi = -1, di0 = 0;
+  auto fetchD = [&]() {
+    ddi = pdI;
+    if (pdI >= 0) {
+      const GemmDesc* p = desc + pdI;
+      dA = p->A;
+      dB = p->B;
+      dM = p->M;
+      dK = p->K;
+      dlda = p->lda;
+      dldb = p->ldb;
+      dtA = p->transA;
+      dtri = p->tri;
+      di0 = 64 * ptI;
+    }
+    fetchI();
+  };
+  // stage L: the item whose chunks are being issued
+  const double *lAr = nullptr, *lB = nullptr;
+  int64_t lsk = 1;
+  int lldb = 0, lkend = 0, lkc = 0, ldi = -1, li0 = 0;
+  bool lrok = false;
+  auto openL = [&]() {
+    ldi = ddi;
+    if (ddi >= 0) {
+      const int row = di0 + warp * 8 + g;
+      lrok = row < dM;
+      lsk = dtA ? dlda : 1;                                   // A(row, k) = A[row*sr + k*sk]
+      lAr = dA + (lrok ? (int64_t)row * (dtA ? 1 : dlda) : 0);
+      lB = dB;
+      lldb = dldb;
+      // triangular records: op(A) lower (tri 1) ends the K range at the tile's last row, op(A)
+      // upper (tri 3) starts it at the tile's first row; the skipped terms are structural zeros
+      lkc = dtri == 3 ? (di0 / RG_K) * RG_K : 0;
+      lkend = dtri == 1 ? min(dK, di0 + 64) : dK;
+      li0 = di0;
+    }
+    fetchD();
+  };
+  // issue the loads of L's next chunk; returns its tag (descriptor id, row tile start, last chunk)
+  auto issue = [&](double* a, int buf, int& tdi, int& ti0, bool& tlast) {
+#pragma unroll
+    for (int s = 0; s < RG_K / 4; ++s) {
+      const int kg = lkc + 4 * s + t4;
+      a[s] = (lrok && kg < lkend) ? __ldg(lAr + (int64_t)kg * lsk) : 0.0;
+    }
+    for (int e = tid; e < RG_K * NT8 * 8; e += NT) {
+      const int kk = e / (NT8 * 8), c = e % (NT8 * 8);
+      const bool ok = lkc + kk < lkend && c < N;
+      cp_async8(&sB[buf][kk * LDB + c], lB + (ok ? (int64_t)(lkc + kk) * lldb + c : 0), ok);
+    }
+    cp_async_commit();
+    tdi = ldi;
+    ti0 = li0;
+    lkc += RG_K;
+    tlast = lkc >= lkend;
+    if (tlast) openL();
+  };
+  fetchI();
+  fetchD();
+  openL();
+  if (ldi < 0) return;
+  double a0[RG_K / 4], a1[RG_K / 4];
+  double acc[NT8][2];
+#pragma unroll
+  for (int y = 0; y < NT8; ++y) acc[y][0] = acc[y][1] = 0.0;
+  int t0di, t0i0, t1di = -1, t1i0 = 0;
+  bool t0last, t1last = false;
+  issue(a0, 0, t0di, t0i0, t0last);
+  int buf = 0;
+  while (true) {
+    const bool more = ldi >= 0;   // (uniform over the CTA: every thread walks the same list)
+    if (more) {
+      issue(a1, buf ^ 1, t1di, t1i0, t1last);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < RG_K / 4; ++s)
+#pragma unroll
+      for (int y = 0; y < NT8; ++y) dmma(acc[y][0], acc[y][1], a0[s], sB[buf][(4 * s + t4) * LDB + y * 8 + g]);
+    if (t0last) {
+      const GemmDesc* p = desc + t0di;
+      const int row = t0i0 + warp * 8 + g;
+      if (row < p->M) {
+        const double alpha = p->alpha, beta = p->beta;
+        double* crow = p->C + (int64_t)row * p->ldc;
+#pragma unroll
+        for (int y = 0; y < NT8; ++y)
+#pragma unroll
+          for (int z = 0; z < 2; ++z) {
+            const int c = y * 8 + 2 * t4 + z;
+            if (c < N) crow[c] = (beta == 0.0 ? 0.0 : beta * crow[c]) + alpha * acc[y][z];
+          }
+      }
+#pragma unroll
+      for (int y = 0; y < NT8; ++y) acc[y][0] = acc[y][1] = 0.0;
+    }
+    __syncthreads();
+    if (!more) break;
+#pragma unroll
+    for (int s = 0; s < RG_K / 4; ++s) a0[s] = a1[s];
+    t0di = t1di;
+    t0i0 = t1i0;
+    t0last = t1last;
+    buf ^= 1;
+  }
+}
+
+// Deep records (mean K >= 128): one item at a time per CTA, K in 64-deep chunks, two-stage
+// operand prefetch inside the item; CTAs are scheduled by the hardware (grid-stride over the list).
+constexpr int RGD_K = 64;
+template <int NT8>
+__global__ void __launch_bounds__(NT) k_rgemm_deep(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork) {
+  constexpr int LDB = NT8 * 8 + 4;
+  __shared__ double sB[2][RGD_K * LDB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
     const GemmDesc d = desc[w_desc[w]];
@@ -2685,45 +2857,45 @@ __global__ void __launch_bounds__(NT) k_rgemm(const GemmDesc* desc, const int* w
     for (int y = 0; y < NT8; ++y) acc[y][0] = acc[y][1] = 0.0;
     auto load_a = [&](double* a, int kc) {
 #pragma unroll
-      for (int s = 0; s < RG_K / 4; ++s) {
+      for (int s = 0; s < RGD_K / 4; ++s) {
         const int kg = kc + 4 * s + t4;
         a[s] = (rok && kg < d.K) ? __ldg(Ar + (int64_t)kg * sk) : 0.0;
       }
     };
     auto stage_b = [&](int buf, int kc) {
-      for (int e = tid; e < RG_K * NT8 * 8; e += NT) {
+      for (int e = tid; e < RGD_K * NT8 * 8; e += NT) {
         const int kk = e / (NT8 * 8), c = e % (NT8 * 8);
         const bool ok = kc + kk < d.K && c < d.N;
         cp_async8(&sB[buf][kk * LDB + c], d.B + (ok ? (int64_t)(kc + kk) * d.ldb + c : 0), ok);
       }
       cp_async_commit();
     };
-    double a0[RG_K / 4], a1[RG_K / 4];
+    double a0[RGD_K / 4], a1[RGD_K / 4];
     // triangular records: op(A) lower (tri 1) ends the K range at the tile's last row, op(A)
     // upper (tri 3) starts it at the tile's first row; the skipped terms are structural zeros
-    const int kbeg = d.tri == 3 ? (i0 / RG_K) * RG_K : 0;
+    const int kbeg = d.tri == 3 ? (i0 / RGD_K) * RGD_K : 0;
     const int kend = d.tri == 1 ? min(d.K, i0 + 64) : d.K;
     __syncthreads();   // previous work item's reads of sB are done
     load_a(a0, kbeg);
     stage_b(0, kbeg);
     int buf = 0;
-    for (int kc = kbeg; kc < kend; kc += RG_K) {
-      const bool more = kc + RG_K < kend;
+    for (int kc = kbeg; kc < kend; kc += RGD_K) {
+      const bool more = kc + RGD_K < kend;
       if (more) {
-        load_a(a1, kc + RG_K);
-        stage_b(buf ^ 1, kc + RG_K);
+        load_a(a1, kc + RGD_K);
+        stage_b(buf ^ 1, kc + RGD_K);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
 #pragma unroll
-      for (int s = 0; s < RG_K / 4; ++s)
+      for (int s = 0; s < RGD_K / 4; ++s)
 #pragma unroll
         for (int y = 0; y < NT8; ++y) dmma(acc[y][0], acc[y][1], a0[s], sB[buf][(4 * s + t4) * LDB + y * 8 + g]);
       __syncthreads();
 #pragma unroll
-      for (int s = 0; s < RG_K / 4; ++s) a0[s] = a1[s];
+      for (int s = 0; s < RGD_K / 4; ++s) a0[s] = a1[s];
       buf ^= 1;
     }
     if (rok) {
@@ -3341,6 +3513,172 @@ __global__ void __launch_bounds__(128) k_apply_skel_warp(ApplySkelArgs a, const 
   for (int e = lane; e < kt * k; e += 32) x[(int64_t)R[e / k] * k + e % k] = Z[e];
 }
 
+// ---------------------------------------------------------------------------
+// Warp-level DMMA replay of the small records for 32 right-hand sides (one warp per record).
+// The record matrices are read straight from global memory as m8n8k4 A fragments (coalesced,
+// every element once, all loads of a row tile in flight together); the right-hand-side rows are
+// staged in shared memory (row stride TW_LD: conflict-free B fragments). No FMA dependency chain
+// and no broadcast loads, which bound the lane-per-RHS kernels above.
+// ---------------------------------------------------------------------------
+constexpr int TW_LD = 36;
+// acc(i, 0:32) = sum_j M(i, j) sB[j][0:32] for i < m, j in the row tile's K range:
+//   M(i, j) = TRANS ? Mg[j*ld + i] : Mg[i*ld + j];  tri 0: j < kk; 1 (lower): j < min(kk, 8mt+8);
+//   3 (upper): j >= 8mt. sB rows up to the next multiple of 4 of kk must be finite (zero padded).
+// epi(row, ok, acc) receives each finished 8-row tile: lane (g, t4) holds row 8mt+g, columns
+// 8y + 2 t4 + {0, 1} in acc[y][0..1].
+template <bool TRANS, typename Epi>
+__device__ __forceinline__ void warp_mm32(const double* __restrict__ Mg, int ld, int m, int kk, int tri,
+                                          const double* sB, Epi epi) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int nmt = (m + 7) >> 3;
+  if (nmt == 0) return;
+  auto klo = [&](int mt) { return tri == 3 ? 8 * mt : 0; };
+  auto khi = [&](int mt) { return tri == 1 ? min(kk, 8 * mt + 8) : kk; };
+  auto load = [&](double* a, int mt, int k0) {
+    const int row = 8 * mt + g, hi = khi(mt);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int kg = k0 + 4 * s + t4;
+      a[s] = (row < m && kg < hi) ? __ldg(TRANS ? Mg + (int64_t)kg * ld + row : Mg + (int64_t)row * ld + kg) : 0.0;
+    }
+  };
+  double a0[8], a1[8], acc[4][2];
+#pragma unroll
+  for (int y = 0; y < 4; ++y) acc[y][0] = acc[y][1] = 0.0;
+  int mt = 0, k0 = klo(0);
+  load(a0, mt, k0);
+  while (mt < nmt) {
+    int nm = mt, nk = k0 + 32;
+    if (nk >= khi(mt)) {
+      nm = mt + 1;
+      nk = klo(nm);
+    }
+    if (nm < nmt) load(a1, nm, nk);
+    const int hi = khi(mt);
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (k0 + 4 * s < hi) {   // (warp-uniform)
+        const double* b = sB + (k0 + 4 * s + t4) * TW_LD + g;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma(acc[y][0], acc[y][1], a0[s], b[8 * y]);
+      }
+    if (nm != mt) {
+      epi(8 * mt + g, 8 * mt + g < m, acc);
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[y][0] = acc[y][1] = 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) a0[s] = a1[s];
+    mt = nm;
+    k0 = nk;
+  }
+}
+
+// stage rows x[idx[i]] (i < n) of a 32-column block into sY (row stride TW_LD), zero rows up to
+// the next multiple of 4; lane = column, 8 row loads in flight
+__device__ __forceinline__ void warp_stage32(double* sY, const double* x, const int* __restrict__ idx, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int q0 = 0; q0 < n; q0 += 32) {
+    const int mine = q0 + lane < n ? __ldg(idx + q0 + lane) : 0;
+    const int lim = min(32, n - q0);
+    for (int q1 = 0; q1 < lim; q1 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int gi = __shfl_sync(0xffffffffu, mine, (q1 + u) & 31);
+        v[u] = q1 + u < lim ? x[(int64_t)gi * 32 + lane] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q1 + u < lim) sY[(q0 + q1 + u) * TW_LD + lane] = v[u];
+    }
+  }
+  for (int i = n; i < ((n + 3) & ~3); ++i) sY[i * TW_LD + lane] = 0.0;
+}
+
+// block-Jacobi records (|g| < APPLY_BIG), 32 right-hand sides: x_g <- L^-1 x_g (up) / L^-T x_g
+__global__ void __launch_bounds__(256) k_apply_prec_mma(ApplyPrecArgs a, double* x, int up, int ldn) {
+  extern __shared__ double smem[];
+  const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t4 = lane & 3;
+  const int wg = blockIdx.x * wpc + warp;
+  if (wg >= a.r) return;
+  const int t = a.list ? a.list[wg] : wg;
+  const int n = a.n[t];
+  const int* I = a.I + a.I_off[t];
+  const double* LiT = a.rec + a.L_off[t] + (int64_t)n * n;
+  double* sY = smem + (size_t)warp * ldn * TW_LD;
+  warp_stage32(sY, x, I, n);
+  __syncwarp();
+  auto epi = [&](int row, bool ok, double (&acc)[4][2]) {
+    if (!ok) return;
+    double* xr = x + (int64_t)__ldg(I + row) * 32 + 2 * t4;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) *reinterpret_cast<double2*>(xr + 8 * y) = make_double2(acc[y][0], acc[y][1]);
+  };
+  if (up) warp_mm32<true>(LiT, n, n, n, 1, sY, epi);    // L^-1 = (L^-T)^T: lower
+  else warp_mm32<false>(LiT, n, n, n, 3, sY, epi);      // L^-T: upper
+}
+
+// small separators (|g| <= 64, r > 0), 32 right-hand sides; records T (r x k~), X~^T (r x k~),
+// L~^-T (k~ x k~):  up:   Y_r -= T^T Y_s ; Z = L~^-1 Y_r ; Y_s -= X~^T Z
+//                    down: Y_r -= X~ Y_s  ; Z = L~^-T Y_r ; Y_s -= T Z      (x_R <- Z, x_S <- Y_s)
+__global__ void __launch_bounds__(128) k_apply_skel_mma(ApplySkelArgs a, const int* list, int n, double* x, int up,
+                                                        int ldrows) {
+  extern __shared__ double smem[];
+  const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t4 = lane & 3;
+  const int idx = blockIdx.x * wpc + warp;
+  if (idx >= n) return;
+  const int t = list[idx];
+  const int r = a.r[t], kt = a.kt[t];
+  const int* S = a.S + a.S_off[t];
+  const int* R = a.R + a.R_off[t];
+  const double* T = a.rec + a.T_off[t];                      // r x kt
+  const double* PB = a.rec + a.P_off[t] + (int64_t)kt * kt;   // X~^T: r x kt
+  const double* LiT = PB + (int64_t)r * kt;                  // L~^-T: kt x kt (upper)
+  const int rp = (r + 3) & ~3, kp = (kt + 3) & ~3;
+  double* sYs = smem + (size_t)warp * ldrows * TW_LD;
+  double* sYr = sYs + (size_t)rp * TW_LD;
+  double* sZ = sYr + (size_t)kp * TW_LD;
+  warp_stage32(sYs, x, S, r);
+  warp_stage32(sYr, x, R, kt);
+  for (int i = kt; i < kp; ++i) sZ[i * TW_LD + lane] = 0.0;
+  __syncwarp();
+  const double* M1 = up ? T : PB;   // Y_r -= M1^T Y_s
+  const double* M3 = up ? PB : T;   // Y_s -= M3 Z
+  warp_mm32<true>(M1, kt, kt, r, 0, sYs, [&](int row, bool ok, double (&acc)[4][2]) {
+    if (!ok) return;
+    double* yr = sYr + row * TW_LD + 2 * t4;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      yr[8 * y] -= acc[y][0];
+      yr[8 * y + 1] -= acc[y][1];
+    }
+  });
+  __syncwarp();
+  auto epi2 = [&](int row, bool ok, double (&acc)[4][2]) {
+    if (!ok) return;
+    double* z = sZ + row * TW_LD + 2 * t4;
+    double* xr = x + (int64_t)__ldg(R + row) * 32 + 2 * t4;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      z[8 * y] = acc[y][0];
+      z[8 * y + 1] = acc[y][1];
+      *reinterpret_cast<double2*>(xr + 8 * y) = make_double2(acc[y][0], acc[y][1]);
+    }
+  };
+  if (up) warp_mm32<true>(LiT, kt, kt, kt, 1, sYr, epi2);
+  else warp_mm32<false>(LiT, kt, kt, kt, 3, sYr, epi2);
+  __syncwarp();
+  warp_mm32<false>(M3, kt, r, kt, 0, sZ, [&](int row, bool ok, double (&acc)[4][2]) {
+    if (!ok) return;
+    const double* ys = sYs + row * TW_LD + 2 * t4;
+    double* xr = x + (int64_t)__ldg(S + row) * 32 + 2 * t4;
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+      *reinterpret_cast<double2*>(xr + 8 * y) = make_double2(ys[8 * y] - acc[y][0], ys[8 * y + 1] - acc[y][1]);
+  });
+}
+
 __global__ void __launch_bounds__(NT) k_apply_skel(ApplySkelArgs a, double* x, int k, int up) {
   extern __shared__ double smem[];
   const int t = a.list ? a.list[blockIdx.x] : blockIdx.x;
@@ -3393,6 +3731,37 @@ __global__ void k_dot_part(const double* a, const double* b, int64_t N, int k, d
   double s = 0.0;
   for (int64_t r = (int64_t)blockIdx.x * lanes + row0; r < N; r += (int64_t)gridDim.x * lanes)
     s += a[r * k + c] * b[r * k + c];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double t = 0.0;
+    for (int l = 0; l < lanes; ++l) t += sh[l * k + threadIdx.x];
+    part[(int64_t)blockIdx.x * k + threadIdx.x] = t;
+  }
+}
+
+// PCG update fused with the residual norm: x += alpha p ; r -= alpha q for active columns, and the
+// per-block partial sums of r.r in the layout (and summation order) of k_dot_part, so the fused
+// pass is bitwise identical to k_axpy, k_axpy, k_dot_part run one after the other
+__global__ void k_pcg_update(double* x, const double* p, double* r, const double* q, const double* alpha,
+                             const int* active, int64_t N, int k, double* part) {
+  extern __shared__ double sh[];
+  const int c = threadIdx.x % k;           // blockDim.x is a multiple of k
+  const int lanes = blockDim.x / k;
+  const int row0 = threadIdx.x / k;
+  const bool on = active[c] != 0;
+  const double al = alpha[c];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * lanes + row0; i < N; i += (int64_t)gridDim.x * lanes) {
+    const int64_t e = i * k + c;
+    double rv = r[e];
+    if (on) {
+      x[e] += 1.0 * al * p[e];
+      rv += -1.0 * al * q[e];
+      r[e] = rv;
+    }
+    s += rv * rv;
+  }
   sh[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x < k) {
@@ -3863,7 +4232,8 @@ void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s) {
   if (a.ntgt == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  k_schur<<<a.ntgt, NT, 0, s>>>(lv, a);
+  const int ny = std::max(1, std::min(64, (148 * 8 + a.ntgt - 1) / a.ntgt));   // row split for few targets
+  k_schur<<<dim3(a.ntgt, ny), NT, 0, s>>>(lv, a);
 }
 void launch_prec_build(const LevelDev& lv, const PrecArgs& a, const int* list, int nbig, cudaStream_t s) {
   if (!nbig) return;
@@ -4080,17 +4450,36 @@ void launch_big_wide(const BigArgs& a, int mode, cudaStream_t s) {
   if (mode == 0) k_big_wide<0><<<a.nwork, NT, W_SMEM, s>>>(a);
   else k_big_wide<1><<<a.nwork, NT, W_SMEM, s>>>(a);
 }
-void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s) {
+void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s,
+                  int kmean) {
   if (!nwork) return;
   if (nrhs > 32) {
     launch_bgemm(desc, w_desc, w_tile, nwork, s);
     return;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const int grid = std::min(nwork, 148 * 16);
-  if (nrhs <= 8) k_rgemm<1><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
-  else if (nrhs <= 16) k_rgemm<2><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
-  else k_rgemm<4><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+  // persistent CTAs, each streaming its items through the cross-item pipeline; the grid is a
+  // multiple (PHIF_RG_WAVES) of the resident CTA count so the static striding balances
+  static const int waves = [] {
+    const char* e = getenv("PHIF_RG_WAVES");
+    return e ? std::max(1, atoi(e)) : 2;
+  }();
+  static const int deep_at = [] {
+    const char* e = getenv("PHIF_RG_DEEP");
+    return e ? atoi(e) : 128;
+  }();
+  const bool deep = kmean >= deep_at;
+  if (deep) {
+    const int grid = std::min(nwork, 148 * 16);
+    if (nrhs <= 8) k_rgemm_deep<1><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+    else if (nrhs <= 16) k_rgemm_deep<2><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+    else k_rgemm_deep<4><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
+  } else {
+    const int grid = std::min(nwork, 148 * 3 * waves);
+    if (nrhs <= 8) k_rgemm<1, 32><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork, nrhs);
+    else if (nrhs <= 16) k_rgemm<2, 32><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork, nrhs);
+    else k_rgemm<4, 32><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork, nrhs);
+  }
 }
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s) {
   if (!nwork) return;
@@ -4141,9 +4530,26 @@ void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, co
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_reduce<<<nblk((int64_t)nd * k, 256), 256, 0, s>>>(dof, off, rows, wbuf, nd, x, k);
 }
+static bool apply_mma_enabled() {
+  static const bool on = !getenv("PHIF_NO_APPLY_MMA");
+  return on;
+}
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s) {
   if (a.r == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (k == 32 && apply_mma_enabled()) {   // warp-level DMMA replay, rows staged in shared memory
+    const int ldn = ((a.ldn > 0 ? a.ldn : 96) + 3) & ~3;
+    const size_t per_warp = (size_t)ldn * TW_LD * sizeof(double);
+    const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (48 * 1024) / per_warp));
+    const size_t bytes = per_warp * wpc;
+    static size_t set_bytes = 0;
+    if (bytes > 48 * 1024 && bytes > set_bytes) {
+      cudaFuncSetAttribute(k_apply_prec_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      set_bytes = bytes;
+    }
+    k_apply_prec_mma<<<(a.r + wpc - 1) / wpc, 32 * wpc, bytes, s>>>(a, x, up ? 1 : 0, ldn);
+    return;
+  }
   const int ldn = k <= 4 ? (a.ldn > 0 ? a.ldn : 96) : 0;   // shared-memory staging only for few RHS
   const size_t per_warp = (size_t)ldn * k * sizeof(double);
   const int wpc = ldn ? (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp)) : 8;
@@ -4174,6 +4580,19 @@ void launch_apply_skel_warp(const ApplySkelArgs& a, const int* list, int n, doub
                             cudaStream_t s) {
   if (n == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (k == 32 && apply_mma_enabled()) {
+    const int ld = ldrows + 12;   // r, k~, k~ rows each padded to a multiple of 4
+    const size_t per_warp = (size_t)ld * TW_LD * sizeof(double);
+    const int wpc = (int)std::max<size_t>(1, std::min<size_t>(4, (64 * 1024) / per_warp));
+    const size_t bytes = per_warp * wpc;
+    static size_t set_bytes = 0;
+    if (bytes > 48 * 1024 && bytes > set_bytes) {
+      cudaFuncSetAttribute(k_apply_skel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      set_bytes = bytes;
+    }
+    k_apply_skel_mma<<<(n + wpc - 1) / wpc, 32 * wpc, bytes, s>>>(a, list, n, x, up ? 1 : 0, ld);
+    return;
+  }
   const size_t per_warp = (size_t)ldrows * k * sizeof(double);
   int wpc = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
   const size_t bytes = per_warp * wpc;
@@ -4202,6 +4621,15 @@ void launch_dot(const double* a, const double* b, int64_t N, int k, double* part
   k_dot_part<<<blocks, threads, threads * sizeof(double), s>>>(a, b, N, k, part);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_dot_final<<<1, 32 * ((k + 31) / 32), 0, s>>>(part, blocks, k, out);
+}
+void launch_pcg_update(double* x, const double* p, double* r, const double* q, const double* alpha, const int* active,
+                       int64_t N, int k, double* part, double* rn2, cudaStream_t s) {
+  const int threads = (256 / k) * k;
+  const int blocks = dot_part_blocks();
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_pcg_update<<<blocks, threads, threads * sizeof(double), s>>>(x, p, r, q, alpha, active, N, k, part);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  k_dot_final<<<1, 32 * ((k + 31) / 32), 0, s>>>(part, blocks, k, rn2);
 }
 void launch_axpy(double* y, const double* x, const double* coef, double sgn, const int* active, int64_t N, int k,
                  cudaStream_t s) {

@@ -95,7 +95,9 @@ void launch_band_check(const int64_t* rowptr, const int* col, const int* gid, co
 void launch_big_zero_upper(const BigArgs& a, cudaStream_t s);   // 0: trailing update, 1: U = X^T X
 void launch_bgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, cudaStream_t s);
 // replay GEMM (N = nrhs <= 32, A streamed from global, B chunk in shared memory); falls back to launch_bgemm
-void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s);
+// kmean: mean K depth per work item of this launch (picks the chunk depth of the kernel)
+void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, int nwork, int nrhs, cudaStream_t s,
+                  int kmean = 0);
 void launch_rows(double* Y, double* x, const int* idx, const int64_t* seg_src, const int64_t* seg_dst,
                  const int* seg_len, int nseg, int k, bool to_x, cudaStream_t s);
 void launch_skel_update(const LevelDev& lv, const SkelArgs& a, const int* list, int count, DevStatus* st,
@@ -119,6 +121,8 @@ void launch_spmv(const int64_t* rowptr, const int* col, const double* val, const
                  int k, cudaStream_t s);
 int dot_part_blocks();
 void launch_dot(const double* a, const double* b, int64_t N, int k, double* part, double* out, cudaStream_t s);
+void launch_pcg_update(double* x, const double* p, double* r, const double* q, const double* alpha, const int* active,
+                       int64_t N, int k, double* part, double* rn2, cudaStream_t s);
 void launch_axpy(double* y, const double* x, const double* coef, double sgn, const int* active, int64_t N, int k,
                  cudaStream_t s);
 void launch_xpby(double* p, const double* z, const double* coef, const int* active, int64_t N, int k,

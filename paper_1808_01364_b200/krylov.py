@@ -42,7 +42,7 @@ def pcg(A, b, precond: Factorization | None = None, tol: float = 1e-12, maxit: i
     flat = B.ndim == 1
     B = np.ascontiguousarray(B.reshape(B.shape[0], -1))
     k = B.shape[1]
-    X = np.zeros_like(B)
+    X = np.empty_like(B)   # phif_pcg overwrites every entry
     iters = np.zeros(k, dtype=np.int32)
     relres = np.zeros(k, dtype=np.float64)
     conv = np.zeros(k, dtype=np.int32)
