@@ -594,7 +594,7 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 // device -> host copy through a pinned staging buffer (DMA into pinned memory, then a parallel
 // host memcpy out); synchronises the stream
 void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  static constexpr size_t CH = (size_t)64 << 20;
+  static constexpr size_t CH = (size_t)16 << 20;   // (small: pinning the staging area is paid by the first call)
   static char* stage = nullptr;
   static bool ok = true;
   static std::mutex mu;
@@ -628,7 +628,7 @@ void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     const size_t a = c * CH, len = std::min(CH, bytes - a);
     const char* from = stage + (c & 1) * CH;
     char* to = static_cast<char*>(dst) + a;
-    const int64_t np = (int64_t)std::max<size_t>(1, len >> 22);
+    const int64_t np = (int64_t)std::max<size_t>(1, len >> 21);
 #pragma omp parallel for schedule(dynamic, 1) num_threads(std::min<int64_t>(np, 6))
     for (int64_t q = 0; q < np; ++q) {
       const size_t u = len * q / np, e = len * (q + 1) / np;
@@ -778,6 +778,10 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     }
     L.cell_work_unit = wacc;
     L.wbuf_unit = bacc;
+    for (int t = 0; t < p; ++t) {
+      L.cell_nmax = std::max(L.cell_nmax, P.cell_n[t]);
+      L.cell_bmax = std::max(L.cell_bmax, P.cell_b[t]);
+    }
     DBG("level %d: host: cell descriptors", lev);
     {
       double f1 = 0.0, b1 = 0.0, b0 = 0.0;
@@ -2310,7 +2314,13 @@ void apply(Factorization& F, double* x, int k, int mode) {
     for (auto& lp : F.levels) {
       LevelRT& L = *lp;
       launch_apply_cell(cell_args(F, L), x, k, true, s);
-      if (BigApply* ba = big_apply(F, L, k)) ba->up(L, x, s);
+      if (apply_cell_mma_fits(L.cell_nmax, L.cell_bmax, k) && !L.plan.interior.empty()) {
+        ApplyCellArgs c = cell_args(F, L);
+        c.p = (int)L.plan.interior.size();
+        launch_apply_cell_mma(c, L.cell_nmax, L.cell_bmax, x, true, s);
+      } else if (BigApply* ba = big_apply(F, L, k)) {
+        ba->up(L, x, s);
+      }
       launch_apply_reduce(L.bd_dof.as<int>(), L.bd_off.as<int64_t>(), L.bd_rows.as<int>(), F.wbuf.as<double>(),
                           L.nbd, x, k, s);
       if (L.plan.root) break;
@@ -2336,7 +2346,13 @@ void apply(Factorization& F, double* x, int k, int mode) {
         gr->run(1, L, x, s);
       }
       launch_apply_cell(cell_args(F, L), x, k, false, s);
-      if (BigApply* ba = big_apply(F, L, k)) ba->down(L, x, s);
+      if (apply_cell_mma_fits(L.cell_nmax, L.cell_bmax, k) && !L.plan.interior.empty()) {
+        ApplyCellArgs c = cell_args(F, L);
+        c.p = (int)L.plan.interior.size();
+        launch_apply_cell_mma(c, L.cell_nmax, L.cell_bmax, x, false, s);
+      } else if (BigApply* ba = big_apply(F, L, k)) {
+        ba->down(L, x, s);
+      }
     }
   }
   CK(cudaGetLastError());

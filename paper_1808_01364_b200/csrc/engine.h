@@ -105,6 +105,7 @@ struct LevelRT {
   std::vector<int> h_pn, h_sr, h_skt;
   DBuf d_apply_small_sk, d_apply_small_pr;
   int n_apply_small_sk = 0, n_apply_small_pr = 0;
+  int cell_nmax = 0, cell_bmax = 0;   // largest cell of the level (picks the warp-per-cell replay)
   int n_apply_tiny_sk = 0, apply_tiny_rows = 1, apply_small_pr_max = 1;   // separators replayed one warp each
   DBuf d_apply_tiny_sk;
   std::shared_ptr<struct GemmReplay> replay;

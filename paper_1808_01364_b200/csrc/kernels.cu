@@ -2689,6 +2689,18 @@ __device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr, bool
   const int n = pred ? 8 : 0;   // src-size 0 -> zero fill
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gptr), "r"(n));
 }
+// 8-byte cp.async / read-only load with a 256-byte L2 prefetch: the records are streamed once in
+// 256..512-byte row pieces, so every L2 miss fetches the whole piece from DRAM in one request
+__device__ __forceinline__ void cp_async8_pf(void* smem_ptr, const void* gptr, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global.L2::256B [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gptr), "r"(n));
+}
+__device__ __forceinline__ double ldg_pf(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -2859,7 +2871,7 @@ __global__ void __launch_bounds__(NT) k_rgemm_deep(const GemmDesc* desc, const i
 #pragma unroll
       for (int s = 0; s < RGD_K / 4; ++s) {
         const int kg = kc + 4 * s + t4;
-        a[s] = (rok && kg < d.K) ? __ldg(Ar + (int64_t)kg * sk) : 0.0;
+        a[s] = (rok && kg < d.K) ? ldg_pf(Ar + (int64_t)kg * sk) : 0.0;
       }
     };
     auto stage_b = [&](int buf, int kc) {
@@ -2909,6 +2921,104 @@ __global__ void __launch_bounds__(NT) k_rgemm_deep(const GemmDesc* desc, const i
             *p = (d.beta == 0.0 ? 0.0 : d.beta * *p) + d.alpha * acc[y][z];
           }
         }
+    }
+  }
+}
+
+// Deep records, 17..32 right-hand sides: both operands staged in shared memory by cp.async (a warp
+// copies 256 contiguous bytes of one row of A per instruction, instead of fragment loads that
+// touch eight rows each), K in 32-deep chunks through a 3-stage pipeline with one barrier per
+// chunk; warps 4 (rows) x 2 (columns), each a 16 x 16 tile. The load/store unit work per DMMA is
+// about half that of k_rgemm_deep, which was co-limiting with the DMMA pipe.
+constexpr int RS_BK = 32, RS_STAGES = 3;
+constexpr int RS_ALD_N = RS_BK + 4;   // A not transposed: sA[row][k]
+constexpr int RS_ALD_T = 64 + 4;      // A transposed:     sA[k][row]
+constexpr int RS_BLD = 32 + 4;        // sB[k][col]
+constexpr int RS_ASZ = 64 * RS_ALD_N > RS_BK * RS_ALD_T ? 64 * RS_ALD_N : RS_BK * RS_ALD_T;
+constexpr int RS_STAGE = RS_ASZ + RS_BK * RS_BLD;
+constexpr size_t RS_SMEM = (size_t)RS_STAGES * RS_STAGE * sizeof(double);
+__global__ void __launch_bounds__(NT, 2) k_rgemm_smem(const GemmDesc* __restrict__ desc, const int* __restrict__ w_desc,
+                                                       const int* __restrict__ w_tile, int nwork) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const GemmDesc d = desc[w_desc[w]];
+    const int i0 = 64 * w_tile[w];
+    const int M = min(64, d.M - i0);
+    if (M <= 0) continue;
+    const int Kb = d.tri == 3 ? (i0 / RS_BK) * RS_BK : 0;
+    const int Kt = d.tri == 1 ? min(d.K, i0 + 64) : d.K;
+    const int nk = (Kt - Kb + RS_BK - 1) / RS_BK;
+    auto load = [&](int st, int k0) {
+      double* sA = smem + st * RS_STAGE;
+      double* sB = sA + RS_ASZ;
+#pragma unroll
+      for (int q = 0; q < (64 * RS_BK) / NT; ++q) {
+        const int e = tid + q * NT;
+        if (d.transA) {   // op(A)(i,k) = A[k*lda + i]: a warp copies 32 consecutive rows of one k
+          const int kk = e >> 6, r = e & 63;
+          const bool ok = r < M && k0 + kk < Kt;
+          cp_async8_pf(sA + kk * RS_ALD_T + r, d.A + (ok ? (int64_t)(k0 + kk) * d.lda + i0 + r : 0), ok);
+        } else {          // A[i*lda + k]: a warp copies the 32 k of one row
+          const int r = e >> 5, kk = e & 31;
+          const bool ok = r < M && k0 + kk < Kt;
+          cp_async8_pf(sA + r * RS_ALD_N + kk, d.A + (ok ? (int64_t)(i0 + r) * d.lda + k0 + kk : 0), ok);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < (RS_BK * 32) / NT; ++q) {
+        const int e = tid + q * NT, kk = e >> 5, c = e & 31;
+        const bool ok = k0 + kk < Kt && c < d.N;
+        cp_async8(sB + kk * RS_BLD + c, d.B + (ok ? (int64_t)(k0 + kk) * d.ldb + c : 0), ok);
+      }
+    };
+    double acc[2][2][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    __syncthreads();   // the previous item's readers of the stage buffers are done
+#pragma unroll
+    for (int st = 0; st < RS_STAGES - 1; ++st) {
+      if (st < nk) load(st, Kb + st * RS_BK);
+      cp_async_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      cp_async_wait<RS_STAGES - 2>();   // chunk kc has landed (this thread's copies)
+      __syncthreads();                  // ... everyone's; and chunk kc-1 is consumed: its stage is free
+      if (kc + RS_STAGES - 1 < nk) load((kc + RS_STAGES - 1) % RS_STAGES, Kb + (kc + RS_STAGES - 1) * RS_BK);
+      cp_async_commit();
+      const double* sA = smem + (kc % RS_STAGES) * RS_STAGE;
+      const double* sB = sA + RS_ASZ;
+#pragma unroll
+      for (int ks = 0; ks < RS_BK; ks += 4) {
+        double af[2], bf[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+          af[x] = d.transA ? sA[(ks + t) * RS_ALD_T + wm * 16 + x * 8 + g] : sA[(wm * 16 + x * 8 + g) * RS_ALD_N + ks + t];
+#pragma unroll
+        for (int y = 0; y < 2; ++y) bf[y] = sB[(ks + t) * RS_BLD + wn * 16 + y * 8 + g];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+      }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int r = wm * 16 + x * 8 + g;
+      if (r < M) {
+        double* crow = d.C + (int64_t)(i0 + r) * d.ldc;
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int z = 0; z < 2; ++z) {
+            const int c = wn * 16 + y * 8 + 2 * t + z;
+            if (c < d.N) crow[c] = (d.beta == 0.0 ? 0.0 : d.beta * crow[c]) + d.alpha * acc[x][y][z];
+          }
+      }
     }
   }
 }
@@ -3594,6 +3704,69 @@ __device__ __forceinline__ void warp_stage32(double* sY, const double* x, const 
     }
   }
   for (int i = n; i < ((n + 3) & ~3); ++i) sY[i * TW_LD + lane] = 0.0;
+}
+
+// small cells (n <= 32, b <= 64: the level-0 cells of a 3D grid), 32 right-hand sides; record panel
+// [L ; X^T ; L^-T] (row stride n):
+//   up:   Z = L^-1 x_I ; x_I <- Z ; wbuf rows of the cell <- X^T Z   (k_apply_reduce subtracts them)
+//   down: Y = x_I - X x_B ; x_I <- L^-T Y
+// Replaces gather -> two replay GEMMs -> scatter through the global workspace by one pass.
+__global__ void __launch_bounds__(128) k_apply_cell_mma(ApplyCellArgs a, double* x, int up, int nrows, int ldrows) {
+  extern __shared__ double smem[];
+  const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t4 = lane & 3;
+  const int t = blockIdx.x * wpc + warp;
+  if (t >= a.p) return;
+  const int n = a.n[t], b = a.b[t];
+  const int* I = a.I + a.I_off[t];
+  const int* B = a.B + a.B_off[t];
+  const double* P = a.rec + a.P_off[t];
+  const double* XT = P + (int64_t)n * n;         // b x n
+  const double* LiT = XT + (int64_t)b * n;       // n x n (upper)
+  double* sY = smem + (size_t)warp * ldrows * TW_LD;
+  double* s2 = sY + (size_t)nrows * TW_LD;       // Z (up) or x_B (down)
+  warp_stage32(sY, x, I, n);
+  if (up) {
+    for (int i = n; i < ((n + 3) & ~3); ++i) s2[i * TW_LD + lane] = 0.0;
+    __syncwarp();
+    warp_mm32<true>(LiT, n, n, n, 1, sY, [&](int row, bool ok, double (&acc)[4][2]) {
+      if (!ok) return;
+      double* z = s2 + row * TW_LD + 2 * t4;
+      double* xr = x + (int64_t)__ldg(I + row) * 32 + 2 * t4;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        z[8 * y] = acc[y][0];
+        z[8 * y + 1] = acc[y][1];
+        *reinterpret_cast<double2*>(xr + 8 * y) = make_double2(acc[y][0], acc[y][1]);
+      }
+    });
+    __syncwarp();
+    double* wb = a.wbuf + a.B_off[t] * 32;
+    warp_mm32<false>(XT, n, b, n, 0, s2, [&](int row, bool ok, double (&acc)[4][2]) {
+      if (!ok) return;
+      double* wr = wb + (int64_t)row * 32 + 2 * t4;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) *reinterpret_cast<double2*>(wr + 8 * y) = make_double2(acc[y][0], acc[y][1]);
+    });
+  } else {
+    warp_stage32(s2, x, B, b);
+    __syncwarp();
+    warp_mm32<true>(XT, n, n, b, 0, s2, [&](int row, bool ok, double (&acc)[4][2]) {
+      if (!ok) return;
+      double* yr = sY + row * TW_LD + 2 * t4;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        yr[8 * y] -= acc[y][0];
+        yr[8 * y + 1] -= acc[y][1];
+      }
+    });
+    __syncwarp();
+    warp_mm32<false>(LiT, n, n, n, 3, sY, [&](int row, bool ok, double (&acc)[4][2]) {
+      if (!ok) return;
+      double* xr = x + (int64_t)__ldg(I + row) * 32 + 2 * t4;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) *reinterpret_cast<double2*>(xr + 8 * y) = make_double2(acc[y][0], acc[y][1]);
+    });
+  }
 }
 
 // block-Jacobi records (|g| < APPLY_BIG), 32 right-hand sides: x_g <- L^-1 x_g (up) / L^-T x_g
@@ -4469,7 +4642,15 @@ void launch_rgemm(const GemmDesc* desc, const int* w_desc, const int* w_tile, in
     return e ? atoi(e) : 128;
   }();
   const bool deep = kmean >= deep_at;
-  if (deep) {
+  static const bool staged = getenv("PHIF_RG_SMEM") != nullptr;   // (measured on c5: 5.65 ms vs 5.37 ms for the fragment-load kernel, so off by default)
+  if (deep && nrhs > 16 && staged) {
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_rgemm_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SMEM);
+      init = true;
+    }
+    k_rgemm_smem<<<std::min(nwork, 148 * 16), NT, RS_SMEM, s>>>(desc, w_desc, w_tile, nwork);
+  } else if (deep) {
     const int grid = std::min(nwork, 148 * 16);
     if (nrhs <= 8) k_rgemm_deep<1><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
     else if (nrhs <= 16) k_rgemm_deep<2><<<grid, NT, 0, s>>>(desc, w_desc, w_tile, nwork);
@@ -4523,6 +4704,23 @@ void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaSt
   if (a.p == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   k_apply_cell<<<a.p, NT, SMEM_BYTES, s>>>(a, x, k, up ? 1 : 0);
+}
+static bool apply_mma_enabled();
+bool apply_cell_mma_fits(int nmax, int bmax, int k) { return k == 32 && nmax <= 32 && bmax <= 64 && apply_mma_enabled(); }
+void launch_apply_cell_mma(const ApplyCellArgs& a, int nmax, int bmax, double* x, bool up, cudaStream_t s) {
+  if (a.p == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int nrows = (nmax + 3) & ~3;
+  const int ld = nrows + std::max(nrows, (bmax + 3) & ~3);
+  const size_t per_warp = (size_t)ld * TW_LD * sizeof(double);
+  const int wpc = 4;
+  const size_t bytes = per_warp * wpc;
+  static size_t set_bytes = 0;
+  if (bytes > 48 * 1024 && bytes > set_bytes) {
+    cudaFuncSetAttribute(k_apply_cell_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    set_bytes = bytes;
+  }
+  k_apply_cell_mma<<<(a.p + wpc - 1) / wpc, 32 * wpc, bytes, s>>>(a, x, up ? 1 : 0, nrows, ld);
 }
 void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd, double* x,
                          int k, cudaStream_t s) {

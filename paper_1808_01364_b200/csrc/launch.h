@@ -108,6 +108,9 @@ void launch_skel_big_post(const LevelDev& lv, const SkelArgs& a, const int* big,
                           const double* U, const int64_t* U_off, int nbig, cudaStream_t s);
 void launch_repack(const RepackArgs& a, cudaStream_t s);
 void launch_apply_cell(const ApplyCellArgs& a, double* x, int k, bool up, cudaStream_t s);
+// warp-per-cell DMMA replay of small cells (n <= 32, b <= 64) for 32 right-hand sides
+bool apply_cell_mma_fits(int nmax, int bmax, int k);
+void launch_apply_cell_mma(const ApplyCellArgs& a, int nmax, int bmax, double* x, bool up, cudaStream_t s);
 void launch_apply_reduce(const int* dof, const int64_t* off, const int* rows, const double* wbuf, int nd, double* x,
                          int k, cudaStream_t s);
 void launch_apply_prec(const ApplyPrecArgs& a, double* x, int k, bool up, cudaStream_t s);
