@@ -1021,19 +1021,18 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
     if (!big_cells.empty() && !banded)
       bp.build(big_cells, P.cell_n, P.cell_b, L.rec.as<double>(), P_off, U.as<double>(), U_off, s);
     DBG("level %d: big plan built (%lld work items)", lev, (long long)bp.nwork_total);
+    if (!big_cells.empty()) upload(bp.d_list, big_cells, s);
     if (timing) CK(cudaEventRecord(ev[2], s));
     if (!small_cells.empty()) {
       ca.list = L.d_small_cells.as<int>();
       launch_cell(dv, ca, (int)small_cells.size(), F->status.as<DevStatus>(), s);
     }
     if (banded) {
-      upload(bp.d_list, big_cells, s);
       DBuf scratch;   // band of L + reciprocals per cell, from the one-warp Cholesky
       scratch.alloc((size_t)big_cells.size() * band_scratch_stride(band_nmax, band_w) * sizeof(double), s);
       launch_cell_band(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), band_nmax, band_bmax, band_w,
                        scratch.as<double>(), F->status.as<DevStatus>(), gid_prof_buffer(), s);
     } else if (!big_cells.empty()) {
-      upload(bp.d_list, big_cells, s);
       launch_big_build(dv, ca, bp.d_list.as<int>(), (int)big_cells.size(), s);
       bp.run(F->status.as<DevStatus>(), s);
     }

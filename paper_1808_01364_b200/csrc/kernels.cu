@@ -195,23 +195,24 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
   BAND_MARK(24)
   BAND_MARK(25)
   if (s_bad >= 0) return;   // (NotSpd: reported by k_band_chol; the factorization stops)
-  // L rows of the record (dense, zeros outside the band)
-  for (int i = warp; i < n; i += NT / 32)   // row i: lanes along columns (no 64-bit division)
-    for (int c = lane; c < n; c += 32) {
-      const int d = i - c;
-      P[(int64_t)i * n + c] = (d >= 0 && d <= w) ? Lb[i * W1 + d] : 0.0;
-    }
   // X = L^-1 A_BI^T (one boundary DOF per thread) and L^-T (row j = L^-1 e_j, one identity column
   // per thread): substitutions in lockstep over 16-row chunks; each warp stages its 32 x 16 chunk
   // in shared memory and writes it out as 16-double row segments (coalesced), zeros included
   double* stg = Xs + (int64_t)warp * 32 * 17;
   auto solve_rows = [&](bool active, const double* S, int wn, int rc, int rhs_one, double* row0, int nrows_warp,
-                        int64_t row_base) {
+                        int64_t row_base, int zero_until) {
     double h[WM];
 #pragma unroll
     for (int q = 0; q < WM; ++q) h[q] = 0.0;
     for (int i0 = 0; i0 < n; i0 += 16) {
       const int cnt = min(16, n - i0);
+      if (i0 + 16 <= zero_until) {   // every right-hand side of the warp is still zero here: no chain
+        for (int e = lane; e < 32 * 16; e += 32) {
+          const int rr = e >> 4, u = e & 15;
+          if (rr < nrows_warp && u < cnt) row0[(row_base + rr) * n + i0 + u] = 0.0;
+        }
+        continue;
+      }
       double a[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u)
@@ -243,8 +244,10 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
     }
   };
   (void)solve_rows;
-  __syncthreads();
-  BAND_MARK(26)
+  // The three record parts only depend on the band of L: no CTA barrier between them. The warps
+  // holding boundary DOFs solve X first (U waits for it), the others go straight to the L rows and
+  // L^-T; a warp's L^-T columns j >= 32*warp are zero above row j, so those chunks are plain zero
+  // stores.
   if (warp * 32 < b) {   // X^T rows n + r
     const int r = tid;
     const bool act = r < b;
@@ -257,39 +260,47 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
       rc = r - ca.nbr_col[jn];
       S = lv.pool + lv.boff[ca.nbr_blk[jn]];   // block (I, h): |I| x wn row-major
     }
-    solve_rows(act, act ? S : Lb, wn, rc, -1, P, min(32, b - warp * 32), (int64_t)n + warp * 32);
+    solve_rows(act, act ? S : Lb, wn, rc, -1, P, min(32, b - warp * 32), (int64_t)n + warp * 32, 0);
   }
-  __syncthreads();   // (the staging area is reused)
   BAND_MARK(27)
+  // L rows of the record (dense, zeros outside the band)
+  for (int i = warp; i < n; i += NT / 32)   // row i: lanes along columns (no 64-bit division)
+    for (int c = lane; c < n; c += 32) {
+      const int d = i - c;
+      P[(int64_t)i * n + c] = (d >= 0 && d <= w) ? Lb[i * W1 + d] : 0.0;
+    }
+  BAND_MARK(26)
   if (warp * 32 < n) {   // L^-T rows n + b + j
     const int j = tid;
-    solve_rows(j < n, nullptr, 1, 0, j, P, min(32, n - warp * 32), (int64_t)n + b + warp * 32);
+    solve_rows(j < n, nullptr, 1, 0, j, P, min(32, n - warp * 32), (int64_t)n + b + warp * 32, warp * 32);
   }
   __syncthreads();   // X^T rows written (global, read back through L2 below)
   BAND_MARK(28)
-  // U = X^T X (b x b): 64-column chunks of X^T in shared memory, a 4 x 4 output block per thread
+  // U = X^T X (b x b): 64-column chunks of X^T in shared memory (row stride 65: a half-warp's 16
+  // rows tj + 16 y fall in 16 different banks), a 4 x 4 interleaved output block per thread
   if (b > 0) {
+    constexpr int XLD = 65;
     double acc[4][4];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-    const int ti = tid / 16, tj = tid % 16;   // rows 4ti.., columns 4tj.. (b <= 64)
+    const int ti = tid / 16, tj = tid % 16;   // rows ti + 16 x, columns tj + 16 y (b <= 64)
     for (int c0 = 0; c0 < n; c0 += 64) {
       const int cw = min(64, n - c0);
       __syncthreads();
       for (int e = tid; e < b * 64; e += NT) {
         const int r = e / 64, c = e % 64;
-        Xs[e] = c < cw ? __ldcg(P + (int64_t)(n + r) * n + c0 + c) : 0.0;
+        Xs[r * XLD + c] = c < cw ? __ldcg(P + (int64_t)(n + r) * n + c0 + c) : 0.0;
       }
       __syncthreads();
       for (int c = 0; c < cw; ++c) {
         double xa[4], xb[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          const int ra = 4 * ti + x, rb = 4 * tj + x;
-          xa[x] = ra < b ? Xs[ra * 64 + c] : 0.0;
-          xb[x] = rb < b ? Xs[rb * 64 + c] : 0.0;
+          const int ra = ti + 16 * x, rb = tj + 16 * x;
+          xa[x] = ra < b ? Xs[ra * XLD + c] : 0.0;
+          xb[x] = rb < b ? Xs[rb * XLD + c] : 0.0;
         }
 #pragma unroll
         for (int x = 0; x < 4; ++x)
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(NT) k_cell_band(LevelDev lv, CellArgs ca, cons
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) {
-        const int ra = 4 * ti + x, rb = 4 * tj + y;
+        const int ra = ti + 16 * x, rb = tj + 16 * y;
         if (ra < b && rb < b) U[(int64_t)ra * b + rb] = acc[x][y];
       }
   }
@@ -4561,7 +4572,7 @@ void launch_big_step(const BigArgs& diag, const BigArgs& trsm, const BigArgs& up
   launch_big_nt(upd, 0, s);
 }
 static size_t band_smem(int nmax, int bmax, int w) {
-  return ((size_t)nmax * (w + 1) + nmax + std::max<size_t>((size_t)bmax * 64, 8 * 32 * 17)) * sizeof(double);
+  return ((size_t)nmax * (w + 1) + nmax + std::max<size_t>((size_t)bmax * 65, 8 * 32 * 17)) * sizeof(double);
 }
 bool band_cells_fit(int nmax, int bmax, int w) {
   const size_t bytes = band_smem(nmax, bmax, w);
