@@ -402,7 +402,11 @@ int64_t sort_unique(DBuf& keys, int64_t n, int end_bit, DBuf& out, Temp& tmp, DB
 bool gpu_plan0_applicable(const Spec& s, int big_cell) {
   int64_t n = 1;
   for (int d = 0; d < s.dim; ++d) n *= (s.m - 1);
-  return n < big_cell;   // level-0 cells on the one-CTA path (no host work lists needed)
+  if (n < big_cell) return true;   // level-0 cells on the one-CTA path
+  // 2D cells on the banded (or tile-parallel) path: their host work lists come from the downloaded plan
+  // (PHIF_HOST_PLAN_2D=1 keeps the host planner for them)
+  static const bool host2d = getenv("PHIF_HOST_PLAN_2D") != nullptr;
+  return !host2d && s.dim == 2;
 }
 
 void plan_level0_device(const Spec& s, const int64_t* rowptr, const int* col, int64_t nnz, LevelPlan& lp,
