@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(256) k_prec_factor_warp(LevelDev lv, PrecArgs 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * 8 + warp;
   if (idx >= n) return;
-  const int ld = kmax + 1;
+  const int ld = (kmax + 1) | 1;   // odd row stride: lanes along rows fall in different banks
   double* D = smem + (size_t)warp * 2 * kmax * ld;
   double* X = D + (size_t)kmax * ld;
   const int t = list ? list[idx] : idx;   // (no list: every group)
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(256) k_prec_scale_warp(LevelDev lv, PrecArgs p
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = blockIdx.x * 8 + warp;
   if (idx >= n) return;
-  const int ld = ldmax + 1;
+  const int ld = (ldmax + 1) | 1;   // odd row stride: lanes along rows fall in different banks
   double* S = smem + (size_t)warp * ldmax * ld;
   const int blk = pa.scale_blk[list ? list[idx] : idx];   // (no list: every scaling block)
   const int g = lv.bg[blk], h = lv.bh[blk];
@@ -2578,7 +2578,10 @@ __global__ void k_big_zero_upper(BigArgs a, int chunks) {
     for (int j = r + 1 + (int)threadIdx.x; j < n; j += blockDim.x) P[(int64_t)r * n + j] = 0.0;
 }
 
-// acc += A (64 x 64) * B^T (64 x 64) on DMMA, both tiles row-major in smem (ld BLD)
+// acc += A (64 x 64) * B^T (64 x 64) on DMMA, both tiles row-major in smem, row stride TLD = 68
+// (TLD mod 16 == 4: the 16 lanes of a half-warp, rows g < 4 and k offsets t < 4, read 16 different
+// 8-byte banks; the stride 65 of the diagonal kernel gave 4-way conflicts on these fragments)
+constexpr int TLD = 68;
 __device__ __forceinline__ void tile_mma_nt(const double* sA, const double* sB, double acc[2][4][2]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
@@ -2586,9 +2589,9 @@ __device__ __forceinline__ void tile_mma_nt(const double* sA, const double* sB, 
   for (int ks = 0; ks < BT; ks += 4) {
     double af[2], bf[4];
 #pragma unroll
-    for (int x = 0; x < 2; ++x) af[x] = sA[(wm * 16 + x * 8 + g) * BLD + ks + t];
+    for (int x = 0; x < 2; ++x) af[x] = sA[(wm * 16 + x * 8 + g) * TLD + ks + t];
 #pragma unroll
-    for (int y = 0; y < 4; ++y) bf[y] = sB[(wn * 32 + y * 8 + g) * BLD + ks + t];
+    for (int y = 0; y < 4; ++y) bf[y] = sB[(wn * 32 + y * 8 + g) * TLD + ks + t];
 #pragma unroll
     for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -2600,7 +2603,7 @@ __device__ __forceinline__ void tile_mma_nt(const double* sA, const double* sB, 
 __global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
   extern __shared__ double smem[];
   double* sA = smem;
-  double* sB = smem + BT * BLD;
+  double* sB = smem + BT * TLD;
   const int c = a.w_cell[blockIdx.x], it = a.w_i[blockIdx.x];
   const int n = a.n[c], rows = a.rows[c], k0 = a.k0, kb = min(BT, n - k0);
   const int r0 = k0 + kb + BT * it;
@@ -2609,8 +2612,8 @@ __global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
   const int tid = threadIdx.x;
   for (int e = tid; e < BT * BT; e += NT) {
     const int i = e / BT, j = e % BT;
-    sA[i * BLD + j] = (r0 + i < rows && j < kb) ? P[(int64_t)(r0 + i) * n + k0 + j] : 0.0;
-    sB[i * BLD + j] = Li[e];
+    sA[i * TLD + j] = (r0 + i < rows && j < kb) ? P[(int64_t)(r0 + i) * n + k0 + j] : 0.0;
+    sB[i * TLD + j] = Li[e];
   }
   __syncthreads();
   double acc[2][4][2] = {};
@@ -4433,14 +4436,14 @@ void launch_prec_factor_warp(const LevelDev& lv, const PrecArgs& a, const int* l
                              cudaStream_t s) {
   if (n == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const size_t bytes = (size_t)8 * 2 * kmax * (kmax + 1) * sizeof(double);
+  const size_t bytes = (size_t)8 * 2 * kmax * ((kmax + 1) | 1) * sizeof(double);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_prec_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_prec_factor_warp<<<(n + 7) / 8, 256, bytes, s>>>(lv, a, list, n, kmax, st);
 }
 void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int ldmax, cudaStream_t s) {
   if (n == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  const size_t bytes = (size_t)8 * ldmax * (ldmax + 1) * sizeof(double);
+  const size_t bytes = (size_t)8 * ldmax * ((ldmax + 1) | 1) * sizeof(double);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_prec_scale_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_prec_scale_warp<<<(n + 7) / 8, 256, bytes, s>>>(lv, a, list, n, ldmax);
 }
@@ -4553,7 +4556,7 @@ int team_max_clusters(int vcap, int kmax, int colcap, int csize) {
   }
   return n;
 }
-static constexpr size_t BIG_SMEM = 2 * BT * BLD * sizeof(double);
+static constexpr size_t BIG_SMEM = 2 * BT * TLD * sizeof(double);
 void launch_big_build(const LevelDev& lv, const CellArgs& ca, const int* big_cells, int nbig, cudaStream_t s) {
   if (!nbig) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
