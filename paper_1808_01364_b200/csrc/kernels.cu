@@ -2599,6 +2599,10 @@ __device__ __forceinline__ void tile_mma_nt(const double* sA, const double* sB, 
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr, bool pred);
+__device__ __forceinline__ void cp_async_commit();
+template <int N>
+__device__ __forceinline__ void cp_async_wait();
 // panel rows below the diagonal block: X = P[rows, k0:k0+64] * Linv^T (in place)
 __global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
   extern __shared__ double smem[];
@@ -2610,11 +2614,17 @@ __global__ void __launch_bounds__(NT) k_big_trsm(BigArgs a) {
   double* P = a.P[c];
   const double* Li = a.Linv + (int64_t)c * BT * BT;
   const int tid = threadIdx.x;
+  // both tiles by cp.async: the 32 copies of a thread are all in flight together (the plain
+  // load -> store loop exposed the global latency several times per CTA)
+#pragma unroll 4
   for (int e = tid; e < BT * BT; e += NT) {
     const int i = e / BT, j = e % BT;
-    sA[i * TLD + j] = (r0 + i < rows && j < kb) ? P[(int64_t)(r0 + i) * n + k0 + j] : 0.0;
-    sB[i * TLD + j] = Li[e];
+    const bool ok = r0 + i < rows && j < kb;
+    cp_async8(sA + i * TLD + j, P + (ok ? (int64_t)(r0 + i) * n + k0 + j : 0), ok);   // (zero fill)
+    cp_async8(sB + i * TLD + j, Li + e, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   double acc[2][4][2] = {};
   tile_mma_nt(sA, sB, acc);
