@@ -3919,6 +3919,20 @@ __global__ void k_spmv(const int64_t* rowptr, const int* col, const double* val,
   y[e] = s;
 }
 
+// 32 right-hand sides: one warp per row, lane = right-hand side (no index division; the row's
+// entries are warp-wide broadcasts, the x rows coalesced 256-byte reads). Same FMA order as k_spmv.
+__global__ void __launch_bounds__(256) k_spmv32(const int64_t* __restrict__ rowptr, const int* __restrict__ col,
+                                                const double* __restrict__ val, const double* x,
+                                                double* y, int64_t N) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= N) return;
+  const int64_t q0 = __ldg(rowptr + r), q1 = __ldg(rowptr + r + 1);
+  double s = 0.0;
+  for (int64_t q = q0; q < q1; ++q) s = __fma_rn(__ldg(val + q), x[(int64_t)__ldg(col + q) * 32 + lane], s);
+  y[r * 32 + lane] = s;
+}
+
 // per-block partial column dot products: part[blk*k + c] = sum over the block's rows
 __global__ void k_dot_part(const double* a, const double* b, int64_t N, int k, double* part) {
   extern __shared__ double sh[];
@@ -4833,6 +4847,10 @@ void launch_apply_skel(const ApplySkelArgs& a, double* x, int k, bool up, cudaSt
 void launch_spmv(const int64_t* rowptr, const int* col, const double* val, const double* x, double* y, int64_t N,
                  int k, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (k == 32) {
+    k_spmv32<<<nblk(N * 32, 256), 256, 0, s>>>(rowptr, col, val, x, y, N);
+    return;
+  }
   k_spmv<<<nblk(N * k, 256), 256, 0, s>>>(rowptr, col, val, x, y, N, k);
 }
 int dot_part_blocks() { return 592; }
