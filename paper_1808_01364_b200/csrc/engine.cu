@@ -1180,6 +1180,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       std::vector<int> w1d, w1t, w2d, w2t;
       int64_t tmp_need = 0;
       int stiny_max = 1;
+      bool ssmall_gemm = true;   // every mid-size block fits the two-GEMM kernel
       if (all_tiny) stiny_max = tiny_max;   // (every scaled block couples two tiny groups)
       for (size_t q = 0; q < P.scale_blk.size() && !all_tiny; ++q) {
         const int b = P.scale_blk[q];
@@ -1189,6 +1190,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
           stiny_max = std::max(stiny_max, std::max(kg, kh));
         } else if (std::max(kg, kh) < BIG_PREC) {
           ssmall.push_back((int)q);
+          ssmall_gemm = ssmall_gemm && kg * kh <= 64 * 64;
         } else {
           tmp_need += (int64_t)kg * kh;
         }
@@ -1197,7 +1199,7 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       PrecArgs pss = pa;
       pss.scale_list = L.d_scale_small.as<int>();
       pss.nscale = (int)ssmall.size();
-      launch_prec_scale(dv, pss, s);
+      launch_prec_scale(dv, pss, s, ssmall_gemm);
       DBuf dstiny;
       if (!all_tiny) upload(dstiny, stiny, s);
       launch_prec_scale_warp(dv, pa, all_tiny ? nullptr : dstiny.as<int>(),

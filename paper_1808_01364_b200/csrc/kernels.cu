@@ -437,6 +437,23 @@ __global__ void __launch_bounds__(NT) k_prec_scale(LevelDev lv, PrecArgs pa) {
   cta_trsm_right_lt(Lh, kh, kh, B, kg, kh, smem);
 }
 
+// The two-GEMM form of k_prec_scale alone (|g| |h| <= PREC_SCALE_T), compiled for three CTAs per SM:
+// the stage is latency-bound (117 K blocks of <= 49 x 49 at c5 level 1), and the substitution
+// path of the general kernel held it at two CTAs per SM by registers.
+__global__ void __launch_bounds__(NT, 3) k_prec_scale_gemm(LevelDev lv, PrecArgs pa) {
+  extern __shared__ double smem[];
+  const int blk = pa.scale_list ? pa.scale_blk[pa.scale_list[blockIdx.x]] : pa.scale_blk[blockIdx.x];
+  const int g = lv.bg[blk], h = lv.bh[blk];
+  const int kg = lv.gsize[g], kh = lv.gsize[h];
+  double* B = lv.pool + lv.boff[blk];
+  const double* Lg = pa.rec + pa.L_off_of_group[g];
+  const double* Lh = pa.rec + pa.L_off_of_group[h];
+  double* T = smem + SMEM_DOUBLES;
+  double* gsm = smem + GEMM_OFF;
+  cta_gemm<true, false>(kg, kh, kg, 1.0, Lg + (int64_t)kg * kg, kg, B, kh, 0.0, T, kh, false, gsm);
+  cta_gemm<false, false>(kg, kh, kh, 1.0, T, kh, Lh + (int64_t)kh * kh, kh, 0.0, B, kh, false, gsm);
+}
+
 // Small block-Jacobi groups (k <= 32): one warp per group instead of one CTA. Same record
 // as k_prec_factor: [A_gg ; I] -> [L ; L^-T] (row-major, strict upper of L zero), A_gg <- I.
 // Cholesky right-looking in the warp's shared tile (lanes along rows); L^-1 by forward
@@ -4471,9 +4488,19 @@ void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* li
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_prec_scale_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_prec_scale_warp<<<(n + 7) / 8, 256, bytes, s>>>(lv, a, list, n, ldmax);
 }
-void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s) {
+void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s, bool gemm_only) {
   if (a.nscale == 0) return;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (gemm_only) {   // every block of the list has |g| |h| <= PREC_SCALE_T
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_prec_scale_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(SMEM_BYTES + PREC_SCALE_T * sizeof(double)));
+      init = true;
+    }
+    k_prec_scale_gemm<<<a.nscale, NT, SMEM_BYTES + PREC_SCALE_T * sizeof(double), s>>>(lv, a);
+    return;
+  }
   k_prec_scale<<<a.nscale, NT, SMEM_BYTES + PREC_SCALE_T * sizeof(double), s>>>(lv, a);
 }
 static long long static_smem(const void* fn) {

@@ -62,7 +62,8 @@ void launch_cell(const LevelDev& lv, const CellArgs& a, int count, DevStatus* st
 void launch_schur(const LevelDev& lv, const SchurArgs& a, cudaStream_t s);
 void launch_prec_build(const LevelDev& lv, const PrecArgs& a, const int* list, int nbig, cudaStream_t s);
 void launch_prec_factor(const LevelDev& lv, const PrecArgs& a, DevStatus* st, cudaStream_t s);
-void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s);
+// gemm_only: every block of the list fits the two-GEMM form (|g| |h| <= 64 x 64)
+void launch_prec_scale(const LevelDev& lv, const PrecArgs& a, cudaStream_t s, bool gemm_only = false);
 void launch_prec_factor_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int kmax, DevStatus* st,
                              cudaStream_t s);
 void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int ldmax, cudaStream_t s);
