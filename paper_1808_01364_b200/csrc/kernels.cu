@@ -69,7 +69,7 @@ __global__ void k_group_pos(LevelDev lv, int* gid, int* pos) {
 // Stage 1: cell elimination.
 // Panel P = [A_II ; A_BI] ((n+b) x n) -> partial Cholesky -> [L ; X^T]; U = X^T X.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_cell(LevelDev lv, CellArgs ca, DevStatus* st) {
+__global__ void __launch_bounds__(NT, 3) k_cell(LevelDev lv, CellArgs ca, DevStatus* st) {
   extern __shared__ double smem[];
   const int t = ca.list ? ca.list[blockIdx.x] : blockIdx.x, tid = threadIdx.x;
   const int I = ca.interior[t], n = ca.n[t], b = ca.b[t];
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(NT) k_schur(LevelDev lv, SchurArgs sa) {
 // Stage 2: block Jacobi.
 // ---------------------------------------------------------------------------
 // record [L ; L^-T] (2k x k): the identity rows below A_gg come out of the partial Cholesky as L^-T
-__global__ void __launch_bounds__(NT) k_prec_factor(LevelDev lv, PrecArgs pa, DevStatus* st) {
+__global__ void __launch_bounds__(NT, 3) k_prec_factor(LevelDev lv, PrecArgs pa, DevStatus* st) {
   extern __shared__ double smem[];
   const int t = pa.list ? pa.list[blockIdx.x] : blockIdx.x, tid = threadIdx.x;
   const int g = pa.groups[t], k = lv.gsize[g];
@@ -2355,7 +2355,7 @@ __global__ void __launch_bounds__(NT, 1) k_skel_team(LevelDev lv, SkelArgs sk, T
 // Stage 3b: zeroing + elimination of the redundant DOFs.
 // Panel [A~_rr ; A~_sr] ((kt+r) x kt) -> [L~ ; X~^T];  A_ss -= X~^T X~.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_skel_update(LevelDev lv, SkelArgs sk, const int* list, DevStatus* st) {
+__global__ void __launch_bounds__(NT, 3) k_skel_update(LevelDev lv, SkelArgs sk, const int* list, DevStatus* st) {
   extern __shared__ double smem[];
   const int tid = threadIdx.x;
   const int s = list ? list[blockIdx.x] : blockIdx.x;
