@@ -1348,11 +1348,13 @@ std::unique_ptr<Factorization> factorize(const Matrix& A, int dim, int n, int m,
       ds.succ = sc.as<int>();
       ka.order = L.s_order.as<int>();
       int64_t need = 0;
+      int sep_kmax = 0;
       for (int t = 0; t < nsk; ++t) {
         const int64_t kk = G.size(P.skeleton[t]);
         need = std::max<int64_t>(need, std::max<int64_t>(rows_bound[t], 1) * kk + 4 * kk + 4);
+        sep_kmax = std::max(sep_kmax, (int)kk);
       }
-      launch_skel_id_dyn(dv, ka, ds, need, s);
+      launch_skel_id_dyn(dv, ka, ds, need, s, sep_kmax);
       CK(cudaGetLastError());
       // (stream-ordered: no host sync needed here; buffers are recycled on the same stream)
     } else {

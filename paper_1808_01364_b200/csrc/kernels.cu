@@ -1444,7 +1444,10 @@ __global__ void __launch_bounds__(NT) k_skel_id(LevelDev lv, SkelArgs sk, int sm
 // topological order (the wave order) from a counter, wait until every earlier coupled separator
 // is done, run the ID, then release the later coupled ones. All CTAs are resident, and each
 // waits only for items handed out before its own, so the chain always makes progress.
-__global__ void __launch_bounds__(NT) k_skel_id_dyn(LevelDev lv, SkelArgs sk, int smem_cap, DynSched ds) {
+// MINB = 3 (80 registers, a few spilled) for levels of tiny separators (k <= 12: occupancy wins,
+// level-0 ID of c5 7.3 -> 5.6 ms); MINB = 2 keeps the pivot-chain state of larger ones in registers.
+template <int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_skel_id_dyn(LevelDev lv, SkelArgs sk, int smem_cap, DynSched ds) {
   __shared__ int s_item;
   __shared__ NbrCache nc;
   for (;;) {
@@ -4507,19 +4510,25 @@ static long long static_smem(const void* fn) {
   cudaFuncAttributes fa{};
   return cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? (long long)fa.sharedSizeBytes : 16 * 1024;
 }
-void launch_skel_id_dyn(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
-                        cudaStream_t s) {
-  if (ds.count == 0) return;
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  const int64_t cap_max = (227 * 1024 - static_smem((const void*)k_skel_id_dyn) - 1024) / 8 - SMEM_DOUBLES;
+template <int MINB>
+static void launch_skel_id_dyn_t(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
+                                 cudaStream_t s) {
+  const int64_t cap_max = (227 * 1024 - static_smem((const void*)k_skel_id_dyn<MINB>) - 1024) / 8 - SMEM_DOUBLES;
   const int cap = (int)std::min<int64_t>(need_doubles, cap_max);
   const size_t bytes = SMEM_BYTES + (size_t)cap * sizeof(double);
-  cudaFuncSetAttribute(k_skel_id_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaFuncSetAttribute(k_skel_id_dyn<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   int per_sm = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_skel_id_dyn, NT, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_skel_id_dyn<MINB>, NT, bytes);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int grid = std::max(1, std::min(ds.count, std::max(per_sm, 1) * sms));
-  k_skel_id_dyn<<<grid, NT, bytes, s>>>(lv, a, cap, ds);
+  k_skel_id_dyn<MINB><<<grid, NT, bytes, s>>>(lv, a, cap, ds);
+}
+void launch_skel_id_dyn(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
+                        cudaStream_t s, int kmax) {
+  if (ds.count == 0) return;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (kmax > 0 && kmax <= 12) launch_skel_id_dyn_t<3>(lv, a, ds, need_doubles, s);
+  else launch_skel_id_dyn_t<2>(lv, a, ds, need_doubles, s);
 }
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t need_doubles, cudaStream_t s) {
   if (count == 0) return;

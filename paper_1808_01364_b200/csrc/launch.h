@@ -68,8 +68,9 @@ void launch_prec_factor_warp(const LevelDev& lv, const PrecArgs& a, const int* l
                              cudaStream_t s);
 void launch_prec_scale_warp(const LevelDev& lv, const PrecArgs& a, const int* list, int n, int ldmax, cudaStream_t s);
 void launch_skel_id(const LevelDev& lv, const SkelArgs& a, int count, int64_t need_doubles, cudaStream_t s);
+// kmax: largest separator of the level (0 = unknown); picks the occupancy variant of the kernel
 void launch_skel_id_dyn(const LevelDev& lv, const SkelArgs& a, const DynSched& ds, int64_t need_doubles,
-                        cudaStream_t s);
+                        cudaStream_t s, int kmax = 0);
 int team_colcap(int vcap, int kmax);
 int team_blocks_per_sm(int vcap, int kmax, int colcap);
 void launch_skel_team(const LevelDev& lv, const SkelArgs& a, const TeamArgs& t, int nblocks, cudaStream_t s);
